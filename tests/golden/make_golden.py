@@ -1,0 +1,176 @@
+"""Generate the golden fixtures in tests/golden/ by running the REFERENCE.
+
+Runs only in a container that has /root/reference (read-only) and numba:
+    python tests/golden/make_golden.py
+Everything written here is produced by the reference's own public objects
+(iscsim.assembly.assemble, iscsim.linsolve.BlockSolver, iscsim.newton.Simulator)
+on seeded inputs that our side regenerates bit-identically
+(paper_1811_11992_b200.configs / synth). Fixture files:
+
+  props_goldens.json   the reference's 31 scalar goldens (pkg/tests/goldens.py)
+  asm_small3d.npz      state -> cell_pass outputs, resid/diag/offd, wells (8x6x4)
+  solve_small3d.npz    decoupled BiCGSTAB du/dbhp/iters for none/bjacobi/ras
+  solve_sub2.npz       32x16x8 grid (2 RAS subdomains): iters + du for each precond
+  synth_16.npz         synthetic 16^3 system: iters for each precond, du (ras)
+  traj_<case>_<tol>.npz  full runs: per-step records and final fields
+"""
+
+import json
+import os
+import sys
+from dataclasses import replace
+
+import numpy as np
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+ROOT = os.path.dirname(os.path.dirname(HERE))
+sys.path.insert(0, ROOT)
+
+from tools.refdeck import import_reference, reference_simulator  # noqa: E402
+from paper_1811_11992_b200 import configs  # noqa: E402
+from paper_1811_11992_b200.synth import synth_system  # noqa: E402
+
+import_reference()
+import iscsim.assembly as A  # noqa: E402
+import iscsim.linsolve as L  # noqa: E402
+from iscsim.grid import build_grid as ref_build_grid  # noqa: E402
+from iscsim.deck import GridSpec, RockSpec  # noqa: E402
+
+
+def random_state(sim, seed):
+    from tests.golden_states import perturb
+    return perturb(sim.state, sim.accn, seed)
+
+
+def state_dict(st, prefix="st_"):
+    return {prefix + f: np.asarray(getattr(st, f)) for f in
+            ("p", "t", "sw", "sg", "x", "y", "cc", "bhp")}
+
+
+def blocks_dict(blocks, prefix="w_"):
+    out = {}
+    for key in ("resid", "dwdb"):
+        out[prefix + key] = np.array([getattr(b, key) for b in blocks])
+    for key in ("wrow", "bcol", "phase_rates", "comp_rates"):
+        out[prefix + key] = np.stack([getattr(b, key) for b in blocks])
+    return out
+
+
+CELL_FIELDS = ("pot", "dpot", "beta", "dbeta", "hph", "dhph", "yfull", "dyfull", "gam",
+               "dgam", "pcv", "dpcv", "kr3", "dkr3", "ktd", "acc", "dacc", "src", "dsrc")
+
+
+def solve_all(sim, blocks, tol, precs=("none", "bjacobi", "ras")):
+    out = {}
+    d0, o0 = sim.ws.diag.copy(), sim.ws.offd.copy()
+    for pc in precs:
+        bs = L.BlockSolver(sim.grid, sim.ws, tol=tol, maxiter=1000, precond=pc)
+        du, dbhp, it = bs.solve(blocks)
+        sim.ws.diag[:] = d0
+        sim.ws.offd[:] = o0
+        out[f"{pc}_du"], out[f"{pc}_dbhp"], out[f"{pc}_iters"] = du, dbhp, np.array(it)
+    return out
+
+
+def make_props():
+    import importlib.util
+    spec = importlib.util.spec_from_file_location(
+        "ref_goldens", "/root/reference/pkg/tests/goldens.py")
+    mod = importlib.util.module_from_spec(spec)
+    spec.loader.exec_module(mod)  # the reference's own golden file
+    GOLDENS = mod.GOLDENS
+    with open(os.path.join(HERE, "props_goldens.json"), "w") as fh:
+        json.dump({"source": "/root/reference/pkg/tests/goldens.py", "goldens": GOLDENS},
+                  fh, indent=1)
+
+
+def make_asm_small3d():
+    sim = reference_simulator(configs.config("small3d"))
+    st, accn = random_state(sim, 5)
+    dt = t_new = 2e-3
+    blocks = A.assemble(sim.grid, sim.pack, sim.ws, sim.wells, sim.streams, st, accn, dt,
+                        t_new, sim.capped)
+    out = {"dt": np.array(dt), "t_new": np.array(t_new), "accn": accn,
+           "capped": sim.capped.copy(), **state_dict(st)}
+    for f in CELL_FIELDS + ("resid", "diag", "offd", "upw"):
+        out[f] = getattr(sim.ws, f).copy()
+    out.update(blocks_dict(blocks))
+    sol = solve_all(sim, blocks, 1e-10)
+    # second assembly with frozen upwinding at a perturbed state (newton.py:279)
+    st2, accn2 = random_state(sim, 6)
+    blocks2 = A.assemble(sim.grid, sim.pack, sim.ws, sim.wells, sim.streams, st2, accn2, dt,
+                         t_new, sim.capped, freeze_upwind=True)
+    out.update(state_dict(st2, "st2_"))
+    out["accn2"] = accn2
+    for f in ("resid", "diag", "offd"):
+        out[f + "2"] = getattr(sim.ws, f).copy()
+    out.update(blocks_dict(blocks2, "w2_"))
+    np.savez_compressed(os.path.join(HERE, "asm_small3d.npz"), **out)
+    np.savez_compressed(os.path.join(HERE, "solve_small3d.npz"), **sol)
+
+
+def make_solve_sub2():
+    sim = reference_simulator(configs.config("sub2"))
+    st, accn = random_state(sim, 11)
+    blocks = A.assemble(sim.grid, sim.pack, sim.ws, sim.wells, sim.streams, st, accn, 2e-3,
+                        2e-3, sim.capped)
+    sol = solve_all(sim, blocks, 1e-10)
+    keep = {k: v for k, v in sol.items() if k.endswith("iters") or k.startswith("ras")}
+    keep["resid_absmax"] = np.abs(sim.ws.resid).max(axis=0)
+    np.savez_compressed(os.path.join(HERE, "solve_sub2.npz"), seed=np.array(11), **keep)
+
+
+def make_synth():
+    nx = ny = nz = 16
+    n = nx * ny * nz
+    ones = (1.0,) * n
+    grid = ref_build_grid(GridSpec(nx, ny, nz, (1.0,) * nx, (1.0,) * ny, (1.0,) * nz),
+                          RockSpec(ones, ones, ones, 0.3))
+    diag, offd, resid = synth_system(grid, 9, seed=7)
+    from types import SimpleNamespace
+    m = grid.nconn
+    cells = np.concatenate([grid.conn_a, grid.conn_b])
+    ics = np.concatenate([np.arange(m), np.arange(m)]).astype(np.int64)
+    sides = np.concatenate([np.zeros(m, np.int8), np.ones(m, np.int8)])
+    order = np.lexsort((ics, cells))
+    ws = SimpleNamespace(diag=diag.copy(), offd=offd.copy(), resid=resid)
+    ws.adj_ptr = np.zeros(n + 1, np.int64)
+    np.cumsum(np.bincount(cells, minlength=n), out=ws.adj_ptr[1:])
+    ws.adj_ids, ws.adj_sides = ics[order], sides[order]
+    out = {}
+    for pc in ("none", "bjacobi", "ras"):
+        ws.diag[:] = diag
+        ws.offd[:] = offd
+        du, _, it = L.BlockSolver(grid, ws, tol=1e-8, maxiter=1000, precond=pc).solve([])
+        out[pc + "_iters"] = np.array(it)
+        if pc == "ras":
+            out["ras_du"] = du
+    out["diag_probe"] = diag[:3].copy()
+    out["offd_probe"] = offd[:3].copy()
+    np.savez_compressed(os.path.join(HERE, "synth_16.npz"), **out)
+
+
+def make_traj(name, ltol):
+    case = configs.config(name)
+    case = replace(case, solver=replace(case.solver, linear_tol=ltol))
+    sim = reference_simulator(case, threads=4)
+    sim.advance()
+    rec = np.array([(s.time, s.dt, s.newton, s.linear, s.solves, s.balance)
+                    for s in sim.steps])
+    out = {"steps": rec, "cum_imbalance": np.array(sim.cumulative_imbalance()),
+           **state_dict(sim.state, "final_")}
+    np.savez_compressed(os.path.join(HERE, f"traj_{name}_{ltol:.0e}.npz"), **out)
+    print(name, ltol, sim.totals())
+
+
+if __name__ == "__main__":
+    make_props()
+    make_asm_small3d()
+    make_solve_sub2()
+    make_synth()
+    make_traj("c1", 1e-10)
+    make_traj("c1", 1e-5)
+    make_traj("c2", 1e-10)
+    make_traj("c2", 1e-5)
+    for f in sorted(os.listdir(HERE)):
+        print(f, os.path.getsize(os.path.join(HERE, f)))
