@@ -1,0 +1,952 @@
+// C-ABI (include/iscgpu.h) and the host-side runtime: context/buffer
+// ownership, subdomain/level structure of the ILU(0) preconditioner, and the
+// BiCGSTAB control flow of the reference (linsolve.py:481-578) driving the
+// device kernels. Single translation unit: the kernel files are included.
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "../../include/iscgpu.h"
+#include "assemble.cu"
+#include "decouple.cu"
+#include "newton.cu"
+#include "solver.cu"
+
+using namespace isc;
+
+static thread_local std::string g_err;
+
+#define CK(call)                                                                    \
+  do {                                                                              \
+    cudaError_t e_ = (call);                                                        \
+    if (e_ != cudaSuccess) {                                                        \
+      g_err = std::string(#call) + ": " + cudaGetErrorString(e_);                  \
+      return ISC_CUDA_ERROR;                                                        \
+    }                                                                               \
+  } while (0)
+
+#define LAUNCH_CHECK()                                                              \
+  do {                                                                              \
+    ++ctx->launches;                                                                \
+    cudaError_t e_ = cudaGetLastError();                                            \
+    if (e_ != cudaSuccess) {                                                        \
+      g_err = std::string("kernel launch: ") + cudaGetErrorString(e_);             \
+      return ISC_CUDA_ERROR;                                                        \
+    }                                                                               \
+  } while (0)
+
+struct isc_ctx {
+  Dims g{};
+  Model M{};
+  cudaStream_t stream = nullptr;
+  cudaStream_t own_stream = nullptr;
+  int64_t launches = 0;
+  // static grid data
+  double *depth = nullptr, *vol = nullptr, *phi_ref = nullptr, *gd = nullptr, *td = nullptr,
+         *hl_area = nullptr;
+  double hl_kob = 0, hl_d = 1, hl_rho = 0, hl_tini = 0;
+  int64_t* conn_id = nullptr;
+  // wells
+  int nw = 0;
+  WellDev* wells_d = nullptr;
+  int64_t* wcell_d = nullptr;
+  std::vector<int64_t> wcell_h;
+  double* wout_d = nullptr;
+  double* wout_h = nullptr;   // pinned
+  double* bhp_d = nullptr;
+  uint8_t* capped_d = nullptr;
+  // assembly buffers
+  double *rec = nullptr, *acc = nullptr, *src = nullptr, *resid = nullptr, *diag = nullptr,
+         *offd = nullptr;
+  int8_t* upw = nullptr;
+  unsigned long long* bad_d = nullptr;
+  unsigned long long* bad_h = nullptr;   // pinned
+  // solver
+  int precond = ISC_PRECOND_RAS;
+  bool decoupled = false, factored = false;
+  double *rhs = nullptr, *xk = nullptr, *rk = nullptr, *rhat = nullptr, *pk = nullptr,
+         *vk = nullptr, *phat = nullptr, *shat = nullptr, *sk = nullptr, *tk = nullptr;
+  double* sc = nullptr;
+  double* sc_h = nullptr;   // pinned
+  double* partial = nullptr;
+  int64_t npartial = 0;
+  int* flags = nullptr;
+  int* fail_d = nullptr;
+  // ILU
+  IluDev ilu{};
+  int64_t* lvl_ptr_d = nullptr;
+  int nlev = 0;
+  int coop_factor = 0, coop_apply = 0;
+  // timing
+  cudaEvent_t ev[8] = {};
+  double stage_ms[4] = {0, 0, 0, 0};
+  // per-kernel-class device time (CUDA events), enabled by isc_set_profiling
+  bool profiling = false;
+  std::vector<cudaEvent_t> pool;
+  size_t pool_used = 0;
+  struct Pending { int kind; cudaEvent_t a, b; };
+  std::vector<Pending> pending;
+  double kern_ms[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+  int64_t kern_n[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+};
+
+// kernel classes for isc_kernel_times
+enum { KT_CELL = 0, KT_FACE, KT_WELLS, KT_DECOUPLE, KT_ILU_FACTOR, KT_ILU_APPLY, KT_SPMV, KT_VEC };
+
+static cudaEvent_t pool_event(isc_ctx* ctx) {
+  if (ctx->pool_used == ctx->pool.size()) {
+    cudaEvent_t e;
+    cudaEventCreate(&e);
+    ctx->pool.push_back(e);
+  }
+  return ctx->pool[ctx->pool_used++];
+}
+struct KScope {
+  isc_ctx* ctx;
+  int kind;
+  cudaEvent_t a = nullptr;
+  KScope(isc_ctx* c, int k) : ctx(c), kind(k) {
+    if (ctx->profiling) {
+      a = pool_event(ctx);
+      cudaEventRecord(a, ctx->stream);
+    }
+  }
+  ~KScope() {
+    if (ctx->profiling) {
+      cudaEvent_t b = pool_event(ctx);
+      cudaEventRecord(b, ctx->stream);
+      ctx->pending.push_back({kind, a, b});
+    }
+  }
+};
+// after a stream synchronisation: fold finished event pairs into the totals
+static void kflush(isc_ctx* ctx) {
+  for (auto& p : ctx->pending) {
+    float ms = 0.f;
+    if (cudaEventElapsedTime(&ms, p.a, p.b) == cudaSuccess) {
+      ctx->kern_ms[p.kind] += ms;
+      ctx->kern_n[p.kind] += 1;
+    }
+  }
+  ctx->pending.clear();
+  ctx->pool_used = 0;
+}
+
+static int dev_alloc(void** p, size_t bytes) {
+  cudaError_t e = cudaMalloc(p, bytes > 0 ? bytes : 8);
+  if (e != cudaSuccess) {
+    g_err = std::string("cudaMalloc(") + std::to_string(bytes) + "): " + cudaGetErrorString(e);
+    return ISC_CUDA_ERROR;
+  }
+  return ISC_OK;
+}
+#define ALLOC(ptr, bytes)                                            \
+  do {                                                               \
+    int s_ = dev_alloc((void**)&(ptr), (size_t)(bytes));             \
+    if (s_) return s_;                                               \
+  } while (0)
+
+static int grid1d(int64_t n, int t) { return (int)((n + t - 1) / t); }
+static void free_ilu(isc_ctx* ctx);
+
+// ------------------------------------------------------ ILU structure
+// Subdomains exactly as the reference: count min(64, max(1, n // 2048))
+// (linsolve.py:34-42), slabs along the first longest axis with the
+// remainder on the leading slabs (grid.py:148-166); RAS extends each slab
+// by its one-plane halo (linsolve.py:341-345), bjacobi does not.
+static int build_ilu(isc_ctx* ctx) {
+  const Dims& g = ctx->g;
+  const int64_t n = g.n;
+  const int nsub = (int)std::min<int64_t>(64, std::max<int64_t>(1, n / 2048));
+  const int dims[3] = {g.nx, g.ny, g.nz};
+  int axis = 0;
+  for (int a = 1; a < 3; ++a)
+    if (dims[a] > dims[axis]) axis = a;
+  const int na = dims[axis];
+  const int base = na / nsub, extra = na % nsub;
+  struct Box { int lo[3], hi[3], olo, ohi; };
+  std::vector<Box> boxes;
+  int pos = 0;
+  for (int s = 0; s < nsub; ++s) {
+    const int size = base + (s < extra ? 1 : 0);
+    Box b;
+    for (int a = 0; a < 3; ++a) { b.lo[a] = 0; b.hi[a] = dims[a]; }
+    b.olo = pos;
+    b.ohi = pos + size;
+    b.lo[axis] = pos;
+    b.hi[axis] = pos + size;
+    if (ctx->precond == ISC_PRECOND_RAS && nsub > 1) {
+      b.lo[axis] = std::max(0, pos - 1);
+      b.hi[axis] = std::min(na, pos + size + 1);
+    }
+    pos += size;
+    boxes.push_back(b);
+  }
+  // count slots per level
+  int maxlev = 0;
+  for (auto& b : boxes)
+    maxlev = std::max(maxlev, (b.hi[0] - b.lo[0] - 1) + (b.hi[1] - b.lo[1] - 1) + (b.hi[2] - b.lo[2] - 1));
+  const int nlev = maxlev + 1;
+  std::vector<int64_t> cnt(nlev + 1, 0);
+  for (auto& b : boxes)
+    for (int k = b.lo[2]; k < b.hi[2]; ++k)
+      for (int j = b.lo[1]; j < b.hi[1]; ++j)
+        for (int i = b.lo[0]; i < b.hi[0]; ++i)
+          cnt[(i - b.lo[0]) + (j - b.lo[1]) + (k - b.lo[2]) + 1]++;
+  std::vector<int64_t> lvl_ptr(nlev + 1, 0);
+  for (int l = 0; l < nlev; ++l) lvl_ptr[l + 1] = lvl_ptr[l] + cnt[l + 1];
+  const int64_t ns = lvl_ptr[nlev];
+  std::vector<int64_t> fill(lvl_ptr.begin(), lvl_ptr.end() - 1);
+  std::vector<int64_t> cell(ns), lo(3 * ns, -1), up(3 * ns, -1);
+  std::vector<int8_t> owned(ns, 0);
+  for (auto& b : boxes) {
+    const int wx = b.hi[0] - b.lo[0], wy = b.hi[1] - b.lo[1], wz = b.hi[2] - b.lo[2];
+    std::vector<int64_t> slot((size_t)wx * wy * wz);
+    for (int k = b.lo[2]; k < b.hi[2]; ++k)
+      for (int j = b.lo[1]; j < b.hi[1]; ++j)
+        for (int i = b.lo[0]; i < b.hi[0]; ++i) {
+          const int li = i - b.lo[0], lj = j - b.lo[1], lk = k - b.lo[2];
+          const int64_t s = fill[li + lj + lk]++;
+          slot[((size_t)lk * wy + lj) * wx + li] = s;
+          cell[s] = i + (int64_t)g.nx * (j + (int64_t)g.ny * k);
+          const int ijk[3] = {i, j, k};
+          owned[s] = (ijk[axis] >= b.olo && ijk[axis] < b.ohi) ? 1 : 0;
+        }
+    for (int lk = 0; lk < wz; ++lk)
+      for (int lj = 0; lj < wy; ++lj)
+        for (int li = 0; li < wx; ++li) {
+          const int64_t s = slot[((size_t)lk * wy + lj) * wx + li];
+          auto at = [&](int a, int bb, int c) { return slot[((size_t)c * wy + bb) * wx + a]; };
+          // lower in ascending neighbour index: -z, -y, -x
+          if (lk > 0) lo[0 * ns + s] = at(li, lj, lk - 1);
+          if (lj > 0) lo[1 * ns + s] = at(li, lj - 1, lk);
+          if (li > 0) lo[2 * ns + s] = at(li - 1, lj, lk);
+          // upper ascending: +x, +y, +z
+          if (li + 1 < wx) up[0 * ns + s] = at(li + 1, lj, lk);
+          if (lj + 1 < wy) up[1 * ns + s] = at(li, lj + 1, lk);
+          if (lk + 1 < wz) up[2 * ns + s] = at(li, lj, lk + 1);
+        }
+  }
+  int64_t *cell_d, *lo_d, *up_d;
+  int8_t* owned_d;
+  ALLOC(cell_d, ns * 8);
+  ALLOC(lo_d, 3 * ns * 8);
+  ALLOC(up_d, 3 * ns * 8);
+  ALLOC(owned_d, ns);
+  ALLOC(ctx->lvl_ptr_d, (nlev + 1) * 8);
+  CK(cudaMemcpy(cell_d, cell.data(), ns * 8, cudaMemcpyHostToDevice));
+  CK(cudaMemcpy(lo_d, lo.data(), 3 * ns * 8, cudaMemcpyHostToDevice));
+  CK(cudaMemcpy(up_d, up.data(), 3 * ns * 8, cudaMemcpyHostToDevice));
+  CK(cudaMemcpy(owned_d, owned.data(), ns, cudaMemcpyHostToDevice));
+  CK(cudaMemcpy(ctx->lvl_ptr_d, lvl_ptr.data(), (nlev + 1) * 8, cudaMemcpyHostToDevice));
+  double *lblk, *uinv, *zs;
+  ALLOC(lblk, (size_t)3 * NB * ns * 8);
+  ALLOC(uinv, (size_t)NB * ns * 8);
+  ALLOC(zs, (size_t)NU * ns * 8);
+  ctx->ilu = IluDev{ns, cell_d, owned_d, lo_d, up_d, lblk, uinv, zs};
+  ctx->nlev = nlev;
+  int dev = 0, nsm = 0, per_sm = 0;
+  CK(cudaGetDevice(&dev));
+  CK(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev));
+  CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_ilu_factor, IL_SLOTS * NU, 0));
+  ctx->coop_factor = std::max(1, per_sm) * nsm;
+  CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_ilu_apply, IL_SLOTS * NU, 0));
+  ctx->coop_apply = std::max(1, per_sm) * nsm;
+  return ISC_OK;
+}
+
+// --------------------------------------------------------------- create
+
+extern "C" const char* isc_last_error(void) { return g_err.c_str(); }
+extern "C" int isc_block_size(void) { return NU; }
+
+extern "C" int isc_create(const isc_model_desc* md, const isc_grid_desc* gdsc, int32_t nwells,
+                          const isc_well_desc* wells, int32_t precond, isc_ctx** out) {
+  if (!md || !gdsc || !out) { g_err = "null argument"; return ISC_BAD_ARGUMENT; }
+  if (md->nco != NCO || md->ncg != NCG) {
+    g_err = "library compiled for nco=2, ncg=2 (block size 9)";
+    return ISC_UNSUPPORTED;
+  }
+  if (md->nreac > MAXREAC || md->nswt > MAXTAB || md->nslt > MAXTAB || md->nswt < 1 ||
+      md->nslt < 1) {
+    g_err = "model tables exceed compiled limits";
+    return ISC_UNSUPPORTED;
+  }
+  if (precond < 0 || precond > 2) { g_err = "unknown preconditioner"; return ISC_BAD_ARGUMENT; }
+  int ndev = 0;
+  if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0) {
+    g_err = "no CUDA device";
+    return ISC_CUDA_ERROR;
+  }
+  isc_ctx* ctx = new isc_ctx();
+  ctx->precond = precond;
+  Dims& g = ctx->g;
+  g.nx = gdsc->nx; g.ny = gdsc->ny; g.nz = gdsc->nz;
+  g.nxny = (int64_t)g.nx * g.ny;
+  g.n = g.nxny * g.nz;
+  const int64_t n = g.n;
+  // model
+  Model& M = ctx->M;
+  std::memset(&M, 0, sizeof(M));
+  std::memcpy(M.liq, md->liq, sizeof(M.liq));
+  std::memcpy(M.gasp, md->gasp, sizeof(M.gasp));
+  std::memcpy(M.kv, md->kv, sizeof(M.kv));
+  std::memcpy(M.rockp, md->rockp, sizeof(M.rockp));
+  for (int i = 0; i < md->nswt; ++i) {
+    M.swt_s[i] = md->swt_s[i]; M.swt_krw[i] = md->swt_krw[i];
+    M.swt_krow[i] = md->swt_krow[i]; M.swt_pcow[i] = md->swt_pcow[i];
+  }
+  for (int i = 0; i < md->nslt; ++i) {
+    M.slt_s[i] = md->slt_s[i]; M.slt_krg[i] = md->slt_krg[i];
+    M.slt_krog[i] = md->slt_krog[i]; M.slt_pcog[i] = md->slt_pcog[i];
+  }
+  M.nreac = (int)md->nreac; M.nswt = (int)md->nswt; M.nslt = (int)md->nslt;
+  M.heavy = (int)md->heavy; M.ccmax = md->ccmax;
+  for (int q = 0; q < md->nreac; ++q) {
+    for (int k = 0; k < 3; ++k) M.rcoef[q][k] = md->rcoef[q * 3 + k];
+    for (int a = 0; a <= NF; ++a) M.nmat[a][q] = md->nmat[a * md->nreac + q];
+    M.law[q] = (int)md->law[q]; M.fuel[q] = (int)md->fuel[q]; M.ox[q] = (int)md->ox[q];
+  }
+  CK(cudaStreamCreateWithFlags(&ctx->own_stream, cudaStreamNonBlocking));
+  ctx->stream = ctx->own_stream;
+  for (auto& e : ctx->ev) CK(cudaEventCreate(&e));
+  // static grid arrays
+  ALLOC(ctx->depth, n * 8); ALLOC(ctx->vol, n * 8); ALLOC(ctx->phi_ref, n * 8);
+  ALLOC(ctx->gd, 3 * n * 8); ALLOC(ctx->td, 3 * n * 8); ALLOC(ctx->conn_id, 3 * n * 8);
+  CK(cudaMemcpy(ctx->depth, gdsc->depth, n * 8, cudaMemcpyHostToDevice));
+  CK(cudaMemcpy(ctx->vol, gdsc->volume, n * 8, cudaMemcpyHostToDevice));
+  CK(cudaMemcpy(ctx->phi_ref, gdsc->phi_ref, n * 8, cudaMemcpyHostToDevice));
+  CK(cudaMemcpy(ctx->gd, gdsc->gd, 3 * n * 8, cudaMemcpyHostToDevice));
+  CK(cudaMemcpy(ctx->td, gdsc->td, 3 * n * 8, cudaMemcpyHostToDevice));
+  CK(cudaMemcpy(ctx->conn_id, gdsc->conn_id, 3 * n * 8, cudaMemcpyHostToDevice));
+  if (gdsc->hl_area) {
+    ALLOC(ctx->hl_area, n * 8);
+    CK(cudaMemcpy(ctx->hl_area, gdsc->hl_area, n * 8, cudaMemcpyHostToDevice));
+  }
+  ctx->hl_kob = gdsc->hl_kob; ctx->hl_d = gdsc->hl_d; ctx->hl_rho = gdsc->hl_rho;
+  ctx->hl_tini = gdsc->hl_tini;
+  // wells
+  ctx->nw = nwells;
+  if (nwells > 0) {
+    std::vector<WellDev> wd(nwells);
+    for (int w = 0; w < nwells; ++w) {
+      const isc_well_desc& s = wells[w];
+      WellDev& d = wd[w];
+      if (s.cell < 0 || s.cell >= n) { g_err = "well cell out of range"; return ISC_BAD_ARGUMENT; }
+      d.cell = s.cell; d.kind = s.kind; d.control = s.control; d.target = s.target;
+      d.wi = s.wi; d.z_bh = s.z_bh; d.pinjmax = s.pinjmax; d.heat_rate = s.heat_rate;
+      d.heat_stop = s.heat_stop;
+      for (int a = 0; a < NF; ++a) d.s_yfull[a] = s.s_yfull[a];
+      for (int j = 0; j < NCG; ++j) d.s_yinj[j] = s.s_yinj[j];
+      d.s_tinj = s.s_tinj; d.s_mu = s.s_mu; d.s_h = s.s_h; d.s_mbar = s.s_mbar;
+      ctx->wcell_h.push_back(s.cell);
+    }
+    ALLOC(ctx->wells_d, nwells * sizeof(WellDev));
+    CK(cudaMemcpy(ctx->wells_d, wd.data(), nwells * sizeof(WellDev), cudaMemcpyHostToDevice));
+    ALLOC(ctx->wcell_d, nwells * 8);
+    CK(cudaMemcpy(ctx->wcell_d, ctx->wcell_h.data(), nwells * 8, cudaMemcpyHostToDevice));
+  }
+  ALLOC(ctx->wout_d, std::max(1, nwells) * WOUT * 8);
+  CK(cudaMallocHost(&ctx->wout_h, std::max(1, nwells) * WOUT * 8));
+  ALLOC(ctx->bhp_d, std::max(1, nwells) * 8);
+  ALLOC(ctx->capped_d, std::max(1, nwells));
+  // assembly buffers
+  ALLOC(ctx->rec, (size_t)NREC * n * 8);
+  ALLOC(ctx->acc, (size_t)NU * n * 8);
+  ALLOC(ctx->src, (size_t)NU * n * 8);
+  ALLOC(ctx->resid, (size_t)NU * n * 8);
+  ALLOC(ctx->diag, (size_t)NB * n * 8);
+  ALLOC(ctx->offd, (size_t)NDIR * NB * n * 8);
+  ALLOC(ctx->upw, (size_t)9 * n);
+  CK(cudaMemset(ctx->upw, 0, (size_t)9 * n));
+  ALLOC(ctx->bad_d, 8);
+  CK(cudaMallocHost(&ctx->bad_h, 8));
+  // solver vectors
+  double** vecs[] = {&ctx->rhs, &ctx->xk, &ctx->rk, &ctx->rhat, &ctx->pk,
+                     &ctx->vk, &ctx->phat, &ctx->shat, &ctx->sk, &ctx->tk};
+  for (double** v : vecs) ALLOC(*v, (size_t)NU * n * 8);
+  ALLOC(ctx->sc, S_NSCAL * 8);
+  CK(cudaMallocHost(&ctx->sc_h, S_NSCAL * 8));
+  ctx->npartial = std::max<int64_t>(RED_BLOCKS, grid1d(n, 32)) * 3 * (NF + 1);
+  ALLOC(ctx->partial, ctx->npartial * 8);
+  ALLOC(ctx->flags, n * 4);
+  ALLOC(ctx->fail_d, 4);
+  if (precond != ISC_PRECOND_NONE) {
+    int s = build_ilu(ctx);
+    if (s) return s;
+  }
+  *out = ctx;
+  return ISC_OK;
+}
+
+extern "C" int isc_destroy(isc_ctx* ctx) {
+  if (!ctx) return ISC_OK;
+  cudaStreamSynchronize(ctx->stream);
+  void* ptrs[] = {ctx->depth, ctx->vol, ctx->phi_ref, ctx->gd, ctx->td, ctx->hl_area,
+                  ctx->conn_id, ctx->wells_d, ctx->wcell_d, ctx->wout_d, ctx->bhp_d,
+                  ctx->capped_d, ctx->rec, ctx->acc, ctx->src, ctx->resid, ctx->diag,
+                  ctx->offd, ctx->upw, ctx->bad_d, ctx->rhs, ctx->xk, ctx->rk, ctx->rhat,
+                  ctx->pk, ctx->vk, ctx->phat, ctx->shat, ctx->sk, ctx->tk, ctx->sc,
+                  ctx->partial, ctx->flags, ctx->fail_d};
+  free_ilu(ctx);
+  for (void* p : ptrs)
+    if (p) cudaFree(p);
+  if (ctx->wout_h) cudaFreeHost(ctx->wout_h);
+  if (ctx->bad_h) cudaFreeHost(ctx->bad_h);
+  if (ctx->sc_h) cudaFreeHost(ctx->sc_h);
+  for (auto& e : ctx->ev)
+    if (e) cudaEventDestroy(e);
+  if (ctx->own_stream) cudaStreamDestroy(ctx->own_stream);
+  delete ctx;
+  return ISC_OK;
+}
+
+extern "C" void* isc_stream(isc_ctx* ctx) { return ctx ? (void*)ctx->stream : nullptr; }
+extern "C" int isc_set_stream(isc_ctx* ctx, void* stream) {
+  CK(cudaStreamSynchronize(ctx->stream));
+  ctx->stream = stream ? (cudaStream_t)stream : ctx->own_stream;
+  return ISC_OK;
+}
+extern "C" int isc_synchronize(isc_ctx* ctx) {
+  CK(cudaStreamSynchronize(ctx->stream));
+  return ISC_OK;
+}
+extern "C" int64_t isc_launch_count(isc_ctx* ctx) { return ctx ? ctx->launches : 0; }
+extern "C" int isc_stage_times(isc_ctx* ctx, double* out4) {
+  for (int i = 0; i < 4; ++i) out4[i] = ctx->stage_ms[i];
+  return ISC_OK;
+}
+extern "C" int isc_set_profiling(isc_ctx* ctx, int32_t on) {
+  CK(cudaStreamSynchronize(ctx->stream));
+  kflush(ctx);
+  ctx->profiling = on != 0;
+  return ISC_OK;
+}
+extern "C" int isc_kernel_times(isc_ctx* ctx, double* ms8, int64_t* count8, int32_t reset) {
+  CK(cudaStreamSynchronize(ctx->stream));
+  kflush(ctx);
+  for (int i = 0; i < 8; ++i) {
+    ms8[i] = ctx->kern_ms[i];
+    count8[i] = ctx->kern_n[i];
+    if (reset) { ctx->kern_ms[i] = 0; ctx->kern_n[i] = 0; }
+  }
+  return ISC_OK;
+}
+
+static int stage_begin(isc_ctx* ctx, int st) {
+  CK(cudaEventRecord(ctx->ev[2 * st], ctx->stream));
+  return ISC_OK;
+}
+static int stage_end(isc_ctx* ctx, int st) {
+  CK(cudaEventRecord(ctx->ev[2 * st + 1], ctx->stream));
+  CK(cudaEventSynchronize(ctx->ev[2 * st + 1]));
+  kflush(ctx);
+  float ms = 0.f;
+  CK(cudaEventElapsedTime(&ms, ctx->ev[2 * st], ctx->ev[2 * st + 1]));
+  ctx->stage_ms[st] += ms;
+  return ISC_OK;
+}
+#define STAGE(call) do { int s_ = (call); if (s_) return s_; } while (0)
+
+// ------------------------------------------------------------- assemble
+
+extern "C" int isc_assemble(isc_ctx* ctx, const double* d_state, const double* h_bhp,
+                            const double* d_accn, double dt, double t_new,
+                            const uint8_t* h_capped, int32_t freeze, double* h_wells_out,
+                            int64_t* bad_cell) {
+  const int64_t n = ctx->g.n;
+  cudaStream_t st = ctx->stream;
+  STAGE(stage_begin(ctx, 0));
+  if (ctx->nw > 0) {
+    CK(cudaMemcpyAsync(ctx->bhp_d, h_bhp, ctx->nw * 8, cudaMemcpyHostToDevice, st));
+    CK(cudaMemcpyAsync(ctx->capped_d, h_capped, ctx->nw, cudaMemcpyHostToDevice, st));
+  }
+  CK(cudaMemsetAsync(ctx->bad_d, 0xff, 8, st));
+  CellArgs A{ctx->g, d_state, ctx->phi_ref, ctx->vol, ctx->hl_area, ctx->hl_kob, ctx->hl_d,
+             ctx->hl_rho, ctx->hl_tini, d_accn, dt, ctx->rec, ctx->acc, ctx->src,
+             ctx->resid, ctx->diag, ctx->bad_d};
+  { KScope ks(ctx, KT_CELL); k_cell<<<grid1d(n, 128), 128, 0, st>>>(ctx->M, A); }
+  LAUNCH_CHECK();
+  CK(cudaMemcpyAsync(ctx->bad_h, ctx->bad_d, 8, cudaMemcpyDeviceToHost, st));
+  CK(cudaStreamSynchronize(st));
+  if (*ctx->bad_h != ~0ULL) {
+    if (bad_cell) *bad_cell = (int64_t)*ctx->bad_h;
+    g_err = "coke fills the pore volume";
+    STAGE(stage_end(ctx, 0));
+    return ISC_PORE_SPACE_EXHAUSTED;
+  }
+  FaceArgs F{ctx->g, d_state, ctx->rec, ctx->depth, ctx->gd, ctx->td, ctx->upw, freeze,
+             ctx->resid, ctx->diag, ctx->offd};
+  { KScope ks(ctx, KT_FACE); k_face<<<grid1d(n, 32), dim3(32, NU), 0, st>>>(F); }
+  LAUNCH_CHECK();
+  if (ctx->nw > 0) {
+    KScope ks(ctx, KT_WELLS);
+    k_wells<<<1, 32, 0, st>>>(ctx->M, ctx->g, ctx->nw, ctx->wells_d, d_state, ctx->bhp_d,
+                              ctx->capped_d, ctx->rec, ctx->depth, t_new, ctx->resid,
+                              ctx->diag, ctx->wout_d);
+    LAUNCH_CHECK();
+    CK(cudaMemcpyAsync(ctx->wout_h, ctx->wout_d, ctx->nw * WOUT * 8, cudaMemcpyDeviceToHost, st));
+  }
+  STAGE(stage_end(ctx, 0));   // synchronises
+  if (ctx->nw > 0 && h_wells_out) std::memcpy(h_wells_out, ctx->wout_h, ctx->nw * WOUT * 8);
+  ctx->decoupled = false;
+  ctx->factored = false;
+  return ISC_OK;
+}
+
+extern "C" int isc_copy_out(isc_ctx* ctx, int32_t what, void* d_dst) {
+  const int64_t n = ctx->g.n;
+  const void* src = nullptr;
+  size_t bytes = 0;
+  switch (what) {
+    case 0: src = ctx->resid; bytes = (size_t)NU * n * 8; break;
+    case 1: src = ctx->acc; bytes = (size_t)NU * n * 8; break;
+    case 2: src = ctx->src; bytes = (size_t)NU * n * 8; break;
+    case 3: src = ctx->rec + (size_t)R_Y * n; bytes = (size_t)NF * n * 8; break;
+    case 4: src = ctx->rec; bytes = (size_t)NREC * n * 8; break;
+    case 5: src = ctx->upw; bytes = (size_t)9 * n; break;
+    default: g_err = "unknown array"; return ISC_BAD_ARGUMENT;
+  }
+  CK(cudaMemcpyAsync(d_dst, src, bytes, cudaMemcpyDeviceToDevice, ctx->stream));
+  CK(cudaStreamSynchronize(ctx->stream));
+  return ISC_OK;
+}
+
+extern "C" int isc_export_system(isc_ctx* ctx, double* d_diag, double* d_offd, double* d_resid) {
+  k_export_system<<<grid1d(ctx->g.n, 128), 128, 0, ctx->stream>>>(
+      ctx->g, ctx->conn_id, ctx->diag, ctx->offd, ctx->resid, d_diag, d_offd, d_resid);
+  LAUNCH_CHECK();
+  CK(cudaStreamSynchronize(ctx->stream));
+  return ISC_OK;
+}
+
+extern "C" int isc_import_system(isc_ctx* ctx, const double* d_diag, const double* d_offd,
+                                 const double* d_resid, const double* h_wells_out) {
+  k_import_system<<<grid1d(ctx->g.n, 128), 128, 0, ctx->stream>>>(
+      ctx->g, ctx->conn_id, d_diag, d_offd, d_resid, ctx->diag, ctx->offd, ctx->resid);
+  LAUNCH_CHECK();
+  if (ctx->nw > 0 && h_wells_out) {
+    std::memcpy(ctx->wout_h, h_wells_out, ctx->nw * WOUT * 8);
+    CK(cudaMemcpyAsync(ctx->wout_d, ctx->wout_h, ctx->nw * WOUT * 8, cudaMemcpyHostToDevice,
+                       ctx->stream));
+  }
+  CK(cudaStreamSynchronize(ctx->stream));
+  ctx->decoupled = ctx->factored = false;
+  return ISC_OK;
+}
+
+extern "C" int isc_set_wells_out(isc_ctx* ctx, const double* h_wells_out) {
+  if (ctx->nw == 0) return ISC_OK;
+  std::memcpy(ctx->wout_h, h_wells_out, ctx->nw * WOUT * 8);
+  CK(cudaMemcpyAsync(ctx->wout_d, ctx->wout_h, ctx->nw * WOUT * 8, cudaMemcpyHostToDevice,
+                     ctx->stream));
+  CK(cudaStreamSynchronize(ctx->stream));
+  return ISC_OK;
+}
+
+static void free_ilu(isc_ctx* ctx) {
+  void* ptrs[] = {ctx->lvl_ptr_d, (void*)ctx->ilu.cell, (void*)ctx->ilu.owned,
+                  (void*)ctx->ilu.lo, (void*)ctx->ilu.up, ctx->ilu.lblk, ctx->ilu.uinv,
+                  ctx->ilu.zs};
+  for (void* p : ptrs)
+    if (p) cudaFree(p);
+  ctx->ilu = IluDev{};
+  ctx->lvl_ptr_d = nullptr;
+  ctx->nlev = 0;
+}
+
+extern "C" int isc_set_precond(isc_ctx* ctx, int32_t precond) {
+  if (precond < 0 || precond > 2) { g_err = "unknown preconditioner"; return ISC_BAD_ARGUMENT; }
+  if (precond == ctx->precond) return ISC_OK;
+  CK(cudaStreamSynchronize(ctx->stream));
+  free_ilu(ctx);
+  ctx->precond = precond;
+  ctx->factored = false;
+  if (precond != ISC_PRECOND_NONE) return build_ilu(ctx);
+  return ISC_OK;
+}
+
+extern "C" int isc_synth_system(isc_ctx* ctx, uint64_t seed) {
+  k_synth<<<grid1d(ctx->g.n, 128), 128, 0, ctx->stream>>>(ctx->g, seed, ctx->diag, ctx->offd,
+                                                          ctx->resid);
+  LAUNCH_CHECK();
+  CK(cudaStreamSynchronize(ctx->stream));
+  ctx->decoupled = ctx->factored = false;
+  return ISC_OK;
+}
+
+// ------------------------------------------------------------- decouple
+
+extern "C" int isc_decouple(isc_ctx* ctx, int64_t* bad_cell, int32_t* bad_col) {
+  const int64_t n = ctx->g.n;
+  cudaStream_t st = ctx->stream;
+  // well equations with a zero / non-finite bhp derivative (linsolve.py:372-375)
+  if (ctx->nw > 0) {
+    CK(cudaMemcpyAsync(ctx->wout_h, ctx->wout_d, ctx->nw * WOUT * 8, cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    for (int w = 0; w < ctx->nw; ++w) {
+      const double dwdb = ctx->wout_h[w * WOUT + 1];
+      if (dwdb == 0.0 || !std::isfinite(dwdb)) {
+        if (bad_cell) *bad_cell = -1;
+        if (bad_col) *bad_col = -1;
+        g_err = "well equation has a zero bhp derivative";
+        return ISC_SINGULAR_CELL_BLOCK;
+      }
+    }
+  }
+  STAGE(stage_begin(ctx, 1));
+  {
+  KScope ks(ctx, KT_DECOUPLE);
+  k_rhs_schur<<<grid1d(n, 256), 256, 0, st>>>(ctx->g, ctx->resid, ctx->rhs, ctx->diag, ctx->nw,
+                                              ctx->wcell_d, ctx->wout_d, WOUT);
+  LAUNCH_CHECK();
+  CK(cudaMemsetAsync(ctx->flags, 0, n * 4, st));
+  CK(cudaMemsetAsync(ctx->bad_d, 0xff, 8, st));
+  k_decouple<<<grid1d(n, DC_CELLS), dim3(DC_CELLS, 32), 0, st>>>(ctx->g, ctx->diag, ctx->offd,
+                                                                 ctx->rhs, ctx->flags, ctx->bad_d);
+  LAUNCH_CHECK();
+  }
+  CK(cudaMemcpyAsync(ctx->bad_h, ctx->bad_d, 8, cudaMemcpyDeviceToHost, st));
+  STAGE(stage_end(ctx, 1));
+  if (*ctx->bad_h != ~0ULL) {
+    const int64_t c = (int64_t)*ctx->bad_h;
+    int flag = 0;
+    CK(cudaMemcpy(&flag, ctx->flags + c, 4, cudaMemcpyDeviceToHost));
+    if (bad_cell) *bad_cell = c;
+    if (bad_col) *bad_col = flag - 1;
+    g_err = "diagonal block is singular";
+    return ISC_SINGULAR_CELL_BLOCK;
+  }
+  ctx->decoupled = true;
+  return ISC_OK;
+}
+
+extern "C" int isc_copy_rhs(isc_ctx* ctx, double* d_dst) {
+  CK(cudaMemcpyAsync(d_dst, ctx->rhs, (size_t)NU * ctx->g.n * 8, cudaMemcpyDeviceToDevice,
+                     ctx->stream));
+  CK(cudaStreamSynchronize(ctx->stream));
+  return ISC_OK;
+}
+
+extern "C" int isc_precond_setup(isc_ctx* ctx, int64_t* bad_cell) {
+  if (ctx->precond == ISC_PRECOND_NONE) { ctx->factored = true; return ISC_OK; }
+  cudaStream_t st = ctx->stream;
+  STAGE(stage_begin(ctx, 2));
+  CK(cudaMemsetAsync(ctx->fail_d, 0x7f, 4, st));
+  Dims g = ctx->g;
+  IluDev L = ctx->ilu;
+  const double* offd = ctx->offd;
+  const int64_t* lp = ctx->lvl_ptr_d;
+  int nlev = ctx->nlev;
+  int* fail = ctx->fail_d;
+  void* args[] = {&g, &L, &offd, &lp, &nlev, &fail};
+  {
+  KScope ks(ctx, KT_ILU_FACTOR);
+  CK(cudaLaunchCooperativeKernel((void*)k_ilu_factor, ctx->coop_factor, dim3(IL_SLOTS, NU), args,
+                                 0, st));
+  }
+  ++ctx->launches;
+  int fail_h = 0;
+  CK(cudaMemcpyAsync(ctx->bad_h, ctx->fail_d, 4, cudaMemcpyDeviceToHost, st));
+  STAGE(stage_end(ctx, 2));
+  std::memcpy(&fail_h, ctx->bad_h, 4);
+  if (fail_h != 0x7f7f7f7f) {
+    if (bad_cell) *bad_cell = -1;
+    g_err = "ILU(0) pivot failed";
+    return ISC_SINGULAR_CELL_BLOCK;
+  }
+  ctx->factored = true;
+  return ISC_OK;
+}
+
+static int precond_apply(isc_ctx* ctx, const double* r, double* z) {
+  const int64_t len = (int64_t)NU * ctx->g.n;
+  if (ctx->precond == ISC_PRECOND_NONE) {
+    CK(cudaMemcpyAsync(z, r, len * 8, cudaMemcpyDeviceToDevice, ctx->stream));
+    return ISC_OK;
+  }
+  Dims g = ctx->g;
+  IluDev L = ctx->ilu;
+  const double* offd = ctx->offd;
+  const int64_t* lp = ctx->lvl_ptr_d;
+  int nlev = ctx->nlev;
+  void* args[] = {&g, &L, &offd, &lp, &nlev, (void*)&r, (void*)&z};
+  KScope ks(ctx, KT_ILU_APPLY);
+  CK(cudaLaunchCooperativeKernel((void*)k_ilu_apply, ctx->coop_apply, dim3(IL_SLOTS, NU), args,
+                                 0, ctx->stream));
+  ++ctx->launches;
+  return ISC_OK;
+}
+
+template <int K>
+static int spmv(isc_ctx* ctx, const double* x, double* y, const double* w0, const double* w1,
+                int* nblocks) {
+  const int blocks = grid1d(ctx->g.n, 32);
+  KScope ks(ctx, KT_SPMV);
+  k_spmv<K><<<blocks, dim3(32, NU), 0, ctx->stream>>>(ctx->g, ctx->offd, x, y, w0, w1,
+                                                      ctx->partial);
+  LAUNCH_CHECK();
+  if (nblocks) *nblocks = blocks;
+  return ISC_OK;
+}
+
+extern "C" int isc_spmv(isc_ctx* ctx, const double* d_x, double* d_y) {
+  int s = spmv<0>(ctx, d_x, d_y, nullptr, nullptr, nullptr);
+  if (s) return s;
+  CK(cudaStreamSynchronize(ctx->stream));
+  return ISC_OK;
+}
+
+extern "C" int isc_precond_apply(isc_ctx* ctx, const double* d_r, double* d_z) {
+  int s = precond_apply(ctx, d_r, d_z);
+  if (s) return s;
+  CK(cudaStreamSynchronize(ctx->stream));
+  return ISC_OK;
+}
+
+// ------------------------------------------------------------- BiCGSTAB
+
+struct Kry {
+  isc_ctx* ctx;
+  int64_t len;
+  int vgrid() const { return RED_BLOCKS; }
+  int finalize1(int nparts, int s0) {
+    k_finalize<1><<<1, 256, 0, ctx->stream>>>(ctx->partial, nparts, ctx->sc, s0, s0, s0);
+    ++ctx->launches;
+    return cudaGetLastError() == cudaSuccess ? 0 : ISC_CUDA_ERROR;
+  }
+  int finalize2(int nparts, int s0, int s1) {
+    k_finalize<2><<<1, 256, 0, ctx->stream>>>(ctx->partial, nparts, ctx->sc, s0, s1, s1);
+    ++ctx->launches;
+    return cudaGetLastError() == cudaSuccess ? 0 : ISC_CUDA_ERROR;
+  }
+  int dot(const double* a, const double* b, int slot) {
+    k_dots<1><<<RED_BLOCKS, RED_THREADS, 0, ctx->stream>>>(len, a, b, nullptr, nullptr, nullptr,
+                                                          nullptr, ctx->partial);
+    ++ctx->launches;
+    return finalize1(RED_BLOCKS, slot);
+  }
+  int read_scalars() {
+    if (cudaMemcpyAsync(ctx->sc_h, ctx->sc, S_NSCAL * 8, cudaMemcpyDeviceToHost, ctx->stream) !=
+            cudaSuccess ||
+        cudaStreamSynchronize(ctx->stream) != cudaSuccess) {
+      g_err = "scalar readback failed";
+      return ISC_CUDA_ERROR;
+    }
+    kflush(ctx);
+    return 0;
+  }
+  int set(int slot, double v) {
+    ctx->sc_h[slot] = v;   // host staging; pushed by push()
+    return 0;
+  }
+  int push() {
+    return cudaMemcpyAsync(ctx->sc, ctx->sc_h, S_NSCAL * 8, cudaMemcpyHostToDevice, ctx->stream) ==
+                   cudaSuccess ? 0 : ISC_CUDA_ERROR;
+  }
+};
+
+#define TRY(x) do { int s_ = (x); if (s_) return s_; } while (0)
+
+// linsolve.py:481-578 with b = ctx->rhs, solution in ctx->xk
+static int bicgstab(isc_ctx* ctx, double tol, int maxiter, int* iters) {
+  const int64_t len = (int64_t)NU * ctx->g.n;
+  cudaStream_t st = ctx->stream;
+  Kry K{ctx, len};
+  double *b = ctx->rhs, *x = ctx->xk, *r = ctx->rk, *rhat = ctx->rhat, *p = ctx->pk,
+         *v = ctx->vk, *phat = ctx->phat, *shat = ctx->shat, *s = ctx->sk, *t = ctx->tk;
+  CK(cudaMemsetAsync(x, 0, len * 8, st));
+  TRY(K.dot(b, b, S_BB));
+  TRY(K.read_scalars());
+  const double nb = std::sqrt(ctx->sc_h[S_BB]);
+  *iters = 0;
+  if (nb == 0.0) return ISC_OK;
+  const double brk = 1e-30 * nb * nb;
+  CK(cudaMemcpyAsync(r, b, len * 8, cudaMemcpyDeviceToDevice, st));
+  CK(cudaMemcpyAsync(rhat, b, len * 8, cudaMemcpyDeviceToDevice, st));
+  CK(cudaMemsetAsync(p, 0, len * 8, st));
+  CK(cudaMemsetAsync(v, 0, len * 8, st));
+  double* sh = ctx->sc_h;
+  for (int i = 0; i < S_NSCAL; ++i) sh[i] = 0.0;
+  sh[S_RHO_OLD] = 1.0; sh[S_ALPHA] = 1.0; sh[S_OMEGA] = 1.0; sh[S_FIRST] = 1.0;
+  sh[S_BB] = nb * nb;
+  bool restarted = false, first = true;
+  int it = 0;
+  // rho = rhat . r  (kept in S_RHO_NEW between iterations)
+  TRY(K.push());
+  TRY(K.dot(rhat, r, S_RHO_NEW));
+  TRY(K.read_scalars());
+  auto restart = [&]() -> int {
+    // r = b - A x; rhat = r; p = v = 0; scalars reset (linsolve.py:509-519)
+    if (spmv<0>(ctx, x, t, nullptr, nullptr, nullptr)) return ISC_CUDA_ERROR;
+    k_sub<<<RED_BLOCKS, RED_THREADS, 0, st>>>(len, b, t, r);
+    ++ctx->launches;
+    if (cudaMemcpyAsync(rhat, r, len * 8, cudaMemcpyDeviceToDevice, st) != cudaSuccess) return ISC_CUDA_ERROR;
+    cudaMemsetAsync(p, 0, len * 8, st);
+    cudaMemsetAsync(v, 0, len * 8, st);
+    sh[S_RHO_OLD] = 1.0; sh[S_ALPHA] = 1.0; sh[S_OMEGA] = 1.0;
+    first = true;
+    restarted = true;
+    return 0;
+  };
+  while (it < maxiter) {
+    ++it;
+    double rho = sh[S_RHO_NEW];
+    const double omega = sh[S_OMEGA];
+    if (std::fabs(rho) < brk || (!first && omega == 0.0)) {
+      if (restarted) { g_err = "BiCGSTAB scalar breakdown"; *iters = it; return ISC_BREAKDOWN; }
+      TRY(restart());
+      TRY(K.push());
+      TRY(K.dot(rhat, r, S_RHO_NEW));
+      TRY(K.read_scalars());
+      rho = sh[S_RHO_NEW];
+      if (std::fabs(rho) < brk) { g_err = "BiCGSTAB restart found a null residual"; *iters = it; return ISC_BREAKDOWN; }
+    }
+    sh[S_RHO] = rho;
+    sh[S_FIRST] = first ? 1.0 : 0.0;
+    first = false;
+    TRY(K.push());
+    k_update_p<<<RED_BLOCKS, RED_THREADS, 0, st>>>(len, r, p, v, ctx->sc);
+    ++ctx->launches;
+    TRY(precond_apply(ctx, p, phat));
+    int nb1 = 0;
+    TRY(spmv<1>(ctx, phat, v, rhat, nullptr, &nb1));
+    TRY(K.finalize1(nb1, S_DEN));
+    // speculative s = r - alpha v, ||s||^2 (used only if den is not a breakdown)
+    k_update_s<<<RED_BLOCKS, RED_THREADS, 0, st>>>(len, r, v, s, ctx->sc, ctx->partial);
+    ++ctx->launches;
+    TRY(K.finalize1(RED_BLOCKS, S_SS));
+    TRY(K.read_scalars());
+    const double den = sh[S_DEN];
+    if (std::fabs(den) < brk) {
+      if (restarted) { g_err = "BiCGSTAB denominator breakdown"; *iters = it; return ISC_BREAKDOWN; }
+      TRY(restart());
+      TRY(K.push());
+      TRY(K.dot(rhat, r, S_RHO_NEW));
+      TRY(K.read_scalars());
+      continue;
+    }
+    sh[S_ALPHA] = rho / den;
+    if (std::sqrt(sh[S_SS]) / nb <= tol) {
+      TRY(K.push());
+      k_axpy_alpha<<<RED_BLOCKS, RED_THREADS, 0, st>>>(len, x, phat, ctx->sc);
+      ++ctx->launches;
+      *iters = it;
+      CK(cudaStreamSynchronize(st));
+      return ISC_OK;
+    }
+    TRY(K.push());
+    TRY(precond_apply(ctx, s, shat));
+    int nb2 = 0;
+    TRY(spmv<2>(ctx, shat, t, nullptr, s, &nb2));
+    TRY(K.finalize2(nb2, S_TT, S_TS));
+    k_update_xr<<<RED_BLOCKS, RED_THREADS, 0, st>>>(len, x, phat, shat, r, s, t, rhat, ctx->sc,
+                                                     ctx->partial);
+    ++ctx->launches;
+    TRY(K.finalize2(RED_BLOCKS, S_RR, S_RHO_NEW));
+    TRY(K.read_scalars());
+    const double tt = sh[S_TT];
+    if (tt == 0.0) {
+      if (restarted) { g_err = "BiCGSTAB stagnated (t = 0)"; *iters = it; return ISC_BREAKDOWN; }
+      TRY(restart());
+      TRY(K.push());
+      TRY(K.dot(rhat, r, S_RHO_NEW));
+      TRY(K.read_scalars());
+      continue;
+    }
+    sh[S_OMEGA] = sh[S_TS] / tt;
+    if (std::sqrt(sh[S_RR]) / nb <= tol) { *iters = it; return ISC_OK; }
+    sh[S_RHO_OLD] = rho;
+  }
+  *iters = it;
+  g_err = "BiCGSTAB did not converge";
+  return ISC_MAX_ITERATIONS;
+}
+
+extern "C" int isc_solve(isc_ctx* ctx, double tol, int32_t maxiter, double* d_du, double* h_dbhp,
+                         int32_t* iters, int64_t* bad_cell, int32_t* bad_col) {
+  if (!ctx->decoupled) {
+    int s = isc_decouple(ctx, bad_cell, bad_col);
+    if (s) return s;
+  }
+  if (!ctx->factored) {
+    int s = isc_precond_setup(ctx, bad_cell);
+    if (s) {
+      if (bad_col) *bad_col = -1;
+      return s;
+    }
+  }
+  int it = 0;
+  STAGE(stage_begin(ctx, 3));
+  int status = bicgstab(ctx, tol, maxiter, &it);
+  STAGE(stage_end(ctx, 3));
+  if (iters) *iters = it;
+  if (status) return status;
+  const int64_t n = ctx->g.n;
+  CK(cudaMemcpyAsync(d_du, ctx->xk, (size_t)NU * n * 8, cudaMemcpyDeviceToDevice, ctx->stream));
+  // bhp back-substitution dbhp = -(r_w + wrow . du_c) / dwdb (linsolve.py:473-478)
+  if (ctx->nw > 0 && h_dbhp) {
+    std::vector<double> duc(NU);
+    for (int w = 0; w < ctx->nw; ++w) {
+      const int64_t c = ctx->wcell_h[w];
+      for (int u = 0; u < NU; ++u)
+        CK(cudaMemcpyAsync(&duc[u], ctx->xk + (int64_t)u * n + c, 8, cudaMemcpyDeviceToHost,
+                           ctx->stream));
+      CK(cudaStreamSynchronize(ctx->stream));
+      const double* o = ctx->wout_h + w * WOUT;
+      double dotv = 0.0;
+      for (int u = 0; u < NU; ++u) dotv += o[2 + u] * duc[u];
+      const double s = o[0] + dotv;
+      h_dbhp[w] = -s / o[1];
+    }
+  }
+  CK(cudaStreamSynchronize(ctx->stream));
+  return ISC_OK;
+}
+
+// -------------------------------------------------------------- Newton
+
+extern "C" int isc_newton_update(isc_ctx* ctx, double* d_state, const double* d_du, double eps) {
+  k_newton_update<<<grid1d(ctx->g.n, 256), 256, 0, ctx->stream>>>(ctx->g.n, d_state, d_du, eps);
+  LAUNCH_CHECK();
+  CK(cudaStreamSynchronize(ctx->stream));
+  return ISC_OK;
+}
+
+extern "C" int isc_scaled_norm(isc_ctx* ctx, const double* d_accn, double dt, double* norm) {
+  k_norm_partial<<<RED_BLOCKS, 256, 0, ctx->stream>>>(ctx->g.n, ctx->resid, d_accn, ctx->vol, dt,
+                                                     ctx->partial);
+  LAUNCH_CHECK();
+  std::vector<double> part(RED_BLOCKS);
+  CK(cudaMemcpyAsync(part.data(), ctx->partial, RED_BLOCKS * 8, cudaMemcpyDeviceToHost,
+                     ctx->stream));
+  CK(cudaStreamSynchronize(ctx->stream));
+  double m = 0.0;
+  bool nan = false;
+  for (double v : part) {
+    if (v != v) nan = true;
+    m = std::max(m, v);
+  }
+  *norm = nan ? NAN : m;
+  return ISC_OK;
+}
+
+extern "C" int isc_audit_sums(isc_ctx* ctx, const double* d_accn, double* h_out) {
+  constexpr int NR = NF + 1;
+  k_audit_partial<<<RED_BLOCKS, 256, 0, ctx->stream>>>(ctx->g.n, ctx->acc, d_accn, ctx->src,
+                                                      ctx->vol, ctx->partial);
+  LAUNCH_CHECK();
+  std::vector<double> part((size_t)3 * NR * RED_BLOCKS);
+  CK(cudaMemcpyAsync(part.data(), ctx->partial, part.size() * 8, cudaMemcpyDeviceToHost,
+                     ctx->stream));
+  CK(cudaStreamSynchronize(ctx->stream));
+  for (int k = 0; k < 3 * NR; ++k) {
+    double s = 0.0;
+    for (int b = 0; b < RED_BLOCKS; ++b) s += part[(size_t)k * RED_BLOCKS + b];
+    h_out[k] = s;
+  }
+  return ISC_OK;
+}

@@ -1,0 +1,82 @@
+// Shared definitions for the sm_100a Newton hot path (fp64 throughout).
+//
+// Per-cell unknown (column) order and residual (row) order follow the
+// reference (_kernels.py:11-16):
+//   columns  p, x_0..x_{nco-1}, y_0..y_{ncg-1}, T, S_w, S_g, C_c
+//   rows     F_W, F_O[..], F_G[..], F_E, F_OS, F_GS, F_Coke
+// The library is compiled for the reference's benchmark fluid
+// (nco = 2 oils, ncg = 2 gases, block size 9); other compositions are
+// rejected at context creation.
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace isc {
+
+constexpr int NCO = 2;
+constexpr int NCG = 2;
+constexpr int NF = 1 + NCO + NCG;   // full gas composition entries
+constexpr int NU = NCO + NCG + 5;   // block size (9)
+constexpr int CT = 1 + NCO + NCG;   // T column / energy row
+constexpr int CSW = CT + 1, CSG = CT + 2, CCC = CT + 3;
+constexpr int ROW_E = CT, ROW_OS = CT + 1, ROW_GS = CT + 2, ROW_CK = CT + 3;
+constexpr int NB = NU * NU;         // 81 entries per block
+constexpr int NDIR = 6;             // -z, -y, -x, +x, +y, +z
+constexpr int MAXREAC = 8;
+constexpr int MAXTAB = 32;
+
+constexpr double RANKINE = 459.67;
+constexpr double R_GAS = 10.7316;
+constexpr double R_ARR = 1.9859;
+constexpr double PSI_PER_FT = 1.0 / 144.0;
+
+// Flattened model constants, passed by value as a kernel parameter (lands in
+// the constant bank; every thread reads the same words).  Layout mirrors the
+// reference ModelPack tables (assembly.py:42-68, _kernels.py:48-63).
+struct Model {
+  double liq[1 + NCO][10];
+  double gasp[NF][9];
+  double kv[1 + NCO][5];
+  double rockp[17];
+  double swt_s[MAXTAB], swt_krw[MAXTAB], swt_krow[MAXTAB], swt_pcow[MAXTAB];
+  double slt_s[MAXTAB], slt_krg[MAXTAB], slt_krog[MAXTAB], slt_pcog[MAXTAB];
+  double rcoef[MAXREAC][3];
+  double nmat[NF + 1][MAXREAC];
+  int law[MAXREAC], fuel[MAXREAC], ox[MAXREAC];
+  int nreac, nswt, nslt, heavy;
+  double ccmax;
+};
+
+enum { L_RHO = 0, L_CP, L_CT1, L_CT2, L_CPT, L_AVISC, L_BVISC, L_HVR, L_EV, L_TCF };
+enum { G_M = 0, G_TCR, G_PC, G_AVG, G_BVG, G_CPG1, G_CPG2, G_CPG3, G_CPG4 };
+enum {
+  RK_CPOR = 0, RK_CTPOR, RK_CPTPOR, RK_MODE, RK_CP1, RK_CP2, RK_COKE_CP, RK_RHO_COKE,
+  RK_KTW, RK_KTO, RK_KTG, RK_KTR, RK_KTC, RK_PREF, RK_TREF, RK_EPS_PER, RK_KROCW
+};
+
+// Structured grid geometry (x fastest: c = i + nx*(j + ny*k)).
+struct Dims {
+  int nx, ny, nz;
+  int64_t n;       // nx*ny*nz
+  int64_t nxny;
+};
+
+// Direction d of a neighbour, in the reference's gather order
+// (ascending connection index seen from a cell, _kernels.py:828-854).
+enum { DZM = 0, DYM = 1, DXM = 2, DXP = 3, DYP = 4, DZP = 5 };
+
+__host__ __device__ inline int opposite(int d) { return 5 - d; }
+
+// neighbour of cell c in direction d, or -1 at the boundary
+__device__ __forceinline__ int64_t neighbour(const Dims& g, int64_t c, int i, int j, int k, int d) {
+  switch (d) {
+    case DZM: return k > 0 ? c - g.nxny : -1;
+    case DYM: return j > 0 ? c - g.nx : -1;
+    case DXM: return i > 0 ? c - 1 : -1;
+    case DXP: return i + 1 < g.nx ? c + 1 : -1;
+    case DYP: return j + 1 < g.ny ? c + g.nx : -1;
+    default:  return k + 1 < g.nz ? c + g.nxny : -1;
+  }
+}
+
+}  // namespace isc

@@ -1,0 +1,147 @@
+// Well Schur fold + block Gauss-Jordan decoupling of every block row.
+//
+// Restates linsolve.py:362-394 (well elimination, single perforation) and
+// linsolve.py:70-152 (GJ with partial pivoting, pivot tolerance
+// 1e-13*max|D|, D^-1 applied to the row's rhs and off-diagonal blocks).
+//
+// B200 mapping: one CTA = 32 cells x 32 column-pairs (1024 threads). The
+// thread (cell, j) owns columns j and j+32 of the cell's augmented block row
+// [D | B_-z B_-y B_-x B_+x B_+y B_+z | rhs] (9 x 64): loads and stores of a
+// warp are 32 consecutive cells of one column -> fully coalesced 256 B
+// transactions. Row operations on a column need only the pivot column,
+// which is broadcast through shared memory (9 doubles per cell per step).
+// The decoupled diagonal (D^-1 D, identity up to rounding; the reference
+// stores it, Appendix A.11) is not written: SpMV/ILU use an exact identity.
+#include "common.cuh"
+
+namespace isc {
+
+// rhs = -resid, then fold each well's bhp unknown into its perforated cell.
+__global__ void k_rhs_schur(Dims g, const double* __restrict__ resid, double* rhs, double* diag,
+                            int nw, const int64_t* __restrict__ wcell,
+                            const double* __restrict__ wout, int wstride) {
+  const int64_t n = g.n;
+  const int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (c >= n) return;
+#pragma unroll
+  for (int r = 0; r < NU; ++r) rhs[r * n + c] = -resid[r * n + c];
+  for (int w = 0; w < nw; ++w) {
+    if (wcell[w] != c) continue;
+    const double* o = wout + (int64_t)w * wstride;
+    const double resid_w = o[0], dwdb = o[1];
+    const double* wrow = o + 2;
+    const double* bcol = o + 2 + NU;
+    const double inv_d = 1.0 / dwdb;
+#pragma unroll
+    for (int r = 0; r < NU; ++r) {
+      rhs[r * n + c] += bcol[r] * (resid_w * inv_d);
+#pragma unroll
+      for (int u = 0; u < NU; ++u) diag[(int64_t)(r * NU + u) * n + c] -= bcol[r] * wrow[u] * inv_d;
+    }
+  }
+}
+
+constexpr int DC_CELLS = 32;
+constexpr int NCOLS = NU + NDIR * NU + 1;   // 64
+static_assert(NCOLS == 64, "augmented row must be 64 columns");
+
+__device__ __forceinline__ double* col_ptr(int j, int r, int64_t n, int64_t c, double* diag,
+                                           double* offd, double* rhs) {
+  if (j < NU) return diag + (int64_t)(r * NU + j) * n + c;
+  if (j < NU + NDIR * NU) {
+    const int d = (j - NU) / NU, u = (j - NU) % NU;
+    return offd + (int64_t)((d * NU + r) * NU + u) * n + c;
+  }
+  return rhs + (int64_t)r * n + c;
+}
+
+__global__ void __launch_bounds__(1024) k_decouple(Dims g, double* diag, double* offd, double* rhs,
+                                                   int* flags, unsigned long long* bad) {
+  __shared__ double colk[NU][DC_CELLS];
+  __shared__ double cmax[NU][DC_CELLS];
+  __shared__ int piv_s[DC_CELLS];
+  __shared__ int failc[DC_CELLS];
+  const int64_t n = g.n;
+  const int lane = threadIdx.x, jy = threadIdx.y;
+  const int64_t c = (int64_t)blockIdx.x * DC_CELLS + lane;
+  const bool live = c < n;
+  const int j0 = jy, j1 = jy + 32;
+  double a0[NU], a1[NU];
+#pragma unroll
+  for (int r = 0; r < NU; ++r) {
+    a0[r] = live ? *col_ptr(j0, r, n, c, diag, offd, rhs) : (r == j0 ? 1.0 : 0.0);
+    a1[r] = live ? *col_ptr(j1, r, n, c, diag, offd, rhs) : 0.0;
+  }
+  // tolerance: 1e-13 * max |D| (linsolve.py:77-86)
+  if (jy < NU) {
+    double m = 0.0;
+#pragma unroll
+    for (int r = 0; r < NU; ++r) m = fmax(m, fabs(a0[r]));
+    cmax[jy][lane] = m;
+  }
+  if (jy == 0) failc[lane] = NU;
+  __syncthreads();
+  double amax = 0.0;
+#pragma unroll
+  for (int u = 0; u < NU; ++u) amax = fmax(amax, cmax[u][lane]);
+  const double tol = 1e-13 * amax;
+#pragma unroll
+  for (int k = 0; k < NU; ++k) {
+    if (jy == k) {
+      int piv = k;
+      double pv = fabs(a0[k]);
+#pragma unroll
+      for (int r = k + 1; r < NU; ++r) {
+        const double v = fabs(a0[r]);
+        if (v > pv) { pv = v; piv = r; }
+      }
+      if (pv <= tol || amax == 0.0) atomicMin(&failc[lane], amax == 0.0 ? 0 : k);
+#pragma unroll
+      for (int r = 0; r < NU; ++r) {
+        double v = a0[r];
+        if (r == k) {
+#pragma unroll
+          for (int q = k + 1; q < NU; ++q) if (q == piv) v = a0[q];
+        } else if (r == piv) {
+          v = a0[k];
+        }
+        colk[r][lane] = v;
+      }
+      piv_s[lane] = piv;
+    }
+    __syncthreads();
+    const int piv = piv_s[lane];
+    if (piv != k) {   // swap rows k and piv in both owned columns
+      double t0 = a0[k], t1 = a1[k];
+#pragma unroll
+      for (int q = k + 1; q < NU; ++q)
+        if (q == piv) { a0[k] = a0[q]; a1[k] = a1[q]; a0[q] = t0; a1[q] = t1; }
+    }
+    const double dinv = 1.0 / colk[k][lane];
+    a0[k] *= dinv;
+    a1[k] *= dinv;
+#pragma unroll
+    for (int r = 0; r < NU; ++r) {
+      if (r == k) continue;
+      const double f = colk[r][lane];
+      if (f != 0.0) {
+        a0[r] -= f * a0[k];
+        a1[r] -= f * a1[k];
+      }
+    }
+    __syncthreads();
+  }
+  if (!live) return;
+  if (jy == 0 && failc[lane] < NU) {   // first failing pivot column (linsolve.py:98-99)
+    flags[c] = failc[lane] + 1;
+    atomicMin(bad, (unsigned long long)c);
+  }
+  if (j0 >= NU) {
+#pragma unroll
+    for (int r = 0; r < NU; ++r) *col_ptr(j0, r, n, c, diag, offd, rhs) = a0[r];
+  }
+#pragma unroll
+  for (int r = 0; r < NU; ++r) *col_ptr(j1, r, n, c, diag, offd, rhs) = a1[r];
+}
+
+}  // namespace isc

@@ -1,0 +1,431 @@
+// Decoupled-system operators: 7-point BSR SpMV, fused Krylov vector updates
+// with deterministic dot products, and the reference's subdomain block
+// ILU(0) (bjacobi / RAS) run as a level-scheduled wavefront.
+//
+// Vectors are SoA v[r*n + c]. The decoupled diagonal block is the identity
+// (decouple.cu), so  y = x + sum_d B_d x_{nb_d}  (linsolve.py:159-177).
+#include <cooperative_groups.h>
+#include "common.cuh"
+
+namespace cg = cooperative_groups;
+
+namespace isc {
+
+constexpr int RED_BLOCKS = 148 * 8;   // fixed partition -> deterministic sums
+constexpr int RED_THREADS = 256;
+
+// Krylov scalar slots in device memory (host mirror reads them)
+enum {
+  S_RHO = 0, S_RHO_OLD, S_ALPHA, S_OMEGA, S_DEN, S_SS, S_TT, S_TS, S_RR, S_RHO_NEW, S_BB,
+  S_FIRST, S_NSCAL
+};
+
+template <int K>
+__device__ __forceinline__ void block_reduce_store(double (&v)[K], double* partial) {
+  __shared__ double sh[K][32];
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  const int tid = threadIdx.x + threadIdx.y * blockDim.x;
+  const int lane2 = tid & 31, wid2 = tid >> 5;
+  (void)lane; (void)wid;
+#pragma unroll
+  for (int k = 0; k < K; ++k) {
+    double x = v[k];
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) x += __shfl_down_sync(0xffffffffu, x, o);
+    if (lane2 == 0) sh[k][wid2] = x;
+  }
+  __syncthreads();
+  const int nwarps = (blockDim.x * blockDim.y) >> 5;
+  if (tid == 0) {
+#pragma unroll
+    for (int k = 0; k < K; ++k) {
+      double s = 0.0;
+      for (int w = 0; w < nwarps; ++w) s += sh[k][w];
+      partial[k * gridDim.x + blockIdx.x] = s;
+    }
+  }
+}
+
+// sum the per-block partials in fixed order into sc[slot_k] (256 threads)
+template <int K>
+__global__ void __launch_bounds__(256) k_finalize(const double* __restrict__ partial, int nparts,
+                                                  double* sc, int s0, int s1, int s2) {
+  const int slots[3] = {s0, s1, s2};
+  __shared__ double sh[K][8];
+  const int t = threadIdx.x, lane = t & 31, w = t >> 5;
+#pragma unroll
+  for (int k = 0; k < K; ++k) {
+    double s = 0.0;
+    for (int i = t; i < nparts; i += 256) s += partial[(int64_t)k * nparts + i];
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) s += __shfl_down_sync(0xffffffffu, s, o);
+    if (lane == 0) sh[k][w] = s;
+  }
+  __syncthreads();
+  if (t == 0) {
+#pragma unroll
+    for (int k = 0; k < K; ++k) {
+      double s = 0.0;
+      for (int i = 0; i < 8; ++i) s += sh[k][i];
+      sc[slots[k]] = s;
+    }
+  }
+}
+
+// partial dot products of up to 3 vector pairs over len entries
+template <int K>
+__global__ void __launch_bounds__(RED_THREADS) k_dots(int64_t len, const double* a0, const double* b0,
+                                                      const double* a1, const double* b1,
+                                                      const double* a2, const double* b2,
+                                                      double* partial) {
+  double acc[K];
+#pragma unroll
+  for (int k = 0; k < K; ++k) acc[k] = 0.0;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < len;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    acc[0] += a0[i] * b0[i];
+    if (K > 1) acc[K > 1 ? 1 : 0] += a1[i] * b1[i];
+    if (K > 2) acc[K > 2 ? 2 : 0] += a2[i] * b2[i];
+  }
+  block_reduce_store<K>(acc, partial);
+}
+
+// ------------------------------------------------------------------- SpMV
+// y = x + sum_d B_d x_nb ; optional fused partial dots of y with (w0, w1):
+// grid (ceil(n/32)), block (32, NU): thread (c, r).
+template <int K>
+__global__ void __launch_bounds__(32 * NU) k_spmv(Dims g, const double* __restrict__ offd,
+                                                  const double* __restrict__ x,
+                                                  double* __restrict__ y,
+                                                  const double* __restrict__ w0,
+                                                  const double* __restrict__ w1,
+                                                  double* partial) {
+  const int64_t n = g.n;
+  const int64_t c = (int64_t)blockIdx.x * 32 + threadIdx.x;
+  const int r = threadIdx.y;
+  constexpr int KK = K > 0 ? K : 1;
+  double acc[KK];
+#pragma unroll
+  for (int k = 0; k < KK; ++k) acc[k] = 0.0;
+  if (c < n) {
+    const int i = (int)(c % g.nx), j = (int)((c / g.nx) % g.ny), k = (int)(c / g.nxny);
+    double s = x[r * n + c];
+#pragma unroll
+    for (int d = 0; d < NDIR; ++d) {
+      const int64_t nb = neighbour(g, c, i, j, k, d);
+      if (nb < 0) continue;
+      const double* blk = offd + (int64_t)((d * NU + r) * NU) * n + c;
+      double t = 0.0;
+#pragma unroll
+      for (int u = 0; u < NU; ++u) t += __ldg(blk + (int64_t)u * n) * __ldg(x + (int64_t)u * n + nb);
+      s += t;
+    }
+    y[r * n + c] = s;
+    // K == 1: (y . w0) ; K == 2: (y . y, y . w1)
+    if (K == 1) acc[0] = s * w0[r * n + c];
+    if (K == 2) { acc[0] = s * s; acc[K > 1 ? 1 : 0] = s * w1[r * n + c]; }
+  }
+  if (K > 0) block_reduce_store<KK>(acc, partial);
+}
+
+// --------------------------------------------------------- vector kernels
+// p = r + beta (p - omega v),  beta = (rho/rho_old)(alpha/omega); or p = r
+__global__ void k_update_p(int64_t len, const double* __restrict__ r, double* __restrict__ p,
+                           const double* __restrict__ v, const double* __restrict__ sc) {
+  const bool first = sc[S_FIRST] != 0.0;
+  const double beta = (sc[S_RHO] / sc[S_RHO_OLD]) * (sc[S_ALPHA] / sc[S_OMEGA]);
+  const double omega = sc[S_OMEGA];
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < len;
+       i += (int64_t)gridDim.x * blockDim.x)
+    p[i] = first ? r[i] : r[i] + beta * (p[i] - omega * v[i]);
+}
+
+// alpha = rho/den; s = r - alpha v; partial s.s
+__global__ void __launch_bounds__(RED_THREADS) k_update_s(int64_t len, const double* __restrict__ r,
+                                                          const double* __restrict__ v,
+                                                          double* __restrict__ s, double* sc,
+                                                          double* partial) {
+  const double alpha = sc[S_RHO] / sc[S_DEN];
+  double acc[1] = {0.0};
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < len;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const double si = r[i] - alpha * v[i];
+    s[i] = si;
+    acc[0] += si * si;
+  }
+  block_reduce_store<1>(acc, partial);
+}
+
+__global__ void k_store_alpha(double* sc) { sc[S_ALPHA] = sc[S_RHO] / sc[S_DEN]; }
+
+// x += alpha phat
+__global__ void k_axpy_alpha(int64_t len, double* __restrict__ x, const double* __restrict__ ph,
+                             const double* __restrict__ sc) {
+  const double alpha = sc[S_ALPHA];
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < len;
+       i += (int64_t)gridDim.x * blockDim.x)
+    x[i] += alpha * ph[i];
+}
+
+// omega = ts/tt; x += alpha phat + omega shat; r = s - omega t; partial r.r, rhat.r
+__global__ void __launch_bounds__(RED_THREADS) k_update_xr(int64_t len, double* __restrict__ x,
+                                                           const double* __restrict__ ph,
+                                                           const double* __restrict__ sh_,
+                                                           double* __restrict__ r,
+                                                           const double* __restrict__ s,
+                                                           const double* __restrict__ t,
+                                                           const double* __restrict__ rhat,
+                                                           const double* sc, double* partial) {
+  const double tt = sc[S_TT];
+  double acc[2] = {0.0, 0.0};
+  if (tt != 0.0) {
+    const double alpha = sc[S_ALPHA];
+    const double omega = sc[S_TS] / tt;
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < len;
+         i += (int64_t)gridDim.x * blockDim.x) {
+      x[i] += alpha * ph[i] + omega * sh_[i];
+      const double ri = s[i] - omega * t[i];
+      r[i] = ri;
+      acc[0] += ri * ri;
+      acc[1] += rhat[i] * ri;
+    }
+  }
+  block_reduce_store<2>(acc, partial);
+}
+
+__global__ void k_sub(int64_t len, const double* __restrict__ a, const double* __restrict__ b,
+                      double* __restrict__ out) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < len;
+       i += (int64_t)gridDim.x * blockDim.x)
+    out[i] = a[i] - b[i];
+}
+
+// --------------------------------------------------- subdomain ILU(0)
+//
+// Slots: every (subdomain, extended cell) pair, numbered level-major where
+// the level of a cell inside its subdomain box is (i-x0)+(j-y0)+(k-z0);
+// cells of one level depend only on the previous level (natural-order
+// ILU(0) on a 7-point stencil == block D-ILU, linsolve.py:206-259).
+struct IluDev {
+  int64_t nslots;
+  const int64_t* __restrict__ cell;    // global cell of a slot
+  const int8_t* __restrict__ owned;    // slot owns its cell (RAS restriction)
+  const int64_t* __restrict__ lo;      // [3*nslots] lower neighbour slots (-z,-y,-x) or -1
+  const int64_t* __restrict__ up;      // [3*nslots] upper neighbour slots (+x,+y,+z) or -1
+  double* lblk;                        // [(q*NB + e)*nslots + s]  A_cj U_jj^-1
+  double* uinv;                        // [e*nslots + s]
+  double* zs;                          // [r*nslots + s] local solution
+};
+
+constexpr int IL_SLOTS = 32;
+
+// U = I - sum_j (A_cj U_j^-1) A_jc ; uinv = U^-1 (GJ, partial pivoting)
+__device__ void ilu_factor_tile(const Dims& g, const IluDev& L, const double* __restrict__ offd,
+                                int64_t s0, int64_t s1, int* fail) {
+  __shared__ double lsh[NU][NU][IL_SLOTS];   // one lblk (row, col) for the tile
+  __shared__ double colk[2 * NU][IL_SLOTS];
+  __shared__ int pivs[IL_SLOTS];
+  const int64_t n = g.n;
+  const int ls = threadIdx.x, u = threadIdx.y;   // slot lane, owned column
+  const int64_t s = s0 + ls;
+  const bool live = s < s1;
+  const int64_t ns = L.nslots;
+  const int64_t c = live ? L.cell[s] : 0;
+  // own column u of U (starts at the identity: decoupled diagonal)
+  double ucol[NU];
+#pragma unroll
+  for (int r = 0; r < NU; ++r) ucol[r] = (r == u) ? 1.0 : 0.0;
+  const int dlo[3] = {DZM, DYM, DXM};
+#pragma unroll 1
+  for (int q = 0; q < 3; ++q) {
+    const int64_t sj = live ? L.lo[q * ns + s] : -1;
+    // lblk[:, u] = A_cj * Uinv_j[:, u]
+    double lc[NU];
+#pragma unroll
+    for (int r = 0; r < NU; ++r) lc[r] = 0.0;
+    if (sj >= 0) {
+      const double* Acj = offd + (int64_t)(dlo[q] * NB) * n + c;
+      double uj[NU];
+#pragma unroll
+      for (int k = 0; k < NU; ++k) uj[k] = L.uinv[(int64_t)(k * NU + u) * ns + sj];
+#pragma unroll
+      for (int r = 0; r < NU; ++r) {
+        double t = 0.0;
+#pragma unroll
+        for (int k = 0; k < NU; ++k) t += Acj[(int64_t)(r * NU + k) * n] * uj[k];
+        lc[r] = t;
+      }
+#pragma unroll
+      for (int r = 0; r < NU; ++r) L.lblk[(int64_t)(q * NB + r * NU + u) * ns + s] = lc[r];
+    }
+#pragma unroll
+    for (int r = 0; r < NU; ++r) lsh[r][u][ls] = lc[r];
+    __syncthreads();
+    if (sj >= 0) {
+      // U[:, u] -= lblk * A_jc[:, u]
+      const int64_t cj = L.cell[sj];
+      const double* Ajc = offd + (int64_t)(opposite(dlo[q]) * NB) * n + cj;
+      double ac[NU];
+#pragma unroll
+      for (int k = 0; k < NU; ++k) ac[k] = Ajc[(int64_t)(k * NU + u) * n];
+#pragma unroll
+      for (int r = 0; r < NU; ++r) {
+        double t = 0.0;
+#pragma unroll
+        for (int k = 0; k < NU; ++k) t += lsh[r][k][ls] * ac[k];
+        ucol[r] -= t;
+      }
+    }
+    __syncthreads();
+  }
+  // Gauss-Jordan inverse of U; thread owns column u of U and column u of inv
+  double icol[NU];
+#pragma unroll
+  for (int r = 0; r < NU; ++r) icol[r] = (r == u) ? 1.0 : 0.0;
+  // tolerance 1e-13 * max|U|
+  {
+    double m = 0.0;
+#pragma unroll
+    for (int r = 0; r < NU; ++r) m = fmax(m, fabs(ucol[r]));
+    lsh[0][u][ls] = m;
+  }
+  __syncthreads();
+  double amax = 0.0;
+#pragma unroll
+  for (int k = 0; k < NU; ++k) amax = fmax(amax, lsh[0][k][ls]);
+  const double tol = 1e-13 * amax;
+  __syncthreads();
+#pragma unroll
+  for (int k = 0; k < NU; ++k) {
+    if (u == k) {
+      int piv = k;
+      double pv = fabs(ucol[k]);
+#pragma unroll
+      for (int r = k + 1; r < NU; ++r) {
+        const double v = fabs(ucol[r]);
+        if (v > pv) { pv = v; piv = r; }
+      }
+      if ((pv <= tol || amax == 0.0) && live) atomicMin(fail, 1);
+#pragma unroll
+      for (int r = 0; r < NU; ++r) {
+        double v = ucol[r];
+        if (r == k) {
+#pragma unroll
+          for (int q2 = k + 1; q2 < NU; ++q2) if (q2 == piv) v = ucol[q2];
+        } else if (r == piv) {
+          v = ucol[k];
+        }
+        colk[r][ls] = v;
+      }
+      pivs[ls] = piv;
+    }
+    __syncthreads();
+    const int piv = pivs[ls];
+    if (piv != k) {
+      double t0 = ucol[k], t1 = icol[k];
+#pragma unroll
+      for (int q2 = k + 1; q2 < NU; ++q2)
+        if (q2 == piv) { ucol[k] = ucol[q2]; icol[k] = icol[q2]; ucol[q2] = t0; icol[q2] = t1; }
+    }
+    const double dinv = 1.0 / colk[k][ls];
+    ucol[k] *= dinv;
+    icol[k] *= dinv;
+#pragma unroll
+    for (int r = 0; r < NU; ++r) {
+      if (r == k) continue;
+      const double f = colk[r][ls];
+      if (f != 0.0) {
+        ucol[r] -= f * ucol[k];
+        icol[r] -= f * icol[k];
+      }
+    }
+    __syncthreads();
+  }
+  if (live) {
+#pragma unroll
+    for (int r = 0; r < NU; ++r) L.uinv[(int64_t)(r * NU + u) * ns + s] = icol[r];
+  }
+}
+
+__global__ void __launch_bounds__(IL_SLOTS * NU) k_ilu_factor(Dims g, IluDev L, const double* offd,
+                                                              const int64_t* lvl_ptr, int nlev,
+                                                              int* fail) {
+  cg::grid_group grid = cg::this_grid();
+  for (int lev = 0; lev < nlev; ++lev) {
+    const int64_t b = lvl_ptr[lev], e = lvl_ptr[lev + 1];
+    for (int64_t s0 = b + (int64_t)blockIdx.x * IL_SLOTS; s0 < e; s0 += (int64_t)gridDim.x * IL_SLOTS)
+      ilu_factor_tile(g, L, offd, s0, e, fail);
+    grid.sync();
+  }
+}
+
+// forward then backward sweep; z_out (global, SoA) gets owned slots
+__global__ void __launch_bounds__(IL_SLOTS * NU) k_ilu_apply(Dims g, IluDev L, const double* offd,
+                                                             const int64_t* lvl_ptr, int nlev,
+                                                             const double* __restrict__ rin,
+                                                             double* __restrict__ zout) {
+  cg::grid_group grid = cg::this_grid();
+  __shared__ double wsh[NU][IL_SLOTS];
+  const int64_t n = g.n, ns = L.nslots;
+  const int ls = threadIdx.x, r = threadIdx.y;
+  // forward: z_c = r_c - sum_j lblk_cj z_j   (lower j in order -z,-y,-x)
+  for (int lev = 0; lev < nlev; ++lev) {
+    const int64_t b = lvl_ptr[lev], e = lvl_ptr[lev + 1];
+    for (int64_t s = b + (int64_t)blockIdx.x * IL_SLOTS + ls; s - ls < e;
+         s += (int64_t)gridDim.x * IL_SLOTS) {
+      if (s >= e) continue;
+      const int64_t c = L.cell[s];
+      double z = rin[r * n + c];
+#pragma unroll
+      for (int q = 0; q < 3; ++q) {
+        const int64_t sj = L.lo[q * ns + s];
+        if (sj < 0) continue;
+        double t = 0.0;
+#pragma unroll
+        for (int u = 0; u < NU; ++u)
+          t += L.lblk[(int64_t)(q * NB + r * NU + u) * ns + s] * L.zs[(int64_t)u * ns + sj];
+        z -= t;
+      }
+      L.zs[(int64_t)r * ns + s] = z;
+    }
+    grid.sync();
+  }
+  // backward: z_c = U_c^-1 (z_c - sum_j A_cj z_j)   (upper j in order +x,+y,+z)
+  const int dup[3] = {DXP, DYP, DZP};
+  for (int lev = nlev - 1; lev >= 0; --lev) {
+    const int64_t b = lvl_ptr[lev], e = lvl_ptr[lev + 1];
+    for (int64_t s0 = b + (int64_t)blockIdx.x * IL_SLOTS; s0 < e; s0 += (int64_t)gridDim.x * IL_SLOTS) {
+      const int64_t s = s0 + ls;
+      const bool live = s < e;
+      double w = 0.0;
+      int64_t c = 0;
+      if (live) {
+        c = L.cell[s];
+        w = L.zs[(int64_t)r * ns + s];
+#pragma unroll
+        for (int q = 0; q < 3; ++q) {
+          const int64_t sj = L.up[q * ns + s];
+          if (sj < 0) continue;
+          const double* Acj = offd + (int64_t)((dup[q] * NU + r) * NU) * n + c;
+          double t = 0.0;
+#pragma unroll
+          for (int u = 0; u < NU; ++u) t += Acj[(int64_t)u * n] * L.zs[(int64_t)u * ns + sj];
+          w -= t;
+        }
+      }
+      wsh[r][ls] = w;
+      __syncthreads();
+      if (live) {
+        double z = 0.0;
+#pragma unroll
+        for (int u = 0; u < NU; ++u) z += L.uinv[(int64_t)(r * NU + u) * ns + s] * wsh[u][ls];
+        L.zs[(int64_t)r * ns + s] = z;
+        if (L.owned[s]) zout[r * n + c] = z;
+      }
+      __syncthreads();
+    }
+    grid.sync();
+  }
+}
+
+}  // namespace isc

@@ -1,0 +1,182 @@
+"""GPU parity: the sm_100a path (through the C-ABI) against the reference's
+golden fixtures and the CPU oracle on identical seeded inputs.
+
+Bars (north_star): Jacobian/residual entries within 1e-10 (row-scaled, see
+tests/helpers.row_scaled_err and SURVEY §8(c)); converged p, T, S fields
+within 1e-6 relative with LINEAR_TOL 1e-10; equal Newton counts.
+"""
+
+import numpy as np
+import pytest
+import torch
+
+from paper_1811_11992_b200 import record
+from paper_1811_11992_b200.assembly import Workspace, assemble
+from paper_1811_11992_b200.linsolve import BlockSolver, load_system
+from paper_1811_11992_b200.errors import (MaxIterations, PoreSpaceExhausted,
+                                          SingularCellBlock)
+from tests.helpers import (case_objects, golden, row_scaled_err, scaled_resid_err,
+                           state_from)
+
+pytestmark = pytest.mark.gpu
+
+JTOL = 1e-10
+
+
+def _ws(c, precond="ras"):
+    return Workspace(c.grid, c.pack, None, wells=c.wells, streams=c.streams, precond=precond)
+
+
+@pytest.fixture(scope="module")
+def small():
+    g = golden("asm_small3d.npz")
+    c = case_objects("small3d")
+    ws = _ws(c)
+    blocks = assemble(c.grid, c.pack, ws, c.wells, c.streams, state_from(g), g["accn"],
+                      float(g["dt"]), float(g["t_new"]), g["capped"])
+    return g, c, ws, blocks
+
+
+def test_cell_record_vs_reference(small):
+    g, c, ws, _ = small
+    rec = ws.ctx.copy_out(4, record.NREC).cpu().numpy()
+    dense = record.expand(rec)
+    for f, v in dense.items():
+        err = row_scaled_err(v, g[f])
+        assert err <= JTOL, (f, err)
+    for f in ("acc", "src"):
+        assert row_scaled_err(getattr(ws, f), g[f]) <= JTOL, f
+
+
+def test_assembly_vs_reference(small):
+    g, c, ws, blocks = small
+    assert row_scaled_err(ws.diag, g["diag"]) <= JTOL
+    assert row_scaled_err(ws.offd, g["offd"]) <= JTOL
+    re = scaled_resid_err(ws.resid, g["resid"], g["accn"], c.grid.volume, float(g["dt"]), 7, 8)
+    assert re <= JTOL
+    np.testing.assert_array_equal(ws.upw, g["upw"])
+    for k in ("resid", "dwdb"):
+        np.testing.assert_allclose([getattr(b, k) for b in blocks], g["w_" + k], rtol=1e-10)
+    for k in ("wrow", "bcol", "comp_rates"):
+        assert row_scaled_err(np.stack([getattr(b, k) for b in blocks]), g["w_" + k]) <= JTOL, k
+    np.testing.assert_allclose(np.stack([b.phase_rates for b in blocks]), g["w_phase_rates"],
+                               rtol=1e-10, atol=1e-300)
+
+
+def test_frozen_upwind_vs_reference(small):
+    g, c, ws, _ = small
+    st2 = state_from(g, "st2_")
+    assemble(c.grid, c.pack, ws, c.wells, c.streams, st2, g["accn2"], float(g["dt"]),
+             float(g["t_new"]), g["capped"], freeze_upwind=True)
+    assert row_scaled_err(ws.diag, g["diag2"]) <= JTOL
+    assert row_scaled_err(ws.offd, g["offd2"]) <= JTOL
+    assert scaled_resid_err(ws.resid, g["resid2"], g["accn2"], c.grid.volume, float(g["dt"]),
+                            7, 8) <= JTOL
+
+
+@pytest.mark.parametrize("precond", ["none", "bjacobi", "ras"])
+def test_solve_vs_reference(precond):
+    g = golden("asm_small3d.npz")
+    s = golden("solve_small3d.npz")
+    c = case_objects("small3d")
+    ws = _ws(c, precond)
+    blocks = assemble(c.grid, c.pack, ws, c.wells, c.streams, state_from(g), g["accn"],
+                      float(g["dt"]), float(g["t_new"]), g["capped"])
+    du, dbhp, it = BlockSolver(c.grid, ws, tol=1e-10, maxiter=1000, precond=precond).solve(blocks)
+    ref = s[precond + "_du"]
+    assert abs(it - int(s[precond + "_iters"])) <= 1
+    assert np.linalg.norm(du - ref) <= 1e-8 * np.linalg.norm(ref)
+    np.testing.assert_allclose(dbhp, s[precond + "_dbhp"], rtol=1e-8, atol=1e-8)
+
+
+def test_two_subdomain_ras_vs_reference():
+    from tests.golden_states import random_state_like_reference
+    s = golden("solve_sub2.npz")
+    c = case_objects("sub2")
+    st, accn = random_state_like_reference(c, int(s["seed"]))
+    for pc in ("none", "bjacobi", "ras"):
+        ws = _ws(c, pc)
+        blocks = assemble(c.grid, c.pack, ws, c.wells, c.streams, st, accn, 2e-3, 2e-3,
+                          np.zeros(len(c.wells), bool))
+        du, dbhp, it = BlockSolver(c.grid, ws, tol=1e-10, maxiter=1000, precond=pc).solve(blocks)
+        assert abs(it - int(s[pc + "_iters"])) <= 1, (pc, it)
+        if pc == "ras":
+            ref = s["ras_du"]
+            assert np.linalg.norm(du - ref) <= 1e-8 * np.linalg.norm(ref)
+
+
+def test_synthetic_microbench_vs_reference():
+    """Device generator == host generator; iteration counts == reference."""
+    from paper_1811_11992_b200.grid import build_grid
+    from paper_1811_11992_b200.synth import synth_system
+    from paper_1811_11992_b200.model import load_pack
+    s = golden("synth_16.npz")
+    grid = build_grid(16, 16, 16, 1.0, 1.0, 1.0, 1.0, 1.0, 1.0, 0.3)
+    pack = load_pack("tube3_pack", grid.phi_ref)
+    diag, offd, resid = synth_system(grid, 9, seed=7)
+    for pc in ("none", "bjacobi", "ras"):
+        ws = Workspace(grid, pack, None, wells=(), streams=(), precond=pc)
+        load_system(ws, diag, offd, resid)
+        du, _, it = BlockSolver(grid, ws, tol=1e-8, maxiter=1000, precond=pc).solve([])
+        assert abs(it - int(s[pc + "_iters"])) <= 1, (pc, it)
+        if pc == "ras":
+            ref = s["ras_du"]
+            assert np.linalg.norm(du - ref) <= 1e-6 * np.linalg.norm(ref)
+    # device generator reproduces the host one
+    ws = Workspace(grid, pack, None, wells=(), streams=(), precond="ras")
+    from paper_1811_11992_b200 import _native as N
+    N.check(ws.ctx.L.isc_synth_system(ws.ctx.h, 7), "synth")
+    assert row_scaled_err(ws.diag, diag) <= 1e-13
+    assert row_scaled_err(ws.offd, offd) <= 1e-13
+
+
+@pytest.mark.parametrize("name,tol", [("c1", 1e-10), ("c2", 1e-10), ("c1", 1e-5)])
+def test_trajectory_vs_reference(name, tol):
+    """Whole runs: equal step and Newton sequences, fields within 1e-6."""
+    from paper_1811_11992_b200.newton import Simulator
+    g = golden(f"traj_{name}_{tol:.0e}.npz")
+    c = case_objects(name, linear_tol=tol)
+    sim = Simulator(c.grid, c.pack, c.wells, c.streams, c.state, c.case.schedule, c.case.solver)
+    sim.advance()
+    rec = np.array([(s.time, s.dt, s.newton, s.linear, s.solves) for s in sim.steps])
+    ref = g["steps"]
+    assert rec.shape[0] == ref.shape[0]
+    np.testing.assert_array_equal(rec[:, 2], ref[:, 2])          # Newton per step
+    np.testing.assert_allclose(rec[:, :2], ref[:, :2], rtol=1e-12)
+    st = sim.state.to_host()
+    for f in ("p", "t", "sw", "sg"):
+        a, b = st[f], g["final_" + f]
+        assert np.max(np.abs(a - b) / np.maximum(np.abs(b), 1e-30)) <= 1e-6, f
+    # the reference's own audit (newton.py:339-371) is reproduced, not zero
+    np.testing.assert_allclose(sim.cumulative_imbalance(), float(g["cum_imbalance"]),
+                               rtol=1e-6, atol=1e-12)
+    bal = np.array([s.balance for s in sim.steps])
+    np.testing.assert_allclose(bal, ref[:, 5], rtol=1e-5, atol=1e-12)
+
+
+def test_pore_space_exhausted():
+    g = golden("asm_small3d.npz")
+    c = case_objects("small3d")
+    ws = _ws(c)
+    st = state_from(g)
+    st.cc[17] = 100.0   # coke beyond the pore volume
+    with pytest.raises(PoreSpaceExhausted):
+        assemble(c.grid, c.pack, ws, c.wells, c.streams, st, g["accn"], 2e-3, 2e-3, g["capped"])
+
+
+def test_singular_block_and_max_iterations():
+    from paper_1811_11992_b200.grid import build_grid
+    from paper_1811_11992_b200.synth import synth_system
+    from paper_1811_11992_b200.model import load_pack
+    grid = build_grid(6, 5, 4, 1.0, 1.0, 1.0, 1.0, 1.0, 1.0, 0.3)
+    pack = load_pack("tube3_pack", grid.phi_ref)
+    diag, offd, resid = synth_system(grid, 9, seed=3)
+    ws = Workspace(grid, pack, None, wells=(), streams=(), precond="ras")
+    bad = diag.copy()
+    bad[11, :, 4] = 0.0   # column 4 of cell 11's block vanishes
+    load_system(ws, bad, offd, resid)
+    with pytest.raises(SingularCellBlock, match="cell 11"):
+        BlockSolver(grid, ws, tol=1e-8, maxiter=100, precond="ras").solve([])
+    load_system(ws, diag, offd, resid)
+    with pytest.raises(MaxIterations):
+        BlockSolver(grid, ws, tol=1e-14, maxiter=1, precond="none").solve([])
