@@ -1,0 +1,401 @@
+"""Benchmark: cell·Newton-iterations per second on the B200 (BASELINE.json).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+
+Workload (BASELINE configs[3], the 2 M-cell case the north star quotes its
+roofline bar on): C4 = 200x200x50 grid, seeded log-normal permeability and
+uniform porosity, 4 air injectors + 4 producers, deck-default solver
+(LINEAR_TOL 1e-5, PRECOND ras, LINEAR_MAX 200). One *step* = one full
+Newton iteration of the first timestep (dt = 2e-3 d): assemble (cell +
+face + wells), well Schur fold + Gauss-Jordan decoupling, RAS block-ILU(0)
+factorisation and the preconditioned BiCGSTAB solve, then the damped
+update. ``value`` = cells x steps / device time (inputs resident in HBM);
+``e2e`` = the same through the drop-in API (assemble/BlockSolver.solve) with
+the state and accumulation copied from pinned host memory and du read back
+every step. The system (9 GB) is far larger than L2, so no flush is needed.
+
+``--impl reference`` times the reference algorithm's CPU implementation (the
+plain-C/numpy oracle port, all host threads) on a bounded C4 sample.
+Multi-GPU (torchrun): every rank runs its own replica (weak scaling);
+device time is the max over ranks.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "cell·Newton-iters/sec (assemble+decouple+solve)"
+UNIT = "cell-iters/s"
+KCLASS = ["cell", "face", "wells", "decouple", "ilu_factor", "ilu_apply", "spmv", "other"]
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", default="c4")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-spmv", action="store_true")
+    return ap.parse_args()
+
+
+def dist_setup(n_gpus):
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return rank, world, local
+
+
+def peaks():
+    path = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(path):
+        d = json.load(open(path))
+        return float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json)"
+    return 6650.0, "fallback (B200_PROFILING.md)"
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons during the timed region."""
+
+    def __init__(self, index=0):
+        self.index, self.samples, self.proc = index, [], None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index),
+                 "--query-gpu=clocks.sm,clocks.max.sm,clocks_event_reasons.active,"
+                 "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+                 "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap",
+                 "--format=csv,noheader,nounits", "-lms", "200"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.thread = threading.Thread(target=self._read, daemon=True)
+            self.thread.start()
+        except Exception:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.samples.append([s.strip() for s in line.split(",")])
+
+    def stop(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except Exception:
+            self.proc.kill()
+        time.sleep(0.05)
+        sm = [float(s[0]) for s in self.samples if len(s) >= 7 and s[0].replace(".", "").isdigit()]
+        mx = [float(s[1]) for s in self.samples if len(s) >= 7 and s[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = set()
+        for s in self.samples:
+            if len(s) < 7:
+                continue
+            for k, nm in enumerate(names):
+                if s[3 + k].lower() == "active":
+                    reasons.add(nm)
+        return {"sm_mhz": float(np.median(sm)) if sm else None,
+                "sm_max_mhz": max(mx) if mx else None, "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+def ilu_bytes(ctx_counts, n, m):
+    """Algorithmic bytes of one RAS ILU(0) apply: matrix data streamed once
+    (U^-1 per slot, L blocks per lower link, A blocks per upper link),
+    the input read and output written once per slot / cell."""
+    nslots, nlow, nup = ctx_counts
+    return 8 * (81 * (nslots + nlow + nup) + 9 * nslots + 9 * n)
+
+
+def ilu_structure_counts(grid):
+    """(slots, lower links, upper links) of the reference's RAS partition."""
+    nsub = min(64, max(1, grid.ncell // 2048))
+    dims = [grid.nx, grid.ny, grid.nz]
+    axis = int(np.argmax(dims))
+    base, extra = divmod(dims[axis], nsub)
+    slots = links = 0
+    pos = 0
+    for s in range(nsub):
+        size = base + (1 if s < extra else 0)
+        lo, hi = pos, pos + size
+        if nsub > 1:
+            lo, hi = max(0, lo - 1), min(dims[axis], hi + 1)
+        w = list(dims)
+        w[axis] = hi - lo
+        slots += w[0] * w[1] * w[2]
+        links += (w[0] - 1) * w[1] * w[2] + w[0] * (w[1] - 1) * w[2] + w[0] * w[1] * (w[2] - 1)
+        pos += size
+    return slots, links, links
+
+
+def algorithmic_bytes(grid, nw):
+    n, m = grid.ncell, grid.nconn
+    return {
+        "cell+face": 8 * (111 * n + 164 * m),              # SURVEY §8(d) assembly
+        "decouple": 8 * (99 * n + 324 * m),
+        "spmv": 8 * (162 * m + 18 * n),
+        "ilu_apply": ilu_bytes(ilu_structure_counts(grid), n, m),
+    }
+
+
+# ------------------------------------------------------------------ ours
+
+def run_ours(args, rank, world, local):
+    import torch
+    from paper_1811_11992_b200 import configs, _native as N
+    from paper_1811_11992_b200.assembly import Workspace, assemble
+    from paper_1811_11992_b200.linsolve import BlockSolver
+    from paper_1811_11992_b200.newton import Simulator
+
+    torch.cuda.set_device(local)
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    case = configs.config(args.config)
+    grid, pack, wells, streams, state = configs.build_case(case)
+    n = grid.ncell
+    sim = Simulator(grid, pack, wells, streams, state, case.schedule, case.solver)
+    ctx = sim.ctx
+    dt = case.schedule.dt_init
+    work = sim.state.copy()
+    capped = sim.capped.copy()
+
+    def barrier():
+        if world > 1:
+            import torch.distributed as dist
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    for _ in range(args.warmup):
+        sim.newton_iteration(work, dt, dt, capped, False)
+    barrier()
+    clocks = ClockSampler(local)
+    clocks.start()
+    N.check(ctx.L.isc_set_profiling(ctx.h, 1), "profiling")
+    ms8, cnt8 = np.zeros(8), np.zeros(8, dtype=np.int64)
+    ctx.L.isc_kernel_times(ctx.h, N.ptr(ms8), N.ptr(cnt8), 1)
+    l0 = ctx.launch_count()
+    its = []
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    barrier()
+    ev0.record()
+    for _ in range(args.steps):
+        its.append(sim.newton_iteration(work, dt, dt, capped, False))
+    ev1.record()
+    barrier()
+    dev_ms = ev0.elapsed_time(ev1)
+    launches = ctx.launch_count() - l0
+    ctx.L.isc_kernel_times(ctx.h, N.ptr(ms8), N.ptr(cnt8), 1)
+    N.check(ctx.L.isc_set_profiling(ctx.h, 0), "profiling")
+    clk = clocks.stop()
+    if world > 1:
+        import torch.distributed as dist
+        t = torch.tensor([dev_ms], device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        dev_ms = float(t.item())
+
+    # ---- e2e through the drop-in API with host buffers -------------------
+    ws = Workspace(grid, pack, None, wells=wells, streams=streams, precond=case.solver.precond)
+    solver = BlockSolver(grid, ws, tol=case.solver.linear_tol, maxiter=case.solver.linear_max,
+                         precond=case.solver.precond)
+    host = work.to_host()
+    st_pin = {k: torch.from_numpy(np.ascontiguousarray(v)).pin_memory().numpy()
+              for k, v in host.items()}
+    from types import SimpleNamespace
+    hstate = SimpleNamespace(**st_pin)
+    accn_h = torch.from_numpy(np.ascontiguousarray(sim.accn.t().cpu().numpy())).pin_memory().numpy()
+    bi = sum(a.nbytes for a in st_pin.values()) + accn_h.nbytes
+    for _ in range(max(1, min(args.warmup, 2))):
+        blocks = assemble(grid, pack, ws, wells, streams, hstate, accn_h, dt, dt, capped)
+        du, dbhp, _ = solver.solve(blocks)
+    barrier()
+    t0 = time.perf_counter()
+    e2e_steps = max(1, min(args.steps, 5))
+    for _ in range(e2e_steps):
+        blocks = assemble(grid, pack, ws, wells, streams, hstate, accn_h, dt, dt, capped)
+        du, dbhp, _ = solver.solve(blocks)
+    barrier()
+    e2e_s = time.perf_counter() - t0
+    bo = du.nbytes + dbhp.nbytes
+    e2e = {"value": n * e2e_steps / e2e_s * world, "unit": UNIT, "h2d_bytes_per_step": int(bi),
+           "d2h_bytes_per_step": int(bo),
+           "path": "assembly.assemble(host State, host accn) + linsolve.BlockSolver.solve -> host du"}
+    ws.ctx.close()
+
+    value = n * args.steps * world / (dev_ms / 1e3)
+    out = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+           "warmup": args.warmup, "ms_per_step": dev_ms / args.steps, "higher_is_better": True,
+           "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+           "data": "synthetic (seeded: log-normal perm, uniform porosity; BASELINE configs[3])",
+           "config": {"workload": f"{args.config.upper()} {grid.nx}x{grid.ny}x{grid.nz} "
+                                  f"({n} cells, {len(wells)} wells), first timestep "
+                                  f"dt={dt} d, Newton iterations",
+                      "precond": case.solver.precond, "linear_tol": case.solver.linear_tol,
+                      "bicgstab_iters_per_step": float(np.mean(its)),
+                      "parallelism": f"replicas x{world}" if world > 1 else "single GPU",
+                      "l2": "inputs larger than L2 (system ~9 GB), no flush"},
+           "e2e": e2e, "gpu_launches": int(launches), "clocks": clk}
+    # ---- roofline of the dominant kernel class ----------------------------
+    hbm, peak_src = peaks()
+    algo = algorithmic_bytes(grid, len(wells))
+    ktimes = {KCLASS[i]: {"ms": float(ms8[i]), "launches": int(cnt8[i])} for i in range(8)}
+    classes = {"ilu_apply": ("ilu_apply",), "spmv": ("spmv",), "decouple": ("decouple",),
+               "cell+face": ("cell", "face")}
+    rows = {}
+    for key, parts in classes.items():
+        ms = sum(ktimes[p]["ms"] for p in parts)
+        nl = ktimes[parts[0]]["launches"]
+        if nl == 0 or ms <= 0:
+            continue
+        per = ms / nl
+        ach = algo[key] / (per / 1e3) / 1e9
+        rows[key] = {"avg_ms": per, "launches": nl, "share": ms / dev_ms,
+                     "algorithmic_bytes": algo[key], "achieved_gbs": ach, "frac": ach / hbm}
+    dom = max(rows, key=lambda k: rows[k]["share"])
+    out["roofline"] = {"kernel": dom, "bound": "hbm", "achieved": rows[dom]["achieved_gbs"],
+                       "peak": hbm, "unit": "GB/s", "frac": rows[dom]["achieved_gbs"] / hbm,
+                       "traffic": None, "peak_source": peak_src, "kernels": rows,
+                       "kernel_ms": ktimes}
+    return out, sim
+
+
+# ------------------------------------------------------ SpMV microbench
+
+def run_spmv_c5(steps=20):
+    """BASELINE configs[4]: 400x400x100 synthetic BSR (16 M block rows),
+    decoupled; SpMV achieved HBM GB/s (CUDA events, inputs >> L2)."""
+    import torch
+    from paper_1811_11992_b200 import _native as N
+    from paper_1811_11992_b200.grid import build_grid
+    from paper_1811_11992_b200.model import load_pack
+    from paper_1811_11992_b200.device import DeviceContext
+    free, _ = torch.cuda.mem_get_info()
+    nx, ny, nz = 400, 400, 100
+    if free < 120e9:
+        nz = max(10, int(100 * free / 140e9))
+    grid = build_grid(nx, ny, nz, 1.0, 1.0, 1.0, 1.0, 1.0, 1.0, 0.3)
+    pack = load_pack("tube3_pack", grid.phi_ref)
+    ctx = DeviceContext(grid, pack, (), (), "none")
+    N.check(ctx.L.isc_synth_system(ctx.h, 7), "synth")
+    import ctypes
+    bc, bcol = ctypes.c_int64(-1), ctypes.c_int32(-1)
+    N.check(ctx.L.isc_decouple(ctx.h, ctypes.byref(bc), ctypes.byref(bcol)), "decouple")
+    x = torch.randn(9, grid.ncell, dtype=torch.float64, device="cuda")
+    y = torch.empty_like(x)
+    for _ in range(3):
+        N.check(ctx.L.isc_spmv(ctx.h, N.ptr(x), N.ptr(y)), "spmv")
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for _ in range(steps):
+        ctx.L.isc_spmv(ctx.h, N.ptr(x), N.ptr(y))
+    e1.record()
+    torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1) / steps
+    nbytes = 8 * (162 * grid.nconn + 18 * grid.ncell)
+    hbm, src = peaks()
+    ctx.close()
+    del x, y
+    torch.cuda.empty_cache()
+    return {"grid": f"{nx}x{ny}x{nz}", "block_rows": grid.ncell, "ms": ms,
+            "algorithmic_bytes": nbytes, "achieved_gbs": nbytes / ms / 1e6,
+            "frac": nbytes / ms / 1e6 / hbm, "peak": hbm, "peak_source": src}
+
+
+# --------------------------------------------------------- CPU oracle arm
+
+def cpu_sample_case():
+    from dataclasses import replace
+    from paper_1811_11992_b200 import configs
+    case = configs.config("c4")
+    return replace(case, nz=2, wells=tuple(replace(w, k=2) for w in case.wells))
+
+
+def run_oracle(steps, warmup, budget_s=None):
+    """Newton iterations of the CPU restatement (oracle port) on a bounded
+    C4 sample (200x200x2 = 80k cells, same fluid/rock/wells pattern)."""
+    ncpu = os.cpu_count() or 1
+    os.environ["OMP_NUM_THREADS"] = str(ncpu)
+    from oracle import isc_oracle as O
+    from paper_1811_11992_b200 import configs
+    case = cpu_sample_case()
+    grid, pack, wells, streams, state = configs.build_case(case)
+    sim = O.Simulator(grid, pack, wells, streams, state, case.schedule, case.solver)
+    dt = case.schedule.dt_init
+    capped = np.zeros(len(wells), dtype=bool)
+    st = sim.state.copy()
+
+    def iteration(st):
+        blocks = O.assemble(grid, sim.model, sim.ws, sim.wells, sim.streams, st, sim.accn, dt,
+                            dt, capped)
+        du, dbhp, it = sim.solver.solve(blocks)
+        return O.apply_update(st, du, dbhp, pack.nco, pack.ncg, case.solver.eps)
+
+    for _ in range(warmup):
+        st = iteration(st)
+    t0 = time.perf_counter()
+    done = 0
+    for _ in range(steps):
+        st = iteration(st)
+        done += 1
+        if budget_s and time.perf_counter() - t0 > budget_s:
+            break
+    el = time.perf_counter() - t0
+    return {"value": grid.ncell * done / el, "unit": UNIT, "cores": ncpu, "kind": "port",
+            "sample": f"C4 sample {grid.nx}x{grid.ny}x{grid.nz} ({grid.ncell} cells), "
+                      f"{done} Newton iterations (assemble+decouple+RAS-ILU BiCGSTAB), "
+                      f"oracle/ C+numpy port, OMP threads={ncpu}",
+            "seconds": el}
+
+
+def main():
+    args = parse()
+    rank, world, local = dist_setup(args.gpus)
+    if args.impl == "reference":
+        if rank != 0:
+            return
+        res = run_oracle(args.steps, args.warmup)
+        line = {"metric": METRIC, "value": res["value"], "unit": UNIT, "n_gpus": args.gpus,
+                "steps": args.steps, "warmup": args.warmup,
+                "ms_per_step": res["seconds"] * 1e3 / max(1, args.steps),
+                "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+                "dtype": "f64", "data": "synthetic (seeded)", "impl": "reference",
+                "config": {"workload": res["sample"]},
+                "cpu_baseline": {k: res[k] for k in ("value", "unit", "cores", "kind", "sample")},
+                "e2e": {"value": res["value"], "unit": UNIT, "h2d_bytes_per_step": 0,
+                        "d2h_bytes_per_step": 0}}
+        print(json.dumps(line))
+        return
+    out, sim = run_ours(args, rank, world, local)
+    sim.ctx.close()
+    if rank == 0 and world == 1:
+        if not args.no_spmv:
+            try:
+                out["spmv_c5"] = run_spmv_c5()
+            except Exception as exc:  # report, never hide
+                out["spmv_c5"] = {"error": repr(exc)}
+        if not args.no_cpu_baseline:
+            cb = run_oracle(steps=3, warmup=0, budget_s=25.0)
+            out["cpu_baseline"] = {k: cb[k] for k in ("value", "unit", "cores", "kind", "sample")}
+    if rank == 0:
+        print(json.dumps(out))
+
+
+if __name__ == "__main__":
+    main()
