@@ -79,7 +79,7 @@ struct isc_ctx {
   IluDev ilu{};
   int64_t* lvl_ptr_d = nullptr;
   int nlev = 0;
-  int coop_factor = 0, coop_apply = 0;
+  int nsub = 1;
   // timing
   cudaEvent_t ev[8] = {};
   double stage_ms[4] = {0, 0, 0, 0};
@@ -185,24 +185,32 @@ static int build_ilu(isc_ctx* ctx) {
     pos += size;
     boxes.push_back(b);
   }
-  // count slots per level
+  // slots: subdomain-major, level-major inside a subdomain box; the level
+  // of a cell is (i-x0)+(j-y0)+(k-z0) (its dependencies sit one level lower)
   int maxlev = 0;
   for (auto& b : boxes)
     maxlev = std::max(maxlev, (b.hi[0] - b.lo[0] - 1) + (b.hi[1] - b.lo[1] - 1) + (b.hi[2] - b.lo[2] - 1));
   const int nlev = maxlev + 1;
-  std::vector<int64_t> cnt(nlev + 1, 0);
-  for (auto& b : boxes)
+  std::vector<int64_t> lvl_ptr((size_t)nsub * (nlev + 1), 0);
+  int64_t total = 0;
+  for (int s = 0; s < nsub; ++s) {
+    const Box& b = boxes[s];
+    std::vector<int64_t> cnt(nlev, 0);
     for (int k = b.lo[2]; k < b.hi[2]; ++k)
       for (int j = b.lo[1]; j < b.hi[1]; ++j)
-        for (int i = b.lo[0]; i < b.hi[0]; ++i)
-          cnt[(i - b.lo[0]) + (j - b.lo[1]) + (k - b.lo[2]) + 1]++;
-  std::vector<int64_t> lvl_ptr(nlev + 1, 0);
-  for (int l = 0; l < nlev; ++l) lvl_ptr[l + 1] = lvl_ptr[l] + cnt[l + 1];
-  const int64_t ns = lvl_ptr[nlev];
-  std::vector<int64_t> fill(lvl_ptr.begin(), lvl_ptr.end() - 1);
+        for (int i = b.lo[0]; i < b.hi[0]; ++i) cnt[(i - b.lo[0]) + (j - b.lo[1]) + (k - b.lo[2])]++;
+    int64_t* lp = lvl_ptr.data() + (size_t)s * (nlev + 1);
+    lp[0] = total;
+    for (int l = 0; l < nlev; ++l) lp[l + 1] = lp[l] + cnt[l];
+    total = lp[nlev];
+  }
+  const int64_t ns = total;
   std::vector<int64_t> cell(ns), lo(3 * ns, -1), up(3 * ns, -1);
   std::vector<int8_t> owned(ns, 0);
-  for (auto& b : boxes) {
+  for (int sidx = 0; sidx < nsub; ++sidx) {
+    const Box& b = boxes[sidx];
+    std::vector<int64_t> fill(lvl_ptr.begin() + (size_t)sidx * (nlev + 1),
+                              lvl_ptr.begin() + (size_t)sidx * (nlev + 1) + nlev);
     const int wx = b.hi[0] - b.lo[0], wy = b.hi[1] - b.lo[1], wz = b.hi[2] - b.lo[2];
     std::vector<int64_t> slot((size_t)wx * wy * wz);
     for (int k = b.lo[2]; k < b.hi[2]; ++k)
@@ -230,31 +238,25 @@ static int build_ilu(isc_ctx* ctx) {
           if (lk + 1 < wz) up[2 * ns + s] = at(li, lj, lk + 1);
         }
   }
+  ctx->nsub = nsub;
   int64_t *cell_d, *lo_d, *up_d;
   int8_t* owned_d;
   ALLOC(cell_d, ns * 8);
   ALLOC(lo_d, 3 * ns * 8);
   ALLOC(up_d, 3 * ns * 8);
   ALLOC(owned_d, ns);
-  ALLOC(ctx->lvl_ptr_d, (nlev + 1) * 8);
+  ALLOC(ctx->lvl_ptr_d, lvl_ptr.size() * 8);
   CK(cudaMemcpy(cell_d, cell.data(), ns * 8, cudaMemcpyHostToDevice));
   CK(cudaMemcpy(lo_d, lo.data(), 3 * ns * 8, cudaMemcpyHostToDevice));
   CK(cudaMemcpy(up_d, up.data(), 3 * ns * 8, cudaMemcpyHostToDevice));
   CK(cudaMemcpy(owned_d, owned.data(), ns, cudaMemcpyHostToDevice));
-  CK(cudaMemcpy(ctx->lvl_ptr_d, lvl_ptr.data(), (nlev + 1) * 8, cudaMemcpyHostToDevice));
+  CK(cudaMemcpy(ctx->lvl_ptr_d, lvl_ptr.data(), lvl_ptr.size() * 8, cudaMemcpyHostToDevice));
   double *lblk, *uinv, *zs;
   ALLOC(lblk, (size_t)3 * NB * ns * 8);
   ALLOC(uinv, (size_t)NB * ns * 8);
   ALLOC(zs, (size_t)NU * ns * 8);
   ctx->ilu = IluDev{ns, cell_d, owned_d, lo_d, up_d, lblk, uinv, zs};
   ctx->nlev = nlev;
-  int dev = 0, nsm = 0, per_sm = 0;
-  CK(cudaGetDevice(&dev));
-  CK(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev));
-  CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_ilu_factor, IL_SLOTS * NU, 0));
-  ctx->coop_factor = std::max(1, per_sm) * nsm;
-  CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_ilu_apply, IL_SLOTS * NU, 0));
-  ctx->coop_apply = std::max(1, per_sm) * nsm;
   return ISC_OK;
 }
 
@@ -642,11 +644,10 @@ extern "C" int isc_precond_setup(isc_ctx* ctx, int64_t* bad_cell) {
   const int64_t* lp = ctx->lvl_ptr_d;
   int nlev = ctx->nlev;
   int* fail = ctx->fail_d;
-  void* args[] = {&g, &L, &offd, &lp, &nlev, &fail};
   {
   KScope ks(ctx, KT_ILU_FACTOR);
-  CK(cudaLaunchCooperativeKernel((void*)k_ilu_factor, ctx->coop_factor, dim3(IL_SLOTS, NU), args,
-                                 0, st));
+  k_ilu_factor<<<ctx->nsub * ILC, dim3(IL_SLOTS, NU), 0, st>>>(g, L, offd, lp, nlev, fail);
+  CK(cudaGetLastError());
   }
   ++ctx->launches;
   int fail_h = 0;
@@ -673,10 +674,9 @@ static int precond_apply(isc_ctx* ctx, const double* r, double* z) {
   const double* offd = ctx->offd;
   const int64_t* lp = ctx->lvl_ptr_d;
   int nlev = ctx->nlev;
-  void* args[] = {&g, &L, &offd, &lp, &nlev, (void*)&r, (void*)&z};
   KScope ks(ctx, KT_ILU_APPLY);
-  CK(cudaLaunchCooperativeKernel((void*)k_ilu_apply, ctx->coop_apply, dim3(IL_SLOTS, NU), args,
-                                 0, ctx->stream));
+  k_ilu_apply<<<ctx->nsub * ILC, dim3(IL_SLOTS, NU), 0, ctx->stream>>>(g, L, offd, lp, nlev, r, z);
+  CK(cudaGetLastError());
   ++ctx->launches;
   return ISC_OK;
 }

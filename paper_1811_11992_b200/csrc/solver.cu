@@ -247,7 +247,7 @@ __device__ void ilu_factor_tile(const Dims& g, const IluDev& L, const double* __
       const double* Acj = offd + (int64_t)(dlo[q] * NB) * n + c;
       double uj[NU];
 #pragma unroll
-      for (int k = 0; k < NU; ++k) uj[k] = L.uinv[(int64_t)(k * NU + u) * ns + sj];
+      for (int k = 0; k < NU; ++k) uj[k] = __ldcg(L.uinv + (int64_t)(k * NU + u) * ns + sj);
 #pragma unroll
       for (int r = 0; r < NU; ++r) {
         double t = 0.0;
@@ -347,33 +347,40 @@ __device__ void ilu_factor_tile(const Dims& g, const IluDev& L, const double* __
   }
 }
 
-__global__ void __launch_bounds__(IL_SLOTS * NU) k_ilu_factor(Dims g, IluDev L, const double* offd,
-                                                              const int64_t* lvl_ptr, int nlev,
-                                                              int* fail) {
-  cg::grid_group grid = cg::this_grid();
+// One thread-block cluster per subdomain (subdomains are independent):
+// levels are separated by a cluster barrier (release/acquire at cluster
+// scope) instead of a grid-wide sync, and values produced by other CTAs of
+// the cluster are read through L2 (__ldcg).
+constexpr int ILC = 4;   // CTAs per cluster
+
+__global__ void __cluster_dims__(ILC, 1, 1) __launch_bounds__(IL_SLOTS * NU)
+    k_ilu_factor(Dims g, IluDev L, const double* offd, const int64_t* __restrict__ sub_ptr,
+                 int nlev, int* fail) {
+  cg::cluster_group cluster = cg::this_cluster();
+  const int sub = blockIdx.x / ILC, crank = blockIdx.x % ILC;
+  const int64_t* lp = sub_ptr + (int64_t)sub * (nlev + 1);
   for (int lev = 0; lev < nlev; ++lev) {
-    const int64_t b = lvl_ptr[lev], e = lvl_ptr[lev + 1];
-    for (int64_t s0 = b + (int64_t)blockIdx.x * IL_SLOTS; s0 < e; s0 += (int64_t)gridDim.x * IL_SLOTS)
+    const int64_t b = lp[lev], e = lp[lev + 1];
+    for (int64_t s0 = b + (int64_t)crank * IL_SLOTS; s0 < e; s0 += (int64_t)ILC * IL_SLOTS)
       ilu_factor_tile(g, L, offd, s0, e, fail);
-    grid.sync();
+    cluster.sync();
   }
 }
 
-// forward then backward sweep; z_out (global, SoA) gets owned slots
-__global__ void __launch_bounds__(IL_SLOTS * NU) k_ilu_apply(Dims g, IluDev L, const double* offd,
-                                                             const int64_t* lvl_ptr, int nlev,
-                                                             const double* __restrict__ rin,
-                                                             double* __restrict__ zout) {
-  cg::grid_group grid = cg::this_grid();
+// forward then backward sweep; z_out (global, SoA) gets the owned slots
+__global__ void __cluster_dims__(ILC, 1, 1) __launch_bounds__(IL_SLOTS * NU)
+    k_ilu_apply(Dims g, IluDev L, const double* offd, const int64_t* __restrict__ sub_ptr,
+                int nlev, const double* __restrict__ rin, double* __restrict__ zout) {
+  cg::cluster_group cluster = cg::this_cluster();
   __shared__ double wsh[NU][IL_SLOTS];
   const int64_t n = g.n, ns = L.nslots;
   const int ls = threadIdx.x, r = threadIdx.y;
+  const int sub = blockIdx.x / ILC, crank = blockIdx.x % ILC;
+  const int64_t* lp = sub_ptr + (int64_t)sub * (nlev + 1);
   // forward: z_c = r_c - sum_j lblk_cj z_j   (lower j in order -z,-y,-x)
   for (int lev = 0; lev < nlev; ++lev) {
-    const int64_t b = lvl_ptr[lev], e = lvl_ptr[lev + 1];
-    for (int64_t s = b + (int64_t)blockIdx.x * IL_SLOTS + ls; s - ls < e;
-         s += (int64_t)gridDim.x * IL_SLOTS) {
-      if (s >= e) continue;
+    const int64_t b = lp[lev], e = lp[lev + 1];
+    for (int64_t s = b + (int64_t)crank * IL_SLOTS + ls; s < e; s += (int64_t)ILC * IL_SLOTS) {
       const int64_t c = L.cell[s];
       double z = rin[r * n + c];
 #pragma unroll
@@ -383,25 +390,25 @@ __global__ void __launch_bounds__(IL_SLOTS * NU) k_ilu_apply(Dims g, IluDev L, c
         double t = 0.0;
 #pragma unroll
         for (int u = 0; u < NU; ++u)
-          t += L.lblk[(int64_t)(q * NB + r * NU + u) * ns + s] * L.zs[(int64_t)u * ns + sj];
+          t += L.lblk[(int64_t)(q * NB + r * NU + u) * ns + s] * __ldcg(L.zs + (int64_t)u * ns + sj);
         z -= t;
       }
       L.zs[(int64_t)r * ns + s] = z;
     }
-    grid.sync();
+    cluster.sync();
   }
   // backward: z_c = U_c^-1 (z_c - sum_j A_cj z_j)   (upper j in order +x,+y,+z)
   const int dup[3] = {DXP, DYP, DZP};
   for (int lev = nlev - 1; lev >= 0; --lev) {
-    const int64_t b = lvl_ptr[lev], e = lvl_ptr[lev + 1];
-    for (int64_t s0 = b + (int64_t)blockIdx.x * IL_SLOTS; s0 < e; s0 += (int64_t)gridDim.x * IL_SLOTS) {
+    const int64_t b = lp[lev], e = lp[lev + 1];
+    for (int64_t s0 = b + (int64_t)crank * IL_SLOTS; s0 < e; s0 += (int64_t)ILC * IL_SLOTS) {
       const int64_t s = s0 + ls;
       const bool live = s < e;
       double w = 0.0;
       int64_t c = 0;
       if (live) {
         c = L.cell[s];
-        w = L.zs[(int64_t)r * ns + s];
+        w = __ldcg(L.zs + (int64_t)r * ns + s);
 #pragma unroll
         for (int q = 0; q < 3; ++q) {
           const int64_t sj = L.up[q * ns + s];
@@ -409,7 +416,7 @@ __global__ void __launch_bounds__(IL_SLOTS * NU) k_ilu_apply(Dims g, IluDev L, c
           const double* Acj = offd + (int64_t)((dup[q] * NU + r) * NU) * n + c;
           double t = 0.0;
 #pragma unroll
-          for (int u = 0; u < NU; ++u) t += Acj[(int64_t)u * n] * L.zs[(int64_t)u * ns + sj];
+          for (int u = 0; u < NU; ++u) t += Acj[(int64_t)u * n] * __ldcg(L.zs + (int64_t)u * ns + sj);
           w -= t;
         }
       }
@@ -424,7 +431,7 @@ __global__ void __launch_bounds__(IL_SLOTS * NU) k_ilu_apply(Dims g, IluDev L, c
       }
       __syncthreads();
     }
-    grid.sync();
+    cluster.sync();
   }
 }
 
