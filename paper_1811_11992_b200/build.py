@@ -43,7 +43,8 @@ def build(force: bool = False, verbose: bool = False) -> str:
     cmd = [NVCC, *FLAGS, "-Xptxas", "-v", "-o", LIB + ".tmp", os.path.join(CSRC, "capi.cu")]
     res = subprocess.run(cmd, cwd=CSRC, capture_output=True, text=True)
     if res.returncode != 0:
-        raise RuntimeError("nvcc failed:\n" + res.stderr[-8000:])
+        errs = [ln for ln in res.stderr.splitlines() if "error" in ln.lower()]
+        raise RuntimeError("nvcc failed:\n" + "\n".join(errs[:40]) + "\n" + res.stderr[-3000:])
     os.replace(LIB + ".tmp", LIB)
     with open(os.path.join(LIB_DIR, "ptxas.log"), "w") as fh:
         fh.write(res.stderr)

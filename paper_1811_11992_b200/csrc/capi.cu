@@ -251,11 +251,12 @@ static int build_ilu(isc_ctx* ctx) {
   CK(cudaMemcpy(up_d, up.data(), 3 * ns * 8, cudaMemcpyHostToDevice));
   CK(cudaMemcpy(owned_d, owned.data(), ns, cudaMemcpyHostToDevice));
   CK(cudaMemcpy(ctx->lvl_ptr_d, lvl_ptr.data(), lvl_ptr.size() * 8, cudaMemcpyHostToDevice));
-  double *lblk, *uinv, *zs;
+  double *lblk, *uinv, *zs, *aup;
+  ALLOC(aup, (size_t)3 * NB * ns * 8);
   ALLOC(lblk, (size_t)3 * NB * ns * 8);
   ALLOC(uinv, (size_t)NB * ns * 8);
   ALLOC(zs, (size_t)NU * ns * 8);
-  ctx->ilu = IluDev{ns, cell_d, owned_d, lo_d, up_d, lblk, uinv, zs};
+  ctx->ilu = IluDev{ns, cell_d, owned_d, lo_d, up_d, lblk, uinv, zs, aup};
   ctx->nlev = nlev;
   return ISC_OK;
 }
@@ -646,7 +647,10 @@ extern "C" int isc_precond_setup(isc_ctx* ctx, int64_t* bad_cell) {
   int* fail = ctx->fail_d;
   {
   KScope ks(ctx, KT_ILU_FACTOR);
-  k_ilu_factor<<<ctx->nsub * ILC, dim3(IL_SLOTS, NU), 0, st>>>(g, L, offd, lp, nlev, fail);
+  CK(cudaFuncSetAttribute(k_ilu_factor, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                          (int)sizeof(FactorSmem)));
+  k_ilu_factor<<<ctx->nsub * ILCF, dim3(IL_SLOTS, NU), sizeof(FactorSmem), st>>>(g, L, offd, lp,
+                                                                               nlev, fail);
   CK(cudaGetLastError());
   }
   ++ctx->launches;

@@ -215,44 +215,78 @@ struct IluDev {
   double* lblk;                        // [(q*NB + e)*nslots + s]  A_cj U_jj^-1
   double* uinv;                        // [e*nslots + s]
   double* zs;                          // [r*nslots + s] local solution
+  double* aup;                         // [(q*NB + e)*nslots + s]  upper blocks, slot order
 };
 
 constexpr int IL_SLOTS = 32;
 
 // U = I - sum_j (A_cj U_j^-1) A_jc ; uinv = U^-1 (GJ, partial pivoting)
+// Thread (slot, column u). The three lower blocks A_cj are staged through
+// shared memory (one scattered column per thread instead of 81 loads), the
+// matching A_jc columns stay in registers and are also written out in slot
+// order as the upper block of slot j (coalesced reads in the apply sweep).
+struct FactorSmem {
+  double ash[3][NU][NU][IL_SLOTS];   // A_cj (q, row, col) for the tile
+  double lsh[NU][NU][IL_SLOTS];      // one lblk (row, col) for the tile
+  double colk[2 * NU][IL_SLOTS];
+  int pivs[IL_SLOTS];
+};
+
 __device__ void ilu_factor_tile(const Dims& g, const IluDev& L, const double* __restrict__ offd,
-                                int64_t s0, int64_t s1, int* fail) {
-  __shared__ double lsh[NU][NU][IL_SLOTS];   // one lblk (row, col) for the tile
-  __shared__ double colk[2 * NU][IL_SLOTS];
-  __shared__ int pivs[IL_SLOTS];
+                                int64_t s0, int64_t s1, int* fail, FactorSmem& S) {
+  auto& ash = S.ash;
+  auto& lsh = S.lsh;
+  auto& colk = S.colk;
+  auto& pivs = S.pivs;
   const int64_t n = g.n;
   const int ls = threadIdx.x, u = threadIdx.y;   // slot lane, owned column
   const int64_t s = s0 + ls;
   const bool live = s < s1;
   const int64_t ns = L.nslots;
   const int64_t c = live ? L.cell[s] : 0;
+  const int dlo[3] = {DZM, DYM, DXM};
+  // independent of the previous level: neighbour slots, A_cj and A_jc columns
+  int64_t sj[3];
+  double ajc[3][NU];
+#pragma unroll
+  for (int q = 0; q < 3; ++q) {
+    sj[q] = live ? L.lo[q * ns + s] : -1;
+    if (sj[q] >= 0) {
+      const double* Acj = offd + (int64_t)(dlo[q] * NB + u) * n + c;
+#pragma unroll
+      for (int r = 0; r < NU; ++r) ash[q][r][u][ls] = Acj[(int64_t)(r * NU) * n];
+      const int64_t cj = L.cell[sj[q]];
+      const double* Ajc = offd + (int64_t)(opposite(dlo[q]) * NB + u) * n + cj;
+#pragma unroll
+      for (int k = 0; k < NU; ++k) ajc[q][k] = Ajc[(int64_t)(k * NU) * n];
+      // upper block of slot j towards this slot (q' = 2 - q: +z, +y, +x order)
+#pragma unroll
+      for (int k = 0; k < NU; ++k) L.aup[(int64_t)((2 - q) * NB + k * NU + u) * ns + sj[q]] = ajc[q][k];
+    } else {
+#pragma unroll
+      for (int k = 0; k < NU; ++k) ajc[q][k] = 0.0;
+    }
+  }
   // own column u of U (starts at the identity: decoupled diagonal)
   double ucol[NU];
 #pragma unroll
   for (int r = 0; r < NU; ++r) ucol[r] = (r == u) ? 1.0 : 0.0;
-  const int dlo[3] = {DZM, DYM, DXM};
-#pragma unroll 1
+  __syncthreads();
+#pragma unroll
   for (int q = 0; q < 3; ++q) {
-    const int64_t sj = live ? L.lo[q * ns + s] : -1;
     // lblk[:, u] = A_cj * Uinv_j[:, u]
     double lc[NU];
 #pragma unroll
     for (int r = 0; r < NU; ++r) lc[r] = 0.0;
-    if (sj >= 0) {
-      const double* Acj = offd + (int64_t)(dlo[q] * NB) * n + c;
+    if (sj[q] >= 0) {
       double uj[NU];
 #pragma unroll
-      for (int k = 0; k < NU; ++k) uj[k] = __ldcg(L.uinv + (int64_t)(k * NU + u) * ns + sj);
+      for (int k = 0; k < NU; ++k) uj[k] = __ldcg(L.uinv + (int64_t)(k * NU + u) * ns + sj[q]);
 #pragma unroll
       for (int r = 0; r < NU; ++r) {
         double t = 0.0;
 #pragma unroll
-        for (int k = 0; k < NU; ++k) t += Acj[(int64_t)(r * NU + k) * n] * uj[k];
+        for (int k = 0; k < NU; ++k) t += ash[q][r][k][ls] * uj[k];
         lc[r] = t;
       }
 #pragma unroll
@@ -261,18 +295,13 @@ __device__ void ilu_factor_tile(const Dims& g, const IluDev& L, const double* __
 #pragma unroll
     for (int r = 0; r < NU; ++r) lsh[r][u][ls] = lc[r];
     __syncthreads();
-    if (sj >= 0) {
+    if (sj[q] >= 0) {
       // U[:, u] -= lblk * A_jc[:, u]
-      const int64_t cj = L.cell[sj];
-      const double* Ajc = offd + (int64_t)(opposite(dlo[q]) * NB) * n + cj;
-      double ac[NU];
-#pragma unroll
-      for (int k = 0; k < NU; ++k) ac[k] = Ajc[(int64_t)(k * NU + u) * n];
 #pragma unroll
       for (int r = 0; r < NU; ++r) {
         double t = 0.0;
 #pragma unroll
-        for (int k = 0; k < NU; ++k) t += lsh[r][k][ls] * ac[k];
+        for (int k = 0; k < NU; ++k) t += lsh[r][k][ls] * ajc[q][k];
         ucol[r] -= t;
       }
     }
@@ -351,18 +380,21 @@ __device__ void ilu_factor_tile(const Dims& g, const IluDev& L, const double* __
 // levels are separated by a cluster barrier (release/acquire at cluster
 // scope) instead of a grid-wide sync, and values produced by other CTAs of
 // the cluster are read through L2 (__ldcg).
-constexpr int ILC = 4;   // CTAs per cluster
+constexpr int ILC = 8;    // CTAs per cluster (apply)
+constexpr int ILCF = 4;   // CTAs per cluster (factor: 2 CTAs/SM -> one resident wave)
 
-__global__ void __cluster_dims__(ILC, 1, 1) __launch_bounds__(IL_SLOTS * NU)
+__global__ void __cluster_dims__(ILCF, 1, 1) __launch_bounds__(IL_SLOTS * NU, 2)
     k_ilu_factor(Dims g, IluDev L, const double* offd, const int64_t* __restrict__ sub_ptr,
                  int nlev, int* fail) {
   cg::cluster_group cluster = cg::this_cluster();
-  const int sub = blockIdx.x / ILC, crank = blockIdx.x % ILC;
+  extern __shared__ __align__(16) unsigned char dsm[];
+  FactorSmem& S = *reinterpret_cast<FactorSmem*>(dsm);
+  const int sub = blockIdx.x / ILCF, crank = blockIdx.x % ILCF;
   const int64_t* lp = sub_ptr + (int64_t)sub * (nlev + 1);
   for (int lev = 0; lev < nlev; ++lev) {
     const int64_t b = lp[lev], e = lp[lev + 1];
-    for (int64_t s0 = b + (int64_t)crank * IL_SLOTS; s0 < e; s0 += (int64_t)ILC * IL_SLOTS)
-      ilu_factor_tile(g, L, offd, s0, e, fail);
+    for (int64_t s0 = b + (int64_t)crank * IL_SLOTS; s0 < e; s0 += (int64_t)ILCF * IL_SLOTS)
+      ilu_factor_tile(g, L, offd, s0, e, fail, S);
     cluster.sync();
   }
 }
@@ -398,7 +430,6 @@ __global__ void __cluster_dims__(ILC, 1, 1) __launch_bounds__(IL_SLOTS * NU)
     cluster.sync();
   }
   // backward: z_c = U_c^-1 (z_c - sum_j A_cj z_j)   (upper j in order +x,+y,+z)
-  const int dup[3] = {DXP, DYP, DZP};
   for (int lev = nlev - 1; lev >= 0; --lev) {
     const int64_t b = lp[lev], e = lp[lev + 1];
     for (int64_t s0 = b + (int64_t)crank * IL_SLOTS; s0 < e; s0 += (int64_t)ILC * IL_SLOTS) {
@@ -413,10 +444,10 @@ __global__ void __cluster_dims__(ILC, 1, 1) __launch_bounds__(IL_SLOTS * NU)
         for (int q = 0; q < 3; ++q) {
           const int64_t sj = L.up[q * ns + s];
           if (sj < 0) continue;
-          const double* Acj = offd + (int64_t)((dup[q] * NU + r) * NU) * n + c;
           double t = 0.0;
 #pragma unroll
-          for (int u = 0; u < NU; ++u) t += Acj[(int64_t)u * n] * __ldcg(L.zs + (int64_t)u * ns + sj);
+          for (int u = 0; u < NU; ++u)
+            t += L.aup[(int64_t)(q * NB + r * NU + u) * ns + s] * __ldcg(L.zs + (int64_t)u * ns + sj);
           w -= t;
         }
       }
