@@ -47,6 +47,8 @@ def parse():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--config", default="c4")
+    ap.add_argument("--precond", default=None,
+                    help="override the deck preconditioner (ras, bjacobi, none, mcilu)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-spmv", action="store_true")
     return ap.parse_args()
@@ -168,6 +170,9 @@ def run_ours(args, rank, world, local):
         import torch.distributed as dist
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     case = configs.config(args.config)
+    if args.precond:
+        from dataclasses import replace
+        case = replace(case, solver=replace(case.solver, precond=args.precond))
     grid, pack, wells, streams, state = configs.build_case(case)
     n = grid.ncell
     sim = Simulator(grid, pack, wells, streams, state, case.schedule, case.solver)

@@ -46,7 +46,11 @@ typedef enum {
   ISC_UNSUPPORTED = 12
 } isc_status;
 
-typedef enum { ISC_PRECOND_NONE = 0, ISC_PRECOND_BJACOBI = 1, ISC_PRECOND_RAS = 2 } isc_precond;
+/* none / bjacobi / ras reproduce the reference (linsolve.py:322-358); mcilu is
+ * the red-black multicolour block ILU(0) of BASELINE's north_star. */
+typedef enum {
+  ISC_PRECOND_NONE = 0, ISC_PRECOND_BJACOBI = 1, ISC_PRECOND_RAS = 2, ISC_PRECOND_MCILU = 3
+} isc_precond;
 
 typedef struct isc_ctx isc_ctx;
 

@@ -20,7 +20,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(HERE, "_lib", "libiscgpu.so")
 
 ISC_OK, ISC_PSE, ISC_SINGULAR, ISC_BREAKDOWN, ISC_MAXIT = 0, 1, 2, 3, 4
-PRECOND = {"none": 0, "bjacobi": 1, "ras": 2}
+PRECOND = {"none": 0, "bjacobi": 1, "ras": 2, "mcilu": 3}
 WELL_OUT = 32
 NREC = 85
 

@@ -80,6 +80,7 @@ struct isc_ctx {
   int64_t* lvl_ptr_d = nullptr;
   int nlev = 0;
   int nsub = 1;
+  double* mc_uinv = nullptr;   // multicolour ILU: U_b^-1 of black cells
   // timing
   cudaEvent_t ev[8] = {};
   double stage_ms[4] = {0, 0, 0, 0};
@@ -278,7 +279,7 @@ extern "C" int isc_create(const isc_model_desc* md, const isc_grid_desc* gdsc, i
     g_err = "model tables exceed compiled limits";
     return ISC_UNSUPPORTED;
   }
-  if (precond < 0 || precond > 2) { g_err = "unknown preconditioner"; return ISC_BAD_ARGUMENT; }
+  if (precond < 0 || precond > 3) { g_err = "unknown preconditioner"; return ISC_BAD_ARGUMENT; }
   int ndev = 0;
   if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0) {
     g_err = "no CUDA device";
@@ -377,9 +378,11 @@ extern "C" int isc_create(const isc_model_desc* md, const isc_grid_desc* gdsc, i
   ALLOC(ctx->partial, ctx->npartial * 8);
   ALLOC(ctx->flags, n * 4);
   ALLOC(ctx->fail_d, 4);
-  if (precond != ISC_PRECOND_NONE) {
+  if (precond == ISC_PRECOND_BJACOBI || precond == ISC_PRECOND_RAS) {
     int s = build_ilu(ctx);
     if (s) return s;
+  } else if (precond == ISC_PRECOND_MCILU) {
+    ALLOC(ctx->mc_uinv, (size_t)NB * n * 8);
   }
   *out = ctx;
   return ISC_OK;
@@ -557,18 +560,21 @@ static void free_ilu(isc_ctx* ctx) {
   for (void* p : ptrs)
     if (p) cudaFree(p);
   ctx->ilu = IluDev{};
+  if (ctx->mc_uinv) cudaFree(ctx->mc_uinv);
+  ctx->mc_uinv = nullptr;
   ctx->lvl_ptr_d = nullptr;
   ctx->nlev = 0;
 }
 
 extern "C" int isc_set_precond(isc_ctx* ctx, int32_t precond) {
-  if (precond < 0 || precond > 2) { g_err = "unknown preconditioner"; return ISC_BAD_ARGUMENT; }
+  if (precond < 0 || precond > 3) { g_err = "unknown preconditioner"; return ISC_BAD_ARGUMENT; }
   if (precond == ctx->precond) return ISC_OK;
   CK(cudaStreamSynchronize(ctx->stream));
   free_ilu(ctx);
   ctx->precond = precond;
   ctx->factored = false;
-  if (precond != ISC_PRECOND_NONE) return build_ilu(ctx);
+  if (precond == ISC_PRECOND_BJACOBI || precond == ISC_PRECOND_RAS) return build_ilu(ctx);
+  if (precond == ISC_PRECOND_MCILU) ALLOC(ctx->mc_uinv, (size_t)NB * ctx->g.n * 8);
   return ISC_OK;
 }
 
@@ -647,11 +653,18 @@ extern "C" int isc_precond_setup(isc_ctx* ctx, int64_t* bad_cell) {
   int* fail = ctx->fail_d;
   {
   KScope ks(ctx, KT_ILU_FACTOR);
+  if (ctx->precond == ISC_PRECOND_MCILU) {
+    KScope ks(ctx, KT_ILU_FACTOR);
+    k_mc_factor<<<grid1d(ctx->g.n, 32), dim3(32, NU), 0, st>>>(ctx->g, ctx->offd, ctx->mc_uinv,
+                                                              ctx->fail_d);
+    CK(cudaGetLastError());
+  } else {
   CK(cudaFuncSetAttribute(k_ilu_factor, cudaFuncAttributeMaxDynamicSharedMemorySize,
                           (int)sizeof(FactorSmem)));
   k_ilu_factor<<<ctx->nsub * ILCF, dim3(IL_SLOTS, NU), sizeof(FactorSmem), st>>>(g, L, offd, lp,
                                                                                nlev, fail);
   CK(cudaGetLastError());
+  }
   }
   ++ctx->launches;
   int fail_h = 0;
@@ -674,6 +687,15 @@ static int precond_apply(isc_ctx* ctx, const double* r, double* z) {
     return ISC_OK;
   }
   Dims g = ctx->g;
+  if (ctx->precond == ISC_PRECOND_MCILU) {
+    KScope ks(ctx, KT_ILU_APPLY);
+    const int blocks = grid1d(g.n, 32);
+    k_mc_apply<1><<<blocks, dim3(32, NU), 0, ctx->stream>>>(g, ctx->offd, ctx->mc_uinv, r, z);
+    k_mc_apply<2><<<blocks, dim3(32, NU), 0, ctx->stream>>>(g, ctx->offd, ctx->mc_uinv, r, z);
+    ctx->launches += 2;
+    CK(cudaGetLastError());
+    return ISC_OK;
+  }
   IluDev L = ctx->ilu;
   const double* offd = ctx->offd;
   const int64_t* lp = ctx->lvl_ptr_d;

@@ -380,7 +380,7 @@ __device__ void ilu_factor_tile(const Dims& g, const IluDev& L, const double* __
 // levels are separated by a cluster barrier (release/acquire at cluster
 // scope) instead of a grid-wide sync, and values produced by other CTAs of
 // the cluster are read through L2 (__ldcg).
-constexpr int ILC = 8;    // CTAs per cluster (apply)
+constexpr int ILC = 4;    // CTAs per cluster (apply; 64 clusters stay resident)
 constexpr int ILCF = 4;   // CTAs per cluster (factor: 2 CTAs/SM -> one resident wave)
 
 __global__ void __cluster_dims__(ILCF, 1, 1) __launch_bounds__(IL_SLOTS * NU, 2)
@@ -463,6 +463,166 @@ __global__ void __cluster_dims__(ILC, 1, 1) __launch_bounds__(IL_SLOTS * NU)
       __syncthreads();
     }
     cluster.sync();
+  }
+}
+
+// ------------------------------------------- multicolour block ILU(0)
+// Red-black ordering (red: i+j+k even) of the decoupled system A = I + sum B_d.
+// Red rows have no lower neighbours, so U_red = I and L_black,red = A; the
+// black pivots are U_b = I - sum_d B_bd B_{nb,-d}. Apply (M = LU):
+//   pass 1 (black):  z_b = U_b^-1 (r_b - sum_d B_bd r_nb)
+//   pass 2 (red):    z_r = r_r - sum_d B_rd z_nb
+// Every pass is fully parallel (no wavefront); BASELINE north_star's
+// "multicolour block-ILU(0)".
+
+__device__ __forceinline__ bool is_black(int i, int j, int k) { return ((i + j + k) & 1) != 0; }
+
+// thread (cell lane, column u); black cells only do work
+__global__ void __launch_bounds__(32 * NU, 2) k_mc_factor(Dims g, const double* __restrict__ offd,
+                                                          double* __restrict__ uinv, int* fail) {
+  __shared__ double bsh[NU][NU][32];   // B_bd (row, col) of the current direction
+  __shared__ double colk[NU][32];
+  __shared__ int pivs[32];
+  const int64_t n = g.n;
+  const int ls = threadIdx.x, u = threadIdx.y;
+  const int64_t c = (int64_t)blockIdx.x * 32 + ls;
+  const bool in = c < n;
+  int i = 0, j = 0, k = 0;
+  if (in) { i = (int)(c % g.nx); j = (int)((c / g.nx) % g.ny); k = (int)(c / g.nxny); }
+  const bool live = in && is_black(i, j, k);
+  double ucol[NU];
+#pragma unroll
+  for (int r = 0; r < NU; ++r) ucol[r] = (r == u) ? 1.0 : 0.0;
+#pragma unroll 1
+  for (int d = 0; d < NDIR; ++d) {
+    const int64_t nb = live ? neighbour(g, c, i, j, k, d) : -1;
+    if (nb >= 0) {
+      const double* B = offd + (int64_t)(d * NB + u) * n + c;
+#pragma unroll
+      for (int r = 0; r < NU; ++r) bsh[r][u][ls] = B[(int64_t)(r * NU) * n];
+    }
+    __syncthreads();
+    if (nb >= 0) {
+      const double* Bo = offd + (int64_t)(opposite(d) * NB + u) * n + nb;   // column u
+      double bc[NU];
+#pragma unroll
+      for (int q = 0; q < NU; ++q) bc[q] = Bo[(int64_t)(q * NU) * n];
+#pragma unroll
+      for (int r = 0; r < NU; ++r) {
+        double t = 0.0;
+#pragma unroll
+        for (int q = 0; q < NU; ++q) t += bsh[r][q][ls] * bc[q];
+        ucol[r] -= t;
+      }
+    }
+    __syncthreads();
+  }
+  // Gauss-Jordan inverse (partial pivoting, tolerance 1e-13 max|U|)
+  double icol[NU];
+#pragma unroll
+  for (int r = 0; r < NU; ++r) icol[r] = (r == u) ? 1.0 : 0.0;
+  {
+    double m = 0.0;
+#pragma unroll
+    for (int r = 0; r < NU; ++r) m = fmax(m, fabs(ucol[r]));
+    bsh[0][u][ls] = m;
+  }
+  __syncthreads();
+  double amax = 0.0;
+#pragma unroll
+  for (int q = 0; q < NU; ++q) amax = fmax(amax, bsh[0][q][ls]);
+  const double tol = 1e-13 * amax;
+  __syncthreads();
+#pragma unroll
+  for (int kk = 0; kk < NU; ++kk) {
+    if (u == kk) {
+      int piv = kk;
+      double pv = fabs(ucol[kk]);
+#pragma unroll
+      for (int r = kk + 1; r < NU; ++r) {
+        const double v = fabs(ucol[r]);
+        if (v > pv) { pv = v; piv = r; }
+      }
+      if (live && (pv <= tol || amax == 0.0)) atomicMin(fail, 1);
+#pragma unroll
+      for (int r = 0; r < NU; ++r) {
+        double v = ucol[r];
+        if (r == kk) {
+#pragma unroll
+          for (int q = kk + 1; q < NU; ++q) if (q == piv) v = ucol[q];
+        } else if (r == piv) {
+          v = ucol[kk];
+        }
+        colk[r][ls] = v;
+      }
+      pivs[ls] = piv;
+    }
+    __syncthreads();
+    const int piv = pivs[ls];
+    if (piv != kk) {
+      double t0 = ucol[kk], t1 = icol[kk];
+#pragma unroll
+      for (int q = kk + 1; q < NU; ++q)
+        if (q == piv) { ucol[kk] = ucol[q]; icol[kk] = icol[q]; ucol[q] = t0; icol[q] = t1; }
+    }
+    const double dinv = 1.0 / colk[kk][ls];
+    ucol[kk] *= dinv;
+    icol[kk] *= dinv;
+#pragma unroll
+    for (int r = 0; r < NU; ++r) {
+      if (r == kk) continue;
+      const double f = colk[r][ls];
+      if (f != 0.0) { ucol[r] -= f * ucol[kk]; icol[r] -= f * icol[kk]; }
+    }
+    __syncthreads();
+  }
+  if (live) {
+#pragma unroll
+    for (int r = 0; r < NU; ++r) uinv[(int64_t)(r * NU + u) * n + c] = icol[r];
+  }
+}
+
+// pass 1 (black rows) / pass 2 (red rows); thread (cell lane, row r)
+template <int PASS>
+__global__ void __launch_bounds__(32 * NU) k_mc_apply(Dims g, const double* __restrict__ offd,
+                                                      const double* __restrict__ uinv,
+                                                      const double* __restrict__ rin,
+                                                      double* __restrict__ z) {
+  __shared__ double wsh[NU][32];
+  const int64_t n = g.n;
+  const int ls = threadIdx.x, r = threadIdx.y;
+  const int64_t c = (int64_t)blockIdx.x * 32 + ls;
+  const bool in = c < n;
+  int i = 0, j = 0, k = 0;
+  if (in) { i = (int)(c % g.nx); j = (int)((c / g.nx) % g.ny); k = (int)(c / g.nxny); }
+  const bool live = in && (is_black(i, j, k) == (PASS == 1));
+  double w = 0.0;
+  if (live) {
+    // pass 1 reads red neighbours of r (z_red = r_red); pass 2 the black z
+    const double* src = PASS == 1 ? rin : z;
+    w = rin[r * n + c];
+#pragma unroll
+    for (int d = 0; d < NDIR; ++d) {
+      const int64_t nb = neighbour(g, c, i, j, k, d);
+      if (nb < 0) continue;
+      const double* blk = offd + (int64_t)((d * NU + r) * NU) * n + c;
+      double t = 0.0;
+#pragma unroll
+      for (int u = 0; u < NU; ++u) t += blk[(int64_t)u * n] * src[(int64_t)u * n + nb];
+      w -= t;
+    }
+  }
+  if (PASS == 2) {
+    if (live) z[r * n + c] = w;
+    return;
+  }
+  wsh[r][ls] = w;
+  __syncthreads();
+  if (live) {
+    double zz = 0.0;
+#pragma unroll
+    for (int u = 0; u < NU; ++u) zz += uinv[(int64_t)(r * NU + u) * n + c] * wsh[u][ls];
+    z[r * n + c] = zz;
   }
 }
 

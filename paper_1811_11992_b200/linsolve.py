@@ -26,7 +26,7 @@ NU = 9
 class BlockSolver:
     def __init__(self, grid, ws: Workspace, tol: float = 1e-5, maxiter: int = 200,
                  precond: str = "ras"):
-        if precond not in ("none", "bjacobi", "ras"):
+        if precond not in ("none", "bjacobi", "ras", "mcilu"):
             raise ValueError(f"unknown preconditioner {precond!r}")
         self.grid, self.ws, self.tol, self.maxiter, self.precond = grid, ws, tol, maxiter, precond
         ws.precond = precond
