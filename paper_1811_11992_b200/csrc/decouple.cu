@@ -55,7 +55,7 @@ __device__ __forceinline__ double* col_ptr(int j, int r, int64_t n, int64_t c, d
   return rhs + (int64_t)r * n + c;
 }
 
-__global__ void __launch_bounds__(1024) k_decouple(Dims g, double* diag, double* offd, double* rhs,
+__global__ void __launch_bounds__(DC_CELLS * 32) k_decouple(Dims g, double* diag, double* offd, double* rhs,
                                                    int* flags, unsigned long long* bad) {
   __shared__ double colk[NU][DC_CELLS];
   __shared__ double cmax[NU][DC_CELLS];
