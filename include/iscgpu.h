@@ -114,6 +114,16 @@ int isc_assemble(isc_ctx *ctx, const double *d_state, const double *h_bhp, const
                  double dt, double t_new, const uint8_t *h_capped, int32_t freeze,
                  double *h_wells_out, int64_t *bad_cell);
 
+/* Same inputs/outputs as isc_assemble, with the well Schur fold and the
+ * Gauss-Jordan decoupling fused into the face kernel (the un-decoupled
+ * blocks are not kept; isc_export_system is not available afterwards).
+ * The following isc_solve skips its decoupling step and reports a singular
+ * block found here. */
+int isc_assemble_decoupled(isc_ctx *ctx, const double *d_state, const double *h_bhp,
+                           const double *d_accn, double dt, double t_new,
+                           const uint8_t *h_capped, int32_t freeze, double *h_wells_out,
+                           int64_t *bad_cell);
+
 /* Copy an internal per-cell array to d_dst: 0 resid (9 x n), 1 acc (9 x n),
  * 2 src (9 x n), 3 yfull (5 x n), 4 record (ISC_NREC x n), 5 upwind flags
  * int8 (3 axes x 3 phases x n). */

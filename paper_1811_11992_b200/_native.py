@@ -62,6 +62,8 @@ _SIGS = {
     "isc_block_size": (ctypes.c_int, []),
     "isc_assemble": (ctypes.c_int, [VP, VP, VP, VP, ctypes.c_double, ctypes.c_double, VP,
                                     ctypes.c_int32, VP, c_int64_p]),
+    "isc_assemble_decoupled": (ctypes.c_int, [VP, VP, VP, VP, ctypes.c_double, ctypes.c_double,
+                                              VP, ctypes.c_int32, VP, c_int64_p]),
     "isc_copy_out": (ctypes.c_int, [VP, ctypes.c_int32, VP]),
     "isc_export_system": (ctypes.c_int, [VP, VP, VP, VP]),
     "isc_import_system": (ctypes.c_int, [VP, VP, VP, VP, VP]),

@@ -12,6 +12,7 @@
 #include "../../include/iscgpu.h"
 #include "assemble.cu"
 #include "decouple.cu"
+#include "fused.cu"
 #include "newton.cu"
 #include "solver.cu"
 
@@ -80,6 +81,9 @@ struct isc_ctx {
   int64_t* lvl_ptr_d = nullptr;
   int nlev = 0;
   int nsub = 1;
+  double* schur = nullptr;        // per-well Schur rhs terms (fused path)
+  int64_t dc_bad_cell = -1;       // singular block found by the fused decoupling
+  int dc_bad_col = -1;
   double* mc_uinv = nullptr;   // multicolour ILU: U_b^-1 of black cells
   // timing
   cudaEvent_t ev[8] = {};
@@ -356,6 +360,7 @@ extern "C" int isc_create(const isc_model_desc* md, const isc_grid_desc* gdsc, i
   ALLOC(ctx->wout_d, std::max(1, nwells) * WOUT * 8);
   CK(cudaMallocHost(&ctx->wout_h, std::max(1, nwells) * WOUT * 8));
   ALLOC(ctx->bhp_d, std::max(1, nwells) * 8);
+  ALLOC(ctx->schur, std::max(1, nwells) * NU * 8);
   ALLOC(ctx->capped_d, std::max(1, nwells));
   // assembly buffers
   ALLOC(ctx->rec, (size_t)NREC * n * 8);
@@ -396,7 +401,7 @@ extern "C" int isc_destroy(isc_ctx* ctx) {
                   ctx->capped_d, ctx->rec, ctx->acc, ctx->src, ctx->resid, ctx->diag,
                   ctx->offd, ctx->upw, ctx->bad_d, ctx->rhs, ctx->xk, ctx->rk, ctx->rhat,
                   ctx->pk, ctx->vk, ctx->phat, ctx->shat, ctx->sk, ctx->tk, ctx->sc,
-                  ctx->partial, ctx->flags, ctx->fail_d};
+                  ctx->partial, ctx->flags, ctx->fail_d, ctx->schur};
   free_ilu(ctx);
   for (void* p : ptrs)
     if (p) cudaFree(p);
@@ -499,6 +504,76 @@ extern "C" int isc_assemble(isc_ctx* ctx, const double* d_state, const double* h
   STAGE(stage_end(ctx, 0));   // synchronises
   if (ctx->nw > 0 && h_wells_out) std::memcpy(h_wells_out, ctx->wout_h, ctx->nw * WOUT * 8);
   ctx->decoupled = false;
+  ctx->factored = false;
+  return ISC_OK;
+}
+
+// Fast path: assemble + well Schur fold + decoupling fused (fused.cu). The
+// un-decoupled diagonal/off-diagonal blocks are never written; a singular
+// block is reported by the following isc_solve, as the reference raises it
+// inside BlockSolver.solve (linsolve.py:458-463).
+extern "C" int isc_assemble_decoupled(isc_ctx* ctx, const double* d_state, const double* h_bhp,
+                                      const double* d_accn, double dt, double t_new,
+                                      const uint8_t* h_capped, int32_t freeze,
+                                      double* h_wells_out, int64_t* bad_cell) {
+  const int64_t n = ctx->g.n;
+  cudaStream_t st = ctx->stream;
+  STAGE(stage_begin(ctx, 0));
+  if (ctx->nw > 0) {
+    CK(cudaMemcpyAsync(ctx->bhp_d, h_bhp, ctx->nw * 8, cudaMemcpyHostToDevice, st));
+    CK(cudaMemcpyAsync(ctx->capped_d, h_capped, ctx->nw, cudaMemcpyHostToDevice, st));
+  }
+  CK(cudaMemsetAsync(ctx->bad_d, 0xff, 8, st));
+  CellArgs A{ctx->g, d_state, ctx->phi_ref, ctx->vol, ctx->hl_area, ctx->hl_kob, ctx->hl_d,
+             ctx->hl_rho, ctx->hl_tini, d_accn, dt, ctx->rec, ctx->acc, ctx->src,
+             ctx->resid, ctx->diag, ctx->bad_d};
+  { KScope ks(ctx, KT_CELL); k_cell<<<grid1d(n, 128), 128, 0, st>>>(ctx->M, A); }
+  LAUNCH_CHECK();
+  CK(cudaMemcpyAsync(ctx->bad_h, ctx->bad_d, 8, cudaMemcpyDeviceToHost, st));
+  CK(cudaStreamSynchronize(st));
+  if (*ctx->bad_h != ~0ULL) {
+    if (bad_cell) *bad_cell = (int64_t)*ctx->bad_h;
+    g_err = "coke fills the pore volume";
+    STAGE(stage_end(ctx, 0));
+    return ISC_PORE_SPACE_EXHAUSTED;
+  }
+  if (ctx->nw > 0) {
+    KScope ks(ctx, KT_WELLS);
+    k_wells<<<1, 32, 0, st>>>(ctx->M, ctx->g, ctx->nw, ctx->wells_d, d_state, ctx->bhp_d,
+                              ctx->capped_d, ctx->rec, ctx->depth, t_new, ctx->resid,
+                              ctx->diag, ctx->wout_d);
+    LAUNCH_CHECK();
+    k_schur_pre<<<1, 32, 0, st>>>(ctx->g, ctx->nw, ctx->wcell_d, ctx->wout_d, WOUT, ctx->diag,
+                                  ctx->schur);
+    LAUNCH_CHECK();
+    CK(cudaMemcpyAsync(ctx->wout_h, ctx->wout_d, ctx->nw * WOUT * 8, cudaMemcpyDeviceToHost, st));
+  }
+  CK(cudaMemsetAsync(ctx->flags, 0, n * 4, st));
+  CK(cudaMemsetAsync(ctx->bad_d, 0xff, 8, st));
+  {
+    KScope ks(ctx, KT_FACE);
+    FaceArgs F{ctx->g, d_state, ctx->rec, ctx->depth, ctx->gd, ctx->td, ctx->upw, freeze,
+               ctx->resid, ctx->diag, ctx->offd};
+    FusedArgs P{F, ctx->resid, ctx->rhs, ctx->nw, ctx->wcell_d, ctx->schur, ctx->flags,
+                ctx->bad_d};
+    CK(cudaFuncSetAttribute(k_face_dc, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                            (int)sizeof(FusedSmem)));
+    k_face_dc<<<grid1d(n, FD_CELLS), FD_CELLS * 64, sizeof(FusedSmem), st>>>(P);
+    LAUNCH_CHECK();
+  }
+  CK(cudaMemcpyAsync(ctx->bad_h, ctx->bad_d, 8, cudaMemcpyDeviceToHost, st));
+  STAGE(stage_end(ctx, 0));   // synchronises
+  if (ctx->nw > 0 && h_wells_out) std::memcpy(h_wells_out, ctx->wout_h, ctx->nw * WOUT * 8);
+  ctx->dc_bad_cell = -1;
+  ctx->dc_bad_col = -1;
+  if (*ctx->bad_h != ~0ULL) {
+    const int64_t c = (int64_t)*ctx->bad_h;
+    int flag = 0;
+    CK(cudaMemcpy(&flag, ctx->flags + c, 4, cudaMemcpyDeviceToHost));
+    ctx->dc_bad_cell = c;
+    ctx->dc_bad_col = flag - 1;
+  }
+  ctx->decoupled = true;
   ctx->factored = false;
   return ISC_OK;
 }
@@ -630,6 +705,7 @@ extern "C" int isc_decouple(isc_ctx* ctx, int64_t* bad_cell, int32_t* bad_col) {
     return ISC_SINGULAR_CELL_BLOCK;
   }
   ctx->decoupled = true;
+  ctx->dc_bad_cell = -1;
   return ISC_OK;
 }
 
@@ -897,6 +973,22 @@ extern "C" int isc_solve(isc_ctx* ctx, double tol, int32_t maxiter, double* d_du
   if (!ctx->decoupled) {
     int s = isc_decouple(ctx, bad_cell, bad_col);
     if (s) return s;
+  } else {
+    for (int w = 0; w < ctx->nw; ++w) {
+      const double dwdb = ctx->wout_h[w * WOUT + 1];
+      if (dwdb == 0.0 || !std::isfinite(dwdb)) {
+        if (bad_cell) *bad_cell = -1;
+        if (bad_col) *bad_col = -1;
+        g_err = "well equation has a zero bhp derivative";
+        return ISC_SINGULAR_CELL_BLOCK;
+      }
+    }
+    if (ctx->dc_bad_cell >= 0) {
+      if (bad_cell) *bad_cell = ctx->dc_bad_cell;
+      if (bad_col) *bad_col = ctx->dc_bad_col;
+      g_err = "diagonal block is singular";
+      return ISC_SINGULAR_CELL_BLOCK;
+    }
   }
   if (!ctx->factored) {
     int s = isc_precond_setup(ctx, bad_cell);

@@ -105,10 +105,12 @@ def desired_capped(wells, capped, bhp, blocks):
 class Simulator:
     """Device-resident mirror of the reference ``Simulator`` (newton.py:214-437)."""
 
-    def __init__(self, grid, pack, wells, streams, state, schedule, solver, heat_loss=None):
+    def __init__(self, grid, pack, wells, streams, state, schedule, solver, heat_loss=None,
+                 fused: bool = True):
         self.grid, self.pack = grid, pack
         self.wells, self.streams = tuple(wells), tuple(streams)
         self.schedule, self.solver_cfg = schedule, solver
+        self.fused = fused   # assemble+Schur+decoupling in one kernel (fused.cu)
         self.ctx = DeviceContext(grid, pack, self.wells, self.streams, solver.precond, heat_loss)
         dev = self.ctx.device
         self.state = DeviceState(state_to_device(state, dev), np.asarray(state.bhp, dtype=float))
@@ -129,7 +131,7 @@ class Simulator:
 
     # -- device operations ------------------------------------------------------
     def _assemble(self, st: DeviceState, accn, dt, t_new, capped, freeze):
-        wout = self.ctx.assemble(st.u, st.bhp, accn, dt, t_new, capped, freeze)
+        wout = self.ctx.assemble(st.u, st.bhp, accn, dt, t_new, capped, freeze, fused=self.fused)
         return blocks_from_wout(self.wells, wout)
 
     def scaled_norm(self, blocks, dt, capped) -> float:
