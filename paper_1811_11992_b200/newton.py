@@ -106,7 +106,7 @@ class Simulator:
     """Device-resident mirror of the reference ``Simulator`` (newton.py:214-437)."""
 
     def __init__(self, grid, pack, wells, streams, state, schedule, solver, heat_loss=None,
-                 fused: bool = True):
+                 fused: bool = False):
         self.grid, self.pack = grid, pack
         self.wells, self.streams = tuple(wells), tuple(streams)
         self.schedule, self.solver_cfg = schedule, solver
