@@ -70,7 +70,7 @@ __global__ void __launch_bounds__(128) k_cell(const Model M, const CellArgs A) {
   double phif, dphif_cc;
   if (rho_coke > 0.0 && isfinite(rho_coke)) { phif = phi - cc / rho_coke; dphif_cc = -1.0 / rho_coke; }
   else { phif = phi; dphif_cc = 0.0; }
-  if (phif <= 0.0) { atomicMin(A.bad, (unsigned long long)c); return; }
+  if (phif <= 0.0) { atomicMin(A.bad, (unsigned long long)cell_of(A.g, c)); return; }
   const double t_ref = rk[RK_TREF], eps_per = rk[RK_EPS_PER];
   double* rec = A.rec;
 #define REC(f) rec[(int64_t)(f) * n + c]
@@ -771,12 +771,12 @@ __device__ __forceinline__ void face_row(const int row, const CellView& A_, cons
 // grid: (ceil(n/32), 1); block: (32, NU) -> threadIdx.y = residual row
 __global__ void __launch_bounds__(32 * NU, 2) k_face(const FaceArgs F) {
   const int64_t n = F.g.n;
-  const int64_t c = (int64_t)blockIdx.x * 32 + threadIdx.x;
+  const int64_t c = (int64_t)blockIdx.x * 32 + threadIdx.x;   // storage position
   const int row = threadIdx.y;
   if (c >= n) return;
-  const int i = (int)(c % F.g.nx);
-  const int j = (int)((c / F.g.nx) % F.g.ny);
-  const int k = (int)(c / F.g.nxny);
+  const int64_t cell = cell_of(F.g, c);
+  int i, j, k;
+  cell_ijk(F.g, cell, i, j, k);
   double res = F.resid[row * n + c];
   double drow[NU];
 #pragma unroll
@@ -784,7 +784,7 @@ __global__ void __launch_bounds__(32 * NU, 2) k_face(const FaceArgs F) {
   const CellView C{F.rec, n, c};
 #pragma unroll 1
   for (int d = 0; d < NDIR; ++d) {
-    const int64_t nb = neighbour(F.g, c, i, j, k, d);
+    const int64_t nb = nb_pos(F.g, cell, i, j, k, d);
     double* orow = F.offd + (int64_t)((d * NU + row) * NU) * n + c;
     if (nb < 0) {
 #pragma unroll
@@ -991,20 +991,22 @@ __global__ void k_export_system(Dims g, const int64_t* __restrict__ conn_id,
                                 const double* __restrict__ resid, double* rdiag, double* roffd,
                                 double* rresid) {
   const int64_t n = g.n;
-  const int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;   // natural cell
   if (c >= n) return;
-  for (int e = 0; e < NB; ++e) rdiag[c * NB + e] = diag[(int64_t)e * n + c];
-  for (int r = 0; r < NU; ++r) rresid[c * NU + r] = resid[(int64_t)r * n + c];
-  const int i = (int)(c % g.nx), j = (int)((c / g.nx) % g.ny), k = (int)(c / g.nxny);
+  const int64_t pc = pos_of(g, c);
+  for (int e = 0; e < NB; ++e) rdiag[c * NB + e] = diag[(int64_t)e * n + pc];
+  for (int r = 0; r < NU; ++r) rresid[c * NU + r] = resid[(int64_t)r * n + pc];
+  int i, j, k;
+  cell_ijk(g, c, i, j, k);
   for (int axis = 0; axis < 3; ++axis) {
     const int64_t ic = conn_id[axis * n + c];
     if (ic < 0) continue;
     const int dplus = DXP + axis;
-    const int64_t nb = neighbour(g, c, i, j, k, dplus);
+    const int64_t nbp = nb_pos(g, c, i, j, k, dplus);
     const int dminus = opposite(dplus);
     for (int e = 0; e < NB; ++e) {
-      roffd[(ic * 2 + 0) * NB + e] = offd[(int64_t)(dplus * NB + e) * n + c];
-      roffd[(ic * 2 + 1) * NB + e] = offd[(int64_t)(dminus * NB + e) * n + nb];
+      roffd[(ic * 2 + 0) * NB + e] = offd[(int64_t)(dplus * NB + e) * n + pc];
+      roffd[(ic * 2 + 1) * NB + e] = offd[(int64_t)(dminus * NB + e) * n + nbp];
     }
   }
 }
@@ -1015,24 +1017,42 @@ __global__ void k_import_system(Dims g, const int64_t* __restrict__ conn_id,
                                 const double* __restrict__ rresid, double* diag, double* offd,
                                 double* resid) {
   const int64_t n = g.n;
-  const int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;   // natural cell
   if (c >= n) return;
-  for (int e = 0; e < NB; ++e) diag[(int64_t)e * n + c] = rdiag[c * NB + e];
+  const int64_t pc = pos_of(g, c);
+  for (int e = 0; e < NB; ++e) diag[(int64_t)e * n + pc] = rdiag[c * NB + e];
   if (resid)
-    for (int r = 0; r < NU; ++r) resid[(int64_t)r * n + c] = rresid[c * NU + r];
-  const int i = (int)(c % g.nx), j = (int)((c / g.nx) % g.ny), k = (int)(c / g.nxny);
+    for (int r = 0; r < NU; ++r) resid[(int64_t)r * n + pc] = rresid[c * NU + r];
+  int i, j, k;
+  cell_ijk(g, c, i, j, k);
   for (int d = 0; d < NDIR; ++d) {
     const int64_t nb = neighbour(g, c, i, j, k, d);
     if (nb < 0) {
-      for (int e = 0; e < NB; ++e) offd[(int64_t)(d * NB + e) * n + c] = 0.0;
+      for (int e = 0; e < NB; ++e) offd[(int64_t)(d * NB + e) * n + pc] = 0.0;
       continue;
     }
     int64_t ic;
     int side;
     if (d >= DXP) { ic = conn_id[(d - DXP) * n + c]; side = 0; }
     else { ic = conn_id[(2 - d) * n + nb]; side = 1; }
-    for (int e = 0; e < NB; ++e) offd[(int64_t)(d * NB + e) * n + c] = roffd[(ic * 2 + side) * NB + e];
+    for (int e = 0; e < NB; ++e) offd[(int64_t)(d * NB + e) * n + pc] = roffd[(ic * 2 + side) * NB + e];
   }
+}
+
+// natural-order SoA (rows x n) <-> storage positions
+template <typename T>
+__global__ void k_to_pos(Dims g, int rows, const T* __restrict__ src, T* __restrict__ dst) {
+  const int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (c >= g.n) return;
+  const int64_t p = pos_of(g, c);
+  for (int r = 0; r < rows; ++r) dst[(int64_t)r * g.n + p] = src[(int64_t)r * g.n + c];
+}
+template <typename T>
+__global__ void k_from_pos(Dims g, int rows, const T* __restrict__ src, T* __restrict__ dst) {
+  const int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (c >= g.n) return;
+  const int64_t p = pos_of(g, c);
+  for (int r = 0; r < rows; ++r) dst[(int64_t)r * g.n + c] = src[(int64_t)r * g.n + p];
 }
 
 }  // namespace isc

@@ -54,7 +54,9 @@ struct isc_ctx {
   int nw = 0;
   WellDev* wells_d = nullptr;
   int64_t* wcell_d = nullptr;
-  std::vector<int64_t> wcell_h;
+  std::vector<int64_t> wcell_h;   // natural cell of each well
+  std::vector<int64_t> wpos_h;    // its storage position
+  double *st_c = nullptr, *accn_c = nullptr;   // state / accn in storage order
   double* wout_d = nullptr;
   double* wout_h = nullptr;   // pinned
   double* bhp_d = nullptr;
@@ -224,7 +226,7 @@ static int build_ilu(isc_ctx* ctx) {
           const int li = i - b.lo[0], lj = j - b.lo[1], lk = k - b.lo[2];
           const int64_t s = fill[li + lj + lk]++;
           slot[((size_t)lk * wy + lj) * wx + li] = s;
-          cell[s] = i + (int64_t)g.nx * (j + (int64_t)g.ny * k);
+          cell[s] = pos_of(g, i + (int64_t)g.nx * (j + (int64_t)g.ny * k));
           const int ijk[3] = {i, j, k};
           owned[s] = (ijk[axis] >= b.olo && ijk[axis] < b.ohi) ? 1 : 0;
         }
@@ -295,6 +297,8 @@ extern "C" int isc_create(const isc_model_desc* md, const isc_grid_desc* gdsc, i
   g.nx = gdsc->nx; g.ny = gdsc->ny; g.nz = gdsc->nz;
   g.nxny = (int64_t)g.nx * g.ny;
   g.n = g.nxny * g.nz;
+  g.colored = (g.nx % 2 == 0) ? 1 : 0;
+  g.half = g.n / 2;
   const int64_t n = g.n;
   // model
   Model& M = ctx->M;
@@ -324,16 +328,31 @@ extern "C" int isc_create(const isc_model_desc* md, const isc_grid_desc* gdsc, i
   // static grid arrays
   ALLOC(ctx->depth, n * 8); ALLOC(ctx->vol, n * 8); ALLOC(ctx->phi_ref, n * 8);
   ALLOC(ctx->gd, 3 * n * 8); ALLOC(ctx->td, 3 * n * 8); ALLOC(ctx->conn_id, 3 * n * 8);
-  CK(cudaMemcpy(ctx->depth, gdsc->depth, n * 8, cudaMemcpyHostToDevice));
-  CK(cudaMemcpy(ctx->vol, gdsc->volume, n * 8, cudaMemcpyHostToDevice));
-  CK(cudaMemcpy(ctx->phi_ref, gdsc->phi_ref, n * 8, cudaMemcpyHostToDevice));
-  CK(cudaMemcpy(ctx->gd, gdsc->gd, 3 * n * 8, cudaMemcpyHostToDevice));
-  CK(cudaMemcpy(ctx->td, gdsc->td, 3 * n * 8, cudaMemcpyHostToDevice));
-  CK(cudaMemcpy(ctx->conn_id, gdsc->conn_id, 3 * n * 8, cudaMemcpyHostToDevice));
-  if (gdsc->hl_area) {
-    ALLOC(ctx->hl_area, n * 8);
-    CK(cudaMemcpy(ctx->hl_area, gdsc->hl_area, n * 8, cudaMemcpyHostToDevice));
+  {
+    // per-cell static arrays in storage order (common.cuh: colour-blocked)
+    std::vector<int64_t> pos(n);
+    for (int64_t c = 0; c < n; ++c) pos[c] = pos_of(g, c);
+    std::vector<double> tmp((size_t)3 * n);
+    auto put = [&](double* dst, const double* src, int rows) -> int {
+      for (int r = 0; r < rows; ++r)
+        for (int64_t c = 0; c < n; ++c) tmp[(size_t)r * n + pos[c]] = src[(size_t)r * n + c];
+      return cudaMemcpy(dst, tmp.data(), (size_t)rows * n * 8, cudaMemcpyHostToDevice) ==
+                     cudaSuccess ? 0 : ISC_CUDA_ERROR;
+    };
+    if (put(ctx->depth, gdsc->depth, 1) || put(ctx->vol, gdsc->volume, 1) ||
+        put(ctx->phi_ref, gdsc->phi_ref, 1) || put(ctx->gd, gdsc->gd, 3) ||
+        put(ctx->td, gdsc->td, 3)) {
+      g_err = "static array upload failed";
+      return ISC_CUDA_ERROR;
+    }
+    CK(cudaMemcpy(ctx->conn_id, gdsc->conn_id, 3 * n * 8, cudaMemcpyHostToDevice));
+    if (gdsc->hl_area) {
+      ALLOC(ctx->hl_area, n * 8);
+      if (put(ctx->hl_area, gdsc->hl_area, 1)) return ISC_CUDA_ERROR;
+    }
   }
+  ALLOC(ctx->st_c, (size_t)NU * n * 8);
+  ALLOC(ctx->accn_c, (size_t)NU * n * 8);
   ctx->hl_kob = gdsc->hl_kob; ctx->hl_d = gdsc->hl_d; ctx->hl_rho = gdsc->hl_rho;
   ctx->hl_tini = gdsc->hl_tini;
   // wells
@@ -351,11 +370,13 @@ extern "C" int isc_create(const isc_model_desc* md, const isc_grid_desc* gdsc, i
       for (int j = 0; j < NCG; ++j) d.s_yinj[j] = s.s_yinj[j];
       d.s_tinj = s.s_tinj; d.s_mu = s.s_mu; d.s_h = s.s_h; d.s_mbar = s.s_mbar;
       ctx->wcell_h.push_back(s.cell);
+      ctx->wpos_h.push_back(pos_of(g, s.cell));
+      d.cell = pos_of(g, s.cell);
     }
     ALLOC(ctx->wells_d, nwells * sizeof(WellDev));
     CK(cudaMemcpy(ctx->wells_d, wd.data(), nwells * sizeof(WellDev), cudaMemcpyHostToDevice));
     ALLOC(ctx->wcell_d, nwells * 8);
-    CK(cudaMemcpy(ctx->wcell_d, ctx->wcell_h.data(), nwells * 8, cudaMemcpyHostToDevice));
+    CK(cudaMemcpy(ctx->wcell_d, ctx->wpos_h.data(), nwells * 8, cudaMemcpyHostToDevice));
   }
   ALLOC(ctx->wout_d, std::max(1, nwells) * WOUT * 8);
   CK(cudaMallocHost(&ctx->wout_h, std::max(1, nwells) * WOUT * 8));
@@ -401,7 +422,7 @@ extern "C" int isc_destroy(isc_ctx* ctx) {
                   ctx->capped_d, ctx->rec, ctx->acc, ctx->src, ctx->resid, ctx->diag,
                   ctx->offd, ctx->upw, ctx->bad_d, ctx->rhs, ctx->xk, ctx->rk, ctx->rhat,
                   ctx->pk, ctx->vk, ctx->phat, ctx->shat, ctx->sk, ctx->tk, ctx->sc,
-                  ctx->partial, ctx->flags, ctx->fail_d, ctx->schur};
+                  ctx->partial, ctx->flags, ctx->fail_d, ctx->schur, ctx->st_c, ctx->accn_c};
   free_ilu(ctx);
   for (void* p : ptrs)
     if (p) cudaFree(p);
@@ -476,6 +497,11 @@ extern "C" int isc_assemble(isc_ctx* ctx, const double* d_state, const double* h
     CK(cudaMemcpyAsync(ctx->capped_d, h_capped, ctx->nw, cudaMemcpyHostToDevice, st));
   }
   CK(cudaMemsetAsync(ctx->bad_d, 0xff, 8, st));
+  k_to_pos<double><<<grid1d(n, 256), 256, 0, st>>>(ctx->g, NU, d_state, ctx->st_c);
+  k_to_pos<double><<<grid1d(n, 256), 256, 0, st>>>(ctx->g, NU, d_accn, ctx->accn_c);
+  ctx->launches += 2;
+  d_state = ctx->st_c;
+  d_accn = ctx->accn_c;
   CellArgs A{ctx->g, d_state, ctx->phi_ref, ctx->vol, ctx->hl_area, ctx->hl_kob, ctx->hl_d,
              ctx->hl_rho, ctx->hl_tini, d_accn, dt, ctx->rec, ctx->acc, ctx->src,
              ctx->resid, ctx->diag, ctx->bad_d};
@@ -524,6 +550,11 @@ extern "C" int isc_assemble_decoupled(isc_ctx* ctx, const double* d_state, const
     CK(cudaMemcpyAsync(ctx->capped_d, h_capped, ctx->nw, cudaMemcpyHostToDevice, st));
   }
   CK(cudaMemsetAsync(ctx->bad_d, 0xff, 8, st));
+  k_to_pos<double><<<grid1d(n, 256), 256, 0, st>>>(ctx->g, NU, d_state, ctx->st_c);
+  k_to_pos<double><<<grid1d(n, 256), 256, 0, st>>>(ctx->g, NU, d_accn, ctx->accn_c);
+  ctx->launches += 2;
+  d_state = ctx->st_c;
+  d_accn = ctx->accn_c;
   CellArgs A{ctx->g, d_state, ctx->phi_ref, ctx->vol, ctx->hl_area, ctx->hl_kob, ctx->hl_d,
              ctx->hl_rho, ctx->hl_tini, d_accn, dt, ctx->rec, ctx->acc, ctx->src,
              ctx->resid, ctx->diag, ctx->bad_d};
@@ -591,7 +622,16 @@ extern "C" int isc_copy_out(isc_ctx* ctx, int32_t what, void* d_dst) {
     case 5: src = ctx->upw; bytes = (size_t)9 * n; break;
     default: g_err = "unknown array"; return ISC_BAD_ARGUMENT;
   }
-  CK(cudaMemcpyAsync(d_dst, src, bytes, cudaMemcpyDeviceToDevice, ctx->stream));
+  // back to natural cell order
+  if (what == 5) {
+    k_from_pos<int8_t><<<grid1d(n, 256), 256, 0, ctx->stream>>>(ctx->g, 9, (const int8_t*)src,
+                                                                (int8_t*)d_dst);
+  } else {
+    const int rows = (int)(bytes / 8 / n);
+    k_from_pos<double><<<grid1d(n, 256), 256, 0, ctx->stream>>>(ctx->g, rows, (const double*)src,
+                                                                (double*)d_dst);
+  }
+  LAUNCH_CHECK();
   CK(cudaStreamSynchronize(ctx->stream));
   return ISC_OK;
 }
@@ -710,8 +750,8 @@ extern "C" int isc_decouple(isc_ctx* ctx, int64_t* bad_cell, int32_t* bad_col) {
 }
 
 extern "C" int isc_copy_rhs(isc_ctx* ctx, double* d_dst) {
-  CK(cudaMemcpyAsync(d_dst, ctx->rhs, (size_t)NU * ctx->g.n * 8, cudaMemcpyDeviceToDevice,
-                     ctx->stream));
+  k_from_pos<double><<<grid1d(ctx->g.n, 256), 256, 0, ctx->stream>>>(ctx->g, NU, ctx->rhs, d_dst);
+  LAUNCH_CHECK();
   CK(cudaStreamSynchronize(ctx->stream));
   return ISC_OK;
 }
@@ -731,8 +771,9 @@ extern "C" int isc_precond_setup(isc_ctx* ctx, int64_t* bad_cell) {
   KScope ks(ctx, KT_ILU_FACTOR);
   if (ctx->precond == ISC_PRECOND_MCILU) {
     KScope ks(ctx, KT_ILU_FACTOR);
-    k_mc_factor<<<grid1d(ctx->g.n, 32), dim3(32, NU), 0, st>>>(ctx->g, ctx->offd, ctx->mc_uinv,
-                                                              ctx->fail_d);
+    const int64_t nblack = ctx->g.colored ? ctx->g.n - ctx->g.half : ctx->g.n;
+    k_mc_factor<<<grid1d(nblack, 32), dim3(32, NU), 0, st>>>(ctx->g, ctx->offd, ctx->mc_uinv,
+                                                            ctx->fail_d);
     CK(cudaGetLastError());
   } else {
   CK(cudaFuncSetAttribute(k_ilu_factor, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -765,9 +806,10 @@ static int precond_apply(isc_ctx* ctx, const double* r, double* z) {
   Dims g = ctx->g;
   if (ctx->precond == ISC_PRECOND_MCILU) {
     KScope ks(ctx, KT_ILU_APPLY);
-    const int blocks = grid1d(g.n, 32);
-    k_mc_apply<1><<<blocks, dim3(32, NU), 0, ctx->stream>>>(g, ctx->offd, ctx->mc_uinv, r, z);
-    k_mc_apply<2><<<blocks, dim3(32, NU), 0, ctx->stream>>>(g, ctx->offd, ctx->mc_uinv, r, z);
+    const int b1 = grid1d(g.colored ? g.n - g.half : g.n, 32);
+    const int b2 = grid1d(g.colored ? g.half : g.n, 32);
+    k_mc_apply<1><<<b1, dim3(32, NU), 0, ctx->stream>>>(g, ctx->offd, ctx->mc_uinv, r, z);
+    k_mc_apply<2><<<b2, dim3(32, NU), 0, ctx->stream>>>(g, ctx->offd, ctx->mc_uinv, r, z);
     ctx->launches += 2;
     CK(cudaGetLastError());
     return ISC_OK;
@@ -796,15 +838,23 @@ static int spmv(isc_ctx* ctx, const double* x, double* y, const double* w0, cons
 }
 
 extern "C" int isc_spmv(isc_ctx* ctx, const double* d_x, double* d_y) {
-  int s = spmv<0>(ctx, d_x, d_y, nullptr, nullptr, nullptr);
+  const int64_t n = ctx->g.n;
+  k_to_pos<double><<<grid1d(n, 256), 256, 0, ctx->stream>>>(ctx->g, NU, d_x, ctx->sk);
+  int s = spmv<0>(ctx, ctx->sk, ctx->tk, nullptr, nullptr, nullptr);
   if (s) return s;
+  k_from_pos<double><<<grid1d(n, 256), 256, 0, ctx->stream>>>(ctx->g, NU, ctx->tk, d_y);
+  LAUNCH_CHECK();
   CK(cudaStreamSynchronize(ctx->stream));
   return ISC_OK;
 }
 
 extern "C" int isc_precond_apply(isc_ctx* ctx, const double* d_r, double* d_z) {
-  int s = precond_apply(ctx, d_r, d_z);
+  const int64_t n = ctx->g.n;
+  k_to_pos<double><<<grid1d(n, 256), 256, 0, ctx->stream>>>(ctx->g, NU, d_r, ctx->sk);
+  int s = precond_apply(ctx, ctx->sk, ctx->tk);
   if (s) return s;
+  k_from_pos<double><<<grid1d(n, 256), 256, 0, ctx->stream>>>(ctx->g, NU, ctx->tk, d_z);
+  LAUNCH_CHECK();
   CK(cudaStreamSynchronize(ctx->stream));
   return ISC_OK;
 }
@@ -1004,12 +1054,13 @@ extern "C" int isc_solve(isc_ctx* ctx, double tol, int32_t maxiter, double* d_du
   if (iters) *iters = it;
   if (status) return status;
   const int64_t n = ctx->g.n;
-  CK(cudaMemcpyAsync(d_du, ctx->xk, (size_t)NU * n * 8, cudaMemcpyDeviceToDevice, ctx->stream));
+  k_from_pos<double><<<grid1d(n, 256), 256, 0, ctx->stream>>>(ctx->g, NU, ctx->xk, d_du);
+  LAUNCH_CHECK();
   // bhp back-substitution dbhp = -(r_w + wrow . du_c) / dwdb (linsolve.py:473-478)
   if (ctx->nw > 0 && h_dbhp) {
     std::vector<double> duc(NU);
     for (int w = 0; w < ctx->nw; ++w) {
-      const int64_t c = ctx->wcell_h[w];
+      const int64_t c = ctx->wpos_h[w];
       for (int u = 0; u < NU; ++u)
         CK(cudaMemcpyAsync(&duc[u], ctx->xk + (int64_t)u * n + c, 8, cudaMemcpyDeviceToHost,
                            ctx->stream));
@@ -1035,8 +1086,9 @@ extern "C" int isc_newton_update(isc_ctx* ctx, double* d_state, const double* d_
 }
 
 extern "C" int isc_scaled_norm(isc_ctx* ctx, const double* d_accn, double dt, double* norm) {
-  k_norm_partial<<<RED_BLOCKS, 256, 0, ctx->stream>>>(ctx->g.n, ctx->resid, d_accn, ctx->vol, dt,
-                                                     ctx->partial);
+  k_to_pos<double><<<grid1d(ctx->g.n, 256), 256, 0, ctx->stream>>>(ctx->g, NU, d_accn, ctx->accn_c);
+  k_norm_partial<<<RED_BLOCKS, 256, 0, ctx->stream>>>(ctx->g.n, ctx->resid, ctx->accn_c, ctx->vol,
+                                                     dt, ctx->partial);
   LAUNCH_CHECK();
   std::vector<double> part(RED_BLOCKS);
   CK(cudaMemcpyAsync(part.data(), ctx->partial, RED_BLOCKS * 8, cudaMemcpyDeviceToHost,
@@ -1054,7 +1106,8 @@ extern "C" int isc_scaled_norm(isc_ctx* ctx, const double* d_accn, double dt, do
 
 extern "C" int isc_audit_sums(isc_ctx* ctx, const double* d_accn, double* h_out) {
   constexpr int NR = NF + 1;
-  k_audit_partial<<<RED_BLOCKS, 256, 0, ctx->stream>>>(ctx->g.n, ctx->acc, d_accn, ctx->src,
+  k_to_pos<double><<<grid1d(ctx->g.n, 256), 256, 0, ctx->stream>>>(ctx->g, NU, d_accn, ctx->accn_c);
+  k_audit_partial<<<RED_BLOCKS, 256, 0, ctx->stream>>>(ctx->g.n, ctx->acc, ctx->accn_c, ctx->src,
                                                       ctx->vol, ctx->partial);
   LAUNCH_CHECK();
   std::vector<double> part((size_t)3 * NR * RED_BLOCKS);

@@ -55,17 +55,68 @@ enum {
 };
 
 // Structured grid geometry (x fastest: c = i + nx*(j + ny*k)).
+//
+// Storage order of every per-cell array in HBM ("position" p): when nx is
+// even the cells are colour-blocked, red (i+j+k even) first, then black,
+// each colour in natural order: p = colour*half + (c >> 1). Each colour's
+// rows are then contiguous, so the multicolour ILU passes and any
+// single-colour sweep stream full 32 B sectors. Neighbours of a cell all
+// have the other colour, so their positions follow from (c ± stride) >> 1.
+// With odd nx the natural order is used (colored = 0).
 struct Dims {
   int nx, ny, nz;
   int64_t n;       // nx*ny*nz
   int64_t nxny;
+  int colored;     // 1: colour-blocked storage
+  int64_t half;    // n/2 (red cells) when colored
 };
+
+__host__ __device__ __forceinline__ void cell_ijk(const Dims& g, int64_t c, int& i, int& j,
+                                                  int& k) {
+  if (g.n < (int64_t)0x7fffffff) {
+    const uint32_t cc = (uint32_t)c, nx = (uint32_t)g.nx, nxny = (uint32_t)g.nxny;
+    const uint32_t kk = cc / nxny, rem = cc - kk * nxny;
+    k = (int)kk;
+    j = (int)(rem / nx);
+    i = (int)(rem - (uint32_t)j * nx);
+  } else {
+    k = (int)(c / g.nxny);
+    const int64_t rem = c - (int64_t)k * g.nxny;
+    j = (int)(rem / g.nx);
+    i = (int)(rem - (int64_t)j * g.nx);
+  }
+}
+
+__host__ __device__ __forceinline__ int64_t pos_of(const Dims& g, int64_t c) {
+  if (!g.colored) return c;
+  int i, j, k;
+  cell_ijk(g, c, i, j, k);
+  return (int64_t)((i + j + k) & 1) * g.half + (c >> 1);
+}
+
+__host__ __device__ __forceinline__ int64_t cell_of(const Dims& g, int64_t p) {
+  if (!g.colored) return p;
+  const int col = p >= g.half ? 1 : 0;
+  const int64_t c0 = 2 * (p - (int64_t)col * g.half);
+  int i, j, k;
+  cell_ijk(g, c0, i, j, k);
+  return (((i + j + k) & 1) == col) ? c0 : c0 + 1;
+}
 
 // Direction d of a neighbour, in the reference's gather order
 // (ascending connection index seen from a cell, _kernels.py:828-854).
 enum { DZM = 0, DYM = 1, DXM = 2, DXP = 3, DYP = 4, DZP = 5 };
 
 __host__ __device__ inline int opposite(int d) { return 5 - d; }
+__device__ __forceinline__ int64_t neighbour(const Dims& g, int64_t c, int i, int j, int k, int d);
+
+// storage position of the neighbour of cell c (at position p) in direction
+// d, or -1 at the boundary
+__device__ __forceinline__ int64_t nb_pos(const Dims& g, int64_t c, int i, int j, int k, int d) {
+  const int64_t nb = neighbour(g, c, i, j, k, d);
+  if (nb < 0 || !g.colored) return nb;
+  return (int64_t)(((i + j + k) & 1) ^ 1) * g.half + (nb >> 1);
+}
 
 // neighbour of cell c in direction d, or -1 at the boundary
 __device__ __forceinline__ int64_t neighbour(const Dims& g, int64_t c, int i, int j, int k, int d) {

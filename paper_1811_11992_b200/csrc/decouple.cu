@@ -133,8 +133,9 @@ __global__ void __launch_bounds__(DC_CELLS * 32) k_decouple(Dims g, double* diag
   }
   if (!live) return;
   if (jy == 0 && failc[lane] < NU) {   // first failing pivot column (linsolve.py:98-99)
-    flags[c] = failc[lane] + 1;
-    atomicMin(bad, (unsigned long long)c);
+    const int64_t cell = cell_of(g, c);
+    flags[cell] = failc[lane] + 1;
+    atomicMin(bad, (unsigned long long)cell);
   }
   if (j0 >= NU) {
 #pragma unroll

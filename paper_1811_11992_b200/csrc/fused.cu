@@ -216,12 +216,13 @@ __global__ void __launch_bounds__(FD_CELLS * 64) k_face_dc(const FusedArgs P) {
   const int64_t c = (int64_t)blockIdx.x * FD_CELLS + cl;
   const bool live = c < n;
   int i = 0, jj = 0, k = 0;
-  if (live) { i = (int)(c % F.g.nx); jj = (int)((c / F.g.nx) % F.g.ny); k = (int)(c / F.g.nxny); }
+  const int64_t cell = live ? cell_of(F.g, c) : 0;
+  if (live) cell_ijk(F.g, cell, i, jj, k);
   double a[NU];   // this thread's column of the augmented block row
   // ---- phase 1: faces -> off-diagonal columns (+ own-derivative columns to smem)
   if (j >= NU && j < NU + NDIR * NU) {
     const int d = (j - NU) / NU, u = (j - NU) % NU;
-    const int64_t nb = live ? neighbour(F.g, c, i, jj, k, d) : -1;
+    const int64_t nb = live ? nb_pos(F.g, cell, i, jj, k, d) : -1;
     double own[NU], fl[NU];
     if (nb >= 0) {
       const bool c_is_a = d >= DXP;
@@ -329,8 +330,8 @@ __global__ void __launch_bounds__(FD_CELLS * 64) k_face_dc(const FusedArgs P) {
   }
   if (!live) return;
   if (j == 0 && S.failc[cl] < NU) {
-    P.flags[c] = S.failc[cl] + 1;
-    atomicMin(P.bad, (unsigned long long)c);
+    P.flags[cell] = S.failc[cl] + 1;
+    atomicMin(P.bad, (unsigned long long)cell);
   }
   if (j >= NU && j < NU + NDIR * NU) {
     const int d = (j - NU) / NU, u = (j - NU) % NU;

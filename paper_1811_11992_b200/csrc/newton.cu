@@ -132,8 +132,9 @@ __device__ __forceinline__ double snormal(uint64_t seed, uint64_t stream, uint64
 
 __global__ void k_synth(Dims g, uint64_t seed, double* diag, double* offd, double* resid) {
   const int64_t n = g.n;
-  const int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;   // natural cell (RNG key)
   if (c >= n) return;
+  const int64_t pc = pos_of(g, c);
   double dmag[NU];
 #pragma unroll
   for (int r = 0; r < NU; ++r) {
@@ -146,10 +147,11 @@ __global__ void k_synth(Dims g, uint64_t seed, double* diag, double* offd, doubl
     v[r] = rs + 1.0;
     dmag[r] = fabs(v[r]);
 #pragma unroll
-    for (int u = 0; u < NU; ++u) diag[(int64_t)(r * NU + u) * n + c] = v[u];
-    resid[(int64_t)r * n + c] = snormal(seed, 2, (uint64_t)(c * NU + r));
+    for (int u = 0; u < NU; ++u) diag[(int64_t)(r * NU + u) * n + pc] = v[u];
+    resid[(int64_t)r * n + pc] = snormal(seed, 2, (uint64_t)(c * NU + r));
   }
-  const int i = (int)(c % g.nx), j = (int)((c / g.nx) % g.ny), k = (int)(c / g.nxny);
+  int i, j, k;
+  cell_ijk(g, c, i, j, k);
   for (int d = 0; d < NDIR; ++d) {
     const bool has = neighbour(g, c, i, j, k, d) >= 0;
 #pragma unroll
@@ -158,7 +160,7 @@ __global__ void k_synth(Dims g, uint64_t seed, double* diag, double* offd, doubl
       for (int u = 0; u < NU; ++u) {
         const double v = has ? 0.1 * snormal(seed, 1, (uint64_t)((c * NDIR + d) * NB + r * NU + u)) * dmag[r]
                              : 0.0;
-        offd[(int64_t)((d * NU + r) * NU + u) * n + c] = v;
+        offd[(int64_t)((d * NU + r) * NU + u) * n + pc] = v;
       }
   }
 }

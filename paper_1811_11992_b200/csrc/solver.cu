@@ -108,11 +108,13 @@ __global__ void __launch_bounds__(32 * NU) k_spmv(Dims g, const double* __restri
 #pragma unroll
   for (int k = 0; k < KK; ++k) acc[k] = 0.0;
   if (c < n) {
-    const int i = (int)(c % g.nx), j = (int)((c / g.nx) % g.ny), k = (int)(c / g.nxny);
+    const int64_t cell = cell_of(g, c);
+    int i, j, k;
+    cell_ijk(g, cell, i, j, k);
     double s = x[r * n + c];
 #pragma unroll
     for (int d = 0; d < NDIR; ++d) {
-      const int64_t nb = neighbour(g, c, i, j, k, d);
+      const int64_t nb = nb_pos(g, cell, i, j, k, d);
       if (nb < 0) continue;
       const double* blk = offd + (int64_t)((d * NU + r) * NU) * n + c;
       double t = 0.0;
@@ -485,17 +487,18 @@ __global__ void __launch_bounds__(32 * NU, 2) k_mc_factor(Dims g, const double* 
   __shared__ int pivs[32];
   const int64_t n = g.n;
   const int ls = threadIdx.x, u = threadIdx.y;
-  const int64_t c = (int64_t)blockIdx.x * 32 + ls;
+  const int64_t c = (int64_t)blockIdx.x * 32 + ls + (g.colored ? g.half : 0);
   const bool in = c < n;
   int i = 0, j = 0, k = 0;
-  if (in) { i = (int)(c % g.nx); j = (int)((c / g.nx) % g.ny); k = (int)(c / g.nxny); }
+  const int64_t cell = in ? cell_of(g, c) : 0;
+  if (in) cell_ijk(g, cell, i, j, k);
   const bool live = in && is_black(i, j, k);
   double ucol[NU];
 #pragma unroll
   for (int r = 0; r < NU; ++r) ucol[r] = (r == u) ? 1.0 : 0.0;
 #pragma unroll 1
   for (int d = 0; d < NDIR; ++d) {
-    const int64_t nb = live ? neighbour(g, c, i, j, k, d) : -1;
+    const int64_t nb = live ? nb_pos(g, cell, i, j, k, d) : -1;
     if (nb >= 0) {
       const double* B = offd + (int64_t)(d * NB + u) * n + c;
 #pragma unroll
@@ -591,10 +594,12 @@ __global__ void __launch_bounds__(32 * NU) k_mc_apply(Dims g, const double* __re
   __shared__ double wsh[NU][32];
   const int64_t n = g.n;
   const int ls = threadIdx.x, r = threadIdx.y;
-  const int64_t c = (int64_t)blockIdx.x * 32 + ls;
-  const bool in = c < n;
+  // colour-blocked storage: pass 1 covers the black half, pass 2 the red half
+  const int64_t c = (int64_t)blockIdx.x * 32 + ls + ((g.colored && PASS == 1) ? g.half : 0);
+  const bool in = g.colored ? (PASS == 1 ? c < n : c < g.half) : c < n;
   int i = 0, j = 0, k = 0;
-  if (in) { i = (int)(c % g.nx); j = (int)((c / g.nx) % g.ny); k = (int)(c / g.nxny); }
+  const int64_t cell = in ? cell_of(g, c) : 0;
+  if (in) cell_ijk(g, cell, i, j, k);
   const bool live = in && (is_black(i, j, k) == (PASS == 1));
   double w = 0.0;
   if (live) {
@@ -603,7 +608,7 @@ __global__ void __launch_bounds__(32 * NU) k_mc_apply(Dims g, const double* __re
     w = rin[r * n + c];
 #pragma unroll
     for (int d = 0; d < NDIR; ++d) {
-      const int64_t nb = neighbour(g, c, i, j, k, d);
+      const int64_t nb = nb_pos(g, cell, i, j, k, d);
       if (nb < 0) continue;
       const double* blk = offd + (int64_t)((d * NU + r) * NU) * n + c;
       double t = 0.0;

@@ -202,14 +202,15 @@ def _dense_decoupled(ws, grid):
     return A
 
 
-def test_multicolour_ilu_matches_dense_factorisation():
+@pytest.mark.parametrize("nx", [4, 5])   # colour-blocked (even nx) and natural storage
+def test_multicolour_ilu_matches_dense_factorisation(nx):
     """mcilu (north_star's multicolour block-ILU(0)): M^-1 r from the device
     equals the red-black ILU(0) computed densely with numpy."""
     from paper_1811_11992_b200 import _native as N
     from paper_1811_11992_b200.grid import build_grid
     from paper_1811_11992_b200.synth import synth_system
     from paper_1811_11992_b200.model import load_pack
-    grid = build_grid(4, 3, 3, 1.0, 1.0, 1.0, 1.0, 1.0, 1.0, 0.3)
+    grid = build_grid(nx, 3, 3, 1.0, 1.0, 1.0, 1.0, 1.0, 1.0, 0.3)
     pack = load_pack("tube3_pack", grid.phi_ref)
     diag, offd, resid = synth_system(grid, 9, seed=5)
     ws = Workspace(grid, pack, None, wells=(), streams=(), precond="mcilu")
