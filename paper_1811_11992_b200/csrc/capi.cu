@@ -859,6 +859,30 @@ extern "C" int isc_precond_apply(isc_ctx* ctx, const double* d_r, double* d_z) {
   return ISC_OK;
 }
 
+// phat = M^-1 p and v = A phat (+ K partial dots of v) for the colour-blocked
+// multicolour preconditioner; returns the number of partial slots.
+template <int K>
+static int mc_apply_spmv(isc_ctx* ctx, const double* p, double* phat, double* v,
+                         const double* w0, const double* w1, int* nparts) {
+  const Dims& g = ctx->g;
+  const int b1 = grid1d(g.n - g.half, 32), b2 = grid1d(g.half, 32);
+  {
+    KScope ks(ctx, KT_ILU_APPLY);
+    k_mc_apply<1><<<b1, dim3(32, NU), 0, ctx->stream>>>(g, ctx->offd, ctx->mc_uinv, p, phat);
+    k_mc_red<K><<<b2, dim3(32, NU), 0, ctx->stream>>>(g, ctx->offd, p, phat, v, w0, w1,
+                                                     ctx->partial, b2 + b1);
+  }
+  {
+    KScope ks(ctx, KT_SPMV);
+    k_mc_black_spmv<K><<<b1, dim3(32, NU), 0, ctx->stream>>>(g, ctx->offd, phat, v, w0, w1,
+                                                            ctx->partial, b2 + b1, b2);
+  }
+  ctx->launches += 3;
+  CK(cudaGetLastError());
+  *nparts = b1 + b2;
+  return ISC_OK;
+}
+
 // ------------------------------------------------------------- BiCGSTAB
 
 struct Kry {
@@ -917,6 +941,7 @@ static int bicgstab(isc_ctx* ctx, double tol, int maxiter, int* iters) {
   *iters = 0;
   if (nb == 0.0) return ISC_OK;
   const double brk = 1e-30 * nb * nb;
+  const bool mc_fused = ctx->precond == ISC_PRECOND_MCILU && ctx->g.colored;
   CK(cudaMemcpyAsync(r, b, len * 8, cudaMemcpyDeviceToDevice, st));
   CK(cudaMemcpyAsync(rhat, b, len * 8, cudaMemcpyDeviceToDevice, st));
   CK(cudaMemsetAsync(p, 0, len * 8, st));
@@ -963,9 +988,13 @@ static int bicgstab(isc_ctx* ctx, double tol, int maxiter, int* iters) {
     TRY(K.push());
     k_update_p<<<RED_BLOCKS, RED_THREADS, 0, st>>>(len, r, p, v, ctx->sc);
     ++ctx->launches;
-    TRY(precond_apply(ctx, p, phat));
     int nb1 = 0;
-    TRY(spmv<1>(ctx, phat, v, rhat, nullptr, &nb1));
+    if (mc_fused) {
+      TRY(mc_apply_spmv<1>(ctx, p, phat, v, rhat, nullptr, &nb1));
+    } else {
+      TRY(precond_apply(ctx, p, phat));
+      TRY(spmv<1>(ctx, phat, v, rhat, nullptr, &nb1));
+    }
     TRY(K.finalize1(nb1, S_DEN));
     // speculative s = r - alpha v, ||s||^2 (used only if den is not a breakdown)
     k_update_s<<<RED_BLOCKS, RED_THREADS, 0, st>>>(len, r, v, s, ctx->sc, ctx->partial);
@@ -991,9 +1020,13 @@ static int bicgstab(isc_ctx* ctx, double tol, int maxiter, int* iters) {
       return ISC_OK;
     }
     TRY(K.push());
-    TRY(precond_apply(ctx, s, shat));
     int nb2 = 0;
-    TRY(spmv<2>(ctx, shat, t, nullptr, s, &nb2));
+    if (mc_fused) {
+      TRY(mc_apply_spmv<2>(ctx, s, shat, t, nullptr, s, &nb2));
+    } else {
+      TRY(precond_apply(ctx, s, shat));
+      TRY(spmv<2>(ctx, shat, t, nullptr, s, &nb2));
+    }
     TRY(K.finalize2(nb2, S_TT, S_TS));
     k_update_xr<<<RED_BLOCKS, RED_THREADS, 0, st>>>(len, x, phat, shat, r, s, t, rhat, ctx->sc,
                                                      ctx->partial);

@@ -631,4 +631,112 @@ __global__ void __launch_bounds__(32 * NU) k_mc_apply(Dims g, const double* __re
   }
 }
 
+// ------------------------- multicolour preconditioner fused with the SpMV
+// BiCGSTAB needs phat = M^-1 p and v = A phat. With M = LU in red-black
+// order, the red rows of A M^-1 p equal p_r exactly (red rows of A are
+// I_r + B_rb and z_r = p_r - B_rb z_b), so only the black rows of the
+// product are formed:  v_r = p_r,  v_b = z_b + B_br z_r.
+// Three passes read each colour's blocks 1.5x instead of 2x+1x.
+
+template <int K>
+__device__ __forceinline__ void block_reduce_store_at(double (&v)[K], double* partial,
+                                                      int stride, int slot) {
+  __shared__ double sh[K][32];
+  const int tid = threadIdx.x + threadIdx.y * blockDim.x;
+  const int lane = tid & 31, wid = tid >> 5;
+#pragma unroll
+  for (int k = 0; k < K; ++k) {
+    double x = v[k];
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) x += __shfl_down_sync(0xffffffffu, x, o);
+    if (lane == 0) sh[k][wid] = x;
+  }
+  __syncthreads();
+  const int nwarps = (blockDim.x * blockDim.y) >> 5;
+  if (tid == 0) {
+#pragma unroll
+    for (int k = 0; k < K; ++k) {
+      double s = 0.0;
+      for (int w = 0; w < nwarps; ++w) s += sh[k][w];
+      partial[(int64_t)k * stride + slot] = s;
+    }
+  }
+}
+
+// pass 2 (red rows): z_r = p_r - sum B_rd z_b, v_r = p_r, partial dots of v_r
+// K == 1: v.w0 ; K == 2: (v.v, v.w1)
+template <int K>
+__global__ void __launch_bounds__(32 * NU) k_mc_red(Dims g, const double* __restrict__ offd,
+                                                    const double* __restrict__ pin,
+                                                    double* __restrict__ z, double* __restrict__ v,
+                                                    const double* __restrict__ w0,
+                                                    const double* __restrict__ w1,
+                                                    double* partial, int stride) {
+  const int64_t n = g.n;
+  const int ls = threadIdx.x, r = threadIdx.y;
+  const int64_t c = (int64_t)blockIdx.x * 32 + ls;   // red half (colour-blocked storage)
+  double acc[K];
+#pragma unroll
+  for (int k = 0; k < K; ++k) acc[k] = 0.0;
+  if (c < g.half) {
+    const int64_t cell = cell_of(g, c);
+    int i, j, k;
+    cell_ijk(g, cell, i, j, k);
+    const double pr = pin[r * n + c];
+    double w = pr;
+#pragma unroll
+    for (int d = 0; d < NDIR; ++d) {
+      const int64_t nb = nb_pos(g, cell, i, j, k, d);
+      if (nb < 0) continue;
+      const double* blk = offd + (int64_t)((d * NU + r) * NU) * n + c;
+      double t = 0.0;
+#pragma unroll
+      for (int u = 0; u < NU; ++u) t += blk[(int64_t)u * n] * z[(int64_t)u * n + nb];
+      w -= t;
+    }
+    z[r * n + c] = w;
+    v[r * n + c] = pr;
+    if (K == 1) acc[0] = pr * w0[r * n + c];
+    if (K == 2) { acc[0] = pr * pr; acc[K - 1] = pr * w1[r * n + c]; }
+  }
+  block_reduce_store_at<K>(acc, partial, stride, blockIdx.x);
+}
+
+// black rows of the product: v_b = z_b + sum B_bd z_r, partial dots of v_b
+template <int K>
+__global__ void __launch_bounds__(32 * NU) k_mc_black_spmv(Dims g, const double* __restrict__ offd,
+                                                           const double* __restrict__ z,
+                                                           double* __restrict__ v,
+                                                           const double* __restrict__ w0,
+                                                           const double* __restrict__ w1,
+                                                           double* partial, int stride,
+                                                           int slot0) {
+  const int64_t n = g.n;
+  const int ls = threadIdx.x, r = threadIdx.y;
+  const int64_t c = (int64_t)blockIdx.x * 32 + ls + g.half;   // black half
+  double acc[K];
+#pragma unroll
+  for (int k = 0; k < K; ++k) acc[k] = 0.0;
+  if (c < n) {
+    const int64_t cell = cell_of(g, c);
+    int i, j, k;
+    cell_ijk(g, cell, i, j, k);
+    double s = z[r * n + c];
+#pragma unroll
+    for (int d = 0; d < NDIR; ++d) {
+      const int64_t nb = nb_pos(g, cell, i, j, k, d);
+      if (nb < 0) continue;
+      const double* blk = offd + (int64_t)((d * NU + r) * NU) * n + c;
+      double t = 0.0;
+#pragma unroll
+      for (int u = 0; u < NU; ++u) t += blk[(int64_t)u * n] * z[(int64_t)u * n + nb];
+      s += t;
+    }
+    v[r * n + c] = s;
+    if (K == 1) acc[0] = s * w0[r * n + c];
+    if (K == 2) { acc[0] = s * s; acc[K - 1] = s * w1[r * n + c]; }
+  }
+  block_reduce_store_at<K>(acc, partial, stride, slot0 + blockIdx.x);
+}
+
 }  // namespace isc
