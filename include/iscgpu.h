@@ -114,6 +114,17 @@ int isc_assemble(isc_ctx *ctx, const double *d_state, const double *h_bhp, const
                  double dt, double t_new, const uint8_t *h_capped, int32_t freeze,
                  double *h_wells_out, int64_t *bad_cell);
 
+/* isc_assemble with the reference's host layout (assembly.py:179-196 State
+ * arrays and accn (n, 9)); d_state == NULL in isc_assemble means "already
+ * staged by this call". Pinned host arrays give full PCIe bandwidth. */
+int isc_assemble_host(isc_ctx *ctx, const double *h_p, const double *h_x, const double *h_y,
+                      const double *h_t, const double *h_sw, const double *h_sg,
+                      const double *h_cc, const double *h_bhp, const double *h_accn, double dt,
+                      double t_new, const uint8_t *h_capped, int32_t freeze,
+                      double *h_wells_out, int64_t *bad_cell);
+/* du of the last isc_solve (called with d_du == NULL) as host (n, 9). */
+int isc_download_du(isc_ctx *ctx, double *h_du);
+
 /* Same inputs/outputs as isc_assemble, with the well Schur fold and the
  * Gauss-Jordan decoupling fused into the face kernel (the un-decoupled
  * blocks are not kept; isc_export_system is not available afterwards).

@@ -138,10 +138,15 @@ def assemble(grid, pack, ws, wells, streams, state, accn, dt, t_new, capped,
     if jacobian != "analytic":
         raise NotImplementedError("numeric (finite-difference) Jacobian is not on the GPU path")
     ctx = ws.bind(wells, streams)
-    d_state = state if isinstance(state, torch.Tensor) else state_to_device(state, ctx.device)
-    d_accn = accn if isinstance(accn, torch.Tensor) else soa_from_rows(accn, ctx.device)
-    bhp = np.asarray(state.bhp if hasattr(state, "bhp") else ws.bhp, dtype=np.float64)
     ws._invalidate()
-    wout = ctx.assemble(d_state, bhp, d_accn, dt, t_new, capped, freeze_upwind)
+    if isinstance(getattr(state, "p", None), np.ndarray) and not isinstance(accn, torch.Tensor):
+        # reference-layout host arrays: staged + transposed inside the library
+        wout = ctx.assemble_host(state, accn, dt, t_new, capped, freeze_upwind)
+    else:
+        u = getattr(state, "u", state)
+        d_state = u if isinstance(u, torch.Tensor) else state_to_device(state, ctx.device)
+        d_accn = accn if isinstance(accn, torch.Tensor) else soa_from_rows(accn, ctx.device)
+        bhp = np.asarray(state.bhp, dtype=np.float64)
+        wout = ctx.assemble(d_state, bhp, d_accn, dt, t_new, capped, freeze_upwind)
     ws.last_wout = wout
     return blocks_from_wout(wells, wout)

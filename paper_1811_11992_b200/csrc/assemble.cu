@@ -1039,6 +1039,41 @@ __global__ void k_import_system(Dims g, const int64_t* __restrict__ conn_id,
   }
 }
 
+// host-layout state (the reference's State arrays + accn (n, NU)) staged in
+// one device buffer -> SoA state / accn in storage order
+__global__ void k_stage_state(Dims g, const double* __restrict__ stage, double* __restrict__ st,
+                              double* __restrict__ accn) {
+  const int64_t n = g.n;
+  const int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;   // natural cell
+  if (c >= n) return;
+  const int64_t p = pos_of(g, c);
+  const double* sp = stage;
+  const double* sx = stage + n;
+  const double* sy = sx + NCO * n;
+  const double* rest = sy + NCG * n;          // t, sw, sg, cc
+  const double* sa = rest + 4 * n;            // accn (n, NU)
+  st[p] = sp[c];
+#pragma unroll
+  for (int i = 0; i < NCO; ++i) st[(int64_t)(1 + i) * n + p] = sx[c * NCO + i];
+#pragma unroll
+  for (int j = 0; j < NCG; ++j) st[(int64_t)(1 + NCO + j) * n + p] = sy[c * NCG + j];
+#pragma unroll
+  for (int q = 0; q < 4; ++q) st[(int64_t)(CT + q) * n + p] = rest[q * n + c];
+  if (accn)
+#pragma unroll
+    for (int r = 0; r < NU; ++r) accn[(int64_t)r * n + p] = sa[c * NU + r];
+}
+
+// SoA (storage order) -> AoS (n, NU) natural order, for a host download
+__global__ void k_unstage_rows(Dims g, const double* __restrict__ v, double* __restrict__ out) {
+  const int64_t n = g.n;
+  const int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (c >= n) return;
+  const int64_t p = pos_of(g, c);
+#pragma unroll
+  for (int r = 0; r < NU; ++r) out[c * NU + r] = v[(int64_t)r * n + p];
+}
+
 // natural-order SoA (rows x n) <-> storage positions
 template <typename T>
 __global__ void k_to_pos(Dims g, int rows, const T* __restrict__ src, T* __restrict__ dst) {

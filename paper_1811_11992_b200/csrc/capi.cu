@@ -57,6 +57,7 @@ struct isc_ctx {
   std::vector<int64_t> wcell_h;   // natural cell of each well
   std::vector<int64_t> wpos_h;    // its storage position
   double *st_c = nullptr, *accn_c = nullptr;   // state / accn in storage order
+  double* stage = nullptr;                      // host-layout staging (18 n doubles)
   double* wout_d = nullptr;
   double* wout_h = nullptr;   // pinned
   double* bhp_d = nullptr;
@@ -352,6 +353,7 @@ extern "C" int isc_create(const isc_model_desc* md, const isc_grid_desc* gdsc, i
     }
   }
   ALLOC(ctx->st_c, (size_t)NU * n * 8);
+  ALLOC(ctx->stage, (size_t)2 * NU * n * 8);
   ALLOC(ctx->accn_c, (size_t)NU * n * 8);
   ctx->hl_kob = gdsc->hl_kob; ctx->hl_d = gdsc->hl_d; ctx->hl_rho = gdsc->hl_rho;
   ctx->hl_tini = gdsc->hl_tini;
@@ -422,7 +424,7 @@ extern "C" int isc_destroy(isc_ctx* ctx) {
                   ctx->capped_d, ctx->rec, ctx->acc, ctx->src, ctx->resid, ctx->diag,
                   ctx->offd, ctx->upw, ctx->bad_d, ctx->rhs, ctx->xk, ctx->rk, ctx->rhat,
                   ctx->pk, ctx->vk, ctx->phat, ctx->shat, ctx->sk, ctx->tk, ctx->sc,
-                  ctx->partial, ctx->flags, ctx->fail_d, ctx->schur, ctx->st_c, ctx->accn_c};
+                  ctx->partial, ctx->flags, ctx->fail_d, ctx->schur, ctx->st_c, ctx->accn_c, ctx->stage};
   free_ilu(ctx);
   for (void* p : ptrs)
     if (p) cudaFree(p);
@@ -497,9 +499,11 @@ extern "C" int isc_assemble(isc_ctx* ctx, const double* d_state, const double* h
     CK(cudaMemcpyAsync(ctx->capped_d, h_capped, ctx->nw, cudaMemcpyHostToDevice, st));
   }
   CK(cudaMemsetAsync(ctx->bad_d, 0xff, 8, st));
-  k_to_pos<double><<<grid1d(n, 256), 256, 0, st>>>(ctx->g, NU, d_state, ctx->st_c);
-  k_to_pos<double><<<grid1d(n, 256), 256, 0, st>>>(ctx->g, NU, d_accn, ctx->accn_c);
-  ctx->launches += 2;
+  if (d_state) {   // NULL: state/accn already staged by isc_assemble_host
+    k_to_pos<double><<<grid1d(n, 256), 256, 0, st>>>(ctx->g, NU, d_state, ctx->st_c);
+    k_to_pos<double><<<grid1d(n, 256), 256, 0, st>>>(ctx->g, NU, d_accn, ctx->accn_c);
+    ctx->launches += 2;
+  }
   d_state = ctx->st_c;
   d_accn = ctx->accn_c;
   CellArgs A{ctx->g, d_state, ctx->phi_ref, ctx->vol, ctx->hl_area, ctx->hl_kob, ctx->hl_d,
@@ -550,9 +554,11 @@ extern "C" int isc_assemble_decoupled(isc_ctx* ctx, const double* d_state, const
     CK(cudaMemcpyAsync(ctx->capped_d, h_capped, ctx->nw, cudaMemcpyHostToDevice, st));
   }
   CK(cudaMemsetAsync(ctx->bad_d, 0xff, 8, st));
-  k_to_pos<double><<<grid1d(n, 256), 256, 0, st>>>(ctx->g, NU, d_state, ctx->st_c);
-  k_to_pos<double><<<grid1d(n, 256), 256, 0, st>>>(ctx->g, NU, d_accn, ctx->accn_c);
-  ctx->launches += 2;
+  if (d_state) {   // NULL: state/accn already staged by isc_assemble_host
+    k_to_pos<double><<<grid1d(n, 256), 256, 0, st>>>(ctx->g, NU, d_state, ctx->st_c);
+    k_to_pos<double><<<grid1d(n, 256), 256, 0, st>>>(ctx->g, NU, d_accn, ctx->accn_c);
+    ctx->launches += 2;
+  }
   d_state = ctx->st_c;
   d_accn = ctx->accn_c;
   CellArgs A{ctx->g, d_state, ctx->phi_ref, ctx->vol, ctx->hl_area, ctx->hl_kob, ctx->hl_d,
@@ -606,6 +612,42 @@ extern "C" int isc_assemble_decoupled(isc_ctx* ctx, const double* d_state, const
   }
   ctx->decoupled = true;
   ctx->factored = false;
+  return ISC_OK;
+}
+
+// Reference-layout host inputs (State arrays p, x (n,nco), y (n,ncg), t, sw,
+// sg, cc and accn (n, NU)): one H2D copy each into a staging buffer, the
+// SoA/storage-order transpose on the device, then isc_assemble.
+extern "C" int isc_assemble_host(isc_ctx* ctx, const double* h_p, const double* h_x,
+                                 const double* h_y, const double* h_t, const double* h_sw,
+                                 const double* h_sg, const double* h_cc, const double* h_bhp,
+                                 const double* h_accn, double dt, double t_new,
+                                 const uint8_t* h_capped, int32_t freeze, double* h_wells_out,
+                                 int64_t* bad_cell) {
+  const int64_t n = ctx->g.n;
+  cudaStream_t st = ctx->stream;
+  double* sg = ctx->stage;
+  const size_t b = (size_t)n * 8;
+  CK(cudaMemcpyAsync(sg, h_p, b, cudaMemcpyHostToDevice, st));
+  CK(cudaMemcpyAsync(sg + n, h_x, b * NCO, cudaMemcpyHostToDevice, st));
+  CK(cudaMemcpyAsync(sg + (1 + NCO) * n, h_y, b * NCG, cudaMemcpyHostToDevice, st));
+  const double* rest[4] = {h_t, h_sw, h_sg, h_cc};
+  for (int q = 0; q < 4; ++q)
+    CK(cudaMemcpyAsync(sg + (1 + NCO + NCG + q) * n, rest[q], b, cudaMemcpyHostToDevice, st));
+  CK(cudaMemcpyAsync(sg + (size_t)(CT + 4) * n, h_accn, b * NU, cudaMemcpyHostToDevice, st));
+  k_stage_state<<<grid1d(n, 256), 256, 0, st>>>(ctx->g, sg, ctx->st_c, ctx->accn_c);
+  LAUNCH_CHECK();
+  return isc_assemble(ctx, nullptr, h_bhp, nullptr, dt, t_new, h_capped, freeze, h_wells_out,
+                      bad_cell);
+}
+
+// du of the last isc_solve as a host (n, NU) array in natural cell order
+extern "C" int isc_download_du(isc_ctx* ctx, double* h_du) {
+  const int64_t n = ctx->g.n;
+  k_unstage_rows<<<grid1d(n, 256), 256, 0, ctx->stream>>>(ctx->g, ctx->xk, ctx->stage);
+  LAUNCH_CHECK();
+  CK(cudaMemcpyAsync(h_du, ctx->stage, (size_t)n * NU * 8, cudaMemcpyDeviceToHost, ctx->stream));
+  CK(cudaStreamSynchronize(ctx->stream));
   return ISC_OK;
 }
 
@@ -1087,8 +1129,10 @@ extern "C" int isc_solve(isc_ctx* ctx, double tol, int32_t maxiter, double* d_du
   if (iters) *iters = it;
   if (status) return status;
   const int64_t n = ctx->g.n;
-  k_from_pos<double><<<grid1d(n, 256), 256, 0, ctx->stream>>>(ctx->g, NU, ctx->xk, d_du);
-  LAUNCH_CHECK();
+  if (d_du) {
+    k_from_pos<double><<<grid1d(n, 256), 256, 0, ctx->stream>>>(ctx->g, NU, ctx->xk, d_du);
+    LAUNCH_CHECK();
+  }
   // bhp back-substitution dbhp = -(r_w + wrow . du_c) / dwdb (linsolve.py:473-478)
   if (ctx->nw > 0 && h_dbhp) {
     std::vector<double> duc(NU);

@@ -51,8 +51,12 @@ class BlockSolver:
         return self._du, dbhp, iters
 
     def solve(self, blocks):
-        du, dbhp, iters = self.solve_device(blocks)
-        return du.t().contiguous().cpu().numpy(), dbhp, iters
+        """Drop-in: du as a host (n, 9) array like the reference."""
+        ctx = self._ctx()
+        if blocks is not None and ctx.nw:
+            ctx.set_wells_out(wout_from_blocks(blocks))
+        self.ws._invalidate()
+        return ctx.solve_host(self.tol, self.maxiter)
 
 
 def load_system(ws: Workspace, diag, offd, resid, blocks=()):
