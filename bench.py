@@ -149,14 +149,23 @@ def ilu_structure_counts(grid):
     return slots, links, links
 
 
-def algorithmic_bytes(grid, nw):
+def algorithmic_bytes(grid, nw, precond="ras"):
+    """Compulsory bytes per launch of each kernel class."""
     n, m = grid.ncell, grid.nconn
-    return {
+    out = {
         "cell+face": 8 * (111 * n + 164 * m),              # SURVEY §8(d) assembly
         "decouple": 8 * (99 * n + 324 * m),                # SURVEY §8(d)
         "spmv": 8 * (162 * m + 18 * n),                    # SURVEY §8(d)
         "ilu_apply": ilu_bytes(ilu_structure_counts(grid), n, m),
     }
+    if precond == "mcilu":
+        # pass 1 (black rows, U_b^-1) + red pass: every off-diagonal block once
+        # (81 m per colour), U_b^-1 (81 n/2), r read, z written, v_r written,
+        # one dot operand read
+        out["ilu_apply"] = 8 * (162 * m + 40.5 * n + 9 * n + 9 * n + 4.5 * n + 4.5 * n)
+        # black rows of A z only (red rows of A M^-1 p equal p)
+        out["spmv"] = 8 * (81 * m + 9 * n + 4.5 * n + 4.5 * n)
+    return out
 
 
 # ------------------------------------------------------------------ ours
@@ -288,7 +297,7 @@ def run_ours(args, rank, world, local):
            "e2e": e2e, "gpu_launches": int(launches), "clocks": clk}
     # ---- roofline of the dominant kernel class ----------------------------
     hbm, peak_src = peaks()
-    algo = algorithmic_bytes(grid, len(wells))
+    algo = algorithmic_bytes(grid, len(wells), case.solver.precond)
     ktimes = {KCLASS[i]: {"ms": float(ms8[i]), "launches": int(cnt8[i])} for i in range(8)}
     classes = {"ilu_apply": ("ilu_apply",), "spmv": ("spmv",), "decouple": ("decouple",),
                "cell+face": ("cell", "face")}
