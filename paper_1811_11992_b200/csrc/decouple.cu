@@ -145,4 +145,90 @@ __global__ void __launch_bounds__(DC_CELLS * 32) k_decouple(Dims g, double* diag
   for (int r = 0; r < NU; ++r) *col_ptr(j1, r, n, c, diag, offd, rhs) = a1[r];
 }
 
+// One column per thread: CTA = DC2_CELLS cells x 64 columns (512 threads),
+// ~40 registers, several CTAs per SM so loads, pivots and stores of
+// different CTAs overlap. Warp = 4 columns x 8 consecutive cells: every
+// load/store is a full 64 B run of one column.
+constexpr int DC2_CELLS = 8;
+
+__global__ void __launch_bounds__(DC2_CELLS * 64, 2) k_decouple2(Dims g, double* diag, double* offd,
+                                                             double* rhs, int* flags,
+                                                             unsigned long long* bad) {
+  __shared__ double colk[NU][DC2_CELLS];
+  __shared__ double cmax[NU][DC2_CELLS];
+  __shared__ int piv_s[DC2_CELLS];
+  __shared__ int failc[DC2_CELLS];
+  const int64_t n = g.n;
+  const int cl = threadIdx.x % DC2_CELLS, j = threadIdx.x / DC2_CELLS;
+  const int64_t c = (int64_t)blockIdx.x * DC2_CELLS + cl;
+  const bool live = c < n;
+  double a[NU];
+#pragma unroll
+  for (int r = 0; r < NU; ++r) a[r] = live ? *col_ptr(j, r, n, c, diag, offd, rhs) : (r == j ? 1.0 : 0.0);
+  if (j < NU) {
+    double m = 0.0;
+#pragma unroll
+    for (int r = 0; r < NU; ++r) m = fmax(m, fabs(a[r]));
+    cmax[j][cl] = m;
+  }
+  if (j == 0) failc[cl] = NU;
+  __syncthreads();
+  double amax = 0.0;
+#pragma unroll
+  for (int u = 0; u < NU; ++u) amax = fmax(amax, cmax[u][cl]);
+  const double tol = 1e-13 * amax;
+#pragma unroll
+  for (int k = 0; k < NU; ++k) {
+    if (j == k) {
+      int piv = k;
+      double pv = fabs(a[k]);
+#pragma unroll
+      for (int r = k + 1; r < NU; ++r) {
+        const double v = fabs(a[r]);
+        if (v > pv) { pv = v; piv = r; }
+      }
+      if (pv <= tol || amax == 0.0) atomicMin(&failc[cl], amax == 0.0 ? 0 : k);
+#pragma unroll
+      for (int r = 0; r < NU; ++r) {
+        double v = a[r];
+        if (r == k) {
+#pragma unroll
+          for (int q = k + 1; q < NU; ++q) if (q == piv) v = a[q];
+        } else if (r == piv) {
+          v = a[k];
+        }
+        colk[r][cl] = v;
+      }
+      piv_s[cl] = piv;
+    }
+    __syncthreads();
+    const int piv = piv_s[cl];
+    if (piv != k) {
+      const double t0 = a[k];
+#pragma unroll
+      for (int q = k + 1; q < NU; ++q)
+        if (q == piv) { a[k] = a[q]; a[q] = t0; }
+    }
+    const double dinv = 1.0 / colk[k][cl];
+    a[k] *= dinv;
+#pragma unroll
+    for (int r = 0; r < NU; ++r) {
+      if (r == k) continue;
+      const double f = colk[r][cl];
+      if (f != 0.0) a[r] -= f * a[k];
+    }
+    __syncthreads();
+  }
+  if (!live) return;
+  if (j == 0 && failc[cl] < NU) {
+    const int64_t cell = cell_of(g, c);
+    flags[cell] = failc[cl] + 1;
+    atomicMin(bad, (unsigned long long)cell);
+  }
+  if (j >= NU) {
+#pragma unroll
+    for (int r = 0; r < NU; ++r) *col_ptr(j, r, n, c, diag, offd, rhs) = a[r];
+  }
+}
+
 }  // namespace isc
