@@ -771,8 +771,8 @@ extern "C" int isc_decouple(isc_ctx* ctx, int64_t* bad_cell, int32_t* bad_col) {
   LAUNCH_CHECK();
   CK(cudaMemsetAsync(ctx->flags, 0, n * 4, st));
   CK(cudaMemsetAsync(ctx->bad_d, 0xff, 8, st));
-  k_decouple2<<<grid1d(n, DC2_CELLS), DC2_CELLS * 64, 0, st>>>(ctx->g, ctx->diag, ctx->offd,
-                                                                ctx->rhs, ctx->flags, ctx->bad_d);
+  k_decouple3<<<grid1d(n, DC3_CELLS), DC3_THREADS, 0, st>>>(ctx->g, ctx->diag, ctx->offd,
+                                                             ctx->rhs, ctx->flags, ctx->bad_d);
   LAUNCH_CHECK();
   }
   CK(cudaMemcpyAsync(ctx->bad_h, ctx->bad_d, 8, cudaMemcpyDeviceToHost, st));
