@@ -241,7 +241,7 @@ __global__ void __launch_bounds__(DC2_CELLS * 64, 2) k_decouple2(Dims g, double*
 constexpr int DC3_CELLS = 16;
 constexpr int DC3_THREADS = 256;
 
-__global__ void __launch_bounds__(DC3_THREADS) k_decouple3(Dims g, const double* __restrict__ diag,
+__global__ void __launch_bounds__(DC3_THREADS, 3) k_decouple3(Dims g, const double* __restrict__ diag,
                                                           double* offd, double* rhs, int* flags,
                                                           unsigned long long* bad) {
   __shared__ double inv[NU][NU][DC3_CELLS];   // D^-1 (row, col, cell)
@@ -334,6 +334,7 @@ __global__ void __launch_bounds__(DC3_THREADS) k_decouple3(Dims g, const double*
   __syncthreads();
   // ---- phase B: columns of the row blocks and the rhs, times D^-1
   constexpr int NCOLB = NDIR * NU + 1;   // 55
+#pragma unroll 2
   for (int task = t; task < NCOLB * DC3_CELLS; task += DC3_THREADS) {
     const int tc = task % DC3_CELLS, col = task / DC3_CELLS;
     const int64_t cc = c0 + tc;
