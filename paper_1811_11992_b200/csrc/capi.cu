@@ -907,17 +907,17 @@ template <int K>
 static int mc_apply_spmv(isc_ctx* ctx, const double* p, double* phat, double* v,
                          const double* w0, const double* w1, int* nparts) {
   const Dims& g = ctx->g;
-  const int b1 = grid1d(g.n - g.half, TC_THREADS), b2 = grid1d(g.half, TC_THREADS);
+  const int b1 = grid1d(g.n - g.half, 32), b2 = grid1d(g.half, 32);
   {
     KScope ks(ctx, KT_ILU_APPLY);
-    k_mc_black_tc<<<b1, TC_THREADS, 0, ctx->stream>>>(g, ctx->offd, ctx->mc_uinv, p, phat);
-    k_mc_red_tc<K><<<b2, TC_THREADS, 0, ctx->stream>>>(g, ctx->offd, p, phat, v, w0, w1,
-                                                      ctx->partial, b2 + b1);
+    k_mc_apply<1><<<b1, dim3(32, NU), 0, ctx->stream>>>(g, ctx->offd, ctx->mc_uinv, p, phat);
+    k_mc_red<K><<<b2, dim3(32, NU), 0, ctx->stream>>>(g, ctx->offd, p, phat, v, w0, w1,
+                                                     ctx->partial, b2 + b1);
   }
   {
     KScope ks(ctx, KT_SPMV);
-    k_mc_spmv_black_tc<K><<<b1, TC_THREADS, 0, ctx->stream>>>(g, ctx->offd, phat, v, w0, w1,
-                                                             ctx->partial, b2 + b1, b2);
+    k_mc_black_spmv<K><<<b1, dim3(32, NU), 0, ctx->stream>>>(g, ctx->offd, phat, v, w0, w1,
+                                                            ctx->partial, b2 + b1, b2);
   }
   ctx->launches += 3;
   CK(cudaGetLastError());

@@ -739,150 +739,4 @@ __global__ void __launch_bounds__(32 * NU) k_mc_black_spmv(Dims g, const double*
   block_reduce_store_at<K>(acc, partial, stride, slot0 + blockIdx.x);
 }
 
-// ---- thread-per-cell variants of the three multicolour passes: the index
-// math and neighbour x loads happen once per cell instead of once per row,
-// every thread streams its cell's 6 x 81 block entries (coalesced across
-// the warp's 32 consecutive cells of one colour).
-constexpr int TC_THREADS = 128;
-
-template <int K>
-__device__ __forceinline__ void reduce_tc(double (&v)[K], double* partial, int stride, int slot) {
-  block_reduce_store_at<K>(v, partial, stride, slot);
-}
-
-// pass 1 (black): z_b = U_b^-1 (r_b - sum_d B_bd r_nb)
-__global__ void __launch_bounds__(TC_THREADS) k_mc_black_tc(Dims g, const double* __restrict__ offd,
-                                                           const double* __restrict__ uinv,
-                                                           const double* __restrict__ rin,
-                                                           double* __restrict__ z) {
-  const int64_t n = g.n;
-  const int64_t c = (int64_t)blockIdx.x * TC_THREADS + threadIdx.x + g.half;
-  if (c >= n) return;
-  const int64_t cell = cell_of(g, c);
-  int i, j, k;
-  cell_ijk(g, cell, i, j, k);
-  double w[NU];
-#pragma unroll
-  for (int r = 0; r < NU; ++r) w[r] = rin[(int64_t)r * n + c];
-#pragma unroll
-  for (int d = 0; d < NDIR; ++d) {
-    const int64_t nb = nb_pos(g, cell, i, j, k, d);
-    if (nb < 0) continue;
-    double xn[NU];
-#pragma unroll
-    for (int u = 0; u < NU; ++u) xn[u] = rin[(int64_t)u * n + nb];
-    const double* blk = offd + (int64_t)(d * NB) * n + c;
-#pragma unroll
-    for (int r = 0; r < NU; ++r) {
-      double t = 0.0;
-#pragma unroll
-      for (int u = 0; u < NU; ++u) t += blk[(int64_t)(r * NU + u) * n] * xn[u];
-      w[r] -= t;
-    }
-  }
-#pragma unroll
-  for (int r = 0; r < NU; ++r) {
-    double zz = 0.0;
-#pragma unroll
-    for (int u = 0; u < NU; ++u) zz += uinv[(int64_t)(r * NU + u) * n + c] * w[u];
-    z[(int64_t)r * n + c] = zz;
-  }
-}
-
-// pass 2 (red) fused with the red rows of the product: z_r, v_r = p_r, dots
-template <int K>
-__global__ void __launch_bounds__(TC_THREADS) k_mc_red_tc(Dims g, const double* __restrict__ offd,
-                                                         const double* __restrict__ pin,
-                                                         double* __restrict__ z,
-                                                         double* __restrict__ v,
-                                                         const double* __restrict__ w0,
-                                                         const double* __restrict__ w1,
-                                                         double* partial, int stride) {
-  const int64_t n = g.n;
-  const int64_t c = (int64_t)blockIdx.x * TC_THREADS + threadIdx.x;
-  double acc[K];
-#pragma unroll
-  for (int q = 0; q < K; ++q) acc[q] = 0.0;
-  if (c < g.half) {
-    const int64_t cell = cell_of(g, c);
-    int i, j, k;
-    cell_ijk(g, cell, i, j, k);
-    double pr[NU], w[NU];
-#pragma unroll
-    for (int r = 0; r < NU; ++r) { pr[r] = pin[(int64_t)r * n + c]; w[r] = pr[r]; }
-#pragma unroll
-    for (int d = 0; d < NDIR; ++d) {
-      const int64_t nb = nb_pos(g, cell, i, j, k, d);
-      if (nb < 0) continue;
-      double xn[NU];
-#pragma unroll
-      for (int u = 0; u < NU; ++u) xn[u] = z[(int64_t)u * n + nb];
-      const double* blk = offd + (int64_t)(d * NB) * n + c;
-#pragma unroll
-      for (int r = 0; r < NU; ++r) {
-        double t = 0.0;
-#pragma unroll
-        for (int u = 0; u < NU; ++u) t += blk[(int64_t)(r * NU + u) * n] * xn[u];
-        w[r] -= t;
-      }
-    }
-#pragma unroll
-    for (int r = 0; r < NU; ++r) {
-      z[(int64_t)r * n + c] = w[r];
-      v[(int64_t)r * n + c] = pr[r];
-      if (K == 1) acc[0] += pr[r] * w0[(int64_t)r * n + c];
-      if (K == 2) { acc[0] += pr[r] * pr[r]; acc[K - 1] += pr[r] * w1[(int64_t)r * n + c]; }
-    }
-  }
-  reduce_tc<K>(acc, partial, stride, blockIdx.x);
-}
-
-// black rows of the product: v_b = z_b + sum_d B_bd z_nb, dots
-template <int K>
-__global__ void __launch_bounds__(TC_THREADS) k_mc_spmv_black_tc(Dims g,
-                                                                const double* __restrict__ offd,
-                                                                const double* __restrict__ z,
-                                                                double* __restrict__ v,
-                                                                const double* __restrict__ w0,
-                                                                const double* __restrict__ w1,
-                                                                double* partial, int stride,
-                                                                int slot0) {
-  const int64_t n = g.n;
-  const int64_t c = (int64_t)blockIdx.x * TC_THREADS + threadIdx.x + g.half;
-  double acc[K];
-#pragma unroll
-  for (int q = 0; q < K; ++q) acc[q] = 0.0;
-  if (c < n) {
-    const int64_t cell = cell_of(g, c);
-    int i, j, k;
-    cell_ijk(g, cell, i, j, k);
-    double s[NU];
-#pragma unroll
-    for (int r = 0; r < NU; ++r) s[r] = z[(int64_t)r * n + c];
-#pragma unroll
-    for (int d = 0; d < NDIR; ++d) {
-      const int64_t nb = nb_pos(g, cell, i, j, k, d);
-      if (nb < 0) continue;
-      double xn[NU];
-#pragma unroll
-      for (int u = 0; u < NU; ++u) xn[u] = z[(int64_t)u * n + nb];
-      const double* blk = offd + (int64_t)(d * NB) * n + c;
-#pragma unroll
-      for (int r = 0; r < NU; ++r) {
-        double t = 0.0;
-#pragma unroll
-        for (int u = 0; u < NU; ++u) t += blk[(int64_t)(r * NU + u) * n] * xn[u];
-        s[r] += t;
-      }
-    }
-#pragma unroll
-    for (int r = 0; r < NU; ++r) {
-      v[(int64_t)r * n + c] = s[r];
-      if (K == 1) acc[0] += s[r] * w0[(int64_t)r * n + c];
-      if (K == 2) { acc[0] += s[r] * s[r]; acc[K - 1] += s[r] * w1[(int64_t)r * n + c]; }
-    }
-  }
-  reduce_tc<K>(acc, partial, stride, slot0 + blockIdx.x);
-}
-
 }  // namespace isc
