@@ -22,7 +22,7 @@ constexpr int CSW = CT + 1, CSG = CT + 2, CCC = CT + 3;
 constexpr int ROW_E = CT, ROW_OS = CT + 1, ROW_GS = CT + 2, ROW_CK = CT + 3;
 constexpr int NB = NU * NU;         // 81 entries per block
 constexpr int NDIR = 6;             // -z, -y, -x, +x, +y, +z
-constexpr int MAXREAC = 8;
+constexpr int MAXREAC = 4;
 constexpr int MAXTAB = 32;
 
 constexpr double RANKINE = 459.67;
