@@ -769,7 +769,7 @@ __device__ __forceinline__ void face_row(const int row, const CellView& A_, cons
 }
 
 // grid: (ceil(n/32), 1); block: (32, NU) -> threadIdx.y = residual row
-__global__ void __launch_bounds__(32 * NU, 2) k_face(const FaceArgs F) {
+__global__ void __launch_bounds__(32 * NU, 3) k_face(const FaceArgs F) {
   const int64_t n = F.g.n;
   const int64_t c = (int64_t)blockIdx.x * 32 + threadIdx.x;   // storage position
   const int row = threadIdx.y;
