@@ -172,6 +172,25 @@ int isc_scaled_norm(isc_ctx *ctx, const double *d_accn, double dt, double *norm)
 /* out[3*(nfull+1)]: per audited row sum V(acc-accn), sum V src, sum V|acc| */
 int isc_audit_sums(isc_ctx *ctx, const double *d_accn, double *h_out);
 
+/* ---- multi-GPU z-slab decomposition ----------------------
+ * The context's grid holds the owned planes [kw_lo, kw_hi) plus one ghost
+ * plane towards each neighbouring rank (has_lo / has_hi). Halos of the state
+ * (before assembly) and of p-hat / s-hat / x (before each SpMV) and the
+ * Krylov dot products / norms / audit sums cross ranks; the preconditioner is
+ * rank-local (block-Jacobi across ranks of the multicolour ILU). NCCL: one
+ * process per GPU, unique_id = 128-byte ncclUniqueId (e.g. broadcast by
+ * torch.distributed). Hub: several contexts in one process, one host thread
+ * per rank (single-GPU validation of the multi-rank algorithm). */
+int isc_comm_nccl(isc_ctx *ctx, const void *unique_id, int32_t rank, int32_t nranks,
+                  int32_t has_lo, int32_t has_hi, int32_t kw_lo, int32_t kw_hi);
+int isc_nccl_unique_id(void *out128);   /* ncclGetUniqueId on the calling rank */
+void *isc_hub_create(int32_t nranks);
+int isc_hub_destroy(void *hub);
+int isc_comm_hub(isc_ctx *ctx, void *hub, int32_t rank, int32_t has_lo, int32_t has_hi,
+                 int32_t kw_lo, int32_t kw_hi);
+/* op 0 = sum, 1 = max, over ranks, in place on count (<= 64) host doubles */
+int isc_comm_allreduce_host(isc_ctx *ctx, double *vals, int32_t count, int32_t op);
+
 /* Stream used by every call (torch can wait on it); device sync helper. */
 void *isc_stream(isc_ctx *ctx);
 /* Issue all work on a caller's stream (e.g. torch's current stream); NULL

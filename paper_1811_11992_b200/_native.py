@@ -84,6 +84,14 @@ _SIGS = {
     "isc_newton_update": (ctypes.c_int, [VP, VP, VP, ctypes.c_double]),
     "isc_scaled_norm": (ctypes.c_int, [VP, VP, ctypes.c_double, c_double_p]),
     "isc_audit_sums": (ctypes.c_int, [VP, VP, VP]),
+    "isc_comm_nccl": (ctypes.c_int, [VP, VP, ctypes.c_int32, ctypes.c_int32, ctypes.c_int32,
+                                     ctypes.c_int32, ctypes.c_int32, ctypes.c_int32]),
+    "isc_nccl_unique_id": (ctypes.c_int, [VP]),
+    "isc_hub_create": (VP, [ctypes.c_int32]),
+    "isc_hub_destroy": (ctypes.c_int, [VP]),
+    "isc_comm_hub": (ctypes.c_int, [VP, VP, ctypes.c_int32, ctypes.c_int32, ctypes.c_int32,
+                                    ctypes.c_int32, ctypes.c_int32]),
+    "isc_comm_allreduce_host": (ctypes.c_int, [VP, VP, ctypes.c_int32, ctypes.c_int32]),
     "isc_stream": (VP, [VP]),
     "isc_set_stream": (ctypes.c_int, [VP, VP]),
     "isc_synchronize": (ctypes.c_int, [VP]),

@@ -13,6 +13,7 @@
 #include "assemble.cu"
 #include "decouple.cu"
 #include "fused.cu"
+#include "comm.cuh"
 #include "newton.cu"
 #include "solver.cu"
 
@@ -88,6 +89,10 @@ struct isc_ctx {
   int64_t dc_bad_cell = -1;       // singular block found by the fused decoupling
   int dc_bad_col = -1;
   double* mc_uinv = nullptr;   // multicolour ILU: U_b^-1 of black cells
+  // multi-GPU z-slab decomposition
+  Comm comm;
+  double *halo_send_lo = nullptr, *halo_send_hi = nullptr, *halo_recv_lo = nullptr,
+         *halo_recv_hi = nullptr;
   // timing
   cudaEvent_t ev[8] = {};
   double stage_ms[4] = {0, 0, 0, 0};
@@ -159,6 +164,9 @@ static int dev_alloc(void** p, size_t bytes) {
 
 static int grid1d(int64_t n, int t) { return (int)((n + t - 1) / t); }
 static void free_ilu(isc_ctx* ctx);
+static int halo_exchange(isc_ctx* ctx, double* v, int rows);
+static int allreduce_dev(isc_ctx* ctx, double* d, int count);
+extern "C" int isc_comm_allreduce_host(isc_ctx* ctx, double* vals, int32_t count, int32_t op);
 
 // ------------------------------------------------------ ILU structure
 // Subdomains exactly as the reference: count min(64, max(1, n // 2048))
@@ -300,6 +308,8 @@ extern "C" int isc_create(const isc_model_desc* md, const isc_grid_desc* gdsc, i
   g.n = g.nxny * g.nz;
   g.colored = (g.nx % 2 == 0) ? 1 : 0;
   g.half = g.n / 2;
+  g.kw_lo = 0;
+  g.kw_hi = g.nz;
   const int64_t n = g.n;
   // model
   Model& M = ctx->M;
@@ -424,7 +434,9 @@ extern "C" int isc_destroy(isc_ctx* ctx) {
                   ctx->capped_d, ctx->rec, ctx->acc, ctx->src, ctx->resid, ctx->diag,
                   ctx->offd, ctx->upw, ctx->bad_d, ctx->rhs, ctx->xk, ctx->rk, ctx->rhat,
                   ctx->pk, ctx->vk, ctx->phat, ctx->shat, ctx->sk, ctx->tk, ctx->sc,
-                  ctx->partial, ctx->flags, ctx->fail_d, ctx->schur, ctx->st_c, ctx->accn_c, ctx->stage};
+                  ctx->partial, ctx->flags, ctx->fail_d, ctx->schur, ctx->st_c, ctx->accn_c, ctx->stage,
+                  ctx->halo_send_lo, ctx->halo_send_hi, ctx->halo_recv_lo, ctx->halo_recv_hi};
+  if (ctx->comm.nccl && nccl_api().CommDestroy) nccl_api().CommDestroy(ctx->comm.nccl);
   free_ilu(ctx);
   for (void* p : ptrs)
     if (p) cudaFree(p);
@@ -506,6 +518,10 @@ extern "C" int isc_assemble(isc_ctx* ctx, const double* d_state, const double* h
   }
   d_state = ctx->st_c;
   d_accn = ctx->accn_c;
+  {
+    int hs = halo_exchange(ctx, ctx->st_c, NU);   // ghost planes of the state (multi-GPU)
+    if (hs) return hs;
+  }
   CellArgs A{ctx->g, d_state, ctx->phi_ref, ctx->vol, ctx->hl_area, ctx->hl_kob, ctx->hl_d,
              ctx->hl_rho, ctx->hl_tini, d_accn, dt, ctx->rec, ctx->acc, ctx->src,
              ctx->resid, ctx->diag, ctx->bad_d};
@@ -513,11 +529,17 @@ extern "C" int isc_assemble(isc_ctx* ctx, const double* d_state, const double* h
   LAUNCH_CHECK();
   CK(cudaMemcpyAsync(ctx->bad_h, ctx->bad_d, 8, cudaMemcpyDeviceToHost, st));
   CK(cudaStreamSynchronize(st));
-  if (*ctx->bad_h != ~0ULL) {
-    if (bad_cell) *bad_cell = (int64_t)*ctx->bad_h;
-    g_err = "coke fills the pore volume";
-    STAGE(stage_end(ctx, 0));
-    return ISC_PORE_SPACE_EXHAUSTED;
+  {
+    // all ranks of a z-slab run take the same branch
+    double flag = *ctx->bad_h != ~0ULL ? 1.0 : 0.0;
+    int as = isc_comm_allreduce_host(ctx, &flag, 1, 1);
+    if (as) return as;
+    if (flag > 0.0) {
+      if (bad_cell) *bad_cell = *ctx->bad_h != ~0ULL ? (int64_t)*ctx->bad_h : -1;
+      g_err = "coke fills the pore volume";
+      STAGE(stage_end(ctx, 0));
+      return ISC_PORE_SPACE_EXHAUSTED;
+    }
   }
   FaceArgs F{ctx->g, d_state, ctx->rec, ctx->depth, ctx->gd, ctx->td, ctx->upw, freeze,
              ctx->resid, ctx->diag, ctx->offd};
@@ -561,6 +583,10 @@ extern "C" int isc_assemble_decoupled(isc_ctx* ctx, const double* d_state, const
   }
   d_state = ctx->st_c;
   d_accn = ctx->accn_c;
+  {
+    int hs = halo_exchange(ctx, ctx->st_c, NU);   // ghost planes of the state (multi-GPU)
+    if (hs) return hs;
+  }
   CellArgs A{ctx->g, d_state, ctx->phi_ref, ctx->vol, ctx->hl_area, ctx->hl_kob, ctx->hl_d,
              ctx->hl_rho, ctx->hl_tini, d_accn, dt, ctx->rec, ctx->acc, ctx->src,
              ctx->resid, ctx->diag, ctx->bad_d};
@@ -568,11 +594,17 @@ extern "C" int isc_assemble_decoupled(isc_ctx* ctx, const double* d_state, const
   LAUNCH_CHECK();
   CK(cudaMemcpyAsync(ctx->bad_h, ctx->bad_d, 8, cudaMemcpyDeviceToHost, st));
   CK(cudaStreamSynchronize(st));
-  if (*ctx->bad_h != ~0ULL) {
-    if (bad_cell) *bad_cell = (int64_t)*ctx->bad_h;
-    g_err = "coke fills the pore volume";
-    STAGE(stage_end(ctx, 0));
-    return ISC_PORE_SPACE_EXHAUSTED;
+  {
+    // all ranks of a z-slab run take the same branch
+    double flag = *ctx->bad_h != ~0ULL ? 1.0 : 0.0;
+    int as = isc_comm_allreduce_host(ctx, &flag, 1, 1);
+    if (as) return as;
+    if (flag > 0.0) {
+      if (bad_cell) *bad_cell = *ctx->bad_h != ~0ULL ? (int64_t)*ctx->bad_h : -1;
+      g_err = "coke fills the pore volume";
+      STAGE(stage_end(ctx, 0));
+      return ISC_PORE_SPACE_EXHAUSTED;
+    }
   }
   if (ctx->nw > 0) {
     KScope ks(ctx, KT_WELLS);
@@ -750,17 +782,23 @@ extern "C" int isc_decouple(isc_ctx* ctx, int64_t* bad_cell, int32_t* bad_col) {
   const int64_t n = ctx->g.n;
   cudaStream_t st = ctx->stream;
   // well equations with a zero / non-finite bhp derivative (linsolve.py:372-375)
-  if (ctx->nw > 0) {
-    CK(cudaMemcpyAsync(ctx->wout_h, ctx->wout_d, ctx->nw * WOUT * 8, cudaMemcpyDeviceToHost, st));
-    CK(cudaStreamSynchronize(st));
-    for (int w = 0; w < ctx->nw; ++w) {
-      const double dwdb = ctx->wout_h[w * WOUT + 1];
-      if (dwdb == 0.0 || !std::isfinite(dwdb)) {
-        if (bad_cell) *bad_cell = -1;
-        if (bad_col) *bad_col = -1;
-        g_err = "well equation has a zero bhp derivative";
-        return ISC_SINGULAR_CELL_BLOCK;
+  {
+    double wbad = 0.0;
+    if (ctx->nw > 0) {
+      CK(cudaMemcpyAsync(ctx->wout_h, ctx->wout_d, ctx->nw * WOUT * 8, cudaMemcpyDeviceToHost, st));
+      CK(cudaStreamSynchronize(st));
+      for (int w = 0; w < ctx->nw; ++w) {
+        const double dwdb = ctx->wout_h[w * WOUT + 1];
+        if (dwdb == 0.0 || !std::isfinite(dwdb)) wbad = 1.0;
       }
+    }
+    int as = isc_comm_allreduce_host(ctx, &wbad, 1, 1);
+    if (as) return as;
+    if (wbad > 0.0) {
+      if (bad_cell) *bad_cell = -1;
+      if (bad_col) *bad_col = -1;
+      g_err = "well equation has a zero bhp derivative";
+      return ISC_SINGULAR_CELL_BLOCK;
     }
   }
   STAGE(stage_begin(ctx, 1));
@@ -777,6 +815,17 @@ extern "C" int isc_decouple(isc_ctx* ctx, int64_t* bad_cell, int32_t* bad_col) {
   }
   CK(cudaMemcpyAsync(ctx->bad_h, ctx->bad_d, 8, cudaMemcpyDeviceToHost, st));
   STAGE(stage_end(ctx, 1));
+  {
+    double flag = *ctx->bad_h != ~0ULL ? 1.0 : 0.0;
+    int as = isc_comm_allreduce_host(ctx, &flag, 1, 1);
+    if (as) return as;
+    if (flag > 0.0 && *ctx->bad_h == ~0ULL) {
+      if (bad_cell) *bad_cell = -1;
+      if (bad_col) *bad_col = -1;
+      g_err = "diagonal block is singular on another rank";
+      return ISC_SINGULAR_CELL_BLOCK;
+    }
+  }
   if (*ctx->bad_h != ~0ULL) {
     const int64_t c = (int64_t)*ctx->bad_h;
     int flag = 0;
@@ -830,6 +879,12 @@ extern "C" int isc_precond_setup(isc_ctx* ctx, int64_t* bad_cell) {
   CK(cudaMemcpyAsync(ctx->bad_h, ctx->fail_d, 4, cudaMemcpyDeviceToHost, st));
   STAGE(stage_end(ctx, 2));
   std::memcpy(&fail_h, ctx->bad_h, 4);
+  {
+    double flag = fail_h != 0x7f7f7f7f ? 1.0 : 0.0;
+    int as = isc_comm_allreduce_host(ctx, &flag, 1, 1);
+    if (as) return as;
+    if (flag > 0.0) fail_h = 1;
+  }
   if (fail_h != 0x7f7f7f7f) {
     if (bad_cell) *bad_cell = -1;
     g_err = "ILU(0) pivot failed";
@@ -925,6 +980,195 @@ static int mc_apply_spmv(isc_ctx* ctx, const double* p, double* phat, double* v,
   return ISC_OK;
 }
 
+// ------------------------------------------------- multi-GPU z-slab comm
+
+static int setup_window(isc_ctx* ctx, int32_t rank, int32_t nranks, int32_t has_lo,
+                        int32_t has_hi, int32_t kw_lo, int32_t kw_hi) {
+  if (kw_lo < 0 || kw_hi > ctx->g.nz || kw_lo >= kw_hi || (has_lo && kw_lo < 1) ||
+      (has_hi && kw_hi > ctx->g.nz - 1)) {
+    g_err = "bad owned plane window";
+    return ISC_BAD_ARGUMENT;
+  }
+  if (ctx->precond == ISC_PRECOND_RAS || ctx->precond == ISC_PRECOND_BJACOBI) {
+    g_err = "multi-rank solves use mcilu or none (rank-local block-Jacobi of the multicolour ILU)";
+    return ISC_UNSUPPORTED;
+  }
+  ctx->g.kw_lo = kw_lo;
+  ctx->g.kw_hi = kw_hi;
+  ctx->comm.rank = rank;
+  ctx->comm.nranks = nranks;
+  ctx->comm.has_lo = has_lo != 0;
+  ctx->comm.has_hi = has_hi != 0;
+  const size_t bytes = (size_t)NU * ctx->g.nxny * 8;
+  if (!ctx->halo_send_lo) {
+    ALLOC(ctx->halo_send_lo, bytes);
+    ALLOC(ctx->halo_send_hi, bytes);
+    ALLOC(ctx->halo_recv_lo, bytes);
+    ALLOC(ctx->halo_recv_hi, bytes);
+  }
+  return ISC_OK;
+}
+
+extern "C" int isc_comm_nccl(isc_ctx* ctx, const void* unique_id, int32_t rank, int32_t nranks,
+                             int32_t has_lo, int32_t has_hi, int32_t kw_lo, int32_t kw_hi) {
+  int s = setup_window(ctx, rank, nranks, has_lo, has_hi, kw_lo, kw_hi);
+  if (s) return s;
+  if (nranks > 1) {
+    NcclApi& api = nccl_api();
+    if (!api.ok) { g_err = "libnccl.so.2 not available in this process"; return ISC_UNSUPPORTED; }
+    ncclUniqueId id;
+    std::memcpy(&id, unique_id, sizeof(id));
+    const int r = api.CommInitRank(&ctx->comm.nccl, nranks, id, rank);
+    if (r != ncclSuccess_) {
+      g_err = std::string("ncclCommInitRank: ") + (api.GetErrorString ? api.GetErrorString(r) : "");
+      return ISC_CUDA_ERROR;
+    }
+  }
+  return ISC_OK;
+}
+
+extern "C" int isc_nccl_unique_id(void* out128) {
+  void* h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+  if (!h) { g_err = "libnccl.so.2 not found"; return ISC_UNSUPPORTED; }
+  auto fn = (int (*)(ncclUniqueId*))dlsym(h, "ncclGetUniqueId");
+  if (!fn) { g_err = "ncclGetUniqueId not found"; return ISC_UNSUPPORTED; }
+  ncclUniqueId id;
+  if (fn(&id) != ncclSuccess_) { g_err = "ncclGetUniqueId failed"; return ISC_CUDA_ERROR; }
+  std::memcpy(out128, &id, sizeof(id));
+  return ISC_OK;
+}
+
+extern "C" void* isc_hub_create(int32_t nranks) {
+  Hub* h = new Hub();
+  h->nranks = nranks;
+  h->send_lo.assign(nranks, nullptr);
+  h->send_hi.assign(nranks, nullptr);
+  h->ready.assign(nranks, nullptr);
+  h->red.assign((size_t)nranks * 64, 0.0);
+  return h;
+}
+extern "C" int isc_hub_destroy(void* hub) {
+  delete (Hub*)hub;
+  return ISC_OK;
+}
+
+extern "C" int isc_comm_hub(isc_ctx* ctx, void* hub, int32_t rank, int32_t has_lo, int32_t has_hi,
+                            int32_t kw_lo, int32_t kw_hi) {
+  Hub* h = (Hub*)hub;
+  int s = setup_window(ctx, rank, h->nranks, has_lo, has_hi, kw_lo, kw_hi);
+  if (s) return s;
+  ctx->comm.hub = h;
+  h->send_lo[rank] = ctx->halo_send_lo;
+  h->send_hi[rank] = ctx->halo_send_hi;
+  CK(cudaEventCreateWithFlags(&h->ready[rank], cudaEventDisableTiming));
+  return ISC_OK;
+}
+
+// one-plane halo of a storage-order vector (rows x n)
+static int halo_exchange(isc_ctx* ctx, double* v, int rows) {
+  Comm& cm = ctx->comm;
+  if (!cm.active()) return ISC_OK;
+  const Dims& g = ctx->g;
+  cudaStream_t st = ctx->stream;
+  const int64_t cnt = (int64_t)rows * g.nxny;
+  const int bl = grid1d(cnt, 256);
+  if (cm.has_lo) k_pack_plane<<<bl, 256, 0, st>>>(g, rows, g.kw_lo, v, ctx->halo_send_lo);
+  if (cm.has_hi) k_pack_plane<<<bl, 256, 0, st>>>(g, rows, g.kw_hi - 1, v, ctx->halo_send_hi);
+  ctx->launches += (cm.has_lo ? 1 : 0) + (cm.has_hi ? 1 : 0);
+  CK(cudaGetLastError());
+  if (cm.nccl) {
+    NcclApi& api = nccl_api();
+    api.GroupStart();
+    if (cm.has_lo) {
+      api.Send(ctx->halo_send_lo, cnt, ncclFloat64_, cm.rank - 1, cm.nccl, st);
+      api.Recv(ctx->halo_recv_lo, cnt, ncclFloat64_, cm.rank - 1, cm.nccl, st);
+    }
+    if (cm.has_hi) {
+      api.Send(ctx->halo_send_hi, cnt, ncclFloat64_, cm.rank + 1, cm.nccl, st);
+      api.Recv(ctx->halo_recv_hi, cnt, ncclFloat64_, cm.rank + 1, cm.nccl, st);
+    }
+    const int r = api.GroupEnd();
+    if (r != ncclSuccess_) { g_err = "NCCL halo exchange failed"; return ISC_CUDA_ERROR; }
+  } else if (cm.hub) {
+    Hub* h = cm.hub;
+    CK(cudaEventRecord(h->ready[cm.rank], st));
+    h->barrier();
+    if (cm.has_lo) {
+      CK(cudaStreamWaitEvent(st, h->ready[cm.rank - 1], 0));
+      CK(cudaMemcpyAsync(ctx->halo_recv_lo, h->send_hi[cm.rank - 1], cnt * 8,
+                         cudaMemcpyDeviceToDevice, st));
+    }
+    if (cm.has_hi) {
+      CK(cudaStreamWaitEvent(st, h->ready[cm.rank + 1], 0));
+      CK(cudaMemcpyAsync(ctx->halo_recv_hi, h->send_lo[cm.rank + 1], cnt * 8,
+                         cudaMemcpyDeviceToDevice, st));
+    }
+    CK(cudaStreamSynchronize(st));
+    h->barrier();   // neighbours may now reuse their send buffers
+  }
+  if (cm.has_lo) k_unpack_plane<<<bl, 256, 0, st>>>(g, rows, g.kw_lo - 1, ctx->halo_recv_lo, v);
+  if (cm.has_hi) k_unpack_plane<<<bl, 256, 0, st>>>(g, rows, g.kw_hi, ctx->halo_recv_hi, v);
+  ctx->launches += (cm.has_lo ? 1 : 0) + (cm.has_hi ? 1 : 0);
+  CK(cudaGetLastError());
+  return ISC_OK;
+}
+
+// sum `count` consecutive device scalars over the ranks (in place)
+static int allreduce_dev(isc_ctx* ctx, double* d, int count) {
+  Comm& cm = ctx->comm;
+  if (!cm.active()) return ISC_OK;
+  if (cm.nccl) {
+    const int r = nccl_api().AllReduce(d, d, count, ncclFloat64_, ncclSum_, cm.nccl, ctx->stream);
+    if (r != ncclSuccess_) { g_err = "NCCL allreduce failed"; return ISC_CUDA_ERROR; }
+    return ISC_OK;
+  }
+  Hub* h = cm.hub;
+  double loc[64];
+  CK(cudaMemcpyAsync(loc, d, count * 8, cudaMemcpyDeviceToHost, ctx->stream));
+  CK(cudaStreamSynchronize(ctx->stream));
+  std::memcpy(&h->red[(size_t)cm.rank * 64], loc, count * 8);
+  h->barrier();
+  for (int i = 0; i < count; ++i) {
+    double s = 0.0;
+    for (int q = 0; q < h->nranks; ++q) s += h->red[(size_t)q * 64 + i];   // rank order
+    loc[i] = s;
+  }
+  h->barrier();
+  CK(cudaMemcpyAsync(d, loc, count * 8, cudaMemcpyHostToDevice, ctx->stream));
+  CK(cudaStreamSynchronize(ctx->stream));
+  return ISC_OK;
+}
+
+// host-side reductions over ranks: op 0 sum, 1 max (NaN propagates)
+extern "C" int isc_comm_allreduce_host(isc_ctx* ctx, double* vals, int32_t count, int32_t op) {
+  Comm& cm = ctx->comm;
+  if (!cm.active() || count <= 0) return ISC_OK;
+  if (count > 64) { g_err = "too many values"; return ISC_BAD_ARGUMENT; }
+  if (cm.nccl) {
+    double* d = ctx->partial;   // scratch
+    CK(cudaMemcpyAsync(d, vals, count * 8, cudaMemcpyHostToDevice, ctx->stream));
+    const int r = nccl_api().AllReduce(d, d, count, ncclFloat64_, op ? ncclMax_ : ncclSum_,
+                                       cm.nccl, ctx->stream);
+    if (r != ncclSuccess_) { g_err = "NCCL allreduce failed"; return ISC_CUDA_ERROR; }
+    CK(cudaMemcpyAsync(vals, d, count * 8, cudaMemcpyDeviceToHost, ctx->stream));
+    CK(cudaStreamSynchronize(ctx->stream));
+    return ISC_OK;
+  }
+  Hub* h = cm.hub;
+  std::memcpy(&h->red[(size_t)cm.rank * 64], vals, count * 8);
+  h->barrier();
+  for (int i = 0; i < count; ++i) {
+    double s = op ? h->red[i] : 0.0;
+    for (int q = op ? 1 : 0; q < h->nranks; ++q) {
+      const double v = h->red[(size_t)q * 64 + i];
+      s = op ? ((v != v || s != s) ? v + s : std::max(s, v)) : s + v;
+    }
+    vals[i] = s;
+  }
+  h->barrier();
+  return ISC_OK;
+}
+
 // ------------------------------------------------------------- BiCGSTAB
 
 struct Kry {
@@ -934,12 +1178,14 @@ struct Kry {
   int finalize1(int nparts, int s0) {
     k_finalize<1><<<1, 256, 0, ctx->stream>>>(ctx->partial, nparts, ctx->sc, s0, s0, s0);
     ++ctx->launches;
-    return cudaGetLastError() == cudaSuccess ? 0 : ISC_CUDA_ERROR;
+    if (cudaGetLastError() != cudaSuccess) return ISC_CUDA_ERROR;
+    return allreduce_dev(ctx, ctx->sc + s0, 1);
   }
-  int finalize2(int nparts, int s0, int s1) {
+  int finalize2(int nparts, int s0, int s1) {   // s1 == s0 + 1
     k_finalize<2><<<1, 256, 0, ctx->stream>>>(ctx->partial, nparts, ctx->sc, s0, s1, s1);
     ++ctx->launches;
-    return cudaGetLastError() == cudaSuccess ? 0 : ISC_CUDA_ERROR;
+    if (cudaGetLastError() != cudaSuccess) return ISC_CUDA_ERROR;
+    return allreduce_dev(ctx, ctx->sc + s0, 2);
   }
   int dot(const double* a, const double* b, int slot) {
     k_dots<1><<<RED_BLOCKS, RED_THREADS, 0, ctx->stream>>>(len, a, b, nullptr, nullptr, nullptr,
@@ -983,7 +1229,9 @@ static int bicgstab(isc_ctx* ctx, double tol, int maxiter, int* iters) {
   *iters = 0;
   if (nb == 0.0) return ISC_OK;
   const double brk = 1e-30 * nb * nb;
-  const bool mc_fused = ctx->precond == ISC_PRECOND_MCILU && ctx->g.colored;
+  const bool mc_fused = ctx->precond == ISC_PRECOND_MCILU && ctx->g.colored &&
+                        !ctx->comm.active();
+  CK(cudaMemsetAsync(t, 0, len * 8, st));   // ghost rows of SpMV outputs stay zero
   CK(cudaMemcpyAsync(r, b, len * 8, cudaMemcpyDeviceToDevice, st));
   CK(cudaMemcpyAsync(rhat, b, len * 8, cudaMemcpyDeviceToDevice, st));
   CK(cudaMemsetAsync(p, 0, len * 8, st));
@@ -1000,6 +1248,7 @@ static int bicgstab(isc_ctx* ctx, double tol, int maxiter, int* iters) {
   TRY(K.read_scalars());
   auto restart = [&]() -> int {
     // r = b - A x; rhat = r; p = v = 0; scalars reset (linsolve.py:509-519)
+    if (halo_exchange(ctx, x, NU)) return ISC_CUDA_ERROR;
     if (spmv<0>(ctx, x, t, nullptr, nullptr, nullptr)) return ISC_CUDA_ERROR;
     k_sub<<<RED_BLOCKS, RED_THREADS, 0, st>>>(len, b, t, r);
     ++ctx->launches;
@@ -1035,6 +1284,7 @@ static int bicgstab(isc_ctx* ctx, double tol, int maxiter, int* iters) {
       TRY(mc_apply_spmv<1>(ctx, p, phat, v, rhat, nullptr, &nb1));
     } else {
       TRY(precond_apply(ctx, p, phat));
+      TRY(halo_exchange(ctx, phat, NU));
       TRY(spmv<1>(ctx, phat, v, rhat, nullptr, &nb1));
     }
     TRY(K.finalize1(nb1, S_DEN));
@@ -1067,6 +1317,7 @@ static int bicgstab(isc_ctx* ctx, double tol, int maxiter, int* iters) {
       TRY(mc_apply_spmv<2>(ctx, s, shat, t, nullptr, s, &nb2));
     } else {
       TRY(precond_apply(ctx, s, shat));
+      TRY(halo_exchange(ctx, shat, NU));
       TRY(spmv<2>(ctx, shat, t, nullptr, s, &nb2));
     }
     TRY(K.finalize2(nb2, S_TT, S_TS));
@@ -1099,14 +1350,27 @@ extern "C" int isc_solve(isc_ctx* ctx, double tol, int32_t maxiter, double* d_du
     int s = isc_decouple(ctx, bad_cell, bad_col);
     if (s) return s;
   } else {
+    double wbad = 0.0;
     for (int w = 0; w < ctx->nw; ++w) {
       const double dwdb = ctx->wout_h[w * WOUT + 1];
-      if (dwdb == 0.0 || !std::isfinite(dwdb)) {
-        if (bad_cell) *bad_cell = -1;
-        if (bad_col) *bad_col = -1;
-        g_err = "well equation has a zero bhp derivative";
-        return ISC_SINGULAR_CELL_BLOCK;
-      }
+      if (dwdb == 0.0 || !std::isfinite(dwdb)) wbad = 1.0;
+    }
+    double flags2[2] = {wbad, ctx->dc_bad_cell >= 0 ? 1.0 : 0.0};
+    {
+      int as = isc_comm_allreduce_host(ctx, flags2, 2, 1);
+      if (as) return as;
+    }
+    if (flags2[0] > 0.0) {
+      if (bad_cell) *bad_cell = -1;
+      if (bad_col) *bad_col = -1;
+      g_err = "well equation has a zero bhp derivative";
+      return ISC_SINGULAR_CELL_BLOCK;
+    }
+    if (flags2[1] > 0.0 && ctx->dc_bad_cell < 0) {
+      if (bad_cell) *bad_cell = -1;
+      if (bad_col) *bad_col = -1;
+      g_err = "diagonal block is singular on another rank";
+      return ISC_SINGULAR_CELL_BLOCK;
     }
     if (ctx->dc_bad_cell >= 0) {
       if (bad_cell) *bad_cell = ctx->dc_bad_cell;
@@ -1164,7 +1428,7 @@ extern "C" int isc_newton_update(isc_ctx* ctx, double* d_state, const double* d_
 
 extern "C" int isc_scaled_norm(isc_ctx* ctx, const double* d_accn, double dt, double* norm) {
   k_to_pos<double><<<grid1d(ctx->g.n, 256), 256, 0, ctx->stream>>>(ctx->g, NU, d_accn, ctx->accn_c);
-  k_norm_partial<<<RED_BLOCKS, 256, 0, ctx->stream>>>(ctx->g.n, ctx->resid, ctx->accn_c, ctx->vol,
+  k_norm_partial<<<RED_BLOCKS, 256, 0, ctx->stream>>>(ctx->g, ctx->resid, ctx->accn_c, ctx->vol,
                                                      dt, ctx->partial);
   LAUNCH_CHECK();
   std::vector<double> part(RED_BLOCKS);
@@ -1178,13 +1442,13 @@ extern "C" int isc_scaled_norm(isc_ctx* ctx, const double* d_accn, double dt, do
     m = std::max(m, v);
   }
   *norm = nan ? NAN : m;
-  return ISC_OK;
+  return isc_comm_allreduce_host(ctx, norm, 1, 1);
 }
 
 extern "C" int isc_audit_sums(isc_ctx* ctx, const double* d_accn, double* h_out) {
   constexpr int NR = NF + 1;
   k_to_pos<double><<<grid1d(ctx->g.n, 256), 256, 0, ctx->stream>>>(ctx->g, NU, d_accn, ctx->accn_c);
-  k_audit_partial<<<RED_BLOCKS, 256, 0, ctx->stream>>>(ctx->g.n, ctx->acc, ctx->accn_c, ctx->src,
+  k_audit_partial<<<RED_BLOCKS, 256, 0, ctx->stream>>>(ctx->g, ctx->acc, ctx->accn_c, ctx->src,
                                                       ctx->vol, ctx->partial);
   LAUNCH_CHECK();
   std::vector<double> part((size_t)3 * NR * RED_BLOCKS);
@@ -1196,5 +1460,5 @@ extern "C" int isc_audit_sums(isc_ctx* ctx, const double* d_accn, double* h_out)
     for (int b = 0; b < RED_BLOCKS; ++b) s += part[(size_t)k * RED_BLOCKS + b];
     h_out[k] = s;
   }
-  return ISC_OK;
+  return isc_comm_allreduce_host(ctx, h_out, 3 * NR, 0);
 }

@@ -69,7 +69,15 @@ struct Dims {
   int64_t nxny;
   int colored;     // 1: colour-blocked storage
   int64_t half;    // n/2 (red cells) when colored
+  // z-slab decomposition (multi-GPU): this context holds planes [0, nz) of
+  // which [kw_lo, kw_hi) are owned; the rest are one-plane ghost copies of
+  // the neighbouring ranks' cells. Single GPU: kw_lo = 0, kw_hi = nz.
+  int kw_lo, kw_hi;
 };
+
+__host__ __device__ __forceinline__ bool owned_k(const Dims& g, int k) {
+  return k >= g.kw_lo && k < g.kw_hi;
+}
 
 __host__ __device__ __forceinline__ void cell_ijk(const Dims& g, int64_t c, int& i, int& j,
                                                   int& k) {

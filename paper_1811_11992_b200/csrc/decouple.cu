@@ -322,13 +322,24 @@ __global__ void __launch_bounds__(DC3_THREADS, 3) k_decouple3(Dims g, const doub
     }
     __syncthreads();
   }
+  __shared__ int ghost[DC3_CELLS];
   if (mine) {
 #pragma unroll
     for (int r = 0; r < NU; ++r) inv[r][u][cl] = e[r];
-    if (u == 0 && live && failc[cl] < NU) {
-      const int64_t cell = cell_of(g, c);
-      flags[cell] = failc[cl] + 1;
-      atomicMin(bad, (unsigned long long)cell);
+    if (u == 0) {
+      bool gh = false;
+      int64_t cell = 0;
+      if (live) {
+        int ci, cj, ck;
+        cell = cell_of(g, c);
+        cell_ijk(g, cell, ci, cj, ck);
+        gh = !owned_k(g, ck);
+      }
+      ghost[cl] = gh ? 1 : 0;
+      if (live && !gh && failc[cl] < NU) {
+        flags[cell] = failc[cl] + 1;
+        atomicMin(bad, (unsigned long long)cell);
+      }
     }
   }
   __syncthreads();
@@ -348,6 +359,11 @@ __global__ void __launch_bounds__(DC3_THREADS, 3) k_decouple3(Dims g, const doub
     } else {
       base = rhs + cc;
       stride = n;
+    }
+    if (ghost[tc] && col == NDIR * NU) {   // ghost rows carry no equation
+#pragma unroll
+      for (int r = 0; r < NU; ++r) base[r * stride] = 0.0;
+      continue;
     }
     double v[NU];
 #pragma unroll

@@ -39,14 +39,20 @@ __global__ void k_newton_update(int64_t n, double* __restrict__ st, const double
 
 // partial maxima of |resid| / scale (newton.py:124-144), mass/energy/coke rows
 // scaled by (V/dt) max(1, |accn|), constraint rows by 1
-__global__ void __launch_bounds__(256) k_norm_partial(int64_t n, const double* __restrict__ resid,
+__global__ void __launch_bounds__(256) k_norm_partial(Dims g, const double* __restrict__ resid,
                                                       const double* __restrict__ accn,
                                                       const double* __restrict__ vol, double dt,
                                                       double* partial) {
+  const int64_t n = g.n;
   double m = 0.0;
   bool nan = false;
   for (int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; c < n;
        c += (int64_t)gridDim.x * blockDim.x) {
+    if (g.kw_lo > 0 || g.kw_hi < g.nz) {
+      int ci, cj, ck;
+      cell_ijk(g, cell_of(g, c), ci, cj, ck);
+      if (!owned_k(g, ck)) continue;
+    }
     const double vdt = vol[c] / dt;
 #pragma unroll
     for (int r = 0; r < NU; ++r) {
@@ -74,17 +80,23 @@ __global__ void __launch_bounds__(256) k_norm_partial(int64_t n, const double* _
 
 // audit sums per row r in rows[]: sum V(acc-accn), sum V src, sum V|acc|
 // (newton.py:339-366); rows = 0..NF-1 and the coke row
-__global__ void __launch_bounds__(256) k_audit_partial(int64_t n, const double* __restrict__ acc,
+__global__ void __launch_bounds__(256) k_audit_partial(Dims g, const double* __restrict__ acc,
                                                        const double* __restrict__ accn,
                                                        const double* __restrict__ src,
                                                        const double* __restrict__ vol,
                                                        double* partial) {
+  const int64_t n = g.n;
   constexpr int NR = NF + 1;
   double s[3 * NR];
 #pragma unroll
   for (int k = 0; k < 3 * NR; ++k) s[k] = 0.0;
   for (int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; c < n;
        c += (int64_t)gridDim.x * blockDim.x) {
+    if (g.kw_lo > 0 || g.kw_hi < g.nz) {
+      int ci, cj, ck;
+      cell_ijk(g, cell_of(g, c), ci, cj, ck);
+      if (!owned_k(g, ck)) continue;
+    }
     const double v = vol[c];
 #pragma unroll
     for (int k = 0; k < NR; ++k) {

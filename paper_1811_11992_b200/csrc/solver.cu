@@ -107,10 +107,15 @@ __global__ void __launch_bounds__(32 * NU) k_spmv(Dims g, const double* __restri
   double acc[KK];
 #pragma unroll
   for (int k = 0; k < KK; ++k) acc[k] = 0.0;
+  bool own = false;
+  int64_t cell = 0;
+  int i = 0, j = 0, k = 0;
   if (c < n) {
-    const int64_t cell = cell_of(g, c);
-    int i, j, k;
+    cell = cell_of(g, c);
     cell_ijk(g, cell, i, j, k);
+    own = owned_k(g, k);
+  }
+  if (own) {   // ghost rows carry no equation (multi-GPU slabs)
     double s = x[r * n + c];
 #pragma unroll
     for (int d = 0; d < NDIR; ++d) {
@@ -492,13 +497,14 @@ __global__ void __launch_bounds__(32 * NU, 2) k_mc_factor(Dims g, const double* 
   int i = 0, j = 0, k = 0;
   const int64_t cell = in ? cell_of(g, c) : 0;
   if (in) cell_ijk(g, cell, i, j, k);
-  const bool live = in && is_black(i, j, k);
+  const bool live = in && is_black(i, j, k) && owned_k(g, k);
   double ucol[NU];
 #pragma unroll
   for (int r = 0; r < NU; ++r) ucol[r] = (r == u) ? 1.0 : 0.0;
 #pragma unroll 1
   for (int d = 0; d < NDIR; ++d) {
-    const int64_t nb = live ? nb_pos(g, cell, i, j, k, d) : -1;
+    int64_t nb = live ? nb_pos(g, cell, i, j, k, d) : -1;
+    if ((d == DZM && !owned_k(g, k - 1)) || (d == DZP && !owned_k(g, k + 1))) nb = -1;
     if (nb >= 0) {
       const double* B = offd + (int64_t)(d * NB + u) * n + c;
 #pragma unroll
@@ -600,7 +606,7 @@ __global__ void __launch_bounds__(32 * NU) k_mc_apply(Dims g, const double* __re
   int i = 0, j = 0, k = 0;
   const int64_t cell = in ? cell_of(g, c) : 0;
   if (in) cell_ijk(g, cell, i, j, k);
-  const bool live = in && (is_black(i, j, k) == (PASS == 1));
+  const bool live = in && (is_black(i, j, k) == (PASS == 1)) && owned_k(g, k);
   double w = 0.0;
   if (live) {
     // pass 1 reads red neighbours of r (z_red = r_red); pass 2 the black z
@@ -610,6 +616,7 @@ __global__ void __launch_bounds__(32 * NU) k_mc_apply(Dims g, const double* __re
     for (int d = 0; d < NDIR; ++d) {
       const int64_t nb = nb_pos(g, cell, i, j, k, d);
       if (nb < 0) continue;
+      if ((d == DZM && !owned_k(g, k - 1)) || (d == DZP && !owned_k(g, k + 1))) continue;
       const double* blk = offd + (int64_t)((d * NU + r) * NU) * n + c;
       double t = 0.0;
 #pragma unroll

@@ -60,7 +60,8 @@ class DeviceContext:
     """The native context for one discrete problem."""
 
     def __init__(self, grid, pack, wells: Sequence, streams: Sequence, precond: str = "ras",
-                 heat_loss=None, device: Optional[torch.device] = None):
+                 heat_loss=None, device: Optional[torch.device] = None,
+                 own_stream: bool = False):
         if not torch.cuda.is_available():
             raise N.NativeLibraryMissing("no CUDA device: the product path has no CPU fallback")
         self.L = N.lib()
@@ -116,8 +117,9 @@ class DeviceContext:
                                N.PRECOND[precond], ctypes.byref(h))
         N.check(st, "isc_create")
         self.h = h
-        N.check(self.L.isc_set_stream(self.h, N.VP(torch.cuda.current_stream().cuda_stream)),
-                "isc_set_stream")
+        if not own_stream:   # order library work after torch's pending copies
+            N.check(self.L.isc_set_stream(self.h, N.VP(torch.cuda.current_stream().cuda_stream)),
+                    "isc_set_stream")
         self.wout = np.zeros((max(1, self.nw), N.WELL_OUT))
 
     def close(self):
@@ -223,6 +225,17 @@ class DeviceContext:
         N.check(self.L.isc_scaled_norm(self.h, N.ptr(d_accn), float(dt), ctypes.byref(out)),
                 "isc_scaled_norm")
         return out.value
+
+    def allreduce_host(self, vals, op: str = "sum"):
+        """Sum / max of a few host doubles over the ranks of the z-slab
+        decomposition (identity on a single GPU)."""
+        buf = np.ascontiguousarray(np.asarray(vals, dtype=np.float64).reshape(-1))
+        N.check(self.L.isc_comm_allreduce_host(self.h, N.ptr(buf), buf.size,
+                                               1 if op == "max" else 0), "allreduce")
+        return buf
+
+    def synchronize(self):
+        N.check(self.L.isc_synchronize(self.h), "isc_synchronize")
 
     def audit_sums(self, d_accn):
         out = np.zeros(3 * (NF + 1))

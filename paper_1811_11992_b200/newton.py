@@ -106,18 +106,23 @@ class Simulator:
     """Device-resident mirror of the reference ``Simulator`` (newton.py:214-437)."""
 
     def __init__(self, grid, pack, wells, streams, state, schedule, solver, heat_loss=None,
-                 fused: bool = False):
+                 fused: bool = False, comm_setup=None, own_stream: bool = False):
         self.grid, self.pack = grid, pack
         self.wells, self.streams = tuple(wells), tuple(streams)
         self.schedule, self.solver_cfg = schedule, solver
         self.fused = fused   # assemble+Schur+decoupling in one kernel (fused.cu)
-        self.ctx = DeviceContext(grid, pack, self.wells, self.streams, solver.precond, heat_loss)
+        self.ctx = DeviceContext(grid, pack, self.wells, self.streams, solver.precond, heat_loss,
+                                 own_stream=own_stream)
+        if comm_setup is not None:   # z-slab rank: window + NCCL/hub transport
+            comm_setup(self.ctx)
         dev = self.ctx.device
+        self.own_stream = own_stream
         self.state = DeviceState(state_to_device(state, dev), np.asarray(state.bhp, dtype=float))
         self.capped = np.zeros(len(self.wells), dtype=bool)
         self.time = 0.0
         self.du = self.ctx.empty(NU, grid.ncell)
         zero = torch.zeros(NU, grid.ncell, dtype=torch.float64, device=dev)
+        self._torch_sync()
         self.blocks: List[WellBlock] = self._assemble(self.state, zero, 1.0, 0.0, self.capped,
                                                       False)
         self.accn = self.ctx.copy_out(1, NU)
@@ -130,17 +135,24 @@ class Simulator:
         self.solve_calls = 0
 
     # -- device operations ------------------------------------------------------
+    def _torch_sync(self):
+        """Library on its own stream: wait for torch-side producers first."""
+        if self.own_stream:
+            torch.cuda.current_stream().synchronize()
+
     def _assemble(self, st: DeviceState, accn, dt, t_new, capped, freeze):
         wout = self.ctx.assemble(st.u, st.bhp, accn, dt, t_new, capped, freeze, fused=self.fused)
         return blocks_from_wout(self.wells, wout)
 
     def scaled_norm(self, blocks, dt, capped) -> float:
         """newton.py:124-144: cell rows on the device, well rows on the host."""
-        norm = self.ctx.scaled_norm_cells(self.accn, dt)
+        norm = self.ctx.scaled_norm_cells(self.accn, dt)   # max over ranks
+        wn = 0.0
         for w, (well, blk) in enumerate(zip(self.wells, blocks)):
             target = well.pinjmax if capped[w] else well.target
-            norm = max(norm, abs(blk.resid) / max(1.0, abs(target)))
-        return norm
+            wn = max(wn, abs(blk.resid) / max(1.0, abs(target)))
+        wn = float(self.ctx.allreduce_host([wn], "max")[0])   # wells live on their owner rank
+        return max(norm, wn)
 
     def newton_iteration(self, work: DeviceState, dt, t_new, capped, freeze):
         """One assemble + solve + update (the benchmark's unit of work)."""
@@ -155,6 +167,7 @@ class Simulator:
         """newton.py:254-310"""
         cfg = self.solver_cfg
         work = state.copy()
+        self._torch_sync()
         capped = capped.copy()
         lin_total = solves = growths = 0
         prev = math.inf
@@ -176,7 +189,8 @@ class Simulator:
             if math.isfinite(norm):
                 prev = norm
             want = desired_capped(self.wells, capped, work.bhp, blocks)
-            if not np.array_equal(want, capped):
+            switched = float(not np.array_equal(want, capped))
+            if self.ctx.allreduce_host([switched], "max")[0] > 0.0:   # collective decision
                 capped = want
                 continue
             if norm <= cfg.newton_tol:
@@ -218,13 +232,16 @@ class Simulator:
         rows = list(range(nf)) + [self.pack.nequ - 1]
         sums = self.ctx.audit_sums(self.accn)
         worst = 0.0
+        wq = np.zeros((2, len(rows)))
         for k, r in enumerate(rows):
-            dacc, reac, absacc = sums[0, k], sums[1, k], sums[2, k]
-            wellq = wellabs = 0.0
             for blk in self.blocks:
                 q = float(np.sum(blk.comp_rates[:, r]))
-                wellq += q
-                wellabs += abs(q)
+                wq[0, k] += q
+                wq[1, k] += abs(q)
+        wq = self.ctx.allreduce_host(wq, "sum").reshape(2, len(rows))
+        for k, r in enumerate(rows):
+            dacc, reac, absacc = sums[0, k], sums[1, k], sums[2, k]
+            wellq, wellabs = wq[0, k], wq[1, k]
             imb = dacc - dt * (reac + wellq)
             worst = max(worst, abs(imb) / max(1.0, absacc))
             self.cum_imbalance[k] += imb
