@@ -102,7 +102,9 @@ struct Comm {
   bool active() const { return nranks > 1; }
 };
 
-// pack / unpack the `rows` x plane-k values of a storage-order vector
+// pack / unpack the `rows` x plane-k values of a storage-order vector. The
+// buffer is in natural cell order within the plane, so ranks whose local
+// colourings of the shared plane differ (odd plane offsets) still agree.
 __global__ void k_pack_plane(Dims g, int rows, int k, const double* __restrict__ v,
                              double* __restrict__ buf) {
   const int64_t m = g.nxny;
@@ -110,14 +112,7 @@ __global__ void k_pack_plane(Dims g, int rows, int k, const double* __restrict__
   if (t >= m * rows) return;
   const int r = (int)(t / m);
   const int64_t q = t - (int64_t)r * m;
-  int64_t p;
-  if (g.colored) {   // plane k occupies [k*m/2, (k+1)*m/2) in each colour half
-    const int64_t hm = m / 2;
-    p = (q < hm ? 0 : g.half) + (int64_t)k * hm + (q < hm ? q : q - hm);
-  } else {
-    p = (int64_t)k * m + q;
-  }
-  buf[t] = v[(int64_t)r * g.n + p];
+  buf[t] = v[(int64_t)r * g.n + pos_of(g, (int64_t)k * m + q)];
 }
 
 __global__ void k_unpack_plane(Dims g, int rows, int k, const double* __restrict__ buf,
@@ -127,14 +122,7 @@ __global__ void k_unpack_plane(Dims g, int rows, int k, const double* __restrict
   if (t >= m * rows) return;
   const int r = (int)(t / m);
   const int64_t q = t - (int64_t)r * m;
-  int64_t p;
-  if (g.colored) {
-    const int64_t hm = m / 2;
-    p = (q < hm ? 0 : g.half) + (int64_t)k * hm + (q < hm ? q : q - hm);
-  } else {
-    p = (int64_t)k * m + q;
-  }
-  v[(int64_t)r * g.n + p] = buf[t];
+  v[(int64_t)r * g.n + pos_of(g, (int64_t)k * m + q)] = buf[t];
 }
 
 }  // namespace isc
