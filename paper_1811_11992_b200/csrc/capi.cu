@@ -310,9 +310,6 @@ extern "C" int isc_create(const isc_model_desc* md, const isc_grid_desc* gdsc, i
   g.half = g.n / 2;
   g.kw_lo = 0;
   g.kw_hi = g.nz;
-  g.f_nx = make_fastdiv((uint32_t)g.nx);
-  g.f_ny = make_fastdiv((uint32_t)g.ny);
-  g.f_nxny = make_fastdiv((uint32_t)g.nxny);
   const int64_t n = g.n;
   // model
   Model& M = ctx->M;

@@ -54,26 +54,6 @@ enum {
   RK_KTW, RK_KTO, RK_KTG, RK_KTR, RK_KTC, RK_PREF, RK_TREF, RK_EPS_PER, RK_KROCW
 };
 
-// Division by a runtime constant via one 64-bit multiply-high: exact for the
-// index ranges used here (numerators < 2^40). M = floor(2^64 / d) + 1.
-struct FastDiv {
-  uint64_t m = 0;
-  uint32_t d = 1;
-  __host__ __device__ __forceinline__ uint64_t div(uint64_t n) const {
-#ifdef __CUDA_ARCH__
-    return d == 1 ? n : __umul64hi(n, m);
-#else
-    return n / d;
-#endif
-  }
-};
-inline FastDiv make_fastdiv(uint32_t d) {
-  FastDiv f;
-  f.d = d;
-  f.m = d <= 1 ? 0 : (uint64_t)(((unsigned __int128)1 << 64) / d) + 1;
-  return f;
-}
-
 // Structured grid geometry (x fastest: c = i + nx*(j + ny*k)).
 //
 // Storage order of every per-cell array in HBM ("position" p): when nx is
@@ -93,7 +73,6 @@ struct Dims {
   // which [kw_lo, kw_hi) are owned; the rest are one-plane ghost copies of
   // the neighbouring ranks' cells. Single GPU: kw_lo = 0, kw_hi = nz.
   int kw_lo, kw_hi;
-  FastDiv f_nx, f_ny, f_nxny;   // index arithmetic without integer division
 };
 
 __host__ __device__ __forceinline__ bool owned_k(const Dims& g, int k) {
@@ -102,14 +81,12 @@ __host__ __device__ __forceinline__ bool owned_k(const Dims& g, int k) {
 
 __host__ __device__ __forceinline__ void cell_ijk(const Dims& g, int64_t c, int& i, int& j,
                                                   int& k) {
-  if (g.n < ((int64_t)1 << 40)) {
-    const uint64_t cc = (uint64_t)c;
-    const uint64_t kk = g.f_nxny.div(cc);
-    const uint64_t rem = cc - kk * (uint64_t)g.nxny;
-    const uint64_t jj = g.f_nx.div(rem);
+  if (g.n < (int64_t)0x7fffffff) {
+    const uint32_t cc = (uint32_t)c, nx = (uint32_t)g.nx, nxny = (uint32_t)g.nxny;
+    const uint32_t kk = cc / nxny, rem = cc - kk * nxny;
     k = (int)kk;
-    j = (int)jj;
-    i = (int)(rem - jj * (uint64_t)g.nx);
+    j = (int)(rem / nx);
+    i = (int)(rem - (uint32_t)j * nx);
   } else {
     k = (int)(c / g.nxny);
     const int64_t rem = c - (int64_t)k * g.nxny;
