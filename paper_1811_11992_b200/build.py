@@ -40,7 +40,8 @@ def build(force: bool = False, verbose: bool = False) -> str:
     if not force and up_to_date():
         return LIB
     os.makedirs(LIB_DIR, exist_ok=True)
-    cmd = [NVCC, *FLAGS, "-Xptxas", "-v", "-o", LIB + ".tmp", os.path.join(CSRC, "capi.cu")]
+    extra = os.environ.get("ISC_NVCC_EXTRA", "").split()   # experiments, e.g. -DMC_MINB=6
+    cmd = [NVCC, *FLAGS, *extra, "-Xptxas", "-v", "-o", LIB + ".tmp", os.path.join(CSRC, "capi.cu")]
     res = subprocess.run(cmd, cwd=CSRC, capture_output=True, text=True)
     if res.returncode != 0:
         errs = [ln for ln in res.stderr.splitlines() if "error" in ln.lower()]

@@ -774,9 +774,8 @@ __global__ void __launch_bounds__(32 * NU, 3) k_face(const FaceArgs F) {
   const int64_t c = (int64_t)blockIdx.x * 32 + threadIdx.x;   // storage position
   const int row = threadIdx.y;
   if (c >= n) return;
-  const int64_t cell = cell_of(F.g, c);
   int i, j, k;
-  cell_ijk(F.g, cell, i, j, k);
+  const int64_t cell = locate(F.g, c, i, j, k);
   double res = F.resid[row * n + c];
   double drow[NU];
 #pragma unroll

@@ -77,6 +77,7 @@ struct isc_ctx {
   double* sc = nullptr;
   double* sc_h = nullptr;   // pinned
   double* partial = nullptr;
+  double* partial2 = nullptr;   // second stage of the fixed-order sums
   int64_t npartial = 0;
   int* flags = nullptr;
   int* fail_d = nullptr;
@@ -308,6 +309,7 @@ extern "C" int isc_create(const isc_model_desc* md, const isc_grid_desc* gdsc, i
   g.n = g.nxny * g.nz;
   g.colored = (g.nx % 2 == 0) ? 1 : 0;
   g.half = g.n / 2;
+  g.ph = g.nxny / 2;
   g.kw_lo = 0;
   g.kw_hi = g.nz;
   const int64_t n = g.n;
@@ -412,7 +414,9 @@ extern "C" int isc_create(const isc_model_desc* md, const isc_grid_desc* gdsc, i
   for (double** v : vecs) ALLOC(*v, (size_t)NU * n * 8);
   ALLOC(ctx->sc, S_NSCAL * 8);
   CK(cudaMallocHost(&ctx->sc_h, S_NSCAL * 8));
-  ctx->npartial = std::max<int64_t>(RED_BLOCKS, grid1d(n, 32)) * 3 * (NF + 1);
+  ctx->npartial = std::max<int64_t>((int64_t)RED_BLOCKS * 3 * (NF + 1),
+                                    ((int64_t)grid1d(n, 32) + 2) * NU * 3);
+  ALLOC(ctx->partial2, (int64_t)FIN_BLOCKS * 3 * 8);
   ALLOC(ctx->partial, ctx->npartial * 8);
   ALLOC(ctx->flags, n * 4);
   ALLOC(ctx->fail_d, 4);
@@ -434,7 +438,7 @@ extern "C" int isc_destroy(isc_ctx* ctx) {
                   ctx->capped_d, ctx->rec, ctx->acc, ctx->src, ctx->resid, ctx->diag,
                   ctx->offd, ctx->upw, ctx->bad_d, ctx->rhs, ctx->xk, ctx->rk, ctx->rhat,
                   ctx->pk, ctx->vk, ctx->phat, ctx->shat, ctx->sk, ctx->tk, ctx->sc,
-                  ctx->partial, ctx->flags, ctx->fail_d, ctx->schur, ctx->st_c, ctx->accn_c, ctx->stage,
+                  ctx->partial, ctx->partial2, ctx->flags, ctx->fail_d, ctx->schur, ctx->st_c, ctx->accn_c, ctx->stage,
                   ctx->halo_send_lo, ctx->halo_send_hi, ctx->halo_recv_lo, ctx->halo_recv_hi};
   if (ctx->comm.nccl && nccl_api().CommDestroy) nccl_api().CommDestroy(ctx->comm.nccl);
   free_ilu(ctx);
@@ -861,7 +865,6 @@ extern "C" int isc_precond_setup(isc_ctx* ctx, int64_t* bad_cell) {
   {
   KScope ks(ctx, KT_ILU_FACTOR);
   if (ctx->precond == ISC_PRECOND_MCILU) {
-    KScope ks(ctx, KT_ILU_FACTOR);
     const int64_t nblack = ctx->g.colored ? ctx->g.n - ctx->g.half : ctx->g.n;
     k_mc_factor<<<grid1d(nblack, 32), dim3(32, NU), 0, st>>>(ctx->g, ctx->offd, ctx->mc_uinv,
                                                             ctx->fail_d);
@@ -930,7 +933,7 @@ static int spmv(isc_ctx* ctx, const double* x, double* y, const double* w0, cons
   k_spmv<K><<<blocks, dim3(32, NU), 0, ctx->stream>>>(ctx->g, ctx->offd, x, y, w0, w1,
                                                       ctx->partial);
   LAUNCH_CHECK();
-  if (nblocks) *nblocks = blocks;
+  if (nblocks) *nblocks = blocks * NU;   // per-warp partials
   return ISC_OK;
 }
 
@@ -976,7 +979,7 @@ static int mc_apply_spmv(isc_ctx* ctx, const double* p, double* phat, double* v,
   }
   ctx->launches += 3;
   CK(cudaGetLastError());
-  *nparts = b1 + b2;
+  *nparts = (b1 + b2) * NU;   // per-warp partials
   return ISC_OK;
 }
 
@@ -1175,15 +1178,26 @@ struct Kry {
   isc_ctx* ctx;
   int64_t len;
   int vgrid() const { return RED_BLOCKS; }
+  // fixed-order sums: one block for RED_BLOCKS partials, two stages for the
+  // per-warp partials of the stencil passes
+  template <int K>
+  void finalize(int nparts, int s0, int s1) {
+    if (nparts <= RED_BLOCKS) {
+      k_finalize<K><<<1, 256, 0, ctx->stream>>>(ctx->partial, nparts, ctx->sc, s0, s1, s1);
+      ++ctx->launches;
+      return;
+    }
+    k_partial_sum<K><<<FIN_BLOCKS, 256, 0, ctx->stream>>>(ctx->partial, nparts, ctx->partial2);
+    k_finalize<K><<<1, 256, 0, ctx->stream>>>(ctx->partial2, FIN_BLOCKS, ctx->sc, s0, s1, s1);
+    ctx->launches += 2;
+  }
   int finalize1(int nparts, int s0) {
-    k_finalize<1><<<1, 256, 0, ctx->stream>>>(ctx->partial, nparts, ctx->sc, s0, s0, s0);
-    ++ctx->launches;
+    finalize<1>(nparts, s0, s0);
     if (cudaGetLastError() != cudaSuccess) return ISC_CUDA_ERROR;
     return allreduce_dev(ctx, ctx->sc + s0, 1);
   }
   int finalize2(int nparts, int s0, int s1) {   // s1 == s0 + 1
-    k_finalize<2><<<1, 256, 0, ctx->stream>>>(ctx->partial, nparts, ctx->sc, s0, s1, s1);
-    ++ctx->launches;
+    finalize<2>(nparts, s0, s1);
     if (cudaGetLastError() != cudaSuccess) return ISC_CUDA_ERROR;
     return allreduce_dev(ctx, ctx->sc + s0, 2);
   }

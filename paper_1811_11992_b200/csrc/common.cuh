@@ -57,18 +57,25 @@ enum {
 // Structured grid geometry (x fastest: c = i + nx*(j + ny*k)).
 //
 // Storage order of every per-cell array in HBM ("position" p): when nx is
-// even the cells are colour-blocked, red (i+j+k even) first, then black,
-// each colour in natural order: p = colour*half + (c >> 1). Each colour's
-// rows are then contiguous, so the multicolour ILU passes and any
-// single-colour sweep stream full 32 B sectors. Neighbours of a cell all
-// have the other colour, so their positions follow from (c ± stride) >> 1.
-// With odd nx the natural order is used (colored = 0).
+// even the cells are colour-blocked plane by plane: plane k occupies
+// positions [k*nxny, (k+1)*nxny), its red cells (i+j+k even) first, then
+// its black cells, each in natural order:
+//   p = k*nxny + colour*ph + (q >> 1),   q = in-plane index, ph = nxny/2
+//     = (c >> 1) + ph*(k + colour).
+// Each colour's rows of a plane are contiguous, so the multicolour ILU
+// passes and any single-colour sweep stream full 32 B sectors, while the
+// working set of a sweep stays within three neighbouring planes (a
+// whole-array red/black split streams 11 % slower on B200: tools/
+// layout_probe.cu). Neighbours of a cell all have the other colour, so their
+// positions follow from (c ± stride) >> 1. With odd nx the natural order is
+// used (colored = 0).
 struct Dims {
   int nx, ny, nz;
   int64_t n;       // nx*ny*nz
   int64_t nxny;
   int colored;     // 1: colour-blocked storage
-  int64_t half;    // n/2 (red cells) when colored
+  int64_t half;    // n/2 (cells of each colour) when colored
+  int64_t ph;      // nxny/2 (cells of each colour in one plane) when colored
   // z-slab decomposition (multi-GPU): this context holds planes [0, nz) of
   // which [kw_lo, kw_hi) are owned; the rest are one-plane ghost copies of
   // the neighbouring ranks' cells. Single GPU: kw_lo = 0, kw_hi = nz.
@@ -99,16 +106,50 @@ __host__ __device__ __forceinline__ int64_t pos_of(const Dims& g, int64_t c) {
   if (!g.colored) return c;
   int i, j, k;
   cell_ijk(g, c, i, j, k);
-  return (int64_t)((i + j + k) & 1) * g.half + (c >> 1);
+  return (c >> 1) + g.ph * (int64_t)(k + ((i + j + k) & 1));
+}
+
+// cell index and (i, j, k) of storage position p (one decomposition)
+__host__ __device__ __forceinline__ int64_t locate(const Dims& g, int64_t p, int& i, int& j,
+                                                   int& k) {
+  if (!g.colored) {
+    cell_ijk(g, p, i, j, k);
+    return p;
+  }
+  int64_t rem;
+  if (g.n < (int64_t)0x7fffffff) {
+    const uint32_t kk = (uint32_t)p / (uint32_t)g.nxny;
+    k = (int)kk;
+    rem = (uint32_t)p - kk * (uint32_t)g.nxny;
+  } else {
+    k = (int)(p / g.nxny);
+    rem = p - (int64_t)k * g.nxny;
+  }
+  const int col = rem >= g.ph ? 1 : 0;
+  const uint32_t q0 = 2u * (uint32_t)(rem - col * g.ph);
+  j = (int)(q0 / (uint32_t)g.nx);
+  i = (int)(q0 - (uint32_t)j * (uint32_t)g.nx);
+  i += (((i + j + k) & 1) != col) ? 1 : 0;
+  return (int64_t)k * g.nxny + (int64_t)j * g.nx + i;
 }
 
 __host__ __device__ __forceinline__ int64_t cell_of(const Dims& g, int64_t p) {
-  if (!g.colored) return p;
-  const int col = p >= g.half ? 1 : 0;
-  const int64_t c0 = 2 * (p - (int64_t)col * g.half);
   int i, j, k;
-  cell_ijk(g, c0, i, j, k);
-  return (((i + j + k) & 1) == col) ? c0 : c0 + 1;
+  return locate(g, p, i, j, k);
+}
+
+// z-plane of storage position p (planes are contiguous in both orders)
+__host__ __device__ __forceinline__ int plane_of(const Dims& g, int64_t p) {
+  if (g.n < (int64_t)0x7fffffff) return (int)((uint32_t)p / (uint32_t)g.nxny);
+  return (int)(p / g.nxny);
+}
+
+// storage position of the t-th cell of colour col (0 <= t < half)
+__host__ __device__ __forceinline__ int64_t colour_pos(const Dims& g, int col, int64_t t) {
+  int64_t kk;
+  if (g.n < (int64_t)0x7fffffff) kk = (uint32_t)t / (uint32_t)g.ph;
+  else kk = t / g.ph;
+  return kk * g.nxny + (int64_t)col * g.ph + (t - kk * g.ph);
 }
 
 // Direction d of a neighbour, in the reference's gather order
@@ -123,7 +164,8 @@ __device__ __forceinline__ int64_t neighbour(const Dims& g, int64_t c, int i, in
 __device__ __forceinline__ int64_t nb_pos(const Dims& g, int64_t c, int i, int j, int k, int d) {
   const int64_t nb = neighbour(g, c, i, j, k, d);
   if (nb < 0 || !g.colored) return nb;
-  return (int64_t)(((i + j + k) & 1) ^ 1) * g.half + (nb >> 1);
+  const int kn = k + (d == DZM ? -1 : (d == DZP ? 1 : 0));
+  return (nb >> 1) + g.ph * (int64_t)(kn + (((i + j + k) & 1) ^ 1));
 }
 
 // neighbour of cell c in direction d, or -1 at the boundary

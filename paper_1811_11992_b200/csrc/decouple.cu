@@ -330,10 +330,8 @@ __global__ void __launch_bounds__(DC3_THREADS, 3) k_decouple3(Dims g, const doub
       bool gh = false;
       int64_t cell = 0;
       if (live) {
-        int ci, cj, ck;
         cell = cell_of(g, c);
-        cell_ijk(g, cell, ci, cj, ck);
-        gh = !owned_k(g, ck);
+        gh = !owned_k(g, plane_of(g, c));
       }
       ghost[cl] = gh ? 1 : 0;
       if (live && !gh && failc[cl] < NU) {

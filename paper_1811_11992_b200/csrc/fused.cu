@@ -216,8 +216,7 @@ __global__ void __launch_bounds__(FD_CELLS * 64) k_face_dc(const FusedArgs P) {
   const int64_t c = (int64_t)blockIdx.x * FD_CELLS + cl;
   const bool live = c < n;
   int i = 0, jj = 0, k = 0;
-  const int64_t cell = live ? cell_of(F.g, c) : 0;
-  if (live) cell_ijk(F.g, cell, i, jj, k);
+  const int64_t cell = live ? locate(F.g, c, i, jj, k) : 0;
   double a[NU];   // this thread's column of the augmented block row
   // ---- phase 1: faces -> off-diagonal columns (+ own-derivative columns to smem)
   if (j >= NU && j < NU + NDIR * NU) {

@@ -49,9 +49,7 @@ __global__ void __launch_bounds__(256) k_norm_partial(Dims g, const double* __re
   for (int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; c < n;
        c += (int64_t)gridDim.x * blockDim.x) {
     if (g.kw_lo > 0 || g.kw_hi < g.nz) {
-      int ci, cj, ck;
-      cell_ijk(g, cell_of(g, c), ci, cj, ck);
-      if (!owned_k(g, ck)) continue;
+      if (!owned_k(g, plane_of(g, c))) continue;
     }
     const double vdt = vol[c] / dt;
 #pragma unroll
@@ -93,9 +91,7 @@ __global__ void __launch_bounds__(256) k_audit_partial(Dims g, const double* __r
   for (int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; c < n;
        c += (int64_t)gridDim.x * blockDim.x) {
     if (g.kw_lo > 0 || g.kw_hi < g.nz) {
-      int ci, cj, ck;
-      cell_ijk(g, cell_of(g, c), ci, cj, ck);
-      if (!owned_k(g, ck)) continue;
+      if (!owned_k(g, plane_of(g, c))) continue;
     }
     const double v = vol[c];
 #pragma unroll

@@ -11,7 +11,20 @@ namespace cg = cooperative_groups;
 
 namespace isc {
 
+// Blocks per SM for the bandwidth-bound stencil passes: fewer resident blocks
+// but more registers per thread keeps more independent loads in flight per
+// warp, which is what these streams need (C4 sweep 2..7: 3 best for the
+// multicolour passes, 4 for the full SpMV; profiles/r1/minb_sweep.md).
+#ifndef MC_MINB
+#define MC_MINB 3
+#endif
+#ifndef SPMV_MINB
+#define SPMV_MINB 4
+#endif
+
+
 constexpr int RED_BLOCKS = 148 * 8;   // fixed partition -> deterministic sums
+constexpr int FIN_BLOCKS = 148;       // first stage of the two-stage partial sums
 constexpr int RED_THREADS = 256;
 
 // Krylov scalar slots in device memory (host mirror reads them)
@@ -42,6 +55,51 @@ __device__ __forceinline__ void block_reduce_store(double (&v)[K], double* parti
       double s = 0.0;
       for (int w = 0; w < nwarps; ++w) s += sh[k][w];
       partial[k * gridDim.x + blockIdx.x] = s;
+    }
+  }
+}
+
+// per-warp partials, no block barrier: lane 0 of warp y (block = 32 x NU)
+// stores partial[k*stride + slot*NU + y]. A block-wide reduction would make
+// every warp of the stencil passes wait for the block's slowest one, which
+// costs ~30 % of their bandwidth (tools/layout_probe.cu).
+template <int K>
+__device__ __forceinline__ void warp_store_at(double (&v)[K], double* partial, int64_t stride,
+                                              int64_t slot) {
+#pragma unroll
+  for (int k = 0; k < K; ++k) {
+    double x = v[k];
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) x += __shfl_down_sync(0xffffffffu, x, o);
+    if (threadIdx.x == 0) partial[(int64_t)k * stride + slot * NU + threadIdx.y] = x;
+  }
+}
+
+// first stage of a two-stage fixed-order sum: block b reduces the contiguous
+// chunk b of each of the K partial arrays into out[k*gridDim.x + b]
+template <int K>
+__global__ void __launch_bounds__(256) k_partial_sum(const double* __restrict__ partial,
+                                                     int64_t nparts, double* __restrict__ out) {
+  __shared__ double sh[K][8];
+  const int t = threadIdx.x, lane = t & 31, w = t >> 5;
+  const int64_t chunk = (nparts + gridDim.x - 1) / gridDim.x;
+  const int64_t lo = (int64_t)blockIdx.x * chunk;
+  const int64_t hi = lo + chunk < nparts ? lo + chunk : nparts;
+#pragma unroll
+  for (int k = 0; k < K; ++k) {
+    double s = 0.0;
+    for (int64_t i = lo + t; i < hi; i += 256) s += partial[(int64_t)k * nparts + i];
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) s += __shfl_down_sync(0xffffffffu, s, o);
+    if (lane == 0) sh[k][w] = s;
+  }
+  __syncthreads();
+  if (t == 0) {
+#pragma unroll
+    for (int k = 0; k < K; ++k) {
+      double s = 0.0;
+      for (int i = 0; i < 8; ++i) s += sh[k][i];
+      out[(int64_t)k * gridDim.x + blockIdx.x] = s;
     }
   }
 }
@@ -94,7 +152,7 @@ __global__ void __launch_bounds__(RED_THREADS) k_dots(int64_t len, const double*
 // y = x + sum_d B_d x_nb ; optional fused partial dots of y with (w0, w1):
 // grid (ceil(n/32)), block (32, NU): thread (c, r).
 template <int K>
-__global__ void __launch_bounds__(32 * NU) k_spmv(Dims g, const double* __restrict__ offd,
+__global__ void __launch_bounds__(32 * NU, SPMV_MINB) k_spmv(Dims g, const double* __restrict__ offd,
                                                   const double* __restrict__ x,
                                                   double* __restrict__ y,
                                                   const double* __restrict__ w0,
@@ -111,8 +169,7 @@ __global__ void __launch_bounds__(32 * NU) k_spmv(Dims g, const double* __restri
   int64_t cell = 0;
   int i = 0, j = 0, k = 0;
   if (c < n) {
-    cell = cell_of(g, c);
-    cell_ijk(g, cell, i, j, k);
+    cell = locate(g, c, i, j, k);
     own = owned_k(g, k);
   }
   if (own) {   // ghost rows carry no equation (multi-GPU slabs)
@@ -132,7 +189,7 @@ __global__ void __launch_bounds__(32 * NU) k_spmv(Dims g, const double* __restri
     if (K == 1) acc[0] = s * w0[r * n + c];
     if (K == 2) { acc[0] = s * s; acc[K > 1 ? 1 : 0] = s * w1[r * n + c]; }
   }
-  if (K > 0) block_reduce_store<KK>(acc, partial);
+  if (K > 0) warp_store_at<KK>(acc, partial, (int64_t)gridDim.x * NU, blockIdx.x);
 }
 
 // --------------------------------------------------------- vector kernels
@@ -492,11 +549,11 @@ __global__ void __launch_bounds__(32 * NU, 2) k_mc_factor(Dims g, const double* 
   __shared__ int pivs[32];
   const int64_t n = g.n;
   const int ls = threadIdx.x, u = threadIdx.y;
-  const int64_t c = (int64_t)blockIdx.x * 32 + ls + (g.colored ? g.half : 0);
-  const bool in = c < n;
+  const int64_t t = (int64_t)blockIdx.x * 32 + ls;   // t-th black cell when colour-blocked
+  const bool in = t < (g.colored ? g.half : n);
+  const int64_t c = g.colored ? (in ? colour_pos(g, 1, t) : 0) : t;
   int i = 0, j = 0, k = 0;
-  const int64_t cell = in ? cell_of(g, c) : 0;
-  if (in) cell_ijk(g, cell, i, j, k);
+  const int64_t cell = in ? locate(g, c, i, j, k) : 0;
   const bool live = in && is_black(i, j, k) && owned_k(g, k);
   double ucol[NU];
 #pragma unroll
@@ -593,7 +650,7 @@ __global__ void __launch_bounds__(32 * NU, 2) k_mc_factor(Dims g, const double* 
 
 // pass 1 (black rows) / pass 2 (red rows); thread (cell lane, row r)
 template <int PASS>
-__global__ void __launch_bounds__(32 * NU) k_mc_apply(Dims g, const double* __restrict__ offd,
+__global__ void __launch_bounds__(32 * NU, MC_MINB) k_mc_apply(Dims g, const double* __restrict__ offd,
                                                       const double* __restrict__ uinv,
                                                       const double* __restrict__ rin,
                                                       double* __restrict__ z) {
@@ -601,11 +658,11 @@ __global__ void __launch_bounds__(32 * NU) k_mc_apply(Dims g, const double* __re
   const int64_t n = g.n;
   const int ls = threadIdx.x, r = threadIdx.y;
   // colour-blocked storage: pass 1 covers the black half, pass 2 the red half
-  const int64_t c = (int64_t)blockIdx.x * 32 + ls + ((g.colored && PASS == 1) ? g.half : 0);
-  const bool in = g.colored ? (PASS == 1 ? c < n : c < g.half) : c < n;
+  const int64_t t = (int64_t)blockIdx.x * 32 + ls;
+  const bool in = t < (g.colored ? g.half : n);
+  const int64_t c = g.colored ? (in ? colour_pos(g, PASS == 1 ? 1 : 0, t) : 0) : t;
   int i = 0, j = 0, k = 0;
-  const int64_t cell = in ? cell_of(g, c) : 0;
-  if (in) cell_ijk(g, cell, i, j, k);
+  const int64_t cell = in ? locate(g, c, i, j, k) : 0;
   const bool live = in && (is_black(i, j, k) == (PASS == 1)) && owned_k(g, k);
   double w = 0.0;
   if (live) {
@@ -673,7 +730,7 @@ __device__ __forceinline__ void block_reduce_store_at(double (&v)[K], double* pa
 // pass 2 (red rows): z_r = p_r - sum B_rd z_b, v_r = p_r, partial dots of v_r
 // K == 1: v.w0 ; K == 2: (v.v, v.w1)
 template <int K>
-__global__ void __launch_bounds__(32 * NU) k_mc_red(Dims g, const double* __restrict__ offd,
+__global__ void __launch_bounds__(32 * NU, MC_MINB) k_mc_red(Dims g, const double* __restrict__ offd,
                                                     const double* __restrict__ pin,
                                                     double* __restrict__ z, double* __restrict__ v,
                                                     const double* __restrict__ w0,
@@ -681,14 +738,14 @@ __global__ void __launch_bounds__(32 * NU) k_mc_red(Dims g, const double* __rest
                                                     double* partial, int stride) {
   const int64_t n = g.n;
   const int ls = threadIdx.x, r = threadIdx.y;
-  const int64_t c = (int64_t)blockIdx.x * 32 + ls;   // red half (colour-blocked storage)
+  const int64_t t = (int64_t)blockIdx.x * 32 + ls;   // t-th red cell (colour-blocked storage)
   double acc[K];
 #pragma unroll
   for (int k = 0; k < K; ++k) acc[k] = 0.0;
-  if (c < g.half) {
-    const int64_t cell = cell_of(g, c);
+  if (t < g.half) {
+    const int64_t c = colour_pos(g, 0, t);
     int i, j, k;
-    cell_ijk(g, cell, i, j, k);
+    const int64_t cell = locate(g, c, i, j, k);
     const double pr = pin[r * n + c];
     double w = pr;
 #pragma unroll
@@ -706,12 +763,12 @@ __global__ void __launch_bounds__(32 * NU) k_mc_red(Dims g, const double* __rest
     if (K == 1) acc[0] = pr * w0[r * n + c];
     if (K == 2) { acc[0] = pr * pr; acc[K - 1] = pr * w1[r * n + c]; }
   }
-  block_reduce_store_at<K>(acc, partial, stride, blockIdx.x);
+  warp_store_at<K>(acc, partial, (int64_t)stride * NU, blockIdx.x);
 }
 
 // black rows of the product: v_b = z_b + sum B_bd z_r, partial dots of v_b
 template <int K>
-__global__ void __launch_bounds__(32 * NU) k_mc_black_spmv(Dims g, const double* __restrict__ offd,
+__global__ void __launch_bounds__(32 * NU, MC_MINB) k_mc_black_spmv(Dims g, const double* __restrict__ offd,
                                                            const double* __restrict__ z,
                                                            double* __restrict__ v,
                                                            const double* __restrict__ w0,
@@ -720,14 +777,14 @@ __global__ void __launch_bounds__(32 * NU) k_mc_black_spmv(Dims g, const double*
                                                            int slot0) {
   const int64_t n = g.n;
   const int ls = threadIdx.x, r = threadIdx.y;
-  const int64_t c = (int64_t)blockIdx.x * 32 + ls + g.half;   // black half
+  const int64_t t = (int64_t)blockIdx.x * 32 + ls;   // t-th black cell
   double acc[K];
 #pragma unroll
   for (int k = 0; k < K; ++k) acc[k] = 0.0;
-  if (c < n) {
-    const int64_t cell = cell_of(g, c);
+  if (t < g.half) {
+    const int64_t c = colour_pos(g, 1, t);
     int i, j, k;
-    cell_ijk(g, cell, i, j, k);
+    const int64_t cell = locate(g, c, i, j, k);
     double s = z[r * n + c];
 #pragma unroll
     for (int d = 0; d < NDIR; ++d) {
@@ -743,7 +800,7 @@ __global__ void __launch_bounds__(32 * NU) k_mc_black_spmv(Dims g, const double*
     if (K == 1) acc[0] = s * w0[r * n + c];
     if (K == 2) { acc[0] = s * s; acc[K - 1] = s * w1[r * n + c]; }
   }
-  block_reduce_store_at<K>(acc, partial, stride, slot0 + blockIdx.x);
+  warp_store_at<K>(acc, partial, (int64_t)stride * NU, slot0 + blockIdx.x);
 }
 
 }  // namespace isc
