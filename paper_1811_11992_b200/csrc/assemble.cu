@@ -659,12 +659,19 @@ struct CellView {
     for (int u = 0; u < NU; ++u) v[u] = 0.0;
     if (m == 0) { v[0] = f(R_DY0_P); v[CT] = f(R_DY0_T); v[CSW] = f(R_DY0_SW); }
     else if (m < 1 + NCO) {
+      // m is a run-time row: compare-and-select keeps v in registers
       const int i = m - 1;
-      v[0] = f(R_DYO + 4 * i); v[CT] = f(R_DYO + 4 * i + 1); v[1 + i] = f(R_DYO + 4 * i + 2);
+      v[0] = f(R_DYO + 4 * i); v[CT] = f(R_DYO + 4 * i + 1);
+      const double dx = f(R_DYO + 4 * i + 2);
+#pragma unroll
+      for (int q = 0; q < NCO; ++q)
+        if (q == i) v[1 + q] = dx;
       const double s = f(R_DYO + 4 * i + 3);
       v[CSW] = s; v[CSG] = s;
     } else {
-      v[m] = 1.0;   // gas m: unit partial at its own column
+#pragma unroll
+      for (int u = 0; u < NU; ++u)
+        if (u == m) v[u] = 1.0;   // gas m: unit partial at its own column
     }
   }
   __device__ void dkt(double* v) const {
@@ -675,9 +682,32 @@ struct CellView {
   }
 };
 
+// Structurally non-zero columns of the per-phase partials (record.cuh). The
+// reference accumulates dense 9-vectors; terms whose partials are literal
+// zeros only add +-0 and are skipped here at compile time (the phase loop is
+// unrolled), which also keeps the face kernel's registers in check.
+__host__ __device__ constexpr unsigned colbit(int u) { return 1u << u; }
+constexpr unsigned XCOLS = ((1u << NCO) - 1u) << 1;   // oil x columns
+constexpr unsigned ALLCOLS = (1u << NU) - 1u;
+__host__ __device__ constexpr unsigned m_dpot(int al) {
+  return al == 0 ? colbit(0) | colbit(CSW) : (al == 1 ? colbit(0) : colbit(0) | colbit(CSG));
+}
+__host__ __device__ constexpr unsigned m_dgam(int al) {
+  return al == 0 ? colbit(0) | colbit(CT) : (al == 1 ? colbit(0) | colbit(CT) | XCOLS : ALLCOLS);
+}
+__host__ __device__ constexpr unsigned m_dbeta(int al) {
+  return al == 0 ? colbit(0) | colbit(CT) | colbit(CSW)
+                 : (al == 1 ? colbit(0) | colbit(CT) | colbit(CSW) | colbit(CSG) | XCOLS : ALLCOLS);
+}
+__host__ __device__ constexpr unsigned m_dhph(int al) {
+  return al == 0 ? colbit(CT) : (al == 1 ? colbit(CT) | XCOLS : ALLCOLS);
+}
+constexpr unsigned M_DKT = colbit(0) | colbit(CT) | colbit(CSW) | colbit(CSG) | colbit(CCC);
+
 // Row `row` of one connection's flux and derivative blocks (a = lower cell).
 // Follows conn_eval's accumulation order exactly (_kernels.py:677-771).
-__device__ __forceinline__ void face_row(const int row, const CellView& A_, const CellView& B_,
+template <int row>
+__device__ __forceinline__ void face_row(const CellView& A_, const CellView& B_,
                                          const double* __restrict__ st, int64_t n, int64_t a,
                                          int64_t b, double za, double zb, double gd, double td,
                                          int8_t* upw, int64_t upw_stride, int freeze,
@@ -719,31 +749,43 @@ __device__ __forceinline__ void face_row(const int row, const CellView& A_, cons
     val = b_up * w_up;
     flux += conv * val;
     if (val != 0.0) {
+      const unsigned mpg = m_dpot(al) | m_dgam(al);
       A_.dpot(al, v1); A_.dgam(al, v2);
 #pragma unroll
-      for (int u = 0; u < NU; ++u) dfa[u] += gd * val * (v1[u] - za * v2[u]);
+      for (int u = 0; u < NU; ++u)
+        if (mpg & colbit(u)) dfa[u] += gd * val * (v1[u] - za * v2[u]);
       B_.dpot(al, v1); B_.dgam(al, v2);
 #pragma unroll
-      for (int u = 0; u < NU; ++u) dfb[u] -= gd * val * (v1[u] - zb * v2[u]);
+      for (int u = 0; u < NU; ++u)
+        if (mpg & colbit(u)) dfb[u] -= gd * val * (v1[u] - zb * v2[u]);
     }
-    double* dtgt = up_a ? dfa : dfb;
     const double beta_up = U.f(R_BETA + al);
     U.dbeta(al, v1);
     if (comp_row) {
       if (al == 2) U.dyfull(m, v2);
+      const unsigned mb = al == 2 ? ALLCOLS : (m_dbeta(al) | (al == 1 ? XCOLS : 0u));
 #pragma unroll
       for (int u = 0; u < NU; ++u) {
+        if (!(mb & colbit(u))) continue;
         double dv = v1[u] * w_up;
         if (al == 1 && u == 1 + m) dv += beta_up;
         else if (al == 2) dv += beta_up * v2[u];
-        if (dv != 0.0) dtgt[u] += conv * dv;
+        if (dv != 0.0) {   // upstream side (no pointer select: stays in registers)
+          if (up_a) dfa[u] += conv * dv;
+          else dfb[u] += conv * dv;
+        }
       }
     } else {
       U.dhph(al, v2);
+      const unsigned mh = m_dbeta(al) | m_dhph(al);
 #pragma unroll
       for (int u = 0; u < NU; ++u) {
+        if (!(mh & colbit(u))) continue;
         double dv = v1[u] * w_up + beta_up * v2[u];
-        if (dv != 0.0) dtgt[u] += conv * dv;
+        if (dv != 0.0) {
+          if (up_a) dfa[u] += conv * dv;
+          else dfb[u] += conv * dv;
+        }
       }
     }
   }
@@ -760,6 +802,7 @@ __device__ __forceinline__ void face_row(const int row, const CellView& A_, cons
         B_.dkt(v2);
 #pragma unroll
         for (int u = 0; u < NU; ++u) {
+          if (!(M_DKT & colbit(u))) continue;
           dfa[u] += td * dt_ab * dh_a * v1[u];
           dfb[u] += td * dt_ab * dh_b * v2[u];
         }
@@ -768,23 +811,33 @@ __device__ __forceinline__ void face_row(const int row, const CellView& A_, cons
   }
 }
 
-// grid: (ceil(n/32), 1); block: (32, NU) -> threadIdx.y = residual row
-__global__ void __launch_bounds__(32 * NU, 3) k_face(const FaceArgs F) {
+// Residual row ROW of one cell: walks the six faces in the reference's
+// gather order, accumulating the cell's own derivative into the diagonal row
+// and writing the neighbour's into the off-diagonal block row. The row is a
+// template parameter so each warp (one row) runs code with only its own
+// phases' terms — far fewer live registers than one body for all rows.
+template <int ROW>
+__device__ __forceinline__ void face_cell_row(const FaceArgs& F, int64_t c, int64_t cell, int i,
+                                              int j, int k) {
   const int64_t n = F.g.n;
-  const int64_t c = (int64_t)blockIdx.x * 32 + threadIdx.x;   // storage position
-  const int row = threadIdx.y;
-  if (c >= n) return;
-  int i, j, k;
-  const int64_t cell = locate(F.g, c, i, j, k);
-  double res = F.resid[row * n + c];
+  if (ROW == ROW_OS || ROW == ROW_GS || ROW == ROW_CK) {
+    // no flux terms: resid/diag rows unchanged, off-diagonal rows zero
+#pragma unroll 1
+    for (int d = 0; d < NDIR; ++d) {
+      double* orow = F.offd + (int64_t)((d * NU + ROW) * NU) * n + c;
+#pragma unroll
+      for (int u = 0; u < NU; ++u) orow[(int64_t)u * n] = 0.0;
+    }
+    return;
+  }
+  double res = F.resid[ROW * n + c];
   double drow[NU];
 #pragma unroll
-  for (int u = 0; u < NU; ++u) drow[u] = F.diag[(int64_t)(row * NU + u) * n + c];
-  const CellView C{F.rec, n, c};
+  for (int u = 0; u < NU; ++u) drow[u] = F.diag[(int64_t)(ROW * NU + u) * n + c];
 #pragma unroll 1
   for (int d = 0; d < NDIR; ++d) {
     const int64_t nb = nb_pos(F.g, cell, i, j, k, d);
-    double* orow = F.offd + (int64_t)((d * NU + row) * NU) * n + c;
+    double* orow = F.offd + (int64_t)((d * NU + ROW) * NU) * n + c;
     if (nb < 0) {
 #pragma unroll
       for (int u = 0; u < NU; ++u) orow[(int64_t)u * n] = 0.0;
@@ -795,9 +848,9 @@ __global__ void __launch_bounds__(32 * NU, 3) k_face(const FaceArgs F) {
     const int axis = c_is_a ? d - DXP : 2 - d;   // -z->2, -y->1, -x->0
     const CellView Av{F.rec, n, a}, Bv{F.rec, n, b};
     double flux, dfa[NU], dfb[NU];
-    face_row(row, Av, Bv, F.st, n, a, b, F.depth[a], F.depth[b], F.gd[axis * n + a],
-             F.td[axis * n + a], F.upw + (int64_t)axis * 3 * n, n, F.freeze,
-             c_is_a && row == 0, flux, dfa, dfb);
+    face_row<ROW>(Av, Bv, F.st, n, a, b, F.depth[a], F.depth[b], F.gd[axis * n + a],
+                  F.td[axis * n + a], F.upw + (int64_t)axis * 3 * n, n, F.freeze,
+                  c_is_a && ROW == 0, flux, dfa, dfb);
     if (c_is_a) {
       res += flux;
 #pragma unroll
@@ -808,10 +861,32 @@ __global__ void __launch_bounds__(32 * NU, 3) k_face(const FaceArgs F) {
       for (int u = 0; u < NU; ++u) { drow[u] -= dfb[u]; orow[(int64_t)u * n] = -dfa[u]; }
     }
   }
-  (void)C;
-  F.resid[row * n + c] = res;
+  F.resid[ROW * n + c] = res;
 #pragma unroll
-  for (int u = 0; u < NU; ++u) F.diag[(int64_t)(row * NU + u) * n + c] = drow[u];
+  for (int u = 0; u < NU; ++u) F.diag[(int64_t)(ROW * NU + u) * n + c] = drow[u];
+}
+
+#ifndef FACE_MINB
+#define FACE_MINB 3
+#endif
+
+// grid: (ceil(n/32), 1); block: (32, NU) -> threadIdx.y = residual row
+__global__ void __launch_bounds__(32 * NU, FACE_MINB) k_face(const FaceArgs F) {
+  const int64_t c = (int64_t)blockIdx.x * 32 + threadIdx.x;   // storage position
+  if (c >= F.g.n) return;
+  int i, j, k;
+  const int64_t cell = locate(F.g, c, i, j, k);
+  switch (threadIdx.y) {   // warp-uniform
+    case 0: face_cell_row<0>(F, c, cell, i, j, k); break;
+    case 1: face_cell_row<1>(F, c, cell, i, j, k); break;
+    case 2: face_cell_row<2>(F, c, cell, i, j, k); break;
+    case 3: face_cell_row<3>(F, c, cell, i, j, k); break;
+    case 4: face_cell_row<4>(F, c, cell, i, j, k); break;
+    case 5: face_cell_row<5>(F, c, cell, i, j, k); break;
+    case 6: face_cell_row<6>(F, c, cell, i, j, k); break;
+    case 7: face_cell_row<7>(F, c, cell, i, j, k); break;
+    default: face_cell_row<8>(F, c, cell, i, j, k); break;
+  }
 }
 
 // ------------------------------------------------------------------- wells
