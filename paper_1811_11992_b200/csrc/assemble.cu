@@ -820,16 +820,11 @@ template <int ROW>
 __device__ __forceinline__ void face_cell_row(const FaceArgs& F, int64_t c, int64_t cell, int i,
                                               int j, int k) {
   const int64_t n = F.g.n;
-  if (ROW == ROW_OS || ROW == ROW_GS || ROW == ROW_CK) {
-    // no flux terms: resid/diag rows unchanged, off-diagonal rows zero
-#pragma unroll 1
-    for (int d = 0; d < NDIR; ++d) {
-      double* orow = F.offd + (int64_t)((d * NU + ROW) * NU) * n + c;
-#pragma unroll
-      for (int u = 0; u < NU; ++u) orow[(int64_t)u * n] = 0.0;
-    }
-    return;
-  }
+  // no flux terms in the constraint/coke rows: resid/diag rows unchanged and
+  // their off-diagonal rows are structural zeros, never written (the
+  // decoupling reads only rows < ROW_OS of an assembled system; exports
+  // materialise the zeros)
+  if (ROW == ROW_OS || ROW == ROW_GS || ROW == ROW_CK) return;
   double res = F.resid[ROW * n + c];
   double drow[NU];
 #pragma unroll
@@ -1063,7 +1058,7 @@ __global__ void k_wells(const Model M, Dims g, int nw, const WellDev* __restrict
 __global__ void k_export_system(Dims g, const int64_t* __restrict__ conn_id,
                                 const double* __restrict__ diag, const double* __restrict__ offd,
                                 const double* __restrict__ resid, double* rdiag, double* roffd,
-                                double* rresid) {
+                                double* rresid, int offd_rows) {
   const int64_t n = g.n;
   const int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;   // natural cell
   if (c >= n) return;
@@ -1079,8 +1074,9 @@ __global__ void k_export_system(Dims g, const int64_t* __restrict__ conn_id,
     const int64_t nbp = nb_pos(g, c, i, j, k, dplus);
     const int dminus = opposite(dplus);
     for (int e = 0; e < NB; ++e) {
-      roffd[(ic * 2 + 0) * NB + e] = offd[(int64_t)(dplus * NB + e) * n + pc];
-      roffd[(ic * 2 + 1) * NB + e] = offd[(int64_t)(dminus * NB + e) * n + nbp];
+      const bool live = e / NU < offd_rows;   // rows >= offd_rows are structural zeros
+      roffd[(ic * 2 + 0) * NB + e] = live ? offd[(int64_t)(dplus * NB + e) * n + pc] : 0.0;
+      roffd[(ic * 2 + 1) * NB + e] = live ? offd[(int64_t)(dminus * NB + e) * n + nbp] : 0.0;
     }
   }
 }

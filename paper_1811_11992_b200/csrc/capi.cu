@@ -72,6 +72,7 @@ struct isc_ctx {
   // solver
   int precond = ISC_PRECOND_RAS;
   bool decoupled = false, factored = false;
+  int offd_rows = NU;   // rows of offd holding data (ROW_OS after an un-decoupled assembly)
   double *rhs = nullptr, *xk = nullptr, *rk = nullptr, *rhat = nullptr, *pk = nullptr,
          *vk = nullptr, *phat = nullptr, *shat = nullptr, *sk = nullptr, *tk = nullptr;
   double* sc = nullptr;
@@ -561,6 +562,7 @@ extern "C" int isc_assemble(isc_ctx* ctx, const double* d_state, const double* h
   if (ctx->nw > 0 && h_wells_out) std::memcpy(h_wells_out, ctx->wout_h, ctx->nw * WOUT * 8);
   ctx->decoupled = false;
   ctx->factored = false;
+  ctx->offd_rows = ROW_OS;   // rows ROW_OS.. of the off-diagonal blocks were not written
   return ISC_OK;
 }
 
@@ -648,6 +650,7 @@ extern "C" int isc_assemble_decoupled(isc_ctx* ctx, const double* d_state, const
   }
   ctx->decoupled = true;
   ctx->factored = false;
+  ctx->offd_rows = NU;
   return ISC_OK;
 }
 
@@ -716,7 +719,8 @@ extern "C" int isc_copy_out(isc_ctx* ctx, int32_t what, void* d_dst) {
 
 extern "C" int isc_export_system(isc_ctx* ctx, double* d_diag, double* d_offd, double* d_resid) {
   k_export_system<<<grid1d(ctx->g.n, 128), 128, 0, ctx->stream>>>(
-      ctx->g, ctx->conn_id, ctx->diag, ctx->offd, ctx->resid, d_diag, d_offd, d_resid);
+      ctx->g, ctx->conn_id, ctx->diag, ctx->offd, ctx->resid, d_diag, d_offd, d_resid,
+      ctx->offd_rows);
   LAUNCH_CHECK();
   CK(cudaStreamSynchronize(ctx->stream));
   return ISC_OK;
@@ -734,6 +738,7 @@ extern "C" int isc_import_system(isc_ctx* ctx, const double* d_diag, const doubl
   }
   CK(cudaStreamSynchronize(ctx->stream));
   ctx->decoupled = ctx->factored = false;
+  ctx->offd_rows = NU;
   return ISC_OK;
 }
 
@@ -777,6 +782,7 @@ extern "C" int isc_synth_system(isc_ctx* ctx, uint64_t seed) {
   LAUNCH_CHECK();
   CK(cudaStreamSynchronize(ctx->stream));
   ctx->decoupled = ctx->factored = false;
+  ctx->offd_rows = NU;
   return ISC_OK;
 }
 
@@ -814,8 +820,10 @@ extern "C" int isc_decouple(isc_ctx* ctx, int64_t* bad_cell, int32_t* bad_col) {
   CK(cudaMemsetAsync(ctx->flags, 0, n * 4, st));
   CK(cudaMemsetAsync(ctx->bad_d, 0xff, 8, st));
   k_decouple3<<<grid1d(n, DC3_CELLS), DC3_THREADS, 0, st>>>(ctx->g, ctx->diag, ctx->offd,
-                                                             ctx->rhs, ctx->flags, ctx->bad_d);
+                                                             ctx->rhs, ctx->flags, ctx->bad_d,
+                                                             ctx->offd_rows);
   LAUNCH_CHECK();
+  ctx->offd_rows = NU;   // the decoupled blocks are dense
   }
   CK(cudaMemcpyAsync(ctx->bad_h, ctx->bad_d, 8, cudaMemcpyDeviceToHost, st));
   STAGE(stage_end(ctx, 1));

@@ -240,10 +240,13 @@ __global__ void __launch_bounds__(DC2_CELLS * 64, 2) k_decouple2(Dims g, double*
 //            loads of a warp = 16 consecutive cells of one column.
 constexpr int DC3_CELLS = 16;
 constexpr int DC3_THREADS = 256;
+#ifndef DC3_MINB
+#define DC3_MINB 4
+#endif
 
-__global__ void __launch_bounds__(DC3_THREADS, 3) k_decouple3(Dims g, const double* __restrict__ diag,
+__global__ void __launch_bounds__(DC3_THREADS, DC3_MINB) k_decouple3(Dims g, const double* __restrict__ diag,
                                                           double* offd, double* rhs, int* flags,
-                                                          unsigned long long* bad) {
+                                                          unsigned long long* bad, int offd_rows) {
   __shared__ double inv[NU][NU][DC3_CELLS];   // D^-1 (row, col, cell)
   __shared__ double colk[2][NU][DC3_CELLS];
   __shared__ double cmax[NU][DC3_CELLS];
@@ -363,14 +366,19 @@ __global__ void __launch_bounds__(DC3_THREADS, 3) k_decouple3(Dims g, const doub
       for (int r = 0; r < NU; ++r) base[r * stride] = 0.0;
       continue;
     }
+    // rows >= offd_rows of an assembled (not yet decoupled) off-diagonal block
+    // are structural zeros and were never written: not read, and their
+    // (+-0) terms are left out of the products
+    const int kin = col < NDIR * NU ? offd_rows : NU;
     double v[NU];
 #pragma unroll
-    for (int r = 0; r < NU; ++r) v[r] = base[r * stride];
+    for (int r = 0; r < NU; ++r) v[r] = r < kin ? base[r * stride] : 0.0;
 #pragma unroll
     for (int r = 0; r < NU; ++r) {
       double s = 0.0;
 #pragma unroll
-      for (int k = 0; k < NU; ++k) s += inv[r][k][tc] * v[k];
+      for (int k = 0; k < NU; ++k)
+        if (k < kin) s += inv[r][k][tc] * v[k];
       base[r * stride] = s;
     }
   }
