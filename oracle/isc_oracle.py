@@ -313,8 +313,8 @@ def well_pass(pack, grid, ws, wells, streams, state, capped, t_new):
 
 
 def assemble(grid, model: Model, ws: Workspace, wells, streams, state, accn, dt, t_new,
-             capped, freeze_upwind=False):
-    """assembly.py:561-598 (analytic Jacobian)."""
+             capped, freeze_upwind=False, jacobian="analytic"):
+    """assembly.py:561-598."""
     L = lib()
     pack = model.pack
     n, m, nu = grid.ncell, grid.nconn, pack.nequ
@@ -337,7 +337,289 @@ def assemble(grid, model: Model, ws: Workspace, wells, streams, state, accn, dt,
     L.orc_gather_pass(ctypes.c_int64(n), ctypes.c_int64(nu), _p(ws.adj_ptr), _p(ws.adj_ids),
                       _p(ws.adj_sides), _p(ws.flux), _p(ws.dfa), _p(ws.dfb), _p(ws.resid),
                       _p(ws.diag), _p(ws.offd))
-    return well_pass(pack, grid, ws, wells, streams, state, capped, t_new)
+    blocks = well_pass(pack, grid, ws, wells, streams, state, capped, t_new)
+    if jacobian == "numeric":
+        numeric_jacobian(grid, model, ws, wells, streams, state, accn, dt, t_new, capped,
+                         blocks, freeze_upwind)
+    return blocks
+
+
+# ------------------------------------------------ numeric (FD) Jacobian
+
+FD_REL_STEP, FD_PRESSURE_FLOOR, FD_UNIT_FLOOR = 1e-6, 1e-3, 5e-5   # assembly.py:33-35
+_CELL_FIELDS = ("pot", "dpot", "beta", "dbeta", "hph", "dhph", "yfull", "dyfull", "gam",
+                "dgam", "pcv", "dpcv", "kr3", "dkr3", "ktd", "acc", "dacc", "src", "dsrc")
+_CONN_FIELDS = ("pot", "dpot", "beta", "dbeta", "hph", "dhph", "yfull", "dyfull", "gam",
+                "dgam", "ktd")
+
+
+class _Probe:
+    """One-cell scratch (assembly.py:605-630 _CellBufs) plus two-cell staging
+    arrays for single-connection conn_eval calls."""
+
+    def __init__(self, ws):
+        for f in _CELL_FIELDS:
+            setattr(self, f, np.zeros((1,) + getattr(ws, f).shape[1:]))
+        self.ok = np.zeros(1, dtype=np.uint8)
+        self.pair = {f: np.zeros((2,) + getattr(ws, f).shape[1:]) for f in _CONN_FIELDS}
+        nu = ws.acc.shape[1]
+        self.flux = np.zeros((1, nu))
+        self.dfa, self.dfb = np.zeros((1, nu, nu)), np.zeros((1, nu, nu))
+        self.ca, self.cb = np.zeros(1, np.int32), np.ones(1, np.int32)
+
+
+class _Shadow:
+    """assembly.py:633-667: index [c] of any field resolves to the probe."""
+
+    def __init__(self, probe):
+        self._p = probe
+
+    def __getattr__(self, f):
+        arr = getattr(self._p, f)[0]
+
+        class _One:
+            def __getitem__(self, key):
+                if isinstance(key, tuple):
+                    return arr[key[1:]] if len(key) > 1 else arr
+                return arr
+        return _One()
+
+
+def _eval_cell(model, probe, scal, phi_ref_c):
+    """assembly.py:670-684"""
+    one = lambda v: np.array([v], dtype=np.float64)   # noqa: E731
+    lib().orc_cell_pass(ctypes.byref(model.s), ctypes.c_int64(1), _p(one(scal["p"])),
+                        _p(one(scal["t"])), _p(one(scal["sw"])), _p(one(scal["sg"])),
+                        _p(_c(scal["x"][None, :])), _p(_c(scal["y"][None, :])),
+                        _p(one(scal["cc"])), _p(one(phi_ref_c)),
+                        *[_p(getattr(probe, f)) for f in _CELL_FIELDS], _p(probe.ok))
+    if not probe.ok[0]:
+        raise PoreSpaceExhausted("coke fills the pore volume at a probed state")
+
+
+def _cell_unknowns(state, c, pack):
+    """assembly.py:687-699"""
+    vals = np.empty(pack.nequ)
+    vals[0] = state.p[c]
+    vals[1:1 + pack.nco] = state.x[c]
+    vals[1 + pack.nco:1 + pack.nco + pack.ncg] = state.y[c]
+    ct = 1 + pack.nco + pack.ncg
+    vals[ct], vals[ct + 1], vals[ct + 2], vals[ct + 3] = (state.t[c], state.sw[c],
+                                                          state.sg[c], state.cc[c])
+    return vals
+
+
+def _apply_unknown(scal, u, val, pack):
+    """assembly.py:702-719"""
+    ct = 1 + pack.nco + pack.ncg
+    if u == 0:
+        scal["p"] = val
+    elif u < 1 + pack.nco:
+        scal["x"][u - 1] = val
+    elif u < ct:
+        scal["y"][u - 1 - pack.nco] = val
+    elif u == ct:
+        scal["t"] = val
+    elif u == ct + 1:
+        scal["sw"] = val
+    elif u == ct + 2:
+        scal["sg"] = val
+    else:
+        scal["cc"] = val
+
+
+def _conn_probe(model, probe, ws, grid, state, ic, scal, side_a, freeze):
+    """conn_eval of connection ic with the probed cell on side a (side_a) or
+    b, the other side from the unperturbed workspace (assembly.py:757-790)."""
+    pack = model.pack
+    a, b = int(grid.conn_a[ic]), int(grid.conn_b[ic])
+    other = b if side_a else a
+    slot_p, slot_o = (0, 1) if side_a else (1, 0)
+    for f in _CONN_FIELDS:
+        probe.pair[f][slot_p] = getattr(probe, f)[0]
+        probe.pair[f][slot_o] = getattr(ws, f)[other]
+    t2 = np.empty(2)
+    x2 = np.empty((2, pack.nco))
+    t2[slot_p], t2[slot_o] = scal["t"], state.t[other]
+    x2[slot_p], x2[slot_o] = scal["x"], state.x[other]
+    depth2 = np.array([grid.depth[a], grid.depth[b]], dtype=np.float64)
+    upw = ws.upw[ic:ic + 1].copy()          # probes never store upstream flags
+    lib().orc_conn_pass(ctypes.c_int64(pack.nco), ctypes.c_int64(pack.ncg), ctypes.c_int64(1),
+                        _p(probe.ca), _p(probe.cb), _p(ws.gd[ic:ic + 1].copy()),
+                        _p(ws.td[ic:ic + 1].copy()), _p(depth2), _p(t2), _p(x2),
+                        *[_p(probe.pair[f]) for f in _CONN_FIELDS], _p(upw),
+                        ctypes.c_int(1 if freeze else 0), _p(probe.flux), _p(probe.dfa),
+                        _p(probe.dfb))
+    return probe.flux[0].copy()
+
+
+def _probe_rows(grid, model, ws, wells, streams, state, accn, dt, c, scal, probe, conn_rows,
+                freeze):
+    """assembly.py:722-804: rows of cell c and of its neighbours at a probe."""
+    pack = model.pack
+    row_e = pack.row_energy
+    row_os, row_gs = row_e + 1, row_e + 2
+    _eval_cell(model, probe, scal, model.phi_ref[c])
+    vdt = grid.volume[c] / dt
+    rows = vdt * (probe.acc[0] - accn[c]) - grid.volume[c] * probe.src[0]
+    rows[row_os] = probe.acc[0, row_os]
+    rows[row_gs] = probe.acc[0, row_gs]
+    if ws.hl_area[c] > 0.0:
+        rows[row_e] += ws.hl_area[c] * ws.hl_kob * ((scal["t"] - ws.hl_tini) / ws.hl_d
+                                                    - ws.hl_rho)
+    for slot, k in enumerate(range(ws.adj_ptr[c], ws.adj_ptr[c + 1])):
+        ic = int(ws.adj_ids[k])
+        if ws.adj_sides[k] == 0:
+            flux = _conn_probe(model, probe, ws, grid, state, ic, scal, True, freeze)
+            rows += flux
+            conn_rows[slot] = -flux
+        else:
+            flux = _conn_probe(model, probe, ws, grid, state, ic, scal, False, freeze)
+            rows -= flux
+            conn_rows[slot] = flux.copy()
+    shadow = _Shadow(probe)
+    fw_parts = {}
+    for wix, well in enumerate(wells):
+        for perf in well.perfs:
+            if perf.cell != c:
+                continue
+            dz = perf.z_bh - grid.depth[c]
+            if well.kind == INJECTOR:
+                prow, _, _, qph, _, _ = _perf_injector(pack, shadow, c, streams[wix],
+                                                       state.bhp[wix], perf.wi, dz)
+            else:
+                prow, _, _, qph, _, _ = _perf_producer(pack, shadow, c, scal["x"],
+                                                       state.bhp[wix], perf.wi, dz)
+            rows -= prow
+            fw_parts[wix] = fw_parts.get(wix, 0.0) + qph.sum()
+    return rows, fw_parts
+
+
+def _fd_points(pack, base, u, sw, sg):
+    """assembly.py:807-840"""
+    ct = 1 + pack.nco + pack.ncg
+    v = base[u]
+    if u == 0:
+        h = max(FD_REL_STEP * abs(v), FD_PRESSURE_FLOOR)
+        return v + h, v - h
+    h = max(FD_REL_STEP * abs(v), FD_UNIT_FLOOR)
+    if u == ct:
+        return v + h, v - h
+    if u == ct + 1 or u == ct + 2:
+        if v - h < 0.0:
+            return v + h, v
+        if 1.0 - sw - sg - h < 0.0:
+            return v, v - h
+        return v + h, v - h
+    if u == ct + 3:
+        if v - h < 0.0:
+            return v + h, v
+        return v + h, v - h
+    if v - h < 0.0:
+        return v + h, v
+    if v + h > 1.0:
+        return v, v - h
+    return v + h, v - h
+
+
+def numeric_jacobian(grid, model, ws, wells, streams, state, accn, dt, t_new, capped, blocks,
+                     freeze=False):
+    """assembly.py:843-939: every Jacobian block by finite differences."""
+    pack = model.pack
+    nu = pack.nequ
+    probe = _Probe(ws)
+    rate_wells = {wix for wix, w in enumerate(wells)
+                  if w.control != CTRL_BHP and not capped[wix]}
+    perf_lookup = {}
+    for wix, well in enumerate(wells):
+        for pix, perf in enumerate(well.perfs):
+            perf_lookup.setdefault(perf.cell, []).append((wix, pix))
+    for c in range(grid.ncell):
+        base = _cell_unknowns(state, c, pack)
+        nadj = int(ws.adj_ptr[c + 1] - ws.adj_ptr[c])
+        rows_cp = [np.zeros(nu) for _ in range(nadj)]
+        rows_cm = [np.zeros(nu) for _ in range(nadj)]
+        for u in range(nu):
+            vp, vm = _fd_points(pack, base, u, state.sw[c], state.sg[c])
+            scal = {"p": state.p[c], "t": state.t[c], "sw": state.sw[c], "sg": state.sg[c],
+                    "cc": state.cc[c], "x": np.array(state.x[c], dtype=np.float64),
+                    "y": np.array(state.y[c], dtype=np.float64)}
+            _apply_unknown(scal, u, vp, pack)
+            rows_p, fw_p = _probe_rows(grid, model, ws, wells, streams, state, accn, dt, c,
+                                       scal, probe, rows_cp, freeze)
+            _apply_unknown(scal, u, vm, pack)
+            rows_m, fw_m = _probe_rows(grid, model, ws, wells, streams, state, accn, dt, c,
+                                       scal, probe, rows_cm, freeze)
+            inv2h = 1.0 / (vp - vm)
+            ws.diag[c][:, u] = (rows_p - rows_m) * inv2h
+            for slot, k in enumerate(range(ws.adj_ptr[c], ws.adj_ptr[c + 1])):
+                ic = ws.adj_ids[k]
+                side = 1 if ws.adj_sides[k] == 0 else 0
+                ws.offd[ic, side][:, u] = (rows_cp[slot] - rows_cm[slot]) * inv2h
+            for wix, pix in perf_lookup.get(c, ()):
+                if wix in rate_wells:
+                    blocks[wix].wrow[pix, u] = (fw_p.get(wix, 0.0) - fw_m.get(wix, 0.0)) * inv2h
+                else:
+                    blocks[wix].wrow[pix, u] = 0.0
+    # bhp columns (assembly.py:903-939)
+    for wix, well in enumerate(wells):
+        h = max(FD_REL_STEP * abs(state.bhp[wix]), FD_PRESSURE_FLOOR)
+        for pix, perf in enumerate(well.perfs):
+            c = perf.cell
+            dz = perf.z_bh - grid.depth[c]
+            outs = []
+            for bhp in (state.bhp[wix] + h, state.bhp[wix] - h):
+                if well.kind == INJECTOR:
+                    prow, _, _, qph, _, _ = _perf_injector(pack, ws, c, streams[wix], bhp,
+                                                           perf.wi, dz)
+                else:
+                    prow, _, _, qph, _, _ = _perf_producer(pack, ws, c, state.x[c], bhp,
+                                                           perf.wi, dz)
+                outs.append((prow, qph.sum()))
+            blocks[wix].bcol[pix] = -(outs[0][0] - outs[1][0]) * (0.5 / h)
+        if well.control == CTRL_BHP or capped[wix]:
+            blocks[wix].dwdb = 1.0
+        else:
+            dq = 0.0
+            for pix, perf in enumerate(well.perfs):
+                c = perf.cell
+                dz = perf.z_bh - grid.depth[c]
+                qs = []
+                for bhp in (state.bhp[wix] + h, state.bhp[wix] - h):
+                    if well.kind == INJECTOR:
+                        _, _, _, qph, _, _ = _perf_injector(pack, ws, c, streams[wix], bhp,
+                                                            perf.wi, dz)
+                    else:
+                        _, _, _, qph, _, _ = _perf_producer(pack, ws, c, state.x[c], bhp,
+                                                            perf.wi, dz)
+                    qs.append(qph.sum())
+                dq += (qs[0] - qs[1]) * 0.5 / h
+            blocks[wix].dwdb = dq
+
+
+def check_jacobian(grid, model, ws, wells, streams, state, accn, dt, t_new, capped):
+    """assembly.py:942-982: worst |analytic - numeric| / max(1, |analytic|)."""
+    blocks = assemble(grid, model, ws, wells, streams, state, accn, dt, t_new, capped)
+    diag_a, offd_a = ws.diag.copy(), ws.offd.copy()
+    wrow_a = [b.wrow.copy() for b in blocks]
+    bcol_a = [b.bcol.copy() for b in blocks]
+    dwdb_a = [b.dwdb for b in blocks]
+    numeric_jacobian(grid, model, ws, wells, streams, state, accn, dt, t_new, capped, blocks)
+
+    def scaled(a, n):
+        return np.max(np.abs(a - n) / np.maximum(1.0, np.abs(a))) if a.size else 0.0
+
+    worst = max(scaled(diag_a, ws.diag), scaled(offd_a, ws.offd))
+    for wix, b in enumerate(blocks):
+        worst = max(worst, scaled(wrow_a[wix], b.wrow), scaled(bcol_a[wix], b.bcol),
+                    abs(dwdb_a[wix] - b.dwdb) / max(1.0, abs(dwdb_a[wix])))
+    ws.diag[:] = diag_a
+    ws.offd[:] = offd_a
+    for wix, b in enumerate(blocks):
+        b.wrow[:] = wrow_a[wix]
+        b.bcol[:] = bcol_a[wix]
+        b.dwdb = dwdb_a[wix]
+    return worst
 
 
 # ------------------------------------------------------------ linear solver

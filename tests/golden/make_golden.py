@@ -13,6 +13,10 @@ on seeded inputs that our side regenerates bit-identically
   solve_sub2.npz       32x16x8 grid (2 RAS subdomains): iters + du for each precond
   synth_16.npz         synthetic 16^3 system: iters for each precond, du (ras)
   traj_<case>_<tol>.npz  full runs: per-step records and final fields
+  numjac_small3d.npz   assemble(jacobian="numeric") blocks (free and frozen upwind)
+                       and check_jacobian's worst discrepancy
+
+    python tests/golden/make_golden.py [name ...]   # regenerate only some
 """
 
 import json
@@ -150,6 +154,32 @@ def make_synth():
     np.savez_compressed(os.path.join(HERE, "synth_16.npz"), **out)
 
 
+def make_numjac_small3d():
+    """The reference's finite-difference Jacobian (assembly.py:843-939) and
+    its analytic-vs-numeric check (assembly.py:942-982) at the seeded states
+    of asm_small3d.npz."""
+    sim = reference_simulator(configs.config("small3d"))
+    st, accn = random_state(sim, 5)
+    dt = t_new = 2e-3
+    out = {}
+    blocks = A.assemble(sim.grid, sim.pack, sim.ws, sim.wells, sim.streams, st, accn, dt,
+                        t_new, sim.capped, jacobian="numeric")
+    for f in ("resid", "diag", "offd", "upw"):
+        out[f] = getattr(sim.ws, f).copy()
+    out.update(blocks_dict(blocks))
+    # frozen upwinding at the second state (flags left by the first call)
+    st2, accn2 = random_state(sim, 6)
+    blocks2 = A.assemble(sim.grid, sim.pack, sim.ws, sim.wells, sim.streams, st2, accn2, dt,
+                         t_new, sim.capped, jacobian="numeric", freeze_upwind=True)
+    for f in ("resid", "diag", "offd"):
+        out[f + "2"] = getattr(sim.ws, f).copy()
+    out.update(blocks_dict(blocks2, "w2_"))
+    out["check"] = np.array(A.check_jacobian(sim.grid, sim.pack, sim.ws, sim.wells, sim.streams,
+                                             st, accn, dt, t_new, sim.capped))
+    np.savez_compressed(os.path.join(HERE, "numjac_small3d.npz"), **out)
+    print("check_jacobian", float(out["check"]))
+
+
 def make_traj(name, ltol):
     case = configs.config(name)
     case = replace(case, solver=replace(case.solver, linear_tol=ltol))
@@ -164,10 +194,15 @@ def make_traj(name, ltol):
 
 
 if __name__ == "__main__":
+    if len(sys.argv) > 1:
+        for name in sys.argv[1:]:
+            globals()["make_" + name]()
+        sys.exit(0)
     make_props()
     make_asm_small3d()
     make_solve_sub2()
     make_synth()
+    make_numjac_small3d()
     make_traj("c1", 1e-10)
     make_traj("c1", 1e-5)
     make_traj("c2", 1e-10)
