@@ -135,6 +135,15 @@ int isc_assemble_decoupled(isc_ctx *ctx, const double *d_state, const double *h_
                            const uint8_t *h_capped, int32_t freeze, double *h_wells_out,
                            int64_t *bad_cell);
 
+/* JACOBIAN numeric (assembly.py:593-597, 843-939; replaces the reference's
+ * _numeric_jacobian): every Jacobian block and the well rows (wrow), bhp
+ * columns (bcol) and dwdb of the last isc_assemble / isc_assemble_host are
+ * replaced by central finite differences at the same inputs (probe points of
+ * _fd_points, assembly.py:807-840); residuals keep the analytic pass's values.
+ * h_wells_out as in isc_assemble. ISC_PORE_SPACE_EXHAUSTED if a probed state
+ * exhausts the pore space (assembly.py:682-684), *bad_cell = lowest cell. */
+int isc_numeric_jacobian(isc_ctx *ctx, double *h_wells_out, int64_t *bad_cell);
+
 /* Copy an internal per-cell array to d_dst: 0 resid (9 x n), 1 acc (9 x n),
  * 2 src (9 x n), 3 yfull (5 x n), 4 record (ISC_NREC x n), 5 upwind flags
  * int8 (3 axes x 3 phases x n). */

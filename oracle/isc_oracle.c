@@ -744,7 +744,7 @@ void orc_cell_pass(const OrcModel *M, int64_t n, const double *p, const double *
                    double *pcv, double *dpcv, double *kr3, double *dkr3, double *ktd,
                    double *acc, double *dacc, double *src, double *dsrc, uint8_t *ok) {
   const int64_t nco = M->nco, ncg = M->ncg, nf = 1 + nco + ncg, nu = nco + ncg + 5;
-#pragma omp parallel for schedule(static)
+#pragma omp parallel for schedule(static) if (n > 256)
   for (int64_t c = 0; c < n; ++c) {
     CellOut O = {pot + 3 * c, dpot + 3 * nu * c, beta + 3 * c, dbeta + 3 * nu * c,
                  hph + 3 * c, dhph + 3 * nu * c, yfull + nf * c, dyfull + nf * nu * c,
@@ -888,7 +888,7 @@ void orc_conn_pass(int64_t nco, int64_t ncg, int64_t m, const int32_t *ca, const
                    const double *dgam, const double *ktd, int8_t *upw, int freeze, double *flux,
                    double *dfa, double *dfb) {
   const int64_t nf = 1 + nco + ncg, nu = nco + ncg + 5;
-#pragma omp parallel for schedule(static)
+#pragma omp parallel for schedule(static) if (m > 256)
   for (int64_t ic = 0; ic < m; ++ic) {
     int64_t a = ca[ic], b = cb[ic];
     conn_eval((int)nco, (int)ncg, gd[ic], td[ic], depth[a], depth[b], t_state[a], t_state[b],

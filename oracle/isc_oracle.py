@@ -940,7 +940,9 @@ class Simulator:
     schedule, solver settings) instead of a deck.
     """
 
-    def __init__(self, grid, pack, wells, streams, state, schedule, solver, heat_loss=None):
+    def __init__(self, grid, pack, wells, streams, state, schedule, solver, heat_loss=None,
+                 jacobian="analytic"):
+        self.jacobian = jacobian   # newton.py:228
         self.grid, self.pack, self.wells, self.streams = grid, pack, tuple(wells), streams
         self.schedule, self.solver_cfg = schedule, solver
         self.model = Model(pack)
@@ -973,7 +975,7 @@ class Simulator:
             t0 = _time.perf_counter()
             blocks = assemble(grid, self.model, self.ws, self.wells, self.streams, work,
                               self.accn, dt, t_new, capped,
-                              freeze_upwind=(it > FREEZE_UPWIND_AFTER))
+                              freeze_upwind=(it > FREEZE_UPWIND_AFTER), jacobian=self.jacobian)
             self.work_seconds += _time.perf_counter() - t0
             norm = scaled_norm(self.ws, self.accn, grid.volume, dt, blocks, self.wells, capped,
                                pack.row_energy + 1, pack.row_energy + 2)

@@ -67,6 +67,7 @@ _SIGS = {
     "isc_assemble_host": (ctypes.c_int, [VP, VP, VP, VP, VP, VP, VP, VP, VP, VP, ctypes.c_double,
                                          ctypes.c_double, VP, ctypes.c_int32, VP, c_int64_p]),
     "isc_download_du": (ctypes.c_int, [VP, VP]),
+    "isc_numeric_jacobian": (ctypes.c_int, [VP, VP, c_int64_p]),
     "isc_copy_out": (ctypes.c_int, [VP, ctypes.c_int32, VP]),
     "isc_export_system": (ctypes.c_int, [VP, VP, VP, VP]),
     "isc_import_system": (ctypes.c_int, [VP, VP, VP, VP, VP]),

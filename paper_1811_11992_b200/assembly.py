@@ -134,9 +134,9 @@ class Workspace:
 
 def assemble(grid, pack, ws, wells, streams, state, accn, dt, t_new, capped,
              jacobian="analytic", freeze_upwind=False) -> List[WellBlock]:
-    """Residual and analytic Jacobian at ``state`` (assembly.py:561-598)."""
-    if jacobian != "analytic":
-        raise NotImplementedError("numeric (finite-difference) Jacobian is not on the GPU path")
+    """Residual and Jacobian at ``state`` (assembly.py:561-598); with
+    ``jacobian == "numeric"`` every block is then replaced by the
+    finite-difference Jacobian (assembly.py:593-597, 843-939) on the device."""
     ctx = ws.bind(wells, streams)
     ws._invalidate()
     if isinstance(getattr(state, "p", None), np.ndarray) and not isinstance(accn, torch.Tensor):
@@ -148,5 +148,29 @@ def assemble(grid, pack, ws, wells, streams, state, accn, dt, t_new, capped,
         d_accn = accn if isinstance(accn, torch.Tensor) else soa_from_rows(accn, ctx.device)
         bhp = np.asarray(state.bhp, dtype=np.float64)
         wout = ctx.assemble(d_state, bhp, d_accn, dt, t_new, capped, freeze_upwind)
+    if jacobian == "numeric":
+        wout = ctx.numeric_jacobian()
     ws.last_wout = wout
     return blocks_from_wout(wells, wout)
+
+
+def check_jacobian(grid, pack, ws, wells, streams, state, accn, dt, t_new, capped) -> float:
+    """Worst |analytic - numeric| / max(1, |analytic|) over the diagonal,
+    off-diagonal and well blocks (assembly.py:942-982); ``ws`` is left holding
+    the analytic system, as in the reference."""
+    blocks = assemble(grid, pack, ws, wells, streams, state, accn, dt, t_new, capped)
+    diag_a, offd_a = ws.diag.copy(), ws.offd.copy()
+    ctx = ws.bind(wells, streams)
+    ws._invalidate()
+    nblocks = blocks_from_wout(wells, ctx.numeric_jacobian())
+
+    def scaled(a, b):
+        return float(np.max(np.abs(a - b) / np.maximum(1.0, np.abs(a)))) if a.size else 0.0
+
+    worst = max(scaled(diag_a, ws.diag), scaled(offd_a, ws.offd))
+    for b, nb in zip(blocks, nblocks):
+        worst = max(worst, scaled(b.wrow, nb.wrow), scaled(b.bcol, nb.bcol),
+                    abs(b.dwdb - nb.dwdb) / max(1.0, abs(b.dwdb)))
+    # restore the analytic system (the reference copies its blocks back)
+    assemble(grid, pack, ws, wells, streams, state, accn, dt, t_new, capped)
+    return worst

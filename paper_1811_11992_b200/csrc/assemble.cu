@@ -46,15 +46,41 @@ struct CellArgs {
   unsigned long long* bad;             // min index of a pore-space-exhausted cell
 };
 
-__global__ void __launch_bounds__(128) k_cell(const Model M, const CellArgs A) {
-  const int64_t n = A.g.n;
-  const int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (c >= n) return;
-  const double* rk = M.rockp;
+// Where one cell evaluation's outputs go. The analytic pass stores them in
+// the workspace arrays; a finite-difference probe keeps the record fields
+// and residual rows in registers and drops every analytic partial (dead code
+// after inlining).
+struct CellSinkGlobal {
+  const CellArgs& A;
+  int64_t n, c;
+  __device__ double& rec(int f) { return A.rec[(int64_t)f * n + c]; }
+  __device__ void acc(int r, double v) { A.acc[r * n + c] = v; }
+  __device__ void src(int r, double v) { A.src[r * n + c] = v; }
+  __device__ void diag(int r, int u, double v) { A.diag[(int64_t)(r * NU + u) * n + c] = v; }
+  __device__ void resid(int r, double v) { A.resid[r * n + c] = v; }
+  __device__ void fail() { atomicMin(A.bad, (unsigned long long)cell_of(A.g, c)); }
+};
 
-  double u_[NU];
-#pragma unroll
-  for (int u = 0; u < NU; ++u) u_[u] = A.st[u * n + c];
+struct CellSinkProbe {
+  double v[NREC];      // record fields at the probed state
+  double rows[NU];     // residual rows of the cell part (compose)
+  bool failed = false;
+  __device__ double& rec(int f) { return v[f]; }
+  __device__ void acc(int, double) {}
+  __device__ void src(int, double) {}
+  __device__ void diag(int, int, double) {}
+  __device__ void resid(int r, double x) { rows[r] = x; }
+  __device__ void fail() { failed = true; }
+  __device__ double f(int k) const { return v[k]; }   // record accessor (flux, wells)
+};
+
+// cell_eval + compose for the cell at position c with unknowns u_
+// (_kernels.py:66-610, 797-825); inputs other than the unknowns from A.
+template <class S>
+__device__ __forceinline__ void cell_eval(const Model& M, const CellArgs& A, int64_t c,
+                                          const double (&u_)[NU], S& s) {
+  const int64_t n = A.g.n;
+  const double* rk = M.rockp;
   const double p = u_[0], t = u_[CT], sw = u_[CSW], sg = u_[CSG], cc = u_[CCC];
   double x[NCO], y[NCG];
 #pragma unroll
@@ -70,10 +96,9 @@ __global__ void __launch_bounds__(128) k_cell(const Model M, const CellArgs A) {
   double phif, dphif_cc;
   if (rho_coke > 0.0 && isfinite(rho_coke)) { phif = phi - cc / rho_coke; dphif_cc = -1.0 / rho_coke; }
   else { phif = phi; dphif_cc = 0.0; }
-  if (phif <= 0.0) { atomicMin(A.bad, (unsigned long long)cell_of(A.g, c)); return; }
+  if (phif <= 0.0) { s.fail(); return; }
   const double t_ref = rk[RK_TREF], eps_per = rk[RK_EPS_PER];
-  double* rec = A.rec;
-#define REC(f) rec[(int64_t)(f) * n + c]
+#define REC(f) s.rec(f)
 
   // water (_kernels.py:139-156)
   double rw, drw_p, drw_t, muw, dmuw_t, hgw, dhgw_t, hvw, dhvw_t;
@@ -566,25 +591,36 @@ __global__ void __launch_bounds__(128) k_cell(const Model M, const CellArgs A) {
         }
       }
     }
-    A.acc[r * n + c] = accr;
-    A.src[r * n + c] = srcr;
+    s.acc(r, accr);
+    s.src(r, srcr);
     double res;
     if (r == ROW_OS || r == ROW_GS) {
       res = accr;
 #pragma unroll
-      for (int u = 0; u < NU; ++u) A.diag[(int64_t)(r * NU + u) * n + c] = dacc[u];
+      for (int u = 0; u < NU; ++u) s.diag(r, u, dacc[u]);
     } else {
       res = vdt * (accr - A.accn[r * n + c]) - vol * srcr;
 #pragma unroll
       for (int u = 0; u < NU; ++u) {
         double dv = vdt * dacc[u] - vol * dsrc[u];
         if (r == ROW_E && u == ROW_E && hl > 0.0) dv += hl * A.hl_kob / A.hl_d;
-        A.diag[(int64_t)(r * NU + u) * n + c] = dv;
+        s.diag(r, u, dv);
       }
     }
     if (r == ROW_E && hl > 0.0) res += hl * A.hl_kob * ((t - A.hl_tini) / A.hl_d - A.hl_rho);
-    A.resid[r * n + c] = res;
+    s.resid(r, res);
   }
+}
+
+__global__ void __launch_bounds__(128) k_cell(const Model M, const CellArgs A) {
+  const int64_t n = A.g.n;
+  const int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (c >= n) return;
+  double u_[NU];
+#pragma unroll
+  for (int u = 0; u < NU; ++u) u_[u] = A.st[u * n + c];
+  CellSinkGlobal s{A, n, c};
+  cell_eval(M, A, c, u_, s);
 }
 
 // -------------------------------------------------------------------- face

@@ -15,6 +15,7 @@
 #include "fused.cu"
 #include "comm.cuh"
 #include "newton.cu"
+#include "numjac.cu"
 #include "solver.cu"
 
 using namespace isc;
@@ -73,6 +74,9 @@ struct isc_ctx {
   int precond = ISC_PRECOND_RAS;
   bool decoupled = false, factored = false;
   int offd_rows = NU;   // rows of offd holding data (ROW_OS after an un-decoupled assembly)
+  bool assembled = false;   // the last assembly was isc_assemble (inputs kept for FD)
+  double asm_dt = 0.0;
+  int asm_freeze = 0;
   double *rhs = nullptr, *xk = nullptr, *rk = nullptr, *rhat = nullptr, *pk = nullptr,
          *vk = nullptr, *phat = nullptr, *shat = nullptr, *sk = nullptr, *tk = nullptr;
   double* sc = nullptr;
@@ -510,6 +514,7 @@ extern "C" int isc_assemble(isc_ctx* ctx, const double* d_state, const double* h
                             int64_t* bad_cell) {
   const int64_t n = ctx->g.n;
   cudaStream_t st = ctx->stream;
+  ctx->assembled = false;
   STAGE(stage_begin(ctx, 0));
   if (ctx->nw > 0) {
     CK(cudaMemcpyAsync(ctx->bhp_d, h_bhp, ctx->nw * 8, cudaMemcpyHostToDevice, st));
@@ -563,6 +568,47 @@ extern "C" int isc_assemble(isc_ctx* ctx, const double* d_state, const double* h
   ctx->decoupled = false;
   ctx->factored = false;
   ctx->offd_rows = ROW_OS;   // rows ROW_OS.. of the off-diagonal blocks were not written
+  ctx->assembled = true;
+  ctx->asm_dt = dt;
+  ctx->asm_freeze = freeze;
+  return ISC_OK;
+}
+
+extern "C" int isc_numeric_jacobian(isc_ctx* ctx, double* h_wells_out, int64_t* bad_cell) {
+  if (!ctx->assembled || ctx->decoupled) {
+    g_err = "isc_numeric_jacobian needs the system of the last isc_assemble";
+    return ISC_BAD_ARGUMENT;
+  }
+  const int64_t n = ctx->g.n;
+  cudaStream_t st = ctx->stream;
+  CK(cudaMemsetAsync(ctx->bad_d, 0xff, 8, st));
+  CellArgs A{ctx->g, ctx->st_c, ctx->phi_ref, ctx->vol, ctx->hl_area, ctx->hl_kob, ctx->hl_d,
+             ctx->hl_rho, ctx->hl_tini, ctx->accn_c, ctx->asm_dt, nullptr, nullptr, nullptr,
+             nullptr, nullptr, ctx->bad_d};
+  NumJacArgs J{A, ctx->rec, ctx->depth, ctx->gd, ctx->td, ctx->upw, ctx->asm_freeze,
+               ctx->diag, ctx->offd, ctx->nw, ctx->wells_d, ctx->bhp_d, ctx->capped_d,
+               ctx->wout_d, ctx->bad_d};
+  k_numjac<<<grid1d(n, 32), dim3(32, NU), 0, st>>>(ctx->M, J);
+  LAUNCH_CHECK();
+  if (ctx->nw > 0) {
+    k_numjac_wells<<<1, 32, 0, st>>>(ctx->M, ctx->g, ctx->nw, ctx->wells_d, ctx->st_c,
+                                     ctx->bhp_d, ctx->capped_d, ctx->rec, ctx->depth,
+                                     ctx->wout_d);
+    LAUNCH_CHECK();
+    CK(cudaMemcpyAsync(ctx->wout_h, ctx->wout_d, ctx->nw * WOUT * 8, cudaMemcpyDeviceToHost, st));
+  }
+  CK(cudaMemcpyAsync(ctx->bad_h, ctx->bad_d, 8, cudaMemcpyDeviceToHost, st));
+  CK(cudaStreamSynchronize(st));
+  ctx->offd_rows = NU;   // every row of every block written
+  double flag = *ctx->bad_h != ~0ULL ? 1.0 : 0.0;
+  int as = isc_comm_allreduce_host(ctx, &flag, 1, 1);
+  if (as) return as;
+  if (flag > 0.0) {
+    if (bad_cell) *bad_cell = *ctx->bad_h != ~0ULL ? (int64_t)*ctx->bad_h : -1;
+    g_err = "coke fills the pore volume at a probed state";
+    return ISC_PORE_SPACE_EXHAUSTED;
+  }
+  if (ctx->nw > 0 && h_wells_out) std::memcpy(h_wells_out, ctx->wout_h, ctx->nw * WOUT * 8);
   return ISC_OK;
 }
 
@@ -651,6 +697,7 @@ extern "C" int isc_assemble_decoupled(isc_ctx* ctx, const double* d_state, const
   ctx->decoupled = true;
   ctx->factored = false;
   ctx->offd_rows = NU;
+  ctx->assembled = false;
   return ISC_OK;
 }
 
@@ -739,6 +786,7 @@ extern "C" int isc_import_system(isc_ctx* ctx, const double* d_diag, const doubl
   CK(cudaStreamSynchronize(ctx->stream));
   ctx->decoupled = ctx->factored = false;
   ctx->offd_rows = NU;
+  ctx->assembled = false;
   return ISC_OK;
 }
 
@@ -783,6 +831,7 @@ extern "C" int isc_synth_system(isc_ctx* ctx, uint64_t seed) {
   CK(cudaStreamSynchronize(ctx->stream));
   ctx->decoupled = ctx->factored = false;
   ctx->offd_rows = NU;
+  ctx->assembled = false;
   return ISC_OK;
 }
 

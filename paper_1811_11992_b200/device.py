@@ -168,6 +168,14 @@ class DeviceContext:
         N.check(st, "isc_assemble", bad_cell=bad.value)
         return self.wout[:self.nw].copy()
 
+    def numeric_jacobian(self):
+        """isc_numeric_jacobian: finite-difference blocks at the inputs of the
+        last assemble (assembly.py:843-939); returns the well outputs."""
+        bad = ctypes.c_int64(-1)
+        st = self.L.isc_numeric_jacobian(self.h, N.ptr(self.wout), ctypes.byref(bad))
+        N.check(st, "isc_numeric_jacobian", bad_cell=bad.value)
+        return self.wout[:self.nw].copy()
+
     def assemble_host(self, state, accn, dt, t_new, capped, freeze):
         """isc_assemble_host: the reference's State arrays and accn (n, 9) on
         the host; copies + transposes happen in the library."""

@@ -106,11 +106,15 @@ class Simulator:
     """Device-resident mirror of the reference ``Simulator`` (newton.py:214-437)."""
 
     def __init__(self, grid, pack, wells, streams, state, schedule, solver, heat_loss=None,
-                 fused: bool = False, comm_setup=None, own_stream: bool = False):
+                 fused: bool = False, comm_setup=None, own_stream: bool = False,
+                 jacobian: str = "analytic"):
         self.grid, self.pack = grid, pack
         self.wells, self.streams = tuple(wells), tuple(streams)
         self.schedule, self.solver_cfg = schedule, solver
         self.fused = fused   # assemble+Schur+decoupling in one kernel (fused.cu)
+        self.jacobian = jacobian   # "numeric": FD blocks every iteration (newton.py:228,278)
+        if jacobian == "numeric" and fused:
+            raise ValueError("the fused assemble+decouple path has no numeric-Jacobian mode")
         self.ctx = DeviceContext(grid, pack, self.wells, self.streams, solver.precond, heat_loss,
                                  own_stream=own_stream)
         if comm_setup is not None:   # z-slab rank: window + NCCL/hub transport
@@ -124,7 +128,7 @@ class Simulator:
         zero = torch.zeros(NU, grid.ncell, dtype=torch.float64, device=dev)
         self._torch_sync()
         self.blocks: List[WellBlock] = self._assemble(self.state, zero, 1.0, 0.0, self.capped,
-                                                      False)
+                                                      False, analytic=True)
         self.accn = self.ctx.copy_out(1, NU)
         self.steps: List[StepRecord] = []
         self.cum_rates = np.zeros((len(self.wells), 3))
@@ -140,8 +144,10 @@ class Simulator:
         if self.own_stream:
             torch.cuda.current_stream().synchronize()
 
-    def _assemble(self, st: DeviceState, accn, dt, t_new, capped, freeze):
+    def _assemble(self, st: DeviceState, accn, dt, t_new, capped, freeze, analytic=False):
         wout = self.ctx.assemble(st.u, st.bhp, accn, dt, t_new, capped, freeze, fused=self.fused)
+        if self.jacobian == "numeric" and not analytic:
+            wout = self.ctx.numeric_jacobian()
         return blocks_from_wout(self.wells, wout)
 
     def scaled_norm(self, blocks, dt, capped) -> float:

@@ -180,16 +180,22 @@ def make_numjac_small3d():
     print("check_jacobian", float(out["check"]))
 
 
-def make_traj(name, ltol):
+def make_traj_numeric():
+    """C1 run in JACOBIAN numeric mode (newton.py:228, 278)."""
+    make_traj("c1", 1e-10, jacobian="numeric")
+
+
+def make_traj(name, ltol, jacobian=None):
     case = configs.config(name)
     case = replace(case, solver=replace(case.solver, linear_tol=ltol))
-    sim = reference_simulator(case, threads=4)
+    sim = reference_simulator(case, threads=4, jacobian=jacobian)
     sim.advance()
     rec = np.array([(s.time, s.dt, s.newton, s.linear, s.solves, s.balance)
                     for s in sim.steps])
     out = {"steps": rec, "cum_imbalance": np.array(sim.cumulative_imbalance()),
            **state_dict(sim.state, "final_")}
-    np.savez_compressed(os.path.join(HERE, f"traj_{name}_{ltol:.0e}.npz"), **out)
+    tag = "" if jacobian is None else f"_{jacobian}"
+    np.savez_compressed(os.path.join(HERE, f"traj_{name}_{ltol:.0e}{tag}.npz"), **out)
     print(name, ltol, sim.totals())
 
 
@@ -203,6 +209,7 @@ if __name__ == "__main__":
     make_solve_sub2()
     make_synth()
     make_numjac_small3d()
+    make_traj_numeric()
     make_traj("c1", 1e-10)
     make_traj("c1", 1e-5)
     make_traj("c2", 1e-10)

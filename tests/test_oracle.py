@@ -16,6 +16,8 @@ import json
 import math
 import os
 
+from dataclasses import replace
+
 import numpy as np
 import pytest
 
@@ -254,6 +256,21 @@ def test_synthetic_microbench_vs_reference():
         assert it == int(s[pc + "_iters"]), pc
         if pc == "ras":
             np.testing.assert_array_equal(du, s["ras_du"])
+
+
+def test_numeric_jacobian_run_prefix_vs_reference():
+    """JACOBIAN numeric mode (newton.py:228,278): the first 4 steps of the
+    reference's C1 run reproduced exactly (the Python-driven FD oracle is too
+    slow for the whole run here; the GPU test runs all 50 steps)."""
+    g = golden("traj_c1_1e-10_numeric.npz")
+    c = case_objects("c1", linear_tol=1e-10)
+    k = 4
+    sched = replace(c.case.schedule, t_end=float(g["steps"][k - 1, 0]))
+    sim = O.Simulator(c.grid, c.pack, c.wells, c.streams, c.state, sched, c.case.solver,
+                      jacobian="numeric")
+    sim.advance()
+    rec = np.array([(s.time, s.dt, s.newton, s.linear, s.solves) for s in sim.steps])
+    np.testing.assert_array_equal(rec, g["steps"][:k, :5])
 
 
 @pytest.mark.parametrize("name,tol", [("c1", 1e-10), ("c1", 1e-5), ("c2", 1e-10)])

@@ -149,7 +149,7 @@ def case_to_deck(case) -> str:
     return "\n".join(out)
 
 
-def reference_simulator(case, threads: int = 1):
+def reference_simulator(case, threads: int = 1, jacobian=None):
     """Reference ``Simulator`` for a case with the per-cell porosity patch."""
     import_reference()
     import iscsim.newton as nw
@@ -166,7 +166,7 @@ def reference_simulator(case, threads: int = 1):
 
     nw.build_grid = patched
     try:
-        sim = nw.Simulator(deck, threads=threads)
+        sim = nw.Simulator(deck, threads=threads, jacobian=jacobian)
     finally:
         nw.build_grid = orig
     return sim
