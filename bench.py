@@ -473,6 +473,36 @@ def run_oracle(steps, warmup, budget_s=None):
             "seconds": el}
 
 
+def run_numjac(config="c4", reps=3):
+    """JACOBIAN numeric (assembly.py:843-939) at the C4 initial
+    state — 2 probes x 9 unknowns per cell, each a full cell_eval + six face
+    fluxes — timed with CUDA events after one analytic assemble."""
+    import torch
+    from paper_1811_11992_b200 import configs
+    from paper_1811_11992_b200.device import DeviceContext, state_to_device
+    case = configs.config(config)
+    grid, pack, wells, streams, state = configs.build_case(case)
+    ctx = DeviceContext(grid, pack, wells, streams, "none")
+    d_state = state_to_device(state, ctx.device)
+    zero = torch.zeros(9, grid.ncell, dtype=torch.float64, device=ctx.device)
+    ctx.assemble(d_state, state.bhp, zero, 1.0, 0.0, np.zeros(len(wells), bool), False)
+    acc = ctx.copy_out(1, 9).clone()
+    ctx.assemble(d_state, state.bhp, acc, 2e-3, 2e-3, np.zeros(len(wells), bool), False)
+    ctx.numeric_jacobian()   # warm-up
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    torch.cuda.synchronize()
+    e0.record()
+    for _ in range(reps):
+        ctx.numeric_jacobian()
+    e1.record()
+    torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1) / reps
+    ctx.close()
+    return {"config": config, "cells": grid.ncell, "ms": ms,
+            "cells_per_s": grid.ncell / (ms / 1e3),
+            "probes_per_s": 18 * grid.ncell / (ms / 1e3)}
+
+
 def main():
     args = parse()
     rank, world, local = dist_setup(args.gpus)
@@ -516,6 +546,11 @@ def main():
                 out["spmv_c5"] = run_spmv_c5()
             except Exception as exc:  # report, never hide
                 out["spmv_c5"] = {"error": repr(exc)}
+        if not args.no_spmv:
+            try:
+                out["numeric_jacobian_c4"] = run_numjac(args.config)
+            except Exception as exc:  # report, never hide
+                out["numeric_jacobian_c4"] = {"error": repr(exc)}
         if not args.no_cpu_baseline:
             cb = run_oracle(steps=3, warmup=0, budget_s=25.0)
             out["cpu_baseline"] = {k: cb[k] for k in ("value", "unit", "cores", "kind", "sample")}
