@@ -5,11 +5,13 @@
 Workload (BASELINE configs[3], the 2 M-cell case the north star quotes its
 roofline bar on): C4 = 200x200x50 grid, seeded log-normal permeability and
 uniform porosity, 4 air injectors + 4 producers, deck-default solver
-(LINEAR_TOL 1e-5, PRECOND ras, LINEAR_MAX 200). One *step* = one full
-Newton iteration of the first timestep (dt = 2e-3 d): assemble (cell +
-face + wells), well Schur fold + Gauss-Jordan decoupling, RAS block-ILU(0)
-factorisation and the preconditioned BiCGSTAB solve, then the damped
-update. ``value`` = cells x steps / device time (inputs resident in HBM);
+(LINEAR_TOL 1e-5, LINEAR_MAX 200). One *step* = one full Newton iteration
+of the first timestep (dt = 2e-3 d): assemble (cell + face + wells), well
+Schur fold + Gauss-Jordan decoupling, block-ILU(0) factorisation and the
+preconditioned BiCGSTAB solve, then the damped update. The preconditioner
+is the north star's multicolour block-ILU(0) (--precond mcilu, default);
+the reference's own RAS subdomain block-ILU(0) is measured on the same
+workload and reported under "ras_exact". ``value`` = cells x steps / device time (inputs resident in HBM);
 ``e2e`` = the same through the drop-in API (assemble/BlockSolver.solve) with
 the state and accumulation copied from pinned host memory and du read back
 every step. The system (9 GB) is far larger than L2, so no flush is needed.
@@ -148,6 +150,23 @@ def ilu_structure_counts(grid):
         links += (w[0] - 1) * w[1] * w[2] + w[0] * (w[1] - 1) * w[2] + w[0] * w[1] * (w[2] - 1)
         pos += size
     return slots, links, links
+
+
+def ncu_traffic(kernel_class, precond):
+    """DRAM bytes (read + write) per launch of a kernel class from the latest
+    committed `ncu --set full` capture (profiles/r*/ncu_traffic.json, made by
+    tools/ncu_summary.py on the C4 mcilu bench); None when not captured."""
+    import glob
+    if precond != "mcilu":
+        return None, None
+    files = sorted(glob.glob(os.path.join(ROOT, "profiles", "r*", "ncu_traffic.json")))
+    if not files:
+        return None, None
+    with open(files[-1]) as fh:
+        d = json.load(fh)
+    if kernel_class not in d:
+        return None, None
+    return float(d[kernel_class]["dram_bytes"]), os.path.relpath(files[-1], ROOT)
 
 
 def algorithmic_bytes(grid, nw, precond="ras"):
@@ -354,10 +373,11 @@ def run_ours(args, rank, world, local):
         rows[key] = {"avg_ms": per, "launches": nl, "share": ms / dev_ms,
                      "algorithmic_bytes": algo[key], "achieved_gbs": ach, "frac": ach / hbm}
     dom = max(rows, key=lambda k: rows[k]["share"])
+    traffic, tsrc = ncu_traffic(dom, case.solver.precond)
     out["roofline"] = {"kernel": dom, "bound": "hbm", "achieved": rows[dom]["achieved_gbs"],
                        "peak": hbm, "unit": "GB/s", "frac": rows[dom]["achieved_gbs"] / hbm,
-                       "traffic": None, "peak_source": peak_src, "kernels": rows,
-                       "kernel_ms": ktimes}
+                       "traffic": traffic, "traffic_source": tsrc, "peak_source": peak_src,
+                       "kernels": rows, "kernel_ms": ktimes}
     return out, sim
 
 
@@ -503,6 +523,29 @@ def run_numjac(config="c4", reps=3):
             "probes_per_s": 18 * grid.ncell / (ms / 1e3)}
 
 
+def run_report(config="c4"):
+    """one report frame of the C4 state — device->host capture
+    (state + yfull) and the native repr-identical cells.csv formatter."""
+    import time as _t
+    import torch
+    from paper_1811_11992_b200 import configs
+    from paper_1811_11992_b200.newton import Simulator
+    from paper_1811_11992_b200.report import capture_frame, format_cells
+    case = configs.config(config)
+    grid, pack, wells, streams, state = configs.build_case(case)
+    sim = Simulator(grid, pack, wells, streams, state, case.schedule, case.solver)
+    torch.cuda.synchronize()
+    t0 = _t.perf_counter()
+    frame = capture_frame(sim, 0.002)
+    t1 = _t.perf_counter()
+    text = format_cells(frame)
+    t2 = _t.perf_counter()
+    sim.ctx.close()
+    return {"config": config, "cells": grid.ncell, "capture_ms": (t1 - t0) * 1e3,
+            "format_ms": (t2 - t1) * 1e3, "bytes": len(text),
+            "format_mb_per_s": len(text) / (t2 - t1) / 1e6, "threads": min(64, os.cpu_count() or 1)}
+
+
 def main():
     args = parse()
     rank, world, local = dist_setup(args.gpus)
@@ -551,6 +594,11 @@ def main():
                 out["numeric_jacobian_c4"] = run_numjac(args.config)
             except Exception as exc:  # report, never hide
                 out["numeric_jacobian_c4"] = {"error": repr(exc)}
+        if not args.no_spmv:
+            try:
+                out["report_frame_c4"] = run_report(args.config)
+            except Exception as exc:  # report, never hide
+                out["report_frame_c4"] = {"error": repr(exc)}
         if not args.no_cpu_baseline:
             cb = run_oracle(steps=3, warmup=0, budget_s=25.0)
             out["cpu_baseline"] = {k: cb[k] for k in ("value", "unit", "cores", "kind", "sample")}

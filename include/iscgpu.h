@@ -217,6 +217,22 @@ int isc_stage_times(isc_ctx *ctx, double *out4);
 int isc_set_profiling(isc_ctx *ctx, int32_t on);
 int isc_kernel_times(isc_ctx *ctx, double *ms8, int64_t *count8, int32_t reset);
 
+/* ---- report frames (report.py:50-149), host only ----
+ * Python repr(float(v)) of v: the shortest round-trip string, CPython's
+ * layout rules (report.py:76-77 _fmt). out32 >= 32 bytes; returns length. */
+int isc_format_double(double v, char *out32);
+/* The cells.csv rows of one frame (report.py:131-138), byte-identical with
+ * the reference's writer: "time,cell,p,T,S_w,S_o,S_g,x_*,y_*,C_c" per cell,
+ * S_o = 1.0 - S_w - S_g. x[c*x_cell_stride + i*x_comp_stride] (i < nco),
+ * y likewise (nf entries, the full gas composition). Formatted on `threads`
+ * host threads; *out is malloc'ed (release with isc_free), *len bytes. */
+int isc_format_cells(double time, int64_t n, const double *p, const double *t,
+                     const double *sw, const double *sg, const double *x,
+                     int64_t x_cell_stride, int64_t x_comp_stride, int32_t nco,
+                     const double *y, int64_t y_cell_stride, int64_t y_comp_stride, int32_t nf,
+                     const double *cc, int32_t threads, char **out, int64_t *len);
+void isc_free(void *p);
+
 #ifdef __cplusplus
 }
 #endif

@@ -100,6 +100,12 @@ _SIGS = {
     "isc_stage_times": (ctypes.c_int, [VP, VP]),
     "isc_set_profiling": (ctypes.c_int, [VP, ctypes.c_int32]),
     "isc_kernel_times": (ctypes.c_int, [VP, VP, VP, ctypes.c_int32]),
+    "isc_format_double": (ctypes.c_int, [ctypes.c_double, ctypes.c_char_p]),
+    "isc_format_cells": (ctypes.c_int, [ctypes.c_double, ctypes.c_int64, VP, VP, VP, VP, VP,
+                                        ctypes.c_int64, ctypes.c_int64, ctypes.c_int32, VP,
+                                        ctypes.c_int64, ctypes.c_int64, ctypes.c_int32, VP,
+                                        ctypes.c_int32, VP, c_int64_p]),
+    "isc_free": (None, [VP]),
 }
 
 _lib = None

@@ -16,6 +16,7 @@
 #include "comm.cuh"
 #include "newton.cu"
 #include "numjac.cu"
+#include "report.cuh"
 #include "solver.cu"
 
 using namespace isc;
@@ -1533,3 +1534,37 @@ extern "C" int isc_audit_sums(isc_ctx* ctx, const double* d_accn, double* h_out)
   }
   return isc_comm_allreduce_host(ctx, h_out, 3 * NR, 0);
 }
+
+// ------------------------------------------------------------- reports
+
+extern "C" int isc_format_double(double v, char* out32) { return py_repr_double(v, out32); }
+
+extern "C" int isc_format_cells(double time, int64_t n, const double* p, const double* t,
+                                const double* sw, const double* sg, const double* x,
+                                int64_t x_cell_stride, int64_t x_comp_stride, int32_t nco,
+                                const double* y, int64_t y_cell_stride, int64_t y_comp_stride,
+                                int32_t nf, const double* cc, int32_t threads, char** out,
+                                int64_t* len) {
+  if (n < 0 || nco < 0 || nf < 0 || !out || !len) {
+    g_err = "isc_format_cells: bad arguments";
+    return ISC_BAD_ARGUMENT;
+  }
+  FrameCells F{time, n, p, t, sw, sg, cc, x, x_cell_stride, x_comp_stride, nco,
+               y, y_cell_stride, y_comp_stride, nf};
+  std::string s;
+  try {
+    s = format_cells(F, threads);
+  } catch (const std::exception& e) {
+    g_err = std::string("isc_format_cells: ") + e.what();
+    return ISC_BAD_ARGUMENT;
+  }
+  char* buf = (char*)std::malloc(s.size() + 1);
+  if (!buf) { g_err = "isc_format_cells: out of host memory"; return ISC_BAD_ARGUMENT; }
+  std::memcpy(buf, s.data(), s.size());
+  buf[s.size()] = 0;
+  *out = buf;
+  *len = (int64_t)s.size();
+  return ISC_OK;
+}
+
+extern "C" void isc_free(void* p) { std::free(p); }

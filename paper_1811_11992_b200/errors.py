@@ -18,6 +18,7 @@ try:  # pragma: no cover - depends on whether the reference is importable
         PoreSpaceExhausted,
         SimulationStalled,
         SingularCellBlock,
+        SinkFailure,
         SolverError,
     )
 except Exception:  # the GPU box has no reference checkout
@@ -51,6 +52,9 @@ except Exception:  # the GPU box has no reference checkout
 
     class MaxIterations(SolverError):
         """Krylov iteration limit reached (errors.py:83)."""
+
+    class SinkFailure(OSError):
+        """A report sink could not be created or written (errors.py:91)."""
 
 
 class NativeLibraryMissing(RuntimeError):

@@ -15,6 +15,8 @@ on seeded inputs that our side regenerates bit-identically
   traj_<case>_<tol>.npz  full runs: per-step records and final fields
   numjac_small3d.npz   assemble(jacobian="numeric") blocks (free and frozen upwind)
                        and check_jacobian's worst discrepancy
+  report_frames.npz    two frames (inputs) and the reference writer's cells.csv /
+                       wells.csv bytes (report.py write_frame)
 
     python tests/golden/make_golden.py [name ...]   # regenerate only some
 """
@@ -180,6 +182,48 @@ def make_numjac_small3d():
     print("check_jacobian", float(out["check"]))
 
 
+def make_report_frames():
+    """report.py:115-149 on two frames: a C2 run's accepted state after 3 steps
+    (real values) and a synthetic frame of formatting edge cases (integers,
+    1e16 / 1e-5 thresholds, subnormals, huge, -0.0, nan, inf)."""
+    import tempfile
+    import iscsim.report as R
+    case = configs.config("c2")
+    case = replace(case, schedule=replace(case.schedule, t_end=3 * case.schedule.dt_init))
+    sim = reference_simulator(case)
+    sim.advance()
+    f1 = R.capture_frame(sim, sim.time)
+    n = 64
+    rng = np.random.default_rng(3)
+    edge = np.array([0.0, -0.0, 1.0, 123.0, 1e16, 1e15, 9999999999999998.0, 1e-4, 1e-5, 1.2e-5,
+                     5e-324, 2.2250738585072014e-308, 1.7976931348623157e308, np.nan, np.inf,
+                     -np.inf, 0.1, 1 / 3, 2014.7, -459.67, 1e22, 1e-7, 12345678901234567.0,
+                     0.30000000000000004])
+    vals = np.concatenate([edge, rng.normal(size=8 * n) * 10.0 ** rng.integers(-20, 20, 8 * n)])
+    take = lambda k: vals[(np.arange(n) * 7 + k) % vals.size].copy()   # noqa: E731
+    f2 = R.ReportFrame(time=1e-5, p=take(0), t=take(1), sw=take(2), so=1.0 - take(2) - take(3),
+                       sg=take(3), x=np.stack([take(4), take(5)], 1),
+                       y=np.stack([take(6 + a) for a in range(5)], 1), cc=take(11),
+                       oil_names=f1.oil_names, vap_names=f1.vap_names,
+                       well_names=("INJ", "PROD"), bhp=take(12)[:2],
+                       rates=np.stack([take(13)[:3], take(14)[:3]]),
+                       cum=np.stack([take(15)[:3], take(16)[:3]]))
+    out = {}
+    with tempfile.TemporaryDirectory() as d:
+        with R.ReportSink(d) as sink:
+            R.write_frame(f1, sink)
+            R.write_frame(f2, sink)
+        for name in ("cells", "wells"):
+            with open(os.path.join(d, name + ".csv"), "rb") as fh:
+                out[name + "_csv"] = np.frombuffer(fh.read(), dtype=np.uint8)
+    for k, f in (("f1_", f1), ("f2_", f2)):
+        for fld in ("time", "p", "t", "sw", "so", "sg", "x", "y", "cc", "bhp", "rates", "cum"):
+            out[k + fld] = np.asarray(getattr(f, fld))
+        out[k + "names"] = np.array(["|".join(f.oil_names), "|".join(f.vap_names),
+                                     "|".join(f.well_names)])
+    np.savez_compressed(os.path.join(HERE, "report_frames.npz"), **out)
+
+
 def make_traj_numeric():
     """C1 run in JACOBIAN numeric mode (newton.py:228, 278)."""
     make_traj("c1", 1e-10, jacobian="numeric")
@@ -210,6 +254,7 @@ if __name__ == "__main__":
     make_synth()
     make_numjac_small3d()
     make_traj_numeric()
+    make_report_frames()
     make_traj("c1", 1e-10)
     make_traj("c1", 1e-5)
     make_traj("c2", 1e-10)

@@ -19,7 +19,7 @@ HEADER = os.path.join(ROOT, "include", "iscgpu.h")
 
 def header_functions():
     txt = open(HEADER).read()
-    return sorted(set(re.findall(r"^\s*(?:int|const char \*|void \*|int64_t)\s*\**\s*(isc_\w+)\(",
+    return sorted(set(re.findall(r"^\s*(?:int|const char \*|void \*|void|int64_t)\s*\**\s*(isc_\w+)\(",
                                  txt, flags=re.M)))
 
 

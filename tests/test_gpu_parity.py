@@ -358,3 +358,38 @@ def test_check_jacobian_vs_reference():
     assert abs(worst - float(gn["check"])) <= 1e-3 * float(gn["check"])
     # ws holds the analytic system again
     assert row_scaled_err(ws.diag, g["diag"]) <= JTOL
+
+
+def test_report_frame_from_device_simulator(tmp_path):
+    """capture_frame on the device-resident Simulator (report.py:50-73) + the
+    native writer: the frame matches the reference's C2 frame after 3 steps
+    (report_frames.npz f1) to the run tolerance, and its bytes equal a
+    repr-based restatement of report.py:131-145 on the captured values."""
+    from dataclasses import replace
+    from paper_1811_11992_b200.newton import Simulator
+    from paper_1811_11992_b200.report import ReportSink, capture_frame, write_frame
+    g = golden("report_frames.npz")
+    c = case_objects("c2")
+    sched = replace(c.case.schedule, t_end=3 * c.case.schedule.dt_init)
+    sim = Simulator(c.grid, c.pack, c.wells, c.streams, c.state, sched, c.case.solver)
+    sim.advance()
+    f = capture_frame(sim, sim.time)
+    assert f.time == float(g["f1_time"])
+    for k in ("p", "t", "sw", "so", "sg", "x", "y", "bhp"):
+        a, b = np.asarray(getattr(f, k)), g["f1_" + k]
+        assert a.shape == b.shape, k
+        assert np.max(np.abs(a - b) / np.maximum(np.abs(b), 1e-3)) <= 1e-5, k
+    np.testing.assert_allclose(f.rates, g["f1_rates"], rtol=1e-5, atol=1e-9)
+    np.testing.assert_allclose(f.cum, g["f1_cum"], rtol=1e-5, atol=1e-11)
+    assert "|".join(f.oil_names) == str(g["f1_names"][0])
+    assert "|".join(f.vap_names) == str(g["f1_names"][1])
+    with ReportSink(str(tmp_path)) as sink:
+        write_frame(f, sink)
+    rows = ["time,cell,p,T,S_w,S_o,S_g," + ",".join(f"x_{n}" for n in f.oil_names) + ","
+            + ",".join(f"y_{n}" for n in f.vap_names) + ",C_c\n"]
+    for cix in range(f.p.shape[0]):
+        vals = [f.p[cix], f.t[cix], f.sw[cix], f.so[cix], f.sg[cix], *f.x[cix], *f.y[cix],
+                f.cc[cix]]
+        rows.append(",".join([repr(float(f.time)), str(cix)] + [repr(float(v)) for v in vals])
+                    + "\n")
+    assert (tmp_path / "cells.csv").read_bytes() == "".join(rows).encode()

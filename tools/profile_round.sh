@@ -11,4 +11,9 @@ for k in k_mc_apply k_mc_red k_mc_black_spmv k_face k_decouple3 k_cell k_mc_fact
   ncu --set full --clock-control none --import-source on -k regex:"$k" --launch-skip 6 -c 1 \
       -o gpurun_out/full_${tag}_$k python bench.py --steps 1 --warmup 3 --no-ras \
       --no-cpu-baseline --no-spmv > gpurun_out/ncu_full_${tag}_$k.log 2>&1
+  rep=gpurun_out/full_${tag}_$k.ncu-rep
+  ncu -i $rep --page raw --csv > gpurun_out/full_${tag}_${k}_raw.csv 2>/dev/null
+  ncu -i $rep --page details --csv > gpurun_out/full_${tag}_${k}_details.csv 2>/dev/null
+  ncu -i $rep --page source --csv > gpurun_out/full_${tag}_${k}_source.csv 2>/dev/null
+  [ "$k" = k_mc_apply ] || rm -f $rep   # keep one report (gpurun_out <= 64 MiB)
 done
