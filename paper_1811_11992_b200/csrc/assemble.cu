@@ -920,6 +920,111 @@ __global__ void __launch_bounds__(32 * NU, FACE_MINB) k_face(const FaceArgs F) {
   }
 }
 
+// ----------------------------------------------------- face-centric variant
+//
+// k_face evaluates every face twice (once from each side's gather). The
+// face-centric pair evaluates it once:
+//   k_face_eval    thread per (lower cell a, axis, row < ROW_OS): flux row
+//                  and both derivative rows of face (a, a+axis); writes
+//                  offd[a][+axis] row = dfb, offd[b][-axis] row = -dfa and
+//                  the flux into fbuf[(axis*ROW_OS + row)*n + a]; zero rows
+//                  for boundary blocks.
+//   k_face_gather  thread per (cell, row < ROW_OS): the reference's gather
+//                  (_kernels.py:828-854) in its fixed order; the diagonal
+//                  contribution of each face is read back as minus the
+//                  neighbour's block pointing at the cell (-(-dfa) = dfa for
+//                  side a, -dfb for side b: the same values and order as the
+//                  two-sided kernel).
+struct FaceArgs2 {
+  FaceArgs F;
+  double* __restrict__ fbuf;   // (3 * ROW_OS) x n face fluxes
+};
+
+template <int ROW>
+__device__ __forceinline__ void face_eval_row(const FaceArgs2& A2, int64_t c, int64_t cell, int i,
+                                              int j, int k, int axis) {
+  const FaceArgs& F = A2.F;
+  const int64_t n = F.g.n;
+  const int dp = DXP + axis, dm = opposite(dp);
+  const bool has_lo = (axis == 0 ? i > 0 : (axis == 1 ? j > 0 : k > 0));
+  if (!has_lo) {   // no face below: the cell's -axis block row is zero
+    double* orow = F.offd + (int64_t)((dm * NU + ROW) * NU) * n + c;
+#pragma unroll
+    for (int u = 0; u < NU; ++u) orow[(int64_t)u * n] = 0.0;
+  }
+  const int64_t nb = nb_pos(F.g, cell, i, j, k, dp);
+  double* orow_a = F.offd + (int64_t)((dp * NU + ROW) * NU) * n + c;
+  if (nb < 0) {
+#pragma unroll
+    for (int u = 0; u < NU; ++u) orow_a[(int64_t)u * n] = 0.0;
+    return;
+  }
+  const CellView Av{F.rec, n, c}, Bv{F.rec, n, nb};
+  double flux, dfa[NU], dfb[NU];
+  face_row<ROW>(Av, Bv, F.st, n, c, nb, F.depth[c], F.depth[nb], F.gd[axis * n + c],
+                F.td[axis * n + c], F.upw + (int64_t)axis * 3 * n, n, F.freeze, ROW == 0, flux,
+                dfa, dfb);
+  double* orow_b = F.offd + (int64_t)((dm * NU + ROW) * NU) * n + nb;
+#pragma unroll
+  for (int u = 0; u < NU; ++u) {
+    orow_a[(int64_t)u * n] = dfb[u];
+    orow_b[(int64_t)u * n] = -dfa[u];
+  }
+  A2.fbuf[(int64_t)(axis * ROW_OS + ROW) * n + c] = flux;
+}
+
+#ifndef FEVAL_MINB
+#define FEVAL_MINB 4
+#endif
+
+// grid (ceil(n/32), 3 axes); block (32, ROW_OS)
+__global__ void __launch_bounds__(32 * ROW_OS, FEVAL_MINB) k_face_eval(const FaceArgs2 A2) {
+  const int64_t c = (int64_t)blockIdx.x * 32 + threadIdx.x;
+  if (c >= A2.F.g.n) return;
+  const int axis = blockIdx.y;
+  int i, j, k;
+  const int64_t cell = locate(A2.F.g, c, i, j, k);
+  switch (threadIdx.y) {   // warp-uniform
+    case 0: face_eval_row<0>(A2, c, cell, i, j, k, axis); break;
+    case 1: face_eval_row<1>(A2, c, cell, i, j, k, axis); break;
+    case 2: face_eval_row<2>(A2, c, cell, i, j, k, axis); break;
+    case 3: face_eval_row<3>(A2, c, cell, i, j, k, axis); break;
+    case 4: face_eval_row<4>(A2, c, cell, i, j, k, axis); break;
+    default: face_eval_row<5>(A2, c, cell, i, j, k, axis); break;
+  }
+}
+
+// grid (ceil(n/32)); block (32, ROW_OS)
+__global__ void __launch_bounds__(32 * ROW_OS) k_face_gather(const FaceArgs2 A2) {
+  const FaceArgs& F = A2.F;
+  const int64_t n = F.g.n;
+  const int64_t c = (int64_t)blockIdx.x * 32 + threadIdx.x;
+  const int row = threadIdx.y;
+  if (c >= n) return;
+  int i, j, k;
+  const int64_t cell = locate(F.g, c, i, j, k);
+  double res = F.resid[row * n + c];
+  double drow[NU];
+#pragma unroll
+  for (int u = 0; u < NU; ++u) drow[u] = F.diag[(int64_t)(row * NU + u) * n + c];
+#pragma unroll
+  for (int d = 0; d < NDIR; ++d) {
+    const int64_t nb = nb_pos(F.g, cell, i, j, k, d);
+    if (nb < 0) continue;
+    const bool c_is_a = d >= DXP;
+    const int axis = c_is_a ? d - DXP : 2 - d;
+    const double flux = A2.fbuf[(int64_t)(axis * ROW_OS + row) * n + (c_is_a ? c : nb)];
+    if (c_is_a) res += flux;
+    else res -= flux;
+    const double* back = F.offd + (int64_t)((opposite(d) * NU + row) * NU) * n + nb;
+#pragma unroll
+    for (int u = 0; u < NU; ++u) drow[u] += -back[(int64_t)u * n];
+  }
+  F.resid[row * n + c] = res;
+#pragma unroll
+  for (int u = 0; u < NU; ++u) F.diag[(int64_t)(row * NU + u) * n + c] = drow[u];
+}
+
 // ------------------------------------------------------------------- wells
 
 // Per-well device record (host mirror in csrc/capi.cu / include/iscgpu.h)

@@ -84,6 +84,7 @@ struct isc_ctx {
   double* sc_h = nullptr;   // pinned
   double* partial = nullptr;
   double* partial2 = nullptr;   // second stage of the fixed-order sums
+  double* fbuf = nullptr;       // face fluxes of the face-centric assembly (3*ROW_OS x n)
   int64_t npartial = 0;
   int* flags = nullptr;
   int* fail_d = nullptr;
@@ -405,6 +406,7 @@ extern "C" int isc_create(const isc_model_desc* md, const isc_grid_desc* gdsc, i
   ALLOC(ctx->capped_d, std::max(1, nwells));
   // assembly buffers
   ALLOC(ctx->rec, (size_t)NREC * n * 8);
+  ALLOC(ctx->fbuf, (size_t)3 * ROW_OS * n * 8);
   ALLOC(ctx->acc, (size_t)NU * n * 8);
   ALLOC(ctx->src, (size_t)NU * n * 8);
   ALLOC(ctx->resid, (size_t)NU * n * 8);
@@ -444,7 +446,7 @@ extern "C" int isc_destroy(isc_ctx* ctx) {
                   ctx->capped_d, ctx->rec, ctx->acc, ctx->src, ctx->resid, ctx->diag,
                   ctx->offd, ctx->upw, ctx->bad_d, ctx->rhs, ctx->xk, ctx->rk, ctx->rhat,
                   ctx->pk, ctx->vk, ctx->phat, ctx->shat, ctx->sk, ctx->tk, ctx->sc,
-                  ctx->partial, ctx->partial2, ctx->flags, ctx->fail_d, ctx->schur, ctx->st_c, ctx->accn_c, ctx->stage,
+                  ctx->partial, ctx->partial2, ctx->fbuf, ctx->flags, ctx->fail_d, ctx->schur, ctx->st_c, ctx->accn_c, ctx->stage,
                   ctx->halo_send_lo, ctx->halo_send_hi, ctx->halo_recv_lo, ctx->halo_recv_hi};
   if (ctx->comm.nccl && nccl_api().CommDestroy) nccl_api().CommDestroy(ctx->comm.nccl);
   free_ilu(ctx);
@@ -554,7 +556,20 @@ extern "C" int isc_assemble(isc_ctx* ctx, const double* d_state, const double* h
   }
   FaceArgs F{ctx->g, d_state, ctx->rec, ctx->depth, ctx->gd, ctx->td, ctx->upw, freeze,
              ctx->resid, ctx->diag, ctx->offd};
-  { KScope ks(ctx, KT_FACE); k_face<<<grid1d(n, 32), dim3(32, NU), 0, st>>>(F); }
+#ifndef FACE_CENTRIC
+#define FACE_CENTRIC 1
+#endif
+  {
+    KScope ks(ctx, KT_FACE);
+    if (FACE_CENTRIC) {
+      FaceArgs2 F2{F, ctx->fbuf};
+      k_face_eval<<<dim3(grid1d(n, 32), 3), dim3(32, ROW_OS), 0, st>>>(F2);
+      k_face_gather<<<grid1d(n, 32), dim3(32, ROW_OS), 0, st>>>(F2);
+      ++ctx->launches;
+    } else {
+      k_face<<<grid1d(n, 32), dim3(32, NU), 0, st>>>(F);
+    }
+  }
   LAUNCH_CHECK();
   if (ctx->nw > 0) {
     KScope ks(ctx, KT_WELLS);
