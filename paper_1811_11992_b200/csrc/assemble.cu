@@ -612,7 +612,10 @@ __device__ __forceinline__ void cell_eval(const Model& M, const CellArgs& A, int
   }
 }
 
-__global__ void __launch_bounds__(128) k_cell(const Model M, const CellArgs A) {
+#ifndef CELL_MINB
+#define CELL_MINB 6   // 85 registers + spills beat 255 registers at 2 blocks (C4 sweep 1..8)
+#endif
+__global__ void __launch_bounds__(128, CELL_MINB) k_cell(const Model M, const CellArgs A) {
   const int64_t n = A.g.n;
   const int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (c >= n) return;

@@ -542,7 +542,10 @@ __global__ void __cluster_dims__(ILC, 1, 1) __launch_bounds__(IL_SLOTS * NU)
 __device__ __forceinline__ bool is_black(int i, int j, int k) { return ((i + j + k) & 1) != 0; }
 
 // thread (cell lane, column u); black cells only do work
-__global__ void __launch_bounds__(32 * NU, 2) k_mc_factor(Dims g, const double* __restrict__ offd,
+#ifndef MCF_MINB
+#define MCF_MINB 3   // C4 sweep 2..5: 3.4 -> 2.5 ms at 3
+#endif
+__global__ void __launch_bounds__(32 * NU, MCF_MINB) k_mc_factor(Dims g, const double* __restrict__ offd,
                                                           double* __restrict__ uinv, int* fail) {
   __shared__ double bsh[NU][NU][32];   // B_bd (row, col) of the current direction
   __shared__ double colk[NU][32];
