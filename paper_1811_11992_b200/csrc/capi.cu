@@ -1431,6 +1431,178 @@ static int bicgstab(isc_ctx* ctx, double tol, int maxiter, int* iters) {
   return ISC_MAX_ITERATIONS;
 }
 
+// BiCGSTAB on the red-eliminated system S x_b = g_b with the multicolour
+// preconditioner acting as block-Jacobi U_b (solver.cu "Schur complement"
+// section): same preconditioner and the same stopping test on the full
+// system's residual (its red rows vanish identically), the Krylov vectors
+// on the black half, each product reading every off-diagonal block once.
+// Control flow as bicgstab() / linsolve.py:481-578.
+static int bicgstab_schur(isc_ctx* ctx, double tol, int maxiter, int* iters) {
+  const int64_t len = (int64_t)NU * ctx->g.n;
+  const Dims& g = ctx->g;
+  cudaStream_t st = ctx->stream;
+  Kry K{ctx, len};
+  double *b = ctx->rhs, *x = ctx->xk, *r = ctx->rk, *rhat = ctx->rhat, *p = ctx->pk,
+         *v = ctx->vk, *phat = ctx->phat, *shat = ctx->shat, *s = ctx->sk, *t = ctx->tk;
+  const double* uinv = ctx->mc_uinv;
+  const int bh = grid1d(g.half, 32);   // blocks of a half pass
+  CK(cudaMemsetAsync(x, 0, len * 8, st));
+  TRY(K.dot(b, b, S_BB));   // ||b|| of the full decoupled rhs (the reference's tolerance base)
+  TRY(K.read_scalars());
+  const double nb = std::sqrt(ctx->sc_h[S_BB]);
+  *iters = 0;
+  if (nb == 0.0) return ISC_OK;
+  const double brk = 1e-30 * nb * nb;
+  CK(cudaMemsetAsync(t, 0, len * 8, st));
+  CK(cudaMemsetAsync(p, 0, len * 8, st));
+  CK(cudaMemsetAsync(v, 0, len * 8, st));
+  {
+    KScope ks(ctx, KT_SPMV);
+    k_sc_rhs<<<bh, dim3(32, NU), 0, st>>>(g, ctx->offd, b, r, rhat);   // g_b
+  }
+  ++ctx->launches;
+  double* sh = ctx->sc_h;
+  for (int i = 0; i < S_NSCAL; ++i) sh[i] = 0.0;
+  sh[S_RHO_OLD] = 1.0; sh[S_ALPHA] = 1.0; sh[S_OMEGA] = 1.0; sh[S_FIRST] = 1.0;
+  sh[S_BB] = nb * nb;
+  bool restarted = false, first = true;
+  int it = 0;
+  auto dot_b = [&](const double* a, const double* c, int slot) -> int {
+    KScope ks(ctx, KT_VEC);
+    k_sc_dot<<<RED_BLOCKS, RED_THREADS, 0, st>>>(g, a, c, ctx->partial);
+    ++ctx->launches;
+    return K.finalize1(RED_BLOCKS, slot);
+  };
+  auto finish = [&]() -> int {   // x_r = b_r - B_rb x_b
+    KScope ks(ctx, KT_SPMV);
+    k_sc_xred<<<bh, dim3(32, NU), 0, st>>>(g, ctx->offd, b, x);
+    ++ctx->launches;
+    return cudaGetLastError() == cudaSuccess ? 0 : ISC_CUDA_ERROR;
+  };
+  TRY(K.push());
+  TRY(dot_b(rhat, r, S_RHO_NEW));
+  TRY(K.read_scalars());
+  auto restart = [&]() -> int {
+    // r_b = g_b - S x_b; rhat = r; p = v = 0 (linsolve.py:509-519)
+    {
+      KScope ks(ctx, KT_SPMV);
+      k_sc_red<<<bh, dim3(32, NU), 0, st>>>(g, ctx->offd, x);   // red part of x: scratch
+      k_mc_black_spmv<1><<<bh, dim3(32, NU), 0, st>>>(g, ctx->offd, x, t, rhat, nullptr,
+                                                      ctx->partial, bh, 0);
+      k_sc_rhs<<<bh, dim3(32, NU), 0, st>>>(g, ctx->offd, b, v, shat);   // g_b (scratch)
+    }
+    k_sc_sub<<<RED_BLOCKS, RED_THREADS, 0, st>>>(g, v, t, r, rhat);
+    ctx->launches += 4;
+    cudaMemsetAsync(p, 0, len * 8, st);
+    cudaMemsetAsync(v, 0, len * 8, st);
+    sh[S_RHO_OLD] = 1.0; sh[S_ALPHA] = 1.0; sh[S_OMEGA] = 1.0;
+    first = true;
+    restarted = true;
+    return cudaGetLastError() == cudaSuccess ? 0 : ISC_CUDA_ERROR;
+  };
+  while (it < maxiter) {
+    ++it;
+    double rho = sh[S_RHO_NEW];
+    const double omega = sh[S_OMEGA];
+    if (std::fabs(rho) < brk || (!first && omega == 0.0)) {
+      if (restarted) { g_err = "BiCGSTAB scalar breakdown"; *iters = it; return ISC_BREAKDOWN; }
+      TRY(restart());
+      TRY(K.push());
+      TRY(dot_b(rhat, r, S_RHO_NEW));
+      TRY(K.read_scalars());
+      rho = sh[S_RHO_NEW];
+      if (std::fabs(rho) < brk) { g_err = "BiCGSTAB restart found a null residual"; *iters = it; return ISC_BREAKDOWN; }
+    }
+    sh[S_RHO] = rho;
+    sh[S_FIRST] = first ? 1.0 : 0.0;
+    first = false;
+    TRY(K.push());
+    {
+      KScope ks(ctx, KT_VEC);
+      k_sc_update_p<<<RED_BLOCKS, RED_THREADS, 0, st>>>(g, r, p, v, uinv, phat, ctx->sc);
+    }
+    {
+      KScope ks(ctx, KT_ILU_APPLY);
+      k_sc_red<<<bh, dim3(32, NU), 0, st>>>(g, ctx->offd, phat);
+    }
+    {
+      KScope ks(ctx, KT_SPMV);
+      k_mc_black_spmv<1><<<bh, dim3(32, NU), 0, st>>>(g, ctx->offd, phat, v, rhat, nullptr,
+                                                      ctx->partial, bh, 0);
+    }
+    ctx->launches += 3;
+    CK(cudaGetLastError());
+    TRY(K.finalize1(bh * NU, S_DEN));
+    {
+      KScope ks(ctx, KT_VEC);
+      k_sc_update_s<<<RED_BLOCKS, RED_THREADS, 0, st>>>(g, r, v, s, uinv, shat, ctx->sc,
+                                                        ctx->partial);
+    }
+    ++ctx->launches;
+    TRY(K.finalize1(RED_BLOCKS, S_SS));
+    TRY(K.read_scalars());
+    const double den = sh[S_DEN];
+    if (std::fabs(den) < brk) {
+      if (restarted) { g_err = "BiCGSTAB denominator breakdown"; *iters = it; return ISC_BREAKDOWN; }
+      TRY(restart());
+      TRY(K.push());
+      TRY(dot_b(rhat, r, S_RHO_NEW));
+      TRY(K.read_scalars());
+      continue;
+    }
+    sh[S_ALPHA] = rho / den;
+    if (std::sqrt(sh[S_SS]) / nb <= tol) {
+      TRY(K.push());
+      k_sc_axpy_alpha<<<RED_BLOCKS, RED_THREADS, 0, st>>>(g, x, phat, ctx->sc);
+      ++ctx->launches;
+      TRY(finish());
+      *iters = it;
+      CK(cudaStreamSynchronize(st));
+      return ISC_OK;
+    }
+    TRY(K.push());
+    {
+      KScope ks(ctx, KT_ILU_APPLY);
+      k_sc_red<<<bh, dim3(32, NU), 0, st>>>(g, ctx->offd, shat);
+    }
+    {
+      KScope ks(ctx, KT_SPMV);
+      k_mc_black_spmv<2><<<bh, dim3(32, NU), 0, st>>>(g, ctx->offd, shat, t, nullptr, s,
+                                                      ctx->partial, bh, 0);
+    }
+    ctx->launches += 2;
+    CK(cudaGetLastError());
+    TRY(K.finalize2(bh * NU, S_TT, S_TS));
+    {
+      KScope ks(ctx, KT_VEC);
+      k_sc_update_xr<<<RED_BLOCKS, RED_THREADS, 0, st>>>(g, x, phat, shat, r, s, t, rhat,
+                                                         ctx->sc, ctx->partial);
+    }
+    ++ctx->launches;
+    TRY(K.finalize2(RED_BLOCKS, S_RR, S_RHO_NEW));
+    TRY(K.read_scalars());
+    const double tt = sh[S_TT];
+    if (tt == 0.0) {
+      if (restarted) { g_err = "BiCGSTAB stagnated (t = 0)"; *iters = it; return ISC_BREAKDOWN; }
+      TRY(restart());
+      TRY(K.push());
+      TRY(dot_b(rhat, r, S_RHO_NEW));
+      TRY(K.read_scalars());
+      continue;
+    }
+    sh[S_OMEGA] = sh[S_TS] / tt;
+    if (std::sqrt(sh[S_RR]) / nb <= tol) {
+      TRY(finish());
+      *iters = it;
+      return ISC_OK;
+    }
+    sh[S_RHO_OLD] = rho;
+  }
+  *iters = it;
+  g_err = "BiCGSTAB did not converge";
+  return ISC_MAX_ITERATIONS;
+}
+
 extern "C" int isc_solve(isc_ctx* ctx, double tol, int32_t maxiter, double* d_du, double* h_dbhp,
                          int32_t* iters, int64_t* bad_cell, int32_t* bad_col) {
   if (!ctx->decoupled) {
@@ -1475,7 +1647,12 @@ extern "C" int isc_solve(isc_ctx* ctx, double tol, int32_t maxiter, double* d_du
   }
   int it = 0;
   STAGE(stage_begin(ctx, 3));
-  int status = bicgstab(ctx, tol, maxiter, &it);
+#ifndef MC_SCHUR
+#define MC_SCHUR 1
+#endif
+  const bool schur = MC_SCHUR && ctx->precond == ISC_PRECOND_MCILU && ctx->g.colored &&
+                     !ctx->comm.active();
+  int status = schur ? bicgstab_schur(ctx, tol, maxiter, &it) : bicgstab(ctx, tol, maxiter, &it);
   STAGE(stage_end(ctx, 3));
   if (iters) *iters = it;
   if (status) return status;

@@ -14,8 +14,8 @@ import sys
 from collections import defaultdict
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
-KERNELS = ["k_mc_apply", "k_mc_red", "k_mc_black_spmv", "k_face", "k_decouple3", "k_cell",
-           "k_mc_factor"]
+KERNELS = ["k_sc_red", "k_mc_black_spmv", "k_sc_update_p", "k_sc_update_s", "k_sc_update_xr",
+           "k_face_eval", "k_face_gather", "k_decouple3", "k_cell", "k_mc_factor"]
 METRICS = [
     ("gpu__time_duration.sum", "duration", 1.0),
     ("dram__bytes_read.sum", "DRAM read", 1.0),
@@ -109,12 +109,12 @@ def main(tag):
                   "|---|---|---|---|"]
         for name, v in sorted(tot.items(), key=lambda kv: -kv[1])[:20]:
             lines.append(f"| {name} | {cnt[name]} | {v:.2f} | {v / s:.3f} |")
-    traffic["ilu_apply"] = {"dram_bytes": sum(traffic[k]["dram_bytes"] for k in
-                                              ("k_mc_apply", "k_mc_red") if k in traffic),
-                            "kernels": ["k_mc_apply<1>", "k_mc_red"]}
+    if "k_sc_red" in traffic:
+        traffic["red_pass"] = {"dram_bytes": traffic["k_sc_red"]["dram_bytes"],
+                               "kernels": ["k_sc_red"]}
     if "k_mc_black_spmv" in traffic:
-        traffic["spmv"] = {"dram_bytes": traffic["k_mc_black_spmv"]["dram_bytes"],
-                           "kernels": ["k_mc_black_spmv"]}
+        traffic["black_pass"] = {"dram_bytes": traffic["k_mc_black_spmv"]["dram_bytes"],
+                                 "kernels": ["k_mc_black_spmv"]}
     with open(os.path.join(dst, "ncu_traffic.json"), "w") as fh:
         json.dump(traffic, fh, indent=1)
     with open(os.path.join(dst, "ncu_summary.md"), "w") as fh:
