@@ -82,6 +82,8 @@ typedef struct {
   const int64_t *conn_id;
   const double *hl_area;
   double hl_kob, hl_d, hl_rho, hl_tini;
+  int32_t k_offset; /* global index of local plane 0 (z-slabs; 0 otherwise): the
+                     * red/black colour is (i + j + k_global) & 1 on every rank */
 } isc_grid_desc;
 
 /* One single-perforation well (wells.py:36-54) and its injector stream

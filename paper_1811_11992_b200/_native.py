@@ -41,7 +41,8 @@ class GridDesc(ctypes.Structure):
     _fields_ = ([("nx", ctypes.c_int32), ("ny", ctypes.c_int32), ("nz", ctypes.c_int32)]
                 + [(f, VP) for f in ("depth", "volume", "phi_ref", "gd", "td", "conn_id",
                                      "hl_area")]
-                + [(f, ctypes.c_double) for f in ("hl_kob", "hl_d", "hl_rho", "hl_tini")])
+                + [(f, ctypes.c_double) for f in ("hl_kob", "hl_d", "hl_rho", "hl_tini")]
+                + [("k_offset", ctypes.c_int32)])
 
 
 class WellDesc(ctypes.Structure):

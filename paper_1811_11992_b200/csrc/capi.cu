@@ -316,6 +316,7 @@ extern "C" int isc_create(const isc_model_desc* md, const isc_grid_desc* gdsc, i
   g.n = g.nxny * g.nz;
   g.colored = (g.nx % 2 == 0) ? 1 : 0;
   g.half = g.n / 2;
+  g.kpar = gdsc->k_offset & 1;
   g.ph = g.nxny / 2;
   g.kw_lo = 0;
   g.kw_hi = g.nz;
@@ -1456,6 +1457,7 @@ static int bicgstab_schur(isc_ctx* ctx, double tol, int maxiter, int* iters) {
   CK(cudaMemsetAsync(t, 0, len * 8, st));
   CK(cudaMemsetAsync(p, 0, len * 8, st));
   CK(cudaMemsetAsync(v, 0, len * 8, st));
+  TRY(halo_exchange(ctx, b, NU));   // slabs: red neighbours on other ranks
   {
     KScope ks(ctx, KT_SPMV);
     k_sc_rhs<<<bh, dim3(32, NU), 0, st>>>(g, ctx->offd, b, r, rhat);   // g_b
@@ -1474,6 +1476,7 @@ static int bicgstab_schur(isc_ctx* ctx, double tol, int maxiter, int* iters) {
     return K.finalize1(RED_BLOCKS, slot);
   };
   auto finish = [&]() -> int {   // x_r = b_r - B_rb x_b
+    if (halo_exchange(ctx, x, NU)) return ISC_CUDA_ERROR;
     KScope ks(ctx, KT_SPMV);
     k_sc_xred<<<bh, dim3(32, NU), 0, st>>>(g, ctx->offd, b, x);
     ++ctx->launches;
@@ -1485,8 +1488,10 @@ static int bicgstab_schur(isc_ctx* ctx, double tol, int maxiter, int* iters) {
   auto restart = [&]() -> int {
     // r_b = g_b - S x_b; rhat = r; p = v = 0 (linsolve.py:509-519)
     {
+      if (halo_exchange(ctx, x, NU)) return ISC_CUDA_ERROR;
       KScope ks(ctx, KT_SPMV);
       k_sc_red<<<bh, dim3(32, NU), 0, st>>>(g, ctx->offd, x);   // red part of x: scratch
+      if (halo_exchange(ctx, x, NU)) return ISC_CUDA_ERROR;
       k_mc_black_spmv<1><<<bh, dim3(32, NU), 0, st>>>(g, ctx->offd, x, t, rhat, nullptr,
                                                       ctx->partial, bh, 0);
       k_sc_rhs<<<bh, dim3(32, NU), 0, st>>>(g, ctx->offd, b, v, shat);   // g_b (scratch)
@@ -1521,10 +1526,12 @@ static int bicgstab_schur(isc_ctx* ctx, double tol, int maxiter, int* iters) {
       KScope ks(ctx, KT_VEC);
       k_sc_update_p<<<RED_BLOCKS, RED_THREADS, 0, st>>>(g, r, p, v, uinv, phat, ctx->sc);
     }
+    TRY(halo_exchange(ctx, phat, NU));   // z_b of other ranks' boundary planes
     {
       KScope ks(ctx, KT_ILU_APPLY);
       k_sc_red<<<bh, dim3(32, NU), 0, st>>>(g, ctx->offd, phat);
     }
+    TRY(halo_exchange(ctx, phat, NU));   // w_r likewise
     {
       KScope ks(ctx, KT_SPMV);
       k_mc_black_spmv<1><<<bh, dim3(32, NU), 0, st>>>(g, ctx->offd, phat, v, rhat, nullptr,
@@ -1561,10 +1568,12 @@ static int bicgstab_schur(isc_ctx* ctx, double tol, int maxiter, int* iters) {
       return ISC_OK;
     }
     TRY(K.push());
+    TRY(halo_exchange(ctx, shat, NU));
     {
       KScope ks(ctx, KT_ILU_APPLY);
       k_sc_red<<<bh, dim3(32, NU), 0, st>>>(g, ctx->offd, shat);
     }
+    TRY(halo_exchange(ctx, shat, NU));
     {
       KScope ks(ctx, KT_SPMV);
       k_mc_black_spmv<2><<<bh, dim3(32, NU), 0, st>>>(g, ctx->offd, shat, t, nullptr, s,
@@ -1650,8 +1659,7 @@ extern "C" int isc_solve(isc_ctx* ctx, double tol, int32_t maxiter, double* d_du
 #ifndef MC_SCHUR
 #define MC_SCHUR 1
 #endif
-  const bool schur = MC_SCHUR && ctx->precond == ISC_PRECOND_MCILU && ctx->g.colored &&
-                     !ctx->comm.active();
+  const bool schur = MC_SCHUR && ctx->precond == ISC_PRECOND_MCILU && ctx->g.colored;
   int status = schur ? bicgstab_schur(ctx, tol, maxiter, &it) : bicgstab(ctx, tol, maxiter, &it);
   STAGE(stage_end(ctx, 3));
   if (iters) *iters = it;

@@ -76,6 +76,7 @@ struct Dims {
   int colored;     // 1: colour-blocked storage
   int64_t half;    // n/2 (cells of each colour) when colored
   int64_t ph;      // nxny/2 (cells of each colour in one plane) when colored
+  int kpar;        // parity of the global index of local plane 0 (z-slabs)
   // z-slab decomposition (multi-GPU): this context holds planes [0, nz) of
   // which [kw_lo, kw_hi) are owned; the rest are one-plane ghost copies of
   // the neighbouring ranks' cells. Single GPU: kw_lo = 0, kw_hi = nz.
@@ -106,7 +107,7 @@ __host__ __device__ __forceinline__ int64_t pos_of(const Dims& g, int64_t c) {
   if (!g.colored) return c;
   int i, j, k;
   cell_ijk(g, c, i, j, k);
-  return (c >> 1) + g.ph * (int64_t)(k + ((i + j + k) & 1));
+  return (c >> 1) + g.ph * (int64_t)(k + ((i + j + k + g.kpar) & 1));
 }
 
 // cell index and (i, j, k) of storage position p (one decomposition)
@@ -129,7 +130,7 @@ __host__ __device__ __forceinline__ int64_t locate(const Dims& g, int64_t p, int
   const uint32_t q0 = 2u * (uint32_t)(rem - col * g.ph);
   j = (int)(q0 / (uint32_t)g.nx);
   i = (int)(q0 - (uint32_t)j * (uint32_t)g.nx);
-  i += (((i + j + k) & 1) != col) ? 1 : 0;
+  i += (((i + j + k + g.kpar) & 1) != col) ? 1 : 0;
   return (int64_t)k * g.nxny + (int64_t)j * g.nx + i;
 }
 
@@ -165,7 +166,7 @@ __device__ __forceinline__ int64_t nb_pos(const Dims& g, int64_t c, int i, int j
   const int64_t nb = neighbour(g, c, i, j, k, d);
   if (nb < 0 || !g.colored) return nb;
   const int kn = k + (d == DZM ? -1 : (d == DZP ? 1 : 0));
-  return (nb >> 1) + g.ph * (int64_t)(kn + (((i + j + k) & 1) ^ 1));
+  return (nb >> 1) + g.ph * (int64_t)(kn + (((i + j + k + g.kpar) & 1) ^ 1));
 }
 
 // neighbour of cell c in direction d, or -1 at the boundary

@@ -539,7 +539,9 @@ __global__ void __cluster_dims__(ILC, 1, 1) __launch_bounds__(IL_SLOTS * NU)
 // Every pass is fully parallel (no wavefront); BASELINE north_star's
 // "multicolour block-ILU(0)".
 
-__device__ __forceinline__ bool is_black(int i, int j, int k) { return ((i + j + k) & 1) != 0; }
+__device__ __forceinline__ bool is_black(const Dims& g, int i, int j, int k) {
+  return ((i + j + k + g.kpar) & 1) != 0;
+}
 
 // thread (cell lane, column u); black cells only do work
 #ifndef MCF_MINB
@@ -557,7 +559,7 @@ __global__ void __launch_bounds__(32 * NU, MCF_MINB) k_mc_factor(Dims g, const d
   const int64_t c = g.colored ? (in ? colour_pos(g, 1, t) : 0) : t;
   int i = 0, j = 0, k = 0;
   const int64_t cell = in ? locate(g, c, i, j, k) : 0;
-  const bool live = in && is_black(i, j, k) && owned_k(g, k);
+  const bool live = in && is_black(g, i, j, k) && owned_k(g, k);
   double ucol[NU];
 #pragma unroll
   for (int r = 0; r < NU; ++r) ucol[r] = (r == u) ? 1.0 : 0.0;
@@ -666,7 +668,7 @@ __global__ void __launch_bounds__(32 * NU, MC_MINB) k_mc_apply(Dims g, const dou
   const int64_t c = g.colored ? (in ? colour_pos(g, PASS == 1 ? 1 : 0, t) : 0) : t;
   int i = 0, j = 0, k = 0;
   const int64_t cell = in ? locate(g, c, i, j, k) : 0;
-  const bool live = in && (is_black(i, j, k) == (PASS == 1)) && owned_k(g, k);
+  const bool live = in && (is_black(g, i, j, k) == (PASS == 1)) && owned_k(g, k);
   double w = 0.0;
   if (live) {
     // pass 1 reads red neighbours of r (z_red = r_red); pass 2 the black z
@@ -800,8 +802,10 @@ __global__ void __launch_bounds__(32 * NU, MC_MINB) k_mc_black_spmv(Dims g, cons
       s += t;
     }
     v[r * n + c] = s;
-    if (K == 1) acc[0] = s * w0[r * n + c];
-    if (K == 2) { acc[0] = s * s; acc[K - 1] = s * w1[r * n + c]; }
+    if (owned_k(g, k)) {   // ghost planes (slabs) stay out of the sums
+      if (K == 1) acc[0] = s * w0[r * n + c];
+      if (K == 2) { acc[0] = s * s; acc[K - 1] = s * w1[r * n + c]; }
+    }
   }
   warp_store_at<K>(acc, partial, (int64_t)stride * NU, slot0 + blockIdx.x);
 }
@@ -900,12 +904,15 @@ __global__ void __launch_bounds__(32 * NU, MC_MINB) k_sc_rhs(Dims g, const doubl
 
 // black-half vector kernels: thread per black cell (all 9 rows), fixed grid
 // and block-order partial sums (deterministic)
+#ifndef VEC_MINB
+#define VEC_MINB 4   // caps the U_b^-1 products at 64 registers (255 unbounded)
+#endif
 #define SC_LOOP(t)                                                                            \
   for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < g.half;               \
        t += (int64_t)gridDim.x * blockDim.x)
 
 // p_b = r_b (first) or r_b + beta (p_b - omega v_b); z_b = U_b^-1 p_b
-__global__ void __launch_bounds__(RED_THREADS) k_sc_update_p(Dims g, const double* __restrict__ r,
+__global__ void __launch_bounds__(RED_THREADS, VEC_MINB) k_sc_update_p(Dims g, const double* __restrict__ r,
                                                              double* __restrict__ p,
                                                              const double* __restrict__ v,
                                                              const double* __restrict__ uinv,
@@ -917,6 +924,11 @@ __global__ void __launch_bounds__(RED_THREADS) k_sc_update_p(Dims g, const doubl
   const double omega = sc[S_OMEGA];
   SC_LOOP(t) {
     const int64_t c = colour_pos(g, 1, t);
+    if (!owned_k(g, plane_of(g, c))) {   // ghost plane (slabs): filled by the halo exchange
+#pragma unroll
+      for (int q = 0; q < NU; ++q) { p[q * n + c] = 0.0; z[q * n + c] = 0.0; }
+      continue;
+    }
     double pv[NU];
 #pragma unroll
     for (int q = 0; q < NU; ++q) {
@@ -935,7 +947,7 @@ __global__ void __launch_bounds__(RED_THREADS) k_sc_update_p(Dims g, const doubl
 }
 
 // alpha = rho/den; s_b = r_b - alpha v_b; partial s.s; shat_b = U_b^-1 s_b
-__global__ void __launch_bounds__(RED_THREADS) k_sc_update_s(Dims g, const double* __restrict__ r,
+__global__ void __launch_bounds__(RED_THREADS, VEC_MINB) k_sc_update_s(Dims g, const double* __restrict__ r,
                                                              const double* __restrict__ v,
                                                              double* __restrict__ s,
                                                              const double* __restrict__ uinv,
@@ -947,13 +959,19 @@ __global__ void __launch_bounds__(RED_THREADS) k_sc_update_s(Dims g, const doubl
   double acc[1] = {0.0};
   SC_LOOP(t) {
     const int64_t c = colour_pos(g, 1, t);
+    if (!owned_k(g, plane_of(g, c))) {   // ghost plane (slabs): filled by the halo exchange
+#pragma unroll
+      for (int q = 0; q < NU; ++q) { s[q * n + c] = 0.0; sh[q * n + c] = 0.0; }
+      continue;
+    }
+    const bool own = true;
     double sv[NU];
 #pragma unroll
     for (int q = 0; q < NU; ++q) {
       const int64_t i = q * n + c;
       sv[q] = r[i] - alpha * v[i];
       s[i] = sv[q];
-      acc[0] += sv[q] * sv[q];
+      if (own) acc[0] += sv[q] * sv[q];
     }
 #pragma unroll
     for (int q = 0; q < NU; ++q) {
@@ -968,7 +986,7 @@ __global__ void __launch_bounds__(RED_THREADS) k_sc_update_s(Dims g, const doubl
 
 // omega = ts/tt; x_b += alpha phat_b + omega shat_b; r_b = s_b - omega t_b;
 // partial r.r, rhat.r
-__global__ void __launch_bounds__(RED_THREADS) k_sc_update_xr(Dims g, double* __restrict__ x,
+__global__ void __launch_bounds__(RED_THREADS, VEC_MINB) k_sc_update_xr(Dims g, double* __restrict__ x,
                                                               const double* __restrict__ ph,
                                                               const double* __restrict__ sh_,
                                                               double* __restrict__ r,
@@ -984,14 +1002,17 @@ __global__ void __launch_bounds__(RED_THREADS) k_sc_update_xr(Dims g, double* __
     const double omega = sc[S_TS] / tt;
     SC_LOOP(t) {
       const int64_t c = colour_pos(g, 1, t);
+      const bool own = owned_k(g, plane_of(g, c));
 #pragma unroll
       for (int q = 0; q < NU; ++q) {
         const int64_t i = q * n + c;
         x[i] += alpha * ph[i] + omega * sh_[i];
         const double ri = s[i] - omega * t_[i];
         r[i] = ri;
-        acc[0] += ri * ri;
-        acc[1] += rhat[i] * ri;
+        if (own) {
+          acc[0] += ri * ri;
+          acc[1] += rhat[i] * ri;
+        }
       }
     }
   }
@@ -1024,13 +1045,14 @@ __global__ void k_sc_sub(Dims g, const double* __restrict__ a, const double* __r
   }
 }
 
-__global__ void __launch_bounds__(RED_THREADS) k_sc_dot(Dims g, const double* __restrict__ a,
+__global__ void __launch_bounds__(RED_THREADS, VEC_MINB) k_sc_dot(Dims g, const double* __restrict__ a,
                                                         const double* __restrict__ b,
                                                         double* partial) {
   const int64_t n = g.n;
   double acc[1] = {0.0};
   SC_LOOP(t) {
     const int64_t c = colour_pos(g, 1, t);
+    if (!owned_k(g, plane_of(g, c))) continue;
 #pragma unroll
     for (int q = 0; q < NU; ++q) acc[0] += a[q * n + c] * b[q * n + c];
   }

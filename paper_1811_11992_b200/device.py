@@ -96,7 +96,8 @@ class DeviceContext:
             volume=hold("volume", grid.volume), phi_ref=hold("phi_ref", pack.phi_ref),
             gd=hold("gd", gd), td=hold("td", td), conn_id=hold("cid", cid, np.int64),
             hl_area=hold("hl", hl_area) if hl_area is not None else N.VP(0),
-            hl_kob=hl_kob, hl_d=hl_d, hl_rho=hl_rho, hl_tini=hl_tini)
+            hl_kob=hl_kob, hl_d=hl_d, hl_rho=hl_rho, hl_tini=hl_tini,
+            k_offset=int(getattr(grid, "k_offset", 0)))
         wd = (N.WellDesc * max(1, self.nw))()
         for w, (well, stream) in enumerate(zip(self.wells, self.streams)):
             d = wd[w]

@@ -84,6 +84,9 @@ def split_case(case: Case, nranks: int, rank: int, rock=None) -> SlabPiece:
                    phi[sl])
     depth = np.repeat(zc[ka:kb], nxny)
     g = replace(g, depth=depth)
+    # global index of local plane 0: the device colours cells by the global
+    # (i + j + k) parity, so neighbouring ranks agree on red/black
+    object.__setattr__(g, "k_offset", ka)
     pack = load_pack(case.pack, g.phi_ref)
     mine = [w for w, s in enumerate(case.wells) if k0 <= s.k - 1 < k1]
     specs = [replace(case.wells[w], k=case.wells[w].k - ka) for w in mine]
