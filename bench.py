@@ -19,8 +19,9 @@ every step. The system (9 GB) is far larger than L2, so no flush is needed.
 ``--impl reference`` times the reference algorithm's CPU implementation (the
 plain-C/numpy oracle port, all host threads) on a bounded C4 sample.
 Multi-GPU (torchrun): the C4 grid is z-slab decomposed over the ranks
-(strong scaling; NCCL halo per SpMV and all-reduced Krylov scalars,
-rank-local multicolour ILU); device time is the max over ranks.
+(strong scaling; NCCL halo per half pass and all-reduced Krylov scalars; the
+multicolour preconditioner includes the cross-rank terms, so BiCGSTAB takes
+the single-GPU iterations); device time is the max over ranks.
 """
 
 from __future__ import annotations
@@ -245,7 +246,8 @@ def run_ours(args, rank, world, local):
         sim = Simulator(grid, pack, wells, streams, state, case.schedule, case.solver,
                         comm_setup=lambda ctx: attach_nccl(ctx, uid[0], piece))
         dist_note = (f"z-slab x{world} (planes {piece.k0}-{piece.k1 - 1} on rank {rank}; NCCL "
-                     f"halo per SpMV + all-reduced Krylov scalars; rank-local mcilu)")
+                     f"halo per half pass + all-reduced Krylov scalars; mcilu with cross-rank "
+                     f"boundary blocks)")
     else:
         grid, pack, wells, streams, state = configs.build_case(case)
         sim = Simulator(grid, pack, wells, streams, state, case.schedule, case.solver)

@@ -940,8 +940,17 @@ extern "C" int isc_precond_setup(isc_ctx* ctx, int64_t* bad_cell) {
   KScope ks(ctx, KT_ILU_FACTOR);
   if (ctx->precond == ISC_PRECOND_MCILU) {
     const int64_t nblack = ctx->g.colored ? ctx->g.n - ctx->g.half : ctx->g.n;
+    // Schur path on slabs: bring the owner ranks' decoupled blocks of the
+    // boundary planes into the ghost planes (the -z blocks of our lowest owned
+    // plane go down, the +z blocks of our highest go up), so U_b — and with it
+    // the Krylov iteration — is the single-GPU one
+    const int cross = (ctx->g.colored && ctx->comm.active()) ? 1 : 0;
+    if (cross) {
+      if (halo_exchange(ctx, ctx->offd + (int64_t)DZM * NB * ctx->g.n, NB)) return ISC_CUDA_ERROR;
+      if (halo_exchange(ctx, ctx->offd + (int64_t)DZP * NB * ctx->g.n, NB)) return ISC_CUDA_ERROR;
+    }
     k_mc_factor<<<grid1d(nblack, 32), dim3(32, NU), 0, st>>>(ctx->g, ctx->offd, ctx->mc_uinv,
-                                                            ctx->fail_d);
+                                                            ctx->fail_d, cross);
     CK(cudaGetLastError());
   } else {
   CK(cudaFuncSetAttribute(k_ilu_factor, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -1076,7 +1085,8 @@ static int setup_window(isc_ctx* ctx, int32_t rank, int32_t nranks, int32_t has_
   ctx->comm.nranks = nranks;
   ctx->comm.has_lo = has_lo != 0;
   ctx->comm.has_hi = has_hi != 0;
-  const size_t bytes = (size_t)NU * ctx->g.nxny * 8;
+  // one plane of up to NB rows (vectors: NU; boundary blocks for the factor: NB)
+  const size_t bytes = (size_t)NB * ctx->g.nxny * 8;
   if (!ctx->halo_send_lo) {
     ALLOC(ctx->halo_send_lo, bytes);
     ALLOC(ctx->halo_send_hi, bytes);

@@ -548,7 +548,8 @@ __device__ __forceinline__ bool is_black(const Dims& g, int i, int j, int k) {
 #define MCF_MINB 3   // C4 sweep 2..5: 3.4 -> 2.5 ms at 3
 #endif
 __global__ void __launch_bounds__(32 * NU, MCF_MINB) k_mc_factor(Dims g, const double* __restrict__ offd,
-                                                          double* __restrict__ uinv, int* fail) {
+                                                          double* __restrict__ uinv, int* fail,
+                                                          int cross) {
   __shared__ double bsh[NU][NU][32];   // B_bd (row, col) of the current direction
   __shared__ double colk[NU][32];
   __shared__ int pivs[32];
@@ -566,7 +567,10 @@ __global__ void __launch_bounds__(32 * NU, MCF_MINB) k_mc_factor(Dims g, const d
 #pragma unroll 1
   for (int d = 0; d < NDIR; ++d) {
     int64_t nb = live ? nb_pos(g, cell, i, j, k, d) : -1;
-    if ((d == DZM && !owned_k(g, k - 1)) || (d == DZP && !owned_k(g, k + 1))) nb = -1;
+    // slabs: a ghost-plane neighbour's block pointing back at this cell is the
+    // owner rank's (exchanged after decoupling) when cross != 0; otherwise the
+    // factor is rank-local
+    if (!cross && ((d == DZM && !owned_k(g, k - 1)) || (d == DZP && !owned_k(g, k + 1)))) nb = -1;
     if (nb >= 0) {
       const double* B = offd + (int64_t)(d * NB + u) * n + c;
 #pragma unroll

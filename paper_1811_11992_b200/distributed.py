@@ -11,10 +11,11 @@ Everything per cell stays rank-local; what crosses GPUs is
   * the BiCGSTAB dot products, the Newton norm and the audit sums
     (all-reduced packed scalars).
 
-Ghost rows carry no equation (the library masks them); the preconditioner is
-rank-local (block-Jacobi across ranks of the multicolour ILU(0)), so BiCGSTAB
-iteration counts grow with the rank count, as in the paper's own runs
-(PAPER.md:1572), while converged solutions agree to the Krylov tolerance.
+Ghost rows carry no equation (the library masks them). Cells are coloured by
+their global plane index (``grid.k_offset``), and the owner ranks' boundary
+blocks are copied into the ghost planes before the multicolour factorisation,
+so the preconditioner — and the BiCGSTAB iteration — is the single-GPU one
+whatever the rank count.
 """
 
 from __future__ import annotations
