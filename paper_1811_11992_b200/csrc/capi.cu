@@ -885,9 +885,29 @@ extern "C" int isc_decouple(isc_ctx* ctx, int64_t* bad_cell, int32_t* bad_col) {
   LAUNCH_CHECK();
   CK(cudaMemsetAsync(ctx->flags, 0, n * 4, st));
   CK(cudaMemsetAsync(ctx->bad_d, 0xff, 8, st));
-  k_decouple3<<<grid1d(n, DC3_CELLS), DC3_THREADS, 0, st>>>(ctx->g, ctx->diag, ctx->offd,
-                                                             ctx->rhs, ctx->flags, ctx->bad_d,
-                                                             ctx->offd_rows);
+#ifndef DECOUPLE_WS
+#define DECOUPLE_WS 1
+#endif
+  if (DECOUPLE_WS) {
+    static bool attr = false;
+    if (!attr) {
+      CK(cudaFuncSetAttribute(k_decouple_ws, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                              (int)sizeof(WsSmem)));
+      attr = true;
+    }
+    int dev = 0, sms = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    const int64_t groups = (n + WS_CELLS - 1) / WS_CELLS;
+    const int grid = (int)std::min<int64_t>(groups, (int64_t)sms * WS_BLOCKS_PER_SM);
+    k_decouple_ws<<<grid, WS_THREADS, sizeof(WsSmem), st>>>(ctx->g, ctx->diag, ctx->offd,
+                                                           ctx->rhs, ctx->flags, ctx->bad_d,
+                                                           ctx->offd_rows);
+  } else {
+    k_decouple3<<<grid1d(n, DC3_CELLS), DC3_THREADS, 0, st>>>(ctx->g, ctx->diag, ctx->offd,
+                                                               ctx->rhs, ctx->flags, ctx->bad_d,
+                                                               ctx->offd_rows);
+  }
   LAUNCH_CHECK();
   ctx->offd_rows = NU;   // the decoupled blocks are dense
   }
