@@ -44,6 +44,7 @@ struct CellArgs {
   double* __restrict__ resid;
   double* __restrict__ diag;
   unsigned long long* bad;             // min index of a pore-space-exhausted cell
+  int64_t c_begin, c_end;              // positions handled by k_cell (pipelined staging)
 };
 
 // Where one cell evaluation's outputs go. The analytic pass stores them in
@@ -617,8 +618,8 @@ __device__ __forceinline__ void cell_eval(const Model& M, const CellArgs& A, int
 #endif
 __global__ void __launch_bounds__(128, CELL_MINB) k_cell(const Model M, const CellArgs A) {
   const int64_t n = A.g.n;
-  const int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (c >= n) return;
+  const int64_t c = A.c_begin + (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (c >= A.c_end) return;
   double u_[NU];
 #pragma unroll
   for (int u = 0; u < NU; ++u) u_[u] = A.st[u * n + c];
@@ -1256,10 +1257,10 @@ __global__ void k_import_system(Dims g, const int64_t* __restrict__ conn_id,
 // host-layout state (the reference's State arrays + accn (n, NU)) staged in
 // one device buffer -> SoA state / accn in storage order
 __global__ void k_stage_state(Dims g, const double* __restrict__ stage, double* __restrict__ st,
-                              double* __restrict__ accn) {
+                              double* __restrict__ accn, int64_t c0, int64_t c1) {
   const int64_t n = g.n;
-  const int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;   // natural cell
-  if (c >= n) return;
+  const int64_t c = c0 + (int64_t)blockIdx.x * blockDim.x + threadIdx.x;   // natural cell
+  if (c >= c1) return;
   const int64_t p = pos_of(g, c);
   const double* sp = stage;
   const double* sx = stage + n;

@@ -47,6 +47,9 @@ struct isc_ctx {
   Model M{};
   cudaStream_t stream = nullptr;
   cudaStream_t own_stream = nullptr;
+  cudaStream_t cstream = nullptr;          // host->device staging copies (isc_assemble_host)
+  cudaEvent_t chunk_ev[8] = {};
+  bool cell_pre = false;                   // k_cell already ran (pipelined host staging)
   int64_t launches = 0;
   // static grid data
   double *depth = nullptr, *vol = nullptr, *phi_ref = nullptr, *gd = nullptr, *td = nullptr,
@@ -345,6 +348,8 @@ extern "C" int isc_create(const isc_model_desc* md, const isc_grid_desc* gdsc, i
   }
   CK(cudaStreamCreateWithFlags(&ctx->own_stream, cudaStreamNonBlocking));
   ctx->stream = ctx->own_stream;
+  CK(cudaStreamCreateWithFlags(&ctx->cstream, cudaStreamNonBlocking));
+  for (auto& e : ctx->chunk_ev) CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
   for (auto& e : ctx->ev) CK(cudaEventCreate(&e));
   // static grid arrays
   ALLOC(ctx->depth, n * 8); ALLOC(ctx->vol, n * 8); ALLOC(ctx->phi_ref, n * 8);
@@ -459,6 +464,9 @@ extern "C" int isc_destroy(isc_ctx* ctx) {
   for (auto& e : ctx->ev)
     if (e) cudaEventDestroy(e);
   if (ctx->own_stream) cudaStreamDestroy(ctx->own_stream);
+  if (ctx->cstream) cudaStreamDestroy(ctx->cstream);
+  for (auto& e : ctx->chunk_ev)
+    if (e) cudaEventDestroy(e);
   delete ctx;
   return ISC_OK;
 }
@@ -524,7 +532,7 @@ extern "C" int isc_assemble(isc_ctx* ctx, const double* d_state, const double* h
     CK(cudaMemcpyAsync(ctx->bhp_d, h_bhp, ctx->nw * 8, cudaMemcpyHostToDevice, st));
     CK(cudaMemcpyAsync(ctx->capped_d, h_capped, ctx->nw, cudaMemcpyHostToDevice, st));
   }
-  CK(cudaMemsetAsync(ctx->bad_d, 0xff, 8, st));
+  if (!ctx->cell_pre) CK(cudaMemsetAsync(ctx->bad_d, 0xff, 8, st));
   if (d_state) {   // NULL: state/accn already staged by isc_assemble_host
     k_to_pos<double><<<grid1d(n, 256), 256, 0, st>>>(ctx->g, NU, d_state, ctx->st_c);
     k_to_pos<double><<<grid1d(n, 256), 256, 0, st>>>(ctx->g, NU, d_accn, ctx->accn_c);
@@ -538,8 +546,12 @@ extern "C" int isc_assemble(isc_ctx* ctx, const double* d_state, const double* h
   }
   CellArgs A{ctx->g, d_state, ctx->phi_ref, ctx->vol, ctx->hl_area, ctx->hl_kob, ctx->hl_d,
              ctx->hl_rho, ctx->hl_tini, d_accn, dt, ctx->rec, ctx->acc, ctx->src,
-             ctx->resid, ctx->diag, ctx->bad_d};
-  { KScope ks(ctx, KT_CELL); k_cell<<<grid1d(n, 128), 128, 0, st>>>(ctx->M, A); }
+             ctx->resid, ctx->diag, ctx->bad_d, 0, n};
+  if (!ctx->cell_pre) {
+    KScope ks(ctx, KT_CELL);
+    k_cell<<<grid1d(n, 128), 128, 0, st>>>(ctx->M, A);
+  }
+  ctx->cell_pre = false;
   LAUNCH_CHECK();
   CK(cudaMemcpyAsync(ctx->bad_h, ctx->bad_d, 8, cudaMemcpyDeviceToHost, st));
   CK(cudaStreamSynchronize(st));
@@ -601,7 +613,7 @@ extern "C" int isc_numeric_jacobian(isc_ctx* ctx, double* h_wells_out, int64_t* 
   CK(cudaMemsetAsync(ctx->bad_d, 0xff, 8, st));
   CellArgs A{ctx->g, ctx->st_c, ctx->phi_ref, ctx->vol, ctx->hl_area, ctx->hl_kob, ctx->hl_d,
              ctx->hl_rho, ctx->hl_tini, ctx->accn_c, ctx->asm_dt, nullptr, nullptr, nullptr,
-             nullptr, nullptr, ctx->bad_d};
+             nullptr, nullptr, ctx->bad_d, 0, n};
   NumJacArgs J{A, ctx->rec, ctx->depth, ctx->gd, ctx->td, ctx->upw, ctx->asm_freeze,
                ctx->diag, ctx->offd, ctx->nw, ctx->wells_d, ctx->bhp_d, ctx->capped_d,
                ctx->wout_d, ctx->bad_d};
@@ -658,7 +670,7 @@ extern "C" int isc_assemble_decoupled(isc_ctx* ctx, const double* d_state, const
   }
   CellArgs A{ctx->g, d_state, ctx->phi_ref, ctx->vol, ctx->hl_area, ctx->hl_kob, ctx->hl_d,
              ctx->hl_rho, ctx->hl_tini, d_accn, dt, ctx->rec, ctx->acc, ctx->src,
-             ctx->resid, ctx->diag, ctx->bad_d};
+             ctx->resid, ctx->diag, ctx->bad_d, 0, n};
   { KScope ks(ctx, KT_CELL); k_cell<<<grid1d(n, 128), 128, 0, st>>>(ctx->M, A); }
   LAUNCH_CHECK();
   CK(cudaMemcpyAsync(ctx->bad_h, ctx->bad_d, 8, cudaMemcpyDeviceToHost, st));
@@ -728,18 +740,50 @@ extern "C" int isc_assemble_host(isc_ctx* ctx, const double* h_p, const double* 
                                  const uint8_t* h_capped, int32_t freeze, double* h_wells_out,
                                  int64_t* bad_cell) {
   const int64_t n = ctx->g.n;
+  const Dims& g = ctx->g;
   cudaStream_t st = ctx->stream;
   double* sg = ctx->stage;
-  const size_t b = (size_t)n * 8;
-  CK(cudaMemcpyAsync(sg, h_p, b, cudaMemcpyHostToDevice, st));
-  CK(cudaMemcpyAsync(sg + n, h_x, b * NCO, cudaMemcpyHostToDevice, st));
-  CK(cudaMemcpyAsync(sg + (1 + NCO) * n, h_y, b * NCG, cudaMemcpyHostToDevice, st));
   const double* rest[4] = {h_t, h_sw, h_sg, h_cc};
-  for (int q = 0; q < 4; ++q)
-    CK(cudaMemcpyAsync(sg + (1 + NCO + NCG + q) * n, rest[q], b, cudaMemcpyHostToDevice, st));
-  CK(cudaMemcpyAsync(sg + (size_t)(CT + 4) * n, h_accn, b * NU, cudaMemcpyHostToDevice, st));
-  k_stage_state<<<grid1d(n, 256), 256, 0, st>>>(ctx->g, sg, ctx->st_c, ctx->accn_c);
+  // Copies of plane chunks on the copy stream, each chunk's transpose and
+  // cell pass on the main stream as soon as it lands: the PCIe transfer
+  // overlaps the cell kernel (one chunk on z-slabs, whose cell pass needs
+  // the halo exchange of the whole state first).
+  const bool pipe = !ctx->comm.active();
+  const int nq = pipe ? std::min(8, g.nz) : 1;
+  CK(cudaMemsetAsync(ctx->bad_d, 0xff, 8, st));
+  CK(cudaEventRecord(ctx->chunk_ev[0], st));
+  CK(cudaStreamWaitEvent(ctx->cstream, ctx->chunk_ev[0], 0));   // stage buffer free
+  CellArgs A{g, ctx->st_c, ctx->phi_ref, ctx->vol, ctx->hl_area, ctx->hl_kob, ctx->hl_d,
+             ctx->hl_rho, ctx->hl_tini, ctx->accn_c, dt, ctx->rec, ctx->acc, ctx->src,
+             ctx->resid, ctx->diag, ctx->bad_d, 0, n};
+  for (int q = 0; q < nq; ++q) {
+    const int64_t k0 = (int64_t)g.nz * q / nq, k1 = (int64_t)g.nz * (q + 1) / nq;
+    const int64_t c0 = k0 * g.nxny, c1 = k1 * g.nxny, cnt = c1 - c0;
+    const size_t b = (size_t)cnt * 8;
+    cudaStream_t cs = ctx->cstream;
+    CK(cudaMemcpyAsync(sg + c0, h_p + c0, b, cudaMemcpyHostToDevice, cs));
+    CK(cudaMemcpyAsync(sg + n + c0 * NCO, h_x + c0 * NCO, b * NCO, cudaMemcpyHostToDevice, cs));
+    CK(cudaMemcpyAsync(sg + (1 + NCO) * n + c0 * NCG, h_y + c0 * NCG, b * NCG,
+                       cudaMemcpyHostToDevice, cs));
+    for (int r = 0; r < 4; ++r)
+      CK(cudaMemcpyAsync(sg + (1 + NCO + NCG + r) * n + c0, rest[r] + c0, b,
+                         cudaMemcpyHostToDevice, cs));
+    CK(cudaMemcpyAsync(sg + (size_t)(CT + 4) * n + c0 * NU, h_accn + c0 * NU, b * NU,
+                       cudaMemcpyHostToDevice, cs));
+    CK(cudaEventRecord(ctx->chunk_ev[q], cs));
+    CK(cudaStreamWaitEvent(st, ctx->chunk_ev[q], 0));
+    k_stage_state<<<grid1d(cnt, 256), 256, 0, st>>>(g, sg, ctx->st_c, ctx->accn_c, c0, c1);
+    ++ctx->launches;
+    if (pipe) {   // planes [k0, k1) occupy positions [c0, c1) in both storage orders
+      A.c_begin = c0;
+      A.c_end = c1;
+      KScope ks(ctx, KT_CELL);
+      k_cell<<<grid1d(cnt, 128), 128, 0, st>>>(ctx->M, A);
+      ++ctx->launches;
+    }
+  }
   LAUNCH_CHECK();
+  ctx->cell_pre = pipe;
   return isc_assemble(ctx, nullptr, h_bhp, nullptr, dt, t_new, h_capped, freeze, h_wells_out,
                       bad_cell);
 }
