@@ -978,17 +978,20 @@ __device__ __forceinline__ void face_eval_row(const FaceArgs2& A2, int64_t c, in
 }
 
 #ifndef FEVAL_MINB
-#define FEVAL_MINB 4
+#define FEVAL_MINB 8
 #endif
 
-// grid (ceil(n/32), 3 axes); block (32, ROW_OS)
-__global__ void __launch_bounds__(32 * ROW_OS, FEVAL_MINB) k_face_eval(const FaceArgs2 A2) {
+// grid (ceil(n/32), ROW_OS rows); block (32, 3 axes). A block holds one row's
+// three axes: the rows' costs differ several-fold (the energy row touches
+// every phase, the oil rows one), and warps of equal cost in a block keep it
+// from being held resident by its slowest warp.
+__global__ void __launch_bounds__(32 * 3, FEVAL_MINB) k_face_eval(const FaceArgs2 A2) {
   const int64_t c = (int64_t)blockIdx.x * 32 + threadIdx.x;
   if (c >= A2.F.g.n) return;
-  const int axis = blockIdx.y;
+  const int axis = threadIdx.y;
   int i, j, k;
   const int64_t cell = locate(A2.F.g, c, i, j, k);
-  switch (threadIdx.y) {   // warp-uniform
+  switch (blockIdx.y) {   // block-uniform
     case 0: face_eval_row<0>(A2, c, cell, i, j, k, axis); break;
     case 1: face_eval_row<1>(A2, c, cell, i, j, k, axis); break;
     case 2: face_eval_row<2>(A2, c, cell, i, j, k, axis); break;

@@ -576,7 +576,7 @@ extern "C" int isc_assemble(isc_ctx* ctx, const double* d_state, const double* h
     KScope ks(ctx, KT_FACE);
     if (FACE_CENTRIC) {
       FaceArgs2 F2{F, ctx->fbuf};
-      k_face_eval<<<dim3(grid1d(n, 32), 3), dim3(32, ROW_OS), 0, st>>>(F2);
+      k_face_eval<<<dim3(grid1d(n, 32), ROW_OS), dim3(32, 3), 0, st>>>(F2);
       k_face_gather<<<grid1d(n, 32), dim3(32, ROW_OS), 0, st>>>(F2);
       ++ctx->launches;
     } else {
