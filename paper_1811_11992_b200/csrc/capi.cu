@@ -5,6 +5,7 @@
 #include <algorithm>
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -50,6 +51,7 @@ struct isc_ctx {
   cudaStream_t cstream = nullptr;          // host->device staging copies (isc_assemble_host)
   cudaEvent_t chunk_ev[8] = {};
   bool cell_pre = false;                   // k_cell already ran (pipelined host staging)
+  bool mc_schur = true;   // mcilu: red-eliminated BiCGSTAB (ISC_MCILU_FULL=1: full system)
   int64_t launches = 0;
   // static grid data
   double *depth = nullptr, *vol = nullptr, *phi_ref = nullptr, *gd = nullptr, *td = nullptr,
@@ -313,6 +315,10 @@ extern "C" int isc_create(const isc_model_desc* md, const isc_grid_desc* gdsc, i
   }
   isc_ctx* ctx = new isc_ctx();
   ctx->precond = precond;
+  {
+    const char* e = std::getenv("ISC_MCILU_FULL");   // A/B switch for the full-system form
+    ctx->mc_schur = !(e && e[0] == '1');
+  }
   Dims& g = ctx->g;
   g.nx = gdsc->nx; g.ny = gdsc->ny; g.nz = gdsc->nz;
   g.nxny = (int64_t)g.nx * g.ny;
@@ -1733,7 +1739,8 @@ extern "C" int isc_solve(isc_ctx* ctx, double tol, int32_t maxiter, double* d_du
 #ifndef MC_SCHUR
 #define MC_SCHUR 1
 #endif
-  const bool schur = MC_SCHUR && ctx->precond == ISC_PRECOND_MCILU && ctx->g.colored;
+  const bool schur = MC_SCHUR && ctx->mc_schur && ctx->precond == ISC_PRECOND_MCILU &&
+                     ctx->g.colored;
   int status = schur ? bicgstab_schur(ctx, tol, maxiter, &it) : bicgstab(ctx, tol, maxiter, &it);
   STAGE(stage_end(ctx, 3));
   if (iters) *iters = it;
