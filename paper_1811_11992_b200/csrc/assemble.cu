@@ -75,6 +75,33 @@ struct CellSinkProbe {
   __device__ double f(int k) const { return v[k]; }   // record accessor (flux, wells)
 };
 
+// dyfull (NF x NU) with its structure (_kernels.py:220-252): the water row
+// has d/dp, d/dT, d/dSw; oil row i has d/dp, d/dT, d/dx_i, d/dSw, d/dSg (the
+// last two non-zero for the heaviest oil only); gas row a is the unit vector
+// of its own column. 13 stored values instead of 45, so the cell kernel keeps
+// them in registers; dy(a, u) and nz(a, u) fold at compile time in unrolled
+// loops, and the sums skip the structural zeros (the reference adds +-0).
+struct DyFull {
+  double w[3];
+  double o[NCO][5];
+  __device__ __forceinline__ double operator()(int a, int u) const {
+    if (a == 0) return u == 0 ? w[0] : (u == CT ? w[1] : (u == CSW ? w[2] : 0.0));
+    if (a < 1 + NCO) {
+      const int i = a - 1;
+      return u == 0 ? o[i][0]
+                    : (u == CT ? o[i][1]
+                               : (u == 1 + i ? o[i][2]
+                                             : (u == CSW ? o[i][3] : (u == CSG ? o[i][4] : 0.0))));
+    }
+    return u == a ? 1.0 : 0.0;
+  }
+  __host__ __device__ static constexpr bool nz(int a, int u) {
+    return a == 0 ? (u == 0 || u == CT || u == CSW)
+                  : (a < 1 + NCO ? (u == 0 || u == CT || u == a || u == CSW || u == CSG)
+                                 : u == a);
+  }
+};
+
 // cell_eval + compose for the cell at position c with unknowns u_
 // (_kernels.py:66-610, 797-825); inputs other than the unknowns from A.
 template <class S>
@@ -152,20 +179,20 @@ __device__ __forceinline__ void cell_eval(const Model& M, const CellArgs& A, int
   for (int i = 0; i < NCO; ++i) dro_x[i] = -ro2 / rho_i[i];
 
   // K-values -> yfull, dyfull (_kernels.py:220-252)
-  double yf[NF], dyf[NF][NU];
+  double yf[NF];
+  DyFull dyf;
 #pragma unroll
-  for (int a = 0; a < NF; ++a) {
+  for (int i = 0; i < NCO; ++i)
 #pragma unroll
-    for (int u = 0; u < NU; ++u) dyf[a][u] = 0.0;
-  }
+    for (int q = 0; q < 5; ++q) dyf.o[i][q] = 0.0;
   {
     double kw, dkw_p, dkw_t, fw, dfw_s;
     k_value(M.kv[0], p, t, kw, dkw_p, dkw_t);
     per_factor(sw, eps_per, fw, dfw_s);
     yf[0] = fw * kw;
-    dyf[0][0] = fw * dkw_p;
-    dyf[0][CT] = fw * dkw_t;
-    dyf[0][CSW] = dfw_s * kw;
+    dyf.w[0] = fw * dkw_p;
+    dyf.w[1] = fw * dkw_t;
+    dyf.w[2] = dfw_s * kw;
     double fo_h, dfo_h;
     per_factor(so, eps_per, fo_h, dfo_h);
 #pragma unroll
@@ -175,36 +202,35 @@ __device__ __forceinline__ void cell_eval(const Model& M, const CellArgs& A, int
       const int cr = 1 + i;
       if (i == M.heavy) {
         yf[cr] = fo_h * ki * x[i];
-        dyf[cr][0] = fo_h * dki_p * x[i];
-        dyf[cr][CT] = fo_h * dki_t * x[i];
-        dyf[cr][1 + i] = fo_h * ki;
-        dyf[cr][CSW] = -dfo_h * ki * x[i];
-        dyf[cr][CSG] = -dfo_h * ki * x[i];
+        dyf.o[i][0] = fo_h * dki_p * x[i];
+        dyf.o[i][1] = fo_h * dki_t * x[i];
+        dyf.o[i][2] = fo_h * ki;
+        dyf.o[i][3] = -dfo_h * ki * x[i];
+        dyf.o[i][4] = -dfo_h * ki * x[i];
       } else {
         yf[cr] = ki * x[i];
-        dyf[cr][0] = dki_p * x[i];
-        dyf[cr][CT] = dki_t * x[i];
-        dyf[cr][1 + i] = ki;
+        dyf.o[i][0] = dki_p * x[i];
+        dyf.o[i][1] = dki_t * x[i];
+        dyf.o[i][2] = ki;
       }
     }
 #pragma unroll
     for (int j = 0; j < NCG; ++j) {
       yf[1 + NCO + j] = y[j];
-      dyf[1 + NCO + j][1 + NCO + j] = 1.0;
     }
   }
   // record: yfull and its structural partials
 #pragma unroll
   for (int a = 0; a < NF; ++a) REC(R_Y + a) = yf[a];
-  REC(R_DY0_P) = dyf[0][0];
-  REC(R_DY0_T) = dyf[0][CT];
-  REC(R_DY0_SW) = dyf[0][CSW];
+  REC(R_DY0_P) = dyf.w[0];
+  REC(R_DY0_T) = dyf.w[1];
+  REC(R_DY0_SW) = dyf.w[2];
 #pragma unroll
   for (int i = 0; i < NCO; ++i) {
-    REC(R_DYO + 4 * i + 0) = dyf[1 + i][0];
-    REC(R_DYO + 4 * i + 1) = dyf[1 + i][CT];
-    REC(R_DYO + 4 * i + 2) = dyf[1 + i][1 + i];
-    REC(R_DYO + 4 * i + 3) = dyf[1 + i][CSW];
+    REC(R_DYO + 4 * i + 0) = dyf.o[i][0];
+    REC(R_DYO + 4 * i + 1) = dyf.o[i][1];
+    REC(R_DYO + 4 * i + 2) = dyf.o[i][2];
+    REC(R_DYO + 4 * i + 3) = dyf.o[i][3];
   }
 
   // gas phase (_kernels.py:254-328)
@@ -219,7 +245,8 @@ __device__ __forceinline__ void cell_eval(const Model& M, const CellArgs& A, int
   for (int a = 0; a < NF; ++a)
     if (dzdw[a] != 0.0) {
 #pragma unroll
-      for (int u = 0; u < NU; ++u) dz[u] += dzdw[a] * dyf[a][u];
+      for (int u = 0; u < NU; ++u)
+        if (DyFull::nz(a, u)) dz[u] += dzdw[a] * dyf(a, u);
     }
   const double tr = t + RANKINE;
   const double rg = p / (z * R_GAS * tr);
@@ -235,7 +262,8 @@ __device__ __forceinline__ void cell_eval(const Model& M, const CellArgs& A, int
   for (int a = 0; a < NF; ++a) {
     mgbar += yf[a] * M.gasp[a][G_M];
 #pragma unroll
-    for (int u = 0; u < NU; ++u) dmg[u] += M.gasp[a][G_M] * dyf[a][u];
+    for (int u = 0; u < NU; ++u)
+      if (DyFull::nz(a, u)) dmg[u] += M.gasp[a][G_M] * dyf(a, u);
   }
   double wsum = 0.0, musum = 0.0, dmusum_t = 0.0, sqm[NF], muc[NF];
 #pragma unroll
@@ -259,7 +287,8 @@ __device__ __forceinline__ void cell_eval(const Model& M, const CellArgs& A, int
       double dmy = sqm[a] * (muc[a] - mug) / wsum;
       if (dmy != 0.0) {
 #pragma unroll
-        for (int u = 0; u < NU; ++u) dmug[u] += dmy * dyf[a][u];
+        for (int u = 0; u < NU; ++u)
+          if (DyFull::nz(a, u)) dmug[u] += dmy * dyf(a, u);
       }
     }
   } else {
@@ -276,7 +305,8 @@ __device__ __forceinline__ void cell_eval(const Model& M, const CellArgs& A, int
     dhg[CT] += yf[a] * dh_c;
     if (h_c != 0.0) {
 #pragma unroll
-      for (int u = 0; u < NU; ++u) dhg[u] += h_c * dyf[a][u];
+      for (int u = 0; u < NU; ++u)
+        if (DyFull::nz(a, u)) dhg[u] += h_c * dyf(a, u);
     }
   }
   const double ug = hg - p / rg;
@@ -422,7 +452,7 @@ __device__ __forceinline__ void cell_eval(const Model& M, const CellArgs& A, int
           for (int a = 0; a < NF; ++a)
             if (a == oxi) {
 #pragma unroll
-              for (int u = 0; u < NU; ++u) dpp[u] = dyf[a][u] * pg;
+              for (int u = 0; u < NU; ++u) dpp[u] = dyf(a, u) * pg;
             }
           dpp[0] += y_ox;
           dpp[CSG] += y_ox * dpcog;
@@ -483,7 +513,7 @@ __device__ __forceinline__ void cell_eval(const Model& M, const CellArgs& A, int
       accr = phif * a_w;
 #pragma unroll
       for (int u = 0; u < NU; ++u) {
-        double d = (drg[u] * sg * yf[0] + mw_g * dyf[0][u]);
+        double d = (drg[u] * sg * yf[0] + mw_g * dyf(0, u));
         if (u == 0) d += drw_p * sw;
         else if (u == CT) d += drw_t * sw;
         else if (u == CSW) d += rw;
@@ -499,7 +529,7 @@ __device__ __forceinline__ void cell_eval(const Model& M, const CellArgs& A, int
       accr = phif * a_i;
 #pragma unroll
       for (int u = 0; u < NU; ++u) {
-        double d = drg[u] * sg * yf[r] + mw_g * dyf[r][u];
+        double d = drg[u] * sg * yf[r] + mw_g * dyf(r, u);
         if (u == 0) d += dro_p * so * x[i];
         else if (u == CT) d += dro_t * so * x[i];
         else if (u == CSW || u == CSG) d += -ro * x[i] + (u == CSG ? rg * yf[r] : 0.0);
@@ -566,7 +596,8 @@ __device__ __forceinline__ void cell_eval(const Model& M, const CellArgs& A, int
       for (int a = 0; a < NF; ++a) {
         sy += yf[a];
 #pragma unroll
-        for (int u = 0; u < NU; ++u) dacc[u] += dyf[a][u];
+        for (int u = 0; u < NU; ++u)
+          if (DyFull::nz(a, u)) dacc[u] += dyf(a, u);
       }
       accr = sy - 1.0;
     } else {  // coke
