@@ -1016,10 +1016,15 @@ __device__ __forceinline__ void face_eval_row(const FaceArgs2& A2, int64_t c, in
 // three axes: the rows' costs differ several-fold (the energy row touches
 // every phase, the oil rows one), and warps of equal cost in a block keep it
 // from being held resident by its slowest warp.
-__global__ void __launch_bounds__(32 * 3, FEVAL_MINB) k_face_eval(const FaceArgs2 A2) {
-  const int64_t c = (int64_t)blockIdx.x * 32 + threadIdx.x;
-  if (c >= A2.F.g.n) return;
-  const int axis = threadIdx.y;
+// Lower cells [c_begin, c_end), axes axis_lo + threadIdx.y (pipelined host
+// staging evaluates the in-plane faces of a chunk of planes as soon as its
+// records exist, the z faces one plane behind).
+__global__ void __launch_bounds__(32 * 3, FEVAL_MINB) k_face_eval(const FaceArgs2 A2,
+                                                                 int64_t c_begin, int64_t c_end,
+                                                                 int axis_lo) {
+  const int64_t c = c_begin + (int64_t)blockIdx.x * 32 + threadIdx.x;
+  if (c >= c_end) return;
+  const int axis = axis_lo + threadIdx.y;
   int i, j, k;
   const int64_t cell = locate(A2.F.g, c, i, j, k);
   switch (blockIdx.y) {   // block-uniform

@@ -51,6 +51,7 @@ struct isc_ctx {
   cudaStream_t cstream = nullptr;          // host->device staging copies (isc_assemble_host)
   cudaEvent_t chunk_ev[8] = {};
   bool cell_pre = false;                   // k_cell already ran (pipelined host staging)
+  bool face_pre = false;                   // k_face_eval too
   bool mc_schur = true;   // mcilu: red-eliminated BiCGSTAB (ISC_MCILU_FULL=1: full system)
   int64_t launches = 0;
   // static grid data
@@ -533,12 +534,15 @@ extern "C" int isc_assemble(isc_ctx* ctx, const double* d_state, const double* h
   const int64_t n = ctx->g.n;
   cudaStream_t st = ctx->stream;
   ctx->assembled = false;
+  // set by isc_assemble_host when it ran these passes while staging
+  const bool cell_pre = ctx->cell_pre, face_pre = ctx->face_pre;
+  ctx->cell_pre = ctx->face_pre = false;
   STAGE(stage_begin(ctx, 0));
   if (ctx->nw > 0) {
     CK(cudaMemcpyAsync(ctx->bhp_d, h_bhp, ctx->nw * 8, cudaMemcpyHostToDevice, st));
     CK(cudaMemcpyAsync(ctx->capped_d, h_capped, ctx->nw, cudaMemcpyHostToDevice, st));
   }
-  if (!ctx->cell_pre) CK(cudaMemsetAsync(ctx->bad_d, 0xff, 8, st));
+  if (!cell_pre) CK(cudaMemsetAsync(ctx->bad_d, 0xff, 8, st));
   if (d_state) {   // NULL: state/accn already staged by isc_assemble_host
     k_to_pos<double><<<grid1d(n, 256), 256, 0, st>>>(ctx->g, NU, d_state, ctx->st_c);
     k_to_pos<double><<<grid1d(n, 256), 256, 0, st>>>(ctx->g, NU, d_accn, ctx->accn_c);
@@ -553,11 +557,10 @@ extern "C" int isc_assemble(isc_ctx* ctx, const double* d_state, const double* h
   CellArgs A{ctx->g, d_state, ctx->phi_ref, ctx->vol, ctx->hl_area, ctx->hl_kob, ctx->hl_d,
              ctx->hl_rho, ctx->hl_tini, d_accn, dt, ctx->rec, ctx->acc, ctx->src,
              ctx->resid, ctx->diag, ctx->bad_d, 0, n};
-  if (!ctx->cell_pre) {
+  if (!cell_pre) {
     KScope ks(ctx, KT_CELL);
     k_cell<<<grid1d(n, 128), 128, 0, st>>>(ctx->M, A);
   }
-  ctx->cell_pre = false;
   LAUNCH_CHECK();
   CK(cudaMemcpyAsync(ctx->bad_h, ctx->bad_d, 8, cudaMemcpyDeviceToHost, st));
   CK(cudaStreamSynchronize(st));
@@ -582,7 +585,8 @@ extern "C" int isc_assemble(isc_ctx* ctx, const double* d_state, const double* h
     KScope ks(ctx, KT_FACE);
     if (FACE_CENTRIC) {
       FaceArgs2 F2{F, ctx->fbuf};
-      k_face_eval<<<dim3(grid1d(n, 32), ROW_OS), dim3(32, 3), 0, st>>>(F2);
+      if (!face_pre)
+        k_face_eval<<<dim3(grid1d(n, 32), ROW_OS), dim3(32, 3), 0, st>>>(F2, 0, n, 0);
       k_face_gather<<<grid1d(n, 32), dim3(32, ROW_OS), 0, st>>>(F2);
       ++ctx->launches;
     } else {
@@ -762,6 +766,9 @@ extern "C" int isc_assemble_host(isc_ctx* ctx, const double* h_p, const double* 
   CellArgs A{g, ctx->st_c, ctx->phi_ref, ctx->vol, ctx->hl_area, ctx->hl_kob, ctx->hl_d,
              ctx->hl_rho, ctx->hl_tini, ctx->accn_c, dt, ctx->rec, ctx->acc, ctx->src,
              ctx->resid, ctx->diag, ctx->bad_d, 0, n};
+  FaceArgs F{g, ctx->st_c, ctx->rec, ctx->depth, ctx->gd, ctx->td, ctx->upw, freeze,
+             ctx->resid, ctx->diag, ctx->offd};
+  FaceArgs2 F2{F, ctx->fbuf};
   for (int q = 0; q < nq; ++q) {
     const int64_t k0 = (int64_t)g.nz * q / nq, k1 = (int64_t)g.nz * (q + 1) / nq;
     const int64_t c0 = k0 * g.nxny, c1 = k1 * g.nxny, cnt = c1 - c0;
@@ -783,13 +790,29 @@ extern "C" int isc_assemble_host(isc_ctx* ctx, const double* h_p, const double* 
     if (pipe) {   // planes [k0, k1) occupy positions [c0, c1) in both storage orders
       A.c_begin = c0;
       A.c_end = c1;
-      KScope ks(ctx, KT_CELL);
-      k_cell<<<grid1d(cnt, 128), 128, 0, st>>>(ctx->M, A);
-      ++ctx->launches;
+      {
+        KScope ks(ctx, KT_CELL);
+        k_cell<<<grid1d(cnt, 128), 128, 0, st>>>(ctx->M, A);
+      }
+      KScope ks(ctx, KT_FACE);
+      // x/y faces of this chunk's cells; z faces of the plane below it and of
+      // all but its last plane (their upper records now exist)
+      k_face_eval<<<dim3(grid1d(cnt, 32), ROW_OS), dim3(32, 2), 0, st>>>(F2, c0, c1, 0);
+      const int64_t z0 = std::max<int64_t>(0, (k0 - 1) * g.nxny), z1 = (k1 - 1) * g.nxny;
+      if (z1 > z0)
+        k_face_eval<<<dim3(grid1d(z1 - z0, 32), ROW_OS), dim3(32, 1), 0, st>>>(F2, z0, z1, 2);
+      ctx->launches += 3;
     }
+  }
+  if (pipe) {   // z faces of the top plane (boundary: zero blocks)
+    KScope ks(ctx, KT_FACE);
+    const int64_t z0 = (int64_t)(g.nz - 1) * g.nxny;
+    k_face_eval<<<dim3(grid1d(n - z0, 32), ROW_OS), dim3(32, 1), 0, st>>>(F2, z0, n, 2);
+    ++ctx->launches;
   }
   LAUNCH_CHECK();
   ctx->cell_pre = pipe;
+  ctx->face_pre = pipe && FACE_CENTRIC;
   return isc_assemble(ctx, nullptr, h_bhp, nullptr, dt, t_new, h_capped, freeze, h_wells_out,
                       bad_cell);
 }
