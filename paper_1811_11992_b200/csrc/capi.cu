@@ -1557,9 +1557,8 @@ static int bicgstab_schur(isc_ctx* ctx, double tol, int maxiter, int* iters) {
   *iters = 0;
   if (nb == 0.0) return ISC_OK;
   const double brk = 1e-30 * nb * nb;
-  CK(cudaMemsetAsync(t, 0, len * 8, st));
-  CK(cudaMemsetAsync(p, 0, len * 8, st));
-  CK(cudaMemsetAsync(v, 0, len * 8, st));
+  // p, v and t need no clearing: p and v are read only after the first
+  // iteration wrote them (S_FIRST), t only where the black pass wrote it
   TRY(halo_exchange(ctx, b, NU));   // slabs: red neighbours on other ranks
   {
     KScope ks(ctx, KT_SPMV);

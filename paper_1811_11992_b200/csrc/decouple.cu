@@ -4,14 +4,11 @@
 // linsolve.py:70-152 (GJ with partial pivoting, pivot tolerance
 // 1e-13*max|D|, D^-1 applied to the row's rhs and off-diagonal blocks).
 //
-// B200 mapping: one CTA = 32 cells x 32 column-pairs (1024 threads). The
-// thread (cell, j) owns columns j and j+32 of the cell's augmented block row
-// [D | B_-z B_-y B_-x B_+x B_+y B_+z | rhs] (9 x 64): loads and stores of a
-// warp are 32 consecutive cells of one column -> fully coalesced 256 B
-// transactions. Row operations on a column need only the pivot column,
-// which is broadcast through shared memory (9 doubles per cell per step).
-// The decoupled diagonal (D^-1 D, identity up to rounding; the reference
-// stores it, Appendix A.11) is not written: SpMV/ILU use an exact identity.
+// Kernels: k_decouple_ws (default; warp-specialised, below) and k_decouple3
+// (the same arithmetic one phase after the other, -DDECOUPLE_WS=0). Loads and
+// stores of a warp are consecutive cells of one column -> coalesced. The
+// decoupled diagonal (D^-1 D, identity up to rounding; the reference stores
+// it, Appendix A.11) is not written: SpMV/ILU use an exact identity.
 #include "common.cuh"
 
 namespace isc {
@@ -38,196 +35,6 @@ __global__ void k_rhs_schur(Dims g, const double* __restrict__ resid, double* rh
 #pragma unroll
       for (int u = 0; u < NU; ++u) diag[(int64_t)(r * NU + u) * n + c] -= bcol[r] * wrow[u] * inv_d;
     }
-  }
-}
-
-constexpr int DC_CELLS = 32;
-constexpr int NCOLS = NU + NDIR * NU + 1;   // 64
-static_assert(NCOLS == 64, "augmented row must be 64 columns");
-
-__device__ __forceinline__ double* col_ptr(int j, int r, int64_t n, int64_t c, double* diag,
-                                           double* offd, double* rhs) {
-  if (j < NU) return diag + (int64_t)(r * NU + j) * n + c;
-  if (j < NU + NDIR * NU) {
-    const int d = (j - NU) / NU, u = (j - NU) % NU;
-    return offd + (int64_t)((d * NU + r) * NU + u) * n + c;
-  }
-  return rhs + (int64_t)r * n + c;
-}
-
-__global__ void __launch_bounds__(DC_CELLS * 32) k_decouple(Dims g, double* diag, double* offd, double* rhs,
-                                                   int* flags, unsigned long long* bad) {
-  __shared__ double colk[NU][DC_CELLS];
-  __shared__ double cmax[NU][DC_CELLS];
-  __shared__ int piv_s[DC_CELLS];
-  __shared__ int failc[DC_CELLS];
-  const int64_t n = g.n;
-  const int lane = threadIdx.x, jy = threadIdx.y;
-  const int64_t c = (int64_t)blockIdx.x * DC_CELLS + lane;
-  const bool live = c < n;
-  const int j0 = jy, j1 = jy + 32;
-  double a0[NU], a1[NU];
-#pragma unroll
-  for (int r = 0; r < NU; ++r) {
-    a0[r] = live ? *col_ptr(j0, r, n, c, diag, offd, rhs) : (r == j0 ? 1.0 : 0.0);
-    a1[r] = live ? *col_ptr(j1, r, n, c, diag, offd, rhs) : 0.0;
-  }
-  // tolerance: 1e-13 * max |D| (linsolve.py:77-86)
-  if (jy < NU) {
-    double m = 0.0;
-#pragma unroll
-    for (int r = 0; r < NU; ++r) m = fmax(m, fabs(a0[r]));
-    cmax[jy][lane] = m;
-  }
-  if (jy == 0) failc[lane] = NU;
-  __syncthreads();
-  double amax = 0.0;
-#pragma unroll
-  for (int u = 0; u < NU; ++u) amax = fmax(amax, cmax[u][lane]);
-  const double tol = 1e-13 * amax;
-#pragma unroll
-  for (int k = 0; k < NU; ++k) {
-    if (jy == k) {
-      int piv = k;
-      double pv = fabs(a0[k]);
-#pragma unroll
-      for (int r = k + 1; r < NU; ++r) {
-        const double v = fabs(a0[r]);
-        if (v > pv) { pv = v; piv = r; }
-      }
-      if (pv <= tol || amax == 0.0) atomicMin(&failc[lane], amax == 0.0 ? 0 : k);
-#pragma unroll
-      for (int r = 0; r < NU; ++r) {
-        double v = a0[r];
-        if (r == k) {
-#pragma unroll
-          for (int q = k + 1; q < NU; ++q) if (q == piv) v = a0[q];
-        } else if (r == piv) {
-          v = a0[k];
-        }
-        colk[r][lane] = v;
-      }
-      piv_s[lane] = piv;
-    }
-    __syncthreads();
-    const int piv = piv_s[lane];
-    if (piv != k) {   // swap rows k and piv in both owned columns
-      double t0 = a0[k], t1 = a1[k];
-#pragma unroll
-      for (int q = k + 1; q < NU; ++q)
-        if (q == piv) { a0[k] = a0[q]; a1[k] = a1[q]; a0[q] = t0; a1[q] = t1; }
-    }
-    const double dinv = 1.0 / colk[k][lane];
-    a0[k] *= dinv;
-    a1[k] *= dinv;
-#pragma unroll
-    for (int r = 0; r < NU; ++r) {
-      if (r == k) continue;
-      const double f = colk[r][lane];
-      if (f != 0.0) {
-        a0[r] -= f * a0[k];
-        a1[r] -= f * a1[k];
-      }
-    }
-    __syncthreads();
-  }
-  if (!live) return;
-  if (jy == 0 && failc[lane] < NU) {   // first failing pivot column (linsolve.py:98-99)
-    const int64_t cell = cell_of(g, c);
-    flags[cell] = failc[lane] + 1;
-    atomicMin(bad, (unsigned long long)cell);
-  }
-  if (j0 >= NU) {
-#pragma unroll
-    for (int r = 0; r < NU; ++r) *col_ptr(j0, r, n, c, diag, offd, rhs) = a0[r];
-  }
-#pragma unroll
-  for (int r = 0; r < NU; ++r) *col_ptr(j1, r, n, c, diag, offd, rhs) = a1[r];
-}
-
-// One column per thread: CTA = DC2_CELLS cells x 64 columns (512 threads),
-// ~40 registers, several CTAs per SM so loads, pivots and stores of
-// different CTAs overlap. Warp = 4 columns x 8 consecutive cells: every
-// load/store is a full 64 B run of one column.
-constexpr int DC2_CELLS = 8;
-
-__global__ void __launch_bounds__(DC2_CELLS * 64, 2) k_decouple2(Dims g, double* diag, double* offd,
-                                                             double* rhs, int* flags,
-                                                             unsigned long long* bad) {
-  __shared__ double colk[NU][DC2_CELLS];
-  __shared__ double cmax[NU][DC2_CELLS];
-  __shared__ int piv_s[DC2_CELLS];
-  __shared__ int failc[DC2_CELLS];
-  const int64_t n = g.n;
-  const int cl = threadIdx.x % DC2_CELLS, j = threadIdx.x / DC2_CELLS;
-  const int64_t c = (int64_t)blockIdx.x * DC2_CELLS + cl;
-  const bool live = c < n;
-  double a[NU];
-#pragma unroll
-  for (int r = 0; r < NU; ++r) a[r] = live ? *col_ptr(j, r, n, c, diag, offd, rhs) : (r == j ? 1.0 : 0.0);
-  if (j < NU) {
-    double m = 0.0;
-#pragma unroll
-    for (int r = 0; r < NU; ++r) m = fmax(m, fabs(a[r]));
-    cmax[j][cl] = m;
-  }
-  if (j == 0) failc[cl] = NU;
-  __syncthreads();
-  double amax = 0.0;
-#pragma unroll
-  for (int u = 0; u < NU; ++u) amax = fmax(amax, cmax[u][cl]);
-  const double tol = 1e-13 * amax;
-#pragma unroll
-  for (int k = 0; k < NU; ++k) {
-    if (j == k) {
-      int piv = k;
-      double pv = fabs(a[k]);
-#pragma unroll
-      for (int r = k + 1; r < NU; ++r) {
-        const double v = fabs(a[r]);
-        if (v > pv) { pv = v; piv = r; }
-      }
-      if (pv <= tol || amax == 0.0) atomicMin(&failc[cl], amax == 0.0 ? 0 : k);
-#pragma unroll
-      for (int r = 0; r < NU; ++r) {
-        double v = a[r];
-        if (r == k) {
-#pragma unroll
-          for (int q = k + 1; q < NU; ++q) if (q == piv) v = a[q];
-        } else if (r == piv) {
-          v = a[k];
-        }
-        colk[r][cl] = v;
-      }
-      piv_s[cl] = piv;
-    }
-    __syncthreads();
-    const int piv = piv_s[cl];
-    if (piv != k) {
-      const double t0 = a[k];
-#pragma unroll
-      for (int q = k + 1; q < NU; ++q)
-        if (q == piv) { a[k] = a[q]; a[q] = t0; }
-    }
-    const double dinv = 1.0 / colk[k][cl];
-    a[k] *= dinv;
-#pragma unroll
-    for (int r = 0; r < NU; ++r) {
-      if (r == k) continue;
-      const double f = colk[r][cl];
-      if (f != 0.0) a[r] -= f * a[k];
-    }
-    __syncthreads();
-  }
-  if (!live) return;
-  if (j == 0 && failc[cl] < NU) {
-    const int64_t cell = cell_of(g, c);
-    flags[cell] = failc[cl] + 1;
-    atomicMin(bad, (unsigned long long)cell);
-  }
-  if (j >= NU) {
-#pragma unroll
-    for (int r = 0; r < NU; ++r) *col_ptr(j, r, n, c, diag, offd, rhs) = a[r];
   }
 }
 

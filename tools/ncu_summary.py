@@ -15,7 +15,7 @@ from collections import defaultdict
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 KERNELS = ["k_sc_red", "k_mc_black_spmv", "k_sc_update_p", "k_sc_update_s", "k_sc_update_xr",
-           "k_face_eval", "k_face_gather", "k_decouple3", "k_cell", "k_mc_factor"]
+           "k_face_eval", "k_face_gather", "k_decouple_ws", "k_cell", "k_mc_factor"]
 METRICS = [
     ("gpu__time_duration.sum", "duration", 1.0),
     ("dram__bytes_read.sum", "DRAM read", 1.0),
