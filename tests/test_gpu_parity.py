@@ -421,3 +421,38 @@ def test_mcilu_red_eliminated_matches_full_system(name, monkeypatch):
     assert np.linalg.norm(du_s - du_f) <= 1e-8 * np.linalg.norm(du_f)
     np.testing.assert_allclose(db_s, db_f, rtol=1e-8, atol=1e-8)
     assert it_s <= it_f + 1, (it_s, it_f)
+
+
+@pytest.mark.parametrize("nx", [6, 5])   # red-eliminated (even nx) and full-system (odd nx)
+def test_mcilu_solve_synthetic_and_error_paths(nx):
+    """mcilu on a synthetic system: du solves the decoupled system to the
+    tolerance (checked against a dense solve), and the reference's error
+    contract holds (SingularCellBlock with the cell, MaxIterations)."""
+    from paper_1811_11992_b200.grid import build_grid
+    from paper_1811_11992_b200.synth import synth_system
+    from paper_1811_11992_b200.model import load_pack
+    grid = build_grid(nx, 5, 4, 1.0, 1.0, 1.0, 1.0, 1.0, 1.0, 0.3)
+    pack = load_pack("tube3_pack", grid.phi_ref)
+    diag, offd, resid = synth_system(grid, 9, seed=5)
+    ws = Workspace(grid, pack, None, wells=(), streams=(), precond="mcilu")
+    load_system(ws, diag, offd, resid)
+    du, _, it = BlockSolver(grid, ws, tol=1e-12, maxiter=500, precond="mcilu").solve([])
+    # dense check in the reference layout: sum of block rows times du = -resid
+    n = grid.ncell
+    A = np.zeros((9 * n, 9 * n))
+    for c in range(n):
+        A[9 * c:9 * c + 9, 9 * c:9 * c + 9] = diag[c]
+    for ic in range(grid.nconn):
+        a, b = int(grid.conn_a[ic]), int(grid.conn_b[ic])
+        A[9 * a:9 * a + 9, 9 * b:9 * b + 9] = offd[ic, 0]
+        A[9 * b:9 * b + 9, 9 * a:9 * a + 9] = offd[ic, 1]
+    ref = np.linalg.solve(A, -resid.reshape(-1)).reshape(n, 9)
+    assert np.linalg.norm(du - ref) <= 1e-9 * np.linalg.norm(ref), it
+    bad = diag.copy()
+    bad[7, :, 2] = 0.0
+    load_system(ws, bad, offd, resid)
+    with pytest.raises(SingularCellBlock, match="cell 7"):
+        BlockSolver(grid, ws, tol=1e-8, maxiter=100, precond="mcilu").solve([])
+    load_system(ws, diag, offd, resid)
+    with pytest.raises(MaxIterations):
+        BlockSolver(grid, ws, tol=1e-14, maxiter=1, precond="mcilu").solve([])

@@ -8,7 +8,7 @@ ncu --metrics gpu__time_duration.sum --clock-control none -c 2000 --csv \
     --log-file gpurun_out/launches_$tag.csv \
     python bench.py --steps 2 --warmup 1 --no-ras --no-cpu-baseline --no-spmv > gpurun_out/ncu_launch_$tag.log 2>&1
 for k in k_sc_red k_mc_black_spmv k_sc_update_p k_sc_update_s k_sc_update_xr k_face_eval k_face_gather k_decouple_ws k_cell k_mc_factor; do
-  ncu --set full --clock-control none --import-source on -k regex:"$k" --launch-skip 6 -c 1 \
+  ncu --set full --clock-control none --import-source on -k regex:"$k" --launch-skip 2 -c 1 \
       -o gpurun_out/full_${tag}_$k python bench.py --steps 1 --warmup 3 --no-ras \
       --no-cpu-baseline --no-spmv > gpurun_out/ncu_full_${tag}_$k.log 2>&1
   rep=gpurun_out/full_${tag}_$k.ncu-rep
