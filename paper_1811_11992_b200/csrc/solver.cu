@@ -795,6 +795,8 @@ __global__ void __launch_bounds__(32 * NU, MC_MINB) k_mc_black_spmv(Dims g, cons
     int i, j, k;
     const int64_t cell = locate(g, c, i, j, k);
     double s = z[r * n + c];
+    // the dot operand is loaded up front, in flight with the block stream
+    const double wdot = K == 1 ? w0[r * n + c] : (K == 2 ? w1[r * n + c] : 0.0);
 #pragma unroll
     for (int d = 0; d < NDIR; ++d) {
       const int64_t nb = nb_pos(g, cell, i, j, k, d);
@@ -807,8 +809,8 @@ __global__ void __launch_bounds__(32 * NU, MC_MINB) k_mc_black_spmv(Dims g, cons
     }
     v[r * n + c] = s;
     if (owned_k(g, k)) {   // ghost planes (slabs) stay out of the sums
-      if (K == 1) acc[0] = s * w0[r * n + c];
-      if (K == 2) { acc[0] = s * s; acc[K - 1] = s * w1[r * n + c]; }
+      if (K == 1) acc[0] = s * wdot;
+      if (K == 2) { acc[0] = s * s; acc[K - 1] = s * wdot; }
     }
   }
   warp_store_at<K>(acc, partial, (int64_t)stride * NU, slot0 + blockIdx.x);
