@@ -1037,13 +1037,14 @@ __global__ void __launch_bounds__(32 * 3, FEVAL_MINB) k_face_eval(const FaceArgs
   }
 }
 
-// grid (ceil(n/32)); block (32, ROW_OS)
+// grid (ceil(owned cells / 32)); block (32, ROW_OS). Owned planes only:
+// ghost rows (z-slabs) carry no equation.
 __global__ void __launch_bounds__(32 * ROW_OS) k_face_gather(const FaceArgs2 A2) {
   const FaceArgs& F = A2.F;
   const int64_t n = F.g.n;
-  const int64_t c = (int64_t)blockIdx.x * 32 + threadIdx.x;
+  const int64_t c = (int64_t)F.g.kw_lo * F.g.nxny + (int64_t)blockIdx.x * 32 + threadIdx.x;
   const int row = threadIdx.y;
-  if (c >= n) return;
+  if (c >= (int64_t)F.g.kw_hi * F.g.nxny) return;
   int i, j, k;
   const int64_t cell = locate(F.g, c, i, j, k);
   double res = F.resid[row * n + c];

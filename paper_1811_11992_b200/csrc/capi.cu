@@ -327,6 +327,8 @@ extern "C" int isc_create(const isc_model_desc* md, const isc_grid_desc* gdsc, i
   g.colored = (g.nx % 2 == 0) ? 1 : 0;
   g.half = g.n / 2;
   g.kpar = gdsc->k_offset & 1;
+  g.tw_lo = 0;
+  g.tw_hi = g.half;
   g.ph = g.nxny / 2;
   g.kw_lo = 0;
   g.kw_hi = g.nz;
@@ -587,7 +589,8 @@ extern "C" int isc_assemble(isc_ctx* ctx, const double* d_state, const double* h
       FaceArgs2 F2{F, ctx->fbuf};
       if (!face_pre)
         k_face_eval<<<dim3(grid1d(n, 32), ROW_OS), dim3(32, 3), 0, st>>>(F2, 0, n, 0);
-      k_face_gather<<<grid1d(n, 32), dim3(32, ROW_OS), 0, st>>>(F2);
+      k_face_gather<<<grid1d((int64_t)(ctx->g.kw_hi - ctx->g.kw_lo) * ctx->g.nxny, 32),
+                      dim3(32, ROW_OS), 0, st>>>(F2);
       ++ctx->launches;
     } else {
       k_face<<<grid1d(n, 32), dim3(32, NU), 0, st>>>(F);
@@ -971,7 +974,8 @@ extern "C" int isc_decouple(isc_ctx* ctx, int64_t* bad_cell, int32_t* bad_col) {
     int dev = 0, sms = 148;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    const int64_t groups = (n + WS_CELLS - 1) / WS_CELLS;
+    const int64_t owned = (int64_t)(ctx->g.kw_hi - ctx->g.kw_lo) * ctx->g.nxny;
+    const int64_t groups = (owned + WS_CELLS - 1) / WS_CELLS;
     const int grid = (int)std::min<int64_t>(groups, (int64_t)sms * WS_BLOCKS_PER_SM);
     k_decouple_ws<<<grid, WS_THREADS, sizeof(WsSmem), st>>>(ctx->g, ctx->diag, ctx->offd,
                                                            ctx->rhs, ctx->flags, ctx->bad_d,
@@ -1174,6 +1178,8 @@ static int setup_window(isc_ctx* ctx, int32_t rank, int32_t nranks, int32_t has_
   }
   ctx->g.kw_lo = kw_lo;
   ctx->g.kw_hi = kw_hi;
+  ctx->g.tw_lo = ctx->g.colored ? (int64_t)kw_lo * ctx->g.ph : 0;
+  ctx->g.tw_hi = ctx->g.colored ? (int64_t)kw_hi * ctx->g.ph : ctx->g.half;
   ctx->comm.rank = rank;
   ctx->comm.nranks = nranks;
   ctx->comm.has_lo = has_lo != 0;
@@ -1549,7 +1555,7 @@ static int bicgstab_schur(isc_ctx* ctx, double tol, int maxiter, int* iters) {
   double *b = ctx->rhs, *x = ctx->xk, *r = ctx->rk, *rhat = ctx->rhat, *p = ctx->pk,
          *v = ctx->vk, *phat = ctx->phat, *shat = ctx->shat, *s = ctx->sk, *t = ctx->tk;
   const double* uinv = ctx->mc_uinv;
-  const int bh = grid1d(g.half, 32);   // blocks of a half pass
+  const int bh = grid1d(g.tw_hi - g.tw_lo, 32);   // blocks of a half pass (owned planes)
   CK(cudaMemsetAsync(x, 0, len * 8, st));
   TRY(K.dot(b, b, S_BB));   // ||b|| of the full decoupled rhs (the reference's tolerance base)
   TRY(K.read_scalars());

@@ -81,6 +81,9 @@ struct Dims {
   // which [kw_lo, kw_hi) are owned; the rest are one-plane ghost copies of
   // the neighbouring ranks' cells. Single GPU: kw_lo = 0, kw_hi = nz.
   int kw_lo, kw_hi;
+  // owned range of the per-colour index t (colour-blocked storage: planes
+  // [kw_lo, kw_hi) hold t in [kw_lo*ph, kw_hi*ph)); single GPU: [0, half)
+  int64_t tw_lo, tw_hi;
 };
 
 __host__ __device__ __forceinline__ bool owned_k(const Dims& g, int k) {

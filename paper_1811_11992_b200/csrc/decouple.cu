@@ -20,6 +20,11 @@ __global__ void k_rhs_schur(Dims g, const double* __restrict__ resid, double* rh
   const int64_t n = g.n;
   const int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (c >= n) return;
+  if (!owned_k(g, plane_of(g, c))) {   // ghost rows (z-slabs) carry no equation
+#pragma unroll
+    for (int r = 0; r < NU; ++r) rhs[r * n + c] = 0.0;
+    return;
+  }
 #pragma unroll
   for (int r = 0; r < NU; ++r) rhs[r * n + c] = -resid[r * n + c];
   for (int w = 0; w < nw; ++w) {
@@ -236,7 +241,10 @@ __global__ void __launch_bounds__(WS_THREADS, WS_BLOCKS_PER_SM) k_decouple_ws(
   extern __shared__ __align__(16) unsigned char ws_raw[];
   WsSmem& S = *reinterpret_cast<WsSmem*>(ws_raw);
   const int64_t n = g.n;
-  const int64_t ngroups = (n + WS_CELLS - 1) / WS_CELLS;
+  // owned planes only (ghost rows carry no equation; the factor takes the
+  // owner ranks' boundary blocks): positions [p0, p1)
+  const int64_t p0 = (int64_t)g.kw_lo * g.nxny, p1 = (int64_t)g.kw_hi * g.nxny;
+  const int64_t ngroups = (p1 - p0 + WS_CELLS - 1) / WS_CELLS;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int nb_threads = 32 * (WS_GJ_WARPS + WS_B_WARPS);
   if (warp < WS_GJ_WARPS) {
@@ -245,8 +253,8 @@ __global__ void __launch_bounds__(WS_THREADS, WS_BLOCKS_PER_SM) k_decouple_ws(
     int i = 0;
     for (int64_t grp = blockIdx.x; grp < ngroups; grp += gridDim.x, ++i) {
       const int buf = i & 1;
-      const int64_t c = grp * WS_CELLS + cl;
-      const bool live = c < n;
+      const int64_t c = p0 + grp * WS_CELLS + cl;
+      const bool live = c < p1;
       double a[NU], e[NU];
 #pragma unroll
       for (int r = 0; r < NU; ++r) {
@@ -334,9 +342,9 @@ __global__ void __launch_bounds__(WS_THREADS, WS_BLOCKS_PER_SM) k_decouple_ws(
     const int64_t mine = (ngroups - blockIdx.x + gridDim.x - 1) / gridDim.x;
     for (int64_t grp = blockIdx.x; grp < ngroups; grp += gridDim.x, ++i) {
       const int buf = i & 1;
-      const int64_t c = grp * WS_CELLS + cl;
+      const int64_t c = p0 + grp * WS_CELLS + cl;
       named_sync(WS_BAR_READY + buf, nb_threads);
-      if (c < n) {
+      if (c < p1) {
         const bool gh = S.ghost[buf][cl] != 0;
 #pragma unroll 1
         for (int col = col0; col < NCOLB; col += WS_B_WARPS) {

@@ -786,11 +786,11 @@ __global__ void __launch_bounds__(32 * NU, MC_MINB) k_mc_black_spmv(Dims g, cons
                                                            int slot0) {
   const int64_t n = g.n;
   const int ls = threadIdx.x, r = threadIdx.y;
-  const int64_t t = (int64_t)blockIdx.x * 32 + ls;   // t-th black cell
+  const int64_t t = g.tw_lo + (int64_t)blockIdx.x * 32 + ls;   // t-th black cell (owned)
   double acc[K];
 #pragma unroll
   for (int k = 0; k < K; ++k) acc[k] = 0.0;
-  if (t < g.half) {
+  if (t < g.tw_hi) {
     const int64_t c = colour_pos(g, 1, t);
     int i, j, k;
     const int64_t cell = locate(g, c, i, j, k);
@@ -836,8 +836,8 @@ __global__ void __launch_bounds__(32 * NU, MC_MINB) k_sc_red(Dims g, const doubl
                                                               double* __restrict__ z) {
   const int64_t n = g.n;
   const int ls = threadIdx.x, r = threadIdx.y;
-  const int64_t t = (int64_t)blockIdx.x * 32 + ls;
-  if (t >= g.half) return;
+  const int64_t t = g.tw_lo + (int64_t)blockIdx.x * 32 + ls;   // owned planes only
+  if (t >= g.tw_hi) return;
   const int64_t c = colour_pos(g, 0, t);
   int i, j, k;
   const int64_t cell = locate(g, c, i, j, k);
@@ -861,8 +861,8 @@ __global__ void __launch_bounds__(32 * NU, MC_MINB) k_sc_xred(Dims g, const doub
                                                                double* __restrict__ x) {
   const int64_t n = g.n;
   const int ls = threadIdx.x, r = threadIdx.y;
-  const int64_t t = (int64_t)blockIdx.x * 32 + ls;
-  if (t >= g.half) return;
+  const int64_t t = g.tw_lo + (int64_t)blockIdx.x * 32 + ls;   // owned planes only
+  if (t >= g.tw_hi) return;
   const int64_t c = colour_pos(g, 0, t);
   int i, j, k;
   const int64_t cell = locate(g, c, i, j, k);
@@ -888,8 +888,8 @@ __global__ void __launch_bounds__(32 * NU, MC_MINB) k_sc_rhs(Dims g, const doubl
                                                               double* __restrict__ rhat) {
   const int64_t n = g.n;
   const int ls = threadIdx.x, r = threadIdx.y;
-  const int64_t t = (int64_t)blockIdx.x * 32 + ls;
-  if (t >= g.half) return;
+  const int64_t t = g.tw_lo + (int64_t)blockIdx.x * 32 + ls;   // owned planes only
+  if (t >= g.tw_hi) return;
   const int64_t c = colour_pos(g, 1, t);
   int i, j, k;
   const int64_t cell = locate(g, c, i, j, k);
@@ -914,7 +914,7 @@ __global__ void __launch_bounds__(32 * NU, MC_MINB) k_sc_rhs(Dims g, const doubl
 #define VEC_MINB 4   // caps the U_b^-1 products at 64 registers (255 unbounded)
 #endif
 #define SC_LOOP(t)                                                                            \
-  for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < g.half;               \
+  for (int64_t t = g.tw_lo + (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < g.tw_hi;    \
        t += (int64_t)gridDim.x * blockDim.x)
 
 // p_b = r_b (first) or r_b + beta (p_b - omega v_b); z_b = U_b^-1 p_b
