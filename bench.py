@@ -272,6 +272,7 @@ def run_ours(args, rank, world, local):
     ms8, cnt8 = np.zeros(8), np.zeros(8, dtype=np.int64)
     ctx.L.isc_kernel_times(ctx.h, N.ptr(ms8), N.ptr(cnt8), 1)
     l0 = ctx.launch_count()
+    st0 = ctx.stage_times()
     its = []
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     barrier()
@@ -282,6 +283,7 @@ def run_ours(args, rank, world, local):
     barrier()
     dev_ms = ev0.elapsed_time(ev1)
     launches = ctx.launch_count() - l0
+    stage_ms = (ctx.stage_times() - st0) / max(1, args.steps)
     ctx.L.isc_kernel_times(ctx.h, N.ptr(ms8), N.ptr(cnt8), 1)
     N.check(ctx.L.isc_set_profiling(ctx.h, 0), "profiling")
     clk = clocks.stop()
@@ -358,7 +360,10 @@ def run_ours(args, rank, world, local):
                       "bicgstab_iters_per_step": float(np.mean(its)),
                       "parallelism": dist_note,
                       "l2": "inputs larger than L2 (system ~9 GB), no flush"},
-           "e2e": e2e, "gpu_launches": int(launches), "clocks": clk}
+           "e2e": e2e, "gpu_launches": int(launches), "clocks": clk,
+           # timers per stage, CUDA events, ms per Newton iteration
+           "stage_ms": {"assemble": float(stage_ms[0]), "decouple": float(stage_ms[1]),
+                        "precond_setup": float(stage_ms[2]), "krylov": float(stage_ms[3])}}
     # ---- roofline of the dominant kernel class ----------------------------
     hbm, peak_src = peaks()
     algo = algorithmic_bytes(grid, len(wells), case.solver.precond)
