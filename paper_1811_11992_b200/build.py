@@ -41,7 +41,10 @@ def build(force: bool = False, verbose: bool = False) -> str:
         return LIB
     os.makedirs(LIB_DIR, exist_ok=True)
     extra = os.environ.get("ISC_NVCC_EXTRA", "").split()   # experiments, e.g. -DMC_MINB=6
-    cmd = [NVCC, *FLAGS, *extra, "-Xptxas", "-v", "-o", LIB + ".tmp", os.path.join(CSRC, "capi.cu")]
+    flags = list(FLAGS)
+    if os.environ.get("ISC_FMAD") == "1":   # experiment: contracted a*b+c (not the reference's order)
+        flags[flags.index("--fmad=false")] = "--fmad=true"
+    cmd = [NVCC, *flags, *extra, "-Xptxas", "-v", "-o", LIB + ".tmp", os.path.join(CSRC, "capi.cu")]
     res = subprocess.run(cmd, cwd=CSRC, capture_output=True, text=True)
     if res.returncode != 0:
         errs = [ln for ln in res.stderr.splitlines() if "error" in ln.lower()]
