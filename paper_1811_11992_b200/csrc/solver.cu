@@ -666,7 +666,7 @@ __global__ void __launch_bounds__(32 * NU, MC_MINB) k_mc_apply(Dims g, const dou
   __shared__ double wsh[NU][32];
   const int64_t n = g.n;
   const int ls = threadIdx.x, r = threadIdx.y;
-  // colour-blocked storage: pass 1 covers the black half, pass 2 the red half
+  // colour-blocked storage: pass 1 covers the black cells, pass 2 the red cells
   const int64_t t = (int64_t)blockIdx.x * 32 + ls;
   const bool in = t < (g.colored ? g.half : n);
   const int64_t c = g.colored ? (in ? colour_pos(g, PASS == 1 ? 1 : 0, t) : 0) : t;
