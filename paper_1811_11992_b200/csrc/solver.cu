@@ -444,7 +444,10 @@ __device__ void ilu_factor_tile(const Dims& g, const IluDev& L, const double* __
 // levels are separated by a cluster barrier (release/acquire at cluster
 // scope) instead of a grid-wide sync, and values produced by other CTAs of
 // the cluster are read through L2 (__ldcg).
-constexpr int ILC = 4;    // CTAs per cluster (apply; 64 clusters stay resident)
+#ifndef ILC_APPLY
+#define ILC_APPLY 4
+#endif
+constexpr int ILC = ILC_APPLY;    // CTAs per cluster (apply; 64 clusters stay resident)
 constexpr int ILCF = 4;   // CTAs per cluster (factor: 2 CTAs/SM -> one resident wave)
 
 __global__ void __cluster_dims__(ILCF, 1, 1) __launch_bounds__(IL_SLOTS * NU, 2)
@@ -464,7 +467,7 @@ __global__ void __cluster_dims__(ILCF, 1, 1) __launch_bounds__(IL_SLOTS * NU, 2)
 }
 
 // forward then backward sweep; z_out (global, SoA) gets the owned slots
-__global__ void __cluster_dims__(ILC, 1, 1) __launch_bounds__(IL_SLOTS * NU)
+__global__ void __cluster_dims__(ILC, 1, 1) __launch_bounds__(IL_SLOTS * NU, 2)
     k_ilu_apply(Dims g, IluDev L, const double* offd, const int64_t* __restrict__ sub_ptr,
                 int nlev, const double* __restrict__ rin, double* __restrict__ zout) {
   cg::cluster_group cluster = cg::this_cluster();
@@ -477,16 +480,29 @@ __global__ void __cluster_dims__(ILC, 1, 1) __launch_bounds__(IL_SLOTS * NU)
   for (int lev = 0; lev < nlev; ++lev) {
     const int64_t b = lp[lev], e = lp[lev + 1];
     for (int64_t s = b + (int64_t)crank * IL_SLOTS + ls; s < e; s += (int64_t)ILC * IL_SLOTS) {
+      // every load of the slot issued before the first use (the level's
+      // latency is one round trip, not one per neighbour)
       const int64_t c = L.cell[s];
+      int64_t sj[3];
+#pragma unroll
+      for (int q = 0; q < 3; ++q) sj[q] = L.lo[q * ns + s];
+      double lb[3][NU], zn[3][NU];
+#pragma unroll
+      for (int q = 0; q < 3; ++q) {
+        const int64_t jj = sj[q] >= 0 ? sj[q] : s;
+#pragma unroll
+        for (int u = 0; u < NU; ++u) {
+          lb[q][u] = L.lblk[(int64_t)(q * NB + r * NU + u) * ns + s];
+          zn[q][u] = __ldcg(L.zs + (int64_t)u * ns + jj);
+        }
+      }
       double z = rin[r * n + c];
 #pragma unroll
       for (int q = 0; q < 3; ++q) {
-        const int64_t sj = L.lo[q * ns + s];
-        if (sj < 0) continue;
+        if (sj[q] < 0) continue;
         double t = 0.0;
 #pragma unroll
-        for (int u = 0; u < NU; ++u)
-          t += L.lblk[(int64_t)(q * NB + r * NU + u) * ns + s] * __ldcg(L.zs + (int64_t)u * ns + sj);
+        for (int u = 0; u < NU; ++u) t += lb[q][u] * zn[q][u];
         z -= t;
       }
       L.zs[(int64_t)r * ns + s] = z;
@@ -503,15 +519,26 @@ __global__ void __cluster_dims__(ILC, 1, 1) __launch_bounds__(IL_SLOTS * NU)
       int64_t c = 0;
       if (live) {
         c = L.cell[s];
+        int64_t sj[3];
+#pragma unroll
+        for (int q = 0; q < 3; ++q) sj[q] = L.up[q * ns + s];
+        double ab[3][NU], zn[3][NU];
+#pragma unroll
+        for (int q = 0; q < 3; ++q) {
+          const int64_t jj = sj[q] >= 0 ? sj[q] : s;
+#pragma unroll
+          for (int u = 0; u < NU; ++u) {
+            ab[q][u] = L.aup[(int64_t)(q * NB + r * NU + u) * ns + s];
+            zn[q][u] = __ldcg(L.zs + (int64_t)u * ns + jj);
+          }
+        }
         w = __ldcg(L.zs + (int64_t)r * ns + s);
 #pragma unroll
         for (int q = 0; q < 3; ++q) {
-          const int64_t sj = L.up[q * ns + s];
-          if (sj < 0) continue;
+          if (sj[q] < 0) continue;
           double t = 0.0;
 #pragma unroll
-          for (int u = 0; u < NU; ++u)
-            t += L.aup[(int64_t)(q * NB + r * NU + u) * ns + s] * __ldcg(L.zs + (int64_t)u * ns + sj);
+          for (int u = 0; u < NU; ++u) t += ab[q][u] * zn[q][u];
           w -= t;
         }
       }
