@@ -448,7 +448,10 @@ __device__ void ilu_factor_tile(const Dims& g, const IluDev& L, const double* __
 #define ILC_APPLY 4
 #endif
 constexpr int ILC = ILC_APPLY;    // CTAs per cluster (apply; 64 clusters stay resident)
-constexpr int ILCF = 4;   // CTAs per cluster (factor: 2 CTAs/SM -> one resident wave)
+#ifndef ILCF_FACTOR
+#define ILCF_FACTOR 4
+#endif
+constexpr int ILCF = ILCF_FACTOR;   // CTAs per cluster (factor: 2 CTAs/SM -> one resident wave)
 
 __global__ void __cluster_dims__(ILCF, 1, 1) __launch_bounds__(IL_SLOTS * NU, 2)
     k_ilu_factor(Dims g, IluDev L, const double* offd, const int64_t* __restrict__ sub_ptr,
