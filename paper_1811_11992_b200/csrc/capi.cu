@@ -50,6 +50,7 @@ struct isc_ctx {
   cudaStream_t own_stream = nullptr;
   cudaStream_t cstream = nullptr;          // host->device staging copies (isc_assemble_host)
   cudaEvent_t chunk_ev[8] = {};
+  cudaEvent_t halo_ev[2] = {};             // halo planes packed / landed
   bool cell_pre = false;                   // k_cell already ran (pipelined host staging)
   bool face_pre = false;                   // k_face_eval too
   bool mc_schur = true;   // mcilu: red-eliminated BiCGSTAB (ISC_MCILU_FULL=1: full system)
@@ -359,6 +360,7 @@ extern "C" int isc_create(const isc_model_desc* md, const isc_grid_desc* gdsc, i
   ctx->stream = ctx->own_stream;
   CK(cudaStreamCreateWithFlags(&ctx->cstream, cudaStreamNonBlocking));
   for (auto& e : ctx->chunk_ev) CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+  for (auto& e : ctx->halo_ev) CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
   for (auto& e : ctx->ev) CK(cudaEventCreate(&e));
   // static grid arrays
   ALLOC(ctx->depth, n * 8); ALLOC(ctx->vol, n * 8); ALLOC(ctx->phi_ref, n * 8);
@@ -475,6 +477,8 @@ extern "C" int isc_destroy(isc_ctx* ctx) {
   if (ctx->own_stream) cudaStreamDestroy(ctx->own_stream);
   if (ctx->cstream) cudaStreamDestroy(ctx->cstream);
   for (auto& e : ctx->chunk_ev)
+    if (e) cudaEventDestroy(e);
+  for (auto& e : ctx->halo_ev)
     if (e) cudaEventDestroy(e);
   delete ctx;
   return ISC_OK;
@@ -1251,7 +1255,12 @@ extern "C" int isc_comm_hub(isc_ctx* ctx, void* hub, int32_t rank, int32_t has_l
 }
 
 // one-plane halo of a storage-order vector (rows x n)
-static int halo_exchange(isc_ctx* ctx, double* v, int rows) {
+// Halo exchange in two halves so that work not touching the ghost planes
+// can run in between: halo_start packs the boundary planes on the main
+// stream; halo_finish moves them on the copy stream (NCCL send/recv, or
+// device copies between hub contexts), unpacks into the ghost planes there
+// and makes the main stream wait for it.
+static int halo_start(isc_ctx* ctx, double* v, int rows) {
   Comm& cm = ctx->comm;
   if (!cm.active()) return ISC_OK;
   const Dims& g = ctx->g;
@@ -1262,41 +1271,61 @@ static int halo_exchange(isc_ctx* ctx, double* v, int rows) {
   if (cm.has_hi) k_pack_plane<<<bl, 256, 0, st>>>(g, rows, g.kw_hi - 1, v, ctx->halo_send_hi);
   ctx->launches += (cm.has_lo ? 1 : 0) + (cm.has_hi ? 1 : 0);
   CK(cudaGetLastError());
+  CK(cudaEventRecord(ctx->halo_ev[0], st));
+  return ISC_OK;
+}
+
+static int halo_finish(isc_ctx* ctx, double* v, int rows) {
+  Comm& cm = ctx->comm;
+  if (!cm.active()) return ISC_OK;
+  const Dims& g = ctx->g;
+  cudaStream_t st = ctx->stream, cs = ctx->cstream;
+  const int64_t cnt = (int64_t)rows * g.nxny;
+  const int bl = grid1d(cnt, 256);
+  CK(cudaStreamWaitEvent(cs, ctx->halo_ev[0], 0));
   if (cm.nccl) {
     NcclApi& api = nccl_api();
     api.GroupStart();
     if (cm.has_lo) {
-      api.Send(ctx->halo_send_lo, cnt, ncclFloat64_, cm.rank - 1, cm.nccl, st);
-      api.Recv(ctx->halo_recv_lo, cnt, ncclFloat64_, cm.rank - 1, cm.nccl, st);
+      api.Send(ctx->halo_send_lo, cnt, ncclFloat64_, cm.rank - 1, cm.nccl, cs);
+      api.Recv(ctx->halo_recv_lo, cnt, ncclFloat64_, cm.rank - 1, cm.nccl, cs);
     }
     if (cm.has_hi) {
-      api.Send(ctx->halo_send_hi, cnt, ncclFloat64_, cm.rank + 1, cm.nccl, st);
-      api.Recv(ctx->halo_recv_hi, cnt, ncclFloat64_, cm.rank + 1, cm.nccl, st);
+      api.Send(ctx->halo_send_hi, cnt, ncclFloat64_, cm.rank + 1, cm.nccl, cs);
+      api.Recv(ctx->halo_recv_hi, cnt, ncclFloat64_, cm.rank + 1, cm.nccl, cs);
     }
     const int r = api.GroupEnd();
     if (r != ncclSuccess_) { g_err = "NCCL halo exchange failed"; return ISC_CUDA_ERROR; }
   } else if (cm.hub) {
     Hub* h = cm.hub;
-    CK(cudaEventRecord(h->ready[cm.rank], st));
+    CK(cudaEventRecord(h->ready[cm.rank], cs));   // after the pack (cs waited for it)
     h->barrier();
     if (cm.has_lo) {
-      CK(cudaStreamWaitEvent(st, h->ready[cm.rank - 1], 0));
+      CK(cudaStreamWaitEvent(cs, h->ready[cm.rank - 1], 0));
       CK(cudaMemcpyAsync(ctx->halo_recv_lo, h->send_hi[cm.rank - 1], cnt * 8,
-                         cudaMemcpyDeviceToDevice, st));
+                         cudaMemcpyDeviceToDevice, cs));
     }
     if (cm.has_hi) {
-      CK(cudaStreamWaitEvent(st, h->ready[cm.rank + 1], 0));
+      CK(cudaStreamWaitEvent(cs, h->ready[cm.rank + 1], 0));
       CK(cudaMemcpyAsync(ctx->halo_recv_hi, h->send_lo[cm.rank + 1], cnt * 8,
-                         cudaMemcpyDeviceToDevice, st));
+                         cudaMemcpyDeviceToDevice, cs));
     }
-    CK(cudaStreamSynchronize(st));
+    CK(cudaStreamSynchronize(cs));
     h->barrier();   // neighbours may now reuse their send buffers
   }
-  if (cm.has_lo) k_unpack_plane<<<bl, 256, 0, st>>>(g, rows, g.kw_lo - 1, ctx->halo_recv_lo, v);
-  if (cm.has_hi) k_unpack_plane<<<bl, 256, 0, st>>>(g, rows, g.kw_hi, ctx->halo_recv_hi, v);
+  if (cm.has_lo) k_unpack_plane<<<bl, 256, 0, cs>>>(g, rows, g.kw_lo - 1, ctx->halo_recv_lo, v);
+  if (cm.has_hi) k_unpack_plane<<<bl, 256, 0, cs>>>(g, rows, g.kw_hi, ctx->halo_recv_hi, v);
   ctx->launches += (cm.has_lo ? 1 : 0) + (cm.has_hi ? 1 : 0);
   CK(cudaGetLastError());
+  CK(cudaEventRecord(ctx->halo_ev[1], cs));
+  CK(cudaStreamWaitEvent(st, ctx->halo_ev[1], 0));
   return ISC_OK;
+}
+
+static int halo_exchange(isc_ctx* ctx, double* v, int rows) {
+  int s = halo_start(ctx, v, rows);
+  if (s) return s;
+  return halo_finish(ctx, v, rows);
 }
 
 // sum `count` consecutive device scalars over the ranks (in place)
@@ -1577,6 +1606,64 @@ static int bicgstab_schur(isc_ctx* ctx, double tol, int maxiter, int* iters) {
   sh[S_BB] = nb * nb;
   bool restarted = false, first = true;
   int it = 0;
+  // One half pass over the owned planes. On slabs the planes next to the
+  // ghost planes wait for the halo exchange of their input, the interior
+  // runs while it is in flight (red: z_b in, w_r out; black: w_r in, v_b and
+  // the dot partials out, partial slots interior | low | high).
+  const bool slab = ctx->comm.active();
+  auto plane_dims = [&](int64_t k0, int64_t k1) {
+    Dims d = g;
+    d.tw_lo = k0 * g.ph;
+    d.tw_hi = k1 * g.ph;
+    return d;
+  };
+  const int64_t klo = g.kw_lo, khi = g.kw_hi;
+  const bool split = slab && khi - klo >= 3;
+  const Dims gi = plane_dims(klo + 1, khi - 1), gl = plane_dims(klo, klo + 1),
+             gh = plane_dims(khi - 1, khi);
+  const int bi = split ? grid1d(gi.tw_hi - gi.tw_lo, 32) : 0;
+  const int bl1 = split ? grid1d(gl.tw_hi - gl.tw_lo, 32) : 0;
+  const int bh1 = split ? grid1d(gh.tw_hi - gh.tw_lo, 32) : 0;
+  const int bparts = split ? bi + bl1 + bh1 : bh;   // black-pass partial slots (blocks)
+  auto red_pass = [&](double* z) -> int {
+    if (!split) {
+      TRY(halo_exchange(ctx, z, NU));
+      k_sc_red<<<bh, dim3(32, NU), 0, st>>>(g, ctx->offd, z);
+      ++ctx->launches;
+      return cudaGetLastError() == cudaSuccess ? 0 : ISC_CUDA_ERROR;
+    }
+    TRY(halo_start(ctx, z, NU));
+    k_sc_red<<<bi, dim3(32, NU), 0, st>>>(gi, ctx->offd, z);
+    TRY(halo_finish(ctx, z, NU));
+    k_sc_red<<<bl1, dim3(32, NU), 0, st>>>(gl, ctx->offd, z);
+    k_sc_red<<<bh1, dim3(32, NU), 0, st>>>(gh, ctx->offd, z);
+    ctx->launches += 3;
+    return cudaGetLastError() == cudaSuccess ? 0 : ISC_CUDA_ERROR;
+  };
+  auto black_pass = [&](int K, double* z, double* vout, const double* w0,
+                        const double* w1) -> int {
+    auto launch = [&](const Dims& d, int blocks, int slot0) {
+      if (K == 1)
+        k_mc_black_spmv<1><<<blocks, dim3(32, NU), 0, st>>>(d, ctx->offd, z, vout, w0, w1,
+                                                            ctx->partial, bparts, slot0);
+      else
+        k_mc_black_spmv<2><<<blocks, dim3(32, NU), 0, st>>>(d, ctx->offd, z, vout, w0, w1,
+                                                            ctx->partial, bparts, slot0);
+    };
+    if (!split) {
+      TRY(halo_exchange(ctx, z, NU));
+      launch(g, bh, 0);
+      ++ctx->launches;
+      return cudaGetLastError() == cudaSuccess ? 0 : ISC_CUDA_ERROR;
+    }
+    TRY(halo_start(ctx, z, NU));
+    launch(gi, bi, 0);
+    TRY(halo_finish(ctx, z, NU));
+    launch(gl, bl1, bi);
+    launch(gh, bh1, bi + bl1);
+    ctx->launches += 3;
+    return cudaGetLastError() == cudaSuccess ? 0 : ISC_CUDA_ERROR;
+  };
   auto dot_b = [&](const double* a, const double* c, int slot) -> int {
     KScope ks(ctx, KT_VEC);
     k_sc_dot<<<RED_BLOCKS, RED_THREADS, 0, st>>>(g, a, c, ctx->partial);
@@ -1596,12 +1683,9 @@ static int bicgstab_schur(isc_ctx* ctx, double tol, int maxiter, int* iters) {
   auto restart = [&]() -> int {
     // r_b = g_b - S x_b; rhat = r; p = v = 0 (linsolve.py:509-519)
     {
-      if (halo_exchange(ctx, x, NU)) return ISC_CUDA_ERROR;
       KScope ks(ctx, KT_SPMV);
-      k_sc_red<<<bh, dim3(32, NU), 0, st>>>(g, ctx->offd, x);   // red part of x: scratch
-      if (halo_exchange(ctx, x, NU)) return ISC_CUDA_ERROR;
-      k_mc_black_spmv<1><<<bh, dim3(32, NU), 0, st>>>(g, ctx->offd, x, t, rhat, nullptr,
-                                                      ctx->partial, bh, 0);
+      if (red_pass(x)) return ISC_CUDA_ERROR;   // red part of x: scratch
+      if (black_pass(1, x, t, rhat, nullptr)) return ISC_CUDA_ERROR;
       k_sc_rhs<<<bh, dim3(32, NU), 0, st>>>(g, ctx->offd, b, v, shat);   // g_b (scratch)
     }
     k_sc_sub<<<RED_BLOCKS, RED_THREADS, 0, st>>>(g, v, t, r, rhat);
@@ -1634,20 +1718,17 @@ static int bicgstab_schur(isc_ctx* ctx, double tol, int maxiter, int* iters) {
       KScope ks(ctx, KT_VEC);
       k_sc_update_p<<<RED_BLOCKS, RED_THREADS, 0, st>>>(g, r, p, v, uinv, phat, ctx->sc);
     }
-    TRY(halo_exchange(ctx, phat, NU));   // z_b of other ranks' boundary planes
+    ++ctx->launches;   // update_p
     {
       KScope ks(ctx, KT_ILU_APPLY);
-      k_sc_red<<<bh, dim3(32, NU), 0, st>>>(g, ctx->offd, phat);
+      TRY(red_pass(phat));
     }
-    TRY(halo_exchange(ctx, phat, NU));   // w_r likewise
     {
       KScope ks(ctx, KT_SPMV);
-      k_mc_black_spmv<1><<<bh, dim3(32, NU), 0, st>>>(g, ctx->offd, phat, v, rhat, nullptr,
-                                                      ctx->partial, bh, 0);
+      TRY(black_pass(1, phat, v, rhat, nullptr));
     }
-    ctx->launches += 3;
     CK(cudaGetLastError());
-    TRY(K.finalize1(bh * NU, S_DEN));
+    TRY(K.finalize1(bparts * NU, S_DEN));
     {
       KScope ks(ctx, KT_VEC);
       k_sc_update_s<<<RED_BLOCKS, RED_THREADS, 0, st>>>(g, r, v, s, uinv, shat, ctx->sc,
@@ -1676,20 +1757,16 @@ static int bicgstab_schur(isc_ctx* ctx, double tol, int maxiter, int* iters) {
       return ISC_OK;
     }
     TRY(K.push());
-    TRY(halo_exchange(ctx, shat, NU));
     {
       KScope ks(ctx, KT_ILU_APPLY);
-      k_sc_red<<<bh, dim3(32, NU), 0, st>>>(g, ctx->offd, shat);
+      TRY(red_pass(shat));
     }
-    TRY(halo_exchange(ctx, shat, NU));
     {
       KScope ks(ctx, KT_SPMV);
-      k_mc_black_spmv<2><<<bh, dim3(32, NU), 0, st>>>(g, ctx->offd, shat, t, nullptr, s,
-                                                      ctx->partial, bh, 0);
+      TRY(black_pass(2, shat, t, nullptr, s));
     }
-    ctx->launches += 2;
     CK(cudaGetLastError());
-    TRY(K.finalize2(bh * NU, S_TT, S_TS));
+    TRY(K.finalize2(bparts * NU, S_TT, S_TS));
     {
       KScope ks(ctx, KT_VEC);
       k_sc_update_xr<<<RED_BLOCKS, RED_THREADS, 0, st>>>(g, x, phat, shat, r, s, t, rhat,
