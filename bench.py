@@ -388,6 +388,8 @@ def run_ours(args, rank, world, local):
     traffic, tsrc = ncu_traffic(dom, case.solver.precond)
     out["roofline"] = {"kernel": dom, "bound": "hbm", "achieved": rows[dom]["achieved_gbs"],
                        "peak": hbm, "unit": "GB/s", "frac": rows[dom]["achieved_gbs"] / hbm,
+                       # north_star quotes the ~8 TB/s HBM3e spec
+                       "frac_of_8tbs_spec": rows[dom]["achieved_gbs"] / 8000.0,
                        "traffic": traffic, "traffic_source": tsrc, "peak_source": peak_src,
                        "kernels": rows, "kernel_ms": ktimes}
     return out, sim
@@ -505,6 +507,33 @@ def run_oracle(steps, warmup, budget_s=None):
             "seconds": el}
 
 
+def run_timesteps(config="c4", nsteps=2):
+    """whole timesteps of the C4 run through newton.Simulator.advance
+    (multicolour solve): Newton counts two ways (residual evaluations, solves),
+    BiCGSTAB iterations, wall time (the driver's host logic included)."""
+    import time as _t
+    import torch
+    from dataclasses import replace
+    from paper_1811_11992_b200 import configs
+    from paper_1811_11992_b200.newton import Simulator
+    case = configs.config(config)
+    case = replace(case, solver=replace(case.solver, precond="mcilu"),
+                   schedule=replace(case.schedule, t_end=nsteps * case.schedule.dt_init))
+    grid, pack, wells, streams, state = configs.build_case(case)
+    sim = Simulator(grid, pack, wells, streams, state, case.schedule, case.solver)
+    torch.cuda.synchronize()
+    t0 = _t.perf_counter()
+    sim.advance()
+    torch.cuda.synchronize()
+    wall = _t.perf_counter() - t0
+    out = {"config": config, "precond": "mcilu",
+           "steps": [{"time": s.time, "dt": s.dt, "newton": s.newton, "solves": s.solves,
+                      "linear": s.linear} for s in sim.steps],
+           "wall_s": wall, "cumulative_imbalance": float(sim.cumulative_imbalance())}
+    sim.ctx.close()
+    return out
+
+
 def run_numjac(config="c4", reps=3):
     """JACOBIAN numeric (assembly.py:843-939) at the C4 initial
     state — 2 probes x 9 unknowns per cell, each a full cell_eval + six face
@@ -601,6 +630,11 @@ def main():
                 out["spmv_c5"] = run_spmv_c5()
             except Exception as exc:  # report, never hide
                 out["spmv_c5"] = {"error": repr(exc)}
+        if not args.no_spmv:
+            try:
+                out["timesteps_c4"] = run_timesteps(args.config)
+            except Exception as exc:  # report, never hide
+                out["timesteps_c4"] = {"error": repr(exc)}
         if not args.no_spmv:
             try:
                 out["numeric_jacobian_c4"] = run_numjac(args.config)
