@@ -969,12 +969,10 @@ extern "C" int isc_decouple(isc_ctx* ctx, int64_t* bad_cell, int32_t* bad_col) {
 #define DECOUPLE_WS 1
 #endif
   if (DECOUPLE_WS) {
-    static bool attr = false;
-    if (!attr) {
-      CK(cudaFuncSetAttribute(k_decouple_ws, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                              (int)sizeof(WsSmem)));
-      attr = true;
-    }
+    // once per process (thread-safe static init: hub ranks share the process)
+    static const cudaError_t attr = cudaFuncSetAttribute(
+        k_decouple_ws, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(WsSmem));
+    CK(attr);
     int dev = 0, sms = 148;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
