@@ -224,6 +224,11 @@ def make_report_frames():
     np.savez_compressed(os.path.join(HERE, "report_frames.npz"), **out)
 
 
+def make_traj_c3():
+    """BASELINE configs[2]: 60x60x20 (72k cells), 20 timesteps, LINEAR_TOL 1e-10."""
+    make_traj("c3", 1e-10)
+
+
 def make_traj_numeric():
     """C1 run in JACOBIAN numeric mode (newton.py:228, 278)."""
     make_traj("c1", 1e-10, jacobian="numeric")
@@ -232,7 +237,7 @@ def make_traj_numeric():
 def make_traj(name, ltol, jacobian=None):
     case = configs.config(name)
     case = replace(case, solver=replace(case.solver, linear_tol=ltol))
-    sim = reference_simulator(case, threads=4, jacobian=jacobian)
+    sim = reference_simulator(case, threads=min(16, os.cpu_count() or 4), jacobian=jacobian)
     sim.advance()
     rec = np.array([(s.time, s.dt, s.newton, s.linear, s.solves, s.balance)
                     for s in sim.steps])
@@ -259,5 +264,6 @@ if __name__ == "__main__":
     make_traj("c1", 1e-5)
     make_traj("c2", 1e-10)
     make_traj("c2", 1e-5)
+    make_traj_c3()
     for f in sorted(os.listdir(HERE)):
         print(f, os.path.getsize(os.path.join(HERE, f)))

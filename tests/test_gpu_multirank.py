@@ -99,14 +99,16 @@ def test_slab_assembly_and_solve_match_single_gpu(nranks):
     hub.close()
 
 
-def test_slab_newton_run_matches_single_gpu():
-    """C2 (20x20x5) split over 2 emulated ranks: 4 timesteps with
-    LINEAR_TOL 1e-10 give the single-GPU Newton counts and fields."""
+@pytest.mark.parametrize("name,nsteps", [("c2", 4), ("c3", 6)])
+def test_slab_newton_run_matches_single_gpu(name, nsteps):
+    """C2 (20x20x5) / C3 (60x60x20, BASELINE's "1 and 2 GPUs" case) split over
+    2 emulated ranks: timesteps with LINEAR_TOL 1e-10 give the single-GPU
+    Newton counts and fields."""
     from dataclasses import replace
     from paper_1811_11992_b200.newton import Simulator
-    case = configs.config("c2")
+    case = configs.config(name)
     case = replace(case, solver=replace(case.solver, linear_tol=1e-10, precond="mcilu"),
-                   schedule=replace(case.schedule, t_end=4 * case.schedule.dt_init))
+                   schedule=replace(case.schedule, t_end=nsteps * case.schedule.dt_init))
     grid, pack, wells, streams, state = configs.build_case(case)
     ref = Simulator(grid, pack, wells, streams, state, case.schedule, case.solver)
     ref.advance()

@@ -133,7 +133,8 @@ def test_synthetic_microbench_vs_reference():
 @pytest.mark.parametrize("name,tol,jac,precond", [
     ("c1", 1e-10, "analytic", None), ("c2", 1e-10, "analytic", None),
     ("c1", 1e-5, "analytic", None), ("c1", 1e-10, "numeric", None),
-    ("c2", 1e-10, "analytic", "mcilu")])
+    ("c2", 1e-10, "analytic", "mcilu"),
+    ("c3", 1e-10, "analytic", None), ("c3", 1e-10, "analytic", "mcilu")])
 def test_trajectory_vs_reference(name, tol, jac, precond):
     """Whole runs: equal step and Newton sequences, fields within 1e-6
     (jac "numeric": the reference's JACOBIAN numeric mode, newton.py:228,278;
