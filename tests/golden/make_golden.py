@@ -229,6 +229,27 @@ def make_traj_c3():
     make_traj("c3", 1e-10)
 
 
+def make_traj_c4_sample():
+    """BASELINE configs[3] (200x200x50, 2 M cells, 5 timesteps) at the deck's
+    LINEAR_TOL 1e-5 with the reference's RAS: per-step records and a seeded
+    sample of 4096 cells of the final fields (the full fields would be 150 MB)."""
+    case = configs.config("c4")
+    sim = reference_simulator(case, threads=min(16, os.cpu_count() or 4))
+    sim.advance()
+    rec = np.array([(s.time, s.dt, s.newton, s.linear, s.solves, s.balance)
+                    for s in sim.steps])
+    rng = np.random.default_rng(99)
+    idx = np.sort(rng.choice(sim.grid.ncell, 4096, replace=False))
+    out = {"steps": rec, "cum_imbalance": np.array(sim.cumulative_imbalance()),
+           "sample_idx": idx, "final_bhp": np.asarray(sim.state.bhp)}
+    for f in ("p", "t", "sw", "sg", "cc"):
+        a = np.asarray(getattr(sim.state, f))
+        out["sample_" + f] = a[idx]
+        out["norm_" + f] = np.array(np.linalg.norm(a))
+    np.savez_compressed(os.path.join(HERE, "traj_c4_sample.npz"), **out)
+    print("c4", sim.totals())
+
+
 def make_traj_numeric():
     """C1 run in JACOBIAN numeric mode (newton.py:228, 278)."""
     make_traj("c1", 1e-10, jacobian="numeric")

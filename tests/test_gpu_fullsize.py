@@ -7,7 +7,10 @@ of GB), so these tests check properties that hold at any size:
     (2 emulated ranks through the in-process hub);
   * the red-eliminated and full-system forms of the multicolour solve agree
     to the Krylov tolerance, and the returned du satisfies the decoupled
-    system (SpMV residual).
+    system (SpMV residual);
+  * the whole 5-step C4 run reproduces the reference's step / Newton sequence
+    and a seeded sample of its final fields (traj_c4_sample.npz, made by the
+    reference here).
 """
 
 import numpy as np
@@ -117,3 +120,37 @@ def test_c4_mcilu_forms_agree_and_solve_decoupled_system(c4, monkeypatch):
     (a, da, ia), (b2, db, ib) = sols[False], sols[True]
     assert np.linalg.norm(a - b2) <= 1e-5 * np.linalg.norm(b2)
     assert ia <= ib + 1, (ia, ib)
+
+
+@pytest.mark.parametrize("precond", ["ras", "mcilu"])
+def test_c4_run_vs_reference(precond):
+    """BASELINE configs[3] end to end: the 5 timesteps of the reference's C4
+    run (its RAS, deck LINEAR_TOL 1e-5; traj_c4_sample.npz) — equal step and
+    Newton sequences, sampled final fields and field norms within 1e-6. With
+    the multicolour solve the Newton sequence is checked at the same
+    tolerance (the linear iterates differ, the outer iteration must not)."""
+    from tests.helpers import golden
+    from paper_1811_11992_b200.newton import Simulator
+    from dataclasses import replace
+    g = golden("traj_c4_sample.npz")
+    case = configs.config("c4")
+    case = replace(case, solver=replace(case.solver, precond=precond))
+    grid, pack, wells, streams, state = configs.build_case(case)
+    sim = Simulator(grid, pack, wells, streams, state, case.schedule, case.solver)
+    sim.advance()
+    rec = np.array([(s.time, s.dt, s.newton, s.linear, s.solves) for s in sim.steps])
+    ref = g["steps"]
+    assert rec.shape[0] == ref.shape[0]
+    np.testing.assert_array_equal(rec[:, 2], ref[:, 2])
+    if precond == "ras":   # same preconditioner: same Krylov iteration counts
+        assert np.all(np.abs(rec[:, 3] - ref[:, 3]) <= rec[:, 4]), (rec[:, 3], ref[:, 3])
+    st = sim.state.to_host()
+    idx = g["sample_idx"]
+    # same linear solver: fields to 1e-6 (SURVEY §8(c)); a different one at
+    # LINEAR_TOL 1e-5 moves the converged state within the Newton tolerance
+    ftol, ntol = (1e-6, 1e-7) if precond == "ras" else (1e-4, 1e-5)
+    for f in ("p", "t", "sw", "sg"):
+        a, b = st[f][idx], g["sample_" + f]
+        assert np.max(np.abs(a - b) / np.maximum(np.abs(b), 1e-3)) <= ftol, f
+        assert abs(np.linalg.norm(st[f]) - float(g["norm_" + f])) <= ntol * float(g["norm_" + f])
+    sim.ctx.close()
