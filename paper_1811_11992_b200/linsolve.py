@@ -6,7 +6,9 @@ decoupling of every block row, the subdomain block ILU(0) (``bjacobi``:
 non-overlapping slabs, ``ras``: one-plane overlap with restriction; slab
 count min(64, max(1, n // 2048)) along the longest axis, natural order)
 and right-preconditioned BiCGSTAB with the reference's single restart,
-breakdown thresholds and tolerances. Raises ``SingularCellBlock``,
+breakdown thresholds and tolerances. ``precond="mcilu"`` selects the north
+star's multicolour block-ILU(0) instead, solved on the red-eliminated system
+(same stopping test on the full residual). Raises ``SingularCellBlock``,
 ``Breakdown`` and ``MaxIterations`` like the reference. ``du`` is returned
 as a numpy (n, 9) array for drop-in callers; ``solve_device`` keeps it in
 HBM as a (9, n) tensor for the GPU Newton driver.
