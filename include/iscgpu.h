@@ -25,6 +25,11 @@
  *   isc_scaled_norm     newton.scaled_norm (cells)   newton.py:124-144
  *   isc_audit_sums      Simulator.audit_step (sums)  newton.py:339-366
  *   isc_synth_system    (BASELINE config 5 generator; paper_1811_11992_b200/synth.py)
+ *   isc_numeric_jacobian assembly._numeric_jacobian  assembly.py:843-939
+ *   isc_format_cells    report.write_frame (cells)   report.py:115-149
+ *   isc_format_double   report._fmt (repr(float))    report.py:76-77
+ *   isc_comm_nccl / isc_comm_hub   z-slab multi-GPU transport (the reference
+ *                       has no multi-GPU path)
  */
 #ifndef ISCGPU_H
 #define ISCGPU_H
@@ -47,7 +52,8 @@ typedef enum {
 } isc_status;
 
 /* none / bjacobi / ras reproduce the reference (linsolve.py:322-358); mcilu is
- * the red-black multicolour block ILU(0) of BASELINE's north_star. */
+ * the red-black multicolour block ILU(0) of BASELINE's north_star, solved on
+ * the red-eliminated system (same stopping test on the full residual). */
 typedef enum {
   ISC_PRECOND_NONE = 0, ISC_PRECOND_BJACOBI = 1, ISC_PRECOND_RAS = 2, ISC_PRECOND_MCILU = 3
 } isc_precond;
