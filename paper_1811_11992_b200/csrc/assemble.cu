@@ -430,7 +430,7 @@ __device__ __forceinline__ void cell_eval(const Model& M, const CellArgs& A, int
   {
     const double pg = p + pcog;
     const double ccr = cc > 0.0 ? cc : 0.0;
-#pragma unroll
+#pragma unroll 1
     for (int q = 0; q < MAXREAC; ++q) {
       rr_on[q] = false;
       rr_v[q] = 0.0;
