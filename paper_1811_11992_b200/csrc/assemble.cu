@@ -505,7 +505,7 @@ __device__ __forceinline__ void cell_eval(const Model& M, const CellArgs& A, int
   const double duc_t = rk[RK_COKE_CP];
   const double hl = A.hl_area ? A.hl_area[c] : 0.0;
 
-#pragma unroll
+#pragma unroll 1
   for (int r = 0; r < NU; ++r) {
     double accr, dacc[NU];
     if (r == 0) {
