@@ -49,7 +49,7 @@ def _single(c, st, accn, precond, tol):
     return out
 
 
-@pytest.mark.parametrize("nranks", [2, 3])
+@pytest.mark.parametrize("nranks", [2, 3, 5])   # 5: ranks with one owned plane
 def test_slab_assembly_and_solve_match_single_gpu(nranks):
     c = case_objects("sub2")
     st, accn = random_state_like_reference(c, 31)
