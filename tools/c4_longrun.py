@@ -1,0 +1,21 @@
+"""Demo: 40 timesteps of C4 (2 M cells) through newton.Simulator.advance with the
+multicolour solve; prints the run totals (steps, Newton evaluations, BiCGSTAB
+iterations), wall time and the conservation audit. B200: 2.5 s for 91 Newton
+iterations."""
+import sys, time
+sys.path.insert(0, ".")
+from dataclasses import replace
+import torch
+from paper_1811_11992_b200 import configs
+from paper_1811_11992_b200.newton import Simulator
+case = configs.config("c4")
+case = replace(case, solver=replace(case.solver, precond="mcilu"),
+               schedule=replace(case.schedule, t_end=40 * case.schedule.dt_init))
+grid, pack, wells, streams, state = configs.build_case(case)
+sim = Simulator(grid, pack, wells, streams, state, case.schedule, case.solver)
+t0 = time.perf_counter()
+sim.advance()
+torch.cuda.synchronize()
+print("steps", len(sim.steps), "totals", sim.totals(), "wall", round(time.perf_counter() - t0, 2),
+      "imbalance", sim.cumulative_imbalance())
+print([ (s.newton, s.solves, s.linear) for s in sim.steps[:10]], "...", [(s.newton, s.solves, s.linear) for s in sim.steps[-5:]])
