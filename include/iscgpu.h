@@ -58,6 +58,13 @@ typedef enum {
   ISC_PRECOND_NONE = 0, ISC_PRECOND_BJACOBI = 1, ISC_PRECOND_RAS = 2, ISC_PRECOND_MCILU = 3
 } isc_precond;
 
+/* Krylov method on the mcilu red-eliminated system: the reference's
+ * BiCGSTAB control flow (default; linsolve.py:481-578) or restarted
+ * right-preconditioned GMRES(m) (north_star "BiCGSTAB/GMRES"; same
+ * preconditioner, same stopping test ||r||/||b|| <= tol). Other
+ * preconditioners always run BiCGSTAB. */
+typedef enum { ISC_KRYLOV_BICGSTAB = 0, ISC_KRYLOV_GMRES = 1 } isc_krylov;
+
 typedef struct isc_ctx isc_ctx;
 
 /* Flattened model constants: the reference's ModelPack (assembly.py:42-68),
@@ -167,6 +174,10 @@ int isc_import_system(isc_ctx *ctx, const double *d_diag, const double *d_offd,
 int isc_set_wells_out(isc_ctx *ctx, const double *h_wells_out);
 /* Switch preconditioner (rebuilds the subdomain/level structure). */
 int isc_set_precond(isc_ctx *ctx, int32_t precond);
+/* Select the Krylov method (isc_krylov); restart = GMRES restart length
+ * 1..31 (0 keeps the current, default 30). No reference counterpart: an
+ * extension of linsolve.BlockSolver's solve (linsolve.py:481-578). */
+int isc_set_krylov(isc_ctx *ctx, int32_t krylov, int32_t restart);
 /* Generate the seeded synthetic system of BASELINE config 5 in place. */
 int isc_synth_system(isc_ctx *ctx, uint64_t seed);
 

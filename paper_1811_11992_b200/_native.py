@@ -21,6 +21,7 @@ LIB_PATH = os.path.join(HERE, "_lib", "libiscgpu.so")
 
 ISC_OK, ISC_PSE, ISC_SINGULAR, ISC_BREAKDOWN, ISC_MAXIT = 0, 1, 2, 3, 4
 PRECOND = {"none": 0, "bjacobi": 1, "ras": 2, "mcilu": 3}
+KRYLOV = {"bicgstab": 0, "gmres": 1}
 WELL_OUT = 32
 NREC = 85
 
@@ -74,6 +75,7 @@ _SIGS = {
     "isc_import_system": (ctypes.c_int, [VP, VP, VP, VP, VP]),
     "isc_set_wells_out": (ctypes.c_int, [VP, VP]),
     "isc_set_precond": (ctypes.c_int, [VP, ctypes.c_int32]),
+    "isc_set_krylov": (ctypes.c_int, [VP, ctypes.c_int32, ctypes.c_int32]),
     "isc_synth_system": (ctypes.c_int, [VP, ctypes.c_uint64]),
     "isc_solve": (ctypes.c_int, [VP, ctypes.c_double, ctypes.c_int32, VP, VP,
                                  ctypes.POINTER(ctypes.c_int32), c_int64_p,

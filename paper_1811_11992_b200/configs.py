@@ -49,6 +49,8 @@ class SolverSettings:
     linear_max: int = 200
     precond: str = "ras"
     eps: float = 1e-4
+    krylov: str = "bicgstab"   # mcilu only: "gmres" = restarted GMRES(gmres_restart)
+    gmres_restart: int = 30
 
 
 @dataclass(frozen=True)

@@ -54,6 +54,10 @@ struct isc_ctx {
   bool cell_pre = false;                   // k_cell already ran (pipelined host staging)
   bool face_pre = false;                   // k_face_eval too
   bool mc_schur = true;   // mcilu: red-eliminated BiCGSTAB (ISC_MCILU_FULL=1: full system)
+  int krylov = ISC_KRYLOV_BICGSTAB;   // mcilu red-eliminated system: BiCGSTAB or GMRES(m)
+  int gm_m = 30;                      // GMRES restart length (<= GM_MAXV - 1)
+  double* gm_V = nullptr;             // GMRES basis, gm_m + 1 full-length vectors (lazy)
+  double* gm_h = nullptr;             // GMRES device scalars: h (2 x GM_MAXV+1), y
   int64_t launches = 0;
   // static grid data
   double *depth = nullptr, *vol = nullptr, *phi_ref = nullptr, *gd = nullptr, *td = nullptr,
@@ -439,7 +443,7 @@ extern "C" int isc_create(const isc_model_desc* md, const isc_grid_desc* gdsc, i
   for (double** v : vecs) ALLOC(*v, (size_t)NU * n * 8);
   ALLOC(ctx->sc, S_NSCAL * 8);
   CK(cudaMallocHost(&ctx->sc_h, S_NSCAL * 8));
-  ctx->npartial = std::max<int64_t>((int64_t)RED_BLOCKS * 3 * (NF + 1),
+  ctx->npartial = std::max<int64_t>((int64_t)RED_BLOCKS * std::max(3 * (NF + 1), GM_MAXV + 1),
                                     ((int64_t)grid1d(n, 32) + 2) * NU * 3);
   ALLOC(ctx->partial2, (int64_t)FIN_BLOCKS * 3 * 8);
   ALLOC(ctx->partial, ctx->npartial * 8);
@@ -464,7 +468,8 @@ extern "C" int isc_destroy(isc_ctx* ctx) {
                   ctx->offd, ctx->upw, ctx->bad_d, ctx->rhs, ctx->xk, ctx->rk, ctx->rhat,
                   ctx->pk, ctx->vk, ctx->phat, ctx->shat, ctx->sk, ctx->tk, ctx->sc,
                   ctx->partial, ctx->partial2, ctx->fbuf, ctx->flags, ctx->fail_d, ctx->schur, ctx->st_c, ctx->accn_c, ctx->stage,
-                  ctx->halo_send_lo, ctx->halo_send_hi, ctx->halo_recv_lo, ctx->halo_recv_hi};
+                  ctx->halo_send_lo, ctx->halo_send_hi, ctx->halo_recv_lo, ctx->halo_recv_hi,
+                  ctx->gm_V, ctx->gm_h};
   if (ctx->comm.nccl && nccl_api().CommDestroy) nccl_api().CommDestroy(ctx->comm.nccl);
   free_ilu(ctx);
   for (void* p : ptrs)
@@ -1795,6 +1800,209 @@ static int bicgstab_schur(isc_ctx* ctx, double tol, int maxiter, int* iters) {
   return ISC_MAX_ITERATIONS;
 }
 
+// Restarted right-preconditioned GMRES(m) on the red-eliminated system
+// S x_b = g_b with U_b block-Jacobi (the north star's "BiCGSTAB/GMRES";
+// optional, isc_set_krylov). Arnoldi with classical Gram-Schmidt and one
+// reorthogonalisation (CGS2): two fused multi-dots and two multi-axpys per
+// step, the second one also giving ||w||; the Hessenberg column goes to the
+// host once per step for the Givens rotations. One product S U_b^-1 per
+// iteration (BiCGSTAB: two). Stopping test as bicgstab_schur: ||r|| / ||b||
+// of the full system (the Givens residual estimate within a cycle, the true
+// reduced residual at each restart).
+static int gmres_schur(isc_ctx* ctx, double tol, int maxiter, int* iters) {
+  const int64_t len = (int64_t)NU * ctx->g.n;
+  const Dims& g = ctx->g;
+  cudaStream_t st = ctx->stream;
+  Kry K{ctx, len};
+  const int m = std::max(1, std::min(ctx->gm_m, GM_MAXV - 1));
+  if (!ctx->gm_V) {
+    if (cudaMalloc(&ctx->gm_V, (size_t)GM_MAXV * len * 8) != cudaSuccess ||
+        cudaMalloc(&ctx->gm_h, (size_t)4 * (GM_MAXV + 1) * 8) != cudaSuccess) {
+      cudaGetLastError();
+      g_err = "cannot allocate the GMRES basis";
+      return ISC_CUDA_ERROR;
+    }
+  }
+  double *b = ctx->rhs, *x = ctx->xk, *r = ctx->rk, *z = ctx->phat, *t = ctx->tk,
+         *gb = ctx->shat, *u = ctx->sk;
+  double* V = ctx->gm_V;
+  double *h1 = ctx->gm_h, *h2 = h1 + (GM_MAXV + 1), *yd = h2 + (GM_MAXV + 1);
+  const double* uinv = ctx->mc_uinv;
+  const int bh = grid1d(g.tw_hi - g.tw_lo, 32);
+  CK(cudaMemsetAsync(x, 0, len * 8, st));
+  TRY(K.dot(b, b, S_BB));
+  TRY(K.read_scalars());
+  const double nb = std::sqrt(ctx->sc_h[S_BB]);
+  *iters = 0;
+  if (nb == 0.0) return ISC_OK;
+  TRY(halo_exchange(ctx, b, NU));
+  {
+    KScope ks(ctx, KT_SPMV);
+    k_sc_rhs<<<bh, dim3(32, NU), 0, st>>>(g, ctx->offd, b, r, gb);   // r = g_b (x_b = 0)
+  }
+  ++ctx->launches;
+  auto matvec = [&](double* zz, double* out) -> int {   // out = S zz (zz: black in, red scratch)
+    {
+      KScope ks(ctx, KT_ILU_APPLY);
+      TRY(halo_exchange(ctx, zz, NU));
+      k_sc_red<<<bh, dim3(32, NU), 0, st>>>(g, ctx->offd, zz);
+    }
+    {
+      KScope ks(ctx, KT_SPMV);
+      TRY(halo_exchange(ctx, zz, NU));
+      k_mc_black_spmv<1><<<bh, dim3(32, NU), 0, st>>>(g, ctx->offd, zz, out, zz, nullptr,
+                                                      ctx->partial, bh, 0);
+    }
+    ctx->launches += 2;
+    return cudaGetLastError() == cudaSuccess ? 0 : ISC_CUDA_ERROR;
+  };
+  auto norm2_into = [&](const double* a, int slot) -> int {
+    KScope ks(ctx, KT_VEC);
+    k_sc_dot<<<RED_BLOCKS, RED_THREADS, 0, st>>>(g, a, a, ctx->partial);
+    ++ctx->launches;
+    return K.finalize1(RED_BLOCKS, slot);
+  };
+  auto multidot = [&](int nv, const double* w, double* hout) -> int {
+    KScope ks(ctx, KT_VEC);
+    k_sc_multidot<<<RED_BLOCKS, RED_THREADS, 0, st>>>(g, V, len, nv, w, ctx->partial);
+    k_sum_partials<<<GM_MAXV + 1, 32, 0, st>>>(ctx->partial, RED_BLOCKS, GM_MAXV + 1, hout);
+    ctx->launches += 2;
+    if (cudaGetLastError() != cudaSuccess) return ISC_CUDA_ERROR;
+    return allreduce_dev(ctx, hout, GM_MAXV + 1);
+  };
+  std::vector<double> H((size_t)(m + 1) * m), cs(m), sn(m), gv(m + 1), hc(2 * (GM_MAXV + 1)),
+      y(m);
+  int it = 0;
+  TRY(norm2_into(r, S_RR));
+  TRY(K.read_scalars());
+  double beta = std::sqrt(ctx->sc_h[S_RR]);
+  for (;;) {
+    if (beta / nb <= tol) break;
+    if (it >= maxiter) {
+      *iters = it;
+      g_err = "GMRES did not converge";
+      return ISC_MAX_ITERATIONS;
+    }
+    {
+      KScope ks(ctx, KT_VEC);
+      k_sc_scale<<<RED_BLOCKS, RED_THREADS, 0, st>>>(g, r, ctx->sc + S_RR, V);   // v0 = r / beta
+    }
+    ++ctx->launches;
+    std::fill(gv.begin(), gv.end(), 0.0);
+    gv[0] = beta;
+    int j = 0;
+    double res = beta;
+    for (; j < m && it < maxiter; ++j) {
+      ++it;
+      double* vj = V + (int64_t)j * len;
+      double* w = V + (int64_t)(j + 1) * len;
+      {
+        KScope ks(ctx, KT_VEC);
+        k_sc_precond<<<RED_BLOCKS, RED_THREADS, 0, st>>>(g, vj, uinv, z);
+      }
+      ++ctx->launches;
+      TRY(matvec(z, w));
+      TRY(multidot(j + 1, w, h1));
+      {
+        KScope ks(ctx, KT_VEC);
+        k_sc_multiaxpy<<<RED_BLOCKS, RED_THREADS, 0, st>>>(g, V, len, j + 1, h1, 1.0, w, 0,
+                                                           nullptr);
+      }
+      ++ctx->launches;
+      TRY(multidot(j + 1, w, h2));
+      {
+        KScope ks(ctx, KT_VEC);
+        k_sc_multiaxpy<<<RED_BLOCKS, RED_THREADS, 0, st>>>(g, V, len, j + 1, h2, 1.0, w, 0,
+                                                           ctx->partial);
+      }
+      ++ctx->launches;
+      TRY(K.finalize1(RED_BLOCKS, S_TT));   // ||w||^2 after CGS2
+      CK(cudaMemcpyAsync(hc.data(), h1, 2 * (GM_MAXV + 1) * 8, cudaMemcpyDeviceToHost, st));
+      TRY(K.read_scalars());
+      double* col = &H[(size_t)j * (m + 1)];
+      for (int i = 0; i <= j; ++i) col[i] = hc[i] + hc[GM_MAXV + 1 + i];
+      const double hn = std::sqrt(ctx->sc_h[S_TT]);
+      col[j + 1] = hn;
+      if (!std::isfinite(hn)) {
+        *iters = it;
+        g_err = "GMRES breakdown (non-finite Arnoldi vector)";
+        return ISC_BREAKDOWN;
+      }
+      if (hn > 0.0) {
+        KScope ks(ctx, KT_VEC);
+        k_sc_scale<<<RED_BLOCKS, RED_THREADS, 0, st>>>(g, w, ctx->sc + S_TT, w);
+        ++ctx->launches;
+      }
+      for (int i = 0; i < j; ++i) {
+        const double a = cs[i] * col[i] + sn[i] * col[i + 1];
+        col[i + 1] = -sn[i] * col[i] + cs[i] * col[i + 1];
+        col[i] = a;
+      }
+      const double rr = std::hypot(col[j], col[j + 1]);
+      if (rr == 0.0) {
+        *iters = it;
+        g_err = "GMRES breakdown (singular Hessenberg)";
+        return ISC_BREAKDOWN;
+      }
+      cs[j] = col[j] / rr;
+      sn[j] = col[j + 1] / rr;
+      col[j] = rr;
+      col[j + 1] = 0.0;
+      gv[j + 1] = -sn[j] * gv[j];
+      gv[j] = cs[j] * gv[j];
+      res = std::fabs(gv[j + 1]);
+      if (res / nb <= tol || hn == 0.0) { ++j; break; }
+    }
+    // y = R^-1 g; x_b += U_b^-1 (V y)
+    for (int i = j - 1; i >= 0; --i) {
+      double a = gv[i];
+      for (int k = i + 1; k < j; ++k) a -= H[(size_t)k * (m + 1) + i] * y[k];
+      y[i] = a / H[(size_t)i * (m + 1) + i];
+    }
+    CK(cudaMemcpyAsync(yd, y.data(), j * 8, cudaMemcpyHostToDevice, st));
+    {
+      KScope ks(ctx, KT_VEC);
+      k_sc_multiaxpy<<<RED_BLOCKS, RED_THREADS, 0, st>>>(g, V, len, j, yd, -1.0, u, 1, nullptr);
+      k_sc_precond<<<RED_BLOCKS, RED_THREADS, 0, st>>>(g, u, uinv, z);
+      k_sc_add<<<RED_BLOCKS, RED_THREADS, 0, st>>>(g, z, x);
+    }
+    ctx->launches += 3;
+    if (res / nb <= tol) break;
+    // restart: r_b = g_b - S x_b
+    CK(cudaMemcpyAsync(u, x, len * 8, cudaMemcpyDeviceToDevice, st));
+    TRY(matvec(u, t));
+    k_sc_sub<<<RED_BLOCKS, RED_THREADS, 0, st>>>(g, gb, t, r, z);
+    ++ctx->launches;
+    TRY(norm2_into(r, S_RR));
+    TRY(K.read_scalars());
+    beta = std::sqrt(ctx->sc_h[S_RR]);
+  }
+  // x_r = b_r - B_rb x_b
+  TRY(halo_exchange(ctx, x, NU));
+  {
+    KScope ks(ctx, KT_SPMV);
+    k_sc_xred<<<bh, dim3(32, NU), 0, st>>>(g, ctx->offd, b, x);
+  }
+  ++ctx->launches;
+  *iters = it;
+  CK(cudaStreamSynchronize(st));
+  return ISC_OK;
+}
+
+extern "C" int isc_set_krylov(isc_ctx* ctx, int32_t krylov, int32_t restart) {
+  if (krylov != ISC_KRYLOV_BICGSTAB && krylov != ISC_KRYLOV_GMRES) {
+    g_err = "unknown Krylov method";
+    return ISC_BAD_ARGUMENT;
+  }
+  if (restart < 0 || restart > GM_MAXV - 1) {
+    g_err = "GMRES restart length out of range (1..31, 0 = default)";
+    return ISC_BAD_ARGUMENT;
+  }
+  ctx->krylov = krylov;
+  if (restart > 0) ctx->gm_m = restart;
+  return ISC_OK;
+}
+
 extern "C" int isc_solve(isc_ctx* ctx, double tol, int32_t maxiter, double* d_du, double* h_dbhp,
                          int32_t* iters, int64_t* bad_cell, int32_t* bad_col) {
   if (!ctx->decoupled) {
@@ -1844,7 +2052,9 @@ extern "C" int isc_solve(isc_ctx* ctx, double tol, int32_t maxiter, double* d_du
 #endif
   const bool schur = MC_SCHUR && ctx->mc_schur && ctx->precond == ISC_PRECOND_MCILU &&
                      ctx->g.colored;
-  int status = schur ? bicgstab_schur(ctx, tol, maxiter, &it) : bicgstab(ctx, tol, maxiter, &it);
+  int status = !schur ? bicgstab(ctx, tol, maxiter, &it)
+               : ctx->krylov == ISC_KRYLOV_GMRES ? gmres_schur(ctx, tol, maxiter, &it)
+                                                 : bicgstab_schur(ctx, tol, maxiter, &it);
   STAGE(stage_end(ctx, 3));
   if (iters) *iters = it;
   if (status) return status;

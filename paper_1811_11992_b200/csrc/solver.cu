@@ -1095,4 +1095,141 @@ __global__ void __launch_bounds__(RED_THREADS, VEC_MINB) k_sc_dot(Dims g, const 
   block_reduce_store<1>(acc, partial);
 }
 
+// ------------------------------------------------ GMRES on the reduced system
+// Right-preconditioned restarted GMRES on S x_b = g_b with U_b block-Jacobi
+// (the north star's "BiCGSTAB/GMRES"): Arnoldi with classical Gram-Schmidt
+// and one reorthogonalisation (CGS2). Vectors are black-half, full-length
+// storage (9n, black positions used), the basis V packed with stride vs.
+constexpr int GM_MAXV = 32;   // basis vectors held (restart length GM_MAXV - 1)
+
+// z_b = U_b^-1 v_b
+__global__ void __launch_bounds__(RED_THREADS, VEC_MINB) k_sc_precond(Dims g,
+                                                                      const double* __restrict__ v,
+                                                                      const double* __restrict__ uinv,
+                                                                      double* __restrict__ z) {
+  const int64_t n = g.n;
+  SC_LOOP(t) {
+    const int64_t c = colour_pos(g, 1, t);
+    if (!owned_k(g, plane_of(g, c))) {   // ghost plane (slabs): filled by the halo exchange
+#pragma unroll
+      for (int q = 0; q < NU; ++q) z[q * n + c] = 0.0;
+      continue;
+    }
+    double pv[NU];
+#pragma unroll
+    for (int q = 0; q < NU; ++q) pv[q] = v[q * n + c];
+#pragma unroll
+    for (int q = 0; q < NU; ++q) {
+      double zz = 0.0;
+#pragma unroll
+      for (int u = 0; u < NU; ++u) zz += uinv[(int64_t)(q * NU + u) * n + c] * pv[u];
+      z[q * n + c] = zz;
+    }
+  }
+}
+
+// per-block partials of h_i = V_i . w (i < nv) and, when w2 == nullptr, of
+// w . w in slot nv; partial[i * gridDim.x + block] (fixed order, owned rows)
+__global__ void __launch_bounds__(RED_THREADS, 2) k_sc_multidot(Dims g, const double* __restrict__ V,
+                                                                int64_t vs, int nv,
+                                                                const double* __restrict__ w,
+                                                                double* partial) {
+  const int64_t n = g.n;
+  double acc[GM_MAXV + 1];
+#pragma unroll
+  for (int i = 0; i <= GM_MAXV; ++i) acc[i] = 0.0;
+  SC_LOOP(t) {
+    const int64_t c = colour_pos(g, 1, t);
+    if (!owned_k(g, plane_of(g, c))) continue;
+#pragma unroll 1
+    for (int q = 0; q < NU; ++q) {
+      const double wq = w[q * n + c];
+#pragma unroll
+      for (int i = 0; i < GM_MAXV; ++i)
+        if (i < nv) acc[i] += V[(int64_t)i * vs + q * n + c] * wq;
+      acc[GM_MAXV] += wq * wq;
+    }
+  }
+  __shared__ double sh[GM_MAXV + 1][RED_THREADS / 32];
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+#pragma unroll
+  for (int i = 0; i <= GM_MAXV; ++i) {
+    double x = acc[i];
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) x += __shfl_down_sync(0xffffffffu, x, o);
+    if (lane == 0) sh[i][wid] = x;
+  }
+  __syncthreads();
+  for (int i = threadIdx.x; i <= GM_MAXV; i += blockDim.x) {
+    double x = 0.0;
+    for (int k = 0; k < RED_THREADS / 32; ++k) x += sh[i][k];
+    partial[(int64_t)i * gridDim.x + blockIdx.x] = x;
+  }
+}
+
+// out[i] = sum_b partial[i * nparts + b] in fixed order (i < nout); one warp per value
+__global__ void k_sum_partials(const double* __restrict__ partial, int nparts, int nout,
+                               double* out) {
+  const int i = blockIdx.x;
+  if (i >= nout) return;
+  double x = 0.0;
+  for (int b = threadIdx.x; b < nparts; b += 32) x += partial[(int64_t)i * nparts + b];
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) x += __shfl_down_sync(0xffffffffu, x, o);
+  if (threadIdx.x == 0) out[i] = x;
+}
+
+// w = (zero ? 0 : w) - sum_{i<nv} h_i V_i over owned black rows; partial w.w
+// (when partial != nullptr)
+__global__ void __launch_bounds__(RED_THREADS, VEC_MINB) k_sc_multiaxpy(Dims g, const double* __restrict__ V,
+                                                                        int64_t vs, int nv,
+                                                                        const double* __restrict__ h,
+                                                                        double hsign,
+                                                                        double* __restrict__ w,
+                                                                        int zero, double* partial) {
+  const int64_t n = g.n;
+  __shared__ double hs[GM_MAXV];
+  for (int i = threadIdx.x; i < GM_MAXV; i += blockDim.x) hs[i] = i < nv ? hsign * h[i] : 0.0;
+  __syncthreads();
+  double acc[1] = {0.0};
+  SC_LOOP(t) {
+    const int64_t c = colour_pos(g, 1, t);
+    if (!owned_k(g, plane_of(g, c))) {
+#pragma unroll
+      for (int q = 0; q < NU; ++q) w[q * n + c] = 0.0;
+      continue;
+    }
+#pragma unroll 1
+    for (int q = 0; q < NU; ++q) {
+      double x = zero ? 0.0 : w[q * n + c];
+      for (int i = 0; i < nv; ++i) x -= hs[i] * V[(int64_t)i * vs + q * n + c];
+      w[q * n + c] = x;
+      acc[0] += x * x;
+    }
+  }
+  if (partial) block_reduce_store<1>(acc, partial);
+}
+
+// out = w / sqrt(nn[0]) (owned black rows)
+__global__ void k_sc_scale(Dims g, const double* __restrict__ w, const double* __restrict__ nn,
+                           double* __restrict__ out) {
+  const int64_t n = g.n;
+  const double inv = 1.0 / sqrt(nn[0]);
+  SC_LOOP(t) {
+    const int64_t c = colour_pos(g, 1, t);
+#pragma unroll
+    for (int q = 0; q < NU; ++q) out[q * n + c] = w[q * n + c] * inv;
+  }
+}
+
+// x_b += z_b
+__global__ void k_sc_add(Dims g, const double* __restrict__ z, double* __restrict__ x) {
+  const int64_t n = g.n;
+  SC_LOOP(t) {
+    const int64_t c = colour_pos(g, 1, t);
+#pragma unroll
+    for (int q = 0; q < NU; ++q) x[q * n + c] += z[q * n + c];
+  }
+}
+
 }  // namespace isc

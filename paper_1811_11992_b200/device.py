@@ -71,6 +71,7 @@ class DeviceContext:
         self.n = grid.ncell
         self.nw = len(self.wells)
         self.precond = precond
+        self.krylov = "bicgstab"
         keep = self._keep = {}
 
         def hold(name, a, dtype=np.float64):
@@ -139,6 +140,12 @@ class DeviceContext:
         if precond != self.precond:
             N.check(self.L.isc_set_precond(self.h, N.PRECOND[precond]), "isc_set_precond")
             self.precond = precond
+
+    def set_krylov(self, krylov: str = "bicgstab", restart: int = 0):
+        """Krylov method of the mcilu red-eliminated solve: the reference's
+        BiCGSTAB (default) or restarted GMRES(restart) (isc_set_krylov)."""
+        N.check(self.L.isc_set_krylov(self.h, N.KRYLOV[krylov], int(restart)), "isc_set_krylov")
+        self.krylov = krylov
 
     def empty(self, *shape, dtype=torch.float64):
         return torch.empty(*shape, dtype=dtype, device=self.device)

@@ -8,7 +8,9 @@ count min(64, max(1, n // 2048)) along the longest axis, natural order)
 and right-preconditioned BiCGSTAB with the reference's single restart,
 breakdown thresholds and tolerances. ``precond="mcilu"`` selects the north
 star's multicolour block-ILU(0) instead, solved on the red-eliminated system
-(same stopping test on the full residual). Raises ``SingularCellBlock``,
+(same stopping test on the full residual), with the
+reference's BiCGSTAB or, ``krylov="gmres"``, restarted GMRES(``restart``).
+Raises ``SingularCellBlock``,
 ``Breakdown`` and ``MaxIterations`` like the reference. ``du`` is returned
 as a numpy (n, 9) array for drop-in callers; ``solve_device`` keeps it in
 HBM as a (9, n) tensor for the GPU Newton driver.
@@ -27,9 +29,12 @@ NU = 9
 
 class BlockSolver:
     def __init__(self, grid, ws: Workspace, tol: float = 1e-5, maxiter: int = 200,
-                 precond: str = "ras"):
+                 precond: str = "ras", krylov: str = "bicgstab", restart: int = 30):
         if precond not in ("none", "bjacobi", "ras", "mcilu"):
             raise ValueError(f"unknown preconditioner {precond!r}")
+        if krylov not in N.KRYLOV:
+            raise ValueError(f"unknown Krylov method {krylov!r}")
+        self.krylov, self.restart = krylov, restart
         self.grid, self.ws, self.tol, self.maxiter, self.precond = grid, ws, tol, maxiter, precond
         ws.precond = precond
         if ws.ctx is not None:
@@ -40,6 +45,8 @@ class BlockSolver:
         if self.ws.ctx is None:
             raise RuntimeError("assemble() must run before solve()")
         self.ws.ctx.set_precond(self.precond)
+        if getattr(self.ws.ctx, "krylov", "bicgstab") != self.krylov:
+            self.ws.ctx.set_krylov(self.krylov, self.restart)
         return self.ws.ctx
 
     def solve_device(self, blocks=None):

@@ -117,6 +117,8 @@ class Simulator:
             raise ValueError("the fused assemble+decouple path has no numeric-Jacobian mode")
         self.ctx = DeviceContext(grid, pack, self.wells, self.streams, solver.precond, heat_loss,
                                  own_stream=own_stream)
+        if getattr(solver, "krylov", "bicgstab") != "bicgstab":
+            self.ctx.set_krylov(solver.krylov, getattr(solver, "gmres_restart", 0))
         if comm_setup is not None:   # z-slab rank: window + NCCL/hub transport
             comm_setup(self.ctx)
         dev = self.ctx.device

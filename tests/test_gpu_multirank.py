@@ -37,8 +37,9 @@ def _slice_state(st, accn, piece, nxny):
     return loc, accn[sl].copy()
 
 
-def _single(c, st, accn, precond, tol):
+def _single(c, st, accn, precond, tol, krylov="bicgstab"):
     ctx = DeviceContext(c.grid, c.pack, c.wells, c.streams, precond)
+    ctx.set_krylov(krylov)
     wout = ctx.assemble(state_to_device(st, ctx.device), st.bhp, soa_from_rows(accn, ctx.device),
                         2e-3, 2e-3, np.zeros(len(c.wells), bool), False)
     resid = ctx.copy_out(0, 9).cpu().numpy()
@@ -49,18 +50,21 @@ def _single(c, st, accn, precond, tol):
     return out
 
 
-@pytest.mark.parametrize("nranks", [2, 3, 5])   # 5: ranks with one owned plane
-def test_slab_assembly_and_solve_match_single_gpu(nranks):
+@pytest.mark.parametrize("nranks,krylov", [(2, "bicgstab"), (3, "bicgstab"),
+                                           (5, "bicgstab"),   # 5: ranks with one owned plane
+                                           (2, "gmres"), (3, "gmres")])
+def test_slab_assembly_and_solve_match_single_gpu(nranks, krylov):
     c = case_objects("sub2")
     st, accn = random_state_like_reference(c, 31)
     nxny = c.grid.nx * c.grid.ny
-    ref_resid, ref_du, ref_dbhp, ref_it, ref_wout = _single(c, st, accn, "mcilu", 1e-10)
+    ref_resid, ref_du, ref_dbhp, ref_it, ref_wout = _single(c, st, accn, "mcilu", 1e-10, krylov)
 
     hub = Hub(nranks)
     pieces = [split_case(c.case, nranks, r) for r in range(nranks)]
     ctxs = []
     for p in pieces:
         ctx = DeviceContext(p.grid, p.pack, p.wells, p.streams, "mcilu", own_stream=True)
+        ctx.set_krylov(krylov)
         attach_hub(ctx, hub.h, p)
         ctxs.append(ctx)
     inputs = []

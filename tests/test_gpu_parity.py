@@ -134,18 +134,24 @@ def test_synthetic_microbench_vs_reference():
     ("c1", 1e-10, "analytic", None), ("c2", 1e-10, "analytic", None),
     ("c1", 1e-5, "analytic", None), ("c1", 1e-10, "numeric", None),
     ("c2", 1e-10, "analytic", "mcilu"),
-    ("c3", 1e-10, "analytic", None), ("c3", 1e-10, "analytic", "mcilu")])
+    ("c3", 1e-10, "analytic", None), ("c3", 1e-10, "analytic", "mcilu"),
+    ("c3", 1e-10, "analytic", "mcilu+gmres")])
 def test_trajectory_vs_reference(name, tol, jac, precond):
     """Whole runs: equal step and Newton sequences, fields within 1e-6
     (jac "numeric": the reference's JACOBIAN numeric mode, newton.py:228,278;
     precond "mcilu": the multicolour solve in place of the reference's RAS —
     at LINEAR_TOL 1e-10 the Newton sequence is solver-independent; not on the
     1-D C1 chain, where red-black ILU(0) needs 100-350 BiCGSTAB iterations per
-    solve against LINEAR_MAX 200, while RAS there is an exact LU)."""
+    solve against LINEAR_MAX 200, while RAS there is an exact LU;
+    "mcilu+gmres": the same preconditioner under restarted GMRES(30))."""
     from paper_1811_11992_b200.newton import Simulator
     tag = "" if jac == "analytic" else "_" + jac
     g = golden(f"traj_{name}_{tol:.0e}{tag}.npz")
-    kw = {"precond": precond} if precond else {}
+    kw = {}
+    if precond:
+        kw["precond"], _, kry = precond.partition("+")
+        if kry:
+            kw["krylov"] = kry
     c = case_objects(name, linear_tol=tol, **kw)
     sim = Simulator(c.grid, c.pack, c.wells, c.streams, c.state, c.case.schedule, c.case.solver,
                     jacobian=jac)
@@ -464,3 +470,49 @@ def test_mcilu_solve_synthetic_and_error_paths(nx):
     load_system(ws, diag, offd, resid)
     with pytest.raises(MaxIterations):
         BlockSolver(grid, ws, tol=1e-14, maxiter=1, precond="mcilu").solve([])
+
+
+@pytest.mark.parametrize("restart", [30, 4])   # 4: several restarts (true-residual path)
+def test_gmres_solve_synthetic_and_error_paths(restart):
+    """Optional GMRES(m) on the red-eliminated system (capi.cu gmres_schur):
+    du solves the decoupled system (dense check), agrees with the default
+    BiCGSTAB, and the error contract is the reference's (MaxIterations,
+    SingularCellBlock, bad arguments)."""
+    from paper_1811_11992_b200.grid import build_grid
+    from paper_1811_11992_b200.synth import synth_system
+    from paper_1811_11992_b200.model import load_pack
+    grid = build_grid(8, 6, 4, 1.0, 1.0, 1.0, 1.0, 1.0, 1.0, 0.3)
+    pack = load_pack("tube3_pack", grid.phi_ref)
+    diag, offd, resid = synth_system(grid, 9, seed=7)
+    ws = Workspace(grid, pack, None, wells=(), streams=(), precond="mcilu")
+    load_system(ws, diag, offd, resid)
+    du_b, _, it_b = BlockSolver(grid, ws, tol=1e-12, maxiter=500, precond="mcilu").solve([])
+    load_system(ws, diag, offd, resid)
+    gm = BlockSolver(grid, ws, tol=1e-12, maxiter=500, precond="mcilu", krylov="gmres",
+                     restart=restart)
+    du, _, it = gm.solve([])
+    n = grid.ncell
+    A = np.zeros((9 * n, 9 * n))
+    for c in range(n):
+        A[9 * c:9 * c + 9, 9 * c:9 * c + 9] = diag[c]
+    for ic in range(grid.nconn):
+        a, b = int(grid.conn_a[ic]), int(grid.conn_b[ic])
+        A[9 * a:9 * a + 9, 9 * b:9 * b + 9] = offd[ic, 0]
+        A[9 * b:9 * b + 9, 9 * a:9 * a + 9] = offd[ic, 1]
+    ref = np.linalg.solve(A, -resid.reshape(-1)).reshape(n, 9)
+    assert np.linalg.norm(du - ref) <= 1e-9 * np.linalg.norm(ref), it
+    assert np.linalg.norm(du - du_b) <= 1e-9 * np.linalg.norm(ref)
+    if restart > it_b:   # one cycle: the minimal residual needs no more products
+        assert it <= 2 * it_b, (it, it_b)
+    load_system(ws, diag, offd, resid)
+    with pytest.raises(MaxIterations):
+        BlockSolver(grid, ws, tol=1e-14, maxiter=2, precond="mcilu", krylov="gmres").solve([])
+    bad = diag.copy()
+    bad[9, :, 3] = 0.0
+    load_system(ws, bad, offd, resid)
+    with pytest.raises(SingularCellBlock, match="cell 9"):
+        BlockSolver(grid, ws, tol=1e-8, maxiter=100, precond="mcilu", krylov="gmres").solve([])
+    with pytest.raises(ValueError):
+        BlockSolver(grid, ws, precond="mcilu", krylov="cg")
+    with pytest.raises(RuntimeError, match="restart"):
+        ws.ctx.set_krylov("gmres", 32)
