@@ -170,7 +170,7 @@ def ncu_traffic(kernel_class, precond):
     return float(d[kernel_class]["dram_bytes"]), os.path.relpath(files[-1], ROOT)
 
 
-def algorithmic_bytes(grid, nw, precond="ras"):
+def algorithmic_bytes(grid, nw, precond="ras", form="explicit"):
     """Compulsory bytes per launch of each kernel class."""
     n, m = grid.ncell, grid.nconn
     out = {
@@ -187,6 +187,14 @@ def algorithmic_bytes(grid, nw, precond="ras"):
         # black pass v_b = z_b + B_br w_r: the black rows' blocks (81 m), w_r and
         # z_b read (9 n), v_b written (9 n/2), one dot operand (9 n/2)
         out["spmv"] = 8 * (81 * m + 18 * n)
+        if form == "compact":
+            # compact operator (csrc/compact.cu): per block only the 6 flux rows
+            # (54 m per colour), plus D^-1[:, :6] of each row's cell (54 n/2)
+            out["ilu_apply"] = 8 * (54 * m + 27 * n + 9 * n)
+            out["spmv"] = 8 * (54 * m + 27 * n + 18 * n)
+            # k_rhs_schur (resid in, rhs out) + k_decouple_compact (diag and rhs
+            # in, D^-1[:, :6] and rhs out)
+            out["decouple"] = 8 * (18 * n + 81 * n + 9 * n + 54 * n + 9 * n)
     return out
 
 
@@ -366,7 +374,7 @@ def run_ours(args, rank, world, local):
                         "precond_setup": float(stage_ms[2]), "krylov": float(stage_ms[3])}}
     # ---- roofline of the dominant kernel class ----------------------------
     hbm, peak_src = peaks()
-    algo = algorithmic_bytes(grid, len(wells), case.solver.precond)
+    algo = algorithmic_bytes(grid, len(wells), case.solver.precond, sim.ctx.decoupled_form)
     ktimes = {KCLASS[i]: {"ms": float(ms8[i]), "launches": int(cnt8[i])} for i in range(8)}
     classes = {"ilu_apply": ("ilu_apply",), "spmv": ("spmv",), "decouple": ("decouple",),
                "cell+face": ("cell", "face")}

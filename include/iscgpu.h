@@ -174,6 +174,11 @@ int isc_import_system(isc_ctx *ctx, const double *d_diag, const double *d_offd,
 int isc_set_wells_out(isc_ctx *ctx, const double *h_wells_out);
 /* Switch preconditioner (rebuilds the subdomain/level structure). */
 int isc_set_precond(isc_ctx *ctx, int32_t precond);
+/* Form of the decoupled system held by the context: 0 not decoupled,
+ * 1 explicit D^-1 B_d blocks (the reference's, linsolve.py:130-152),
+ * 2 compact (mcilu on an assembled system: raw flux rows of B_d and
+ * D^-1[:, :6], the same operator). */
+int isc_decoupled_form(const isc_ctx *ctx);
 /* Select the Krylov method (isc_krylov); restart = GMRES restart length
  * 1..31 (0 keeps the current, default 30). No reference counterpart: an
  * extension of linsolve.BlockSolver's solve (linsolve.py:481-578). */
@@ -187,7 +192,8 @@ int isc_synth_system(isc_ctx *ctx, uint64_t seed);
  * status 2, *bad_cell/*bad_col identify the block (-1 when not a cell). */
 int isc_solve(isc_ctx *ctx, double tol, int32_t maxiter, double *d_du, double *h_dbhp,
               int32_t *iters, int64_t *bad_cell, int32_t *bad_col);
-/* Decouple only (tests): leaves D^-1-scaled blocks/rhs inside the context. */
+/* Decouple only (tests): leaves D^-1-scaled blocks/rhs inside the context
+ * (the compact form for mcilu on an assembled system: isc_decoupled_form). */
 int isc_decouple(isc_ctx *ctx, int64_t *bad_cell, int32_t *bad_col);
 int isc_precond_setup(isc_ctx *ctx, int64_t *bad_cell);
 int isc_spmv(isc_ctx *ctx, const double *d_x, double *d_y);

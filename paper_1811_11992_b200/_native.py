@@ -76,6 +76,7 @@ _SIGS = {
     "isc_set_wells_out": (ctypes.c_int, [VP, VP]),
     "isc_set_precond": (ctypes.c_int, [VP, ctypes.c_int32]),
     "isc_set_krylov": (ctypes.c_int, [VP, ctypes.c_int32, ctypes.c_int32]),
+    "isc_decoupled_form": (ctypes.c_int, [VP]),
     "isc_synth_system": (ctypes.c_int, [VP, ctypes.c_uint64]),
     "isc_solve": (ctypes.c_int, [VP, ctypes.c_double, ctypes.c_int32, VP, VP,
                                  ctypes.POINTER(ctypes.c_int32), c_int64_p,

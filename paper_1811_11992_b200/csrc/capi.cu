@@ -19,6 +19,11 @@
 #include "numjac.cu"
 #include "report.cuh"
 #include "solver.cu"
+#include "compact.cu"
+
+#ifndef MC_SCHUR
+#define MC_SCHUR 1   // mcilu on the red-eliminated system (0: full-system fused form)
+#endif
 
 using namespace isc;
 
@@ -86,6 +91,8 @@ struct isc_ctx {
   int precond = ISC_PRECOND_RAS;
   bool decoupled = false, factored = false;
   int offd_rows = NU;   // rows of offd holding data (ROW_OS after an un-decoupled assembly)
+  bool compact = false;   // decoupled in compact form (compact.cu): diag = D^-1[:, :CR], offd raw
+  bool compact_ok = true; // ISC_COMPACT=0 disables the compact form (A/B switch)
   bool assembled = false;   // the last assembly was isc_assemble (inputs kept for FD)
   double asm_dt = 0.0;
   int asm_freeze = 0;
@@ -324,6 +331,8 @@ extern "C" int isc_create(const isc_model_desc* md, const isc_grid_desc* gdsc, i
   {
     const char* e = std::getenv("ISC_MCILU_FULL");   // A/B switch for the full-system form
     ctx->mc_schur = !(e && e[0] == '1');
+    const char* e2 = std::getenv("ISC_COMPACT");
+    ctx->compact_ok = !(e2 && e2[0] == '0');
   }
   Dims& g = ctx->g;
   g.nx = gdsc->nx; g.ny = gdsc->ny; g.nz = gdsc->nz;
@@ -617,6 +626,7 @@ extern "C" int isc_assemble(isc_ctx* ctx, const double* d_state, const double* h
   STAGE(stage_end(ctx, 0));   // synchronises
   if (ctx->nw > 0 && h_wells_out) std::memcpy(h_wells_out, ctx->wout_h, ctx->nw * WOUT * 8);
   ctx->decoupled = false;
+  ctx->compact = false;
   ctx->factored = false;
   ctx->offd_rows = ROW_OS;   // rows ROW_OS.. of the off-diagonal blocks were not written
   ctx->assembled = true;
@@ -745,6 +755,7 @@ extern "C" int isc_assemble_decoupled(isc_ctx* ctx, const double* d_state, const
     ctx->dc_bad_cell = c;
     ctx->dc_bad_col = flag - 1;
   }
+  ctx->compact = false;
   ctx->decoupled = true;
   ctx->factored = false;
   ctx->offd_rows = NU;
@@ -887,6 +898,7 @@ extern "C" int isc_import_system(isc_ctx* ctx, const double* d_diag, const doubl
   }
   CK(cudaStreamSynchronize(ctx->stream));
   ctx->decoupled = ctx->factored = false;
+  ctx->compact = false;
   ctx->offd_rows = NU;
   ctx->assembled = false;
   return ISC_OK;
@@ -917,6 +929,10 @@ static void free_ilu(isc_ctx* ctx) {
 extern "C" int isc_set_precond(isc_ctx* ctx, int32_t precond) {
   if (precond < 0 || precond > 3) { g_err = "unknown preconditioner"; return ISC_BAD_ARGUMENT; }
   if (precond == ctx->precond) return ISC_OK;
+  if (ctx->compact && ctx->decoupled) {
+    g_err = "system decoupled in the multicolour compact form: assemble again first";
+    return ISC_UNSUPPORTED;
+  }
   CK(cudaStreamSynchronize(ctx->stream));
   free_ilu(ctx);
   ctx->precond = precond;
@@ -932,6 +948,7 @@ extern "C" int isc_synth_system(isc_ctx* ctx, uint64_t seed) {
   LAUNCH_CHECK();
   CK(cudaStreamSynchronize(ctx->stream));
   ctx->decoupled = ctx->factored = false;
+  ctx->compact = false;
   ctx->offd_rows = NU;
   ctx->assembled = false;
   return ISC_OK;
@@ -973,7 +990,15 @@ extern "C" int isc_decouple(isc_ctx* ctx, int64_t* bad_cell, int32_t* bad_col) {
 #ifndef DECOUPLE_WS
 #define DECOUPLE_WS 1
 #endif
-  if (DECOUPLE_WS) {
+  // compact form: the red-eliminated multicolour solve of an assembled
+  // system (compact.cu)
+  ctx->compact = ctx->compact_ok && ctx->precond == ISC_PRECOND_MCILU && ctx->g.colored &&
+                 ctx->mc_schur && MC_SCHUR && ctx->offd_rows == ROW_OS;
+  if (ctx->compact) {
+    const int64_t owned = (int64_t)(ctx->g.kw_hi - ctx->g.kw_lo) * ctx->g.nxny;
+    k_decouple_compact<<<grid1d(owned, 32), dim3(32, NU), 0, st>>>(ctx->g, ctx->diag, ctx->rhs,
+                                                                  ctx->flags, ctx->bad_d);
+  } else if (DECOUPLE_WS) {
     // once per process (thread-safe static init: hub ranks share the process)
     static const cudaError_t attr = cudaFuncSetAttribute(
         k_decouple_ws, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(WsSmem));
@@ -993,7 +1018,7 @@ extern "C" int isc_decouple(isc_ctx* ctx, int64_t* bad_cell, int32_t* bad_col) {
                                                                ctx->offd_rows);
   }
   LAUNCH_CHECK();
-  ctx->offd_rows = NU;   // the decoupled blocks are dense
+  if (!ctx->compact) ctx->offd_rows = NU;   // the decoupled blocks are dense
   }
   CK(cudaMemcpyAsync(ctx->bad_h, ctx->bad_d, 8, cudaMemcpyDeviceToHost, st));
   STAGE(stage_end(ctx, 1));
@@ -1052,9 +1077,15 @@ extern "C" int isc_precond_setup(isc_ctx* ctx, int64_t* bad_cell) {
     if (cross) {
       if (halo_exchange(ctx, ctx->offd + (int64_t)DZM * NB * ctx->g.n, NB)) return ISC_CUDA_ERROR;
       if (halo_exchange(ctx, ctx->offd + (int64_t)DZP * NB * ctx->g.n, NB)) return ISC_CUDA_ERROR;
+      // compact form: the owner's D^-1[:, :CR] of the ghost planes as well
+      if (ctx->compact && halo_exchange(ctx, ctx->diag, CR * NU)) return ISC_CUDA_ERROR;
     }
-    k_mc_factor<<<grid1d(nblack, 32), dim3(32, NU), 0, st>>>(ctx->g, ctx->offd, ctx->mc_uinv,
-                                                            ctx->fail_d, cross);
+    if (ctx->compact)
+      k_mc_factor_compact<<<grid1d(ctx->g.tw_hi - ctx->g.tw_lo, 32), dim3(32, NU), 0, st>>>(
+          ctx->g, ctx->offd, ctx->diag, ctx->mc_uinv, ctx->fail_d);
+    else
+      k_mc_factor<<<grid1d(nblack, 32), dim3(32, NU), 0, st>>>(ctx->g, ctx->offd, ctx->mc_uinv,
+                                                              ctx->fail_d, cross);
     CK(cudaGetLastError());
   } else {
   CK(cudaFuncSetAttribute(k_ilu_factor, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -1127,8 +1158,19 @@ static int spmv(isc_ctx* ctx, const double* x, double* y, const double* w0, cons
 extern "C" int isc_spmv(isc_ctx* ctx, const double* d_x, double* d_y) {
   const int64_t n = ctx->g.n;
   k_to_pos<double><<<grid1d(n, 256), 256, 0, ctx->stream>>>(ctx->g, NU, d_x, ctx->sk);
-  int s = spmv<0>(ctx, ctx->sk, ctx->tk, nullptr, nullptr, nullptr);
-  if (s) return s;
+  if (ctx->compact) {   // y = x + sum_d (D^-1 B_d) x, one pass per colour
+    const Dims& g = ctx->g;
+    const int blocks = grid1d(g.tw_hi - g.tw_lo, 32);
+    KScope ks(ctx, KT_SPMV);
+    k_cc_spmv<0><<<blocks, dim3(32, CR), 0, ctx->stream>>>(
+        g, ctx->offd, ctx->diag, ctx->sk, ctx->sk, ctx->tk, nullptr, nullptr, nullptr, nullptr, 0, 0);
+    k_cc_spmv<1><<<blocks, dim3(32, CR), 0, ctx->stream>>>(
+        g, ctx->offd, ctx->diag, ctx->sk, ctx->sk, ctx->tk, nullptr, nullptr, nullptr, nullptr, 0, 0);
+    LAUNCH_CHECK();
+  } else {
+    int s = spmv<0>(ctx, ctx->sk, ctx->tk, nullptr, nullptr, nullptr);
+    if (s) return s;
+  }
   k_from_pos<double><<<grid1d(n, 256), 256, 0, ctx->stream>>>(ctx->g, NU, ctx->tk, d_y);
   LAUNCH_CHECK();
   CK(cudaStreamSynchronize(ctx->stream));
@@ -1137,6 +1179,10 @@ extern "C" int isc_spmv(isc_ctx* ctx, const double* d_x, double* d_y) {
 
 extern "C" int isc_precond_apply(isc_ctx* ctx, const double* d_r, double* d_z) {
   const int64_t n = ctx->g.n;
+  if (ctx->compact) {
+    g_err = "the compact multicolour form applies its preconditioner inside the reduced solve";
+    return ISC_UNSUPPORTED;
+  }
   k_to_pos<double><<<grid1d(n, 256), 256, 0, ctx->stream>>>(ctx->g, NU, d_r, ctx->sk);
   int s = precond_apply(ctx, ctx->sk, ctx->tk);
   if (s) return s;
@@ -1573,6 +1619,43 @@ static int bicgstab(isc_ctx* ctx, double tol, int maxiter, int* iters) {
   return ISC_MAX_ITERATIONS;
 }
 
+// Half passes of the red-eliminated product, explicit decoupled blocks or
+// the compact form (compact.cu); `blocks` covers g's [tw_lo, tw_hi)
+static void sc_rhs_launch(isc_ctx* ctx, const Dims& g, int blocks, const double* b, double* o1,
+                          double* o2) {
+  if (ctx->compact)
+    k_cc_rhs<<<blocks, dim3(32, CR), 0, ctx->stream>>>(
+        g, ctx->offd, ctx->diag, b, b, o1, o2, nullptr, nullptr, nullptr, 0, 0);
+  else
+    k_sc_rhs<<<blocks, dim3(32, NU), 0, ctx->stream>>>(g, ctx->offd, b, o1, o2);
+}
+static void sc_red_launch(isc_ctx* ctx, const Dims& g, int blocks, double* z) {
+  if (ctx->compact)
+    k_cc_red<<<blocks, dim3(32, CR), 0, ctx->stream>>>(
+        g, ctx->offd, ctx->diag, z, nullptr, z, nullptr, nullptr, nullptr, nullptr, 0, 0);
+  else
+    k_sc_red<<<blocks, dim3(32, NU), 0, ctx->stream>>>(g, ctx->offd, z);
+}
+static void sc_xred_launch(isc_ctx* ctx, const Dims& g, int blocks, const double* b, double* x) {
+  if (ctx->compact)
+    k_cc_xred<<<blocks, dim3(32, CR), 0, ctx->stream>>>(
+        g, ctx->offd, ctx->diag, x, b, x, nullptr, nullptr, nullptr, nullptr, 0, 0);
+  else
+    k_sc_xred<<<blocks, dim3(32, NU), 0, ctx->stream>>>(g, ctx->offd, b, x);
+}
+// black pass with K dot products; per-warp partial slots: stride x rows_per_block()
+template <int K>
+static void sc_black_launch(isc_ctx* ctx, const Dims& g, int blocks, const double* z, double* v,
+                            const double* w0, const double* w1, int stride, int slot0) {
+  if (ctx->compact)
+    k_cc_black<K><<<blocks, dim3(32, CR), 0, ctx->stream>>>(
+        g, ctx->offd, ctx->diag, z, z, v, nullptr, w0, w1, ctx->partial, stride, slot0);
+  else
+    k_mc_black_spmv<K><<<blocks, dim3(32, NU), 0, ctx->stream>>>(g, ctx->offd, z, v, w0, w1,
+                                                                ctx->partial, stride, slot0);
+}
+static int sc_warps(const isc_ctx* ctx) { return ctx->compact ? CR : NU; }
+
 // BiCGSTAB on the red-eliminated system S x_b = g_b with the multicolour
 // preconditioner acting as block-Jacobi U_b (solver.cu "Schur complement"
 // section): same preconditioner and the same stopping test on the full
@@ -1600,7 +1683,7 @@ static int bicgstab_schur(isc_ctx* ctx, double tol, int maxiter, int* iters) {
   TRY(halo_exchange(ctx, b, NU));   // slabs: red neighbours on other ranks
   {
     KScope ks(ctx, KT_SPMV);
-    k_sc_rhs<<<bh, dim3(32, NU), 0, st>>>(g, ctx->offd, b, r, rhat);   // g_b
+    sc_rhs_launch(ctx, g, bh, b, r, rhat);   // g_b
   }
   ++ctx->launches;
   double* sh = ctx->sc_h;
@@ -1631,15 +1714,15 @@ static int bicgstab_schur(isc_ctx* ctx, double tol, int maxiter, int* iters) {
   auto red_pass = [&](double* z) -> int {
     if (!split) {
       TRY(halo_exchange(ctx, z, NU));
-      k_sc_red<<<bh, dim3(32, NU), 0, st>>>(g, ctx->offd, z);
+      sc_red_launch(ctx, g, bh, z);
       ++ctx->launches;
       return cudaGetLastError() == cudaSuccess ? 0 : ISC_CUDA_ERROR;
     }
     TRY(halo_start(ctx, z, NU));
-    k_sc_red<<<bi, dim3(32, NU), 0, st>>>(gi, ctx->offd, z);
+    sc_red_launch(ctx, gi, bi, z);
     TRY(halo_finish(ctx, z, NU));
-    k_sc_red<<<bl1, dim3(32, NU), 0, st>>>(gl, ctx->offd, z);
-    k_sc_red<<<bh1, dim3(32, NU), 0, st>>>(gh, ctx->offd, z);
+    sc_red_launch(ctx, gl, bl1, z);
+    sc_red_launch(ctx, gh, bh1, z);
     ctx->launches += 3;
     return cudaGetLastError() == cudaSuccess ? 0 : ISC_CUDA_ERROR;
   };
@@ -1647,11 +1730,9 @@ static int bicgstab_schur(isc_ctx* ctx, double tol, int maxiter, int* iters) {
                         const double* w1) -> int {
     auto launch = [&](const Dims& d, int blocks, int slot0) {
       if (K == 1)
-        k_mc_black_spmv<1><<<blocks, dim3(32, NU), 0, st>>>(d, ctx->offd, z, vout, w0, w1,
-                                                            ctx->partial, bparts, slot0);
+        sc_black_launch<1>(ctx, d, blocks, z, vout, w0, w1, bparts, slot0);
       else
-        k_mc_black_spmv<2><<<blocks, dim3(32, NU), 0, st>>>(d, ctx->offd, z, vout, w0, w1,
-                                                            ctx->partial, bparts, slot0);
+        sc_black_launch<2>(ctx, d, blocks, z, vout, w0, w1, bparts, slot0);
     };
     if (!split) {
       TRY(halo_exchange(ctx, z, NU));
@@ -1676,7 +1757,7 @@ static int bicgstab_schur(isc_ctx* ctx, double tol, int maxiter, int* iters) {
   auto finish = [&]() -> int {   // x_r = b_r - B_rb x_b
     if (halo_exchange(ctx, x, NU)) return ISC_CUDA_ERROR;
     KScope ks(ctx, KT_SPMV);
-    k_sc_xred<<<bh, dim3(32, NU), 0, st>>>(g, ctx->offd, b, x);
+    sc_xred_launch(ctx, g, bh, b, x);
     ++ctx->launches;
     return cudaGetLastError() == cudaSuccess ? 0 : ISC_CUDA_ERROR;
   };
@@ -1689,7 +1770,7 @@ static int bicgstab_schur(isc_ctx* ctx, double tol, int maxiter, int* iters) {
       KScope ks(ctx, KT_SPMV);
       if (red_pass(x)) return ISC_CUDA_ERROR;   // red part of x: scratch
       if (black_pass(1, x, t, rhat, nullptr)) return ISC_CUDA_ERROR;
-      k_sc_rhs<<<bh, dim3(32, NU), 0, st>>>(g, ctx->offd, b, v, shat);   // g_b (scratch)
+      sc_rhs_launch(ctx, g, bh, b, v, shat);   // g_b (scratch)
     }
     k_sc_sub<<<RED_BLOCKS, RED_THREADS, 0, st>>>(g, v, t, r, rhat);
     ctx->launches += 4;
@@ -1731,7 +1812,7 @@ static int bicgstab_schur(isc_ctx* ctx, double tol, int maxiter, int* iters) {
       TRY(black_pass(1, phat, v, rhat, nullptr));
     }
     CK(cudaGetLastError());
-    TRY(K.finalize1(bparts * NU, S_DEN));
+    TRY(K.finalize1(bparts * sc_warps(ctx), S_DEN));
     {
       KScope ks(ctx, KT_VEC);
       k_sc_update_s<<<RED_BLOCKS, RED_THREADS, 0, st>>>(g, r, v, s, uinv, shat, ctx->sc,
@@ -1769,7 +1850,7 @@ static int bicgstab_schur(isc_ctx* ctx, double tol, int maxiter, int* iters) {
       TRY(black_pass(2, shat, t, nullptr, s));
     }
     CK(cudaGetLastError());
-    TRY(K.finalize2(bparts * NU, S_TT, S_TS));
+    TRY(K.finalize2(bparts * sc_warps(ctx), S_TT, S_TS));
     {
       KScope ks(ctx, KT_VEC);
       k_sc_update_xr<<<RED_BLOCKS, RED_THREADS, 0, st>>>(g, x, phat, shat, r, s, t, rhat,
@@ -1838,20 +1919,19 @@ static int gmres_schur(isc_ctx* ctx, double tol, int maxiter, int* iters) {
   TRY(halo_exchange(ctx, b, NU));
   {
     KScope ks(ctx, KT_SPMV);
-    k_sc_rhs<<<bh, dim3(32, NU), 0, st>>>(g, ctx->offd, b, r, gb);   // r = g_b (x_b = 0)
+    sc_rhs_launch(ctx, g, bh, b, r, gb);   // r = g_b (x_b = 0)
   }
   ++ctx->launches;
   auto matvec = [&](double* zz, double* out) -> int {   // out = S zz (zz: black in, red scratch)
     {
       KScope ks(ctx, KT_ILU_APPLY);
       TRY(halo_exchange(ctx, zz, NU));
-      k_sc_red<<<bh, dim3(32, NU), 0, st>>>(g, ctx->offd, zz);
+      sc_red_launch(ctx, g, bh, zz);
     }
     {
       KScope ks(ctx, KT_SPMV);
       TRY(halo_exchange(ctx, zz, NU));
-      k_mc_black_spmv<1><<<bh, dim3(32, NU), 0, st>>>(g, ctx->offd, zz, out, zz, nullptr,
-                                                      ctx->partial, bh, 0);
+      sc_black_launch<1>(ctx, g, bh, zz, out, zz, nullptr, bh, 0);
     }
     ctx->launches += 2;
     return cudaGetLastError() == cudaSuccess ? 0 : ISC_CUDA_ERROR;
@@ -1981,12 +2061,17 @@ static int gmres_schur(isc_ctx* ctx, double tol, int maxiter, int* iters) {
   TRY(halo_exchange(ctx, x, NU));
   {
     KScope ks(ctx, KT_SPMV);
-    k_sc_xred<<<bh, dim3(32, NU), 0, st>>>(g, ctx->offd, b, x);
+    sc_xred_launch(ctx, g, bh, b, x);
   }
   ++ctx->launches;
   *iters = it;
   CK(cudaStreamSynchronize(st));
   return ISC_OK;
+}
+
+// 0: not decoupled, 1: explicit decoupled blocks, 2: compact form (compact.cu)
+extern "C" int isc_decoupled_form(const isc_ctx* ctx) {
+  return !ctx->decoupled ? 0 : (ctx->compact ? 2 : 1);
 }
 
 extern "C" int isc_set_krylov(isc_ctx* ctx, int32_t krylov, int32_t restart) {
@@ -2047,9 +2132,6 @@ extern "C" int isc_solve(isc_ctx* ctx, double tol, int32_t maxiter, double* d_du
   }
   int it = 0;
   STAGE(stage_begin(ctx, 3));
-#ifndef MC_SCHUR
-#define MC_SCHUR 1
-#endif
   const bool schur = MC_SCHUR && ctx->mc_schur && ctx->precond == ISC_PRECOND_MCILU &&
                      ctx->g.colored;
   int status = !schur ? bicgstab(ctx, tol, maxiter, &it)

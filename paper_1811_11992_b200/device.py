@@ -147,6 +147,12 @@ class DeviceContext:
         N.check(self.L.isc_set_krylov(self.h, N.KRYLOV[krylov], int(restart)), "isc_set_krylov")
         self.krylov = krylov
 
+    @property
+    def decoupled_form(self) -> str:
+        """Form of the decoupled system: "none", "explicit" (D^-1 B_d blocks,
+        as the reference) or "compact" (mcilu: raw flux rows + D^-1[:, :6])."""
+        return ("none", "explicit", "compact")[self.L.isc_decoupled_form(self.h)]
+
     def empty(self, *shape, dtype=torch.float64):
         return torch.empty(*shape, dtype=dtype, device=self.device)
 

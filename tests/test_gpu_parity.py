@@ -411,30 +411,39 @@ def test_report_frame_from_device_simulator(tmp_path):
 
 @pytest.mark.parametrize("name", ["small3d", "sub2"])
 def test_mcilu_red_eliminated_matches_full_system(name, monkeypatch):
-    """The red-eliminated BiCGSTAB (capi.cu bicgstab_schur, default) and the
-    full-system form with the same multicolour preconditioner
-    (ISC_MCILU_FULL=1) converge to the same du; the reduced form never needs
-    more iterations than the full one (its red residual is zero from the
-    start)."""
+    """The red-eliminated BiCGSTAB (capi.cu bicgstab_schur, default; with
+    the compact operator of csrc/compact.cu and with explicit decoupled
+    blocks) and the full-system form with the same multicolour
+    preconditioner (ISC_MCILU_FULL=1) converge to the same du; the reduced
+    form never needs more iterations than the full one (its red residual is
+    zero from the start)."""
     from tests.golden_states import random_state_like_reference
     c = case_objects(name)
     st, accn = random_state_like_reference(c, 17)
     out = {}
-    for full in (False, True):
-        if full:
-            monkeypatch.setenv("ISC_MCILU_FULL", "1")
-        else:
-            monkeypatch.delenv("ISC_MCILU_FULL", raising=False)
+    # reduced system with the compact operator (default), with the explicit
+    # decoupled blocks (ISC_COMPACT=0), and the full-system form
+    for mode, env in (("compact", {}), ("explicit", {"ISC_COMPACT": "0"}),
+                      ("full", {"ISC_MCILU_FULL": "1"})):
+        for k in ("ISC_COMPACT", "ISC_MCILU_FULL"):
+            monkeypatch.delenv(k, raising=False)
+        for k, v in env.items():
+            monkeypatch.setenv(k, v)
         ws = _ws(c, "mcilu")
         blocks = assemble(c.grid, c.pack, ws, c.wells, c.streams, st, accn, 2e-3, 2e-3,
                           np.zeros(len(c.wells), bool))
-        out[full] = BlockSolver(c.grid, ws, tol=1e-10, maxiter=1000,
+        out[mode] = BlockSolver(c.grid, ws, tol=1e-10, maxiter=1000,
                                 precond="mcilu").solve(blocks)
+        assert ws.ctx.decoupled_form == ("compact" if mode == "compact" else "explicit")
         ws.ctx.close()
-    (du_s, db_s, it_s), (du_f, db_f, it_f) = out[False], out[True]
-    assert np.linalg.norm(du_s - du_f) <= 1e-8 * np.linalg.norm(du_f)
-    np.testing.assert_allclose(db_s, db_f, rtol=1e-8, atol=1e-8)
-    assert it_s <= it_f + 1, (it_s, it_f)
+    du_f, db_f, it_f = out["full"]
+    for mode in ("compact", "explicit"):
+        du_s, db_s, it_s = out[mode]
+        assert np.linalg.norm(du_s - du_f) <= 1e-8 * np.linalg.norm(du_f), mode
+        np.testing.assert_allclose(db_s, db_f, rtol=1e-8, atol=1e-8)
+        assert it_s <= it_f + 1, (mode, it_s, it_f)
+    # the compact operator is the same matrix: same Krylov iterations
+    assert abs(out["compact"][2] - out["explicit"][2]) <= 1
 
 
 @pytest.mark.parametrize("nx", [6, 5])   # red-eliminated (even nx) and full-system (odd nx)

@@ -14,8 +14,10 @@ import sys
 from collections import defaultdict
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
-KERNELS = ["k_sc_red", "k_mc_black_spmv", "k_sc_update_p", "k_sc_update_s", "k_sc_update_xr",
-           "k_face_eval", "k_face_gather", "k_decouple_ws", "k_cell", "k_mc_factor"]
+KERNELS = ["k_cc_red", "k_cc_black", "k_sc_update_p", "k_sc_update_s", "k_sc_update_xr",
+           "k_face_eval", "k_face_gather", "k_decouple_compact", "k_cell", "k_mc_factor_compact",
+           # explicit decoupled form (ISC_COMPACT=0 / round-1 first captures)
+           "k_sc_red", "k_mc_black_spmv", "k_decouple_ws", "k_mc_factor"]
 METRICS = [
     ("gpu__time_duration.sum", "duration", 1.0),
     ("dram__bytes_read.sum", "DRAM read", 1.0),
@@ -109,12 +111,13 @@ def main(tag):
                   "|---|---|---|---|"]
         for name, v in sorted(tot.items(), key=lambda kv: -kv[1])[:20]:
             lines.append(f"| {name} | {cnt[name]} | {v:.2f} | {v / s:.3f} |")
-    if "k_sc_red" in traffic:
-        traffic["red_pass"] = {"dram_bytes": traffic["k_sc_red"]["dram_bytes"],
-                               "kernels": ["k_sc_red"]}
-    if "k_mc_black_spmv" in traffic:
-        traffic["black_pass"] = {"dram_bytes": traffic["k_mc_black_spmv"]["dram_bytes"],
-                                 "kernels": ["k_mc_black_spmv"]}
+    for cls, names in (("red_pass", ("k_cc_red", "k_sc_red")),
+                       ("black_pass", ("k_cc_black", "k_mc_black_spmv")),
+                       ("decouple", ("k_decouple_compact", "k_decouple_ws"))):
+        for k in names:
+            if k in traffic:
+                traffic[cls] = {"dram_bytes": traffic[k]["dram_bytes"], "kernels": [k]}
+                break
     with open(os.path.join(dst, "ncu_traffic.json"), "w") as fh:
         json.dump(traffic, fh, indent=1)
     with open(os.path.join(dst, "ncu_summary.md"), "w") as fh:
