@@ -188,10 +188,13 @@ def algorithmic_bytes(grid, nw, precond="ras", form="explicit"):
         # z_b read (9 n), v_b written (9 n/2), one dot operand (9 n/2)
         out["spmv"] = 8 * (81 * m + 18 * n)
         if form == "compact":
-            # compact operator (csrc/compact.cu): per block only the 6 flux rows
-            # (54 m per colour), plus D^-1[:, :6] of each row's cell (54 n/2)
-            out["ilu_apply"] = 8 * (54 * m + 27 * n + 9 * n)
-            out["spmv"] = 8 * (54 * m + 27 * n + 18 * n)
+            # compact operator (csrc/compact.cu)
+            # red pass y_r = B_rb z_b: 54 per red block, z_b gathered (9 n/2),
+            # y written (6 n/2); black pass v_b = z_b - D_b^-1[:, :6] B'_br y: 36
+            # per black block, D_b^-1[:, :6] (54 n/2), y gathered (6 n/2), z_b,
+            # v_b and the dot operand (3 x 9 n/2)
+            out["ilu_apply"] = 8 * (54 * m + 7.5 * n)
+            out["spmv"] = 8 * (36 * m + 43.5 * n)
             # k_rhs_schur (resid in, rhs out) + k_decouple_compact (diag and rhs
             # in, D^-1[:, :6] and rhs out)
             out["decouple"] = 8 * (18 * n + 81 * n + 9 * n + 54 * n + 9 * n)

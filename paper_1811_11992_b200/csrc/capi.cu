@@ -93,6 +93,7 @@ struct isc_ctx {
   int offd_rows = NU;   // rows of offd holding data (ROW_OS after an un-decoupled assembly)
   bool compact = false;   // decoupled in compact form (compact.cu): diag = D^-1[:, :CR], offd raw
   bool compact_ok = true; // ISC_COMPACT=0 disables the compact form (A/B switch)
+  double* cbp = nullptr;  // compact form: B'_bd = B_bd[:6, :] D_nb^-1[:, :6] of black cells
   bool assembled = false;   // the last assembly was isc_assemble (inputs kept for FD)
   double asm_dt = 0.0;
   int asm_freeze = 0;
@@ -478,7 +479,7 @@ extern "C" int isc_destroy(isc_ctx* ctx) {
                   ctx->pk, ctx->vk, ctx->phat, ctx->shat, ctx->sk, ctx->tk, ctx->sc,
                   ctx->partial, ctx->partial2, ctx->fbuf, ctx->flags, ctx->fail_d, ctx->schur, ctx->st_c, ctx->accn_c, ctx->stage,
                   ctx->halo_send_lo, ctx->halo_send_hi, ctx->halo_recv_lo, ctx->halo_recv_hi,
-                  ctx->gm_V, ctx->gm_h};
+                  ctx->gm_V, ctx->gm_h, ctx->cbp};
   if (ctx->comm.nccl && nccl_api().CommDestroy) nccl_api().CommDestroy(ctx->comm.nccl);
   free_ilu(ctx);
   for (void* p : ptrs)
@@ -994,6 +995,12 @@ extern "C" int isc_decouple(isc_ctx* ctx, int64_t* bad_cell, int32_t* bad_col) {
   // system (compact.cu)
   ctx->compact = ctx->compact_ok && ctx->precond == ISC_PRECOND_MCILU && ctx->g.colored &&
                  ctx->mc_schur && MC_SCHUR && ctx->offd_rows == ROW_OS;
+  if (ctx->compact && !ctx->cbp &&
+      cudaMalloc(&ctx->cbp, (size_t)NDIR * CR * CR * n * 8) != cudaSuccess) {
+    cudaGetLastError();
+    ctx->cbp = nullptr;
+    ctx->compact = false;   // no room for B': the explicit form
+  }
   if (ctx->compact) {
     const int64_t owned = (int64_t)(ctx->g.kw_hi - ctx->g.kw_lo) * ctx->g.nxny;
     k_decouple_compact<<<grid1d(owned, 32), dim3(32, NU), 0, st>>>(ctx->g, ctx->diag, ctx->rhs,
@@ -1082,7 +1089,7 @@ extern "C" int isc_precond_setup(isc_ctx* ctx, int64_t* bad_cell) {
     }
     if (ctx->compact)
       k_mc_factor_compact<<<grid1d(ctx->g.tw_hi - ctx->g.tw_lo, 32), dim3(32, NU), 0, st>>>(
-          ctx->g, ctx->offd, ctx->diag, ctx->mc_uinv, ctx->fail_d);
+          ctx->g, ctx->offd, ctx->diag, ctx->mc_uinv, ctx->cbp, ctx->fail_d);
     else
       k_mc_factor<<<grid1d(nblack, 32), dim3(32, NU), 0, st>>>(ctx->g, ctx->offd, ctx->mc_uinv,
                                                               ctx->fail_d, cross);
@@ -1631,8 +1638,7 @@ static void sc_rhs_launch(isc_ctx* ctx, const Dims& g, int blocks, const double*
 }
 static void sc_red_launch(isc_ctx* ctx, const Dims& g, int blocks, double* z) {
   if (ctx->compact)
-    k_cc_red<<<blocks, dim3(32, CR), 0, ctx->stream>>>(
-        g, ctx->offd, ctx->diag, z, nullptr, z, nullptr, nullptr, nullptr, nullptr, 0, 0);
+    k_cc_red<<<blocks, dim3(32, CR), 0, ctx->stream>>>(g, ctx->offd, z);
   else
     k_sc_red<<<blocks, dim3(32, NU), 0, ctx->stream>>>(g, ctx->offd, z);
 }
@@ -1648,8 +1654,8 @@ template <int K>
 static void sc_black_launch(isc_ctx* ctx, const Dims& g, int blocks, const double* z, double* v,
                             const double* w0, const double* w1, int stride, int slot0) {
   if (ctx->compact)
-    k_cc_black<K><<<blocks, dim3(32, CR), 0, ctx->stream>>>(
-        g, ctx->offd, ctx->diag, z, z, v, nullptr, w0, w1, ctx->partial, stride, slot0);
+    k_cc_black<K><<<blocks, dim3(32, CR), 0, ctx->stream>>>(g, ctx->cbp, ctx->diag, z, v, w0, w1,
+                                                            ctx->partial, stride, slot0);
   else
     k_mc_black_spmv<K><<<blocks, dim3(32, NU), 0, ctx->stream>>>(g, ctx->offd, z, v, w0, w1,
                                                                 ctx->partial, stride, slot0);

@@ -213,13 +213,6 @@ __device__ __forceinline__ void cpass(
       double* __restrict__ out2, const double* __restrict__ w0, const double* __restrict__ w1,   \
       double *partial, int stride, int slot0
 #define CP_PASS offd, dinv, src, base, out, out2, w0, w1, partial, stride, slot0
-__global__ void __launch_bounds__(32 * CR, CP_MINB) k_cc_red(CP_ARGS) {
-  cpass<0, -1, false, 0>(g, CP_PASS);
-}
-template <int K>
-__global__ void __launch_bounds__(32 * CR, CP_MINB) k_cc_black(CP_ARGS) {
-  cpass<1, 1, true, K>(g, CP_PASS);
-}
 __global__ void __launch_bounds__(32 * CR, CP_MINB) k_cc_rhs(CP_ARGS) {
   cpass<1, -1, true, 0>(g, CP_PASS);
 }
@@ -231,14 +224,113 @@ __global__ void __launch_bounds__(32 * CR, CP_MINB) k_cc_spmv(CP_ARGS) {
   cpass<COL, 1, true, 0>(g, CP_PASS);
 }
 
+// The product S z_b of the Krylov iteration, in two half passes that need
+// no D^-1 on the red side:
+//   red pass   y_r = sum_d B_rd[:CR, :] z_b(nb)                 (CR rows)
+//   black pass v_b = z_b - D_b^-1[:, :CR] sum_d B'_bd y(nb),
+//              B'_bd = B_bd[:CR, :] D_nb^-1[:, :CR]   (CR x CR, from the factorisation)
+// since (D_b^-1 B_bd)(D_r^-1 B_rd') = D_b^-1[:, :CR] B'_bd B_rd'[:CR, :].
+// Per product 6x54 + 6x36 + 54 matrix values per cell pair instead of
+// 2 x (6x54 + 54). y lives in rows 0..CR-1 of z's red positions.
+#ifndef CC_MINB
+#define CC_MINB 4
+#endif
+__global__ void __launch_bounds__(32 * CR, CC_MINB) k_cc_red(Dims g, const double* __restrict__ offd,
+                                                             double* __restrict__ z) {
+  const int64_t n = g.n;
+  const int ls = threadIdx.x, r = threadIdx.y;
+  const int64_t t = g.tw_lo + (int64_t)blockIdx.x * 32 + ls;
+  if (t >= g.tw_hi) return;
+  const int64_t c = colour_pos(g, 0, t);
+  int i, j, k;
+  const int64_t cell = locate(g, c, i, j, k);
+  double s = 0.0;
+#pragma unroll
+  for (int d = 0; d < NDIR; ++d) {
+    const int64_t nb = nb_pos(g, cell, i, j, k, d);
+    if (nb < 0) continue;
+    const double* blk = offd + (int64_t)((d * NU + r) * NU) * n + c;
+    double tt = 0.0;
+#pragma unroll
+    for (int u = 0; u < NU; ++u) tt += blk[(int64_t)u * n] * z[(int64_t)u * n + nb];
+    s += tt;
+  }
+  z[(int64_t)r * n + c] = s;
+}
+
+// K = 1: per-warp partials of v . w0; K = 2: v . v and v . w1
+// (partial[k*stride*CR + slot*CR + y])
+template <int K>
+__global__ void __launch_bounds__(32 * CR, CC_MINB) k_cc_black(
+    Dims g, const double* __restrict__ bp, const double* __restrict__ dinv,
+    const double* __restrict__ z, double* __restrict__ v, const double* __restrict__ w0,
+    const double* __restrict__ w1, double* partial, int stride, int slot0) {
+  __shared__ double ts[CR][32];
+  const int64_t n = g.n;
+  const int ls = threadIdx.x, r = threadIdx.y;
+  const int64_t t = g.tw_lo + (int64_t)blockIdx.x * 32 + ls;
+  const bool live = t < g.tw_hi;
+  int64_t c = 0;
+  int k = 0;
+  double acc[K];
+#pragma unroll
+  for (int q = 0; q < K; ++q) acc[q] = 0.0;
+  if (live) {
+    c = colour_pos(g, 1, t);
+    int i, j;
+    const int64_t cell = locate(g, c, i, j, k);
+    double s = 0.0;
+#pragma unroll
+    for (int d = 0; d < NDIR; ++d) {
+      const int64_t nb = nb_pos(g, cell, i, j, k, d);
+      if (nb < 0) continue;
+      const double* blk = bp + (int64_t)((d * CR + r) * CR) * n + c;
+      double tt = 0.0;
+#pragma unroll
+      for (int e = 0; e < CR; ++e) tt += blk[(int64_t)e * n] * z[(int64_t)e * n + nb];
+      s += tt;
+    }
+    ts[r][ls] = s;
+  }
+  __syncthreads();
+  if (live) {
+    const bool own = owned_k(g, k);
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const int q = r + h * CR;
+      if (q >= NU) break;
+      const double wd = K == 1 ? w0[(int64_t)q * n + c] : w1[(int64_t)q * n + c];
+      double m = 0.0;
+#pragma unroll
+      for (int rr = 0; rr < CR; ++rr) m += dinv[(int64_t)(q * CR + rr) * n + c] * ts[rr][ls];
+      const double val = z[(int64_t)q * n + c] - m;
+      v[(int64_t)q * n + c] = val;
+      if (own) {
+        if (K == 1) acc[0] += val * wd;
+        if (K == 2) { acc[0] += val * val; acc[K - 1] += val * wd; }
+      }
+    }
+  }
+#pragma unroll
+  for (int q = 0; q < K; ++q) {
+    double x = acc[q];
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) x += __shfl_down_sync(0xffffffffu, x, o);
+    if (ls == 0) partial[(int64_t)q * stride * CR + (int64_t)(slot0 + blockIdx.x) * CR + r] = x;
+  }
+}
+
 // U_b = I - D_b^-1 sum_d B_bd D_nb^-1 B_nb,back (the multicolour ILU(0)
 // pivot block, k_mc_factor's product with the decoupled blocks formed on the
-// fly), then its Gauss-Jordan inverse. Thread (black cell lane, column u).
+// fly), then its Gauss-Jordan inverse; B'_bd = B_bd[:CR, :] D_nb^-1[:, :CR]
+// is kept for the black passes (bp[((d*CR + q)*CR + s)*n + p]). Thread
+// (black cell lane, column u).
 __global__ void __launch_bounds__(32 * NU, MCF_MINB) k_mc_factor_compact(
     Dims g, const double* __restrict__ offd, const double* __restrict__ dinv,
-    double* __restrict__ uinv, int* fail) {
+    double* __restrict__ uinv, double* __restrict__ bp, int* fail) {
   __shared__ double bsh[CR][NU][32];    // B_bd flux rows of the black cell
   __shared__ double dsh[NU][CR][32];    // D_nb^-1[:, :CR] of the red neighbour
+  __shared__ double bpsh[CR][CR][32];   // B'_bd = B_bd[:CR, :] D_nb^-1[:, :CR]
   __shared__ double colk[NU][32];
   __shared__ int pivs[32];
   const int64_t n = g.n;
@@ -249,7 +341,7 @@ __global__ void __launch_bounds__(32 * NU, MCF_MINB) k_mc_factor_compact(
   int i = 0, j = 0, k = 0;
   const int64_t cell = in ? locate(g, c, i, j, k) : 0;
   const bool live = in && owned_k(g, k);
-  double qcol[CR];   // Q[:, u] = sum_d B_bd (D_nb^-1 B_back)[:, u]
+  double qcol[CR];   // Q[:, u] = sum_d B'_bd B_back[:CR, u]
 #pragma unroll
   for (int q = 0; q < CR; ++q) qcol[q] = 0.0;
 #pragma unroll 1
@@ -267,24 +359,31 @@ __global__ void __launch_bounds__(32 * NU, MCF_MINB) k_mc_factor_compact(
       }
     }
     __syncthreads();
-    if (nb >= 0) {
+    if (nb >= 0) {   // B'_bd: 36 entries, 4 per thread; kept for the black passes
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        const int idx = u * 4 + e;
+        if (idx < CR * CR) {
+          const int q = idx / CR, s2 = idx % CR;
+          double s = 0.0;
+#pragma unroll
+          for (int a = 0; a < NU; ++a) s += bsh[q][a][ls] * dsh[a][s2][ls];
+          bpsh[q][s2][ls] = s;
+          bp[(int64_t)((d * CR + q) * CR + s2) * n + c] = s;
+        }
+      }
+    }
+    __syncthreads();
+    if (nb >= 0) {   // Q[:, u] += B'_bd B_back[:CR, u]
       const double* Bo = offd + (int64_t)(opposite(d) * NB + u) * n + nb;   // column u
       double bc[CR];
 #pragma unroll
       for (int r = 0; r < CR; ++r) bc[r] = Bo[(int64_t)(r * NU) * n];
-      double cc[NU];   // (D_nb^-1 B_back)[:, u]
-#pragma unroll
-      for (int a = 0; a < NU; ++a) {
-        double s = 0.0;
-#pragma unroll
-        for (int r = 0; r < CR; ++r) s += dsh[a][r][ls] * bc[r];
-        cc[a] = s;
-      }
 #pragma unroll
       for (int q = 0; q < CR; ++q) {
         double s = 0.0;
 #pragma unroll
-        for (int a = 0; a < NU; ++a) s += bsh[q][a][ls] * cc[a];
+        for (int r = 0; r < CR; ++r) s += bpsh[q][r][ls] * bc[r];
         qcol[q] += s;
       }
     }
