@@ -94,6 +94,7 @@ struct isc_ctx {
   bool compact = false;   // decoupled in compact form (compact.cu): diag = D^-1[:, :CR], offd raw
   bool compact_ok = true; // ISC_COMPACT=0 disables the compact form (A/B switch)
   double* cbp = nullptr;  // compact form: B'_bd = B_bd[:6, :] D_nb^-1[:, :6] of black cells
+  bool gb_fresh = false;  // compact form: the factorisation left g_b in rk / rhat
   bool assembled = false;   // the last assembly was isc_assemble (inputs kept for FD)
   double asm_dt = 0.0;
   int asm_freeze = 0;
@@ -1087,10 +1088,14 @@ extern "C" int isc_precond_setup(isc_ctx* ctx, int64_t* bad_cell) {
       // compact form: the owner's D^-1[:, :CR] of the ghost planes as well
       if (ctx->compact && halo_exchange(ctx, ctx->diag, CR * NU)) return ISC_CUDA_ERROR;
     }
-    if (ctx->compact)
+    if (ctx->compact) {
+      // the reduced rhs g_b is formed on the way (red neighbours' b: halo on slabs)
+      if (cross && halo_exchange(ctx, ctx->rhs, NU)) return ISC_CUDA_ERROR;
       k_mc_factor_compact<<<grid1d(ctx->g.tw_hi - ctx->g.tw_lo, 32), dim3(32, NU), 0, st>>>(
-          ctx->g, ctx->offd, ctx->diag, ctx->mc_uinv, ctx->cbp, ctx->fail_d);
-    else
+          ctx->g, ctx->offd, ctx->diag, ctx->mc_uinv, ctx->cbp, ctx->fail_d, ctx->rhs, ctx->rk,
+          ctx->rhat);
+      ctx->gb_fresh = true;
+    } else
       k_mc_factor<<<grid1d(nblack, 32), dim3(32, NU), 0, st>>>(ctx->g, ctx->offd, ctx->mc_uinv,
                                                               ctx->fail_d, cross);
     CK(cudaGetLastError());
@@ -1686,12 +1691,16 @@ static int bicgstab_schur(isc_ctx* ctx, double tol, int maxiter, int* iters) {
   const double brk = 1e-30 * nb * nb;
   // p, v and t need no clearing: p and v are read only after the first
   // iteration wrote them (S_FIRST), t only where the black pass wrote it
-  TRY(halo_exchange(ctx, b, NU));   // slabs: red neighbours on other ranks
-  {
-    KScope ks(ctx, KT_SPMV);
-    sc_rhs_launch(ctx, g, bh, b, r, rhat);   // g_b
+  if (ctx->compact && ctx->gb_fresh) {
+    ctx->gb_fresh = false;   // g_b already in r and rhat (k_mc_factor_compact)
+  } else {
+    TRY(halo_exchange(ctx, b, NU));   // slabs: red neighbours on other ranks
+    {
+      KScope ks(ctx, KT_SPMV);
+      sc_rhs_launch(ctx, g, bh, b, r, rhat);   // g_b
+    }
+    ++ctx->launches;
   }
-  ++ctx->launches;
   double* sh = ctx->sc_h;
   for (int i = 0; i < S_NSCAL; ++i) sh[i] = 0.0;
   sh[S_RHO_OLD] = 1.0; sh[S_ALPHA] = 1.0; sh[S_OMEGA] = 1.0; sh[S_FIRST] = 1.0;
@@ -1922,12 +1931,17 @@ static int gmres_schur(isc_ctx* ctx, double tol, int maxiter, int* iters) {
   const double nb = std::sqrt(ctx->sc_h[S_BB]);
   *iters = 0;
   if (nb == 0.0) return ISC_OK;
-  TRY(halo_exchange(ctx, b, NU));
-  {
-    KScope ks(ctx, KT_SPMV);
-    sc_rhs_launch(ctx, g, bh, b, r, gb);   // r = g_b (x_b = 0)
+  if (ctx->compact && ctx->gb_fresh) {   // g_b from the factorisation
+    ctx->gb_fresh = false;
+    CK(cudaMemcpyAsync(gb, r, len * 8, cudaMemcpyDeviceToDevice, st));
+  } else {
+    TRY(halo_exchange(ctx, b, NU));
+    {
+      KScope ks(ctx, KT_SPMV);
+      sc_rhs_launch(ctx, g, bh, b, r, gb);   // r = g_b (x_b = 0)
+    }
+    ++ctx->launches;
   }
-  ++ctx->launches;
   auto matvec = [&](double* zz, double* out) -> int {   // out = S zz (zz: black in, red scratch)
     {
       KScope ks(ctx, KT_ILU_APPLY);

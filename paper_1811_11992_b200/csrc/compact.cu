@@ -28,7 +28,10 @@ constexpr int CR = ROW_OS;   // flux rows of an assembled off-diagonal block
 
 // D^-1 of every owned cell (reference GJ: pivot tolerance 1e-13 max|D|,
 // partial pivoting) and rhs <- D^-1 rhs; block (32 cells, column u)
-__global__ void __launch_bounds__(32 * NU, 2) k_decouple_compact(Dims g, double* diag, double* rhs,
+#ifndef DCC_MINB
+#define DCC_MINB 3   // C4 sweep 2..4: 1.76 -> 1.61 ms at 3
+#endif
+__global__ void __launch_bounds__(32 * NU, DCC_MINB) k_decouple_compact(Dims g, double* diag, double* rhs,
                                                                  int* flags,
                                                                  unsigned long long* bad) {
   __shared__ double inv[NU][NU][32];
@@ -233,7 +236,7 @@ __global__ void __launch_bounds__(32 * CR, CP_MINB) k_cc_spmv(CP_ARGS) {
 // Per product 6x54 + 6x36 + 54 matrix values per cell pair instead of
 // 2 x (6x54 + 54). y lives in rows 0..CR-1 of z's red positions.
 #ifndef CC_MINB
-#define CC_MINB 4
+#define CC_MINB 6   // C4 sweep 3..6: 0.402/0.420 -> 0.396/0.407 ms (red/black) at 6
 #endif
 __global__ void __launch_bounds__(32 * CR, CC_MINB) k_cc_red(Dims g, const double* __restrict__ offd,
                                                              double* __restrict__ z) {
@@ -323,11 +326,17 @@ __global__ void __launch_bounds__(32 * CR, CC_MINB) k_cc_black(
 // U_b = I - D_b^-1 sum_d B_bd D_nb^-1 B_nb,back (the multicolour ILU(0)
 // pivot block, k_mc_factor's product with the decoupled blocks formed on the
 // fly), then its Gauss-Jordan inverse; B'_bd = B_bd[:CR, :] D_nb^-1[:, :CR]
-// is kept for the black passes (bp[((d*CR + q)*CR + s)*n + p]). Thread
-// (black cell lane, column u).
-__global__ void __launch_bounds__(32 * NU, MCF_MINB) k_mc_factor_compact(
+// is kept for the black passes (bp[((d*CR + q)*CR + s)*n + p]). With
+// g1 != nullptr the reduced rhs g_b = b_b - D_b^-1[:, :CR] sum_d B_bd b_r(nb)
+// is formed on the way (the blocks are in shared memory anyway) and written
+// to g1 and g2. Thread (black cell lane, column u).
+#ifndef MCFC_MINB
+#define MCFC_MINB 3   // C4 sweep 2..4: 4.06 / 3.51 / 3.46 ms (4 spills once g_b is folded in)
+#endif
+__global__ void __launch_bounds__(32 * NU, MCFC_MINB) k_mc_factor_compact(
     Dims g, const double* __restrict__ offd, const double* __restrict__ dinv,
-    double* __restrict__ uinv, double* __restrict__ bp, int* fail) {
+    double* __restrict__ uinv, double* __restrict__ bp, int* fail, const double* __restrict__ b,
+    double* __restrict__ g1, double* __restrict__ g2) {
   __shared__ double bsh[CR][NU][32];    // B_bd flux rows of the black cell
   __shared__ double dsh[NU][CR][32];    // D_nb^-1[:, :CR] of the red neighbour
   __shared__ double bpsh[CR][CR][32];   // B'_bd = B_bd[:CR, :] D_nb^-1[:, :CR]
@@ -341,6 +350,7 @@ __global__ void __launch_bounds__(32 * NU, MCF_MINB) k_mc_factor_compact(
   int i = 0, j = 0, k = 0;
   const int64_t cell = in ? locate(g, c, i, j, k) : 0;
   const bool live = in && owned_k(g, k);
+  double grow = 0.0;   // (sum_d B_bd b_r(nb))[u], u < CR
   double qcol[CR];   // Q[:, u] = sum_d B'_bd B_back[:CR, u]
 #pragma unroll
   for (int q = 0; q < CR; ++q) qcol[q] = 0.0;
@@ -359,6 +369,12 @@ __global__ void __launch_bounds__(32 * NU, MCF_MINB) k_mc_factor_compact(
       }
     }
     __syncthreads();
+    if (g1 && nb >= 0 && u < CR) {
+      double s = 0.0;
+#pragma unroll
+      for (int a = 0; a < NU; ++a) s += bsh[u][a][ls] * b[(int64_t)a * n + nb];
+      grow += s;
+    }
     if (nb >= 0) {   // B'_bd: 36 entries, 4 per thread; kept for the black passes
 #pragma unroll
       for (int e = 0; e < 4; ++e) {
@@ -397,7 +413,16 @@ __global__ void __launch_bounds__(32 * NU, MCF_MINB) k_mc_factor_compact(
       dsh[idx / CR][idx % CR][ls] = dinv[(int64_t)idx * n + c];
     }
   }
+  if (u < CR) colk[u][ls] = grow;
   __syncthreads();
+  if (g1 && live) {
+    double m = 0.0;
+#pragma unroll
+    for (int r = 0; r < CR; ++r) m += dsh[u][r][ls] * colk[r][ls];
+    const double gv = b[(int64_t)u * n + c] - m;
+    g1[(int64_t)u * n + c] = gv;
+    g2[(int64_t)u * n + c] = gv;
+  }
   double ucol[NU], icol[NU];
 #pragma unroll
   for (int q = 0; q < NU; ++q) {

@@ -525,3 +525,48 @@ def test_gmres_solve_synthetic_and_error_paths(restart):
         BlockSolver(grid, ws, precond="mcilu", krylov="cg")
     with pytest.raises(RuntimeError, match="restart"):
         ws.ctx.set_krylov("gmres", 32)
+
+
+@pytest.mark.parametrize("krylov", ["bicgstab", "gmres"])
+def test_compact_form_repeated_solve(krylov):
+    """Compact form (csrc/compact.cu): the factorisation forms the reduced rhs
+    on the way; a second solve of the same decoupled system (no new
+    factorisation) forms it with the separate pass — same du. The
+    decoupled operator applied by isc_spmv is the explicit one's."""
+    import ctypes
+    from paper_1811_11992_b200 import _native as N
+    from paper_1811_11992_b200.device import DeviceContext, soa_from_rows, state_to_device
+    from tests.golden_states import random_state_like_reference
+    c = case_objects("sub2")
+    st, accn = random_state_like_reference(c, 29)
+    res = {}
+    for form in ("compact", "explicit"):
+        import os
+        if form == "explicit":
+            os.environ["ISC_COMPACT"] = "0"
+        try:
+            ctx = DeviceContext(c.grid, c.pack, c.wells, c.streams, "mcilu")
+        finally:
+            os.environ.pop("ISC_COMPACT", None)
+        ctx.set_krylov(krylov)
+        ctx.assemble(state_to_device(st, ctx.device), st.bhp, soa_from_rows(accn, ctx.device),
+                     2e-3, 2e-3, np.zeros(len(c.wells), bool), False)
+        dus = []
+        for _ in range(2):
+            du = ctx.empty(9, c.grid.ncell)
+            ctx.solve(1e-10, 1000, du)
+            dus.append(du.cpu().numpy())
+        assert ctx.decoupled_form == form
+        x = torch.from_numpy(np.random.default_rng(4).normal(size=(9, c.grid.ncell))).cuda()
+        y = torch.empty_like(x)
+        N.check(ctx.L.isc_spmv(ctx.h, N.ptr(x), N.ptr(y)), "spmv")
+        b = ctx.empty(9, c.grid.ncell)
+        N.check(ctx.L.isc_copy_rhs(ctx.h, N.ptr(b)), "rhs")
+        res[form] = (dus, y.cpu().numpy(), b.cpu().numpy())
+        ctx.close()
+    (d0, d1), y_c, b_c = res["compact"]
+    assert np.linalg.norm(d0 - d1) <= 1e-9 * np.linalg.norm(d0)
+    (e0, _), y_e, b_e = res["explicit"]
+    assert np.linalg.norm(d0 - e0) <= 1e-8 * np.linalg.norm(e0)
+    assert np.max(np.abs(y_c - y_e)) <= 1e-11 * np.max(np.abs(y_e))
+    assert np.max(np.abs(b_c - b_e)) <= 1e-12 * np.max(np.abs(b_e))
