@@ -174,7 +174,12 @@ def algorithmic_bytes(grid, nw, precond="ras", form="explicit"):
     """Compulsory bytes per launch of each kernel class."""
     n, m = grid.ncell, grid.nconn
     out = {
-        "cell+face": 8 * (111 * n + 164 * m),              # SURVEY §8(d) assembly
+        # SURVEY §8(d) assembly 8(111n + 164m), split by kernel: the cell pass
+        # reads state, phi_ref, accn, V, depth (21 n) and writes resid + the
+        # diagonal blocks (90 n); the face passes read gd + td (2 m) and write
+        # both off-diagonal blocks of every connection (162 m)
+        "cell": 8 * 111 * n,
+        "face": 8 * 164 * m,
         "decouple": 8 * (99 * n + 324 * m),                # SURVEY §8(d)
         "spmv": 8 * (162 * m + 18 * n),                    # SURVEY §8(d)
         "ilu_apply": ilu_bytes(ilu_structure_counts(grid), n, m),
@@ -187,6 +192,9 @@ def algorithmic_bytes(grid, nw, precond="ras", form="explicit"):
         # black pass v_b = z_b + B_br w_r: the black rows' blocks (81 m), w_r and
         # z_b read (9 n), v_b written (9 n/2), one dot operand (9 n/2)
         out["spmv"] = 8 * (81 * m + 18 * n)
+        # k_mc_factor: the black rows' blocks and the red neighbours' blocks
+        # pointing back (81 m each), U_b^-1 out (81 n/2)
+        out["mc_factor"] = 8 * (162 * m + 40.5 * n)
         if form == "compact":
             # compact operator (csrc/compact.cu)
             # red pass y_r = B_rb z_b: 54 per red block, z_b gathered (9 n/2),
@@ -198,6 +206,11 @@ def algorithmic_bytes(grid, nw, precond="ras", form="explicit"):
             # k_rhs_schur (resid in, rhs out) + k_decouple_compact (diag and rhs
             # in, D^-1[:, :6] and rhs out)
             out["decouple"] = 8 * (18 * n + 81 * n + 9 * n + 54 * n + 9 * n)
+            # k_mc_factor_compact per black cell: B_bd and B_back flux rows
+            # (54 m each colour), D^-1[:, :6] of both colours (27 n each), the red
+            # neighbours' b (9 n/2), B' out (36 m), U_b^-1 out (81 n/2), g_b out
+            # twice (9 n)
+            out["mc_factor"] = 8 * (144 * m + 54 * n + 4.5 * n + 40.5 * n + 9 * n)
     return out
 
 
@@ -380,10 +393,11 @@ def run_ours(args, rank, world, local):
     algo = algorithmic_bytes(grid, len(wells), case.solver.precond, sim.ctx.decoupled_form)
     ktimes = {KCLASS[i]: {"ms": float(ms8[i]), "launches": int(cnt8[i])} for i in range(8)}
     classes = {"ilu_apply": ("ilu_apply",), "spmv": ("spmv",), "decouple": ("decouple",),
-               "cell+face": ("cell", "face")}
+               "cell": ("cell",), "face": ("face",)}
     if case.solver.precond == "mcilu":   # red pass / black pass of S U_b^-1
         classes = {"red_pass": ("ilu_apply",), "black_pass": ("spmv",),
-                   "decouple": ("decouple",), "cell+face": ("cell", "face")}
+                   "decouple": ("decouple",), "cell": ("cell",), "face": ("face",),
+                   "mc_factor": ("ilu_factor",)}
         algo = dict(algo, red_pass=algo["ilu_apply"], black_pass=algo["spmv"])
     rows = {}
     for key, parts in classes.items():
