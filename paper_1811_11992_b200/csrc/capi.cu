@@ -898,10 +898,23 @@ extern "C" int isc_import_system(isc_ctx* ctx, const double* d_diag, const doubl
     CK(cudaMemcpyAsync(ctx->wout_d, ctx->wout_h, ctx->nw * WOUT * 8, cudaMemcpyHostToDevice,
                        ctx->stream));
   }
+  // flux-only off-diagonal rows (an assembled system's structure): the
+  // multicolour solve may use the compact form
+  int rows = NU;
+  if (ctx->g.colored) {
+    CK(cudaMemsetAsync(ctx->fail_d, 0, 4, ctx->stream));
+    k_flux_rows_only<<<grid1d(ctx->g.n, 256), 256, 0, ctx->stream>>>(ctx->g, ctx->offd,
+                                                                      ctx->fail_d);
+    LAUNCH_CHECK();
+    int nz = 1;
+    CK(cudaMemcpyAsync(&nz, ctx->fail_d, 4, cudaMemcpyDeviceToHost, ctx->stream));
+    CK(cudaStreamSynchronize(ctx->stream));
+    if (nz == 0) rows = ROW_OS;
+  }
   CK(cudaStreamSynchronize(ctx->stream));
   ctx->decoupled = ctx->factored = false;
   ctx->compact = false;
-  ctx->offd_rows = NU;
+  ctx->offd_rows = rows;
   ctx->assembled = false;
   return ISC_OK;
 }

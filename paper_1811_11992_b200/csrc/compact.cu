@@ -493,4 +493,23 @@ __global__ void __launch_bounds__(32 * NU, MCFC_MINB) k_mc_factor_compact(
   }
 }
 
+// An imported system qualifies for the compact form when every
+// off-diagonal block of an existing connection has zero rows CR..8 (the
+// structure an assembled system has): *flag = 1 otherwise.
+__global__ void k_flux_rows_only(Dims g, const double* __restrict__ offd, int* flag) {
+  const int64_t n = g.n;
+  const int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (c >= n) return;
+  int i, j, k;
+  const int64_t cell = locate(g, c, i, j, k);
+  bool nz = false;
+  for (int d = 0; d < NDIR; ++d) {
+    if (nb_pos(g, cell, i, j, k, d) < 0) continue;
+    for (int r = CR; r < NU; ++r)
+#pragma unroll
+      for (int u = 0; u < NU; ++u) nz |= offd[(int64_t)((d * NU + r) * NU + u) * n + c] != 0.0;
+  }
+  if (nz) atomicOr(flag, 1);
+}
+
 }  // namespace isc

@@ -570,3 +570,45 @@ def test_compact_form_repeated_solve(krylov):
     assert np.linalg.norm(d0 - e0) <= 1e-8 * np.linalg.norm(e0)
     assert np.max(np.abs(y_c - y_e)) <= 1e-11 * np.max(np.abs(y_e))
     assert np.max(np.abs(b_c - b_e)) <= 1e-12 * np.max(np.abs(b_e))
+
+
+@pytest.mark.parametrize("krylov", ["bicgstab", "gmres"])
+def test_compact_form_on_imported_flux_row_system(krylov):
+    """An imported system whose off-diagonal blocks have the assembled
+    structure (rows 6..8 zero) takes the compact form: du solves it (dense
+    check), a singular diagonal block is reported with its cell and column
+    (k_decouple_compact), and the preconditioner-only entry point refuses
+    the compact form instead of applying a wrong operator."""
+    from paper_1811_11992_b200 import _native as N
+    from paper_1811_11992_b200.grid import build_grid
+    from paper_1811_11992_b200.synth import synth_system
+    from paper_1811_11992_b200.model import load_pack
+    grid = build_grid(6, 4, 4, 1.0, 1.0, 1.0, 1.0, 1.0, 1.0, 0.3)
+    pack = load_pack("tube3_pack", grid.phi_ref)
+    diag, offd, resid = synth_system(grid, 9, seed=11)
+    offd = offd.copy()
+    offd[:, :, 6:, :] = 0.0
+    ws = Workspace(grid, pack, None, wells=(), streams=(), precond="mcilu")
+    load_system(ws, diag, offd, resid)
+    du, _, it = BlockSolver(grid, ws, tol=1e-12, maxiter=500, precond="mcilu",
+                            krylov=krylov).solve([])
+    assert ws.ctx.decoupled_form == "compact"
+    n = grid.ncell
+    A = np.zeros((9 * n, 9 * n))
+    for c in range(n):
+        A[9 * c:9 * c + 9, 9 * c:9 * c + 9] = diag[c]
+    for ic in range(grid.nconn):
+        a, b = int(grid.conn_a[ic]), int(grid.conn_b[ic])
+        A[9 * a:9 * a + 9, 9 * b:9 * b + 9] = offd[ic, 0]
+        A[9 * b:9 * b + 9, 9 * a:9 * a + 9] = offd[ic, 1]
+    ref = np.linalg.solve(A, -resid.reshape(-1)).reshape(n, 9)
+    assert np.linalg.norm(du - ref) <= 1e-9 * np.linalg.norm(ref), it
+    r_t = torch.zeros(9, n, dtype=torch.float64, device=ws.ctx.device)
+    with pytest.raises(RuntimeError, match="compact"):
+        N.check(ws.ctx.L.isc_precond_apply(ws.ctx.h, N.ptr(r_t), N.ptr(r_t)), "apply")
+    bad = diag.copy()
+    bad[13, :, 5] = 0.0
+    load_system(ws, bad, offd, resid)
+    with pytest.raises(SingularCellBlock, match="cell 13 is singular at column 5"):
+        BlockSolver(grid, ws, tol=1e-8, maxiter=100, precond="mcilu", krylov=krylov).solve([])
+    assert ws.ctx.decoupled_form == "none"
