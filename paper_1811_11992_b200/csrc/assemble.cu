@@ -45,6 +45,7 @@ struct CellArgs {
   double* __restrict__ diag;
   unsigned long long* bad;             // min index of a pore-space-exhausted cell
   int64_t c_begin, c_end;              // positions handled by k_cell (pipelined staging)
+  double* __restrict__ mid = nullptr;  // NMID x n: property values for k_cell_rows (split pass)
 };
 
 // Where one cell evaluation's outputs go. The analytic pass stores them in
@@ -52,6 +53,7 @@ struct CellArgs {
 // and residual rows in registers and drops every analytic partial (dead code
 // after inlining).
 struct CellSinkGlobal {
+  static constexpr bool kMidOut = false, kUnroll = false;
   const CellArgs& A;
   int64_t n, c;
   __device__ double& rec(int f) { return A.rec[(int64_t)f * n + c]; }
@@ -62,7 +64,11 @@ struct CellSinkGlobal {
   __device__ void fail() { atomicMin(A.bad, (unsigned long long)cell_of(A.g, c)); }
 };
 
+#ifndef PROBE_UNROLL
+#define PROBE_UNROLL true   // numeric Jacobian at C4: 72 -> 30.5 ms unrolled
+#endif
 struct CellSinkProbe {
+  static constexpr bool kMidOut = false, kUnroll = PROBE_UNROLL;
   double v[NREC];      // record fields at the probed state
   double rows[NU];     // residual rows of the cell part (compose)
   bool failed = false;
@@ -73,6 +79,21 @@ struct CellSinkProbe {
   __device__ void resid(int r, double x) { rows[r] = x; }
   __device__ void fail() { failed = true; }
   __device__ double f(int k) const { return v[k]; }   // record accessor (flux, wells)
+};
+
+// The property half of the split cell pass: the record and the values the
+// reaction / accumulation rows need (A.mid), nothing else.
+struct CellSinkProps {
+  static constexpr bool kMidOut = true, kUnroll = false;
+  const CellArgs& A;
+  int64_t n, c;
+  __device__ double& rec(int f) { return A.rec[(int64_t)f * n + c]; }
+  __device__ void mid(int f, double v) { A.mid[(int64_t)f * n + c] = v; }
+  __device__ void acc(int, double) {}
+  __device__ void src(int, double) {}
+  __device__ void diag(int, int, double) {}
+  __device__ void resid(int, double) {}
+  __device__ void fail() { atomicMin(A.bad, (unsigned long long)cell_of(A.g, c)); }
 };
 
 // dyfull (NF x NU) with its structure (_kernels.py:220-252): the water row
@@ -102,6 +123,287 @@ struct DyFull {
   }
 };
 
+// Values of the property pass that the reaction / accumulation rows use
+// besides the record: stored per cell by k_cell_props for k_cell_rows
+// (mid[f*n + c]), or kept in registers when one thread does both (probes).
+enum MidField {
+  MI_PHI, MI_DPHI_P, MI_DPHI_T, MI_PHIF, MI_DPHIF_CC, MI_PCOG, MI_RO, MI_DRO_P, MI_DRO_T,
+  MI_DRO_X, MI_RG = MI_DRO_X + NCO, MI_DRG, MI_RW = MI_DRG + NU, MI_DRW_P, MI_DRW_T, MI_UW,
+  MI_DUW_P, MI_DUW_T, MI_UO, MI_DUO_P, MI_DUO_T, MI_UG, MI_DUG, NMID = MI_DUG + NU
+};
+struct CellMid {   // register form
+  double v[NMID];
+  DyFull dyf;
+  double yf[NF], dpcog, hli[NCO];
+};
+
+// Reactions, accumulation rows and the cell-local composition of one cell
+// (_kernels.py:430-608, 797-825) from the property pass's values m.
+template <class S, bool kUnroll = false>
+__device__ __forceinline__ void cell_rows(const Model& M, const CellArgs& A, int64_t c,
+                                          const double (&u_)[NU], const CellMid& m, S& s) {
+  const int64_t n = A.g.n;
+  const double* rk = M.rockp;
+  const double p = u_[0], t = u_[CT], sw = u_[CSW], sg = u_[CSG], cc = u_[CCC];
+  double x[NCO], y[NCG];
+#pragma unroll
+  for (int i = 0; i < NCO; ++i) x[i] = u_[1 + i];
+#pragma unroll
+  for (int j = 0; j < NCG; ++j) y[j] = u_[1 + NCO + j];
+  const double so = 1.0 - sw - sg;
+  const double t_ref = rk[RK_TREF];
+  const double phi = m.v[MI_PHI], dphi_p = m.v[MI_DPHI_P], dphi_t = m.v[MI_DPHI_T];
+  const double phif = m.v[MI_PHIF], dphif_cc = m.v[MI_DPHIF_CC];
+  const double pcog = m.v[MI_PCOG], dpcog = m.dpcog;
+  const double ro = m.v[MI_RO], dro_p = m.v[MI_DRO_P], dro_t = m.v[MI_DRO_T], ro2 = ro * ro;
+  double dro_x[NCO], hli[NCO];
+#pragma unroll
+  for (int i = 0; i < NCO; ++i) { dro_x[i] = m.v[MI_DRO_X + i]; hli[i] = m.hli[i]; }
+  const double rg = m.v[MI_RG];
+  double drg[NU], dug[NU];
+#pragma unroll
+  for (int u = 0; u < NU; ++u) { drg[u] = m.v[MI_DRG + u]; dug[u] = m.v[MI_DUG + u]; }
+  const double rw = m.v[MI_RW], drw_p = m.v[MI_DRW_P], drw_t = m.v[MI_DRW_T];
+  const double uw = m.v[MI_UW], duw_p = m.v[MI_DUW_P], duw_t = m.v[MI_DUW_T];
+  const double uo = m.v[MI_UO], duo_p = m.v[MI_DUO_P], duo_t = m.v[MI_DUO_T];
+  const double ug = m.v[MI_UG];
+  const DyFull dyf = m.dyf;
+  double yf[NF];
+#pragma unroll
+  for (int a = 0; a < NF; ++a) yf[a] = m.yf[a];
+
+  // reactions first (_kernels.py:537-608): r and d r / d u per reaction
+  double rr_v[MAXREAC], rr_d[MAXREAC][NU];
+  bool rr_on[MAXREAC];
+  {
+    const double pg = p + pcog;
+    const double ccr = cc > 0.0 ? cc : 0.0;
+auto react = [&](const int q) {
+      rr_on[q] = false;
+      rr_v[q] = 0.0;
+#pragma unroll
+      for (int u = 0; u < NU; ++u) rr_d[q][u] = 0.0;
+      if (q >= M.nreac) return;
+      double dpp[NU], dfm[NU];
+#pragma unroll
+      for (int u = 0; u < NU; ++u) { dpp[u] = 0.0; dfm[u] = 0.0; }
+      const int oxi = M.ox[q];
+      double pp = 0.0;
+      if (oxi >= 0) {
+        double y_ox = 0.0;
+#pragma unroll
+        for (int a = 0; a < NF; ++a) if (a == oxi) y_ox = yf[a];
+        pp = y_ox * pg;
+        if (pp > 0.0) {
+#pragma unroll
+          for (int a = 0; a < NF; ++a)
+            if (a == oxi) {
+#pragma unroll
+              for (int u = 0; u < NU; ++u) dpp[u] = dyf(a, u) * pg;
+            }
+          dpp[0] += y_ox;
+          dpp[CSG] += y_ox * dpcog;
+        } else {
+          pp = 0.0;
+        }
+      }
+      const int fui = M.fuel[q];
+      double fm = 0.0;
+      if (fui >= 0) {
+        double xf = 0.0;
+#pragma unroll
+        for (int i = 0; i < NCO; ++i) if (i == fui) xf = x[i];
+        fm = phif * so * ro * xf;
+        if (fm > 0.0) {
+          const double base = so * ro * xf;
+          dfm[0] = dphi_p * base + phif * so * dro_p * xf;
+          dfm[CT] = dphi_t * base + phif * so * dro_t * xf;
+          dfm[CSW] = -phif * ro * xf;
+          dfm[CSG] = -phif * ro * xf;
+          dfm[CCC] = dphif_cc * base;
+#pragma unroll
+          for (int i = 0; i < NCO; ++i) dfm[1 + i] = phif * so * dro_x[i] * xf;
+#pragma unroll
+          for (int i = 0; i < NCO; ++i) if (i == fui) dfm[1 + i] += phif * so * ro;
+        } else {
+          fm = 0.0;
+        }
+      }
+      double o[5];
+      reaction_rate_one(M.law[q], M.rcoef[q][0], M.rcoef[q][1], t, pp, fm, ccr, M.ccmax, o);
+      if (o[0] == 0.0 && o[1] == 0.0 && o[2] == 0.0 && o[3] == 0.0 && o[4] == 0.0) return;
+      rr_on[q] = true;
+      rr_v[q] = o[0];
+#pragma unroll
+      for (int u = 0; u < NU; ++u) rr_d[q][u] = o[2] * dpp[u] + o[3] * dfm[u];
+      rr_d[q][CT] += o[1];
+      if (o[4] != 0.0 && cc >= 0.0) rr_d[q][CCC] += o[4];
+        };
+    if constexpr (kUnroll) {
+#pragma unroll
+      for (int q = 0; q < MAXREAC; ++q) react(q);
+    } else {
+#pragma unroll 1
+      for (int q = 0; q < MAXREAC; ++q) react(q);
+    }
+  }
+
+  // accumulation rows + composition, row by row (_kernels.py:430-535, 797-825)
+  const double mw_g = rg * sg;
+  const double vol = A.vol[c];
+  const double vdt = vol / A.dt;
+  double ur, dur_t;
+  ur = rk[RK_CP1] * (t - t_ref) + 0.5 * rk[RK_CP2] * (t * t - t_ref * t_ref);   // _props.py:208-213
+  dur_t = rk[RK_CP1] + rk[RK_CP2] * t;
+  const double uc = rk[RK_COKE_CP] * (t - t_ref);
+  const double duc_t = rk[RK_COKE_CP];
+  const double hl = A.hl_area ? A.hl_area[c] : 0.0;
+
+auto row = [&](const int r) {
+    double accr, dacc[NU];
+    if (r == 0) {
+      const double a_w = rw * sw + mw_g * yf[0];
+      accr = phif * a_w;
+#pragma unroll
+      for (int u = 0; u < NU; ++u) {
+        double d = (drg[u] * sg * yf[0] + mw_g * dyf(0, u));
+        if (u == 0) d += drw_p * sw;
+        else if (u == CT) d += drw_t * sw;
+        else if (u == CSW) d += rw;
+        if (u == CSG) d += rg * yf[0];
+        dacc[u] = phif * d;
+      }
+      dacc[0] += dphi_p * a_w;
+      dacc[CT] += dphi_t * a_w;
+      dacc[CCC] += dphif_cc * a_w;
+    } else if (r < 1 + NCO) {
+      const int i = r - 1;
+      const double a_i = ro * so * x[i] + mw_g * yf[r];
+      accr = phif * a_i;
+#pragma unroll
+      for (int u = 0; u < NU; ++u) {
+        double d = drg[u] * sg * yf[r] + mw_g * dyf(r, u);
+        if (u == 0) d += dro_p * so * x[i];
+        else if (u == CT) d += dro_t * so * x[i];
+        else if (u == CSW || u == CSG) d += -ro * x[i] + (u == CSG ? rg * yf[r] : 0.0);
+        if (1 <= u && u < 1 + NCO) {
+          d += dro_x[u - 1] * so * x[i];
+          if (u - 1 == i) d += ro * so;
+        }
+        dacc[u] = phif * d;
+      }
+      dacc[0] += dphi_p * a_i;
+      dacc[CT] += dphi_t * a_i;
+      dacc[CCC] += dphif_cc * a_i;
+    } else if (r < NF) {
+      const int j = r - 1 - NCO;
+      const double a_j = mw_g * y[j];
+      accr = phif * a_j;
+#pragma unroll
+      for (int u = 0; u < NU; ++u) {
+        double d = drg[u] * sg * y[j];
+        if (u == CSG) d += rg * y[j];
+        if (u == 1 + NCO + j) d += mw_g;
+        dacc[u] = phif * d;
+      }
+      dacc[0] += dphi_p * a_j;
+      dacc[CT] += dphi_t * a_j;
+      dacc[CCC] += dphif_cc * a_j;
+    } else if (r == ROW_E) {
+      const double a_e = rw * sw * uw + ro * so * uo + mw_g * ug;
+      accr = phif * a_e + (1.0 - phi) * ur + cc * uc;
+#pragma unroll
+      for (int u = 0; u < NU; ++u) {
+        double d = drg[u] * sg * ug + mw_g * dug[u];
+        if (u == 0) {
+          d += drw_p * sw * uw + rw * sw * duw_p;
+          d += dro_p * so * uo + ro * so * duo_p;
+        } else if (u == CT) {
+          d += drw_t * sw * uw + rw * sw * duw_t;
+          d += dro_t * so * uo + ro * so * duo_t;
+        } else if (u == CSW) {
+          d += rw * uw - ro * uo;
+        }
+        if (u == CSG) d += -ro * uo + rg * ug;
+        if (1 <= u && u < 1 + NCO) {
+          const double duo_xi = hli[u - 1] + p * dro_x[u - 1] / ro2;
+          d += dro_x[u - 1] * so * uo + ro * so * duo_xi;
+        }
+        dacc[u] = phif * d;
+      }
+      dacc[0] += dphi_p * a_e - dphi_p * ur;
+      dacc[CT] += dphi_t * a_e - dphi_t * ur + (1.0 - phi) * dur_t + cc * duc_t;
+      dacc[CCC] += dphif_cc * a_e + uc;
+    } else if (r == ROW_OS) {
+      double sx = 0.0;
+#pragma unroll
+      for (int u = 0; u < NU; ++u) dacc[u] = 0.0;
+#pragma unroll
+      for (int i = 0; i < NCO; ++i) { sx += x[i]; dacc[1 + i] = 1.0; }
+      accr = sx - 1.0;
+    } else if (r == ROW_GS) {
+      double sy = 0.0;
+#pragma unroll
+      for (int u = 0; u < NU; ++u) dacc[u] = 0.0;
+#pragma unroll
+      for (int a = 0; a < NF; ++a) {
+        sy += yf[a];
+#pragma unroll
+        for (int u = 0; u < NU; ++u)
+          if (DyFull::nz(a, u)) dacc[u] += dyf(a, u);
+      }
+      accr = sy - 1.0;
+    } else {  // coke
+#pragma unroll
+      for (int u = 0; u < NU; ++u) dacc[u] = 0.0;
+      dacc[CCC] = 1.0;
+      accr = cc;
+    }
+    // reaction source row r (stoichiometric row: nmat row r for r < NF,
+    // nmat row NF for the coke row, heats for the energy row)
+    double srcr = 0.0, dsrc[NU];
+#pragma unroll
+    for (int u = 0; u < NU; ++u) dsrc[u] = 0.0;
+    if (r < NF || r == ROW_CK || r == ROW_E) {
+#pragma unroll
+      for (int q = 0; q < MAXREAC; ++q) {
+        if (!rr_on[q]) continue;
+        const double s = r < NF ? M.nmat[r][q] : (r == ROW_CK ? M.nmat[NF][q] : M.rcoef[q][2]);
+        if (s != 0.0) {
+          srcr += s * rr_v[q];
+#pragma unroll
+          for (int u = 0; u < NU; ++u) dsrc[u] += s * rr_d[q][u];
+        }
+      }
+    }
+    s.acc(r, accr);
+    s.src(r, srcr);
+    double res;
+    if (r == ROW_OS || r == ROW_GS) {
+      res = accr;
+#pragma unroll
+      for (int u = 0; u < NU; ++u) s.diag(r, u, dacc[u]);
+    } else {
+      res = vdt * (accr - A.accn[r * n + c]) - vol * srcr;
+#pragma unroll
+      for (int u = 0; u < NU; ++u) {
+        double dv = vdt * dacc[u] - vol * dsrc[u];
+        if (r == ROW_E && u == ROW_E && hl > 0.0) dv += hl * A.hl_kob / A.hl_d;
+        s.diag(r, u, dv);
+      }
+    }
+    if (r == ROW_E && hl > 0.0) res += hl * A.hl_kob * ((t - A.hl_tini) / A.hl_d - A.hl_rho);
+    s.resid(r, res);
+    };
+  if constexpr (kUnroll) {
+#pragma unroll
+    for (int r = 0; r < NU; ++r) row(r);
+  } else {
+#pragma unroll 1
+    for (int r = 0; r < NU; ++r) row(r);
+  }
+}
+
 // cell_eval + compose for the cell at position c with unknowns u_
 // (_kernels.py:66-610, 797-825); inputs other than the unknowns from A.
 template <class S>
@@ -124,6 +426,7 @@ __device__ __forceinline__ void cell_eval(const Model& M, const CellArgs& A, int
   double phif, dphif_cc;
   if (rho_coke > 0.0 && isfinite(rho_coke)) { phif = phi - cc / rho_coke; dphif_cc = -1.0 / rho_coke; }
   else { phif = phi; dphif_cc = 0.0; }
+  if constexpr (S::kMidOut) s.mid(MI_PHIF, phif);   // k_cell_rows skips failed cells
   if (phif <= 0.0) { s.fail(); return; }
   const double t_ref = rk[RK_TREF], eps_per = rk[RK_EPS_PER];
 #define REC(f) s.rec(f)
@@ -424,223 +727,41 @@ __device__ __forceinline__ void cell_eval(const Model& M, const CellArgs& A, int
   }
 #undef REC
 
-  // reactions first (_kernels.py:537-608): r and d r / d u per reaction
-  double rr_v[MAXREAC], rr_d[MAXREAC][NU];
-  bool rr_on[MAXREAC];
-  {
-    const double pg = p + pcog;
-    const double ccr = cc > 0.0 ? cc : 0.0;
-#pragma unroll 1
-    for (int q = 0; q < MAXREAC; ++q) {
-      rr_on[q] = false;
-      rr_v[q] = 0.0;
+  // the reaction / accumulation rows (cell_rows) from the property values
+  if constexpr (S::kMidOut) {
+    s.mid(MI_PHI, phi); s.mid(MI_DPHI_P, dphi_p); s.mid(MI_DPHI_T, dphi_t);
+    s.mid(MI_PHIF, phif); s.mid(MI_DPHIF_CC, dphif_cc); s.mid(MI_PCOG, pcog);
+    s.mid(MI_RO, ro); s.mid(MI_DRO_P, dro_p); s.mid(MI_DRO_T, dro_t);
 #pragma unroll
-      for (int u = 0; u < NU; ++u) rr_d[q][u] = 0.0;
-      if (q >= M.nreac) continue;
-      double dpp[NU], dfm[NU];
+    for (int i = 0; i < NCO; ++i) s.mid(MI_DRO_X + i, dro_x[i]);
+    s.mid(MI_RG, rg);
 #pragma unroll
-      for (int u = 0; u < NU; ++u) { dpp[u] = 0.0; dfm[u] = 0.0; }
-      const int oxi = M.ox[q];
-      double pp = 0.0;
-      if (oxi >= 0) {
-        double y_ox = 0.0;
+    for (int u = 0; u < NU; ++u) s.mid(MI_DRG + u, drg[u]);
+    s.mid(MI_RW, rw); s.mid(MI_DRW_P, drw_p); s.mid(MI_DRW_T, drw_t);
+    s.mid(MI_UW, uw); s.mid(MI_DUW_P, duw_p); s.mid(MI_DUW_T, duw_t);
+    s.mid(MI_UO, uo); s.mid(MI_DUO_P, duo_p); s.mid(MI_DUO_T, duo_t);
+    s.mid(MI_UG, ug);
 #pragma unroll
-        for (int a = 0; a < NF; ++a) if (a == oxi) y_ox = yf[a];
-        pp = y_ox * pg;
-        if (pp > 0.0) {
+    for (int u = 0; u < NU; ++u) s.mid(MI_DUG + u, dug[u]);
+  } else {
+    CellMid m;
+    m.v[MI_PHI] = phi; m.v[MI_DPHI_P] = dphi_p; m.v[MI_DPHI_T] = dphi_t;
+    m.v[MI_PHIF] = phif; m.v[MI_DPHIF_CC] = dphif_cc; m.v[MI_PCOG] = pcog;
+    m.v[MI_RO] = ro; m.v[MI_DRO_P] = dro_p; m.v[MI_DRO_T] = dro_t;
 #pragma unroll
-          for (int a = 0; a < NF; ++a)
-            if (a == oxi) {
+    for (int i = 0; i < NCO; ++i) { m.v[MI_DRO_X + i] = dro_x[i]; m.hli[i] = hli[i]; }
+    m.v[MI_RG] = rg;
 #pragma unroll
-              for (int u = 0; u < NU; ++u) dpp[u] = dyf(a, u) * pg;
-            }
-          dpp[0] += y_ox;
-          dpp[CSG] += y_ox * dpcog;
-        } else {
-          pp = 0.0;
-        }
-      }
-      const int fui = M.fuel[q];
-      double fm = 0.0;
-      if (fui >= 0) {
-        double xf = 0.0;
+    for (int u = 0; u < NU; ++u) { m.v[MI_DRG + u] = drg[u]; m.v[MI_DUG + u] = dug[u]; }
+    m.v[MI_RW] = rw; m.v[MI_DRW_P] = drw_p; m.v[MI_DRW_T] = drw_t;
+    m.v[MI_UW] = uw; m.v[MI_DUW_P] = duw_p; m.v[MI_DUW_T] = duw_t;
+    m.v[MI_UO] = uo; m.v[MI_DUO_P] = duo_p; m.v[MI_DUO_T] = duo_t;
+    m.v[MI_UG] = ug;
+    m.dyf = dyf;
 #pragma unroll
-        for (int i = 0; i < NCO; ++i) if (i == fui) xf = x[i];
-        fm = phif * so * ro * xf;
-        if (fm > 0.0) {
-          const double base = so * ro * xf;
-          dfm[0] = dphi_p * base + phif * so * dro_p * xf;
-          dfm[CT] = dphi_t * base + phif * so * dro_t * xf;
-          dfm[CSW] = -phif * ro * xf;
-          dfm[CSG] = -phif * ro * xf;
-          dfm[CCC] = dphif_cc * base;
-#pragma unroll
-          for (int i = 0; i < NCO; ++i) dfm[1 + i] = phif * so * dro_x[i] * xf;
-#pragma unroll
-          for (int i = 0; i < NCO; ++i) if (i == fui) dfm[1 + i] += phif * so * ro;
-        } else {
-          fm = 0.0;
-        }
-      }
-      double o[5];
-      reaction_rate_one(M.law[q], M.rcoef[q][0], M.rcoef[q][1], t, pp, fm, ccr, M.ccmax, o);
-      if (o[0] == 0.0 && o[1] == 0.0 && o[2] == 0.0 && o[3] == 0.0 && o[4] == 0.0) continue;
-      rr_on[q] = true;
-      rr_v[q] = o[0];
-#pragma unroll
-      for (int u = 0; u < NU; ++u) rr_d[q][u] = o[2] * dpp[u] + o[3] * dfm[u];
-      rr_d[q][CT] += o[1];
-      if (o[4] != 0.0 && cc >= 0.0) rr_d[q][CCC] += o[4];
-    }
-  }
-
-  // accumulation rows + composition, row by row (_kernels.py:430-535, 797-825)
-  const double mw_g = rg * sg;
-  const double vol = A.vol[c];
-  const double vdt = vol / A.dt;
-  double ur, dur_t;
-  ur = rk[RK_CP1] * (t - t_ref) + 0.5 * rk[RK_CP2] * (t * t - t_ref * t_ref);   // _props.py:208-213
-  dur_t = rk[RK_CP1] + rk[RK_CP2] * t;
-  const double uc = rk[RK_COKE_CP] * (t - t_ref);
-  const double duc_t = rk[RK_COKE_CP];
-  const double hl = A.hl_area ? A.hl_area[c] : 0.0;
-
-#pragma unroll 1
-  for (int r = 0; r < NU; ++r) {
-    double accr, dacc[NU];
-    if (r == 0) {
-      const double a_w = rw * sw + mw_g * yf[0];
-      accr = phif * a_w;
-#pragma unroll
-      for (int u = 0; u < NU; ++u) {
-        double d = (drg[u] * sg * yf[0] + mw_g * dyf(0, u));
-        if (u == 0) d += drw_p * sw;
-        else if (u == CT) d += drw_t * sw;
-        else if (u == CSW) d += rw;
-        if (u == CSG) d += rg * yf[0];
-        dacc[u] = phif * d;
-      }
-      dacc[0] += dphi_p * a_w;
-      dacc[CT] += dphi_t * a_w;
-      dacc[CCC] += dphif_cc * a_w;
-    } else if (r < 1 + NCO) {
-      const int i = r - 1;
-      const double a_i = ro * so * x[i] + mw_g * yf[r];
-      accr = phif * a_i;
-#pragma unroll
-      for (int u = 0; u < NU; ++u) {
-        double d = drg[u] * sg * yf[r] + mw_g * dyf(r, u);
-        if (u == 0) d += dro_p * so * x[i];
-        else if (u == CT) d += dro_t * so * x[i];
-        else if (u == CSW || u == CSG) d += -ro * x[i] + (u == CSG ? rg * yf[r] : 0.0);
-        if (1 <= u && u < 1 + NCO) {
-          d += dro_x[u - 1] * so * x[i];
-          if (u - 1 == i) d += ro * so;
-        }
-        dacc[u] = phif * d;
-      }
-      dacc[0] += dphi_p * a_i;
-      dacc[CT] += dphi_t * a_i;
-      dacc[CCC] += dphif_cc * a_i;
-    } else if (r < NF) {
-      const int j = r - 1 - NCO;
-      const double a_j = mw_g * y[j];
-      accr = phif * a_j;
-#pragma unroll
-      for (int u = 0; u < NU; ++u) {
-        double d = drg[u] * sg * y[j];
-        if (u == CSG) d += rg * y[j];
-        if (u == 1 + NCO + j) d += mw_g;
-        dacc[u] = phif * d;
-      }
-      dacc[0] += dphi_p * a_j;
-      dacc[CT] += dphi_t * a_j;
-      dacc[CCC] += dphif_cc * a_j;
-    } else if (r == ROW_E) {
-      const double a_e = rw * sw * uw + ro * so * uo + mw_g * ug;
-      accr = phif * a_e + (1.0 - phi) * ur + cc * uc;
-#pragma unroll
-      for (int u = 0; u < NU; ++u) {
-        double d = drg[u] * sg * ug + mw_g * dug[u];
-        if (u == 0) {
-          d += drw_p * sw * uw + rw * sw * duw_p;
-          d += dro_p * so * uo + ro * so * duo_p;
-        } else if (u == CT) {
-          d += drw_t * sw * uw + rw * sw * duw_t;
-          d += dro_t * so * uo + ro * so * duo_t;
-        } else if (u == CSW) {
-          d += rw * uw - ro * uo;
-        }
-        if (u == CSG) d += -ro * uo + rg * ug;
-        if (1 <= u && u < 1 + NCO) {
-          const double duo_xi = hli[u - 1] + p * dro_x[u - 1] / ro2;
-          d += dro_x[u - 1] * so * uo + ro * so * duo_xi;
-        }
-        dacc[u] = phif * d;
-      }
-      dacc[0] += dphi_p * a_e - dphi_p * ur;
-      dacc[CT] += dphi_t * a_e - dphi_t * ur + (1.0 - phi) * dur_t + cc * duc_t;
-      dacc[CCC] += dphif_cc * a_e + uc;
-    } else if (r == ROW_OS) {
-      double sx = 0.0;
-#pragma unroll
-      for (int u = 0; u < NU; ++u) dacc[u] = 0.0;
-#pragma unroll
-      for (int i = 0; i < NCO; ++i) { sx += x[i]; dacc[1 + i] = 1.0; }
-      accr = sx - 1.0;
-    } else if (r == ROW_GS) {
-      double sy = 0.0;
-#pragma unroll
-      for (int u = 0; u < NU; ++u) dacc[u] = 0.0;
-#pragma unroll
-      for (int a = 0; a < NF; ++a) {
-        sy += yf[a];
-#pragma unroll
-        for (int u = 0; u < NU; ++u)
-          if (DyFull::nz(a, u)) dacc[u] += dyf(a, u);
-      }
-      accr = sy - 1.0;
-    } else {  // coke
-#pragma unroll
-      for (int u = 0; u < NU; ++u) dacc[u] = 0.0;
-      dacc[CCC] = 1.0;
-      accr = cc;
-    }
-    // reaction source row r (stoichiometric row: nmat row r for r < NF,
-    // nmat row NF for the coke row, heats for the energy row)
-    double srcr = 0.0, dsrc[NU];
-#pragma unroll
-    for (int u = 0; u < NU; ++u) dsrc[u] = 0.0;
-    if (r < NF || r == ROW_CK || r == ROW_E) {
-#pragma unroll
-      for (int q = 0; q < MAXREAC; ++q) {
-        if (!rr_on[q]) continue;
-        const double s = r < NF ? M.nmat[r][q] : (r == ROW_CK ? M.nmat[NF][q] : M.rcoef[q][2]);
-        if (s != 0.0) {
-          srcr += s * rr_v[q];
-#pragma unroll
-          for (int u = 0; u < NU; ++u) dsrc[u] += s * rr_d[q][u];
-        }
-      }
-    }
-    s.acc(r, accr);
-    s.src(r, srcr);
-    double res;
-    if (r == ROW_OS || r == ROW_GS) {
-      res = accr;
-#pragma unroll
-      for (int u = 0; u < NU; ++u) s.diag(r, u, dacc[u]);
-    } else {
-      res = vdt * (accr - A.accn[r * n + c]) - vol * srcr;
-#pragma unroll
-      for (int u = 0; u < NU; ++u) {
-        double dv = vdt * dacc[u] - vol * dsrc[u];
-        if (r == ROW_E && u == ROW_E && hl > 0.0) dv += hl * A.hl_kob / A.hl_d;
-        s.diag(r, u, dv);
-      }
-    }
-    if (r == ROW_E && hl > 0.0) res += hl * A.hl_kob * ((t - A.hl_tini) / A.hl_d - A.hl_rho);
-    s.resid(r, res);
+    for (int a = 0; a < NF; ++a) m.yf[a] = yf[a];
+    m.dpcog = dpcog;
+    cell_rows<S, S::kUnroll>(M, A, c, u_, m, s);
   }
 }
 
@@ -656,6 +777,58 @@ __global__ void __launch_bounds__(128, CELL_MINB) k_cell(const Model M, const Ce
   for (int u = 0; u < NU; ++u) u_[u] = A.st[u * n + c];
   CellSinkGlobal s{A, n, c};
   cell_eval(M, A, c, u_, s);
+}
+
+// The same cell pass split in two kernels with fewer live values each: the
+// properties (record + A.mid) and then the reaction / accumulation rows
+// (cell_rows over the stored values). Same arithmetic, same results.
+#ifndef CELLP_MINB
+#define CELLP_MINB 8   // C4 sweep 4..12 (rows at 2): 8 best
+#endif
+#ifndef CELLR_MINB
+#define CELLR_MINB 2   // C4 sweep 1..6 (props at 8): 1-2 best (255 registers, 128 B spilled)
+#endif
+#ifndef CELLR_UNROLL
+#define CELLR_UNROLL true
+#endif
+__global__ void __launch_bounds__(128, CELLP_MINB) k_cell_props(const Model M, const CellArgs A) {
+  const int64_t n = A.g.n;
+  const int64_t c = A.c_begin + (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (c >= A.c_end) return;
+  double u_[NU];
+#pragma unroll
+  for (int u = 0; u < NU; ++u) u_[u] = A.st[u * n + c];
+  CellSinkProps s{A, n, c};
+  cell_eval(M, A, c, u_, s);
+}
+
+__global__ void __launch_bounds__(128, CELLR_MINB) k_cell_rows(const Model M, const CellArgs A) {
+  const int64_t n = A.g.n;
+  const int64_t c = A.c_begin + (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (c >= A.c_end) return;
+  if (A.mid[(int64_t)MI_PHIF * n + c] <= 0.0) return;   // pore space exhausted (reported)
+  double u_[NU];
+#pragma unroll
+  for (int u = 0; u < NU; ++u) u_[u] = A.st[u * n + c];
+  CellMid m;
+#pragma unroll
+  for (int f = 0; f < NMID; ++f) m.v[f] = A.mid[(int64_t)f * n + c];
+  const double* rec = A.rec + c;
+#pragma unroll
+  for (int a = 0; a < NF; ++a) m.yf[a] = rec[(int64_t)(R_Y + a) * n];
+  m.dyf.w[0] = rec[(int64_t)R_DY0_P * n];
+  m.dyf.w[1] = rec[(int64_t)R_DY0_T * n];
+  m.dyf.w[2] = rec[(int64_t)R_DY0_SW * n];
+#pragma unroll
+  for (int i = 0; i < NCO; ++i) {
+#pragma unroll
+    for (int q = 0; q < 4; ++q) m.dyf.o[i][q] = rec[(int64_t)(R_DYO + 4 * i + q) * n];
+    m.dyf.o[i][4] = i == M.heavy ? m.dyf.o[i][3] : 0.0;   // d/dSg == d/dSw (heaviest oil)
+    m.hli[i] = rec[(int64_t)(R_DHPH1_X + i) * n];
+  }
+  m.dpcog = rec[(int64_t)R_DPOT2_SG * n];
+  CellSinkGlobal s{A, n, c};
+  cell_rows<CellSinkGlobal, CELLR_UNROLL>(M, A, c, u_, m, s);
 }
 
 // -------------------------------------------------------------------- face

@@ -21,6 +21,10 @@
 #include "solver.cu"
 #include "compact.cu"
 
+#ifndef CELL_SPLIT
+#define CELL_SPLIT 1   // cell pass as k_cell_props + k_cell_rows
+#endif
+
 #ifndef MC_SCHUR
 #define MC_SCHUR 1   // mcilu on the red-eliminated system (0: full-system fused form)
 #endif
@@ -93,6 +97,7 @@ struct isc_ctx {
   int offd_rows = NU;   // rows of offd holding data (ROW_OS after an un-decoupled assembly)
   bool compact = false;   // decoupled in compact form (compact.cu): diag = D^-1[:, :CR], offd raw
   bool compact_ok = true; // ISC_COMPACT=0 disables the compact form (A/B switch)
+  double* cmid = nullptr; // split cell pass: property values for k_cell_rows (NMID x n)
   double* cbp = nullptr;  // compact form: B'_bd = B_bd[:6, :] D_nb^-1[:, :6] of black cells
   bool gb_fresh = false;  // compact form: the factorisation left g_b in rk / rhat
   bool assembled = false;   // the last assembly was isc_assemble (inputs kept for FD)
@@ -438,6 +443,7 @@ extern "C" int isc_create(const isc_model_desc* md, const isc_grid_desc* gdsc, i
   ALLOC(ctx->capped_d, std::max(1, nwells));
   // assembly buffers
   ALLOC(ctx->rec, (size_t)NREC * n * 8);
+  if (CELL_SPLIT) ALLOC(ctx->cmid, (size_t)NMID * n * 8);
   ALLOC(ctx->fbuf, (size_t)3 * ROW_OS * n * 8);
   ALLOC(ctx->acc, (size_t)NU * n * 8);
   ALLOC(ctx->src, (size_t)NU * n * 8);
@@ -480,7 +486,7 @@ extern "C" int isc_destroy(isc_ctx* ctx) {
                   ctx->pk, ctx->vk, ctx->phat, ctx->shat, ctx->sk, ctx->tk, ctx->sc,
                   ctx->partial, ctx->partial2, ctx->fbuf, ctx->flags, ctx->fail_d, ctx->schur, ctx->st_c, ctx->accn_c, ctx->stage,
                   ctx->halo_send_lo, ctx->halo_send_hi, ctx->halo_recv_lo, ctx->halo_recv_hi,
-                  ctx->gm_V, ctx->gm_h, ctx->cbp};
+                  ctx->gm_V, ctx->gm_h, ctx->cbp, ctx->cmid};
   if (ctx->comm.nccl && nccl_api().CommDestroy) nccl_api().CommDestroy(ctx->comm.nccl);
   free_ilu(ctx);
   for (void* p : ptrs)
@@ -549,6 +555,20 @@ static int stage_end(isc_ctx* ctx, int st) {
 
 // ------------------------------------------------------------- assemble
 
+// the cell pass over positions [A.c_begin, A.c_end): one kernel, or the
+// property and row halves (fewer live values per kernel; assemble.cu)
+static void launch_cell(isc_ctx* ctx, CellArgs A, cudaStream_t st) {
+  const int blocks = grid1d(A.c_end - A.c_begin, 128);
+  if (CELL_SPLIT) {
+    A.mid = ctx->cmid;
+    k_cell_props<<<blocks, 128, 0, st>>>(ctx->M, A);
+    k_cell_rows<<<blocks, 128, 0, st>>>(ctx->M, A);
+    ++ctx->launches;
+  } else {
+    k_cell<<<blocks, 128, 0, st>>>(ctx->M, A);
+  }
+}
+
 extern "C" int isc_assemble(isc_ctx* ctx, const double* d_state, const double* h_bhp,
                             const double* d_accn, double dt, double t_new,
                             const uint8_t* h_capped, int32_t freeze, double* h_wells_out,
@@ -581,7 +601,7 @@ extern "C" int isc_assemble(isc_ctx* ctx, const double* d_state, const double* h
              ctx->resid, ctx->diag, ctx->bad_d, 0, n};
   if (!cell_pre) {
     KScope ks(ctx, KT_CELL);
-    k_cell<<<grid1d(n, 128), 128, 0, st>>>(ctx->M, A);
+    launch_cell(ctx, A, st);
   }
   LAUNCH_CHECK();
   CK(cudaMemcpyAsync(ctx->bad_h, ctx->bad_d, 8, cudaMemcpyDeviceToHost, st));
@@ -705,7 +725,7 @@ extern "C" int isc_assemble_decoupled(isc_ctx* ctx, const double* d_state, const
   CellArgs A{ctx->g, d_state, ctx->phi_ref, ctx->vol, ctx->hl_area, ctx->hl_kob, ctx->hl_d,
              ctx->hl_rho, ctx->hl_tini, d_accn, dt, ctx->rec, ctx->acc, ctx->src,
              ctx->resid, ctx->diag, ctx->bad_d, 0, n};
-  { KScope ks(ctx, KT_CELL); k_cell<<<grid1d(n, 128), 128, 0, st>>>(ctx->M, A); }
+  { KScope ks(ctx, KT_CELL); launch_cell(ctx, A, st); }
   LAUNCH_CHECK();
   CK(cudaMemcpyAsync(ctx->bad_h, ctx->bad_d, 8, cudaMemcpyDeviceToHost, st));
   CK(cudaStreamSynchronize(st));
@@ -817,7 +837,7 @@ extern "C" int isc_assemble_host(isc_ctx* ctx, const double* h_p, const double* 
       A.c_end = c1;
       {
         KScope ks(ctx, KT_CELL);
-        k_cell<<<grid1d(cnt, 128), 128, 0, st>>>(ctx->M, A);
+        launch_cell(ctx, A, st);
       }
       KScope ks(ctx, KT_FACE);
       // x/y faces of this chunk's cells; z faces of the plane below it and of
