@@ -1210,6 +1210,41 @@ __global__ void __launch_bounds__(32 * 3, FEVAL_MINB) k_face_eval(const FaceArgs
   }
 }
 
+// The light rows (0..4) and the energy row (5, every phase) as separate
+// kernels so that each gets its own register budget / occupancy.
+#ifndef FEVL_MINB
+#define FEVL_MINB 8
+#endif
+#ifndef FEVE_MINB
+#define FEVE_MINB 5   // C4 sweep 4..8: face pair 4.06 -> 3.97 ms at 5
+#endif
+__global__ void __launch_bounds__(32 * 3, FEVL_MINB) k_face_eval_light(const FaceArgs2 A2,
+                                                                       int64_t c_begin,
+                                                                       int64_t c_end, int axis_lo) {
+  const int64_t c = c_begin + (int64_t)blockIdx.x * 32 + threadIdx.x;
+  if (c >= c_end) return;
+  const int axis = axis_lo + threadIdx.y;
+  int i, j, k;
+  const int64_t cell = locate(A2.F.g, c, i, j, k);
+  switch (blockIdx.y) {   // block-uniform
+    case 0: face_eval_row<0>(A2, c, cell, i, j, k, axis); break;
+    case 1: face_eval_row<1>(A2, c, cell, i, j, k, axis); break;
+    case 2: face_eval_row<2>(A2, c, cell, i, j, k, axis); break;
+    case 3: face_eval_row<3>(A2, c, cell, i, j, k, axis); break;
+    default: face_eval_row<4>(A2, c, cell, i, j, k, axis); break;
+  }
+}
+__global__ void __launch_bounds__(32 * 3, FEVE_MINB) k_face_eval_energy(const FaceArgs2 A2,
+                                                                        int64_t c_begin,
+                                                                        int64_t c_end, int axis_lo) {
+  const int64_t c = c_begin + (int64_t)blockIdx.x * 32 + threadIdx.x;
+  if (c >= c_end) return;
+  const int axis = axis_lo + threadIdx.y;
+  int i, j, k;
+  const int64_t cell = locate(A2.F.g, c, i, j, k);
+  face_eval_row<ROW_E>(A2, c, cell, i, j, k, axis);
+}
+
 // grid (ceil(owned cells / 32)); block (32, ROW_OS). Owned planes only:
 // ghost rows (z-slabs) carry no equation.
 __global__ void __launch_bounds__(32 * ROW_OS) k_face_gather(const FaceArgs2 A2) {

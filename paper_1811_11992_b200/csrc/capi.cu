@@ -21,6 +21,9 @@
 #include "solver.cu"
 #include "compact.cu"
 
+#ifndef FACE_SPLIT
+#define FACE_SPLIT 1   // k_face_eval as light rows + energy row kernels
+#endif
 #ifndef CELL_SPLIT
 #define CELL_SPLIT 1   // cell pass as k_cell_props + k_cell_rows
 #endif
@@ -555,6 +558,18 @@ static int stage_end(isc_ctx* ctx, int st) {
 
 // ------------------------------------------------------------- assemble
 
+// face evaluation over lower cells [c0, c1), axes axis_lo .. axis_lo+naxes-1
+static void launch_face_eval(const FaceArgs2& F2, int64_t c0, int64_t c1, int axis_lo, int naxes,
+                             cudaStream_t st) {
+  const int blocks = grid1d(c1 - c0, 32);
+  if (FACE_SPLIT) {
+    k_face_eval_light<<<dim3(blocks, ROW_E), dim3(32, naxes), 0, st>>>(F2, c0, c1, axis_lo);
+    k_face_eval_energy<<<blocks, dim3(32, naxes), 0, st>>>(F2, c0, c1, axis_lo);
+  } else {
+    k_face_eval<<<dim3(blocks, ROW_OS), dim3(32, naxes), 0, st>>>(F2, c0, c1, axis_lo);
+  }
+}
+
 // the cell pass over positions [A.c_begin, A.c_end): one kernel, or the
 // property and row halves (fewer live values per kernel; assemble.cu)
 static void launch_cell(isc_ctx* ctx, CellArgs A, cudaStream_t st) {
@@ -628,7 +643,7 @@ extern "C" int isc_assemble(isc_ctx* ctx, const double* d_state, const double* h
     if (FACE_CENTRIC) {
       FaceArgs2 F2{F, ctx->fbuf};
       if (!face_pre)
-        k_face_eval<<<dim3(grid1d(n, 32), ROW_OS), dim3(32, 3), 0, st>>>(F2, 0, n, 0);
+        launch_face_eval(F2, 0, n, 0, 3, st);
       k_face_gather<<<grid1d((int64_t)(ctx->g.kw_hi - ctx->g.kw_lo) * ctx->g.nxny, 32),
                       dim3(32, ROW_OS), 0, st>>>(F2);
       ++ctx->launches;
@@ -842,17 +857,17 @@ extern "C" int isc_assemble_host(isc_ctx* ctx, const double* h_p, const double* 
       KScope ks(ctx, KT_FACE);
       // x/y faces of this chunk's cells; z faces of the plane below it and of
       // all but its last plane (their upper records now exist)
-      k_face_eval<<<dim3(grid1d(cnt, 32), ROW_OS), dim3(32, 2), 0, st>>>(F2, c0, c1, 0);
+      launch_face_eval(F2, c0, c1, 0, 2, st);
       const int64_t z0 = std::max<int64_t>(0, (k0 - 1) * g.nxny), z1 = (k1 - 1) * g.nxny;
       if (z1 > z0)
-        k_face_eval<<<dim3(grid1d(z1 - z0, 32), ROW_OS), dim3(32, 1), 0, st>>>(F2, z0, z1, 2);
+        launch_face_eval(F2, z0, z1, 2, 1, st);
       ctx->launches += 3;
     }
   }
   if (pipe) {   // z faces of the top plane (boundary: zero blocks)
     KScope ks(ctx, KT_FACE);
     const int64_t z0 = (int64_t)(g.nz - 1) * g.nxny;
-    k_face_eval<<<dim3(grid1d(n - z0, 32), ROW_OS), dim3(32, 1), 0, st>>>(F2, z0, n, 2);
+    launch_face_eval(F2, z0, n, 2, 1, st);
     ++ctx->launches;
   }
   LAUNCH_CHECK();
