@@ -1,7 +1,9 @@
 """Demo: 40 timesteps of C4 (2 M cells) through newton.Simulator.advance with the
 multicolour solve; prints the run totals (steps, Newton evaluations, BiCGSTAB
-iterations), wall time and the conservation audit. B200: 2.5 s for 91 Newton
-iterations."""
+iterations), wall time and the conservation audit. B200: 1.87 s for 91 Newton
+iterations with the compact operator, 2.44 s with ISC_COMPACT=0 (explicit
+decoupled blocks) — the same 40 steps, Newton and BiCGSTAB counts
+(40, 91, 427) and audit (8.0157e-4) both ways."""
 import sys, time
 sys.path.insert(0, ".")
 from dataclasses import replace
