@@ -9,17 +9,23 @@
 //     (D^-1 B_d) x = D^-1[:, :CR] (B_d[:CR, :] x),   CR = ROW_OS = 6,
 // and the operator is kept as the raw flux rows of B_d (54 values per
 // direction) plus the first CR columns of D^-1 (54 values per cell, stored
-// over the diagonal block): 378 doubles per cell and product instead of the
-// 486 of the explicit decoupled blocks, and the decoupling no longer reads
-// and rewrites the 7.8 GB of off-diagonal blocks at C4 — it only inverts the
+// over the diagonal block). The decoupling (k_decouple_compact) no longer
+// reads and rewrites the 7.8 GB of off-diagonal blocks at C4: it inverts the
 // diagonal blocks (same Gauss-Jordan, pivot rule and failure reporting as
-// k_decouple_ws) and decouples the rhs. The operator is the same matrix; only
-// the rounding of its products differs from the explicit form (which the
+// k_decouple_ws) and decouples the rhs. The factorisation keeps the 6x6
+// blocks B'_bd = B_bd[:CR, :] D_nb^-1[:, :CR] of the black cells, so the
+// product S z_b of the Krylov iteration is
+//     y_r = B_rb z_b (raw rows, k_cc_red),  v_b = z_b - D_b^-1[:, :CR] B'_br y
+//     (k_cc_black)
+// — 6x54 + 6x36 + 54 = 594 matrix values per red/black cell pair against
+// 2 x 6 x 81 = 972 for the explicit blocks. The operator is the same matrix;
+// only the rounding of its products differs from the explicit form (which the
 // mcilu iterates never matched bit for bit anyway: a different
 // preconditioner from the reference's RAS).
 //
-//   dinv[(q*CR + r)*n + p]  q < 9, r < CR   (over diag)
+//   dinv[(q*CR + r)*n + p]          q < 9, r < CR        (over diag)
 //   offd rows r < CR as assembled (undecoupled)
+//   bp[((d*CR + q)*CR + s)*n + p]   black cells, B'_bd   (ctx->cbp)
 #include "common.cuh"
 
 namespace isc {
