@@ -1045,7 +1045,7 @@ extern "C" int isc_decouple(isc_ctx* ctx, int64_t* bad_cell, int32_t* bad_col) {
   ctx->compact = ctx->compact_ok && ctx->precond == ISC_PRECOND_MCILU && ctx->g.colored &&
                  ctx->mc_schur && MC_SCHUR && ctx->offd_rows == ROW_OS;
   if (ctx->compact && !ctx->cbp &&
-      cudaMalloc(&ctx->cbp, (size_t)NDIR * CR * CR * n * 8) != cudaSuccess) {
+      cudaMalloc(&ctx->cbp, (size_t)NDIR * CR * CR * ctx->g.half * 8) != cudaSuccess) {
     cudaGetLastError();
     ctx->cbp = nullptr;
     ctx->compact = false;   // no room for B': the explicit form

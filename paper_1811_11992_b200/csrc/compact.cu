@@ -25,7 +25,7 @@
 //
 //   dinv[(q*CR + r)*n + p]          q < 9, r < CR        (over diag)
 //   offd rows r < CR as assembled (undecoupled)
-//   bp[((d*CR + q)*CR + s)*n + p]   black cells, B'_bd   (ctx->cbp)
+//   bp[((d*CR + q)*CR + s)*half + t] t-th black cell, B'_bd (ctx->cbp)
 #include "common.cuh"
 
 namespace isc {
@@ -293,10 +293,10 @@ __global__ void __launch_bounds__(32 * CR, CC_MINB) k_cc_black(
     for (int d = 0; d < NDIR; ++d) {
       const int64_t nb = nb_pos(g, cell, i, j, k, d);
       if (nb < 0) continue;
-      const double* blk = bp + (int64_t)((d * CR + r) * CR) * n + c;
+      const double* blk = bp + (int64_t)((d * CR + r) * CR) * g.half + t;
       double tt = 0.0;
 #pragma unroll
-      for (int e = 0; e < CR; ++e) tt += blk[(int64_t)e * n] * z[(int64_t)e * n + nb];
+      for (int e = 0; e < CR; ++e) tt += blk[(int64_t)e * g.half] * z[(int64_t)e * n + nb];
       s += tt;
     }
     ts[r][ls] = s;
@@ -332,7 +332,7 @@ __global__ void __launch_bounds__(32 * CR, CC_MINB) k_cc_black(
 // U_b = I - D_b^-1 sum_d B_bd D_nb^-1 B_nb,back (the multicolour ILU(0)
 // pivot block, k_mc_factor's product with the decoupled blocks formed on the
 // fly), then its Gauss-Jordan inverse; B'_bd = B_bd[:CR, :] D_nb^-1[:, :CR]
-// is kept for the black passes (bp[((d*CR + q)*CR + s)*n + p]). With
+// is kept for the black passes (bp[((d*CR + q)*CR + s)*half + t]). With
 // g1 != nullptr the reduced rhs g_b = b_b - D_b^-1[:, :CR] sum_d B_bd b_r(nb)
 // is formed on the way (the blocks are in shared memory anyway) and written
 // to g1 and g2. Thread (black cell lane, column u).
@@ -391,7 +391,7 @@ __global__ void __launch_bounds__(32 * NU, MCFC_MINB) k_mc_factor_compact(
 #pragma unroll
           for (int a = 0; a < NU; ++a) s += bsh[q][a][ls] * dsh[a][s2][ls];
           bpsh[q][s2][ls] = s;
-          bp[(int64_t)((d * CR + q) * CR + s2) * n + c] = s;
+          bp[(int64_t)((d * CR + q) * CR + s2) * g.half + t] = s;
         }
       }
     }
