@@ -1295,9 +1295,17 @@ __global__ void k_wells(const Model M, Dims g, int nw, const WellDev* __restrict
                         const uint8_t* __restrict__ capped, const double* __restrict__ rec,
                         const double* __restrict__ depth, double t_new,
                         double* resid, double* diag, double* wout) {
-  if (threadIdx.x != 0 || blockIdx.x != 0) return;
+  // one thread per well evaluates its perforation (independent of the other
+  // wells); the cell rows are then applied by one thread in well order, the
+  // reference's sequence of updates (wells sharing a cell stay bit-exact)
+  constexpr int WB = 32;
+  __shared__ double s_rows[WB][NU], s_drows[WB][NU][NU], s_heat[WB];
+  __shared__ int64_t s_cell[WB];
   const int64_t n = g.n;
-  for (int w = 0; w < nw; ++w) {
+  for (int base = 0; base < nw; base += WB) {
+  const int w = base + threadIdx.x;
+  const int tw = threadIdx.x;
+  if (w < nw) {
     const WellDev W = wells[w];
     const int64_t c = W.cell;
     const CellView V{rec, n, c};
@@ -1418,14 +1426,16 @@ __global__ void k_wells(const Model M, Dims g, int nw, const WellDev* __restrict
     const bool heater = W.heat_rate != 0.0 && t_new <= W.heat_stop;
 #pragma unroll
     for (int r = 0; r < NU; ++r) {
-      resid[r * n + c] -= rows[r];
+      s_rows[tw][r] = rows[r];
 #pragma unroll
-      for (int u = 0; u < NU; ++u) diag[(int64_t)(r * NU + u) * n + c] -= drows[r][u];
+      for (int u = 0; u < NU; ++u) s_drows[tw][r][u] = drows[r][u];
       o[2 + NU + r] = -brows[r];                       // bcol
       o[2 + 2 * NU + 3 + r] = rows[r];                 // comp_rates
     }
+    s_cell[tw] = c;
+    s_heat[tw] = 0.0;
     if (heater) {
-      resid[ROW_E * n + c] -= W.heat_rate;
+      s_heat[tw] = W.heat_rate;
       o[2 + 2 * NU + 3 + ROW_E] += W.heat_rate;
     }
     o[2 + 2 * NU + 0] = qph[0];
@@ -1441,6 +1451,19 @@ __global__ void k_wells(const Model M, Dims g, int nw, const WellDev* __restrict
     o[1] = dwdb;
 #pragma unroll
     for (int u = 0; u < NU; ++u) o[2 + u] = zero_row ? 0.0 : dqs[u];   // wrow
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    for (int q = 0; q < WB && base + q < nw; ++q) {
+      const int64_t c = s_cell[q];
+      for (int r = 0; r < NU; ++r) {
+        resid[r * n + c] -= s_rows[q][r];
+        for (int u = 0; u < NU; ++u) diag[(int64_t)(r * NU + u) * n + c] -= s_drows[q][r][u];
+      }
+      if (s_heat[q] != 0.0) resid[ROW_E * n + c] -= s_heat[q];
+    }
+  }
+  __syncthreads();
   }
 }
 
