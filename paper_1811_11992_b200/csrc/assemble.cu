@@ -53,7 +53,7 @@ struct CellArgs {
 // and residual rows in registers and drops every analytic partial (dead code
 // after inlining).
 struct CellSinkGlobal {
-  static constexpr bool kMidOut = false, kUnroll = false;
+  static constexpr bool kMidOut = false, kUnroll = false, kSplitGas = false;
   const CellArgs& A;
   int64_t n, c;
   __device__ double& rec(int f) { return A.rec[(int64_t)f * n + c]; }
@@ -68,7 +68,7 @@ struct CellSinkGlobal {
 #define PROBE_UNROLL true   // numeric Jacobian at C4: 72 -> 30.5 ms unrolled
 #endif
 struct CellSinkProbe {
-  static constexpr bool kMidOut = false, kUnroll = PROBE_UNROLL;
+  static constexpr bool kMidOut = false, kUnroll = PROBE_UNROLL, kSplitGas = false;
   double v[NREC];      // record fields at the probed state
   double rows[NU];     // residual rows of the cell part (compose)
   bool failed = false;
@@ -81,10 +81,13 @@ struct CellSinkProbe {
   __device__ double f(int k) const { return v[k]; }   // record accessor (flux, wells)
 };
 
+#ifndef CELL_GAS_SPLIT
+#define CELL_GAS_SPLIT 1   // split cell pass: the gas phase in its own kernel (k_cell_gas)
+#endif
 // The property half of the split cell pass: the record and the values the
 // reaction / accumulation rows need (A.mid), nothing else.
 struct CellSinkProps {
-  static constexpr bool kMidOut = true, kUnroll = false;
+  static constexpr bool kMidOut = true, kUnroll = false, kSplitGas = CELL_GAS_SPLIT;
   const CellArgs& A;
   int64_t n, c;
   __device__ double& rec(int f) { return A.rec[(int64_t)f * n + c]; }
@@ -404,6 +407,102 @@ auto row = [&](const int r) {
   }
 }
 
+// gas phase (_kernels.py:254-328): density, molar mass, viscosity and
+// enthalpy of the gas with their partials
+struct GasPhase {
+  double rg, drg[NU], mgbar, dmg[NU], mug, dmug[NU], hg, dhg[NU], ug, dug[NU];
+};
+__device__ __forceinline__ void gas_phase(const Model& M, double p, double t, double t_ref,
+                                          const double (&yf)[NF], const DyFull& dyf,
+                                          GasPhase& G) {
+  double dzdw[NF], dz_p, dz_t;
+  const double z = z_factor_mix<NF>(yf, M.gasp, p, t, dzdw, dz_p, dz_t);
+  double dz[NU];
+#pragma unroll
+  for (int u = 0; u < NU; ++u) dz[u] = 0.0;
+  dz[0] = dz_p;
+  dz[CT] += dz_t;
+#pragma unroll
+  for (int a = 0; a < NF; ++a)
+    if (dzdw[a] != 0.0) {
+#pragma unroll
+      for (int u = 0; u < NU; ++u)
+        if (DyFull::nz(a, u)) dz[u] += dzdw[a] * dyf(a, u);
+    }
+  const double tr = t + RANKINE;
+  const double rg = p / (z * R_GAS * tr);
+  double drg[NU];
+#pragma unroll
+  for (int u = 0; u < NU; ++u) drg[u] = -rg * dz[u] / z;
+  drg[0] += rg / p;
+  drg[CT] -= rg / tr;
+  double mgbar = 0.0, dmg[NU];
+#pragma unroll
+  for (int u = 0; u < NU; ++u) dmg[u] = 0.0;
+#pragma unroll
+  for (int a = 0; a < NF; ++a) {
+    mgbar += yf[a] * M.gasp[a][G_M];
+#pragma unroll
+    for (int u = 0; u < NU; ++u)
+      if (DyFull::nz(a, u)) dmg[u] += M.gasp[a][G_M] * dyf(a, u);
+  }
+  double wsum = 0.0, musum = 0.0, dmusum_t = 0.0, sqm[NF], muc[NF];
+#pragma unroll
+  for (int a = 0; a < NF; ++a) {
+    sqm[a] = sqrt(M.gasp[a][G_M]);
+    double m_c, dm_c;
+    gas_component_viscosity(M.gasp[a][G_AVG], M.gasp[a][G_BVG], t, m_c, dm_c);
+    muc[a] = m_c;
+    wsum += yf[a] * sqm[a];
+    musum += yf[a] * m_c * sqm[a];
+    dmusum_t += yf[a] * dm_c * sqm[a];
+  }
+  double dmug[NU], mug;
+#pragma unroll
+  for (int u = 0; u < NU; ++u) dmug[u] = 0.0;
+  if (wsum > 1e-30) {
+    mug = musum / wsum;
+    dmug[CT] += dmusum_t / wsum;
+#pragma unroll
+    for (int a = 0; a < NF; ++a) {
+      double dmy = sqm[a] * (muc[a] - mug) / wsum;
+      if (dmy != 0.0) {
+#pragma unroll
+        for (int u = 0; u < NU; ++u)
+          if (DyFull::nz(a, u)) dmug[u] += dmy * dyf(a, u);
+      }
+    }
+  } else {
+    mug = 1.0;
+  }
+  double hg = 0.0, dhg[NU];
+#pragma unroll
+  for (int u = 0; u < NU; ++u) dhg[u] = 0.0;
+#pragma unroll
+  for (int a = 0; a < NF; ++a) {
+    double h_c, dh_c;
+    gas_enthalpy(M.gasp[a], t_ref, t, h_c, dh_c);
+    hg += yf[a] * h_c;
+    dhg[CT] += yf[a] * dh_c;
+    if (h_c != 0.0) {
+#pragma unroll
+      for (int u = 0; u < NU; ++u)
+        if (DyFull::nz(a, u)) dhg[u] += h_c * dyf(a, u);
+    }
+  }
+  const double ug = hg - p / rg;
+  double dug[NU];
+#pragma unroll
+  for (int u = 0; u < NU; ++u) dug[u] = dhg[u] + p * drg[u] / (rg * rg);
+  dug[0] -= 1.0 / rg;
+
+  G.rg = rg; G.mgbar = mgbar; G.mug = mug; G.hg = hg; G.ug = ug;
+#pragma unroll
+  for (int u = 0; u < NU; ++u) {
+    G.drg[u] = drg[u]; G.dmg[u] = dmg[u]; G.dmug[u] = dmug[u]; G.dhg[u] = dhg[u]; G.dug[u] = dug[u];
+  }
+}
+
 // cell_eval + compose for the cell at position c with unknowns u_
 // (_kernels.py:66-610, 797-825); inputs other than the unknowns from A.
 template <class S>
@@ -536,87 +635,15 @@ __device__ __forceinline__ void cell_eval(const Model& M, const CellArgs& A, int
     REC(R_DYO + 4 * i + 3) = dyf.o[i][3];
   }
 
-  // gas phase (_kernels.py:254-328)
-  double dzdw[NF], dz_p, dz_t;
-  const double z = z_factor_mix<NF>(yf, M.gasp, p, t, dzdw, dz_p, dz_t);
-  double dz[NU];
-#pragma unroll
-  for (int u = 0; u < NU; ++u) dz[u] = 0.0;
-  dz[0] = dz_p;
-  dz[CT] += dz_t;
-#pragma unroll
-  for (int a = 0; a < NF; ++a)
-    if (dzdw[a] != 0.0) {
-#pragma unroll
-      for (int u = 0; u < NU; ++u)
-        if (DyFull::nz(a, u)) dz[u] += dzdw[a] * dyf(a, u);
-    }
-  const double tr = t + RANKINE;
-  const double rg = p / (z * R_GAS * tr);
-  double drg[NU];
-#pragma unroll
-  for (int u = 0; u < NU; ++u) drg[u] = -rg * dz[u] / z;
-  drg[0] += rg / p;
-  drg[CT] -= rg / tr;
-  double mgbar = 0.0, dmg[NU];
-#pragma unroll
-  for (int u = 0; u < NU; ++u) dmg[u] = 0.0;
-#pragma unroll
-  for (int a = 0; a < NF; ++a) {
-    mgbar += yf[a] * M.gasp[a][G_M];
-#pragma unroll
-    for (int u = 0; u < NU; ++u)
-      if (DyFull::nz(a, u)) dmg[u] += M.gasp[a][G_M] * dyf(a, u);
-  }
-  double wsum = 0.0, musum = 0.0, dmusum_t = 0.0, sqm[NF], muc[NF];
-#pragma unroll
-  for (int a = 0; a < NF; ++a) {
-    sqm[a] = sqrt(M.gasp[a][G_M]);
-    double m_c, dm_c;
-    gas_component_viscosity(M.gasp[a][G_AVG], M.gasp[a][G_BVG], t, m_c, dm_c);
-    muc[a] = m_c;
-    wsum += yf[a] * sqm[a];
-    musum += yf[a] * m_c * sqm[a];
-    dmusum_t += yf[a] * dm_c * sqm[a];
-  }
-  double dmug[NU], mug;
-#pragma unroll
-  for (int u = 0; u < NU; ++u) dmug[u] = 0.0;
-  if (wsum > 1e-30) {
-    mug = musum / wsum;
-    dmug[CT] += dmusum_t / wsum;
-#pragma unroll
-    for (int a = 0; a < NF; ++a) {
-      double dmy = sqm[a] * (muc[a] - mug) / wsum;
-      if (dmy != 0.0) {
-#pragma unroll
-        for (int u = 0; u < NU; ++u)
-          if (DyFull::nz(a, u)) dmug[u] += dmy * dyf(a, u);
-      }
-    }
-  } else {
-    mug = 1.0;
-  }
-  double hg = 0.0, dhg[NU];
-#pragma unroll
-  for (int u = 0; u < NU; ++u) dhg[u] = 0.0;
-#pragma unroll
-  for (int a = 0; a < NF; ++a) {
-    double h_c, dh_c;
-    gas_enthalpy(M.gasp[a], t_ref, t, h_c, dh_c);
-    hg += yf[a] * h_c;
-    dhg[CT] += yf[a] * dh_c;
-    if (h_c != 0.0) {
-#pragma unroll
-      for (int u = 0; u < NU; ++u)
-        if (DyFull::nz(a, u)) dhg[u] += h_c * dyf(a, u);
-    }
-  }
-  const double ug = hg - p / rg;
-  double dug[NU];
-#pragma unroll
-  for (int u = 0; u < NU; ++u) dug[u] = dhg[u] + p * drg[u] / (rg * rg);
-  dug[0] -= 1.0 / rg;
+  // gas phase (_kernels.py:254-328); the split property pass leaves it to k_cell_gas
+  GasPhase G;
+  if constexpr (!S::kSplitGas) gas_phase(M, p, t, t_ref, yf, dyf, G);
+  const double rg = G.rg, mgbar = G.mgbar, mug = G.mug, hg = G.hg, ug = G.ug;
+  const double (&drg)[NU] = G.drg;
+  const double (&dmg)[NU] = G.dmg;
+  const double (&dmug)[NU] = G.dmug;
+  const double (&dhg)[NU] = G.dhg;
+  const double (&dug)[NU] = G.dug;
 
   // relperm + capillary pressure (_kernels.py:330-353)
   double krw, dkrw, krow, dkrow, pcow, dpcow, krg, dkrg, krog, dkrog, pcog, dpcog, s2[5];
@@ -648,9 +675,11 @@ __device__ __forceinline__ void cell_eval(const Model& M, const CellArgs& A, int
 #pragma unroll
   for (int i = 0; i < NCO; ++i)
     REC(R_DGAM1_X + i) = (dro_x[i] * mobar + ro * M.gasp[1 + i][G_M]) * PSI_PER_FT;
+  if constexpr (!S::kSplitGas) {
 #pragma unroll
-  for (int u = 0; u < NU; ++u) REC(R_DGAM2 + u) = (drg[u] * mgbar + rg * dmg[u]) * PSI_PER_FT;
-  REC(R_GAM + 2) = rg * mgbar * PSI_PER_FT;
+    for (int u = 0; u < NU; ++u) REC(R_DGAM2 + u) = (drg[u] * mgbar + rg * dmg[u]) * PSI_PER_FT;
+    REC(R_GAM + 2) = rg * mgbar * PSI_PER_FT;
+  }
 
   // phase pressures (_kernels.py:375-385)
   REC(R_POT + 0) = p - pcow;
@@ -690,6 +719,7 @@ __device__ __forceinline__ void cell_eval(const Model& M, const CellArgs& A, int
 #pragma unroll
     for (int i = 0; i < NCO; ++i) REC(R_DBETA1_X + i) = b1x[i];
   }
+  if constexpr (!S::kSplitGas) {
   {
     const bool on = krg > 0.0 || dkrg != 0.0;
 #pragma unroll
@@ -703,6 +733,7 @@ __device__ __forceinline__ void cell_eval(const Model& M, const CellArgs& A, int
     }
   }
   REC(R_BETA + 2) = rg * krg / mug;
+  }
 
   // phase enthalpies (_kernels.py:410-419)
   REC(R_HPH + 0) = hw;
@@ -711,9 +742,11 @@ __device__ __forceinline__ void cell_eval(const Model& M, const CellArgs& A, int
   REC(R_DHPH1_T) = dho_t;
 #pragma unroll
   for (int i = 0; i < NCO; ++i) REC(R_DHPH1_X + i) = hli[i];
-  REC(R_HPH + 2) = hg;
+  if constexpr (!S::kSplitGas) {
+    REC(R_HPH + 2) = hg;
 #pragma unroll
-  for (int u = 0; u < NU; ++u) REC(R_DHPH2 + u) = dhg[u];
+    for (int u = 0; u < NU; ++u) REC(R_DHPH2 + u) = dhg[u];
+  }
 
   // thermal conductivity (_kernels.py:421-428)
   {
@@ -734,15 +767,19 @@ __device__ __forceinline__ void cell_eval(const Model& M, const CellArgs& A, int
     s.mid(MI_RO, ro); s.mid(MI_DRO_P, dro_p); s.mid(MI_DRO_T, dro_t);
 #pragma unroll
     for (int i = 0; i < NCO; ++i) s.mid(MI_DRO_X + i, dro_x[i]);
-    s.mid(MI_RG, rg);
+    if constexpr (!S::kSplitGas) {
+      s.mid(MI_RG, rg);
 #pragma unroll
-    for (int u = 0; u < NU; ++u) s.mid(MI_DRG + u, drg[u]);
+      for (int u = 0; u < NU; ++u) s.mid(MI_DRG + u, drg[u]);
+    }
     s.mid(MI_RW, rw); s.mid(MI_DRW_P, drw_p); s.mid(MI_DRW_T, drw_t);
     s.mid(MI_UW, uw); s.mid(MI_DUW_P, duw_p); s.mid(MI_DUW_T, duw_t);
     s.mid(MI_UO, uo); s.mid(MI_DUO_P, duo_p); s.mid(MI_DUO_T, duo_t);
-    s.mid(MI_UG, ug);
+    if constexpr (!S::kSplitGas) {
+      s.mid(MI_UG, ug);
 #pragma unroll
-    for (int u = 0; u < NU; ++u) s.mid(MI_DUG + u, dug[u]);
+      for (int u = 0; u < NU; ++u) s.mid(MI_DUG + u, dug[u]);
+    }
   } else {
     CellMid m;
     m.v[MI_PHI] = phi; m.v[MI_DPHI_P] = dphi_p; m.v[MI_DPHI_T] = dphi_t;
@@ -783,7 +820,7 @@ __global__ void __launch_bounds__(128, CELL_MINB) k_cell(const Model M, const Ce
 // properties (record + A.mid) and then the reaction / accumulation rows
 // (cell_rows over the stored values). Same arithmetic, same results.
 #ifndef CELLP_MINB
-#define CELLP_MINB 8   // C4 sweep 4..12 (rows at 2): 8 best
+#define CELLP_MINB 7   // C4 sweep 4..12 (rows at 2): 8 best before the gas split, 6-7 after
 #endif
 #ifndef CELLR_MINB
 #define CELLR_MINB 2   // C4 sweep 1..6 (props at 8): 1-2 best (255 registers, 128 B spilled)
@@ -800,6 +837,65 @@ __global__ void __launch_bounds__(128, CELLP_MINB) k_cell_props(const Model M, c
   for (int u = 0; u < NU; ++u) u_[u] = A.st[u * n + c];
   CellSinkProps s{A, n, c};
   cell_eval(M, A, c, u_, s);
+}
+
+// the gas phase of the split cell pass: record fields of the gas and the
+// values the rows need (after k_cell_props: yfull / dyfull from the record)
+#ifndef CELLG_MINB
+#define CELLG_MINB 4   // C4 sweep 2..8: 4 best
+#endif
+__global__ void __launch_bounds__(128, CELLG_MINB) k_cell_gas(const Model M, const CellArgs A) {
+  const int64_t n = A.g.n;
+  const int64_t c = A.c_begin + (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (c >= A.c_end) return;
+  const double p = A.st[c], t = A.st[CT * n + c], sg = A.st[CSG * n + c];
+  double* rec = A.rec + c;
+  double yf[NF];
+#pragma unroll
+  for (int a = 0; a < NF; ++a) yf[a] = rec[(int64_t)(R_Y + a) * n];
+  DyFull dyf;
+  dyf.w[0] = rec[(int64_t)R_DY0_P * n];
+  dyf.w[1] = rec[(int64_t)R_DY0_T * n];
+  dyf.w[2] = rec[(int64_t)R_DY0_SW * n];
+#pragma unroll
+  for (int i = 0; i < NCO; ++i) {
+#pragma unroll
+    for (int q = 0; q < 4; ++q) dyf.o[i][q] = rec[(int64_t)(R_DYO + 4 * i + q) * n];
+    dyf.o[i][4] = i == M.heavy ? dyf.o[i][3] : 0.0;
+  }
+  GasPhase G;
+  gas_phase(M, p, t, M.rockp[RK_TREF], yf, dyf, G);
+  double krg, dkrg;
+  interp1(M.nslt, M.slt_s, M.slt_krg, sg, krg, dkrg);
+#define REC(f) rec[(int64_t)(f) * n]
+#pragma unroll
+  for (int u = 0; u < NU; ++u) REC(R_DGAM2 + u) = (G.drg[u] * G.mgbar + G.rg * G.dmg[u]) * PSI_PER_FT;
+  REC(R_GAM + 2) = G.rg * G.mgbar * PSI_PER_FT;
+  {
+    const bool on = krg > 0.0 || dkrg != 0.0;
+#pragma unroll
+    for (int u = 0; u < NU; ++u) {
+      double v = 0.0;
+      if (on) {
+        v = (G.drg[u] * krg - G.rg * krg * G.dmug[u] / G.mug) / G.mug;
+        if (u == CSG) v += G.rg * dkrg / G.mug;
+      }
+      REC(R_DBETA2 + u) = v;
+    }
+  }
+  REC(R_BETA + 2) = G.rg * krg / G.mug;
+  REC(R_HPH + 2) = G.hg;
+#pragma unroll
+  for (int u = 0; u < NU; ++u) REC(R_DHPH2 + u) = G.dhg[u];
+#undef REC
+  double* mid = A.mid + c;
+  mid[(int64_t)MI_RG * n] = G.rg;
+  mid[(int64_t)MI_UG * n] = G.ug;
+#pragma unroll
+  for (int u = 0; u < NU; ++u) {
+    mid[(int64_t)(MI_DRG + u) * n] = G.drg[u];
+    mid[(int64_t)(MI_DUG + u) * n] = G.dug[u];
+  }
 }
 
 __global__ void __launch_bounds__(128, CELLR_MINB) k_cell_rows(const Model M, const CellArgs A) {

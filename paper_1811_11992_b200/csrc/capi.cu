@@ -577,6 +577,10 @@ static void launch_cell(isc_ctx* ctx, CellArgs A, cudaStream_t st) {
   if (CELL_SPLIT) {
     A.mid = ctx->cmid;
     k_cell_props<<<blocks, 128, 0, st>>>(ctx->M, A);
+    if (CELL_GAS_SPLIT) {
+      k_cell_gas<<<blocks, 128, 0, st>>>(ctx->M, A);
+      ++ctx->launches;
+    }
     k_cell_rows<<<blocks, 128, 0, st>>>(ctx->M, A);
     ++ctx->launches;
   } else {
