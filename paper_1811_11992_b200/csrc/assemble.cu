@@ -1343,7 +1343,10 @@ __global__ void __launch_bounds__(32 * 3, FEVE_MINB) k_face_eval_energy(const Fa
 
 // grid (ceil(owned cells / 32)); block (32, ROW_OS). Owned planes only:
 // ghost rows (z-slabs) carry no equation.
-__global__ void __launch_bounds__(32 * ROW_OS) k_face_gather(const FaceArgs2 A2) {
+#ifndef FG_MINB
+#define FG_MINB 4   // C4 sweep 1..8: 4 (85 registers) best; without a minimum the compiler capped at 64
+#endif
+__global__ void __launch_bounds__(32 * ROW_OS, FG_MINB) k_face_gather(const FaceArgs2 A2) {
   const FaceArgs& F = A2.F;
   const int64_t n = F.g.n;
   const int64_t c = (int64_t)F.g.kw_lo * F.g.nxny + (int64_t)blockIdx.x * 32 + threadIdx.x;
