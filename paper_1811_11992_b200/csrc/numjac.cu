@@ -156,7 +156,10 @@ struct NumJacArgs {
 };
 
 // grid (ceil(n/32)), block (32, NU): threadIdx.y = unknown u
-__global__ void __launch_bounds__(32 * NU) k_numjac(const Model M, const NumJacArgs J) {
+#ifndef NJ_MINB
+#define NJ_MINB 3   // C4 FD Jacobian: 30.3 / 27.6 / 22.9 / 23.3 ms at 1..4
+#endif
+__global__ void __launch_bounds__(32 * NU, NJ_MINB) k_numjac(const Model M, const NumJacArgs J) {
   const Dims& g = J.A.g;
   const int64_t n = g.n;
   const int64_t c = (int64_t)blockIdx.x * 32 + threadIdx.x;
