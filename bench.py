@@ -197,11 +197,13 @@ def algorithmic_bytes(grid, nw, precond="ras", form="explicit"):
         out["mc_factor"] = 8 * (162 * m + 40.5 * n)
         if form == "compact":
             # compact operator (csrc/compact.cu)
-            # red pass y_r = B_rb z_b: 54 per red block, z_b gathered (9 n/2),
-            # y written (6 n/2); black pass v_b = z_b - D_b^-1[:, :6] B'_br y: 36
+            # red pass y_r = B_rb z_b: 54 per red block of which 49 are loaded (the
+            # component rows' coke column is structurally zero and skipped while
+            # the assembly saw no nonzero there), z_b gathered (9 n/2), y written
+            # (6 n/2); black pass v_b = z_b - D_b^-1[:, :6] B'_br y: 36
             # per black block, D_b^-1[:, :6] (54 n/2), y gathered (6 n/2), z_b,
             # v_b and the dot operand (3 x 9 n/2)
-            out["ilu_apply"] = 8 * (54 * m + 7.5 * n)
+            out["ilu_apply"] = 8 * (49 * m + 7.5 * n)
             out["spmv"] = 8 * (36 * m + 43.5 * n)
             # k_rhs_schur (resid in, rhs out) + k_decouple_compact (diag and rhs
             # in, D^-1[:, :6] and rhs out)

@@ -941,6 +941,7 @@ struct FaceArgs {
   double* __restrict__ resid;
   double* __restrict__ diag;
   double* __restrict__ offd;
+  int* ccnz;   // set to 1 when a flux row < ROW_E gets a nonzero coke-column entry
 };
 
 // dense 9-vectors of a cell's record partials
@@ -1274,6 +1275,9 @@ __device__ __forceinline__ void face_eval_row(const FaceArgs2& A2, int64_t c, in
     orow_a[(int64_t)u * n] = dfb[u];
     orow_b[(int64_t)u * n] = -dfa[u];
   }
+  // the component rows' coke column is zero for an assembled system (no
+  // flux term depends on C_c); k_cc_red skips its loads while none is set
+  if (ROW < ROW_E && (dfa[CCC] != 0.0 || dfb[CCC] != 0.0)) *F.ccnz = 1;
   A2.fbuf[(int64_t)(axis * ROW_OS + ROW) * n + c] = flux;
 }
 

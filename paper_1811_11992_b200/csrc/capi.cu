@@ -116,6 +116,7 @@ struct isc_ctx {
   int64_t npartial = 0;
   int* flags = nullptr;
   int* fail_d = nullptr;
+  int* ccnz_d = nullptr;   // != 0: a flux row < ROW_E has a coke column entry (k_cc_red reads it)
   // ILU
   IluDev ilu{};
   int64_t* lvl_ptr_d = nullptr;
@@ -469,6 +470,8 @@ extern "C" int isc_create(const isc_model_desc* md, const isc_grid_desc* gdsc, i
   ALLOC(ctx->partial, ctx->npartial * 8);
   ALLOC(ctx->flags, n * 4);
   ALLOC(ctx->fail_d, 4);
+  ALLOC(ctx->ccnz_d, 4);
+  CK(cudaMemset(ctx->ccnz_d, 0xff, 4));
   if (precond == ISC_PRECOND_BJACOBI || precond == ISC_PRECOND_RAS) {
     int s = build_ilu(ctx);
     if (s) return s;
@@ -487,7 +490,7 @@ extern "C" int isc_destroy(isc_ctx* ctx) {
                   ctx->capped_d, ctx->rec, ctx->acc, ctx->src, ctx->resid, ctx->diag,
                   ctx->offd, ctx->upw, ctx->bad_d, ctx->rhs, ctx->xk, ctx->rk, ctx->rhat,
                   ctx->pk, ctx->vk, ctx->phat, ctx->shat, ctx->sk, ctx->tk, ctx->sc,
-                  ctx->partial, ctx->partial2, ctx->fbuf, ctx->flags, ctx->fail_d, ctx->schur, ctx->st_c, ctx->accn_c, ctx->stage,
+                  ctx->partial, ctx->partial2, ctx->fbuf, ctx->flags, ctx->fail_d, ctx->ccnz_d, ctx->schur, ctx->st_c, ctx->accn_c, ctx->stage,
                   ctx->halo_send_lo, ctx->halo_send_hi, ctx->halo_recv_lo, ctx->halo_recv_hi,
                   ctx->gm_V, ctx->gm_h, ctx->cbp, ctx->cmid};
   if (ctx->comm.nccl && nccl_api().CommDestroy) nccl_api().CommDestroy(ctx->comm.nccl);
@@ -638,7 +641,7 @@ extern "C" int isc_assemble(isc_ctx* ctx, const double* d_state, const double* h
     }
   }
   FaceArgs F{ctx->g, d_state, ctx->rec, ctx->depth, ctx->gd, ctx->td, ctx->upw, freeze,
-             ctx->resid, ctx->diag, ctx->offd};
+             ctx->resid, ctx->diag, ctx->offd, ctx->ccnz_d};
 #ifndef FACE_CENTRIC
 #define FACE_CENTRIC 1
 #endif
@@ -646,12 +649,15 @@ extern "C" int isc_assemble(isc_ctx* ctx, const double* d_state, const double* h
     KScope ks(ctx, KT_FACE);
     if (FACE_CENTRIC) {
       FaceArgs2 F2{F, ctx->fbuf};
-      if (!face_pre)
+      if (!face_pre) {
+        CK(cudaMemsetAsync(ctx->ccnz_d, 0, 4, st));   // set by k_face_eval* on a nonzero
         launch_face_eval(F2, 0, n, 0, 3, st);
+      }
       k_face_gather<<<grid1d((int64_t)(ctx->g.kw_hi - ctx->g.kw_lo) * ctx->g.nxny, 32),
                       dim3(32, ROW_OS), 0, st>>>(F2);
       ++ctx->launches;
     } else {
+      CK(cudaMemsetAsync(ctx->ccnz_d, 0xff, 4, st));   // two-sided kernel: not tracked
       k_face<<<grid1d(n, 32), dim3(32, NU), 0, st>>>(F);
     }
   }
@@ -776,7 +782,8 @@ extern "C" int isc_assemble_decoupled(isc_ctx* ctx, const double* d_state, const
   {
     KScope ks(ctx, KT_FACE);
     FaceArgs F{ctx->g, d_state, ctx->rec, ctx->depth, ctx->gd, ctx->td, ctx->upw, freeze,
-               ctx->resid, ctx->diag, ctx->offd};
+               ctx->resid, ctx->diag, ctx->offd, ctx->ccnz_d};
+    CK(cudaMemsetAsync(ctx->ccnz_d, 0xff, 4, st));   // decoupled (dense) blocks
     FusedArgs P{F, ctx->resid, ctx->rhs, ctx->nw, ctx->wcell_d, ctx->schur, ctx->flags,
                 ctx->bad_d};
     CK(cudaFuncSetAttribute(k_face_dc, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -831,8 +838,9 @@ extern "C" int isc_assemble_host(isc_ctx* ctx, const double* h_p, const double* 
              ctx->hl_rho, ctx->hl_tini, ctx->accn_c, dt, ctx->rec, ctx->acc, ctx->src,
              ctx->resid, ctx->diag, ctx->bad_d, 0, n};
   FaceArgs F{g, ctx->st_c, ctx->rec, ctx->depth, ctx->gd, ctx->td, ctx->upw, freeze,
-             ctx->resid, ctx->diag, ctx->offd};
+             ctx->resid, ctx->diag, ctx->offd, ctx->ccnz_d};
   FaceArgs2 F2{F, ctx->fbuf};
+  if (pipe && FACE_CENTRIC) CK(cudaMemsetAsync(ctx->ccnz_d, 0, 4, st));
   for (int q = 0; q < nq; ++q) {
     const int64_t k0 = (int64_t)g.nz * q / nq, k1 = (int64_t)g.nz * (q + 1) / nq;
     const int64_t c0 = k0 * g.nxny, c1 = k1 * g.nxny, cnt = c1 - c0;
@@ -929,6 +937,7 @@ extern "C" int isc_export_system(isc_ctx* ctx, double* d_diag, double* d_offd, d
 
 extern "C" int isc_import_system(isc_ctx* ctx, const double* d_diag, const double* d_offd,
                                  const double* d_resid, const double* h_wells_out) {
+  CK(cudaMemsetAsync(ctx->ccnz_d, 0xff, 4, ctx->stream));   // imported blocks: full rows
   k_import_system<<<grid1d(ctx->g.n, 128), 128, 0, ctx->stream>>>(
       ctx->g, ctx->conn_id, d_diag, d_offd, d_resid, ctx->diag, ctx->offd, ctx->resid);
   LAUNCH_CHECK();
@@ -1695,7 +1704,7 @@ static void sc_rhs_launch(isc_ctx* ctx, const Dims& g, int blocks, const double*
 }
 static void sc_red_launch(isc_ctx* ctx, const Dims& g, int blocks, double* z) {
   if (ctx->compact)
-    k_cc_red<<<blocks, dim3(32, CR), 0, ctx->stream>>>(g, ctx->offd, z);
+    k_cc_red<<<blocks, dim3(32, CR), 0, ctx->stream>>>(g, ctx->offd, ctx->ccnz_d, z);
   else
     k_sc_red<<<blocks, dim3(32, NU), 0, ctx->stream>>>(g, ctx->offd, z);
 }

@@ -244,12 +244,18 @@ __global__ void __launch_bounds__(32 * CR, CP_MINB) k_cc_spmv(CP_ARGS) {
 #ifndef CC_MINB
 #define CC_MINB 6   // C4 sweep 3..6: 0.402/0.420 -> 0.396/0.407 ms (red/black) at 6
 #endif
+// ccnz: 0 while every component row (< ROW_E) of the blocks has a zero coke
+// column (the face evaluation clears it per assembly and sets it on a
+// nonzero; imports and other writers set it) -- those 5 of the 54 row values
+// are then not loaded (adding their zero products changes no bit).
 __global__ void __launch_bounds__(32 * CR, CC_MINB) k_cc_red(Dims g, const double* __restrict__ offd,
+                                                             const int* __restrict__ ccnz,
                                                              double* __restrict__ z) {
   const int64_t n = g.n;
   const int ls = threadIdx.x, r = threadIdx.y;
   const int64_t t = g.tw_lo + (int64_t)blockIdx.x * 32 + ls;
   if (t >= g.tw_hi) return;
+  const bool skip_cc = r < ROW_E && *ccnz == 0;   // warp-uniform (one row per warp)
   const int64_t c = colour_pos(g, 0, t);
   int i, j, k;
   const int64_t cell = locate(g, c, i, j, k);
@@ -261,7 +267,10 @@ __global__ void __launch_bounds__(32 * CR, CC_MINB) k_cc_red(Dims g, const doubl
     const double* blk = offd + (int64_t)((d * NU + r) * NU) * n + c;
     double tt = 0.0;
 #pragma unroll
-    for (int u = 0; u < NU; ++u) tt += blk[(int64_t)u * n] * z[(int64_t)u * n + nb];
+    for (int u = 0; u < NU; ++u) {
+      if (u == CCC && skip_cc) continue;
+      tt += blk[(int64_t)u * n] * z[(int64_t)u * n + nb];
+    }
     s += tt;
   }
   z[(int64_t)r * n + c] = s;

@@ -481,6 +481,36 @@ def test_mcilu_solve_synthetic_and_error_paths(nx):
         BlockSolver(grid, ws, tol=1e-14, maxiter=1, precond="mcilu").solve([])
 
 
+def test_mcilu_compact_imported_coke_column():
+    """An imported system with flux-only off-diagonal rows takes the compact
+    form, and a nonzero coke column in its component rows (which an assembled
+    system never has, so k_cc_red skips it after an assembly) is still applied:
+    du matches a dense solve."""
+    from paper_1811_11992_b200.grid import build_grid
+    from paper_1811_11992_b200.synth import synth_system
+    from paper_1811_11992_b200.model import load_pack
+    grid = build_grid(6, 4, 4, 1.0, 1.0, 1.0, 1.0, 1.0, 1.0, 0.3)
+    pack = load_pack("tube3_pack", grid.phi_ref)
+    diag, offd, resid = synth_system(grid, 9, seed=11)
+    offd = offd.copy()
+    offd[:, :, 6:, :] = 0.0           # constraint / coke rows carry no flux
+    offd[:, :, :5, 8] = 0.05          # but a coke column in the component rows
+    ws = Workspace(grid, pack, None, wells=(), streams=(), precond="mcilu")
+    load_system(ws, diag, offd, resid)
+    du, _, it = BlockSolver(grid, ws, tol=1e-12, maxiter=500, precond="mcilu").solve([])
+    assert ws.ctx.decoupled_form == "compact"
+    n = grid.ncell
+    A = np.zeros((9 * n, 9 * n))
+    for c in range(n):
+        A[9 * c:9 * c + 9, 9 * c:9 * c + 9] = diag[c]
+    for ic in range(grid.nconn):
+        a, b = int(grid.conn_a[ic]), int(grid.conn_b[ic])
+        A[9 * a:9 * a + 9, 9 * b:9 * b + 9] = offd[ic, 0]
+        A[9 * b:9 * b + 9, 9 * a:9 * a + 9] = offd[ic, 1]
+    ref = np.linalg.solve(A, -resid.reshape(-1)).reshape(n, 9)
+    assert np.linalg.norm(du - ref) <= 1e-9 * np.linalg.norm(ref), it
+
+
 @pytest.mark.parametrize("restart", [30, 4])   # 4: several restarts (true-residual path)
 def test_gmres_solve_synthetic_and_error_paths(restart):
     """Optional GMRES(m) on the red-eliminated system (capi.cu gmres_schur):
