@@ -1359,6 +1359,9 @@ __global__ void __launch_bounds__(32 * ROW_OS, FG_MINB) k_face_gather(const Face
   int i, j, k;
   const int64_t cell = locate(F.g, c, i, j, k);
   double res = F.resid[row * n + c];
+  // the face evaluation of this assembly found the component rows' coke
+  // column zero: those back-block loads are skipped (warp-uniform)
+  const bool skip_cc = row < ROW_E && *F.ccnz == 0;
   double drow[NU];
 #pragma unroll
   for (int u = 0; u < NU; ++u) drow[u] = F.diag[(int64_t)(row * NU + u) * n + c];
@@ -1373,7 +1376,10 @@ __global__ void __launch_bounds__(32 * ROW_OS, FG_MINB) k_face_gather(const Face
     else res -= flux;
     const double* back = F.offd + (int64_t)((opposite(d) * NU + row) * NU) * n + nb;
 #pragma unroll
-    for (int u = 0; u < NU; ++u) drow[u] += -back[(int64_t)u * n];
+    for (int u = 0; u < NU; ++u) {
+      if (u == CCC && skip_cc) continue;
+      drow[u] += -back[(int64_t)u * n];
+    }
   }
   F.resid[row * n + c] = res;
 #pragma unroll
