@@ -1065,8 +1065,15 @@ extern "C" int isc_decouple(isc_ctx* ctx, int64_t* bad_cell, int32_t* bad_col) {
   }
   if (ctx->compact) {
     const int64_t owned = (int64_t)(ctx->g.kw_hi - ctx->g.kw_lo) * ctx->g.nxny;
-    k_decouple_compact<<<grid1d(owned, 32), dim3(32, NU), 0, st>>>(ctx->g, ctx->diag, ctx->rhs,
-                                                                  ctx->flags, ctx->bad_d);
+#ifndef DCC_THREAD
+#define DCC_THREAD 1   // thread per cell (k_decouple_compact_t); 0: thread per column
+#endif
+    if (DCC_THREAD)
+      k_decouple_compact_t<<<grid1d(owned, DCT_THREADS), DCT_THREADS, 0, st>>>(
+          ctx->g, ctx->diag, ctx->rhs, ctx->flags, ctx->bad_d);
+    else
+      k_decouple_compact<<<grid1d(owned, 32), dim3(32, NU), 0, st>>>(ctx->g, ctx->diag, ctx->rhs,
+                                                                    ctx->flags, ctx->bad_d);
   } else if (DECOUPLE_WS) {
     // once per process (thread-safe static init: hub ranks share the process)
     static const cudaError_t attr = cudaFuncSetAttribute(

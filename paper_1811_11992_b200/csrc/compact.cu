@@ -134,6 +134,128 @@ __global__ void __launch_bounds__(32 * NU, DCC_MINB) k_decouple_compact(Dims g, 
   rhs[(int64_t)u * n + c] = gh ? 0.0 : s;
 }
 
+// The same inversion with one thread per cell, the block held in registers
+// (in-place Gauss-Jordan: once column k is eliminated its slot holds column
+// perm[k] of the inverse, where perm tracks the row interchanges). Same
+// pivot rule, tolerance, scaling by the reciprocal and elimination order as
+// k_decouple_compact, so the same values; no shared memory and no barriers
+// (the column-per-thread form is barrier- and issue-bound).
+#ifndef DCT_THREADS
+#define DCT_THREADS 128
+#endif
+// opaque selects: a plain `q == piv ? x : y` chain over an unrolled register
+// array is folded back into a dynamically indexed (local-memory) array
+__device__ __forceinline__ double sel_d(bool p, double x, double y) {
+  double r;
+  asm("{\n\t.reg .pred q;\n\tsetp.ne.u32 q, %3, 0;\n\tselp.f64 %0, %1, %2, q;\n\t}"
+      : "=d"(r) : "d"(x), "d"(y), "r"((unsigned)p));
+  return r;
+}
+__device__ __forceinline__ int sel_i(bool p, int x, int y) {
+  int r;
+  asm("{\n\t.reg .pred q;\n\tsetp.ne.u32 q, %3, 0;\n\tselp.b32 %0, %1, %2, q;\n\t}"
+      : "=r"(r) : "r"(x), "r"(y), "r"((unsigned)p));
+  return r;
+}
+__global__ void __launch_bounds__(DCT_THREADS) k_decouple_compact_t(Dims g, double* diag,
+                                                                   double* rhs, int* flags,
+                                                                   unsigned long long* bad) {
+  const int64_t n = g.n;
+  const int64_t p0 = (int64_t)g.kw_lo * g.nxny, p1 = (int64_t)g.kw_hi * g.nxny;
+  const int64_t c = p0 + (int64_t)blockIdx.x * DCT_THREADS + threadIdx.x;
+  if (c >= p1) return;
+  double a[NU][NU];   // a[r][j]: row r, slot j
+  double amax = 0.0;
+#pragma unroll
+  for (int r = 0; r < NU; ++r)
+#pragma unroll
+    for (int j = 0; j < NU; ++j) {
+      a[r][j] = diag[(int64_t)(r * NU + j) * n + c];
+      amax = fmax(amax, fabs(a[r][j]));
+    }
+  const double tol = 1e-13 * amax;
+  int perm[NU];
+#pragma unroll
+  for (int r = 0; r < NU; ++r) perm[r] = r;
+  int failc = NU;
+#pragma unroll
+  for (int k = 0; k < NU; ++k) {
+    int piv = k;
+    double pv = fabs(a[k][k]);
+#pragma unroll
+    for (int r = k + 1; r < NU; ++r) {
+      const double v = fabs(a[r][k]);
+      if (v > pv) { pv = v; piv = r; }
+    }
+    if (pv <= tol || amax == 0.0) failc = amax == 0.0 ? 0 : min(failc, k);
+#pragma unroll
+    for (int q = k + 1; q < NU; ++q) {
+      const bool sw = q == piv;
+#pragma unroll
+      for (int j = 0; j < NU; ++j) {
+        const double t = a[k][j];
+        a[k][j] = sel_d(sw, a[q][j], t);
+        a[q][j] = sel_d(sw, t, a[q][j]);
+      }
+      const int t = perm[k];
+      perm[k] = sel_i(sw, perm[q], t);
+      perm[q] = sel_i(sw, t, perm[q]);
+    }
+    const double dv = 1.0 / a[k][k];
+    // row k: the pivot slot becomes column perm[k] of the inverse (1 * dv)
+#pragma unroll
+    for (int j = 0; j < NU; ++j) a[k][j] = (j == k ? 1.0 : a[k][j]) * dv;
+#pragma unroll
+    for (int r = 0; r < NU; ++r) {
+      if (r == k) continue;
+      const double f = a[r][k];
+      if (f != 0.0) {
+#pragma unroll
+        for (int j = 0; j < NU; ++j) a[r][j] = (j == k ? 0.0 : a[r][j]) - f * a[k][j];
+      }
+    }
+  }
+  const bool gh = !owned_k(g, plane_of(g, c));
+  if (!gh && failc < NU) {
+    const int64_t cell = cell_of(g, c);
+    flags[cell] = failc + 1;
+    atomicMin(bad, (unsigned long long)cell);
+  }
+  // D^-1[:, :CR] over the diagonal block: slot j is inverse column perm[j]
+#pragma unroll
+  for (int j = 0; j < NU; ++j) {
+    const int col = perm[j];
+    if (col < CR) {
+#pragma unroll
+      for (int r = 0; r < NU; ++r) diag[(int64_t)(r * CR + col) * n + c] = a[r][j];
+    }
+  }
+  // rhs row u: sequential k sum as the reference's _mv (slot of inverse
+  // column k: iperm[k])
+  double rv[NU];
+  int iperm[NU];
+#pragma unroll
+  for (int k = 0; k < NU; ++k) {
+    rv[k] = rhs[(int64_t)k * n + c];
+    int jk = 0;
+#pragma unroll
+    for (int j = 1; j < NU; ++j) jk = perm[j] == k ? j : jk;
+    iperm[k] = jk;
+  }
+#pragma unroll
+  for (int u = 0; u < NU; ++u) {
+    double s = 0.0;
+#pragma unroll
+    for (int k = 0; k < NU; ++k) {
+      double x = a[u][0];
+#pragma unroll
+      for (int j = 1; j < NU; ++j) x = sel_d(iperm[k] == j, a[u][j], x);
+      s += x * rv[k];
+    }
+    rhs[(int64_t)u * n + c] = gh ? 0.0 : s;
+  }
+}
+
 // One half pass of the compact operator over the owned cells of one colour
 // (thread (cell lane, flux row r < CR), then output rows q = y, y + CR):
 //   out_q = base_q + SIGN * sum_r dinv[q][r] * (sum_d B_d[r, :] src(nb))
