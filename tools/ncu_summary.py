@@ -15,7 +15,7 @@ from collections import defaultdict
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 KERNELS = ["k_cc_red", "k_cc_black", "k_sc_update_p", "k_sc_update_s", "k_sc_update_xr",
-           "k_face_eval_light", "k_face_eval_energy", "k_face_gather", "k_decouple_compact",
+           "k_face_eval_light", "k_face_eval_energy", "k_face_gather", "k_decouple_compact_t", "k_decouple_compact",
            "k_cell_props", "k_cell_gas", "k_cell_rows", "k_mc_factor_compact",
            # one-kernel variants (CELL_SPLIT=0 / FACE_SPLIT=0, earlier captures)
            "k_face_eval", "k_cell",
@@ -116,7 +116,7 @@ def main(tag):
             lines.append(f"| {name} | {cnt[name]} | {v:.2f} | {v / s:.3f} |")
     for cls, names in (("red_pass", ("k_cc_red", "k_sc_red")),
                        ("black_pass", ("k_cc_black", "k_mc_black_spmv")),
-                       ("decouple", ("k_decouple_compact", "k_decouple_ws"))):
+                       ("decouple", ("k_decouple_compact_t", "k_decouple_compact", "k_decouple_ws"))):
         for k in names:
             if k in traffic:
                 traffic[cls] = {"dram_bytes": traffic[k]["dram_bytes"], "kernels": [k]}
