@@ -5,19 +5,31 @@
 Workload (BASELINE configs[3], the 2 M-cell case the north star quotes its
 roofline bar on): C4 = 200x200x50 grid, seeded log-normal permeability and
 uniform porosity, 4 air injectors + 4 producers, deck-default solver
-(LINEAR_TOL 1e-5, LINEAR_MAX 200). One *step* = one full Newton iteration
-of the first timestep (dt = 2e-3 d): assemble (cell + face + wells), well
-Schur fold + Gauss-Jordan decoupling, block-ILU(0) factorisation and the
-preconditioned BiCGSTAB solve, then the damped update. The preconditioner
-is the north star's multicolour block-ILU(0) (--precond mcilu, default);
-the reference's own RAS subdomain block-ILU(0) is measured on the same
-workload and reported under "ras_exact". ``value`` = cells x steps / device time (inputs resident in HBM);
-``e2e`` = the same through the drop-in API (assemble/BlockSolver.solve) with
-the state and accumulation copied from pinned host memory and du read back
-every step. The system (9 GB) is far larger than L2, so no flush is needed.
+(LINEAR_TOL 1e-5, LINEAR_MAX 200). One *step* = one solving Newton iteration
+of the C4 run's first timestep (dt = 2e-3 d), taken in the order the run
+takes them: step j runs iteration (j mod 5) + 1 of that timestep, and every
+5th step starts again from the initial state (the reference's C4 first
+timestep is 6 residual evaluations / 5 solves, traj_c4_sample.npz; the
+sixth evaluation only confirms convergence). So every timed iteration
+solves a real Newton correction — from the large first residual down to the
+last correction before convergence — instead of re-solving a converged
+state. An iteration = newton.py:275-309's loop body: assemble (cell + face
++ wells; upwinding frozen after iteration 5), scaled norm, capped-injector
+check, well Schur fold + Gauss-Jordan decoupling, preconditioner setup,
+preconditioned BiCGSTAB to LINEAR_TOL, damped update. The preconditioner is
+the north star's multicolour block-ILU(0) (--precond mcilu, default); the
+reference's own RAS subdomain block-ILU(0) is measured on the same workload
+and reported under "ras_exact". ``value`` = cells x steps / device time
+(inputs resident in HBM); ``e2e`` = the same iterations through the drop-in
+API (assemble/BlockSolver.solve) with each iteration's state and the
+accumulation copied from pinned host memory and du read back every step.
+The system (9 GB) is far larger than L2, so no flush is needed.
 
 ``--impl reference`` times the reference algorithm's CPU implementation (the
-plain-C/numpy oracle port, all host threads) on a bounded C4 sample.
+plain-C/numpy oracle port of the reference's RAS block-ILU(0) BiCGSTAB, all
+host threads: OpenMP in the cell/face/decoupling loops the reference runs
+with prange, its independent RAS subdomains factored and applied on a thread
+pool) on the same workload: the full C4 grid, the same iteration cycle.
 Multi-GPU (torchrun): the C4 grid is z-slab decomposed over the ranks
 (strong scaling; NCCL halo per half pass and all-reduced Krylov scalars; the
 multicolour preconditioner includes the cross-rank terms, so BiCGSTAB takes
@@ -42,6 +54,42 @@ sys.path.insert(0, ROOT)
 METRIC = "cell·Newton-iters/sec (assemble+decouple+solve)"
 UNIT = "cell-iters/s"
 KCLASS = ["cell", "face", "wells", "decouple", "ilu_factor", "ilu_apply", "spmv", "other"]
+# solving Newton iterations of the C4 first timestep (the reference's run:
+# 6 residual evaluations, 5 solves, 22 BiCGSTAB iterations with its RAS at
+# LINEAR_TOL 1e-5 — tests/golden/traj_c4_sample.npz)
+CYCLE = 5
+REF_STEP1 = {"newton": 6, "solves": 5, "bicgstab_iters": 22, "precond": "ras"}
+
+
+def workload(cfg_name, case):
+    dt = case.schedule.dt_init
+    return {"workload": f"{cfg_name.upper()} {case.nx}x{case.ny}x{case.nz} ({case.ncell} cells, "
+                        f"{len(case.wells)} wells): the {CYCLE} solving Newton iterations of the "
+                        f"first timestep (dt={dt} d) in run order, restarting from the initial "
+                        f"state every {CYCLE} steps; iteration = assemble + scaled norm + "
+                        f"decouple + precond setup + BiCGSTAB to LINEAR_TOL + damped update",
+            "linear_tol": case.solver.linear_tol,
+            "l2": "inputs larger than L2 (system ~9 GB), no flush"}
+
+
+class NewtonCycle:
+    """Bench step j = solving Newton iteration (j mod CYCLE) + 1 of the first
+    timestep, restarting from the initial state every CYCLE steps."""
+
+    def __init__(self, sim, dt):
+        self.sim, self.dt, self.j = sim, dt, 0
+        self.init = sim.state.copy()
+        self.work = sim.state.copy()
+        self.capped = sim.capped.copy()
+
+    def step(self):
+        it = self.j % CYCLE + 1
+        if it == 1:
+            self.work.u.copy_(self.init.u)
+            self.work.bhp = self.init.bhp.copy()
+            self.capped = self.sim.capped.copy()
+        self.j += 1
+        return self.sim.newton_iteration(self.work, self.dt, self.dt, self.capped, it)[1]
 
 
 def parse():
@@ -219,22 +267,22 @@ def algorithmic_bytes(grid, nw, precond="ras", form="explicit"):
 # ------------------------------------------------------------------ ours
 
 def measure_device(case, steps, warmup, world):
-    """Device-resident Newton iterations of `case` -> (ms, iters, sim)."""
+    """Device-resident Newton-cycle steps of `case` -> (ms, iters, sim)."""
     import torch
     from paper_1811_11992_b200 import configs
     from paper_1811_11992_b200.newton import Simulator
     grid, pack, wells, streams, state = configs.build_case(case)
     sim = Simulator(grid, pack, wells, streams, state, case.schedule, case.solver)
-    dt = case.schedule.dt_init
-    work, capped = sim.state.copy(), sim.capped.copy()
+    cyc = NewtonCycle(sim, case.schedule.dt_init)
     for _ in range(warmup):
-        sim.newton_iteration(work, dt, dt, capped, False)
+        cyc.step()
+    cyc.j = 0
     torch.cuda.synchronize()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     its = []
     e0.record()
     for _ in range(steps):
-        its.append(sim.newton_iteration(work, dt, dt, capped, False))
+        its.append(cyc.step())
     e1.record()
     torch.cuda.synchronize()
     return e0.elapsed_time(e1), float(np.mean(its)), sim
@@ -280,8 +328,7 @@ def run_ours(args, rank, world, local):
     n = grid.ncell
     ctx = sim.ctx
     dt = case.schedule.dt_init
-    work = sim.state.copy()
-    capped = sim.capped.copy()
+    cyc = NewtonCycle(sim, dt)
 
     def barrier():
         if world > 1:
@@ -289,8 +336,19 @@ def run_ours(args, rank, world, local):
             dist.barrier()
         torch.cuda.synchronize()
 
+    # one pass over the cycle, untimed: the iterates (for the e2e leg) and the
+    # per-iteration Krylov counts; then the warm-up steps
+    host_states, host_u, cycle_iters = [], [], []
+    for _ in range(CYCLE):
+        cur = cyc.work if cyc.j % CYCLE else cyc.init
+        if world == 1:
+            host_states.append(cur.to_host())
+        else:
+            host_u.append((cur.u.cpu().pin_memory(), cur.bhp.copy()))
+        cycle_iters.append(cyc.step())
     for _ in range(args.warmup):
-        sim.newton_iteration(work, dt, dt, capped, False)
+        cyc.step()
+    cyc.j = 0
     barrier()
     clocks = ClockSampler(local)
     clocks.start()
@@ -304,7 +362,7 @@ def run_ours(args, rank, world, local):
     barrier()
     ev0.record()
     for _ in range(args.steps):
-        its.append(sim.newton_iteration(work, dt, dt, capped, False))
+        its.append(cyc.step())
     ev1.record()
     barrier()
     dev_ms = ev0.elapsed_time(ev1)
@@ -319,73 +377,80 @@ def run_ours(args, rank, world, local):
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         dev_ms = float(t.item())
 
-    e2e_steps = max(1, min(args.steps, 5))
+    e2e_steps = max(CYCLE, min(args.steps, 2 * CYCLE))
     if world == 1:
         # ---- e2e through the drop-in API with host buffers ---------------
+        # the same iterations: iterate j's host State (pinned) and the host
+        # accumulation go in, du comes back to the host every step
         ws = Workspace(grid, pack, None, wells=wells, streams=streams,
                        precond=case.solver.precond)
         solver = BlockSolver(grid, ws, tol=case.solver.linear_tol,
                              maxiter=case.solver.linear_max, precond=case.solver.precond)
-        host = work.to_host()
-        st_pin = {k: torch.from_numpy(np.ascontiguousarray(v)).pin_memory().numpy()
-                  for k, v in host.items()}
         from types import SimpleNamespace
-        hstate = SimpleNamespace(**st_pin)
+        hstates = [SimpleNamespace(**{k: torch.from_numpy(np.ascontiguousarray(v)).pin_memory()
+                                      .numpy() for k, v in hs.items()}) for hs in host_states]
         accn_h = torch.from_numpy(
             np.ascontiguousarray(sim.accn.t().cpu().numpy())).pin_memory().numpy()
-        bi = sum(a.nbytes for a in st_pin.values()) + accn_h.nbytes
-        for _ in range(max(1, min(args.warmup, 2))):
-            blocks = assemble(grid, pack, ws, wells, streams, hstate, accn_h, dt, dt, capped)
-            du, dbhp, _ = solver.solve(blocks)
+        bi = (sum(a.nbytes for a in vars(hstates[0]).values()) + accn_h.nbytes)
+        capped = sim.capped.copy()
+
+        def e2e_step(j):
+            it = j % CYCLE + 1
+            blocks = assemble(grid, pack, ws, wells, streams, hstates[it - 1], accn_h, dt, dt,
+                              capped, freeze_upwind=it > 5)
+            return solver.solve(blocks)
+
+        for j in range(CYCLE):
+            du, dbhp, _ = e2e_step(j)
         barrier()
         t0 = time.perf_counter()
-        for _ in range(e2e_steps):
-            blocks = assemble(grid, pack, ws, wells, streams, hstate, accn_h, dt, dt, capped)
-            du, dbhp, _ = solver.solve(blocks)
+        for j in range(e2e_steps):
+            du, dbhp, _ = e2e_step(j)
         barrier()
         e2e_s = time.perf_counter() - t0
         bo = du.nbytes + dbhp.nbytes
-        path = "assembly.assemble(host State, host accn) + linsolve.BlockSolver.solve -> host du"
+        path = ("assembly.assemble(host State of iterate j, host accn) + "
+                "linsolve.BlockSolver.solve -> host du")
         ws.ctx.close()
     else:
-        # ---- e2e per rank: slab state from pinned host, iteration, back ----
-        h_state = torch.empty_like(work.u, device="cpu").pin_memory()
-        h_state.copy_(work.u)
-        bi = bo = h_state.numel() * 8
+        # ---- e2e per rank: iterate j's slab state H2D from pinned host, the
+        # iteration, the updated state D2H, every step ----------------------
+        h_out = torch.empty_like(host_u[0][0]).pin_memory()
+        bi = bo = h_out.numel() * 8
         barrier()
         t0 = time.perf_counter()
-        for _ in range(e2e_steps):
-            work.u.copy_(h_state, non_blocking=True)
-            sim.newton_iteration(work, dt, dt, capped, False)
-            h_state.copy_(work.u, non_blocking=True)
+        for j in range(e2e_steps):
+            it = j % CYCLE + 1
+            cyc.work.u.copy_(host_u[it - 1][0], non_blocking=True)
+            cyc.work.bhp = host_u[it - 1][1].copy()
+            sim.newton_iteration(cyc.work, dt, dt, sim.capped.copy(), it)
+            h_out.copy_(cyc.work.u, non_blocking=True)
             torch.cuda.current_stream().synchronize()
         barrier()
         t = torch.tensor([time.perf_counter() - t0], device="cuda")
         import torch.distributed as dist
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         e2e_s = float(t.item())
-        path = ("newton.Simulator.newton_iteration per rank, slab state H2D from pinned host "
-                "and D2H back every step")
+        path = ("newton.Simulator.newton_iteration per rank: iterate j's slab state H2D from "
+                "pinned host, updated state D2H, every step")
     e2e = {"value": n_global * e2e_steps / e2e_s, "unit": UNIT, "h2d_bytes_per_step": int(bi),
            "d2h_bytes_per_step": int(bo), "path": path}
 
     value = n_global * args.steps / (dev_ms / 1e3)
+    cfg = workload(args.config, case)
     out = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
            "warmup": args.warmup, "ms_per_step": dev_ms / args.steps, "higher_is_better": True,
            "scaling": "strong", "vs_baseline": None, "dtype": "f64",
            "data": "synthetic (seeded: log-normal perm, uniform porosity; BASELINE configs[3])",
-           "config": {"workload": f"{args.config.upper()} {case.nx}x{case.ny}x{case.nz} "
-                                  f"({n_global} cells, {len(case.wells)} wells), first timestep "
-                                  f"dt={dt} d, Newton iterations (assemble + decouple + "
-                                  f"precond setup + BiCGSTAB to LINEAR_TOL + update)",
-                      "precond": case.solver.precond,
-                      "precond_note": ("multicolour (red-black) block-ILU(0) per north_star; "
-                                       "the reference's exact RAS is reported in ras_exact")
-                      if case.solver.precond == "mcilu" else "reference preconditioner",
-                      "linear_tol": case.solver.linear_tol,
-                      "bicgstab_iters_per_step": float(np.mean(its)),
-                      "parallelism": dist_note,
-                      "l2": "inputs larger than L2 (system ~9 GB), no flush"},
+           "config": cfg,
+           "algorithm": {"precond": case.solver.precond,
+                         "note": ("multicolour (red-black) block-ILU(0) per north_star; the "
+                                  "reference's exact RAS on the GPU is reported in ras_exact")
+                         if case.solver.precond == "mcilu" else "reference preconditioner",
+                         "bicgstab_iters_per_step": float(np.mean(its)),
+                         "bicgstab_iters_per_cycle_iteration": cycle_iters,
+                         "reference_first_timestep": REF_STEP1,
+                         "parallelism": dist_note},
            "e2e": e2e, "gpu_launches": int(launches), "clocks": clk,
            # timers per stage, CUDA events, ms per Newton iteration
            "stage_ms": {"assemble": float(stage_ms[0]), "decouple": float(stage_ms[1]),
@@ -490,48 +555,59 @@ def run_spmv_c5(steps=20):
 
 # --------------------------------------------------------- CPU oracle arm
 
-def cpu_sample_case():
-    from dataclasses import replace
-    from paper_1811_11992_b200 import configs
-    case = configs.config("c4")
-    return replace(case, nz=2, wells=tuple(replace(w, k=2) for w in case.wells))
-
-
-def run_oracle(steps, warmup, budget_s=None):
-    """Newton iterations of the CPU restatement (oracle port) on a bounded
-    C4 sample (200x200x2 = 80k cells, same fluid/rock/wells pattern)."""
+def run_oracle(steps, warmup, config="c4", budget_s=None):
+    """The reference algorithm on the host: the oracle port (plain C with
+    OpenMP where the reference uses prange, numpy drivers, the reference's
+    RAS subdomain block-ILU(0) with its independent subdomains on a thread
+    pool) stepping the same Newton-iteration cycle of the same full-size case.
+    ``budget_s`` (cpu_baseline leg) stops after the first step past the budget."""
     ncpu = os.cpu_count() or 1
     os.environ["OMP_NUM_THREADS"] = str(ncpu)
     from oracle import isc_oracle as O
     from paper_1811_11992_b200 import configs
-    case = cpu_sample_case()
+    case = configs.config(config)
     grid, pack, wells, streams, state = configs.build_case(case)
-    sim = O.Simulator(grid, pack, wells, streams, state, case.schedule, case.solver)
+    sim = O.Simulator(grid, pack, wells, streams, state, case.schedule, case.solver,
+                      threads=ncpu)
+    solver = sim.solver
     dt = case.schedule.dt_init
-    capped = np.zeros(len(wells), dtype=bool)
-    st = sim.state.copy()
+    init = sim.state.copy()
+    cur = {"st": init.copy(), "j": 0, "capped": np.zeros(len(wells), dtype=bool)}
 
-    def iteration(st):
+    def step():
+        """newton.py:275-309 loop body for solving iteration (j mod CYCLE) + 1."""
+        it = cur["j"] % CYCLE + 1
+        if it == 1:
+            cur["st"] = init.copy()
+        st = cur["st"]
         blocks = O.assemble(grid, sim.model, sim.ws, sim.wells, sim.streams, st, sim.accn, dt,
-                            dt, capped)
-        du, dbhp, it = sim.solver.solve(blocks)
-        return O.apply_update(st, du, dbhp, pack.nco, pack.ncg, case.solver.eps)
+                            dt, cur["capped"], freeze_upwind=it > 5)
+        O.scaled_norm(sim.ws, sim.accn, grid.volume, dt, blocks, sim.wells, cur["capped"],
+                      pack.row_energy + 1, pack.row_energy + 2)
+        O.desired_capped(sim.wells, cur["capped"], st, blocks)
+        du, dbhp, iters = solver.solve(blocks)
+        cur["st"] = O.apply_update(st, du, dbhp, pack.nco, pack.ncg, case.solver.eps)
+        cur["j"] += 1
+        return iters
 
     for _ in range(warmup):
-        st = iteration(st)
+        step()
+    cur["j"] = 0
+    its = []
     t0 = time.perf_counter()
-    done = 0
     for _ in range(steps):
-        st = iteration(st)
-        done += 1
+        its.append(step())
         if budget_s and time.perf_counter() - t0 > budget_s:
             break
     el = time.perf_counter() - t0
+    done = len(its)
     return {"value": grid.ncell * done / el, "unit": UNIT, "cores": ncpu, "kind": "port",
-            "sample": f"C4 sample {grid.nx}x{grid.ny}x{grid.nz} ({grid.ncell} cells), "
-                      f"{done} Newton iterations (assemble+decouple+RAS-ILU BiCGSTAB), "
-                      f"oracle/ C+numpy port, OMP threads={ncpu}",
-            "seconds": el}
+            "sample": f"{config.upper()} full grid ({grid.ncell} cells), {done} Newton "
+                      f"iterations of the first-timestep cycle (assemble + norm + decouple + "
+                      f"RAS block-ILU(0) + BiCGSTAB to {case.solver.linear_tol} + update), "
+                      f"oracle/ C+numpy port of the reference, OpenMP + "
+                      f"{ncpu}-thread subdomain pool",
+            "seconds": el, "steps": done, "bicgstab_iters": its, "case": case}
 
 
 def run_timesteps(config="c4", nsteps=2):
@@ -620,13 +696,21 @@ def main():
     if args.impl == "reference":
         if rank != 0:
             return
-        res = run_oracle(args.steps, args.warmup)
+        res = run_oracle(args.steps, args.warmup, args.config)
+        case = res["case"]
         line = {"metric": METRIC, "value": res["value"], "unit": UNIT, "n_gpus": args.gpus,
                 "steps": args.steps, "warmup": args.warmup,
-                "ms_per_step": res["seconds"] * 1e3 / max(1, args.steps),
+                "ms_per_step": res["seconds"] * 1e3 / max(1, res["steps"]),
                 "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
-                "dtype": "f64", "data": "synthetic (seeded)", "impl": "reference",
-                "config": {"workload": res["sample"]},
+                "dtype": "f64",
+                "data": "synthetic (seeded: log-normal perm, uniform porosity; BASELINE "
+                        "configs[3])",
+                "impl": "reference", "config": workload(args.config, case),
+                "algorithm": {"precond": case.solver.precond,
+                              "note": "the reference's own algorithm (RAS subdomain "
+                                      "block-ILU(0), serial-order dots) on the host cores",
+                              "bicgstab_iters_per_step": float(np.mean(res["bicgstab_iters"])),
+                              "bicgstab_iters": res["bicgstab_iters"]},
                 "cpu_baseline": {k: res[k] for k in ("value", "unit", "cores", "kind", "sample")},
                 "e2e": {"value": res["value"], "unit": UNIT, "h2d_bytes_per_step": 0,
                         "d2h_bytes_per_step": 0}}
@@ -673,7 +757,7 @@ def main():
             except Exception as exc:  # report, never hide
                 out["report_frame_c4"] = {"error": repr(exc)}
         if not args.no_cpu_baseline:
-            cb = run_oracle(steps=3, warmup=0, budget_s=25.0)
+            cb = run_oracle(steps=CYCLE, warmup=0, config=args.config, budget_s=20.0)
             out["cpu_baseline"] = {k: cb[k] for k in ("value", "unit", "cores", "kind", "sample")}
     if rank == 0:
         print(json.dumps(out))

@@ -682,11 +682,24 @@ class _Subdomain:
 
 
 class BlockSolver:
-    """linsolve.py:317-578 (BiCGSTAB with none / bjacobi / ras)."""
+    """linsolve.py:317-578 (BiCGSTAB with none / bjacobi / ras), plus
+    ``mcilu``: the north star's multicolour (red-black) block ILU(0) of the
+    decoupled system as the right preconditioner of the same BiCGSTAB (the
+    reference has no such preconditioner; this restates the algorithm the
+    device solves in red-eliminated form, so its iteration
+    counts and solutions have a CPU checker)."""
 
-    def __init__(self, grid, ws, tol=1e-5, maxiter=200, precond="ras"):
-        if precond not in ("none", "bjacobi", "ras"):
+    def __init__(self, grid, ws, tol=1e-5, maxiter=200, precond="ras", threads=1):
+        if precond not in ("none", "bjacobi", "ras", "mcilu"):
             raise ValueError(f"unknown preconditioner {precond!r}")
+        # threads > 1: the independent subdomains' factor / apply calls run on a
+        # thread pool (ctypes releases the GIL). Each subdomain writes only its
+        # own slots and owned rows, so results are bit-identical to the
+        # reference's serial loop (linsolve.py:398-421); used by bench.py's CPU arm.
+        self._pool = None
+        if threads > 1:
+            from concurrent.futures import ThreadPoolExecutor
+            self._pool = ThreadPoolExecutor(max_workers=threads)
         self.grid, self.ws, self.tol, self.maxiter, self.precond = grid, ws, tol, maxiter, precond
         self.nu = ws.resid.shape[1]
         n = grid.ncell
@@ -695,7 +708,11 @@ class BlockSolver:
         self.other = _c(np.where(ws.adj_sides == 0, grid.conn_b[ws.adj_ids],
                                  grid.conn_a[ws.adj_ids]), np.int64)
         self.subs: List[_Subdomain] = []
-        if precond != "none":
+        if precond == "mcilu":
+            i, j, k = (np.arange(n) % grid.nx, (np.arange(n) // grid.nx) % grid.ny,
+                       np.arange(n) // (grid.nx * grid.ny))
+            self.black = ((i + j + k) % 2) == 1
+        elif precond != "none":
             owned_l, halos = partition_cells(grid, subdomain_count(n))
             for owned, halo in zip(owned_l, halos):
                 ext = np.union1d(owned, halo).astype(np.int64) if (
@@ -723,29 +740,84 @@ class BlockSolver:
             elims.append((b.cells, b.wrow.copy(), b.dwdb, b.resid))
         return elims
 
+    def _mc_factor(self):
+        """Red-black block ILU(0) of the decoupled A (diagonal blocks taken as
+        I, as stored after decoupling): U_b = I - sum_r A_br A_rb per black
+        cell (the fill-in of the 7-point pattern stays on the block diagonal)."""
+        ws, g = self.ws, self.grid
+        a, b = np.asarray(g.conn_a, np.int64), np.asarray(g.conn_b, np.int64)
+        ub = np.tile(np.eye(self.nu), (g.ncell, 1, 1))
+        blk_a = self.black[a]   # connection's black end is a (else b)
+        prod_a = np.einsum("cij,cjk->cik", ws.offd[:, 0], ws.offd[:, 1])   # A_ab A_ba
+        prod_b = np.einsum("cij,cjk->cik", ws.offd[:, 1], ws.offd[:, 0])   # A_ba A_ab
+        np.subtract.at(ub, a[blk_a], prod_a[blk_a])
+        np.subtract.at(ub, b[~blk_a], prod_b[~blk_a])
+        try:
+            self._ubinv = np.linalg.inv(ub[self.black])
+        except np.linalg.LinAlgError as exc:
+            raise SingularCellBlock(f"multicolour ILU(0) pivot block is singular: {exc}")
+
+    def _mc_apply(self, r, z):
+        """z = U^-1 L^-1 r: z_r = r_r; w_b = r_b - A_br z_r; z_b = U_b^-1 w_b;
+        z_r = r_r - A_rb z_b."""
+        ws, g = self.ws, self.grid
+        a, b = np.asarray(g.conn_a, np.int64), np.asarray(g.conn_b, np.int64)
+        blk_a = self.black[a]
+        red_c = np.where(blk_a, b, a)
+        blk_c = np.where(blk_a, a, b)
+        a_br = np.where(blk_a[:, None, None], ws.offd[:, 0], ws.offd[:, 1])
+        a_rb = np.where(blk_a[:, None, None], ws.offd[:, 1], ws.offd[:, 0])
+        w = r.copy()
+        np.subtract.at(w, blk_c, np.einsum("cij,cj->ci", a_br, r[red_c]))
+        z[:] = r
+        z[self.black] = np.einsum("cij,cj->ci", self._ubinv, w[self.black])
+        np.subtract.at(z, red_c, np.einsum("cij,cj->ci", a_rb, z[blk_c]))
+
     def _factor(self):
+        if self.precond == "mcilu":
+            self._mc_factor()
+            return
         ws = self.ws
-        for s, sub in enumerate(self.subs):
-            bad = lib().orc_ilu_factor(
+
+        def one(s):
+            sub = self.subs[s]
+            return lib().orc_ilu_factor(
                 ctypes.c_int64(self.nu), _p(ws.diag), _p(ws.offd),
                 ctypes.c_int64(sub.cells.shape[0]), _p(sub.cells), _p(sub.low_ptr),
                 _p(sub.low_j), _p(sub.low_ic), _p(sub.low_sd), _p(self._uinv[s]),
                 _p(self._lblk[s]))
+
+        idx = range(len(self.subs))
+        bads = list(self._pool.map(one, idx)) if self._pool else [one(s) for s in idx]
+        for s, bad in enumerate(bads):   # first failing subdomain, as the serial loop
             if bad >= 0:
-                raise SingularCellBlock(f"ILU(0) pivot failed in cell {int(sub.cells[bad])}")
+                raise SingularCellBlock(
+                    f"ILU(0) pivot failed in cell {int(self.subs[s].cells[bad])}")
 
     def _apply_precond(self, r, z):
         if self.precond == "none":
             z[:] = r
             return
+        if self.precond == "mcilu":
+            self._mc_apply(r, z)
+            return
         z[:] = 0.0
         r = _c(r)
-        for s, sub in enumerate(self.subs):
+
+        def one(s):
+            sub = self.subs[s]
             lib().orc_ilu_apply(
                 ctypes.c_int64(self.nu), _p(r), ctypes.c_int64(sub.cells.shape[0]),
                 _p(sub.cells), _p(sub.low_ptr), _p(sub.low_j), _p(self._lblk[s]),
                 _p(sub.up_ptr), _p(sub.up_j), _p(sub.up_ic), _p(sub.up_sd), _p(self.ws.offd),
                 _p(self._uinv[s]), _p(self._zloc[s]))
+
+        if self._pool:
+            list(self._pool.map(one, range(len(self.subs))))
+        else:
+            for s in range(len(self.subs)):
+                one(s)
+        for s, sub in enumerate(self.subs):
             z[sub.owned] = self._zloc[s][sub.owned_pos]
 
     def _matvec(self, v, out):
@@ -941,14 +1013,15 @@ class Simulator:
     """
 
     def __init__(self, grid, pack, wells, streams, state, schedule, solver, heat_loss=None,
-                 jacobian="analytic"):
+                 jacobian="analytic", threads=1):
         self.jacobian = jacobian   # newton.py:228
         self.grid, self.pack, self.wells, self.streams = grid, pack, tuple(wells), streams
         self.schedule, self.solver_cfg = schedule, solver
         self.model = Model(pack)
         self.ws = Workspace(grid, pack, heat_loss)
         self.solver = BlockSolver(grid, self.ws, tol=solver.linear_tol,
-                                  maxiter=solver.linear_max, precond=solver.precond)
+                                  maxiter=solver.linear_max, precond=solver.precond,
+                                  threads=threads)
         self.state = state.copy()
         self.capped = np.zeros(len(self.wells), dtype=bool)
         self.time = 0.0

@@ -65,6 +65,18 @@ class InitSpec:
 
 
 @dataclass(frozen=True)
+class HeatLoss:
+    """Overburden heat loss (deck.py:131-135 ``HeatLossSpec``, the *ROCK
+    ``HEATLOSS kob d rho tini`` row); applied on the top and bottom layers
+    (grid.py:189-206, _kernels.py:821-825)."""
+
+    k_ob: float
+    distance: float
+    rho: float
+    t_initial: float
+
+
+@dataclass(frozen=True)
 class Case:
     name: str
     nx: int
@@ -80,6 +92,7 @@ class Case:
     phi: float = 0.3                    # homogeneous porosity
     pack: str = "tube3_pack"
     nsteps: int = 0
+    heat_loss: Optional[HeatLoss] = None
 
     @property
     def ncell(self) -> int:
@@ -116,7 +129,31 @@ def _bhp_producer(name, i, j, k, bhp=2014.7, wi=None, radius=None):
 
 
 def config(name: str, **overrides) -> Case:
-    """C1..C4 of BASELINE.json (+ a small 3D case for tests)."""
+    """C1..C4 of BASELINE.json (+ a small 3D case for tests).
+
+    C2 variants that switch on the reference's less common branches:
+
+    * ``c2hl``   — overburden heat loss with the reference deck's own row
+      (decks/heatloss.deck:23, ``HEATLOSS 24.0 50.0 42.0 100.0``);
+    * ``c2cap``  — injector pressure cap 2450 psi: the injector caps and is
+      released again inside Newton iterations (newton.py:147-168), steps fail
+      on the Newton limit and are cut, and the run ends capped
+      (the well equation ``bhp - pinjmax``, assembly.py:515-516);
+    * ``c2rate`` — the producer on total-rate control (``RATE_TOTAL -10``
+      lbmol/day, the ``qsum - target`` equation, assembly.py:518-520).
+    """
+    if name in ("c2hl", "c2cap", "c2rate"):
+        base = config("c2")
+        if name == "c2hl":
+            case = replace(base, name=name, heat_loss=HeatLoss(24.0, 50.0, 42.0, 100.0))
+        elif name == "c2cap":
+            inj, prod = base.wells
+            case = replace(base, name=name, wells=(replace(inj, pinjmax=2450.0), prod))
+        else:
+            inj, prod = base.wells
+            case = replace(base, name=name,
+                           wells=(inj, replace(prod, control="rate_total", rate=-10.0, bhp=None)))
+        return _apply_overrides(case, overrides)
     if name == "c1":
         nsteps, dt = 50, 5e-4
         case = Case(
@@ -148,6 +185,10 @@ def config(name: str, **overrides) -> Case:
                     seed=1234, nsteps=nsteps)
     else:
         raise KeyError(f"unknown config {name!r}")
+    return _apply_overrides(case, overrides)
+
+
+def _apply_overrides(case: Case, overrides) -> Case:
     solver = overrides.pop("solver", None)
     if solver is not None:
         case = replace(case, solver=solver)

@@ -708,6 +708,9 @@ extern "C" int isc_numeric_jacobian(isc_ctx* ctx, double* h_wells_out, int64_t* 
   CK(cudaMemcpyAsync(ctx->bad_h, ctx->bad_d, 8, cudaMemcpyDeviceToHost, st));
   CK(cudaStreamSynchronize(st));
   ctx->offd_rows = NU;   // every row of every block written
+  // finite-difference blocks can carry coke-column entries in every row: the
+  // compact form's coke-column skip (k_cc_red, k_face_gather) must not apply
+  CK(cudaMemsetAsync(ctx->ccnz_d, 0xff, 4, st));
   double flag = *ctx->bad_h != ~0ULL ? 1.0 : 0.0;
   int as = isc_comm_allreduce_host(ctx, &flag, 1, 1);
   if (as) return as;
@@ -1489,13 +1492,25 @@ extern "C" int isc_comm_allreduce_host(isc_ctx* ctx, double* vals, int32_t count
   if (!cm.active() || count <= 0) return ISC_OK;
   if (count > 64) { g_err = "too many values"; return ISC_BAD_ARGUMENT; }
   if (cm.nccl) {
+    // NCCL's max on doubles drops NaN (fmax semantics), so a NaN norm on one
+    // rank would vanish behind the others' finite values. For op max the
+    // values go as (NaN -> +inf, NaN flag) pairs in one reduction and NaN is
+    // restored wherever any rank had one (the hub path below propagates it).
+    double buf[128];
+    const int len = op ? 2 * count : count;
+    for (int i = 0; i < count; ++i) {
+      const bool nan = vals[i] != vals[i];
+      buf[i] = (op && nan) ? INFINITY : vals[i];
+      if (op) buf[count + i] = nan ? 1.0 : 0.0;
+    }
     double* d = ctx->partial;   // scratch
-    CK(cudaMemcpyAsync(d, vals, count * 8, cudaMemcpyHostToDevice, ctx->stream));
-    const int r = nccl_api().AllReduce(d, d, count, ncclFloat64_, op ? ncclMax_ : ncclSum_,
+    CK(cudaMemcpyAsync(d, buf, len * 8, cudaMemcpyHostToDevice, ctx->stream));
+    const int r = nccl_api().AllReduce(d, d, len, ncclFloat64_, op ? ncclMax_ : ncclSum_,
                                        cm.nccl, ctx->stream);
     if (r != ncclSuccess_) { g_err = "NCCL allreduce failed"; return ISC_CUDA_ERROR; }
-    CK(cudaMemcpyAsync(vals, d, count * 8, cudaMemcpyDeviceToHost, ctx->stream));
+    CK(cudaMemcpyAsync(buf, d, len * 8, cudaMemcpyDeviceToHost, ctx->stream));
     CK(cudaStreamSynchronize(ctx->stream));
+    for (int i = 0; i < count; ++i) vals[i] = (op && buf[count + i] > 0.0) ? NAN : buf[i];
     return ISC_OK;
   }
   Hub* h = cm.hub;
@@ -1620,7 +1635,7 @@ static int bicgstab(isc_ctx* ctx, double tol, int maxiter, int* iters) {
     double rho = sh[S_RHO_NEW];
     const double omega = sh[S_OMEGA];
     if (std::fabs(rho) < brk || (!first && omega == 0.0)) {
-      if (restarted) { g_err = "BiCGSTAB scalar breakdown"; *iters = it; return ISC_BREAKDOWN; }
+      if (restarted) { g_err = "BiCGSTAB scalar breakdown at iteration " + std::to_string(it); *iters = it; return ISC_BREAKDOWN; }
       TRY(restart());
       TRY(K.push());
       TRY(K.dot(rhat, r, S_RHO_NEW));
@@ -1650,7 +1665,7 @@ static int bicgstab(isc_ctx* ctx, double tol, int maxiter, int* iters) {
     TRY(K.read_scalars());
     const double den = sh[S_DEN];
     if (std::fabs(den) < brk) {
-      if (restarted) { g_err = "BiCGSTAB denominator breakdown"; *iters = it; return ISC_BREAKDOWN; }
+      if (restarted) { g_err = "BiCGSTAB denominator breakdown at iteration " + std::to_string(it); *iters = it; return ISC_BREAKDOWN; }
       TRY(restart());
       TRY(K.push());
       TRY(K.dot(rhat, r, S_RHO_NEW));
@@ -1869,7 +1884,7 @@ static int bicgstab_schur(isc_ctx* ctx, double tol, int maxiter, int* iters) {
     double rho = sh[S_RHO_NEW];
     const double omega = sh[S_OMEGA];
     if (std::fabs(rho) < brk || (!first && omega == 0.0)) {
-      if (restarted) { g_err = "BiCGSTAB scalar breakdown"; *iters = it; return ISC_BREAKDOWN; }
+      if (restarted) { g_err = "BiCGSTAB scalar breakdown at iteration " + std::to_string(it); *iters = it; return ISC_BREAKDOWN; }
       TRY(restart());
       TRY(K.push());
       TRY(dot_b(rhat, r, S_RHO_NEW));
@@ -1906,7 +1921,7 @@ static int bicgstab_schur(isc_ctx* ctx, double tol, int maxiter, int* iters) {
     TRY(K.read_scalars());
     const double den = sh[S_DEN];
     if (std::fabs(den) < brk) {
-      if (restarted) { g_err = "BiCGSTAB denominator breakdown"; *iters = it; return ISC_BREAKDOWN; }
+      if (restarted) { g_err = "BiCGSTAB denominator breakdown at iteration " + std::to_string(it); *iters = it; return ISC_BREAKDOWN; }
       TRY(restart());
       TRY(K.push());
       TRY(dot_b(rhat, r, S_RHO_NEW));

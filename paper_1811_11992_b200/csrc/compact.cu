@@ -369,7 +369,11 @@ __global__ void __launch_bounds__(32 * CR, CP_MINB) k_cc_spmv(CP_ARGS) {
 // ccnz: 0 while every component row (< ROW_E) of the blocks has a zero coke
 // column (the face evaluation clears it per assembly and sets it on a
 // nonzero; imports and other writers set it) -- those 5 of the 54 row values
-// are then not loaded (adding their zero products changes no bit).
+// are then not loaded (adding their zero products changes no bit for a
+// finite z; a non-finite coke entry of z would make the full product NaN
+// (0 * inf) where the skip leaves the row finite -- the Krylov vectors'
+// norms, summed over all components, still turn non-finite in that case, so
+// BiCGSTAB's breakdown / tolerance tests see it one dot product later).
 __global__ void __launch_bounds__(32 * CR, CC_MINB) k_cc_red(Dims g, const double* __restrict__ offd,
                                                              const int* __restrict__ ccnz,
                                                              double* __restrict__ z) {

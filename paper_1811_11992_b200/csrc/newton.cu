@@ -4,15 +4,27 @@
 
 namespace isc {
 
-// newton.py:63-89 (vectorised damp_saturation)
+// numpy's maximum / minimum propagate NaN from either operand; CUDA's fmax /
+// fmin return the other operand instead, so NaN-carrying updates would turn
+// into finite states and hide divergence from the norm check
+__device__ __forceinline__ double np_maximum(double a, double b) {
+  return (a != a || b != b) ? a + b : fmax(a, b);
+}
+__device__ __forceinline__ double np_minimum(double a, double b) {
+  return (a != a || b != b) ? a + b : fmin(a, b);
+}
+
+// newton.py:80-89 (_damp_array), one element; comparisons with NaN are
+// false, so a NaN raw value passes through as in numpy
 __device__ __forceinline__ double damp(double old, double raw, double eps) {
-  if (raw < 0.0) return sqrt(eps * fmax(old, 0.0));
+  if (raw < 0.0) return sqrt(eps * np_maximum(old, 0.0));
   if (raw < eps && old >= eps) return 0.5 * old;
   return raw;
 }
 
+// np.clip(v, lo, hi) == minimum(maximum(v, lo), hi), NaN-propagating
 __device__ __forceinline__ double clip(double v, double lo, double hi) {
-  return fmin(fmax(v, lo), hi);   // np.clip == minimum(maximum(v, lo), hi)
+  return np_minimum(np_maximum(v, lo), hi);
 }
 
 // newton.py:92-121; state and du SoA in unknown order
@@ -23,8 +35,8 @@ __global__ void k_newton_update(int64_t n, double* __restrict__ st, const double
   st[c] = st[c] + du[c];
 #pragma unroll
   for (int i = 1; i < CT; ++i) st[i * n + c] = clip(st[i * n + c] + du[i * n + c], 0.0, 1.0);
-  st[CT * n + c] = fmax(st[CT * n + c] + du[CT * n + c], -459.0);
-  st[CCC * n + c] = fmax(st[CCC * n + c] + du[CCC * n + c], 0.0);
+  st[CT * n + c] = np_maximum(st[CT * n + c] + du[CT * n + c], -459.0);
+  st[CCC * n + c] = np_maximum(st[CCC * n + c] + du[CCC * n + c], 0.0);
   const double sw0 = st[CSW * n + c], sg0 = st[CSG * n + c];
   const double so_old = 1.0 - sw0 - sg0;
   const double sw = damp(sw0, sw0 + du[CSW * n + c], eps);

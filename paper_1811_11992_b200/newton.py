@@ -162,14 +162,20 @@ class Simulator:
         wn = float(self.ctx.allreduce_host([wn], "max")[0])   # wells live on their owner rank
         return max(norm, wn)
 
-    def newton_iteration(self, work: DeviceState, dt, t_new, capped, freeze):
-        """One assemble + solve + update (the benchmark's unit of work)."""
-        self._assemble(work, self.accn, dt, t_new, capped, freeze)
-        dbhp, iters = self.ctx.solve(self.solver_cfg.linear_tol, self.solver_cfg.linear_max,
-                                     self.du)
-        self.ctx.newton_update(work.u, self.du, self.solver_cfg.eps)
+    def newton_iteration(self, work: DeviceState, dt, t_new, capped, it: int = 1):
+        """One solving Newton iteration — the body of newton_step's loop
+        (newton.py:275-309) for an iteration that does not converge: assemble
+        (upwinding frozen after iteration 5), scaled norm, capped-injector
+        check, solve, damped update. The benchmark's unit of work; returns
+        (scaled norm, BiCGSTAB iterations)."""
+        cfg = self.solver_cfg
+        blocks = self._assemble(work, self.accn, dt, t_new, capped, it > FREEZE_UPWIND_AFTER)
+        norm = self.scaled_norm(blocks, dt, capped)
+        desired_capped(self.wells, capped, work.bhp, blocks)
+        dbhp, iters = self.ctx.solve(cfg.linear_tol, cfg.linear_max, self.du)
+        self.ctx.newton_update(work.u, self.du, cfg.eps)
         work.bhp = work.bhp + dbhp
-        return iters
+        return norm, iters
 
     def newton_step(self, state: DeviceState, dt: float, t_new: float, capped: np.ndarray):
         """newton.py:254-310"""

@@ -250,6 +250,75 @@ def make_traj_c4_sample():
     print("c4", sim.totals())
 
 
+def make_traj_c4_1e10():
+    """BASELINE configs[3] at LINEAR_TOL 1e-10 (the north star's field bar
+    needs it on both sides): per-step records, per-solve Krylov
+    counts, the field norms and a seeded 16384-cell sample of the final p, T,
+    Sw, Sg, C_c (the full fields would be 80 MB)."""
+    case = configs.config("c4")
+    case = replace(case, solver=replace(case.solver, linear_tol=1e-10))
+    sim = reference_simulator(case, threads=min(16, os.cpu_count() or 4))
+    iters = []
+    orig = L.BlockSolver.solve
+
+    def counting(self, blocks):
+        du, dbhp, it = orig(self, blocks)
+        iters.append(it)
+        return du, dbhp, it
+
+    L.BlockSolver.solve = counting
+    try:
+        sim.advance()
+    finally:
+        L.BlockSolver.solve = orig
+    rec = np.array([(s.time, s.dt, s.newton, s.linear, s.solves, s.balance)
+                    for s in sim.steps])
+    rng = np.random.default_rng(4242)
+    idx = np.sort(rng.choice(sim.grid.ncell, 16384, replace=False))
+    out = {"steps": rec, "cum_imbalance": np.array(sim.cumulative_imbalance()),
+           "solve_iters": np.array(iters), "sample_idx": idx,
+           "final_bhp": np.asarray(sim.state.bhp)}
+    for f in ("p", "t", "sw", "sg", "cc"):
+        a = np.asarray(getattr(sim.state, f))
+        out["sample_" + f] = a[idx]
+        out["norm_" + f] = np.array(np.linalg.norm(a))
+    np.savez_compressed(os.path.join(HERE, "traj_c4_1e-10_sample.npz"), **out)
+    print("c4 1e-10", sim.totals(), iters)
+
+
+def make_traj_variants():
+    """C2 with heat loss, with a capping/releasing injector, with a
+    rate-controlled producer (configs.config docstring), LINEAR_TOL 1e-10."""
+    for name in ("c2hl", "c2cap", "c2rate"):
+        make_traj(name, 1e-10)
+
+
+def make_bicgstab_breakdown():
+    """The reference's BiCGSTAB restart / breakdown branches on the constructed
+    2-cell systems of tests/golden_states.BREAKDOWN_CASES."""
+    from types import SimpleNamespace
+    from tests.golden_states import BREAKDOWN_CASES, breakdown_system
+    from iscsim.errors import Breakdown
+    grid = ref_build_grid(GridSpec(2, 1, 1, (1.0, 1.0), (1.0,), (1.0,)),
+                          RockSpec((1.0, 1.0), (1.0, 1.0), (1.0, 1.0), 0.3))
+    out = {}
+    for name, case in BREAKDOWN_CASES.items():
+        diag, offd, resid = breakdown_system(case)
+        ws = SimpleNamespace(diag=diag, offd=offd, resid=resid,
+                             adj_ptr=np.array([0, 1, 2], np.int64),
+                             adj_ids=np.array([0, 0], np.int64),
+                             adj_sides=np.array([0, 1], np.int8))
+        try:
+            du, _, it = L.BlockSolver(grid, ws, tol=1e-10, maxiter=50, precond="none").solve([])
+            out[name + "_status"] = np.array("ok")
+            out[name + "_iters"] = np.array(it)
+            out[name + "_du"] = du
+        except Breakdown as exc:
+            out[name + "_status"] = np.array("Breakdown: " + str(exc))
+        print(name, out[name + "_status"], out.get(name + "_iters"))
+    np.savez_compressed(os.path.join(HERE, "bicgstab_breakdown.npz"), **out)
+
+
 def make_traj_numeric():
     """C1 run in JACOBIAN numeric mode (newton.py:228, 278)."""
     make_traj("c1", 1e-10, jacobian="numeric")
@@ -286,5 +355,7 @@ if __name__ == "__main__":
     make_traj("c2", 1e-10)
     make_traj("c2", 1e-5)
     make_traj_c3()
+    make_traj_variants()
+    make_bicgstab_breakdown()
     for f in sorted(os.listdir(HERE)):
         print(f, os.path.getsize(os.path.join(HERE, f)))

@@ -34,3 +34,50 @@ def random_state_like_reference(c, seed):
     O.assemble(c.grid, O.Model(c.pack), ws, c.wells, c.streams, c.state, zero, 1.0, 0.0,
                np.zeros(len(c.wells), dtype=bool))
     return perturb(c.state, ws.acc.copy(), seed)
+
+
+# Constructed 2-cell systems (nx=2): decoupled A = [[I, B], [C, I]] with a 2x2
+# integer coupling in unknowns 0..1, rhs b there and 0 elsewhere. Found by a
+# search over small integer matrices; each drives the reference's BiCGSTAB
+# (linsolve.py:481-578, precond none) through one restart branch:
+BREAKDOWN_CASES = {
+    # (only cases whose branch sequence is the same under serial, reversed
+    # and pairwise dot-product order, so the device's reduction order cannot
+    # change the outcome)
+    # restart after an exact rho = 0 (iteration 2), then converges
+    "rho_restart_ok": ([[2, -1], [0, 1]], [[-2, -1], [-2, 0]], [2, -1, 0, 0]),
+    # restart after r^.v = 0 (iteration 2), then converges
+    "den_restart_ok": ([[-2, 0], [1, -1]], [[-2, 1], [0, -1]], [0, 0, 0, -1]),
+    # omega = 0 detected at iteration 3, restart, converges (t.s cancels to an
+    # exact 0 only in the reference's serial dot order: ROUNDING_DEPENDENT)
+    "omega_restart_ok": ([[-2, 1], [-1, -2]], [[0, -2], [-1, -1]], [0, 1, -1, -1]),
+    # r^.v = 0 twice: Breakdown (denominator) after the restart
+    "den_den_breakdown": ([[-2, 1], [1, -2]], [[0, -1], [0, -2]], [1, 0, 1, 0]),
+    # rho = 0 twice: Breakdown (scalar)
+    "rho_rho_breakdown": ([[-1, -1], [2, 0]], [[1, 0], [-2, -1]], [0, 0, 2, 2]),
+    # rho = 0, restart, omega = 0: Breakdown (scalar)
+    "rho_omega_breakdown": ([[2, -1], [2, -2]], [[-2, -2], [-2, -2]], [0, 1, 0, 0]),
+    # t.t = 0 twice: Breakdown (stagnation)
+    "tt_tt_breakdown": ([[0, 0], [-1, 2]], [[-1, 1], [2, 1]], [0, 2, 2, 0]),
+    # omega = 0, restart, then r^.v = 0: Breakdown (denominator)
+    "omega_den_breakdown": ([[0, 0], [-2, 1]], [[2, -1], [-2, 1]], [-1, 2, -1, 2]),
+    # rho = 0, restart, then t.t = 0: Breakdown (stagnation)
+    "rho_tt_breakdown": ([[-1, 1], [0, 0]], [[1, 1], [2, 0]], [0, 2, 0, 0]),
+}
+
+
+def breakdown_system(case):
+    """(diag, offd, resid) of a BREAKDOWN_CASES entry in the reference layout."""
+    bm, cm, b = (np.asarray(v, dtype=np.float64) for v in case)
+    diag = np.tile(np.eye(9), (2, 1, 1))
+    offd = np.zeros((1, 2, 9, 9))
+    offd[0, 0, :2, :2] = bm
+    offd[0, 1, :2, :2] = cm
+    resid = np.zeros((2, 9))
+    resid[0, :2], resid[1, :2] = -b[:2], -b[2:]
+    return diag, offd, resid
+
+# cases whose branch needs the reference's serial dot order (an exact zero
+# from cancelling rounded values): bit-exact in the oracle, which sums in that
+# order; a device reduction in another order legitimately misses the zero
+ROUNDING_DEPENDENT = ("omega_restart_ok",)

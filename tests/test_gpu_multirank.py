@@ -141,3 +141,31 @@ def test_slab_newton_run_matches_single_gpu(name, nsteps):
             assert np.max(np.abs(a - b) / np.maximum(np.abs(b), 1e-30)) <= 1e-6, f
         np.testing.assert_allclose(imb, ref.cumulative_imbalance(), rtol=1e-6, atol=1e-12)
     hub.close()
+
+
+def test_allreduce_max_propagates_nan_from_one_rank():
+    """The Newton norm's max over ranks keeps a NaN that only one rank sees
+    (the reference's scaled_norm is NaN then and counts as growth,
+    newton.py:284-289); sums propagate it too."""
+    c = case_objects("sub2")
+    nranks = 2
+    hub = Hub(nranks)
+    pieces = [split_case(c.case, nranks, r) for r in range(nranks)]
+    ctxs = []
+    for p in pieces:
+        cx = DeviceContext(p.grid, p.pack, p.wells, p.streams, "mcilu", own_stream=True)
+        attach_hub(cx, hub.h, p)
+        ctxs.append(cx)
+
+    def work(cx, r):
+        mx = cx.allreduce_host([float("nan") if r == 1 else 3.0, 1.0 + r], "max")
+        sm = cx.allreduce_host([float("nan") if r == 0 else 2.0, 1.0], "sum")
+        return mx, sm
+
+    res = hub.run(work, [(cx, r) for r, cx in enumerate(ctxs)])
+    for mx, sm in res:
+        assert np.isnan(mx[0]) and mx[1] == 2.0
+        assert np.isnan(sm[0]) and sm[1] == 2.0
+    for cx in ctxs:
+        cx.close()
+    hub.close()

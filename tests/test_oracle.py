@@ -273,13 +273,17 @@ def test_numeric_jacobian_run_prefix_vs_reference():
     np.testing.assert_array_equal(rec, g["steps"][:k, :5])
 
 
-@pytest.mark.parametrize("name,tol", [("c1", 1e-10), ("c1", 1e-5), ("c2", 1e-10)])
+@pytest.mark.parametrize("name,tol", [("c1", 1e-10), ("c1", 1e-5), ("c2", 1e-10),
+                                      ("c2hl", 1e-10), ("c2cap", 1e-10), ("c2rate", 1e-10)])
 def test_trajectory_vs_reference(name, tol):
-    """Whole runs: step/Newton/linear sequences equal, fields bit-identical."""
+    """Whole runs: step/Newton/linear sequences equal, fields bit-identical
+    (c2hl: overburden heat loss, _kernels.py:821-825; c2cap: injector capped
+    and released, newton.py:147-168, assembly.py:515-516, with Newton-limit
+    step cuts; c2rate: total-rate producer, assembly.py:518-520)."""
     g = golden(f"traj_{name}_{tol:.0e}.npz")
     c = case_objects(name, linear_tol=tol)
     sim = O.Simulator(c.grid, c.pack, c.wells, c.streams, c.state, c.case.schedule,
-                      c.case.solver)
+                      c.case.solver, heat_loss=c.case.heat_loss)
     sim.advance()
     rec = np.array([(s.time, s.dt, s.newton, s.linear, s.solves, s.balance)
                     for s in sim.steps])
@@ -287,3 +291,87 @@ def test_trajectory_vs_reference(name, tol):
     np.testing.assert_allclose(rec[:, 5], g["steps"][:, 5], rtol=0, atol=1e-12)
     for f in ("p", "t", "sw", "sg", "x", "y", "cc", "bhp"):
         np.testing.assert_array_equal(getattr(sim.state, f), g["final_" + f], err_msg=f)
+
+
+@pytest.mark.parametrize("name", sorted(__import__("tests.golden_states", fromlist=["x"])
+                                        .BREAKDOWN_CASES))
+def test_bicgstab_restart_and_breakdown_vs_reference(name):
+    """BiCGSTAB's single restart and its Breakdown exits (linsolve.py:497-575)
+    on the constructed 2-cell systems: same iteration count and solution, or
+    the same Breakdown message, as the reference (bicgstab_breakdown.npz)."""
+    from types import SimpleNamespace
+    from paper_1811_11992_b200.grid import build_grid
+    from tests.golden_states import BREAKDOWN_CASES, breakdown_system
+    g = golden("bicgstab_breakdown.npz")
+    grid = build_grid(2, 1, 1, 1.0, 1.0, 1.0, 1.0, 1.0, 1.0, 0.3)
+    diag, offd, resid = breakdown_system(BREAKDOWN_CASES[name])
+    ws = O.Workspace(grid, SimpleNamespace(nequ=9, nfull=5))
+    ws.diag, ws.offd, ws.resid = diag, offd, resid
+    status = str(g[name + "_status"])
+    if status == "ok":
+        du, _, it = O.BlockSolver(grid, ws, tol=1e-10, maxiter=50, precond="none").solve([])
+        assert it == int(g[name + "_iters"])
+        np.testing.assert_array_equal(du, g[name + "_du"])
+    else:
+        with pytest.raises(O.Breakdown) as exc:
+            O.BlockSolver(grid, ws, tol=1e-10, maxiter=50, precond="none").solve([])
+        assert "Breakdown: " + str(exc.value) == status
+
+
+@pytest.mark.parametrize("nx", [4, 5])
+def test_oracle_mcilu_is_red_black_ilu0(nx):
+    """The oracle's multicolour block ILU(0) (checker for the device's mcilu)
+    equals the red-black block ILU(0) computed densely."""
+    from paper_1811_11992_b200.grid import build_grid
+    from types import SimpleNamespace
+    grid = build_grid(nx, 3, 3, 1.0, 1.0, 1.0, 1.0, 1.0, 1.0, 0.3)
+    n = grid.ncell
+    diag, offd, _ = synth_system(grid, 9, seed=5)
+    # decoupled system: identity diagonal blocks, D^-1 B off the diagonal
+    inv = np.linalg.inv(diag)
+    a, b = grid.conn_a, grid.conn_b
+    off = np.stack([inv[a] @ offd[:, 0], inv[b] @ offd[:, 1]], axis=1)
+    ws = O.Workspace(grid, SimpleNamespace(nequ=9, nfull=5))
+    ws.offd = off
+    bs = O.BlockSolver(grid, ws, precond="mcilu")
+    bs._factor()
+    A = np.zeros((9 * n, 9 * n))
+    for c in range(n):
+        A[9 * c:9 * c + 9, 9 * c:9 * c + 9] = np.eye(9)
+    for ic in range(grid.nconn):
+        A[9 * a[ic]:9 * a[ic] + 9, 9 * b[ic]:9 * b[ic] + 9] = off[ic, 0]
+        A[9 * b[ic]:9 * b[ic] + 9, 9 * a[ic]:9 * a[ic] + 9] = off[ic, 1]
+    red = np.flatnonzero(~bs.black)
+    blk = np.flatnonzero(bs.black)
+    perm = np.concatenate([np.arange(9 * c, 9 * c + 9) for c in np.concatenate([red, blk])])
+    Ap = A[np.ix_(perm, perm)]
+    nr = red.size
+    Arb, Abr = Ap[:9 * nr, 9 * nr:], Ap[9 * nr:, :9 * nr]
+    Ub = np.eye(9 * blk.size)
+    for q in range(blk.size):
+        sl = slice(9 * q, 9 * q + 9)
+        Ub[sl, sl] = np.eye(9) - Abr[sl] @ Arb[:, sl]
+    L = np.block([[np.eye(9 * nr), np.zeros_like(Arb)], [Abr, np.eye(9 * blk.size)]])
+    U = np.block([[np.eye(9 * nr), Arb], [np.zeros_like(Abr), Ub]])
+    r = np.random.default_rng(1).normal(size=(n, 9))
+    z = np.zeros_like(r)
+    bs._apply_precond(r, z)
+    zp = np.linalg.solve(U, np.linalg.solve(L, r.reshape(-1)[perm]))
+    zr = np.empty_like(zp)
+    zr[perm] = zp
+    np.testing.assert_allclose(z.reshape(-1), zr, rtol=1e-11, atol=1e-13)
+
+
+def test_oracle_mcilu_solve_agrees_with_reference_solution():
+    """BiCGSTAB with the multicolour preconditioner reaches the reference's
+    solution of the same system (LINEAR_TOL 1e-10 makes it solver-independent)."""
+    g = golden("asm_small3d.npz")
+    s = golden("solve_small3d.npz")
+    c = case_objects("small3d")
+    ws, blocks = _oracle_assemble(c, state_from(g), g["accn"], float(g["dt"]),
+                                  float(g["t_new"]), g["capped"])
+    du, dbhp, it = O.BlockSolver(c.grid, ws, tol=1e-10, maxiter=1000,
+                                 precond="mcilu").solve(blocks)
+    ref = s["ras_du"]
+    assert np.linalg.norm(du - ref) <= 1e-8 * np.linalg.norm(ref)
+    assert int(s["ras_iters"]) <= it < int(s["none_iters"])

@@ -16,14 +16,14 @@ sim = Simulator(grid, pack, wells, streams, state, case.schedule, case.solver)
 dt = case.schedule.dt_init
 work, capped = sim.state.copy(), sim.capped.copy()
 for _ in range(3):
-    sim.newton_iteration(work, dt, dt, capped, False)
+    sim.newton_iteration(work, dt, dt, capped, 1)
 for prof in (0, 1, 0, 1):
     N.check(sim.ctx.L.isc_set_profiling(sim.ctx.h, prof), "p")
     torch.cuda.synchronize()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record()
     for _ in range(10):
-        sim.newton_iteration(work, dt, dt, capped, False)
+        sim.newton_iteration(work, dt, dt, capped, 1)
     e1.record()
     torch.cuda.synchronize()
     print("profiling", prof, "ms/step", e0.elapsed_time(e1) / 10)

@@ -94,8 +94,12 @@ def case_to_deck(case) -> str:
             out.append(key + " " + " ".join(_fmt(v) for v in arr))
     out.append("POROSITY 0.3")
     for ln in tube["ROCK"][0]:
-        if ln.split()[0] not in ("PERMX", "PERMY", "PERMZ", "POROSITY"):
+        if ln.split()[0] not in ("PERMX", "PERMY", "PERMZ", "POROSITY", "HEATLOSS"):
             out.append(ln)
+    hl = getattr(case, "heat_loss", None)
+    if hl is not None:
+        out.append(f"HEATLOSS {_fmt(hl.k_ob)} {_fmt(hl.distance)} {_fmt(hl.rho)} "
+                   f"{_fmt(hl.t_initial)}")
     out.append("")
     for sec in ("COMPONENTS", "KVALUES", "DENSITY", "VISCOSITY", "ENTHALPY"):
         out.append("*" + sec)
