@@ -98,7 +98,12 @@ def parse():
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--config", default="c4")
+    ap.add_argument("--config", default="c4",
+                    help="c4 (headline, BASELINE configs[3]) or c5 (configs[4] linear-solver "
+                         "microbench)")
+    ap.add_argument("--scaling", default="strong", choices=["strong", "weak"],
+                    help="c5 under torchrun: strong = 400x400x100 split over the ranks, weak = "
+                         "400x400x(100*ranks)")
     ap.add_argument("--precond", default="mcilu",
                     help="GPU preconditioner for the headline: mcilu (north_star's multicolour "
                          "block-ILU(0), default) or the reference's ras / bjacobi / none")
@@ -553,6 +558,124 @@ def run_spmv_c5(steps=20):
                       "block_rows_per_s": grid.ncell / ((dec_ms + solve_ms) / 1e3)}}
 
 
+def run_c5(args, rank, world, local):
+    """BASELINE configs[4]: seeded synthetic 7-point BSR (400x400x100, 16 M
+    block rows; weak scaling: 400x400x(100*ranks)), Gauss-Jordan decoupled
+    once, then every step = multicolour ILU(0) setup + BiCGSTAB to 1e-8.
+    Under torchrun each rank generates its z-slab rows of the global system
+    (isc_synth_system_slab, keyed by global cell index) and the solve runs
+    over NCCL (halo per half pass, all-reduced Krylov scalars)."""
+    import ctypes
+    import torch
+    from dataclasses import replace
+    from paper_1811_11992_b200 import configs, _native as N
+    from paper_1811_11992_b200.device import DeviceContext
+    torch.cuda.set_device(local)
+    case = configs.config("c5")
+    if args.scaling == "weak" and world > 1:
+        case = replace(case, nz=case.nz * world)
+    n_global = case.ncell
+    if world > 1:
+        import torch.distributed as dist
+        from paper_1811_11992_b200.distributed import attach_nccl, nccl_unique_id, split_case
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        uid = [nccl_unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(uid, src=0)
+        piece = split_case(case, world, rank)
+        grid, pack = piece.grid, piece.pack
+        ctx = DeviceContext(grid, pack, (), (), "mcilu")
+        attach_nccl(ctx, uid[0], piece)
+        note = f"z-slab x{world} ({args.scaling}), planes {piece.k0}-{piece.k1 - 1} on rank {rank}"
+    else:
+        grid, pack, _, _, _ = configs.build_case(case)
+        ctx = DeviceContext(grid, pack, (), (), "mcilu")
+        note = "single GPU"
+
+    def barrier():
+        if world > 1:
+            import torch.distributed as dist
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    N.check(ctx.L.isc_synth_system_slab(ctx.h, 7, case.nz), "synth")
+    bc, bcol = ctypes.c_int64(-1), ctypes.c_int32(-1)
+    it = ctypes.c_int32(0)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    barrier()
+    e0.record()
+    N.check(ctx.L.isc_decouple(ctx.h, ctypes.byref(bc), ctypes.byref(bcol)), "decouple")
+    e1.record()
+    barrier()
+    dec_ms = e0.elapsed_time(e1)
+    du = ctx.empty(9, grid.ncell)
+
+    def step():
+        N.check(ctx.L.isc_precond_setup(ctx.h, ctypes.byref(bc)), "setup")
+        N.check(ctx.L.isc_solve(ctx.h, case.solver.linear_tol, case.solver.linear_max,
+                                N.ptr(du), N.VP(0), ctypes.byref(it), ctypes.byref(bc),
+                                ctypes.byref(bcol)), "c5 solve")
+        return it.value
+
+    for _ in range(args.warmup):
+        step()
+    barrier()
+    clocks = ClockSampler(local)
+    clocks.start()
+    l0 = ctx.launch_count()
+    its = []
+    e0.record()
+    for _ in range(args.steps):
+        its.append(step())
+    e1.record()
+    barrier()
+    dev_ms = e0.elapsed_time(e1)
+    launches = ctx.launch_count() - l0
+    clk = clocks.stop()
+    # host-buffer leg: a new decoupled rhs from pinned host memory per solve
+    # (isc_set_rhs), du back to pinned host memory
+    rhs = ctx.empty(9, grid.ncell)
+    N.check(ctx.L.isc_copy_rhs(ctx.h, N.ptr(rhs)), "rhs")
+    h_rhs = rhs.cpu().pin_memory()
+    h_du = torch.empty_like(h_rhs).pin_memory()
+    e2e_steps = max(1, min(args.steps, 3))
+    barrier()
+    t0 = time.perf_counter()
+    for _ in range(e2e_steps):
+        rhs.copy_(h_rhs, non_blocking=True)
+        N.check(ctx.L.isc_set_rhs(ctx.h, N.ptr(rhs)), "set rhs")
+        step()
+        h_du.copy_(du, non_blocking=True)
+        torch.cuda.current_stream().synchronize()
+    barrier()
+    e2e_s = time.perf_counter() - t0
+    if world > 1:
+        import torch.distributed as dist
+        t = torch.tensor([dev_ms, e2e_s, dec_ms], device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        dev_ms, e2e_s, dec_ms = (float(v) for v in t.tolist())
+    ctx.close()
+    unit = "block-rows/s"
+    out = {"metric": "block-rows/s (multicolour ILU(0) setup + BiCGSTAB to 1e-8, decoupled "
+                     "7-point BSR)",
+           "value": n_global * args.steps / (dev_ms / 1e3), "unit": unit, "n_gpus": world,
+           "steps": args.steps, "warmup": args.warmup, "ms_per_step": dev_ms / args.steps,
+           "higher_is_better": True, "scaling": args.scaling if world > 1 else "strong",
+           "vs_baseline": None, "dtype": "f64",
+           "data": "synthetic (seeded BSR of BASELINE configs[4], keyed by global cell index)",
+           "config": {"workload": f"C5 {case.nx}x{case.ny}x{case.nz} ({n_global} block rows), "
+                                  f"decoupled once ({dec_ms:.1f} ms), step = mcilu setup + "
+                                  f"BiCGSTAB to {case.solver.linear_tol}",
+                      "l2": "inputs larger than L2 (system ~72 GB per 16 M rows), no flush"},
+           "algorithm": {"precond": "mcilu", "bicgstab_iters": its, "parallelism": note},
+           "e2e": {"value": n_global * e2e_steps / e2e_s, "unit": unit,
+                   "h2d_bytes_per_step": int(h_rhs.numel() * 8 * world),
+                   "d2h_bytes_per_step": int(h_du.numel() * 8 * world),
+                   "path": "isc_set_rhs (pinned host rhs) + isc_precond_setup + isc_solve -> "
+                           "pinned host du"},
+           "gpu_launches": int(launches), "clocks": clk, "decouple_ms": dec_ms}
+    return out
+
+
 # --------------------------------------------------------- CPU oracle arm
 
 def run_oracle(steps, warmup, config="c4", budget_s=None):
@@ -608,6 +731,46 @@ def run_oracle(steps, warmup, config="c4", budget_s=None):
                       f"oracle/ C+numpy port of the reference, OpenMP + "
                       f"{ncpu}-thread subdomain pool",
             "seconds": el, "steps": done, "bicgstab_iters": its, "case": case}
+
+
+def run_oracle_c5(steps, warmup):
+    """Reference arm of the C5 microbench: the reference's solver (oracle
+    port: RAS block-ILU(0) on its subdomain thread pool, BiCGSTAB to 1e-8) on
+    a bounded C5 sample (the host-side generator's 200x200x10 system, the
+    reference's layout), decoupled once; step = factorisation + BiCGSTAB."""
+    ncpu = os.cpu_count() or 1
+    os.environ["OMP_NUM_THREADS"] = str(ncpu)
+    import ctypes
+    from types import SimpleNamespace
+    from oracle import isc_oracle as O
+    from paper_1811_11992_b200.grid import build_grid
+    from paper_1811_11992_b200.synth import synth_system
+    grid = build_grid(200, 200, 10, 1.0, 1.0, 1.0, 1.0, 1.0, 1.0, 0.3)
+    diag, offd, resid = synth_system(grid, 9, seed=7)
+    ws = O.Workspace(grid, SimpleNamespace(nequ=9, nfull=5))
+    ws.diag, ws.offd, ws.resid = diag, offd, resid
+    bs = O.BlockSolver(grid, ws, tol=1e-8, maxiter=1000, precond="ras", threads=ncpu)
+    rhs = -resid
+    O.lib().orc_decouple_pass(ctypes.c_int64(grid.ncell), ctypes.c_int64(9), O._p(ws.diag),
+                              O._p(rhs), O._p(ws.offd), O._p(ws.adj_ptr), O._p(ws.adj_ids),
+                              O._p(ws.adj_sides), O._p(bs.invs), O._p(bs.flags))
+
+    def step():
+        bs._factor()
+        return bs._bicgstab(rhs)[1]
+
+    for _ in range(warmup):
+        step()
+    its = []
+    t0 = time.perf_counter()
+    for _ in range(steps):
+        its.append(step())
+    el = time.perf_counter() - t0
+    return {"value": grid.ncell * steps / el, "unit": "block-rows/s", "cores": ncpu,
+            "kind": "port", "seconds": el, "bicgstab_iters": its,
+            "sample": f"C5 sample {grid.nx}x{grid.ny}x{grid.nz} ({grid.ncell} block rows): RAS "
+                      f"block-ILU(0) setup + BiCGSTAB to 1e-8, oracle/ C+numpy port, OpenMP + "
+                      f"{ncpu}-thread subdomain pool"}
 
 
 def run_timesteps(config="c4", nsteps=2):
@@ -693,8 +856,31 @@ def run_report(config="c4"):
 def main():
     args = parse()
     rank, world, local = dist_setup(args.gpus)
+    if world > 1:
+        # NCCL's init lines (ranks, transports, NVLS) on stderr: the JSON line
+        # stays alone on stdout
+        os.environ.setdefault("NCCL_DEBUG", "INFO")
+        os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
+        os.environ.setdefault("NCCL_DEBUG_FILE", "/dev/stderr")
     if args.impl == "reference":
         if rank != 0:
+            return
+        if args.config == "c5":
+            res = run_oracle_c5(args.steps, args.warmup)
+            line = {"metric": "block-rows/s (multicolour ILU(0) setup + BiCGSTAB to 1e-8, "
+                              "decoupled 7-point BSR)",
+                    "value": res["value"], "unit": res["unit"], "n_gpus": args.gpus,
+                    "steps": args.steps, "warmup": args.warmup,
+                    "ms_per_step": res["seconds"] * 1e3 / max(1, args.steps),
+                    "higher_is_better": True, "scaling": args.scaling, "vs_baseline": None,
+                    "dtype": "f64", "data": "synthetic (seeded BSR of BASELINE configs[4])",
+                    "impl": "reference", "config": {"workload": res["sample"]},
+                    "algorithm": {"precond": "ras", "bicgstab_iters": res["bicgstab_iters"]},
+                    "cpu_baseline": {k: res[k] for k in ("value", "unit", "cores", "kind",
+                                                         "sample")},
+                    "e2e": {"value": res["value"], "unit": res["unit"], "h2d_bytes_per_step": 0,
+                            "d2h_bytes_per_step": 0}}
+            print(json.dumps(line))
             return
         res = run_oracle(args.steps, args.warmup, args.config)
         case = res["case"]
@@ -715,6 +901,11 @@ def main():
                 "e2e": {"value": res["value"], "unit": UNIT, "h2d_bytes_per_step": 0,
                         "d2h_bytes_per_step": 0}}
         print(json.dumps(line))
+        return
+    if args.config == "c5":
+        out = run_c5(args, rank, world, local)
+        if rank == 0:
+            print(json.dumps(out))
         return
     out, sim = run_ours(args, rank, world, local)
     sim.ctx.close()

@@ -186,6 +186,12 @@ int isc_set_krylov(isc_ctx *ctx, int32_t krylov, int32_t restart);
 /* Generate the seeded synthetic system of BASELINE config 5 in place. */
 int isc_synth_system(isc_ctx *ctx, uint64_t seed);
 
+/* Same, for a z-slab context (grid k_offset = global index of local plane 0)
+ * of a global grid with nz_global planes: every value is keyed by the global
+ * cell index and z-faces follow the global boundary, so each rank holds its
+ * rows of the single-GPU system bit for bit. nz_global <= 0: k_offset + nz. */
+int isc_synth_system_slab(isc_ctx *ctx, uint64_t seed, int32_t nz_global);
+
 /* Well Schur fold, GJ decoupling, preconditioner setup and BiCGSTAB on the
  * current system; d_du (SoA 9 x n) receives the cell update, h_dbhp the
  * nwells bhp updates. Status 2/3/4 as the reference's exceptions; for
@@ -200,6 +206,11 @@ int isc_spmv(isc_ctx *ctx, const double *d_x, double *d_y);
 int isc_precond_apply(isc_ctx *ctx, const double *d_r, double *d_z);
 /* decoupled rhs (after isc_decouple) -> d_dst (9 x n) */
 int isc_copy_rhs(isc_ctx *ctx, double *d_dst);
+
+/* Replace the decoupled right-hand side of a decoupled system (natural order,
+ * SoA (9, n) device array); the next isc_solve refactors. Used by the C5
+ * microbench's host-buffer leg (a new rhs per solve). */
+int isc_set_rhs(isc_ctx *ctx, const double *d_src);
 
 int isc_newton_update(isc_ctx *ctx, double *d_state, const double *d_du, double eps);
 int isc_scaled_norm(isc_ctx *ctx, const double *d_accn, double dt, double *norm);

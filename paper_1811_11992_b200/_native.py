@@ -78,6 +78,7 @@ _SIGS = {
     "isc_set_krylov": (ctypes.c_int, [VP, ctypes.c_int32, ctypes.c_int32]),
     "isc_decoupled_form": (ctypes.c_int, [VP]),
     "isc_synth_system": (ctypes.c_int, [VP, ctypes.c_uint64]),
+    "isc_synth_system_slab": (ctypes.c_int, [VP, ctypes.c_uint64, ctypes.c_int32]),
     "isc_solve": (ctypes.c_int, [VP, ctypes.c_double, ctypes.c_int32, VP, VP,
                                  ctypes.POINTER(ctypes.c_int32), c_int64_p,
                                  ctypes.POINTER(ctypes.c_int32)]),
@@ -86,6 +87,7 @@ _SIGS = {
     "isc_spmv": (ctypes.c_int, [VP, VP, VP]),
     "isc_precond_apply": (ctypes.c_int, [VP, VP, VP]),
     "isc_copy_rhs": (ctypes.c_int, [VP, VP]),
+    "isc_set_rhs": (ctypes.c_int, [VP, VP]),
     "isc_newton_update": (ctypes.c_int, [VP, VP, VP, ctypes.c_double]),
     "isc_scaled_norm": (ctypes.c_int, [VP, VP, ctypes.c_double, c_double_p]),
     "isc_audit_sums": (ctypes.c_int, [VP, VP, VP]),

@@ -154,6 +154,16 @@ def config(name: str, **overrides) -> Case:
             case = replace(base, name=name,
                            wells=(inj, replace(prod, control="rate_total", rate=-10.0, bhp=None)))
         return _apply_overrides(case, overrides)
+    if name == "c5":
+        # BASELINE configs[4]: the linear-solver microbench grid (400x400x100,
+        # 16 M block rows). Only the grid matters: the system is the seeded
+        # synthetic BSR of synth.py / isc_synth_system(_slab), decoupled and
+        # solved with the multicolour ILU(0) + BiCGSTAB to 1e-8.
+        case = Case(name="c5", nx=400, ny=400, nz=100, d=(1.0, 1.0, 1.0), wells=(),
+                    schedule=_fixed_schedule(1, 1.0),
+                    solver=SolverSettings(linear_tol=1e-8, linear_max=1000, precond="mcilu"),
+                    perm=1.0, phi=0.3, nsteps=1)
+        return _apply_overrides(case, overrides)
     if name == "c1":
         nsteps, dt = 50, 5e-4
         case = Case(

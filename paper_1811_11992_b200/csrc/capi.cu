@@ -58,6 +58,7 @@ static thread_local std::string g_err;
 struct isc_ctx {
   Dims g{};
   Model M{};
+  int k_offset = 0;                        // global index of local plane 0 (z-slabs)
   cudaStream_t stream = nullptr;
   cudaStream_t own_stream = nullptr;
   cudaStream_t cstream = nullptr;          // host->device staging copies (isc_assemble_host)
@@ -352,6 +353,7 @@ extern "C" int isc_create(const isc_model_desc* md, const isc_grid_desc* gdsc, i
   g.colored = (g.nx % 2 == 0) ? 1 : 0;
   g.half = g.n / 2;
   g.kpar = gdsc->k_offset & 1;
+  ctx->k_offset = gdsc->k_offset;
   g.tw_lo = 0;
   g.tw_hi = g.half;
   g.ph = g.nxny / 2;
@@ -1008,9 +1010,14 @@ extern "C" int isc_set_precond(isc_ctx* ctx, int32_t precond) {
   return ISC_OK;
 }
 
-extern "C" int isc_synth_system(isc_ctx* ctx, uint64_t seed) {
-  k_synth<<<grid1d(ctx->g.n, 128), 128, 0, ctx->stream>>>(ctx->g, seed, ctx->diag, ctx->offd,
-                                                          ctx->resid);
+extern "C" int isc_synth_system_slab(isc_ctx* ctx, uint64_t seed, int32_t nz_global) {
+  if (nz_global <= 0) nz_global = ctx->k_offset + ctx->g.nz;
+  if (ctx->k_offset < 0 || ctx->k_offset + ctx->g.nz > nz_global) {
+    g_err = "isc_synth_system_slab: local planes outside the global grid";
+    return ISC_BAD_ARGUMENT;
+  }
+  k_synth<<<grid1d(ctx->g.n, 128), 128, 0, ctx->stream>>>(ctx->g, seed, ctx->k_offset, nz_global,
+                                                          ctx->diag, ctx->offd, ctx->resid);
   LAUNCH_CHECK();
   CK(cudaStreamSynchronize(ctx->stream));
   ctx->decoupled = ctx->factored = false;
@@ -1018,6 +1025,10 @@ extern "C" int isc_synth_system(isc_ctx* ctx, uint64_t seed) {
   ctx->offd_rows = NU;
   ctx->assembled = false;
   return ISC_OK;
+}
+
+extern "C" int isc_synth_system(isc_ctx* ctx, uint64_t seed) {
+  return isc_synth_system_slab(ctx, seed, 0);
 }
 
 // ------------------------------------------------------------- decouple
@@ -1130,6 +1141,20 @@ extern "C" int isc_copy_rhs(isc_ctx* ctx, double* d_dst) {
   k_from_pos<double><<<grid1d(ctx->g.n, 256), 256, 0, ctx->stream>>>(ctx->g, NU, ctx->rhs, d_dst);
   LAUNCH_CHECK();
   CK(cudaStreamSynchronize(ctx->stream));
+  return ISC_OK;
+}
+
+// Replace the decoupled right-hand side (natural order, SoA (9, n)) of a
+// decoupled system; the next isc_solve refactors (the multicolour setup also
+// forms the reduced right-hand side from it).
+extern "C" int isc_set_rhs(isc_ctx* ctx, const double* d_src) {
+  if (!ctx->decoupled) {
+    g_err = "isc_set_rhs needs a decoupled system";
+    return ISC_BAD_ARGUMENT;
+  }
+  k_to_pos<double><<<grid1d(ctx->g.n, 256), 256, 0, ctx->stream>>>(ctx->g, NU, d_src, ctx->rhs);
+  LAUNCH_CHECK();
+  ctx->factored = false;
   return ISC_OK;
 }
 

@@ -150,11 +150,16 @@ __device__ __forceinline__ double snormal(uint64_t seed, uint64_t stream, uint64
   return sqrt(-2.0 * log(a)) * cos(6.283185307179586 * b);
 }
 
-__global__ void k_synth(Dims g, uint64_t seed, double* diag, double* offd, double* resid) {
+// On a z-slab (k_offset > 0 or nz < nz_global) every value is keyed by the
+// cell's GLOBAL index and the z-faces by the global grid's boundary, so each
+// rank generates exactly its rows of the single-GPU system.
+__global__ void k_synth(Dims g, uint64_t seed, int k_offset, int nz_global, double* diag,
+                        double* offd, double* resid) {
   const int64_t n = g.n;
-  const int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;   // natural cell (RNG key)
-  if (c >= n) return;
-  const int64_t pc = pos_of(g, c);
+  const int64_t cl = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;   // local natural cell
+  if (cl >= n) return;
+  const int64_t c = cl + (int64_t)k_offset * g.nxny;                   // global cell (RNG key)
+  const int64_t pc = pos_of(g, cl);
   double dmag[NU];
 #pragma unroll
   for (int r = 0; r < NU; ++r) {
@@ -171,9 +176,12 @@ __global__ void k_synth(Dims g, uint64_t seed, double* diag, double* offd, doubl
     resid[(int64_t)r * n + pc] = snormal(seed, 2, (uint64_t)(c * NU + r));
   }
   int i, j, k;
-  cell_ijk(g, c, i, j, k);
+  cell_ijk(g, cl, i, j, k);
+  const int kg = k + k_offset;
   for (int d = 0; d < NDIR; ++d) {
-    const bool has = neighbour(g, c, i, j, k, d) >= 0;
+    const bool has = d == DZM ? kg > 0
+                   : d == DZP ? kg + 1 < nz_global
+                              : neighbour(g, cl, i, j, k, d) >= 0;
 #pragma unroll
     for (int r = 0; r < NU; ++r)
 #pragma unroll
