@@ -69,6 +69,7 @@ struct isc_ctx {
   bool mc_schur = true;   // mcilu: red-eliminated BiCGSTAB (ISC_MCILU_FULL=1: full system)
   int krylov = ISC_KRYLOV_BICGSTAB;   // mcilu red-eliminated system: BiCGSTAB or GMRES(m)
   int gm_m = 30;                      // GMRES restart length (<= GM_MAXV - 1)
+  int bicg_last_iters = 0;            // previous red-eliminated BiCGSTAB count (chunk size)
   double* gm_V = nullptr;             // GMRES basis, gm_m + 1 full-length vectors (lazy)
   double* gm_h = nullptr;             // GMRES device scalars: h (2 x GM_MAXV+1), y
   int64_t launches = 0;
@@ -1187,7 +1188,10 @@ extern "C" int isc_precond_setup(isc_ctx* ctx, int64_t* bad_cell) {
     if (ctx->compact) {
       // the reduced rhs g_b is formed on the way (red neighbours' b: halo on slabs)
       if (cross && halo_exchange(ctx, ctx->rhs, NU)) return ISC_CUDA_ERROR;
-      k_mc_factor_compact<<<grid1d(ctx->g.tw_hi - ctx->g.tw_lo, 32), dim3(32, NU), 0, st>>>(
+      CK(cudaFuncSetAttribute(k_mc_factor_compact, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                              (int)sizeof(McfcSmem)));
+      k_mc_factor_compact<<<grid1d(ctx->g.tw_hi - ctx->g.tw_lo, 32), dim3(32, NU),
+                            sizeof(McfcSmem), st>>>(
           ctx->g, ctx->offd, ctx->diag, ctx->mc_uinv, ctx->cbp, ctx->fail_d, ctx->rhs, ctx->rk,
           ctx->rhat);
       ctx->gb_fresh = true;
@@ -1316,7 +1320,7 @@ static int mc_apply_spmv(isc_ctx* ctx, const double* p, double* phat, double* v,
   {
     KScope ks(ctx, KT_SPMV);
     k_mc_black_spmv<K><<<b1, dim3(32, NU), 0, ctx->stream>>>(g, ctx->offd, phat, v, w0, w1,
-                                                            ctx->partial, b2 + b1, b2);
+                                                            ctx->partial, b2 + b1, b2, nullptr);
   }
   ctx->launches += 3;
   CK(cudaGetLastError());
@@ -1558,18 +1562,22 @@ extern "C" int isc_comm_allreduce_host(isc_ctx* ctx, double* vals, int32_t count
 struct Kry {
   isc_ctx* ctx;
   int64_t len;
+  const double* stop = nullptr;   // device-driven iterations: S_STOP guard of the sums
   int vgrid() const { return RED_BLOCKS; }
   // fixed-order sums: one block for RED_BLOCKS partials, two stages for the
   // per-warp partials of the stencil passes
   template <int K>
   void finalize(int nparts, int s0, int s1) {
     if (nparts <= RED_BLOCKS) {
-      k_finalize<K><<<1, 256, 0, ctx->stream>>>(ctx->partial, nparts, ctx->sc, s0, s1, s1);
+      k_finalize<K><<<1, 256, 0, ctx->stream>>>(ctx->partial, nparts, ctx->sc, s0, s1, s1,
+                                                stop);
       ++ctx->launches;
       return;
     }
-    k_partial_sum<K><<<FIN_BLOCKS, 256, 0, ctx->stream>>>(ctx->partial, nparts, ctx->partial2);
-    k_finalize<K><<<1, 256, 0, ctx->stream>>>(ctx->partial2, FIN_BLOCKS, ctx->sc, s0, s1, s1);
+    k_partial_sum<K><<<FIN_BLOCKS, 256, 0, ctx->stream>>>(ctx->partial, nparts, ctx->partial2,
+                                                          stop);
+    k_finalize<K><<<1, 256, 0, ctx->stream>>>(ctx->partial2, FIN_BLOCKS, ctx->sc, s0, s1, s1,
+                                              stop);
     ctx->launches += 2;
   }
   int finalize1(int nparts, int s0) {
@@ -1749,11 +1757,12 @@ static void sc_rhs_launch(isc_ctx* ctx, const Dims& g, int blocks, const double*
   else
     k_sc_rhs<<<blocks, dim3(32, NU), 0, ctx->stream>>>(g, ctx->offd, b, o1, o2);
 }
-static void sc_red_launch(isc_ctx* ctx, const Dims& g, int blocks, double* z) {
+static void sc_red_launch(isc_ctx* ctx, const Dims& g, int blocks, double* z,
+                          const double* stop = nullptr) {
   if (ctx->compact)
-    k_cc_red<<<blocks, dim3(32, CR), 0, ctx->stream>>>(g, ctx->offd, ctx->ccnz_d, z);
+    k_cc_red<<<blocks, dim3(32, CR), 0, ctx->stream>>>(g, ctx->offd, ctx->ccnz_d, z, stop);
   else
-    k_sc_red<<<blocks, dim3(32, NU), 0, ctx->stream>>>(g, ctx->offd, z);
+    k_sc_red<<<blocks, dim3(32, NU), 0, ctx->stream>>>(g, ctx->offd, z, stop);
 }
 static void sc_xred_launch(isc_ctx* ctx, const Dims& g, int blocks, const double* b, double* x) {
   if (ctx->compact)
@@ -1765,13 +1774,15 @@ static void sc_xred_launch(isc_ctx* ctx, const Dims& g, int blocks, const double
 // black pass with K dot products; per-warp partial slots: stride x rows_per_block()
 template <int K>
 static void sc_black_launch(isc_ctx* ctx, const Dims& g, int blocks, const double* z, double* v,
-                            const double* w0, const double* w1, int stride, int slot0) {
+                            const double* w0, const double* w1, int stride, int slot0,
+                            const double* stop = nullptr) {
   if (ctx->compact)
     k_cc_black<K><<<blocks, dim3(32, CR), 0, ctx->stream>>>(g, ctx->cbp, ctx->diag, z, v, w0, w1,
-                                                            ctx->partial, stride, slot0);
+                                                            ctx->partial, stride, slot0, stop);
   else
     k_mc_black_spmv<K><<<blocks, dim3(32, NU), 0, ctx->stream>>>(g, ctx->offd, z, v, w0, w1,
-                                                                ctx->partial, stride, slot0);
+                                                                ctx->partial, stride, slot0,
+                                                                stop);
 }
 static int sc_warps(const isc_ctx* ctx) { return ctx->compact ? CR : NU; }
 
@@ -1834,28 +1845,28 @@ static int bicgstab_schur(isc_ctx* ctx, double tol, int maxiter, int* iters) {
   const int bl1 = split ? grid1d(gl.tw_hi - gl.tw_lo, 32) : 0;
   const int bh1 = split ? grid1d(gh.tw_hi - gh.tw_lo, 32) : 0;
   const int bparts = split ? bi + bl1 + bh1 : bh;   // black-pass partial slots (blocks)
-  auto red_pass = [&](double* z) -> int {
+  auto red_pass = [&](double* z, const double* stop) -> int {
     if (!split) {
       TRY(halo_exchange(ctx, z, NU));
-      sc_red_launch(ctx, g, bh, z);
+      sc_red_launch(ctx, g, bh, z, stop);
       ++ctx->launches;
       return cudaGetLastError() == cudaSuccess ? 0 : ISC_CUDA_ERROR;
     }
     TRY(halo_start(ctx, z, NU));
-    sc_red_launch(ctx, gi, bi, z);
+    sc_red_launch(ctx, gi, bi, z, stop);
     TRY(halo_finish(ctx, z, NU));
-    sc_red_launch(ctx, gl, bl1, z);
-    sc_red_launch(ctx, gh, bh1, z);
+    sc_red_launch(ctx, gl, bl1, z, stop);
+    sc_red_launch(ctx, gh, bh1, z, stop);
     ctx->launches += 3;
     return cudaGetLastError() == cudaSuccess ? 0 : ISC_CUDA_ERROR;
   };
   auto black_pass = [&](int K, double* z, double* vout, const double* w0,
-                        const double* w1) -> int {
+                        const double* w1, const double* stop) -> int {
     auto launch = [&](const Dims& d, int blocks, int slot0) {
       if (K == 1)
-        sc_black_launch<1>(ctx, d, blocks, z, vout, w0, w1, bparts, slot0);
+        sc_black_launch<1>(ctx, d, blocks, z, vout, w0, w1, bparts, slot0, stop);
       else
-        sc_black_launch<2>(ctx, d, blocks, z, vout, w0, w1, bparts, slot0);
+        sc_black_launch<2>(ctx, d, blocks, z, vout, w0, w1, bparts, slot0, stop);
     };
     if (!split) {
       TRY(halo_exchange(ctx, z, NU));
@@ -1891,8 +1902,8 @@ static int bicgstab_schur(isc_ctx* ctx, double tol, int maxiter, int* iters) {
     // r_b = g_b - S x_b; rhat = r; p = v = 0 (linsolve.py:509-519)
     {
       KScope ks(ctx, KT_SPMV);
-      if (red_pass(x)) return ISC_CUDA_ERROR;   // red part of x: scratch
-      if (black_pass(1, x, t, rhat, nullptr)) return ISC_CUDA_ERROR;
+      if (red_pass(x, nullptr)) return ISC_CUDA_ERROR;   // red part of x: scratch
+      if (black_pass(1, x, t, rhat, nullptr, nullptr)) return ISC_CUDA_ERROR;
       sc_rhs_launch(ctx, g, bh, b, v, shat);   // g_b (scratch)
     }
     k_sc_sub<<<RED_BLOCKS, RED_THREADS, 0, st>>>(g, v, t, r, rhat);
@@ -1904,104 +1915,133 @@ static int bicgstab_schur(isc_ctx* ctx, double tol, int maxiter, int* iters) {
     restarted = true;
     return cudaGetLastError() == cudaSuccess ? 0 : ISC_CUDA_ERROR;
   };
-  while (it < maxiter) {
-    ++it;
-    double rho = sh[S_RHO_NEW];
-    const double omega = sh[S_OMEGA];
-    if (std::fabs(rho) < brk || (!first && omega == 0.0)) {
-      if (restarted) { g_err = "BiCGSTAB scalar breakdown at iteration " + std::to_string(it); *iters = it; return ISC_BREAKDOWN; }
-      TRY(restart());
-      TRY(K.push());
-      TRY(dot_b(rhat, r, S_RHO_NEW));
-      TRY(K.read_scalars());
-      rho = sh[S_RHO_NEW];
-      if (std::fabs(rho) < brk) { g_err = "BiCGSTAB restart found a null residual"; *iters = it; return ISC_BREAKDOWN; }
-    }
-    sh[S_RHO] = rho;
-    sh[S_FIRST] = first ? 1.0 : 0.0;
-    first = false;
-    TRY(K.push());
+  // Device-driven iterations: the scalar logic runs in k_bicg_* between the
+  // vector kernels and every kernel returns at once after S_STOP is set, so
+  // chunks of iterations are enqueued without a host round trip (the
+  // host-driven form synchronised twice per iteration). The first chunk is
+  // sized from the previous solve's count, then two at a time. The host
+  // handles each stop code exactly as linsolve.py:500-578 branches.
+  // (After a stop, the skipped finalize kernels leave their slots alone but
+  // a multi-rank all-reduce still sums them again; only slots the next
+  // restart or iteration recomputes are affected.)
+  double* stop = ctx->sc + S_STOP;
+  K.stop = stop;
+  sh[S_STOP] = STOP_RUN;
+  sh[S_IT] = 0.0;
+  sh[S_MAXIT] = (double)maxiter;
+  sh[S_NB] = nb;
+  sh[S_TOL] = tol;
+  sh[S_BRK] = brk;
+  TRY(K.push());
+  auto enqueue_iteration = [&]() -> int {
+    k_bicg_top<<<1, 1, 0, st>>>(ctx->sc);
     {
       KScope ks(ctx, KT_VEC);
-      k_sc_update_p<<<RED_BLOCKS, RED_THREADS, 0, st>>>(g, r, p, v, uinv, phat, ctx->sc);
+      k_sc_update_p<<<RED_BLOCKS, RED_THREADS, 0, st>>>(g, r, p, v, uinv, phat, ctx->sc, stop);
     }
-    ++ctx->launches;   // update_p
     {
       KScope ks(ctx, KT_ILU_APPLY);
-      TRY(red_pass(phat));
+      TRY(red_pass(phat, stop));
     }
     {
       KScope ks(ctx, KT_SPMV);
-      TRY(black_pass(1, phat, v, rhat, nullptr));
+      TRY(black_pass(1, phat, v, rhat, nullptr, stop));
     }
     CK(cudaGetLastError());
     TRY(K.finalize1(bparts * sc_warps(ctx), S_DEN));
+    k_bicg_den<<<1, 1, 0, st>>>(ctx->sc);
     {
       KScope ks(ctx, KT_VEC);
       k_sc_update_s<<<RED_BLOCKS, RED_THREADS, 0, st>>>(g, r, v, s, uinv, shat, ctx->sc,
-                                                        ctx->partial);
+                                                        ctx->partial, stop);
     }
-    ++ctx->launches;
     TRY(K.finalize1(RED_BLOCKS, S_SS));
-    TRY(K.read_scalars());
-    const double den = sh[S_DEN];
-    if (std::fabs(den) < brk) {
-      if (restarted) { g_err = "BiCGSTAB denominator breakdown at iteration " + std::to_string(it); *iters = it; return ISC_BREAKDOWN; }
-      TRY(restart());
-      TRY(K.push());
-      TRY(dot_b(rhat, r, S_RHO_NEW));
-      TRY(K.read_scalars());
-      continue;
-    }
-    sh[S_ALPHA] = rho / den;
-    if (std::sqrt(sh[S_SS]) / nb <= tol) {
-      TRY(K.push());
-      k_sc_axpy_alpha<<<RED_BLOCKS, RED_THREADS, 0, st>>>(g, x, phat, ctx->sc);
-      ++ctx->launches;
-      TRY(finish());
-      *iters = it;
-      CK(cudaStreamSynchronize(st));
-      return ISC_OK;
-    }
-    TRY(K.push());
+    k_bicg_ss<<<1, 1, 0, st>>>(ctx->sc);
     {
       KScope ks(ctx, KT_ILU_APPLY);
-      TRY(red_pass(shat));
+      TRY(red_pass(shat, stop));
     }
     {
       KScope ks(ctx, KT_SPMV);
-      TRY(black_pass(2, shat, t, nullptr, s));
+      TRY(black_pass(2, shat, t, nullptr, s, stop));
     }
     CK(cudaGetLastError());
     TRY(K.finalize2(bparts * sc_warps(ctx), S_TT, S_TS));
     {
       KScope ks(ctx, KT_VEC);
       k_sc_update_xr<<<RED_BLOCKS, RED_THREADS, 0, st>>>(g, x, phat, shat, r, s, t, rhat,
-                                                         ctx->sc, ctx->partial);
+                                                         ctx->sc, ctx->partial, stop);
     }
-    ++ctx->launches;
     TRY(K.finalize2(RED_BLOCKS, S_RR, S_RHO_NEW));
+    k_bicg_end<<<1, 1, 0, st>>>(ctx->sc);
+    ctx->launches += 7;   // 3 vector updates + 4 control kernels (passes and sums count themselves)
+    return cudaGetLastError() == cudaSuccess ? 0 : ISC_CUDA_ERROR;
+  };
+  // a restart by the host: device state -> sh, restart, new rho, state -> HBM
+  auto host_restart = [&]() -> int {
+    sh[S_STOP] = STOP_RUN;
+    K.stop = nullptr;
+    TRY(K.push());
+    TRY(restart());
+    sh[S_FIRST] = 1.0;
+    TRY(K.push());
+    TRY(dot_b(rhat, r, S_RHO_NEW));
     TRY(K.read_scalars());
-    const double tt = sh[S_TT];
-    if (tt == 0.0) {
-      if (restarted) { g_err = "BiCGSTAB stagnated (t = 0)"; *iters = it; return ISC_BREAKDOWN; }
-      TRY(restart());
+    K.stop = stop;
+    return 0;
+  };
+  int chunk = std::max(1, std::min(16, ctx->bicg_last_iters > 0 ? ctx->bicg_last_iters - 1 : 4));
+  for (;;) {
+    for (int c = 0; c < chunk; ++c) TRY(enqueue_iteration());
+    TRY(K.read_scalars());
+    chunk = 2;
+    const int code = (int)sh[S_STOP];
+    it = (int)sh[S_IT];
+    if (code == STOP_RUN) continue;
+    *iters = it;
+    ctx->bicg_last_iters = it;
+    if (code == STOP_CONV_S) {   // ||s|| / ||b|| <= tol: x += alpha phat (linsolve.py:550-552)
+      sh[S_STOP] = STOP_RUN;
       TRY(K.push());
-      TRY(dot_b(rhat, r, S_RHO_NEW));
-      TRY(K.read_scalars());
-      continue;
-    }
-    sh[S_OMEGA] = sh[S_TS] / tt;
-    if (std::sqrt(sh[S_RR]) / nb <= tol) {
+      k_sc_axpy_alpha<<<RED_BLOCKS, RED_THREADS, 0, st>>>(g, x, phat, ctx->sc);
+      ++ctx->launches;
       TRY(finish());
-      *iters = it;
+      CK(cudaStreamSynchronize(st));
       return ISC_OK;
     }
-    sh[S_RHO_OLD] = rho;
+    if (code == STOP_CONV) {
+      sh[S_STOP] = STOP_RUN;
+      TRY(K.push());
+      TRY(finish());
+      return ISC_OK;
+    }
+    if (code == STOP_MAXIT) {
+      sh[S_STOP] = STOP_RUN;
+      TRY(K.push());
+      g_err = "BiCGSTAB did not converge";
+      return ISC_MAX_ITERATIONS;
+    }
+    if (restarted) {
+      sh[S_STOP] = STOP_RUN;
+      TRY(K.push());
+      g_err = code == STOP_TOP ? "BiCGSTAB scalar breakdown at iteration " + std::to_string(it)
+            : code == STOP_DEN ? "BiCGSTAB denominator breakdown at iteration " + std::to_string(it)
+                               : std::string("BiCGSTAB stagnated (t = 0)");
+      return ISC_BREAKDOWN;
+    }
+    TRY(host_restart());   // the single restart from the current iterate
+    if (code == STOP_TOP) {
+      // restart at the loop head: the same iteration continues with the new
+      // rho (linsolve.py:509-522) -- the next k_bicg_top counts it again
+      if (std::fabs(sh[S_RHO_NEW]) < brk) {
+        g_err = "BiCGSTAB restart found a null residual";
+        return ISC_BREAKDOWN;
+      }
+      sh[S_IT] = it - 1;
+      TRY(K.push());
+    }
+    chunk = 1;
   }
-  *iters = it;
-  g_err = "BiCGSTAB did not converge";
-  return ISC_MAX_ITERATIONS;
 }
 
 // Restarted right-preconditioned GMRES(m) on the red-eliminated system

@@ -140,6 +140,19 @@ __global__ void __launch_bounds__(32 * NU, DCC_MINB) k_decouple_compact(Dims g, 
 // pivot rule, tolerance, scaling by the reciprocal and elimination order as
 // k_decouple_compact, so the same values; no shared memory and no barriers
 // (the column-per-thread form is barrier- and issue-bound).
+// cp.async (LDGSTS): global -> shared without register staging
+__device__ __forceinline__ void cp_async8(void* smem, const void* gmem) {
+  const unsigned sa = (unsigned)__cvta_generic_to_shared(smem);
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(sa), "l"(gmem) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() {
+  asm volatile("cp.async.commit_group;\n" ::: "memory");
+}
+template <int N>
+__device__ __forceinline__ void cp_async_wait() {
+  asm volatile("cp.async.wait_group %0;\n" ::"n"(N) : "memory");
+}
+
 #ifndef DCT_THREADS
 #define DCT_THREADS 128
 #endif
@@ -376,7 +389,9 @@ __global__ void __launch_bounds__(32 * CR, CP_MINB) k_cc_spmv(CP_ARGS) {
 // BiCGSTAB's breakdown / tolerance tests see it one dot product later).
 __global__ void __launch_bounds__(32 * CR, CC_MINB) k_cc_red(Dims g, const double* __restrict__ offd,
                                                              const int* __restrict__ ccnz,
-                                                             double* __restrict__ z) {
+                                                             double* __restrict__ z,
+                                                             const double* stop) {
+  if (stopped(stop)) return;
   const int64_t n = g.n;
   const int ls = threadIdx.x, r = threadIdx.y;
   const int64_t t = g.tw_lo + (int64_t)blockIdx.x * 32 + ls;
@@ -408,7 +423,8 @@ template <int K>
 __global__ void __launch_bounds__(32 * CR, CC_MINB) k_cc_black(
     Dims g, const double* __restrict__ bp, const double* __restrict__ dinv,
     const double* __restrict__ z, double* __restrict__ v, const double* __restrict__ w0,
-    const double* __restrict__ w1, double* partial, int stride, int slot0) {
+    const double* __restrict__ w1, double* partial, int stride, int slot0, const double* stop) {
+  if (stopped(stop)) return;   // block-uniform: before the barrier
   __shared__ double ts[CR][32];
   const int64_t n = g.n;
   const int ls = threadIdx.x, r = threadIdx.y;
@@ -472,17 +488,36 @@ __global__ void __launch_bounds__(32 * CR, CC_MINB) k_cc_black(
 // is formed on the way (the blocks are in shared memory anyway) and written
 // to g1 and g2. Thread (black cell lane, column u).
 #ifndef MCFC_MINB
-#define MCFC_MINB 3   // C4 sweep 2..4: 4.06 / 3.51 / 3.46 ms (4 spills once g_b is folded in)
+#define MCFC_MINB 2   // two CTAs per SM: the double-buffered stages take ~99 KB of smem each
 #endif
+// Direction tiles are double-buffered with cp.async (LDGSTS: global -> shared
+// without register staging): the loads of direction d+1 -- B_bd rows, the red
+// neighbour's D^-1[:, :CR] and back block rows, its b -- are in flight while
+// direction d is multiplied, so the six directions' HBM round trips overlap
+// the products instead of alternating with them (round 1: one exposed round
+// trip per tile and 2.8 TB/s).
+struct McfcStage {
+  double b[CR][NU][32];      // B_bd flux rows of the black cell
+  double d[NU][CR][32];      // D_nb^-1[:, :CR] of the red neighbour
+  double o[CR][NU][32];      // B_nb,back flux rows (the red neighbour's block pointing back)
+  double r[NU][32];          // b(nb): the red neighbour's decoupled rhs
+};
+struct McfcSmem {
+  McfcStage st[2];
+  double bpsh[CR][CR][32];   // B'_bd = B_bd[:CR, :] D_nb^-1[:, :CR]
+  double colk[NU][32];
+  int pivs[32];
+};
+
 __global__ void __launch_bounds__(32 * NU, MCFC_MINB) k_mc_factor_compact(
     Dims g, const double* __restrict__ offd, const double* __restrict__ dinv,
     double* __restrict__ uinv, double* __restrict__ bp, int* fail, const double* __restrict__ b,
     double* __restrict__ g1, double* __restrict__ g2) {
-  __shared__ double bsh[CR][NU][32];    // B_bd flux rows of the black cell
-  __shared__ double dsh[NU][CR][32];    // D_nb^-1[:, :CR] of the red neighbour
-  __shared__ double bpsh[CR][CR][32];   // B'_bd = B_bd[:CR, :] D_nb^-1[:, :CR]
-  __shared__ double colk[NU][32];
-  __shared__ int pivs[32];
+  extern __shared__ __align__(16) unsigned char mcfc_raw[];
+  McfcSmem& S = *reinterpret_cast<McfcSmem*>(mcfc_raw);
+  auto& bpsh = S.bpsh;
+  auto& colk = S.colk;
+  auto& pivs = S.pivs;
   const int64_t n = g.n;
   const int ls = threadIdx.x, u = threadIdx.y;
   const int64_t t = g.tw_lo + (int64_t)blockIdx.x * 32 + ls;
@@ -491,29 +526,44 @@ __global__ void __launch_bounds__(32 * NU, MCFC_MINB) k_mc_factor_compact(
   int i = 0, j = 0, k = 0;
   const int64_t cell = in ? locate(g, c, i, j, k) : 0;
   const bool live = in && owned_k(g, k);
+  int64_t nbs[NDIR];
+#pragma unroll
+  for (int d = 0; d < NDIR; ++d) nbs[d] = live ? nb_pos(g, cell, i, j, k, d) : -1;
+  // issue direction d's tiles into stage s (6 + 6 + 6 B_bd / D^-1 / back
+  // values per thread, b(nb)[u] by every thread)
+  auto issue = [&](int d, int sidx) {
+    const int64_t nb = nbs[d];
+    if (nb < 0) return;
+    McfcStage& T = S.st[sidx];
+#pragma unroll
+    for (int e = 0; e < CR; ++e) {
+      const int idx = u * CR + e;   // 0..53
+      const int br = idx / NU, bu = idx % NU;
+      cp_async8(&T.b[br][bu][ls], offd + (int64_t)((d * NU + br) * NU + bu) * n + c);
+      const int dq = idx / CR, dr = idx % CR;
+      cp_async8(&T.d[dq][dr][ls], dinv + (int64_t)(dq * CR + dr) * n + nb);
+      cp_async8(&T.o[e][u][ls], offd + (int64_t)((opposite(d) * NU + e) * NU + u) * n + nb);
+    }
+    if (g1) cp_async8(&T.r[u][ls], b + (int64_t)u * n + nb);
+  };
   double grow = 0.0;   // (sum_d B_bd b_r(nb))[u], u < CR
   double qcol[CR];   // Q[:, u] = sum_d B'_bd B_back[:CR, u]
 #pragma unroll
   for (int q = 0; q < CR; ++q) qcol[q] = 0.0;
+  issue(0, 0);
+  cp_async_commit();
 #pragma unroll 1
   for (int d = 0; d < NDIR; ++d) {
-    const int64_t nb = live ? nb_pos(g, cell, i, j, k, d) : -1;
-    if (nb >= 0) {
-      // cooperative loads: 54 values of B_bd and of D_nb^-1, 6 per thread
-#pragma unroll
-      for (int e = 0; e < CR; ++e) {
-        const int idx = u * CR + e;   // 0..53
-        const int br = idx / NU, bu = idx % NU;
-        bsh[br][bu][ls] = offd[(int64_t)((d * NU + br) * NU + bu) * n + c];
-        const int dq = idx / CR, dr = idx % CR;
-        dsh[dq][dr][ls] = dinv[(int64_t)(dq * CR + dr) * n + nb];
-      }
-    }
+    if (d + 1 < NDIR) issue(d + 1, (d + 1) & 1);
+    cp_async_commit();   // (possibly empty group: keeps the wait count uniform)
+    cp_async_wait<1>();
     __syncthreads();
+    const McfcStage& T = S.st[d & 1];
+    const int64_t nb = nbs[d];
     if (g1 && nb >= 0 && u < CR) {
       double s = 0.0;
 #pragma unroll
-      for (int a = 0; a < NU; ++a) s += bsh[u][a][ls] * b[(int64_t)a * n + nb];
+      for (int a = 0; a < NU; ++a) s += T.b[u][a][ls] * T.r[a][ls];
       grow += s;
     }
     if (nb >= 0) {   // B'_bd: 36 entries, 4 per thread; kept for the black passes
@@ -524,7 +574,7 @@ __global__ void __launch_bounds__(32 * NU, MCFC_MINB) k_mc_factor_compact(
           const int q = idx / CR, s2 = idx % CR;
           double s = 0.0;
 #pragma unroll
-          for (int a = 0; a < NU; ++a) s += bsh[q][a][ls] * dsh[a][s2][ls];
+          for (int a = 0; a < NU; ++a) s += T.b[q][a][ls] * T.d[a][s2][ls];
           bpsh[q][s2][ls] = s;
           bp[(int64_t)((d * CR + q) * CR + s2) * g.half + t] = s;
         }
@@ -532,20 +582,18 @@ __global__ void __launch_bounds__(32 * NU, MCFC_MINB) k_mc_factor_compact(
     }
     __syncthreads();
     if (nb >= 0) {   // Q[:, u] += B'_bd B_back[:CR, u]
-      const double* Bo = offd + (int64_t)(opposite(d) * NB + u) * n + nb;   // column u
-      double bc[CR];
-#pragma unroll
-      for (int r = 0; r < CR; ++r) bc[r] = Bo[(int64_t)(r * NU) * n];
 #pragma unroll
       for (int q = 0; q < CR; ++q) {
         double s = 0.0;
 #pragma unroll
-        for (int r = 0; r < CR; ++r) s += bpsh[q][r][ls] * bc[r];
+        for (int r = 0; r < CR; ++r) s += bpsh[q][r][ls] * T.o[r][u][ls];
         qcol[q] += s;
       }
     }
-    __syncthreads();
+    __syncthreads();   // stage d & 1 is refilled by the next iteration's issue
   }
+  cp_async_wait<0>();
+  auto& dsh = S.st[0].d;
   // U[:, u] = e_u - D_b^-1[:, :CR] Q[:, u]
   if (in) {
 #pragma unroll
@@ -577,12 +625,12 @@ __global__ void __launch_bounds__(32 * NU, MCFC_MINB) k_mc_factor_compact(
     double m = 0.0;
 #pragma unroll
     for (int r = 0; r < NU; ++r) m = fmax(m, fabs(ucol[r]));
-    bsh[0][u][ls] = m;
+    S.st[1].b[0][u][ls] = m;
   }
   __syncthreads();
   double amax = 0.0;
 #pragma unroll
-  for (int q = 0; q < NU; ++q) amax = fmax(amax, bsh[0][q][ls]);
+  for (int q = 0; q < NU; ++q) amax = fmax(amax, S.st[1].b[0][q][ls]);
   const double tol = 1e-13 * amax;
   __syncthreads();
 #pragma unroll

@@ -30,8 +30,18 @@ constexpr int RED_THREADS = 256;
 // Krylov scalar slots in device memory (host mirror reads them)
 enum {
   S_RHO = 0, S_RHO_OLD, S_ALPHA, S_OMEGA, S_DEN, S_SS, S_TT, S_TS, S_RR, S_RHO_NEW, S_BB,
-  S_FIRST, S_NSCAL
+  S_FIRST,
+  // device-driven BiCGSTAB (bicgstab_schur): control state kept in HBM
+  S_STOP, S_IT, S_MAXIT, S_NB, S_TOL, S_BRK,
+  S_NSCAL
 };
+// S_STOP codes: why the device-driven iteration stopped (0 = running)
+enum { STOP_RUN = 0, STOP_TOP = 1, STOP_DEN = 2, STOP_CONV_S = 3, STOP_TT = 4, STOP_CONV = 5,
+       STOP_MAXIT = 6 };
+
+// every kernel of a device-driven iteration returns at once when `stop`
+// (nullable: host-driven callers) holds a nonzero code
+__device__ __forceinline__ bool stopped(const double* stop) { return stop && *stop != 0.0; }
 
 template <int K>
 __device__ __forceinline__ void block_reduce_store(double (&v)[K], double* partial) {
@@ -79,7 +89,9 @@ __device__ __forceinline__ void warp_store_at(double (&v)[K], double* partial, i
 // chunk b of each of the K partial arrays into out[k*gridDim.x + b]
 template <int K>
 __global__ void __launch_bounds__(256) k_partial_sum(const double* __restrict__ partial,
-                                                     int64_t nparts, double* __restrict__ out) {
+                                                     int64_t nparts, double* __restrict__ out,
+                                                     const double* stop) {
+  if (stopped(stop)) return;
   __shared__ double sh[K][8];
   const int t = threadIdx.x, lane = t & 31, w = t >> 5;
   const int64_t chunk = (nparts + gridDim.x - 1) / gridDim.x;
@@ -107,7 +119,9 @@ __global__ void __launch_bounds__(256) k_partial_sum(const double* __restrict__ 
 // sum the per-block partials in fixed order into sc[slot_k] (256 threads)
 template <int K>
 __global__ void __launch_bounds__(256) k_finalize(const double* __restrict__ partial, int nparts,
-                                                  double* sc, int s0, int s1, int s2) {
+                                                  double* sc, int s0, int s1, int s2,
+                                                  const double* stop) {
+  if (stopped(stop)) return;
   const int slots[3] = {s0, s1, s2};
   __shared__ double sh[K][8];
   const int t = threadIdx.x, lane = t & 31, w = t >> 5;
@@ -819,7 +833,8 @@ __global__ void __launch_bounds__(32 * NU, MC_MINB) k_mc_black_spmv(Dims g, cons
                                                            const double* __restrict__ w0,
                                                            const double* __restrict__ w1,
                                                            double* partial, int stride,
-                                                           int slot0) {
+                                                           int slot0, const double* stop) {
+  if (stopped(stop)) return;
   const int64_t n = g.n;
   const int ls = threadIdx.x, r = threadIdx.y;
   const int64_t t = g.tw_lo + (int64_t)blockIdx.x * 32 + ls;   // t-th black cell (owned)
@@ -869,7 +884,9 @@ __global__ void __launch_bounds__(32 * NU, MC_MINB) k_mc_black_spmv(Dims g, cons
 
 // red pass: z_r = -sum_d B_rd z_b(nb)  (z holds z_b at black positions)
 __global__ void __launch_bounds__(32 * NU, MC_MINB) k_sc_red(Dims g, const double* __restrict__ offd,
-                                                              double* __restrict__ z) {
+                                                              double* __restrict__ z,
+                                                              const double* stop) {
+  if (stopped(stop)) return;
   const int64_t n = g.n;
   const int ls = threadIdx.x, r = threadIdx.y;
   const int64_t t = g.tw_lo + (int64_t)blockIdx.x * 32 + ls;   // owned planes only
@@ -959,7 +976,9 @@ __global__ void __launch_bounds__(RED_THREADS, VEC_MINB) k_sc_update_p(Dims g, c
                                                              const double* __restrict__ v,
                                                              const double* __restrict__ uinv,
                                                              double* __restrict__ z,
-                                                             const double* __restrict__ sc) {
+                                                             const double* __restrict__ sc,
+                                                             const double* stop) {
+  if (stopped(stop)) return;
   const int64_t n = g.n;
   const bool first = sc[S_FIRST] != 0.0;
   const double beta = (sc[S_RHO] / sc[S_RHO_OLD]) * (sc[S_ALPHA] / sc[S_OMEGA]);
@@ -995,7 +1014,8 @@ __global__ void __launch_bounds__(RED_THREADS, VEC_MINB) k_sc_update_s(Dims g, c
                                                              const double* __restrict__ uinv,
                                                              double* __restrict__ sh,
                                                              const double* __restrict__ sc,
-                                                             double* partial) {
+                                                             double* partial, const double* stop) {
+  if (stopped(stop)) return;
   const int64_t n = g.n;
   const double alpha = sc[S_RHO] / sc[S_DEN];
   double acc[1] = {0.0};
@@ -1035,7 +1055,9 @@ __global__ void __launch_bounds__(RED_THREADS, VEC_MINB) k_sc_update_xr(Dims g, 
                                                               const double* __restrict__ s,
                                                               const double* __restrict__ t_,
                                                               const double* __restrict__ rhat,
-                                                              const double* sc, double* partial) {
+                                                              const double* sc, double* partial,
+                                                              const double* stop) {
+  if (stopped(stop)) return;
   const int64_t n = g.n;
   const double tt = sc[S_TT];
   double acc[2] = {0.0, 0.0};
@@ -1059,6 +1081,43 @@ __global__ void __launch_bounds__(RED_THREADS, VEC_MINB) k_sc_update_xr(Dims g, 
     }
   }
   block_reduce_store<2>(acc, partial);
+}
+
+// Device-driven BiCGSTAB control (one thread each): the scalar logic of
+// linsolve.py:500-575 evaluated in HBM between the vector kernels, so a
+// chunk of iterations runs without a host round trip. Any exit -- a
+// breakdown test, the tolerance, the iteration limit -- only sets S_STOP;
+// the host reads it after the chunk and runs the branch (restart, Breakdown,
+// MaxIterations, final update) exactly as the host-driven loop does.
+__global__ void k_bicg_top(double* sc) {     // loop head: it += 1; rho / omega tests
+  if (sc[S_STOP] != 0.0) return;
+  if (sc[S_IT] >= sc[S_MAXIT]) { sc[S_STOP] = STOP_MAXIT; return; }
+  sc[S_IT] += 1.0;
+  const double rho = sc[S_RHO_NEW];
+  if (fabs(rho) < sc[S_BRK] || (sc[S_FIRST] == 0.0 && sc[S_OMEGA] == 0.0)) {
+    sc[S_STOP] = STOP_TOP;
+    return;
+  }
+  sc[S_RHO] = rho;
+}
+__global__ void k_bicg_den(double* sc) {     // after r^.v: denominator test, alpha
+  if (sc[S_STOP] != 0.0) return;
+  const double den = sc[S_DEN];
+  if (fabs(den) < sc[S_BRK]) { sc[S_STOP] = STOP_DEN; return; }
+  sc[S_ALPHA] = sc[S_RHO] / den;
+}
+__global__ void k_bicg_ss(double* sc) {      // after ||s||: early convergence
+  if (sc[S_STOP] != 0.0) return;
+  if (sqrt(sc[S_SS]) / sc[S_NB] <= sc[S_TOL]) sc[S_STOP] = STOP_CONV_S;
+}
+__global__ void k_bicg_end(double* sc) {     // after t.t, t.s, ||r||, r^.r
+  if (sc[S_STOP] != 0.0) return;
+  const double tt = sc[S_TT];
+  if (tt == 0.0) { sc[S_STOP] = STOP_TT; return; }
+  sc[S_OMEGA] = sc[S_TS] / tt;
+  if (sqrt(sc[S_RR]) / sc[S_NB] <= sc[S_TOL]) { sc[S_STOP] = STOP_CONV; return; }
+  sc[S_RHO_OLD] = sc[S_RHO];
+  sc[S_FIRST] = 0.0;
 }
 
 // black-half helpers: x_b += alpha phat_b;  out_b = a_b - b_b;  dot over black rows
