@@ -140,16 +140,6 @@ int isc_assemble_host(isc_ctx *ctx, const double *h_p, const double *h_x, const 
 /* du of the last isc_solve (called with d_du == NULL) as host (n, 9). */
 int isc_download_du(isc_ctx *ctx, double *h_du);
 
-/* Same inputs/outputs as isc_assemble, with the well Schur fold and the
- * Gauss-Jordan decoupling fused into the face kernel (the un-decoupled
- * blocks are not kept; isc_export_system is not available afterwards).
- * The following isc_solve skips its decoupling step and reports a singular
- * block found here. */
-int isc_assemble_decoupled(isc_ctx *ctx, const double *d_state, const double *h_bhp,
-                           const double *d_accn, double dt, double t_new,
-                           const uint8_t *h_capped, int32_t freeze, double *h_wells_out,
-                           int64_t *bad_cell);
-
 /* JACOBIAN numeric (assembly.py:593-597, 843-939; replaces the reference's
  * _numeric_jacobian): every Jacobian block and the well rows (wrow), bhp
  * columns (bcol) and dwdb of the last isc_assemble / isc_assemble_host are

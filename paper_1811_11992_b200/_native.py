@@ -64,8 +64,6 @@ _SIGS = {
     "isc_block_size": (ctypes.c_int, []),
     "isc_assemble": (ctypes.c_int, [VP, VP, VP, VP, ctypes.c_double, ctypes.c_double, VP,
                                     ctypes.c_int32, VP, c_int64_p]),
-    "isc_assemble_decoupled": (ctypes.c_int, [VP, VP, VP, VP, ctypes.c_double, ctypes.c_double,
-                                              VP, ctypes.c_int32, VP, c_int64_p]),
     "isc_assemble_host": (ctypes.c_int, [VP, VP, VP, VP, VP, VP, VP, VP, VP, VP, ctypes.c_double,
                                          ctypes.c_double, VP, ctypes.c_int32, VP, c_int64_p]),
     "isc_download_du": (ctypes.c_int, [VP, VP]),

@@ -81,13 +81,10 @@ struct CellSinkProbe {
   __device__ double f(int k) const { return v[k]; }   // record accessor (flux, wells)
 };
 
-#ifndef CELL_GAS_SPLIT
-#define CELL_GAS_SPLIT 1   // split cell pass: the gas phase in its own kernel (k_cell_gas)
-#endif
 // The property half of the split cell pass: the record and the values the
 // reaction / accumulation rows need (A.mid), nothing else.
 struct CellSinkProps {
-  static constexpr bool kMidOut = true, kUnroll = false, kSplitGas = CELL_GAS_SPLIT;
+  static constexpr bool kMidOut = true, kUnroll = false, kSplitGas = true;   // the gas phase runs in k_cell_gas
   const CellArgs& A;
   int64_t n, c;
   __device__ double& rec(int f) { return A.rec[(int64_t)f * n + c]; }
@@ -802,23 +799,9 @@ __device__ __forceinline__ void cell_eval(const Model& M, const CellArgs& A, int
   }
 }
 
-#ifndef CELL_MINB
-#define CELL_MINB 6   // 85 registers + spills beat 255 registers at 2 blocks (C4 sweep 1..8)
-#endif
-__global__ void __launch_bounds__(128, CELL_MINB) k_cell(const Model M, const CellArgs A) {
-  const int64_t n = A.g.n;
-  const int64_t c = A.c_begin + (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (c >= A.c_end) return;
-  double u_[NU];
-#pragma unroll
-  for (int u = 0; u < NU; ++u) u_[u] = A.st[u * n + c];
-  CellSinkGlobal s{A, n, c};
-  cell_eval(M, A, c, u_, s);
-}
-
-// The same cell pass split in two kernels with fewer live values each: the
-// properties (record + A.mid) and then the reaction / accumulation rows
-// (cell_rows over the stored values). Same arithmetic, same results.
+// The cell pass in three kernels with fewer live values each: the
+// properties (record + A.mid), the gas phase, then the reaction /
+// accumulation rows (cell_rows over the stored values).
 #ifndef CELLP_MINB
 #define CELLP_MINB 7   // C4 sweep 4..12 (rows at 2): 8 best before the gas split, 6-7 after
 #endif
@@ -1152,83 +1135,9 @@ __device__ __forceinline__ void face_row(const CellView& A_, const CellView& B_,
   }
 }
 
-// Residual row ROW of one cell: walks the six faces in the reference's
-// gather order, accumulating the cell's own derivative into the diagonal row
-// and writing the neighbour's into the off-diagonal block row. The row is a
-// template parameter so each warp (one row) runs code with only its own
-// phases' terms — far fewer live registers than one body for all rows.
-template <int ROW>
-__device__ __forceinline__ void face_cell_row(const FaceArgs& F, int64_t c, int64_t cell, int i,
-                                              int j, int k) {
-  const int64_t n = F.g.n;
-  // no flux terms in the constraint/coke rows: resid/diag rows unchanged and
-  // their off-diagonal rows are structural zeros, never written (the
-  // decoupling reads only rows < ROW_OS of an assembled system; exports
-  // materialise the zeros)
-  if (ROW == ROW_OS || ROW == ROW_GS || ROW == ROW_CK) return;
-  double res = F.resid[ROW * n + c];
-  double drow[NU];
-#pragma unroll
-  for (int u = 0; u < NU; ++u) drow[u] = F.diag[(int64_t)(ROW * NU + u) * n + c];
-#pragma unroll 1
-  for (int d = 0; d < NDIR; ++d) {
-    const int64_t nb = nb_pos(F.g, cell, i, j, k, d);
-    double* orow = F.offd + (int64_t)((d * NU + ROW) * NU) * n + c;
-    if (nb < 0) {
-#pragma unroll
-      for (int u = 0; u < NU; ++u) orow[(int64_t)u * n] = 0.0;
-      continue;
-    }
-    const bool c_is_a = d >= DXP;
-    const int64_t a = c_is_a ? c : nb, b = c_is_a ? nb : c;
-    const int axis = c_is_a ? d - DXP : 2 - d;   // -z->2, -y->1, -x->0
-    const CellView Av{F.rec, n, a}, Bv{F.rec, n, b};
-    double flux, dfa[NU], dfb[NU];
-    face_row<ROW>(Av, Bv, F.st, n, a, b, F.depth[a], F.depth[b], F.gd[axis * n + a],
-                  F.td[axis * n + a], F.upw + (int64_t)axis * 3 * n, n, F.freeze,
-                  c_is_a && ROW == 0, flux, dfa, dfb);
-    if (c_is_a) {
-      res += flux;
-#pragma unroll
-      for (int u = 0; u < NU; ++u) { drow[u] += dfa[u]; orow[(int64_t)u * n] = dfb[u]; }
-    } else {
-      res -= flux;
-#pragma unroll
-      for (int u = 0; u < NU; ++u) { drow[u] -= dfb[u]; orow[(int64_t)u * n] = -dfa[u]; }
-    }
-  }
-  F.resid[ROW * n + c] = res;
-#pragma unroll
-  for (int u = 0; u < NU; ++u) F.diag[(int64_t)(ROW * NU + u) * n + c] = drow[u];
-}
-
-#ifndef FACE_MINB
-#define FACE_MINB 3
-#endif
-
-// grid: (ceil(n/32), 1); block: (32, NU) -> threadIdx.y = residual row
-__global__ void __launch_bounds__(32 * NU, FACE_MINB) k_face(const FaceArgs F) {
-  const int64_t c = (int64_t)blockIdx.x * 32 + threadIdx.x;   // storage position
-  if (c >= F.g.n) return;
-  int i, j, k;
-  const int64_t cell = locate(F.g, c, i, j, k);
-  switch (threadIdx.y) {   // warp-uniform
-    case 0: face_cell_row<0>(F, c, cell, i, j, k); break;
-    case 1: face_cell_row<1>(F, c, cell, i, j, k); break;
-    case 2: face_cell_row<2>(F, c, cell, i, j, k); break;
-    case 3: face_cell_row<3>(F, c, cell, i, j, k); break;
-    case 4: face_cell_row<4>(F, c, cell, i, j, k); break;
-    case 5: face_cell_row<5>(F, c, cell, i, j, k); break;
-    case 6: face_cell_row<6>(F, c, cell, i, j, k); break;
-    case 7: face_cell_row<7>(F, c, cell, i, j, k); break;
-    default: face_cell_row<8>(F, c, cell, i, j, k); break;
-  }
-}
-
-// ----------------------------------------------------- face-centric variant
+// ------------------------------------------------------- face-centric pair
 //
-// k_face evaluates every face twice (once from each side's gather). The
-// face-centric pair evaluates it once:
+// Each face is evaluated once:
 //   k_face_eval    thread per (lower cell a, axis, row < ROW_OS): flux row
 //                  and both derivative rows of face (a, a+axis); writes
 //                  offd[a][+axis] row = dfb, offd[b][-axis] row = -dfa and
@@ -1279,35 +1188,6 @@ __device__ __forceinline__ void face_eval_row(const FaceArgs2& A2, int64_t c, in
   // flux term depends on C_c); k_cc_red skips its loads while none is set
   if (ROW < ROW_E && (dfa[CCC] != 0.0 || dfb[CCC] != 0.0)) *F.ccnz = 1;
   A2.fbuf[(int64_t)(axis * ROW_OS + ROW) * n + c] = flux;
-}
-
-#ifndef FEVAL_MINB
-#define FEVAL_MINB 8
-#endif
-
-// grid (ceil(n/32), ROW_OS rows); block (32, 3 axes). A block holds one row's
-// three axes: the rows' costs differ several-fold (the energy row touches
-// every phase, the oil rows one), and warps of equal cost in a block keep it
-// from being held resident by its slowest warp.
-// Lower cells [c_begin, c_end), axes axis_lo + threadIdx.y (pipelined host
-// staging evaluates the in-plane faces of a chunk of planes as soon as its
-// records exist, the z faces one plane behind).
-__global__ void __launch_bounds__(32 * 3, FEVAL_MINB) k_face_eval(const FaceArgs2 A2,
-                                                                 int64_t c_begin, int64_t c_end,
-                                                                 int axis_lo) {
-  const int64_t c = c_begin + (int64_t)blockIdx.x * 32 + threadIdx.x;
-  if (c >= c_end) return;
-  const int axis = axis_lo + threadIdx.y;
-  int i, j, k;
-  const int64_t cell = locate(A2.F.g, c, i, j, k);
-  switch (blockIdx.y) {   // block-uniform
-    case 0: face_eval_row<0>(A2, c, cell, i, j, k, axis); break;
-    case 1: face_eval_row<1>(A2, c, cell, i, j, k, axis); break;
-    case 2: face_eval_row<2>(A2, c, cell, i, j, k, axis); break;
-    case 3: face_eval_row<3>(A2, c, cell, i, j, k, axis); break;
-    case 4: face_eval_row<4>(A2, c, cell, i, j, k, axis); break;
-    default: face_eval_row<5>(A2, c, cell, i, j, k, axis); break;
-  }
 }
 
 // The light rows (0..4) and the energy row (5, every phase) as separate

@@ -9,7 +9,7 @@
 //     (D^-1 B_d) x = D^-1[:, :CR] (B_d[:CR, :] x),   CR = ROW_OS = 6,
 // and the operator is kept as the raw flux rows of B_d (54 values per
 // direction) plus the first CR columns of D^-1 (54 values per cell, stored
-// over the diagonal block). The decoupling (k_decouple_compact) no longer
+// over the diagonal block). The decoupling (k_decouple_compact_t) no longer
 // reads and rewrites the 7.8 GB of off-diagonal blocks at C4: it inverts the
 // diagonal blocks (same Gauss-Jordan, pivot rule and failure reporting as
 // k_decouple_ws) and decouples the rhs. The factorisation keeps the 6x6
@@ -32,114 +32,6 @@ namespace isc {
 
 constexpr int CR = ROW_OS;   // flux rows of an assembled off-diagonal block
 
-// D^-1 of every owned cell (reference GJ: pivot tolerance 1e-13 max|D|,
-// partial pivoting) and rhs <- D^-1 rhs; block (32 cells, column u)
-#ifndef DCC_MINB
-#define DCC_MINB 3   // C4 sweep 2..4: 1.76 -> 1.61 ms at 3
-#endif
-__global__ void __launch_bounds__(32 * NU, DCC_MINB) k_decouple_compact(Dims g, double* diag, double* rhs,
-                                                                 int* flags,
-                                                                 unsigned long long* bad) {
-  __shared__ double inv[NU][NU][32];
-  __shared__ double colk[NU][32];
-  __shared__ double cmax[NU][32];
-  __shared__ int piv_s[32];
-  __shared__ int failc[32];
-  const int64_t n = g.n;
-  const int cl = threadIdx.x, u = threadIdx.y;
-  const int64_t p0 = (int64_t)g.kw_lo * g.nxny, p1 = (int64_t)g.kw_hi * g.nxny;
-  const int64_t c = p0 + (int64_t)blockIdx.x * 32 + cl;
-  const bool live = c < p1;
-  double a[NU], e[NU];
-#pragma unroll
-  for (int r = 0; r < NU; ++r) {
-    a[r] = live ? diag[(int64_t)(r * NU + u) * n + c] : (r == u ? 1.0 : 0.0);
-    e[r] = (r == u) ? 1.0 : 0.0;
-  }
-  const double rv = live ? rhs[(int64_t)u * n + c] : 0.0;
-  {
-    double m = 0.0;
-#pragma unroll
-    for (int r = 0; r < NU; ++r) m = fmax(m, fabs(a[r]));
-    cmax[u][cl] = m;
-    if (u == 0) failc[cl] = NU;
-  }
-  __syncthreads();   // every load of this CTA's diagonal blocks is done: dinv may go over them
-  double amax = 0.0;
-#pragma unroll
-  for (int q = 0; q < NU; ++q) amax = fmax(amax, cmax[q][cl]);
-  const double tol = 1e-13 * amax;
-#pragma unroll
-  for (int k = 0; k < NU; ++k) {
-    if (u == k) {
-      int piv = k;
-      double pv = fabs(a[k]);
-#pragma unroll
-      for (int r = k + 1; r < NU; ++r) {
-        const double v = fabs(a[r]);
-        if (v > pv) { pv = v; piv = r; }
-      }
-      if (pv <= tol || amax == 0.0) failc[cl] = amax == 0.0 ? 0 : min(failc[cl], k);
-#pragma unroll
-      for (int r = 0; r < NU; ++r) {
-        double v = a[r];
-        if (r == k) {
-#pragma unroll
-          for (int q = k + 1; q < NU; ++q) if (q == piv) v = a[q];
-        } else if (r == piv) {
-          v = a[k];
-        }
-        colk[r][cl] = v;
-      }
-      piv_s[cl] = piv;
-    }
-    __syncthreads();
-    const int piv = piv_s[cl];
-    if (piv != k) {
-      const double t0 = a[k], t1 = e[k];
-#pragma unroll
-      for (int q = k + 1; q < NU; ++q)
-        if (q == piv) { a[k] = a[q]; e[k] = e[q]; a[q] = t0; e[q] = t1; }
-    }
-    const double dv = 1.0 / colk[k][cl];
-    a[k] *= dv;
-    e[k] *= dv;
-#pragma unroll
-    for (int r = 0; r < NU; ++r) {
-      if (r == k) continue;
-      const double f = colk[r][cl];
-      if (f != 0.0) { a[r] -= f * a[k]; e[r] -= f * e[k]; }
-    }
-    __syncthreads();
-  }
-#pragma unroll
-  for (int r = 0; r < NU; ++r) inv[r][u][cl] = e[r];
-  colk[u][cl] = rv;
-  __syncthreads();
-  if (!live) return;
-  const bool gh = !owned_k(g, plane_of(g, c));
-  if (u == 0 && !gh && failc[cl] < NU) {
-    const int64_t cell = cell_of(g, c);
-    flags[cell] = failc[cl] + 1;
-    atomicMin(bad, (unsigned long long)cell);
-  }
-  if (u < CR) {
-#pragma unroll
-    for (int r = 0; r < NU; ++r) diag[(int64_t)(r * CR + u) * n + c] = e[r];
-  }
-  // rhs row u: sequential k sum as the reference's _mv
-  double s = 0.0;
-#pragma unroll
-  for (int k = 0; k < NU; ++k) s += inv[u][k][cl] * colk[k][cl];
-  rhs[(int64_t)u * n + c] = gh ? 0.0 : s;
-}
-
-// The same inversion with one thread per cell, the block held in registers
-// (in-place Gauss-Jordan: once column k is eliminated its slot holds column
-// perm[k] of the inverse, where perm tracks the row interchanges). Same
-// pivot rule, tolerance, scaling by the reciprocal and elimination order as
-// k_decouple_compact, so the same values; no shared memory and no barriers
-// (the column-per-thread form is barrier- and issue-bound).
 // cp.async (LDGSTS): global -> shared without register staging
 __device__ __forceinline__ void cp_async8(void* smem, const void* gmem) {
   const unsigned sa = (unsigned)__cvta_generic_to_shared(smem);
@@ -170,6 +62,12 @@ __device__ __forceinline__ int sel_i(bool p, int x, int y) {
       : "=r"(r) : "r"(x), "r"(y), "r"((unsigned)p));
   return r;
 }
+// D^-1 of every owned cell and rhs <- D^-1 rhs, one thread per cell with the
+// block held in registers: in-place Gauss-Jordan (once column k is
+// eliminated its slot holds column perm[k] of the inverse, where perm tracks
+// the row interchanges) with the reference's pivot rule (partial pivoting,
+// failure below 1e-13 max|D|, _gj_inverse linsolve.py:70-119), scaling by the
+// reciprocal and elimination order; no shared memory and no barriers.
 __global__ void __launch_bounds__(DCT_THREADS) k_decouple_compact_t(Dims g, double* diag,
                                                                    double* rhs, int* flags,
                                                                    unsigned long long* bad) {

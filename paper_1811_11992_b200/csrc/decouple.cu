@@ -43,165 +43,10 @@ __global__ void k_rhs_schur(Dims g, const double* __restrict__ resid, double* rh
   }
 }
 
-// D^-1 first, then D^-1 x [B_-z .. B_+z | rhs]: exactly the reference's
-// order of operations (_gj_inverse on [D | I], then _mm/_mv with sequential
-// k sums, linsolve.py:130-152). CTA = 16 cells, 256 threads:
-//   phase A: threads (cell, u < 9) own column u of D and of I, Gauss-Jordan
-//            with partial pivoting (pivot column broadcast via smem);
-//   phase B: the 55 (cell, column) products are spread over all threads,
-//            loads of a warp = 16 consecutive cells of one column.
-constexpr int DC3_CELLS = 16;
-constexpr int DC3_THREADS = 256;
-#ifndef DC3_MINB
-#define DC3_MINB 4
-#endif
-
-__global__ void __launch_bounds__(DC3_THREADS, DC3_MINB) k_decouple3(Dims g, const double* __restrict__ diag,
-                                                          double* offd, double* rhs, int* flags,
-                                                          unsigned long long* bad, int offd_rows) {
-  __shared__ double inv[NU][NU][DC3_CELLS];   // D^-1 (row, col, cell)
-  __shared__ double colk[2][NU][DC3_CELLS];
-  __shared__ double cmax[NU][DC3_CELLS];
-  __shared__ int piv_s[DC3_CELLS];
-  __shared__ int failc[DC3_CELLS];
-  const int64_t n = g.n;
-  const int t = threadIdx.x;
-  const int64_t c0 = (int64_t)blockIdx.x * DC3_CELLS;
-  // ---- phase A: D^-1 by Gauss-Jordan (linsolve.py:70-119)
-  const int cl = t % DC3_CELLS, u = t / DC3_CELLS;
-  const int64_t c = c0 + cl;
-  const bool mine = u < NU;
-  const bool live = mine && c < n;
-  double a[NU], e[NU];
-  if (mine) {
-#pragma unroll
-    for (int r = 0; r < NU; ++r) {
-      a[r] = live ? diag[(int64_t)(r * NU + u) * n + c] : (r == u ? 1.0 : 0.0);
-      e[r] = (r == u) ? 1.0 : 0.0;
-    }
-    double m = 0.0;
-#pragma unroll
-    for (int r = 0; r < NU; ++r) m = fmax(m, fabs(a[r]));
-    cmax[u][cl] = m;
-    if (u == 0) failc[cl] = NU;
-  }
-  __syncthreads();
-  double amax = 0.0;
-  if (mine) {
-#pragma unroll
-    for (int q = 0; q < NU; ++q) amax = fmax(amax, cmax[q][cl]);
-  }
-  const double tol = 1e-13 * amax;
-#pragma unroll
-  for (int k = 0; k < NU; ++k) {
-    if (mine && u == k) {
-      int piv = k;
-      double pv = fabs(a[k]);
-#pragma unroll
-      for (int r = k + 1; r < NU; ++r) {
-        const double v = fabs(a[r]);
-        if (v > pv) { pv = v; piv = r; }
-      }
-      if (pv <= tol || amax == 0.0) atomicMin(&failc[cl], amax == 0.0 ? 0 : k);
-#pragma unroll
-      for (int r = 0; r < NU; ++r) {
-        double v = a[r];
-        if (r == k) {
-#pragma unroll
-          for (int q = k + 1; q < NU; ++q) if (q == piv) v = a[q];
-        } else if (r == piv) {
-          v = a[k];
-        }
-        colk[0][r][cl] = v;
-      }
-      piv_s[cl] = piv;
-    }
-    __syncthreads();
-    if (mine) {
-      const int piv = piv_s[cl];
-      if (piv != k) {
-        const double t0 = a[k], t1 = e[k];
-#pragma unroll
-        for (int q = k + 1; q < NU; ++q)
-          if (q == piv) { a[k] = a[q]; e[k] = e[q]; a[q] = t0; e[q] = t1; }
-      }
-      const double dinv = 1.0 / colk[0][k][cl];
-      a[k] *= dinv;
-      e[k] *= dinv;
-#pragma unroll
-      for (int r = 0; r < NU; ++r) {
-        if (r == k) continue;
-        const double f = colk[0][r][cl];
-        if (f != 0.0) { a[r] -= f * a[k]; e[r] -= f * e[k]; }
-      }
-    }
-    __syncthreads();
-  }
-  __shared__ int ghost[DC3_CELLS];
-  if (mine) {
-#pragma unroll
-    for (int r = 0; r < NU; ++r) inv[r][u][cl] = e[r];
-    if (u == 0) {
-      bool gh = false;
-      int64_t cell = 0;
-      if (live) {
-        cell = cell_of(g, c);
-        gh = !owned_k(g, plane_of(g, c));
-      }
-      ghost[cl] = gh ? 1 : 0;
-      if (live && !gh && failc[cl] < NU) {
-        flags[cell] = failc[cl] + 1;
-        atomicMin(bad, (unsigned long long)cell);
-      }
-    }
-  }
-  __syncthreads();
-  // ---- phase B: columns of the row blocks and the rhs, times D^-1
-  constexpr int NCOLB = NDIR * NU + 1;   // 55
-#pragma unroll 2
-  for (int task = t; task < NCOLB * DC3_CELLS; task += DC3_THREADS) {
-    const int tc = task % DC3_CELLS, col = task / DC3_CELLS;
-    const int64_t cc = c0 + tc;
-    if (cc >= n) continue;
-    double* base;
-    int64_t stride;
-    if (col < NDIR * NU) {
-      const int d = col / NU, uu = col % NU;
-      base = offd + (int64_t)(d * NB + uu) * n + cc;   // row r at + r*NU*n
-      stride = (int64_t)NU * n;
-    } else {
-      base = rhs + cc;
-      stride = n;
-    }
-    if (ghost[tc] && col == NDIR * NU) {   // ghost rows carry no equation
-#pragma unroll
-      for (int r = 0; r < NU; ++r) base[r * stride] = 0.0;
-      continue;
-    }
-    // rows >= offd_rows of an assembled (not yet decoupled) off-diagonal block
-    // are structural zeros and were never written: not read, and their
-    // (+-0) terms are left out of the products
-    const int kin = col < NDIR * NU ? offd_rows : NU;
-    double v[NU];
-#pragma unroll
-    for (int r = 0; r < NU; ++r) v[r] = r < kin ? base[r * stride] : 0.0;
-#pragma unroll
-    for (int r = 0; r < NU; ++r) {
-      double s = 0.0;
-#pragma unroll
-      for (int k = 0; k < NU; ++k)
-        if (k < kin) s += inv[r][k][tc] * v[k];
-      base[r * stride] = s;
-    }
-  }
-}
-
-}  // namespace isc
-
-namespace isc {
-
-// k_decouple_ws: the k_decouple3 arithmetic in a warp-specialised persistent
-// pipeline. Per CTA, 9 "inverse" warps run Gauss-Jordan on [D | I] for groups
+// k_decouple_ws: D^-1 first, then D^-1 x [B_-z .. B_+z | rhs] -- exactly
+// the reference's order of operations (_gj_inverse on [D | I], then _mm/_mv
+// with sequential k sums, linsolve.py:130-152) -- in a warp-specialised
+// persistent pipeline. Per CTA, 9 "inverse" warps run Gauss-Jordan on [D | I] for groups
 // of 32 cells (warp u owns column u of every cell in the group; one named
 // barrier per pivot step, the pivot column double-buffered) and hand D^-1
 // over in a double-buffered shared tile; 8 "product" warps stream the 55

@@ -170,14 +170,12 @@ class DeviceContext:
         return out
 
     # -- hot path ---------------------------------------------------------------
-    def assemble(self, d_state, bhp, d_accn, dt, t_new, capped, freeze, fused=False):
-        """isc_assemble (or the fused assemble+decouple); returns the (nw, 32)
-        well outputs (host)."""
+    def assemble(self, d_state, bhp, d_accn, dt, t_new, capped, freeze):
+        """isc_assemble; returns the (nw, 32) well outputs (host)."""
         bhp = _c(bhp if self.nw else np.zeros(1))
         cap = np.ascontiguousarray(np.asarray(capped if self.nw else [0], dtype=np.uint8))
         bad = ctypes.c_int64(-1)
-        fn = self.L.isc_assemble_decoupled if fused else self.L.isc_assemble
-        st = fn(self.h, N.ptr(d_state), N.ptr(bhp), N.ptr(d_accn), float(dt), float(t_new),
+        st = self.L.isc_assemble(self.h, N.ptr(d_state), N.ptr(bhp), N.ptr(d_accn), float(dt), float(t_new),
                 N.ptr(cap), int(bool(freeze)), N.ptr(self.wout), ctypes.byref(bad))
         N.check(st, "isc_assemble", bad_cell=bad.value)
         return self.wout[:self.nw].copy()

@@ -106,15 +106,11 @@ class Simulator:
     """Device-resident mirror of the reference ``Simulator`` (newton.py:214-437)."""
 
     def __init__(self, grid, pack, wells, streams, state, schedule, solver, heat_loss=None,
-                 fused: bool = False, comm_setup=None, own_stream: bool = False,
-                 jacobian: str = "analytic"):
+                 comm_setup=None, own_stream: bool = False, jacobian: str = "analytic"):
         self.grid, self.pack = grid, pack
         self.wells, self.streams = tuple(wells), tuple(streams)
         self.schedule, self.solver_cfg = schedule, solver
-        self.fused = fused   # assemble+Schur+decoupling in one kernel (fused.cu)
         self.jacobian = jacobian   # "numeric": FD blocks every iteration (newton.py:228,278)
-        if jacobian == "numeric" and fused:
-            raise ValueError("the fused assemble+decouple path has no numeric-Jacobian mode")
         self.ctx = DeviceContext(grid, pack, self.wells, self.streams, solver.precond, heat_loss,
                                  own_stream=own_stream)
         if getattr(solver, "krylov", "bicgstab") != "bicgstab":
@@ -147,7 +143,7 @@ class Simulator:
             torch.cuda.current_stream().synchronize()
 
     def _assemble(self, st: DeviceState, accn, dt, t_new, capped, freeze, analytic=False):
-        wout = self.ctx.assemble(st.u, st.bhp, accn, dt, t_new, capped, freeze, fused=self.fused)
+        wout = self.ctx.assemble(st.u, st.bhp, accn, dt, t_new, capped, freeze)
         if self.jacobian == "numeric" and not analytic:
             wout = self.ctx.numeric_jacobian()
         return blocks_from_wout(self.wells, wout)

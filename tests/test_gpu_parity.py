@@ -335,41 +335,6 @@ def test_bicgstab_restart_and_breakdown_vs_reference(name):
         assert "Breakdown: " + str(exc.value) == status
 
 
-def test_fused_assembly_decoupling_matches_unfused():
-    """isc_assemble_decoupled (face + Schur + GJ in one kernel) == isc_assemble
-    followed by isc_decouple: decoupled rhs, residual and the decoupled
-    operator applied to a random vector (1e-10 relative)."""
-    import ctypes
-    from paper_1811_11992_b200 import _native as N
-    from paper_1811_11992_b200.device import DeviceContext, soa_from_rows, state_to_device
-    from tests.golden_states import random_state_like_reference
-    c = case_objects("sub2")
-    st, accn = random_state_like_reference(c, 21)
-    outs = []
-    for fused in (False, True):
-        ctx = DeviceContext(c.grid, c.pack, c.wells, c.streams, "ras")
-        d_st = state_to_device(st, ctx.device)
-        d_accn = soa_from_rows(accn, ctx.device)
-        wout = ctx.assemble(d_st, st.bhp, d_accn, 2e-3, 2e-3, np.zeros(len(c.wells), bool),
-                            False, fused=fused)
-        resid = ctx.copy_out(0, 9).cpu().numpy()
-        if not fused:
-            bc, bcol = ctypes.c_int64(-1), ctypes.c_int32(-1)
-            N.check(ctx.L.isc_decouple(ctx.h, ctypes.byref(bc), ctypes.byref(bcol)), "dec")
-        rhs = ctx.empty(9, c.grid.ncell)
-        N.check(ctx.L.isc_copy_rhs(ctx.h, N.ptr(rhs)), "rhs")
-        x = torch.from_numpy(np.random.default_rng(2).normal(size=(9, c.grid.ncell))).cuda()
-        y = torch.empty_like(x)
-        N.check(ctx.L.isc_spmv(ctx.h, N.ptr(x), N.ptr(y)), "spmv")
-        outs.append((wout, resid, rhs.cpu().numpy(), y.cpu().numpy()))
-        ctx.close()
-    (w0, r0, b0, y0), (w1, r1, b1, y1) = outs
-    np.testing.assert_allclose(w1, w0, rtol=1e-12, atol=1e-300)
-    assert row_scaled_err(r1.T, r0.T) <= 1e-10
-    assert np.max(np.abs(b1 - b0)) <= 1e-10 * np.max(np.abs(b0))
-    assert np.max(np.abs(y1 - y0)) <= 1e-10 * np.max(np.abs(y0))
-
-
 def _fd_err(a, b):
     """The reference's check_jacobian element metric |a-b| / max(1, |b|)."""
     a, b = np.asarray(a), np.asarray(b)
