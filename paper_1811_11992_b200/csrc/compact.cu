@@ -444,10 +444,16 @@ __global__ void __launch_bounds__(32 * NU, MCFC_MINB) k_mc_factor_compact(
     }
     if (g1) cp_async8(&T.r[u][ls], b + (int64_t)u * n + nb);
   };
-  double grow = 0.0;   // (sum_d B_bd b_r(nb))[u], u < CR
-  double qcol[CR];   // Q[:, u] = sum_d B'_bd B_back[:CR, u]
+  // Register-blocked products (the smem pipe bounds this kernel): thread
+  // u = 3 tq + tc owns the 2x2 block B'[2tq.., 2tc..] and the 2x3 block
+  // Q[2tq.., 3tc..]; each entry is summed in the same order as a plain loop
+  double grow[2] = {0.0, 0.0};   // (sum_d B_bd b_r(nb))[2tq + qq], by the tc == 0 threads
+  double qacc[2][3];             // Q[2tq + qq][3tc + uu] = sum_d B'_bd B_back[:CR, :]
 #pragma unroll
-  for (int q = 0; q < CR; ++q) qcol[q] = 0.0;
+  for (int qq = 0; qq < 2; ++qq)
+#pragma unroll
+    for (int uu = 0; uu < 3; ++uu) qacc[qq][uu] = 0.0;
+  const int tq = u / 3, tc = u - 3 * (u / 3);
   issue(0, 0);
   cp_async_commit();
 #pragma unroll 1
@@ -458,37 +464,77 @@ __global__ void __launch_bounds__(32 * NU, MCFC_MINB) k_mc_factor_compact(
     __syncthreads();
     const McfcStage& T = S.st[d & 1];
     const int64_t nb = nbs[d];
-    if (g1 && nb >= 0 && u < CR) {
-      double s = 0.0;
+    if (nb >= 0) {
+      double brow[2][NU];
 #pragma unroll
-      for (int a = 0; a < NU; ++a) s += T.b[u][a][ls] * T.r[a][ls];
-      grow += s;
-    }
-    if (nb >= 0) {   // B'_bd: 36 entries, 4 per thread; kept for the black passes
+      for (int qq = 0; qq < 2; ++qq)
 #pragma unroll
-      for (int e = 0; e < 4; ++e) {
-        const int idx = u * 4 + e;
-        if (idx < CR * CR) {
-          const int q = idx / CR, s2 = idx % CR;
-          double s = 0.0;
+        for (int a = 0; a < NU; ++a) brow[qq][a] = T.b[2 * tq + qq][a][ls];
+      if (g1 && tc == 0) {
 #pragma unroll
-          for (int a = 0; a < NU; ++a) s += T.b[q][a][ls] * T.d[a][s2][ls];
-          bpsh[q][s2][ls] = s;
-          bp[(int64_t)((d * CR + q) * CR + s2) * g.half + t] = s;
+        for (int qq = 0; qq < 2; ++qq) {
+          double sr = 0.0;
+#pragma unroll
+          for (int a = 0; a < NU; ++a) sr += brow[qq][a] * T.r[a][ls];
+          grow[qq] += sr;
+        }
+      }
+      // B'_bd = B_bd[:CR, :] D_nb^-1[:, :CR]; kept for the black passes
+#pragma unroll
+      for (int ss = 0; ss < 2; ++ss) {
+        double dcol[NU];
+#pragma unroll
+        for (int a = 0; a < NU; ++a) dcol[a] = T.d[a][2 * tc + ss][ls];
+#pragma unroll
+        for (int qq = 0; qq < 2; ++qq) {
+          double sb = 0.0;
+#pragma unroll
+          for (int a = 0; a < NU; ++a) sb += brow[qq][a] * dcol[a];
+          const int q = 2 * tq + qq, s2 = 2 * tc + ss;
+          bpsh[q][s2][ls] = sb;
+          bp[(int64_t)((d * CR + q) * CR + s2) * g.half + t] = sb;
         }
       }
     }
     __syncthreads();
-    if (nb >= 0) {   // Q[:, u] += B'_bd B_back[:CR, u]
+    if (nb >= 0) {   // Q[2tq.., 3tc..] += B'_bd[2tq.., :] B_back[:CR, 3tc..]
+      double bpr[2][CR];
 #pragma unroll
-      for (int q = 0; q < CR; ++q) {
-        double s = 0.0;
+      for (int qq = 0; qq < 2; ++qq)
 #pragma unroll
-        for (int r = 0; r < CR; ++r) s += bpsh[q][r][ls] * T.o[r][u][ls];
-        qcol[q] += s;
+        for (int r = 0; r < CR; ++r) bpr[qq][r] = bpsh[2 * tq + qq][r][ls];
+#pragma unroll
+      for (int uu = 0; uu < 3; ++uu) {
+        double ocol[CR];
+#pragma unroll
+        for (int r = 0; r < CR; ++r) ocol[r] = T.o[r][3 * tc + uu][ls];
+#pragma unroll
+        for (int qq = 0; qq < 2; ++qq) {
+          double sq = 0.0;
+#pragma unroll
+          for (int r = 0; r < CR; ++r) sq += bpr[qq][r] * ocol[r];
+          qacc[qq][uu] += sq;
+        }
       }
     }
     __syncthreads();   // stage d & 1 is refilled by the next iteration's issue
+  }
+  // Q and grow back to the column-per-thread layout of the Gauss-Jordan:
+  // qcol[q] = Q[q][u]
+  double qcol[CR];
+  {
+    double (*qsh)[NU][32] = reinterpret_cast<double (*)[NU][32]>(&S.st[1].o[0][0][0]);
+#pragma unroll
+    for (int qq = 0; qq < 2; ++qq)
+#pragma unroll
+      for (int uu = 0; uu < 3; ++uu) qsh[2 * tq + qq][3 * tc + uu][ls] = qacc[qq][uu];
+    if (tc == 0) {
+      colk[2 * tq][ls] = grow[0];
+      colk[2 * tq + 1][ls] = grow[1];
+    }
+    __syncthreads();
+#pragma unroll
+    for (int q = 0; q < CR; ++q) qcol[q] = qsh[q][u][ls];
   }
   cp_async_wait<0>();
   auto& dsh = S.st[0].d;
@@ -500,7 +546,6 @@ __global__ void __launch_bounds__(32 * NU, MCFC_MINB) k_mc_factor_compact(
       dsh[idx / CR][idx % CR][ls] = dinv[(int64_t)idx * n + c];
     }
   }
-  if (u < CR) colk[u][ls] = grow;
   __syncthreads();
   if (g1 && live) {
     double m = 0.0;

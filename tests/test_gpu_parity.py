@@ -697,3 +697,58 @@ def test_newton_update_matches_reference_incl_nan():
     exp = np.vstack([ref.p, ref.x.T, ref.y.T, ref.t, ref.sw, ref.sg, ref.cc])
     np.testing.assert_array_equal(got, exp)
     ctx.close()
+
+
+@pytest.mark.parametrize("seed", [2, 3])
+def test_compact_decoupling_pivoting_vs_oracle(seed):
+    """k_decouple_compact_t (thread-per-cell Gauss-Jordan of the compact form)
+    on diagonal blocks whose rows are permuted and scaled so that partial
+    pivoting swaps rows at almost every step: the mcilu solve matches the
+    oracle's (the reference's _gj_inverse, linsolve.py:70-119, then the
+    red-black ILU(0)) to 1e-8 with the same iteration count (+-1); a block
+    made singular at one column is reported with the reference's cell/column."""
+    from oracle import isc_oracle as O
+    from types import SimpleNamespace
+    from paper_1811_11992_b200.grid import build_grid
+    from paper_1811_11992_b200.synth import synth_system
+    from paper_1811_11992_b200.model import load_pack
+    grid = build_grid(6, 4, 4, 1.0, 1.0, 1.0, 1.0, 1.0, 1.0, 0.3)
+    pack = load_pack("tube3_pack", grid.phi_ref)
+    diag, offd, resid = synth_system(grid, 9, seed=seed)
+    offd = offd.copy()
+    offd[:, :, 6:, :] = 0.0       # flux rows only: the compact form applies
+    # pivot-heavy: every block row is left-multiplied by a row permutation
+    # (within the flux rows 0..5 and within 6..8, so rows 6..8 of the
+    # off-diagonal blocks stay zero) and a scaling spread over 1e-3..1e3 --
+    # the decoupled system D^-1 B is unchanged, the Gauss-Jordan must pivot
+    rng = np.random.default_rng(seed)
+    diag, resid = diag.copy(), resid.copy()
+    a, b = grid.conn_a, grid.conn_b
+    for c in range(grid.ncell):
+        perm = np.concatenate([rng.permutation(6), 6 + rng.permutation(3)])
+        sc = 10.0 ** rng.uniform(-3, 3, 9)
+        diag[c] = diag[c][perm] * sc[:, None]
+        resid[c] = resid[c][perm] * sc
+        for ic in np.flatnonzero(a == c):
+            offd[ic, 0] = offd[ic, 0][perm] * sc[:, None]
+        for ic in np.flatnonzero(b == c):
+            offd[ic, 1] = offd[ic, 1][perm] * sc[:, None]
+    ows = O.Workspace(grid, SimpleNamespace(nequ=9, nfull=5))
+    ows.diag, ows.offd, ows.resid = diag.copy(), offd.copy(), resid.copy()
+    odu, _, oit = O.BlockSolver(grid, ows, tol=1e-10, maxiter=500, precond="mcilu").solve([])
+    ws = Workspace(grid, pack, None, wells=(), streams=(), precond="mcilu")
+    load_system(ws, diag, offd, resid)
+    du, _, it = BlockSolver(grid, ws, tol=1e-10, maxiter=500, precond="mcilu").solve([])
+    assert ws.ctx.decoupled_form == "compact"
+    assert abs(it - oit) <= 1, (it, oit)
+    assert np.linalg.norm(du - odu) <= 1e-8 * np.linalg.norm(odu)
+    # singular block: column 3 of cell 7 (after the row shuffle) vanishes
+    bad = diag.copy()
+    bad[7, :, 3] = 0.0
+    ows.diag, ows.offd, ows.resid = bad.copy(), offd.copy(), resid.copy()
+    with pytest.raises(O.SingularCellBlock) as oexc:
+        O.BlockSolver(grid, ows, tol=1e-10, maxiter=500, precond="mcilu").solve([])
+    load_system(ws, bad, offd, resid)
+    with pytest.raises(SingularCellBlock) as exc:
+        BlockSolver(grid, ws, tol=1e-10, maxiter=500, precond="mcilu").solve([])
+    assert str(exc.value) == str(oexc.value)
