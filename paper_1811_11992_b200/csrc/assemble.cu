@@ -1442,14 +1442,22 @@ __global__ void k_wells(const Model M, Dims g, int nw, const WellDev* __restrict
     for (int u = 0; u < NU; ++u) o[2 + u] = zero_row ? 0.0 : dqs[u];   // wrow
   }
   __syncthreads();
-  if (threadIdx.x == 0) {
-    for (int q = 0; q < WB && base + q < nw; ++q) {
+  // apply the rows: lane e owns matrix/residual entry e of the perforated
+  // cell and walks the wells in order, so every address sees the reference's
+  // sequence of updates (wells sharing a cell included; the heater after its
+  // well's rows) while the 90 entries proceed in parallel (one thread walking
+  // them all serialised 8 x 90 dependent read-modify-writes)
+  const int nq = min(WB, nw - base);
+  for (int e = threadIdx.x; e < NB + NU; e += blockDim.x) {
+    for (int q = 0; q < nq; ++q) {
       const int64_t c = s_cell[q];
-      for (int r = 0; r < NU; ++r) {
+      if (e < NB) {
+        diag[(int64_t)e * n + c] -= s_drows[q][e / NU][e % NU];
+      } else {
+        const int r = e - NB;
         resid[r * n + c] -= s_rows[q][r];
-        for (int u = 0; u < NU; ++u) diag[(int64_t)(r * NU + u) * n + c] -= s_drows[q][r][u];
+        if (r == ROW_E && s_heat[q] != 0.0) resid[ROW_E * n + c] -= s_heat[q];
       }
-      if (s_heat[q] != 0.0) resid[ROW_E * n + c] -= s_heat[q];
     }
   }
   __syncthreads();

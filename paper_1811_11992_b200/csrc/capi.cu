@@ -148,7 +148,7 @@ extern "C" int isc_create(const isc_model_desc* md, const isc_grid_desc* gdsc, i
   ALLOC(ctx->upw, (size_t)9 * n);
   CK(cudaMemset(ctx->upw, 0, (size_t)9 * n));
   ALLOC(ctx->bad_d, 8);
-  CK(cudaMallocHost(&ctx->bad_h, 8));
+  CK(cudaMallocHost(&ctx->bad_h, 16));   // [0] bad cell (cell pass / decoupling), [1] factor status
   // solver vectors
   double** vecs[] = {&ctx->rhs, &ctx->xk, &ctx->rk, &ctx->rhat, &ctx->pk,
                      &ctx->vk, &ctx->phat, &ctx->shat, &ctx->sk, &ctx->tk};
@@ -215,6 +215,7 @@ extern "C" int isc_synchronize(isc_ctx* ctx) {
 }
 extern "C" int64_t isc_launch_count(isc_ctx* ctx) { return ctx ? ctx->launches : 0; }
 extern "C" int isc_stage_times(isc_ctx* ctx, double* out4) {
+  STAGE(sync_stream(ctx));
   for (int i = 0; i < 4; ++i) out4[i] = ctx->stage_ms[i];
   return ISC_OK;
 }
@@ -293,20 +294,12 @@ extern "C" int isc_assemble(isc_ctx* ctx, const double* d_state, const double* h
     launch_cell(ctx, A, st);
   }
   LAUNCH_CHECK();
+  // the pore-space test (assembly.py:548-552) is read back with the well
+  // outputs at the end -- one synchronisation per assembly; on failure the
+  // face and well passes ran on the failed state and their results are
+  // discarded with the status (the upwind flags they wrote are rewritten by
+  // the retried step's first, unfrozen iterations, newton.py:279)
   CK(cudaMemcpyAsync(ctx->bad_h, ctx->bad_d, 8, cudaMemcpyDeviceToHost, st));
-  CK(cudaStreamSynchronize(st));
-  {
-    // all ranks of a z-slab run take the same branch
-    double flag = *ctx->bad_h != ~0ULL ? 1.0 : 0.0;
-    int as = isc_comm_allreduce_host(ctx, &flag, 1, 1);
-    if (as) return as;
-    if (flag > 0.0) {
-      if (bad_cell) *bad_cell = *ctx->bad_h != ~0ULL ? (int64_t)*ctx->bad_h : -1;
-      g_err = "coke fills the pore volume";
-      STAGE(stage_end(ctx, 0));
-      return ISC_PORE_SPACE_EXHAUSTED;
-    }
-  }
   FaceArgs F{ctx->g, d_state, ctx->rec, ctx->depth, ctx->gd, ctx->td, ctx->upw, freeze,
              ctx->resid, ctx->diag, ctx->offd, ctx->ccnz_d};
   {
@@ -329,7 +322,19 @@ extern "C" int isc_assemble(isc_ctx* ctx, const double* d_state, const double* h
     LAUNCH_CHECK();
     CK(cudaMemcpyAsync(ctx->wout_h, ctx->wout_d, ctx->nw * WOUT * 8, cudaMemcpyDeviceToHost, st));
   }
-  STAGE(stage_end(ctx, 0));   // synchronises
+  STAGE(stage_end(ctx, 0));
+  STAGE(sync_stream(ctx));
+  {
+    // all ranks of a z-slab run take the same branch
+    double flag = *ctx->bad_h != ~0ULL ? 1.0 : 0.0;
+    int as = isc_comm_allreduce_host(ctx, &flag, 1, 1);
+    if (as) return as;
+    if (flag > 0.0) {
+      if (bad_cell) *bad_cell = *ctx->bad_h != ~0ULL ? (int64_t)*ctx->bad_h : -1;
+      g_err = "coke fills the pore volume";
+      return ISC_PORE_SPACE_EXHAUSTED;
+    }
+  }
   if (ctx->nw > 0 && h_wells_out) std::memcpy(h_wells_out, ctx->wout_h, ctx->nw * WOUT * 8);
   ctx->decoupled = false;
   ctx->compact = false;
@@ -599,15 +604,18 @@ extern "C" int isc_synth_system(isc_ctx* ctx, uint64_t seed) {
 
 // ------------------------------------------------------------- decouple
 
-extern "C" int isc_decouple(isc_ctx* ctx, int64_t* bad_cell, int32_t* bad_col) {
+// Decoupling in two halves: decouple_enqueue launches the well Schur fold and
+// the Gauss-Jordan pass and queues the read-back of the first singular cell;
+// decouple_check (after a synchronisation) reports it. isc_solve queues the
+// preconditioner setup in between, so the two share one synchronisation.
+static int decouple_enqueue(isc_ctx* ctx, int64_t* bad_cell, int32_t* bad_col) {
   const int64_t n = ctx->g.n;
   cudaStream_t st = ctx->stream;
-  // well equations with a zero / non-finite bhp derivative (linsolve.py:372-375)
+  // well equations with a zero / non-finite bhp derivative (linsolve.py:372-375);
+  // wout_h is current (isc_assemble / isc_numeric_jacobian / isc_set_wells_out)
   {
     double wbad = 0.0;
     if (ctx->nw > 0) {
-      CK(cudaMemcpyAsync(ctx->wout_h, ctx->wout_d, ctx->nw * WOUT * 8, cudaMemcpyDeviceToHost, st));
-      CK(cudaStreamSynchronize(st));
       for (int w = 0; w < ctx->nw; ++w) {
         const double dwdb = ctx->wout_h[w * WOUT + 1];
         if (dwdb == 0.0 || !std::isfinite(dwdb)) wbad = 1.0;
@@ -664,6 +672,10 @@ extern "C" int isc_decouple(isc_ctx* ctx, int64_t* bad_cell, int32_t* bad_col) {
   }
   CK(cudaMemcpyAsync(ctx->bad_h, ctx->bad_d, 8, cudaMemcpyDeviceToHost, st));
   STAGE(stage_end(ctx, 1));
+  return ISC_OK;
+}
+
+static int decouple_check(isc_ctx* ctx, int64_t* bad_cell, int32_t* bad_col) {
   {
     double flag = *ctx->bad_h != ~0ULL ? 1.0 : 0.0;
     int as = isc_comm_allreduce_host(ctx, &flag, 1, 1);
@@ -688,6 +700,12 @@ extern "C" int isc_decouple(isc_ctx* ctx, int64_t* bad_cell, int32_t* bad_col) {
   return ISC_OK;
 }
 
+extern "C" int isc_decouple(isc_ctx* ctx, int64_t* bad_cell, int32_t* bad_col) {
+  STAGE(decouple_enqueue(ctx, bad_cell, bad_col));
+  STAGE(sync_stream(ctx));
+  return decouple_check(ctx, bad_cell, bad_col);
+}
+
 extern "C" int isc_copy_rhs(isc_ctx* ctx, double* d_dst) {
   k_from_pos<double><<<grid1d(ctx->g.n, 256), 256, 0, ctx->stream>>>(ctx->g, NU, ctx->rhs, d_dst);
   LAUNCH_CHECK();
@@ -709,8 +727,11 @@ extern "C" int isc_set_rhs(isc_ctx* ctx, const double* d_src) {
   return ISC_OK;
 }
 
-extern "C" int isc_precond_setup(isc_ctx* ctx, int64_t* bad_cell) {
-  if (ctx->precond == ISC_PRECOND_NONE) { ctx->factored = true; return ISC_OK; }
+// Preconditioner setup in two halves as the decoupling: precond_enqueue
+// launches the factorisation and queues the read-back of its status,
+// precond_check reports it after a synchronisation.
+static int precond_enqueue(isc_ctx* ctx) {
+  if (ctx->precond == ISC_PRECOND_NONE) return ISC_OK;
   cudaStream_t st = ctx->stream;
   STAGE(stage_begin(ctx, 2));
   CK(cudaMemsetAsync(ctx->fail_d, 0x7f, 4, st));
@@ -740,7 +761,7 @@ extern "C" int isc_precond_setup(isc_ctx* ctx, int64_t* bad_cell) {
       if (cross && halo_exchange(ctx, ctx->rhs, NU)) return ISC_CUDA_ERROR;
       CK(cudaFuncSetAttribute(k_mc_factor_compact, cudaFuncAttributeMaxDynamicSharedMemorySize,
                               (int)sizeof(McfcSmem)));
-      k_mc_factor_compact<<<grid1d(ctx->g.tw_hi - ctx->g.tw_lo, 32), dim3(32, NU),
+      k_mc_factor_compact<<<grid1d(ctx->g.tw_hi - ctx->g.tw_lo, MCFC_CELLS), dim3(MCFC_CELLS, NU),
                             sizeof(McfcSmem), st>>>(
           ctx->g, ctx->offd, ctx->diag, ctx->mc_uinv, ctx->cbp, ctx->fail_d, ctx->rhs, ctx->rk,
           ctx->rhat);
@@ -758,10 +779,15 @@ extern "C" int isc_precond_setup(isc_ctx* ctx, int64_t* bad_cell) {
   }
   }
   ++ctx->launches;
-  int fail_h = 0;
-  CK(cudaMemcpyAsync(ctx->bad_h, ctx->fail_d, 4, cudaMemcpyDeviceToHost, st));
+  CK(cudaMemcpyAsync(ctx->bad_h + 1, ctx->fail_d, 4, cudaMemcpyDeviceToHost, st));
   STAGE(stage_end(ctx, 2));
-  std::memcpy(&fail_h, ctx->bad_h, 4);
+  return ISC_OK;
+}
+
+static int precond_check(isc_ctx* ctx, int64_t* bad_cell) {
+  if (ctx->precond == ISC_PRECOND_NONE) { ctx->factored = true; return ISC_OK; }
+  int fail_h = 0;
+  std::memcpy(&fail_h, ctx->bad_h + 1, 4);
   {
     double flag = fail_h != 0x7f7f7f7f ? 1.0 : 0.0;
     int as = isc_comm_allreduce_host(ctx, &flag, 1, 1);
@@ -775,6 +801,12 @@ extern "C" int isc_precond_setup(isc_ctx* ctx, int64_t* bad_cell) {
   }
   ctx->factored = true;
   return ISC_OK;
+}
+
+extern "C" int isc_precond_setup(isc_ctx* ctx, int64_t* bad_cell) {
+  STAGE(precond_enqueue(ctx));
+  STAGE(sync_stream(ctx));
+  return precond_check(ctx, bad_cell);
 }
 
 static int precond_apply(isc_ctx* ctx, const double* r, double* z) {
@@ -901,12 +933,22 @@ extern "C" int isc_set_krylov(isc_ctx* ctx, int32_t krylov, int32_t restart) {
 
 extern "C" int isc_solve(isc_ctx* ctx, double tol, int32_t maxiter, double* d_du, double* h_dbhp,
                          int32_t* iters, int64_t* bad_cell, int32_t* bad_col) {
-  if (!ctx->decoupled) {   // (a decoupled system was checked by its isc_decouple)
-    int s = isc_decouple(ctx, bad_cell, bad_col);
+  // decoupling and preconditioner setup queued back to back, one
+  // synchronisation, then their checks in the reference's order
+  // (SingularCellBlock from the decoupling first, linsolve.py:458-463)
+  const bool dec = !ctx->decoupled, fac = !ctx->factored;
+  if (dec) {   // (a decoupled system was checked by its isc_decouple)
+    int s = decouple_enqueue(ctx, bad_cell, bad_col);
     if (s) return s;
   }
-  if (!ctx->factored) {
-    int s = isc_precond_setup(ctx, bad_cell);
+  if (fac) STAGE(precond_enqueue(ctx));
+  if (dec || fac) STAGE(sync_stream(ctx));
+  if (dec) {
+    int s = decouple_check(ctx, bad_cell, bad_col);
+    if (s) return s;
+  }
+  if (fac) {
+    int s = precond_check(ctx, bad_cell);
     if (s) {
       if (bad_col) *bad_col = -1;
       return s;

@@ -385,8 +385,11 @@ __global__ void __launch_bounds__(32 * CR, CC_MINB) k_cc_black(
 // g1 != nullptr the reduced rhs g_b = b_b - D_b^-1[:, :CR] sum_d B_bd b_r(nb)
 // is formed on the way (the blocks are in shared memory anyway) and written
 // to g1 and g2. Thread (black cell lane, column u).
+#ifndef MCFC_CELLS
+#define MCFC_CELLS 32   // black cells per CTA (thread (cell lane, column u): 288 threads)
+#endif
 #ifndef MCFC_MINB
-#define MCFC_MINB 2   // two CTAs per SM: the double-buffered stages take ~99 KB of smem each
+#define MCFC_MINB 2     // two CTAs per SM: the double-buffered stages take ~99 KB of smem each (16 cells at 3 or 4 per SM: no faster)
 #endif
 // Direction tiles are double-buffered with cp.async (LDGSTS: global -> shared
 // without register staging): the loads of direction d+1 -- B_bd rows, the red
@@ -395,19 +398,19 @@ __global__ void __launch_bounds__(32 * CR, CC_MINB) k_cc_black(
 // the products instead of alternating with them (round 1: one exposed round
 // trip per tile and 2.8 TB/s).
 struct McfcStage {
-  double b[CR][NU][32];      // B_bd flux rows of the black cell
-  double d[NU][CR][32];      // D_nb^-1[:, :CR] of the red neighbour
-  double o[CR][NU][32];      // B_nb,back flux rows (the red neighbour's block pointing back)
-  double r[NU][32];          // b(nb): the red neighbour's decoupled rhs
+  double b[CR][NU][MCFC_CELLS];      // B_bd flux rows of the black cell
+  double d[NU][CR][MCFC_CELLS];      // D_nb^-1[:, :CR] of the red neighbour
+  double o[CR][NU][MCFC_CELLS];      // B_nb,back flux rows (the red neighbour's block pointing back)
+  double r[NU][MCFC_CELLS];          // b(nb): the red neighbour's decoupled rhs
 };
 struct McfcSmem {
   McfcStage st[2];
-  double bpsh[CR][CR][32];   // B'_bd = B_bd[:CR, :] D_nb^-1[:, :CR]
-  double colk[NU][32];
-  int pivs[32];
+  double bpsh[CR][CR][MCFC_CELLS];   // B'_bd = B_bd[:CR, :] D_nb^-1[:, :CR]
+  double colk[NU][MCFC_CELLS];
+  int pivs[MCFC_CELLS];
 };
 
-__global__ void __launch_bounds__(32 * NU, MCFC_MINB) k_mc_factor_compact(
+__global__ void __launch_bounds__(MCFC_CELLS * NU, MCFC_MINB) k_mc_factor_compact(
     Dims g, const double* __restrict__ offd, const double* __restrict__ dinv,
     double* __restrict__ uinv, double* __restrict__ bp, int* fail, const double* __restrict__ b,
     double* __restrict__ g1, double* __restrict__ g2) {
@@ -418,7 +421,7 @@ __global__ void __launch_bounds__(32 * NU, MCFC_MINB) k_mc_factor_compact(
   auto& pivs = S.pivs;
   const int64_t n = g.n;
   const int ls = threadIdx.x, u = threadIdx.y;
-  const int64_t t = g.tw_lo + (int64_t)blockIdx.x * 32 + ls;
+  const int64_t t = g.tw_lo + (int64_t)blockIdx.x * MCFC_CELLS + ls;
   const bool in = t < g.tw_hi;
   const int64_t c = in ? colour_pos(g, 1, t) : 0;
   int i = 0, j = 0, k = 0;
@@ -427,10 +430,11 @@ __global__ void __launch_bounds__(32 * NU, MCFC_MINB) k_mc_factor_compact(
   int64_t nbs[NDIR];
 #pragma unroll
   for (int d = 0; d < NDIR; ++d) nbs[d] = live ? nb_pos(g, cell, i, j, k, d) : -1;
+  auto nb_of = [&](int d) -> int64_t { return nbs[d]; };
   // issue direction d's tiles into stage s (6 + 6 + 6 B_bd / D^-1 / back
   // values per thread, b(nb)[u] by every thread)
   auto issue = [&](int d, int sidx) {
-    const int64_t nb = nbs[d];
+    const int64_t nb = nb_of(d);
     if (nb < 0) return;
     McfcStage& T = S.st[sidx];
 #pragma unroll
@@ -463,7 +467,7 @@ __global__ void __launch_bounds__(32 * NU, MCFC_MINB) k_mc_factor_compact(
     cp_async_wait<1>();
     __syncthreads();
     const McfcStage& T = S.st[d & 1];
-    const int64_t nb = nbs[d];
+    const int64_t nb = nb_of(d);
     if (nb >= 0) {
       double brow[2][NU];
 #pragma unroll
@@ -523,7 +527,7 @@ __global__ void __launch_bounds__(32 * NU, MCFC_MINB) k_mc_factor_compact(
   // qcol[q] = Q[q][u]
   double qcol[CR];
   {
-    double (*qsh)[NU][32] = reinterpret_cast<double (*)[NU][32]>(&S.st[1].o[0][0][0]);
+    double (*qsh)[NU][MCFC_CELLS] = reinterpret_cast<double (*)[NU][MCFC_CELLS]>(&S.st[1].o[0][0][0]);
 #pragma unroll
     for (int qq = 0; qq < 2; ++qq)
 #pragma unroll

@@ -248,12 +248,18 @@ static int bicgstab_schur(isc_ctx* ctx, double tol, int maxiter, int* iters) {
   const double* uinv = ctx->mc_uinv;
   const int bh = grid1d(g.tw_hi - g.tw_lo, 32);   // blocks of a half pass (owned planes)
   CK(cudaMemsetAsync(x, 0, len * 8, st));
-  TRY(K.dot(b, b, S_BB));   // ||b|| of the full decoupled rhs (the reference's tolerance base)
-  TRY(K.read_scalars());
-  const double nb = std::sqrt(ctx->sc_h[S_BB]);
   *iters = 0;
-  if (nb == 0.0) return ISC_OK;
-  const double brk = 1e-30 * nb * nb;
+  // control state first (the dots below write their slots after this push);
+  // ||b||, the breakdown threshold and r^.r are formed on the device, so the
+  // first chunk of iterations is queued without a host round trip
+  double* sh = ctx->sc_h;
+  for (int i = 0; i < S_NSCAL; ++i) sh[i] = 0.0;
+  sh[S_RHO_OLD] = 1.0; sh[S_ALPHA] = 1.0; sh[S_OMEGA] = 1.0; sh[S_FIRST] = 1.0;
+  sh[S_STOP] = STOP_RUN;
+  sh[S_MAXIT] = (double)maxiter;
+  sh[S_TOL] = tol;
+  TRY(K.push());
+  TRY(K.dot(b, b, S_BB));   // ||b|| of the full decoupled rhs (the reference's tolerance base)
   // p, v and t need no clearing: p and v are read only after the first
   // iteration wrote them (S_FIRST), t only where the black pass wrote it
   if (ctx->compact && ctx->gb_fresh) {
@@ -266,10 +272,6 @@ static int bicgstab_schur(isc_ctx* ctx, double tol, int maxiter, int* iters) {
     }
     ++ctx->launches;
   }
-  double* sh = ctx->sc_h;
-  for (int i = 0; i < S_NSCAL; ++i) sh[i] = 0.0;
-  sh[S_RHO_OLD] = 1.0; sh[S_ALPHA] = 1.0; sh[S_OMEGA] = 1.0; sh[S_FIRST] = 1.0;
-  sh[S_BB] = nb * nb;
   bool restarted = false, first = true;
   int it = 0;
   // One half pass over the owned planes. On slabs the planes next to the
@@ -341,9 +343,9 @@ static int bicgstab_schur(isc_ctx* ctx, double tol, int maxiter, int* iters) {
     ++ctx->launches;
     return cudaGetLastError() == cudaSuccess ? 0 : ISC_CUDA_ERROR;
   };
-  TRY(K.push());
   TRY(dot_b(rhat, r, S_RHO_NEW));
-  TRY(K.read_scalars());
+  k_bicg_init<<<1, 1, 0, st>>>(ctx->sc);   // S_NB, S_BRK; ||b|| = 0 stops at once
+  ++ctx->launches;
   auto restart = [&]() -> int {
     // r_b = g_b - S x_b; rhat = r; p = v = 0 (linsolve.py:509-519)
     {
@@ -372,13 +374,6 @@ static int bicgstab_schur(isc_ctx* ctx, double tol, int maxiter, int* iters) {
   // restart or iteration recomputes are affected.)
   double* stop = ctx->sc + S_STOP;
   K.stop = stop;
-  sh[S_STOP] = STOP_RUN;
-  sh[S_IT] = 0.0;
-  sh[S_MAXIT] = (double)maxiter;
-  sh[S_NB] = nb;
-  sh[S_TOL] = tol;
-  sh[S_BRK] = brk;
-  TRY(K.push());
   auto enqueue_iteration = [&]() -> int {
     k_bicg_top<<<1, 1, 0, st>>>(ctx->sc);
     {
@@ -445,7 +440,12 @@ static int bicgstab_schur(isc_ctx* ctx, double tol, int maxiter, int* iters) {
     it = (int)sh[S_IT];
     if (code == STOP_RUN) continue;
     *iters = it;
+    if (code == STOP_ZERO) {   // b = 0: x = 0 (linsolve.py:486-487)
+      sh[S_STOP] = STOP_RUN;
+      return K.push();
+    }
     ctx->bicg_last_iters = it;
+    const double brk = sh[S_BRK];
     if (code == STOP_CONV_S) {   // ||s|| / ||b|| <= tol: x += alpha phat (linsolve.py:550-552)
       sh[S_STOP] = STOP_RUN;
       TRY(K.push());

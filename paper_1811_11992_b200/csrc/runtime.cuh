@@ -125,7 +125,11 @@ struct isc_ctx {
   std::vector<cudaEvent_t> pool;
   size_t pool_used = 0;
   struct Pending { int kind; cudaEvent_t a, b; };
-  std::vector<Pending> pending;
+  std::vector<Pending> pending;         // kernel-class event pairs (profiling)
+  std::vector<Pending> stage_pending;   // stage event pairs (always; no sync to take them)
+  cudaEvent_t stage_open[4] = {};
+  bool stage_is_open[4] = {false, false, false, false};
+  int stages_open = 0;                  // begun, not yet ended (their events stay reserved)
   double kern_ms[8] = {0, 0, 0, 0, 0, 0, 0, 0};
   int64_t kern_n[8] = {0, 0, 0, 0, 0, 0, 0, 0};
 };
@@ -159,17 +163,29 @@ struct KScope {
     }
   }
 };
-// after a stream synchronisation: fold finished event pairs into the totals
+// fold the finished event pairs into the totals (pairs whose end event has
+// not completed yet stay pending; the pool is recycled once none is left)
 static void kflush(isc_ctx* ctx) {
-  for (auto& p : ctx->pending) {
-    float ms = 0.f;
-    if (cudaEventElapsedTime(&ms, p.a, p.b) == cudaSuccess) {
-      ctx->kern_ms[p.kind] += ms;
-      ctx->kern_n[p.kind] += 1;
+  auto fold = [&](std::vector<isc_ctx::Pending>& v, double* ms_out, int64_t* n_out) {
+    size_t keep = 0;
+    for (size_t i = 0; i < v.size(); ++i) {
+      if (cudaEventQuery(v[i].b) != cudaSuccess) {
+        cudaGetLastError();   // cudaErrorNotReady is not an error here
+        v[keep++] = v[i];
+        continue;
+      }
+      float ms = 0.f;
+      if (cudaEventElapsedTime(&ms, v[i].a, v[i].b) == cudaSuccess) {
+        ms_out[v[i].kind] += ms;
+        if (n_out) n_out[v[i].kind] += 1;
+      }
     }
-  }
-  ctx->pending.clear();
-  ctx->pool_used = 0;
+    v.resize(keep);
+  };
+  fold(ctx->pending, ctx->kern_ms, ctx->kern_n);
+  fold(ctx->stage_pending, ctx->stage_ms, nullptr);
+  if (ctx->pending.empty() && ctx->stage_pending.empty() && ctx->stages_open == 0)
+    ctx->pool_used = 0;
 }
 
 static int dev_alloc(void** p, size_t bytes) {
@@ -192,17 +208,28 @@ static int halo_exchange(isc_ctx* ctx, double* v, int rows);
 static int allreduce_dev(isc_ctx* ctx, double* d, int count);
 extern "C" int isc_comm_allreduce_host(isc_ctx* ctx, double* vals, int32_t count, int32_t op);
 
+// stage timers (assemble / decouple / preconditioner setup / Krylov): event
+// pairs on the stream, folded at the next synchronisation -- taking a time
+// never adds one
 static int stage_begin(isc_ctx* ctx, int st) {
-  CK(cudaEventRecord(ctx->ev[2 * st], ctx->stream));
+  ctx->stage_open[st] = pool_event(ctx);
+  if (!ctx->stage_is_open[st]) ++ctx->stages_open;   // (an error path may skip an end)
+  ctx->stage_is_open[st] = true;
+  CK(cudaEventRecord(ctx->stage_open[st], ctx->stream));
   return ISC_OK;
 }
 static int stage_end(isc_ctx* ctx, int st) {
-  CK(cudaEventRecord(ctx->ev[2 * st + 1], ctx->stream));
-  CK(cudaEventSynchronize(ctx->ev[2 * st + 1]));
+  cudaEvent_t b = pool_event(ctx);
+  CK(cudaEventRecord(b, ctx->stream));
+  ctx->stage_pending.push_back({st, ctx->stage_open[st], b});
+  if (ctx->stage_is_open[st]) --ctx->stages_open;
+  ctx->stage_is_open[st] = false;
+  return ISC_OK;
+}
+// synchronise the context's stream and fold the timers
+static int sync_stream(isc_ctx* ctx) {
+  CK(cudaStreamSynchronize(ctx->stream));
   kflush(ctx);
-  float ms = 0.f;
-  CK(cudaEventElapsedTime(&ms, ctx->ev[2 * st], ctx->ev[2 * st + 1]));
-  ctx->stage_ms[st] += ms;
   return ISC_OK;
 }
 #define STAGE(call) do { int s_ = (call); if (s_) return s_; } while (0)

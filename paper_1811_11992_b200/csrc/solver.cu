@@ -37,7 +37,7 @@ enum {
 };
 // S_STOP codes: why the device-driven iteration stopped (0 = running)
 enum { STOP_RUN = 0, STOP_TOP = 1, STOP_DEN = 2, STOP_CONV_S = 3, STOP_TT = 4, STOP_CONV = 5,
-       STOP_MAXIT = 6 };
+       STOP_MAXIT = 6, STOP_ZERO = 7 };
 
 // every kernel of a device-driven iteration returns at once when `stop`
 // (nullable: host-driven callers) holds a nonzero code
@@ -1089,6 +1089,12 @@ __global__ void __launch_bounds__(RED_THREADS, VEC_MINB) k_sc_update_xr(Dims g, 
 // breakdown test, the tolerance, the iteration limit -- only sets S_STOP;
 // the host reads it after the chunk and runs the branch (restart, Breakdown,
 // MaxIterations, final update) exactly as the host-driven loop does.
+__global__ void k_bicg_init(double* sc) {    // ||b||, breakdown threshold 1e-30 ||b||^2
+  const double nb = sqrt(sc[S_BB]);
+  sc[S_NB] = nb;
+  sc[S_BRK] = 1e-30 * nb * nb;
+  if (nb == 0.0) sc[S_STOP] = STOP_ZERO;
+}
 __global__ void k_bicg_top(double* sc) {     // loop head: it += 1; rho / omega tests
   if (sc[S_STOP] != 0.0) return;
   if (sc[S_IT] >= sc[S_MAXIT]) { sc[S_STOP] = STOP_MAXIT; return; }

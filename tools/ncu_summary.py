@@ -16,7 +16,8 @@ from collections import defaultdict
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 KERNELS = ["k_cc_red", "k_cc_black", "k_sc_update_p", "k_sc_update_s", "k_sc_update_xr",
            "k_face_eval_light", "k_face_eval_energy", "k_face_gather", "k_decouple_compact_t", "k_decouple_compact",
-           "k_cell_props", "k_cell_gas", "k_cell_rows", "k_mc_factor_compact",
+           "k_cell_props", "k_cell_gas", "k_cell_rows", "k_mc_factor_compact", "k_cc_xred",
+           "k_wells",
            # one-kernel variants (CELL_SPLIT=0 / FACE_SPLIT=0, earlier captures)
            "k_face_eval", "k_cell",
            # explicit decoupled form (ISC_COMPACT=0 / round-1 first captures)
