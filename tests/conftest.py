@@ -6,6 +6,14 @@ import pytest
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 if ROOT not in sys.path:
     sys.path.insert(0, ROOT)
+# The unmodified reference package, when installed into baseline/_ref (see
+# tests/test_gpu_dropin_reference.py): importable by the whole session, so the
+# drop-in modules bind the reference's exception classes at import, as in a
+# reference run with the device path patched in (errors.py).
+_REF = os.path.join(ROOT, "baseline", "_ref")
+if os.path.isdir(os.path.join(_REF, "iscsim")) and _REF not in sys.path:
+    os.environ.setdefault("NUMBA_CACHE_DIR", os.path.join("/tmp", "numba_cache_iscsim_tests"))
+    sys.path.append(_REF)
 
 
 def pytest_configure(config):

@@ -319,6 +319,18 @@ def make_bicgstab_breakdown():
     np.savez_compressed(os.path.join(HERE, "bicgstab_breakdown.npz"), **out)
 
 
+def make_c2_deck():
+    """The reference deck text of config C2 at LINEAR_TOL 1e-10 (tools/refdeck.py:
+    the reference's tube.deck fluid with the case's grid, rock, wells and
+    schedule), for the drop-in test that runs the unmodified reference driver
+    with the device path patched in (tests/test_gpu_dropin_reference.py)."""
+    from tools.refdeck import case_to_deck
+    case = configs.config("c2")
+    case = replace(case, solver=replace(case.solver, linear_tol=1e-10))
+    with open(os.path.join(HERE, "c2_deck_1e-10.txt"), "w") as fh:
+        fh.write(case_to_deck(case))
+
+
 def make_traj_numeric():
     """C1 run in JACOBIAN numeric mode (newton.py:228, 278)."""
     make_traj("c1", 1e-10, jacobian="numeric")
@@ -357,5 +369,6 @@ if __name__ == "__main__":
     make_traj_c3()
     make_traj_variants()
     make_bicgstab_breakdown()
+    make_c2_deck()
     for f in sorted(os.listdir(HERE)):
         print(f, os.path.getsize(os.path.join(HERE, f)))
