@@ -650,7 +650,9 @@ static int decouple_enqueue(isc_ctx* ctx, int64_t* bad_cell, int32_t* bad_col) {
   }
   if (ctx->compact) {
     const int64_t owned = (int64_t)(ctx->g.kw_hi - ctx->g.kw_lo) * ctx->g.nxny;
-    k_decouple_compact_t<<<grid1d(owned, DCT_THREADS), DCT_THREADS, 0, st>>>(
+    CK(cudaFuncSetAttribute(k_decouple_compact_t, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                            DCT_SMEM));
+    k_decouple_compact_t<<<grid1d(owned, DCT_THREADS), DCT_THREADS, DCT_SMEM, st>>>(
         ctx->g, ctx->diag, ctx->rhs, ctx->flags, ctx->bad_d);
   } else {
     // once per process (thread-safe static init: hub ranks share the process)

@@ -141,31 +141,30 @@ __global__ void __launch_bounds__(DCT_THREADS) k_decouple_compact_t(Dims g, doub
       for (int r = 0; r < NU; ++r) diag[(int64_t)(r * CR + col) * n + c] = a[r][j];
     }
   }
-  // rhs row u: sequential k sum as the reference's _mv (slot of inverse
-  // column k: iperm[k])
-  double rv[NU];
-  int iperm[NU];
+  // rhs row u: sequential k sum as the reference's _mv. The inverse's
+  // columns are un-permuted through this thread's shared-memory slot (a
+  // dynamically indexed store; selecting slot iperm[k] for each (u, k) from
+  // registers took 648 double selects)
+  extern __shared__ double dct_inv[];   // [NB][DCT_THREADS]
+  double* mine = dct_inv + threadIdx.x;
 #pragma unroll
-  for (int k = 0; k < NU; ++k) {
-    rv[k] = rhs[(int64_t)k * n + c];
-    int jk = 0;
+  for (int j = 0; j < NU; ++j) {
+    const int col = perm[j];
 #pragma unroll
-    for (int j = 1; j < NU; ++j) jk = perm[j] == k ? j : jk;
-    iperm[k] = jk;
+    for (int u = 0; u < NU; ++u) mine[(u * NU + col) * DCT_THREADS] = a[u][j];
   }
+  double rv[NU];
+#pragma unroll
+  for (int k = 0; k < NU; ++k) rv[k] = rhs[(int64_t)k * n + c];
 #pragma unroll
   for (int u = 0; u < NU; ++u) {
     double s = 0.0;
 #pragma unroll
-    for (int k = 0; k < NU; ++k) {
-      double x = a[u][0];
-#pragma unroll
-      for (int j = 1; j < NU; ++j) x = sel_d(iperm[k] == j, a[u][j], x);
-      s += x * rv[k];
-    }
+    for (int k = 0; k < NU; ++k) s += mine[(u * NU + k) * DCT_THREADS] * rv[k];
     rhs[(int64_t)u * n + c] = gh ? 0.0 : s;
   }
 }
+constexpr int DCT_SMEM = NB * DCT_THREADS * 8;
 
 // One half pass of the compact operator over the owned cells of one colour
 // (thread (cell lane, flux row r < CR), then output rows q = y, y + CR):
