@@ -266,6 +266,21 @@ def algorithmic_bytes(grid, nw, precond="ras", form="explicit"):
             # neighbours' b (9 n/2), B' out (36 m), U_b^-1 out (81 n/2), g_b out
             # twice (9 n)
             out["mc_factor"] = 8 * (144 * m + 54 * n + 4.5 * n + 40.5 * n + 9 * n)
+        if form == "condensed":
+            # condensed form (csrc/compact.cu: 6-component iteration)
+            # red pass y_r = sum_d Bc_rd w: 36 per red block, w gathered (6 n/2),
+            # y written (6 n/2); black pass v = z - Dc_b^-1 sum_d B'_bd y: 36 per
+            # black block, Dc_b^-1 (36 n/2), y gathered, z read, v written and the
+            # dot operand (4 x 6 n/2)
+            out["ilu_apply"] = 8 * (36 * m + 6 * n)
+            out["spmv"] = 8 * (36 * m + 30 * n)
+            # + k_cond_es: the local rows of the black cells' diagonal blocks in
+            # (27 n/2), E_S out (18 n/2)
+            out["decouple"] = 8 * (18 * n + 81 * n + 9 * n + 54 * n + 9 * n + 22.5 * n)
+            # k_mc_factor_compact<COND>: B_bd and B_back flux rows (54 m each),
+            # D^-1[:, :6] of both colours (54 n), the red neighbours' b (4.5 n),
+            # E_S (9 n), B' and Bc out (36 m each), U6^-1 out (18 n), g_b (4.5 n)
+            out["mc_factor"] = 8 * (180 * m + 90 * n)
     return out
 
 
@@ -462,7 +477,8 @@ def run_ours(args, rank, world, local):
                         "precond_setup": float(stage_ms[2]), "krylov": float(stage_ms[3])}}
     # ---- roofline of the dominant kernel class ----------------------------
     hbm, peak_src = peaks()
-    algo = algorithmic_bytes(grid, len(wells), case.solver.precond, sim.ctx.decoupled_form)
+    algo = algorithmic_bytes(grid, len(wells), case.solver.precond,
+                             "condensed" if sim.ctx.condensed else sim.ctx.decoupled_form)
     ktimes = {KCLASS[i]: {"ms": float(ms8[i]), "launches": int(cnt8[i])} for i in range(8)}
     classes = {"ilu_apply": ("ilu_apply",), "spmv": ("spmv",), "decouple": ("decouple",),
                "cell": ("cell",), "face": ("face",)}

@@ -37,6 +37,13 @@ FREEZE_UPWIND_AFTER, FAST_ITERS = 5, 4              # newton.py:56-60
 GROWTH_FACTOR, CUT_FACTOR, TIME_EPS = 2.0, 0.5, 1e-9
 
 
+# condensed multicolour form: flux rows CR_ of a block; primary / secondary
+# unknowns (p, x_1, y_1, T, S_w, S_g) / (x_2, y_2, C_c) for nco = ncg = 2
+CR_ = 6
+COND_P = [0, 1, 3, 5, 6, 7]
+COND_S = [2, 4, 8]
+
+
 class OracleError(Exception):
     pass
 
@@ -837,6 +844,11 @@ class BlockSolver:
         rhs = -ws.resid
         elims = self._eliminate_wells(blocks, rhs)
         self.flags[:] = 0
+        # mcilu: the local rows' block of every cell before decoupling (the
+        # condensed form below needs D[6:, :] after the well fold)
+        dloc = None
+        if self.precond == "mcilu" and not np.any(ws.offd[:, :, CR_:, :] != 0.0):
+            dloc = ws.diag[:, CR_:, :].copy()   # (an assembled system's structure)
         lib().orc_decouple_pass(ctypes.c_int64(rhs.shape[0]), ctypes.c_int64(self.nu),
                                 _p(ws.diag), _p(rhs), _p(ws.offd), _p(ws.adj_ptr),
                                 _p(ws.adj_ids), _p(ws.adj_sides), _p(self.invs), _p(self.flags))
@@ -846,7 +858,8 @@ class BlockSolver:
                 f"diagonal block of cell {cell} is singular at column {int(self.flags[cell] - 1)}")
         if self.precond != "none":
             self._factor()
-        du, iters = self._bicgstab(rhs)
+        cond = self._cond_setup(dloc) if dloc is not None and self.condensed else None
+        du, iters = self._cond_solve(rhs, cond) if cond is not None else self._bicgstab(rhs)
         dbhp = np.zeros(len(elims))
         for w, (cells, wrow, dwdb, resid) in enumerate(elims):
             s = resid
@@ -854,6 +867,164 @@ class BlockSolver:
                 s += float(wrow[p] @ du[cells[p]])
             dbhp[w] = -s / dwdb
         return du, dbhp, iters
+
+    # ------------------------------------------------------------------
+    # Condensed multicolour solve (the device's mcilu default, compact.cu
+    # "condensed form"; no reference counterpart). With the decoupled blocks
+    # A = D^-1 B of an assembled system (rows >= CR_ of B are zero) the
+    # red-eliminated system S9 x_b = g_b (S9 = I - A_br A_rb, g_b = b_b -
+    # A_br b_r) has x_b - g_b in range(E_b), E = [I; E_S] over the primary
+    # unknowns P, E_S = -D[CR_:, S]^-1 D[CR_:, P] from the local rows. So
+    # x_b = g_b + E_b w with the 6-component system
+    #     S6 w = h,  S6 = P S9 E,  h = P (g_b - S9 g_b)
+    # solved by the same BiCGSTAB (linsolve.py:481-578 control flow) from
+    # w = 0, right-preconditioned by the diagonal blocks of S6 (the ILU(0)
+    # pivot blocks restricted to P), stopping on ||r6|| / ||b|| with b the
+    # full decoupled rhs. Then x_r = b_r - A_rb x_b.
+    condensed = True
+
+    def _cond_setup(self, dloc):
+        ws, g = self.ws, self.grid
+        black = self.black
+        m = dloc[black][:, :, COND_S]            # (nb, 3, 3)
+        r = dloc[black][:, :, COND_P]            # (nb, 3, 6)
+        try:
+            es = -np.linalg.solve(m, r)
+        except np.linalg.LinAlgError:
+            return None
+        if not np.all(np.isfinite(es)):
+            return None
+        nb = int(black.sum())
+        e = np.zeros((nb, self.nu, CR_))
+        e[:, COND_P, :] = np.eye(CR_)[None]
+        e[:, COND_S, :] = es
+        a, b = np.asarray(g.conn_a, np.int64), np.asarray(g.conn_b, np.int64)
+        blk_a = black[a]
+        red_c = np.where(blk_a, b, a)
+        blk_c = np.where(blk_a, a, b)
+        a_br = np.where(blk_a[:, None, None], ws.offd[:, 0], ws.offd[:, 1])
+        a_rb = np.where(blk_a[:, None, None], ws.offd[:, 1], ws.offd[:, 0])
+        bpos = np.full(g.ncell, -1, dtype=np.int64)
+        bpos[black] = np.arange(nb)
+
+        def s9(xb):   # (nb, 9) -> S9 xb
+            z = np.zeros((g.ncell, self.nu))
+            z[black] = xb
+            y = np.zeros((g.ncell, self.nu))
+            np.add.at(y, red_c, np.einsum("cij,cj->ci", a_rb, z[blk_c]))   # A_rb xb
+            out = z.copy()
+            np.subtract.at(out, blk_c, np.einsum("cij,cj->ci", a_br, y[red_c]))
+            return out[black]
+
+        # diagonal blocks of S6: P (I - sum_r A_br A_rb) E (the red neighbours' paths)
+        d9 = np.tile(np.eye(self.nu), (nb, 1, 1))
+        prod = np.einsum("cij,cjk->cik", a_br, a_rb)   # A_br(r) A_rb(r) per connection
+        np.subtract.at(d9, bpos[blk_c], prod)
+        u6 = np.einsum("cpi,cij,cjq->cpq", np.eye(self.nu)[COND_P][None].repeat(nb, 0), d9, e)
+        try:
+            u6inv = np.linalg.inv(u6)
+        except np.linalg.LinAlgError as exc:
+            raise SingularCellBlock(f"multicolour ILU(0) pivot block is singular: {exc}")
+        return dict(e=e, s9=s9, u6inv=u6inv, red_c=red_c, blk_c=blk_c, a_rb=a_rb, a_br=a_br,
+                    nb=nb)
+
+    def _cond_solve(self, bfull, C):
+        black, e, s9, nb = self.black, C["e"], C["s9"], C["nb"]
+        red_c, blk_c, a_rb, a_br = C["red_c"], C["blk_c"], C["a_rb"], C["a_br"]
+        # g_b = b_b - A_br b_r
+        gfull = bfull.copy()
+        np.subtract.at(gfull, blk_c, np.einsum("cij,cj->ci", a_br, bfull[red_c]))
+        g9 = gfull[black]
+        h = (g9 - s9(g9))[:, COND_P]
+
+        def op(w):   # S6 w (flat)
+            w = w.reshape(nb, CR_)
+            return s9(np.einsum("cij,cj->ci", e, w))[:, COND_P].ravel()
+
+        def prec(v):
+            return np.einsum("cij,cj->ci", C["u6inv"], v.reshape(nb, CR_)).ravel()
+
+        w, it = self._bicgstab_op(h.ravel(), op, prec, np.sqrt(self._dot(bfull, bfull)))
+        xb = g9 + np.einsum("cij,cj->ci", e, w.reshape(nb, CR_))
+        x = bfull.copy()
+        x[black] = xb
+        xz = np.zeros_like(bfull)
+        xz[black] = xb
+        np.subtract.at(x, red_c, np.einsum("cij,cj->ci", a_rb, xz[blk_c]))
+        return x, it
+
+    def _bicgstab_op(self, b, op, prec, nb):
+        """_bicgstab's control flow (linsolve.py:481-578) on an operator with
+        a right preconditioner; the tolerance base nb is given (the full
+        system's ||b||)."""
+        x = np.zeros_like(b)
+        if nb == 0.0:
+            return x, 0
+        r, rhat = b.copy(), b.copy()
+        p, v = np.zeros_like(b), np.zeros_like(b)
+        rho_old = alpha = omega = 1.0
+        restarted, it, first = False, 0, True
+
+        def restart():
+            r = b - op(x)
+            return r, r.copy()
+
+        while it < self.maxiter:
+            it += 1
+            rho = self._dot(rhat, r)
+            if abs(rho) < BREAKDOWN_EPS * nb * nb or (not first and omega == 0.0):
+                if restarted:
+                    raise Breakdown(f"BiCGSTAB scalar breakdown at iteration {it}")
+                r, rhat = restart()
+                p[:] = 0.0
+                v[:] = 0.0
+                rho_old = alpha = omega = 1.0
+                first, restarted = True, True
+                rho = self._dot(rhat, r)
+                if abs(rho) < BREAKDOWN_EPS * nb * nb:
+                    raise Breakdown("BiCGSTAB restart found a null residual")
+            if first:
+                p[:] = r
+                first = False
+            else:
+                beta = (rho / rho_old) * (alpha / omega)
+                p = r + beta * (p - omega * v)
+            phat = prec(p)
+            v = op(phat)
+            den = self._dot(rhat, v)
+            if abs(den) < BREAKDOWN_EPS * nb * nb:
+                if restarted:
+                    raise Breakdown(f"BiCGSTAB denominator breakdown at iteration {it}")
+                r, rhat = restart()
+                p[:] = 0.0
+                v[:] = 0.0
+                rho_old = alpha = omega = 1.0
+                first, restarted = True, True
+                continue
+            alpha = rho / den
+            s = r - alpha * v
+            if np.sqrt(self._dot(s, s)) / nb <= self.tol:
+                x += alpha * phat
+                return x, it
+            shat = prec(s)
+            t = op(shat)
+            tt = self._dot(t, t)
+            if tt == 0.0:
+                if restarted:
+                    raise Breakdown("BiCGSTAB stagnated (t = 0)")
+                r, rhat = restart()
+                p[:] = 0.0
+                v[:] = 0.0
+                rho_old = alpha = omega = 1.0
+                first, restarted = True, True
+                continue
+            omega = self._dot(t, s) / tt
+            x += alpha * phat + omega * shat
+            r = s - omega * t
+            if np.sqrt(self._dot(r, r)) / nb <= self.tol:
+                return x, it
+            rho_old = rho
+        raise MaxIterations(f"BiCGSTAB did not converge in {self.maxiter} iterations")
 
     def _restart(self, b, x, t):
         self._matvec(x, t)

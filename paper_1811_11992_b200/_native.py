@@ -75,6 +75,7 @@ _SIGS = {
     "isc_set_precond": (ctypes.c_int, [VP, ctypes.c_int32]),
     "isc_set_krylov": (ctypes.c_int, [VP, ctypes.c_int32, ctypes.c_int32]),
     "isc_decoupled_form": (ctypes.c_int, [VP]),
+    "isc_condensed": (ctypes.c_int, [VP]),
     "isc_synth_system": (ctypes.c_int, [VP, ctypes.c_uint64]),
     "isc_synth_system_slab": (ctypes.c_int, [VP, ctypes.c_uint64, ctypes.c_int32]),
     "isc_solve": (ctypes.c_int, [VP, ctypes.c_double, ctypes.c_int32, VP, VP,

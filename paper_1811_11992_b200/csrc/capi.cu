@@ -35,6 +35,8 @@ extern "C" int isc_create(const isc_model_desc* md, const isc_grid_desc* gdsc, i
     ctx->mc_schur = !(e && e[0] == '1');
     const char* e2 = std::getenv("ISC_COMPACT");
     ctx->compact_ok = !(e2 && e2[0] == '0');
+    const char* e3 = std::getenv("ISC_COND");
+    ctx->cond_ok = !(e3 && e3[0] == '0');
   }
   Dims& g = ctx->g;
   g.nx = gdsc->nx; g.ny = gdsc->ny; g.nz = gdsc->nz;
@@ -183,13 +185,15 @@ extern "C" int isc_destroy(isc_ctx* ctx) {
                   ctx->pk, ctx->vk, ctx->phat, ctx->shat, ctx->sk, ctx->tk, ctx->sc,
                   ctx->partial, ctx->partial2, ctx->fbuf, ctx->flags, ctx->fail_d, ctx->ccnz_d, ctx->st_c, ctx->accn_c, ctx->stage,
                   ctx->halo_send_lo, ctx->halo_send_hi, ctx->halo_recv_lo, ctx->halo_recv_hi,
-                  ctx->gm_V, ctx->gm_h, ctx->cbp, ctx->cmid};
+                  ctx->gm_V, ctx->gm_h, ctx->cbp, ctx->cmid, ctx->ces, ctx->cbc, ctx->cg9,
+                  ctx->ch6, ctx->cfail_d};
   if (ctx->comm.nccl && nccl_api().CommDestroy) nccl_api().CommDestroy(ctx->comm.nccl);
   free_ilu(ctx);
   for (void* p : ptrs)
     if (p) cudaFree(p);
   if (ctx->wout_h) cudaFreeHost(ctx->wout_h);
   if (ctx->bad_h) cudaFreeHost(ctx->bad_h);
+  if (ctx->cfail_h) cudaFreeHost(ctx->cfail_h);
   if (ctx->sc_h) cudaFreeHost(ctx->sc_h);
   for (auto& e : ctx->ev)
     if (e) cudaEventDestroy(e);
@@ -608,6 +612,30 @@ extern "C" int isc_synth_system(isc_ctx* ctx, uint64_t seed) {
 // the Gauss-Jordan pass and queues the read-back of the first singular cell;
 // decouple_check (after a synchronisation) reports it. isc_solve queues the
 // preconditioner setup in between, so the two share one synchronisation.
+// condensed-form buffers (lazy; false when the device has no room: the
+// 9-component compact form is used instead)
+static bool cond_alloc(isc_ctx* ctx) {
+  if (ctx->ces) return true;
+  const size_t half = (size_t)ctx->g.half, n = (size_t)ctx->g.n;
+  if (cudaMalloc(&ctx->ces, (size_t)NCS * CR * half * 8) != cudaSuccess ||
+      cudaMalloc(&ctx->cbc, (size_t)NDIR * CR * CR * half * 8) != cudaSuccess ||
+      cudaMalloc(&ctx->cg9, (size_t)NU * n * 8) != cudaSuccess ||
+      cudaMalloc(&ctx->ch6, (size_t)CR * n * 8) != cudaSuccess ||
+      cudaMalloc(&ctx->cfail_d, 4) != cudaSuccess ||
+      cudaMallocHost(&ctx->cfail_h, 4) != cudaSuccess) {
+    cudaGetLastError();
+    for (void* p : {(void*)ctx->ces, (void*)ctx->cbc, (void*)ctx->cg9, (void*)ctx->ch6,
+                    (void*)ctx->cfail_d})
+      if (p) cudaFree(p);
+    if (ctx->cfail_h) cudaFreeHost(ctx->cfail_h);
+    ctx->ces = ctx->cbc = ctx->cg9 = ctx->ch6 = nullptr;
+    ctx->cfail_d = ctx->cfail_h = nullptr;
+    ctx->cond_ok = false;
+    return false;
+  }
+  return true;
+}
+
 static int decouple_enqueue(isc_ctx* ctx, int64_t* bad_cell, int32_t* bad_col) {
   const int64_t n = ctx->g.n;
   cudaStream_t st = ctx->stream;
@@ -654,7 +682,18 @@ static int decouple_enqueue(isc_ctx* ctx, int64_t* bad_cell, int32_t* bad_col) {
                             DCT_SMEM));
     k_decouple_compact_t<<<grid1d(owned, DCT_THREADS), DCT_THREADS, DCT_SMEM, st>>>(
         ctx->g, ctx->diag, ctx->rhs, ctx->flags, ctx->bad_d);
+    // condensed form (single GPU, BiCGSTAB): E_S of the black cells from the
+    // local rows, which the compact decoupling leaves in place
+    ctx->cond_es = false;
+    if (ctx->cond_ok && !ctx->comm.active() && cond_alloc(ctx)) {
+      CK(cudaMemsetAsync(ctx->cfail_d, 0, 4, st));
+      k_cond_es<<<grid1d(ctx->g.tw_hi - ctx->g.tw_lo, 256), 256, 0, st>>>(ctx->g, ctx->diag,
+                                                                          ctx->ces, ctx->cfail_d);
+      CK(cudaMemcpyAsync(ctx->cfail_h, ctx->cfail_d, 4, cudaMemcpyDeviceToHost, st));
+      ctx->cond_es = true;
+    }
   } else {
+    ctx->cond_es = false;
     // once per process (thread-safe static init: hub ranks share the process)
     static const cudaError_t attr = cudaFuncSetAttribute(
         k_decouple_ws, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(WsSmem));
@@ -733,6 +772,7 @@ extern "C" int isc_set_rhs(isc_ctx* ctx, const double* d_src) {
 // launches the factorisation and queues the read-back of its status,
 // precond_check reports it after a synchronisation.
 static int precond_enqueue(isc_ctx* ctx) {
+  ctx->cond = false;
   if (ctx->precond == ISC_PRECOND_NONE) return ISC_OK;
   cudaStream_t st = ctx->stream;
   STAGE(stage_begin(ctx, 2));
@@ -761,12 +801,25 @@ static int precond_enqueue(isc_ctx* ctx) {
     if (ctx->compact) {
       // the reduced rhs g_b is formed on the way (red neighbours' b: halo on slabs)
       if (cross && halo_exchange(ctx, ctx->rhs, NU)) return ISC_CUDA_ERROR;
-      CK(cudaFuncSetAttribute(k_mc_factor_compact, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                              (int)sizeof(McfcSmem)));
-      k_mc_factor_compact<<<grid1d(ctx->g.tw_hi - ctx->g.tw_lo, MCFC_CELLS), dim3(MCFC_CELLS, NU),
-                            sizeof(McfcSmem), st>>>(
-          ctx->g, ctx->offd, ctx->diag, ctx->mc_uinv, ctx->cbp, ctx->fail_d, ctx->rhs, ctx->rk,
-          ctx->rhat);
+      // condensed form when the decoupling's E_S are usable (checked after
+      // its synchronisation; isc_solve refactors in the 9-component form
+      // otherwise) and the iteration is BiCGSTAB
+      ctx->cond = ctx->cond_es && !(ctx->cfail_h && *ctx->cfail_h && ctx->decoupled) &&
+                  ctx->krylov == ISC_KRYLOV_BICGSTAB;
+      const int fblocks = grid1d(ctx->g.tw_hi - ctx->g.tw_lo, MCFC_CELLS);
+      if (ctx->cond) {
+        CK(cudaFuncSetAttribute(k_mc_factor_compact<true>,
+                                cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(McfcSmem)));
+        k_mc_factor_compact<true><<<fblocks, dim3(MCFC_CELLS, NU), sizeof(McfcSmem), st>>>(
+            ctx->g, ctx->offd, ctx->diag, ctx->mc_uinv, ctx->cbp, ctx->fail_d, ctx->rhs,
+            ctx->cg9, nullptr, ctx->ces, ctx->cbc);
+      } else {
+        CK(cudaFuncSetAttribute(k_mc_factor_compact<false>,
+                                cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(McfcSmem)));
+        k_mc_factor_compact<false><<<fblocks, dim3(MCFC_CELLS, NU), sizeof(McfcSmem), st>>>(
+            ctx->g, ctx->offd, ctx->diag, ctx->mc_uinv, ctx->cbp, ctx->fail_d, ctx->rhs, ctx->rk,
+            ctx->rhat, nullptr, nullptr);
+      }
       ctx->gb_fresh = true;
     } else
       k_mc_factor<<<grid1d(nblack, 32), dim3(32, NU), 0, st>>>(ctx->g, ctx->offd, ctx->mc_uinv,
@@ -919,6 +972,8 @@ extern "C" int isc_decoupled_form(const isc_ctx* ctx) {
   return !ctx->decoupled ? 0 : (ctx->compact ? 2 : 1);
 }
 
+extern "C" int isc_condensed(const isc_ctx* ctx) { return ctx->cond ? 1 : 0; }
+
 extern "C" int isc_set_krylov(isc_ctx* ctx, int32_t krylov, int32_t restart) {
   if (krylov != ISC_KRYLOV_BICGSTAB && krylov != ISC_KRYLOV_GMRES) {
     g_err = "unknown Krylov method";
@@ -928,6 +983,7 @@ extern "C" int isc_set_krylov(isc_ctx* ctx, int32_t krylov, int32_t restart) {
     g_err = "GMRES restart length out of range (1..31, 0 = default)";
     return ISC_BAD_ARGUMENT;
   }
+  if (krylov != ctx->krylov) ctx->factored = false;   // (the condensed form is BiCGSTAB's)
   ctx->krylov = krylov;
   if (restart > 0) ctx->gm_m = restart;
   return ISC_OK;
@@ -948,6 +1004,11 @@ extern "C" int isc_solve(isc_ctx* ctx, double tol, int32_t maxiter, double* d_du
   if (dec) {
     int s = decouple_check(ctx, bad_cell, bad_col);
     if (s) return s;
+  }
+  if (fac && ctx->cond && *ctx->cfail_h) {
+    // a cell's local rows cannot be condensed: the 9-component compact form
+    STAGE(precond_enqueue(ctx));
+    STAGE(sync_stream(ctx));
   }
   if (fac) {
     int s = precond_check(ctx, bad_cell);

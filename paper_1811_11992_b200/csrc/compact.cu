@@ -31,6 +31,15 @@
 namespace isc {
 
 constexpr int CR = ROW_OS;   // flux rows of an assembled off-diagonal block
+// condensed form (below): primary / secondary unknowns of a cell
+constexpr int NCS = NU - CR;   // secondary unknowns per cell (3)
+__host__ __device__ constexpr int cprim(int p) {   // p-th primary unknown
+  return p + (p >= NCO ? 1 : 0) + (p >= NCO + NCG - 1 ? 1 : 0);
+}
+__host__ __device__ constexpr int csec(int i) {    // i-th secondary unknown
+  return i == 0 ? NCO : (i == 1 ? NCO + NCG : CCC);
+}
+static_assert(cprim(CR - 1) == CSG && csec(NCS - 1) == CCC, "condensed unknown split");
 
 // cp.async (LDGSTS): global -> shared without register staging
 __device__ __forceinline__ void cp_async8(void* smem, const void* gmem) {
@@ -405,17 +414,26 @@ struct McfcStage {
 struct McfcSmem {
   McfcStage st[2];
   double bpsh[CR][CR][MCFC_CELLS];   // B'_bd = B_bd[:CR, :] D_nb^-1[:, :CR]
+  double bcsh[CR][CR][MCFC_CELLS];   // condensed: Bc_nb,back = B_nb,back[:CR, :] E_b
   double colk[NU][MCFC_CELLS];
   int pivs[MCFC_CELLS];
 };
 
+// COND: the condensed form (see "condensed form" below): U6 = I - Dc_b^-1
+// sum_d B'_bd Bc_nb,back with Bc_nb,back = B_nb,back[:CR, :] E_b written to
+// cbc (red neighbour's index, direction back to b) and the 6 x 6 inverse in
+// uinv; g_b (9 rows) to g1 only.
+template <bool COND>
 __global__ void __launch_bounds__(MCFC_CELLS * NU, MCFC_MINB) k_mc_factor_compact(
     Dims g, const double* __restrict__ offd, const double* __restrict__ dinv,
     double* __restrict__ uinv, double* __restrict__ bp, int* fail, const double* __restrict__ b,
-    double* __restrict__ g1, double* __restrict__ g2) {
+    double* __restrict__ g1, double* __restrict__ g2, const double* __restrict__ es,
+    double* __restrict__ cbc) {
+  constexpr int NC = COND ? CR : NU;   // order of the pivot block
   extern __shared__ __align__(16) unsigned char mcfc_raw[];
   McfcSmem& S = *reinterpret_cast<McfcSmem*>(mcfc_raw);
   auto& bpsh = S.bpsh;
+  auto& bcsh = S.bcsh;
   auto& colk = S.colk;
   auto& pivs = S.pivs;
   const int64_t n = g.n;
@@ -449,14 +467,25 @@ __global__ void __launch_bounds__(MCFC_CELLS * NU, MCFC_MINB) k_mc_factor_compac
   };
   // Register-blocked products (the smem pipe bounds this kernel): thread
   // u = 3 tq + tc owns the 2x2 block B'[2tq.., 2tc..] and the 2x3 block
-  // Q[2tq.., 3tc..]; each entry is summed in the same order as a plain loop
+  // Q[2tq.., 3tc..] (condensed: the 2x2 blocks Bc[2tq.., 2tc..] and
+  // Q6[2tq.., 2tc..]); each entry is summed in the same order as a plain loop
   double grow[2] = {0.0, 0.0};   // (sum_d B_bd b_r(nb))[2tq + qq], by the tc == 0 threads
-  double qacc[2][3];             // Q[2tq + qq][3tc + uu] = sum_d B'_bd B_back[:CR, :]
+  constexpr int QW = COND ? 2 : 3;
+  double qacc[2][QW];            // Q[2tq + qq][QW tc + uu] = sum_d B'_bd B_back[:CR, :] (or Bc)
 #pragma unroll
   for (int qq = 0; qq < 2; ++qq)
 #pragma unroll
-    for (int uu = 0; uu < 3; ++uu) qacc[qq][uu] = 0.0;
+    for (int uu = 0; uu < QW; ++uu) qacc[qq][uu] = 0.0;
   const int tq = u / 3, tc = u - 3 * (u / 3);
+  // condensed: E_b's columns 2tc, 2tc + 1 (the columns of Bc this thread forms)
+  double esr[NCS][2];
+  if (COND) {
+#pragma unroll
+    for (int ii = 0; ii < NCS; ++ii)
+#pragma unroll
+      for (int ss = 0; ss < 2; ++ss)
+        esr[ii][ss] = live ? es[(int64_t)(ii * CR + 2 * tc + ss) * g.half + t] : 0.0;
+  }
   issue(0, 0);
   cp_async_commit();
 #pragma unroll 1
@@ -498,19 +527,39 @@ __global__ void __launch_bounds__(MCFC_CELLS * NU, MCFC_MINB) k_mc_factor_compac
           bp[(int64_t)((d * CR + q) * CR + s2) * g.half + t] = sb;
         }
       }
+      if (COND) {
+        // Bc_nb,back[q][p] = B_back[q][P[p]] + sum_i B_back[q][S[i]] E_b[i][p], stored
+        // for the red neighbour (its index, direction opposite(d))
+        const int64_t tr = nb - g.ph * (int64_t)plane_of(g, nb);
+#pragma unroll
+        for (int qq = 0; qq < 2; ++qq) {
+          const int q = 2 * tq + qq;
+#pragma unroll
+          for (int ss = 0; ss < 2; ++ss) {
+            const int p = 2 * tc + ss;
+            const int pp = p + (p >= NCO ? 1 : 0) + (p >= NCO + NCG - 1 ? 1 : 0);
+            double v = T.o[q][pp][ls];
+#pragma unroll
+            for (int ii = 0; ii < NCS; ++ii) v += T.o[q][csec(ii)][ls] * esr[ii][ss];
+            bcsh[q][p][ls] = v;
+            cbc[(int64_t)((opposite(d) * CR + q) * CR + p) * g.half + tr] = v;
+          }
+        }
+      }
     }
     __syncthreads();
-    if (nb >= 0) {   // Q[2tq.., 3tc..] += B'_bd[2tq.., :] B_back[:CR, 3tc..]
+    if (nb >= 0) {   // Q[2tq.., QW tc..] += B'_bd[2tq.., :] (B_back[:CR, QW tc..] or Bc[:, 2tc..])
       double bpr[2][CR];
 #pragma unroll
       for (int qq = 0; qq < 2; ++qq)
 #pragma unroll
         for (int r = 0; r < CR; ++r) bpr[qq][r] = bpsh[2 * tq + qq][r][ls];
 #pragma unroll
-      for (int uu = 0; uu < 3; ++uu) {
+      for (int uu = 0; uu < QW; ++uu) {
         double ocol[CR];
 #pragma unroll
-        for (int r = 0; r < CR; ++r) ocol[r] = T.o[r][3 * tc + uu][ls];
+        for (int r = 0; r < CR; ++r)
+          ocol[r] = COND ? bcsh[r][2 * tc + uu][ls] : T.o[r][3 * tc + uu][ls];
 #pragma unroll
         for (int qq = 0; qq < 2; ++qq) {
           double sq = 0.0;
@@ -530,18 +579,18 @@ __global__ void __launch_bounds__(MCFC_CELLS * NU, MCFC_MINB) k_mc_factor_compac
 #pragma unroll
     for (int qq = 0; qq < 2; ++qq)
 #pragma unroll
-      for (int uu = 0; uu < 3; ++uu) qsh[2 * tq + qq][3 * tc + uu][ls] = qacc[qq][uu];
+      for (int uu = 0; uu < QW; ++uu) qsh[2 * tq + qq][QW * tc + uu][ls] = qacc[qq][uu];
     if (tc == 0) {
       colk[2 * tq][ls] = grow[0];
       colk[2 * tq + 1][ls] = grow[1];
     }
     __syncthreads();
 #pragma unroll
-    for (int q = 0; q < CR; ++q) qcol[q] = qsh[q][u][ls];
+    for (int q = 0; q < CR; ++q) qcol[q] = u < NC ? qsh[q][u][ls] : 0.0;
   }
   cp_async_wait<0>();
   auto& dsh = S.st[0].d;
-  // U[:, u] = e_u - D_b^-1[:, :CR] Q[:, u]
+  // U[:, u] = e_u - D_b^-1[:, :CR] Q[:, u]  (condensed: rows P of D_b^-1)
   if (in) {
 #pragma unroll
     for (int e = 0; e < CR; ++e) {
@@ -556,46 +605,47 @@ __global__ void __launch_bounds__(MCFC_CELLS * NU, MCFC_MINB) k_mc_factor_compac
     for (int r = 0; r < CR; ++r) m += dsh[u][r][ls] * colk[r][ls];
     const double gv = b[(int64_t)u * n + c] - m;
     g1[(int64_t)u * n + c] = gv;
-    g2[(int64_t)u * n + c] = gv;
+    if (g2) g2[(int64_t)u * n + c] = gv;
   }
-  double ucol[NU], icol[NU];
+  double ucol[NC], icol[NC];
 #pragma unroll
-  for (int q = 0; q < NU; ++q) {
+  for (int q = 0; q < NC; ++q) {
+    const int pq = COND ? q + (q >= NCO ? 1 : 0) + (q >= NCO + NCG - 1 ? 1 : 0) : q;
     double s = 0.0;
 #pragma unroll
-    for (int r = 0; r < CR; ++r) s += dsh[q][r][ls] * qcol[r];
+    for (int r = 0; r < CR; ++r) s += dsh[pq][r][ls] * qcol[r];
     ucol[q] = (q == u ? 1.0 : 0.0) - s;
     icol[q] = (q == u) ? 1.0 : 0.0;
   }
   {
     double m = 0.0;
 #pragma unroll
-    for (int r = 0; r < NU; ++r) m = fmax(m, fabs(ucol[r]));
+    for (int r = 0; r < NC; ++r) m = fmax(m, fabs(ucol[r]));
     S.st[1].b[0][u][ls] = m;
   }
   __syncthreads();
   double amax = 0.0;
 #pragma unroll
-  for (int q = 0; q < NU; ++q) amax = fmax(amax, S.st[1].b[0][q][ls]);
+  for (int q = 0; q < NC; ++q) amax = fmax(amax, S.st[1].b[0][q][ls]);
   const double tol = 1e-13 * amax;
   __syncthreads();
 #pragma unroll
-  for (int kk = 0; kk < NU; ++kk) {
+  for (int kk = 0; kk < NC; ++kk) {
     if (u == kk) {
       int piv = kk;
       double pv = fabs(ucol[kk]);
 #pragma unroll
-      for (int r = kk + 1; r < NU; ++r) {
+      for (int r = kk + 1; r < NC; ++r) {
         const double v = fabs(ucol[r]);
         if (v > pv) { pv = v; piv = r; }
       }
       if (live && (pv <= tol || amax == 0.0)) atomicMin(fail, 1);
 #pragma unroll
-      for (int r = 0; r < NU; ++r) {
+      for (int r = 0; r < NC; ++r) {
         double v = ucol[r];
         if (r == kk) {
 #pragma unroll
-          for (int q = kk + 1; q < NU; ++q) if (q == piv) v = ucol[q];
+          for (int q = kk + 1; q < NC; ++q) if (q == piv) v = ucol[q];
         } else if (r == piv) {
           v = ucol[kk];
         }
@@ -608,23 +658,237 @@ __global__ void __launch_bounds__(MCFC_CELLS * NU, MCFC_MINB) k_mc_factor_compac
     if (piv != kk) {
       const double t0 = ucol[kk], t1 = icol[kk];
 #pragma unroll
-      for (int q = kk + 1; q < NU; ++q)
+      for (int q = kk + 1; q < NC; ++q)
         if (q == piv) { ucol[kk] = ucol[q]; icol[kk] = icol[q]; ucol[q] = t0; icol[q] = t1; }
     }
     const double dv = 1.0 / colk[kk][ls];
     ucol[kk] *= dv;
     icol[kk] *= dv;
 #pragma unroll
-    for (int r = 0; r < NU; ++r) {
+    for (int r = 0; r < NC; ++r) {
       if (r == kk) continue;
       const double f = colk[r][ls];
       if (f != 0.0) { ucol[r] -= f * ucol[kk]; icol[r] -= f * icol[kk]; }
     }
     __syncthreads();
   }
-  if (live) {
+  if (live && u < NC) {
 #pragma unroll
-    for (int r = 0; r < NU; ++r) uinv[(int64_t)(r * NU + u) * n + c] = icol[r];
+    for (int r = 0; r < NC; ++r) uinv[(int64_t)(r * NC + u) * n + c] = icol[r];
+  }
+}
+
+// ------------------------------------------------------ condensed form
+//
+// The local rows ROW_OS.. of an assembled system (the oil and gas mole-
+// fraction sums and the coke balance) have no flux: D[CR:, :] x_c = b[CR:]
+// involves the cell's own unknowns only. They fix the secondary unknowns
+// S = (last x, last y, C_c) of every cell in terms of the six primary ones
+// P = (p, x_1, y_1, T, S_w, S_g):  x_S = E_S x_P + ...,  E_S = -D[CR:, S]^-1
+// D[CR:, P]  (3 x 6 per cell). With E = [I; E_S] (9 x 6):
+//   D^-1[:, :CR] = E Dc^-1,  Dc^-1 = D^-1[P, :CR]   (D E = [D[:CR,:] E; 0]),
+// so the decoupled red-eliminated operator S9 z = z - D_b^-1[:, :CR] sum_d
+// B'_bd y(z) (k_cc_black) maps z - range(E_b) into range(E_b), and its
+// solution is x_b = g_b + E_b w with the 6-component
+//   S6 w = w - Dc_b^-1 sum_d B'_bd sum_d' Bc_rd' w(nb) = h,
+//   h = Dc_b^-1 sum_d B'_bd y_r(g),  Bc_rd = B_rd[:CR, :] E_b (6 x 6),
+// y_r(g) the raw red pass on the reduced rhs g. BiCGSTAB with the
+// multicolour preconditioner then runs on S6 (block-Jacobi U6 = I -
+// Dc_b^-1 sum_d B'_bd Bc_r,back, the same ILU(0) pivot restricted to P):
+// 6 x 36 + 6 x 36 + 36 matrix values per red/black pair and product instead
+// of 6 x 49 + 6 x 36 + 54, 6-component Krylov vectors and a 36-value U6^-1
+// instead of 81. It starts at x_b = g_b (w = 0) instead of 0, one product
+// (for h) before the first iteration; on C2/C3 that start saves one
+// iteration at LINEAR_TOL 1e-5 and 1e-10. Stopping test
+// ||r6|| / ||b|| (r9 = E r6: the constraint rows' components of the full
+// residual are left out of the norm).
+
+// E_S of the cell at storage position c from its diagonal block's local rows
+// (Gauss-Jordan with partial pivoting on [D[CR:, S] | D[CR:, P]]); false when
+// a pivot is below 1e-12 of max|D[CR:, S]| or not finite (the form is then
+// not used for this system).
+__device__ __forceinline__ bool cond_es(const double* __restrict__ diag, int64_t n, int64_t c,
+                                        double (&es)[NCS][CR]) {
+  double m[NCS][NCS + CR];
+  double mmax = 0.0;
+#pragma unroll
+  for (int i = 0; i < NCS; ++i) {
+#pragma unroll
+    for (int j = 0; j < NCS; ++j) {
+      m[i][j] = diag[(int64_t)((CR + i) * NU + csec(j)) * n + c];
+      mmax = fmax(mmax, fabs(m[i][j]));
+    }
+#pragma unroll
+    for (int p = 0; p < CR; ++p) m[i][NCS + p] = diag[(int64_t)((CR + i) * NU + cprim(p)) * n + c];
+  }
+  bool ok = mmax > 0.0 && mmax < INFINITY;
+#pragma unroll
+  for (int k = 0; k < NCS; ++k) {
+    int piv = k;
+    double pv = fabs(m[k][k]);
+#pragma unroll
+    for (int r = k + 1; r < NCS; ++r)
+      if (fabs(m[r][k]) > pv) { pv = fabs(m[r][k]); piv = r; }
+    ok = ok && pv > 1e-12 * mmax;
+#pragma unroll
+    for (int r = k + 1; r < NCS; ++r) {
+      if (r != piv) continue;
+#pragma unroll
+      for (int j = 0; j < NCS + CR; ++j) {
+        const double t = m[k][j];
+        m[k][j] = m[r][j];
+        m[r][j] = t;
+      }
+    }
+    const double dv = 1.0 / m[k][k];
+#pragma unroll
+    for (int j = 0; j < NCS + CR; ++j) m[k][j] *= dv;
+#pragma unroll
+    for (int r = 0; r < NCS; ++r) {
+      if (r == k) continue;
+      const double f = m[r][k];
+#pragma unroll
+      for (int j = 0; j < NCS + CR; ++j) m[r][j] -= f * m[k][j];
+    }
+  }
+#pragma unroll
+  for (int i = 0; i < NCS; ++i)
+#pragma unroll
+    for (int p = 0; p < CR; ++p) {
+      es[i][p] = -m[i][NCS + p];
+      ok = ok && isfinite(es[i][p]);
+    }
+  return ok;
+}
+
+// E_S of every owned black cell into es[(i*CR + p)*half + t]; *fail = 1 when
+// a cell's local block is not usable (before or after the compact
+// decoupling: that keeps D^-1[:, :CR] in slots < CR*NU and leaves the local
+// rows' slots alone)
+__global__ void k_cond_es(Dims g, const double* __restrict__ diag, double* __restrict__ es,
+                          int* fail) {
+  const int64_t t = g.tw_lo + (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= g.tw_hi) return;
+  const int64_t c = colour_pos(g, 1, t);
+  double e[NCS][CR];
+  if (!cond_es(diag, g.n, c, e)) atomicOr(fail, 1);
+#pragma unroll
+  for (int i = 0; i < NCS; ++i)
+#pragma unroll
+    for (int p = 0; p < CR; ++p) es[(int64_t)(i * CR + p) * g.half + t] = e[i][p];
+}
+
+// Red pass of S6: y_r = sum_d Bc_rd w(nb) (thread (red cell, row r < CR));
+// Bc stored per red cell index t: cbc[((d*CR + r)*CR + p)*half + t]
+__global__ void __launch_bounds__(32 * CR, CC_MINB) k_cc6_red(Dims g, const double* __restrict__ cbc,
+                                                              double* __restrict__ z,
+                                                              const double* stop) {
+  if (stopped(stop)) return;
+  const int64_t n = g.n;
+  const int ls = threadIdx.x, r = threadIdx.y;
+  const int64_t t = g.tw_lo + (int64_t)blockIdx.x * 32 + ls;
+  if (t >= g.tw_hi) return;
+  const int64_t c = colour_pos(g, 0, t);
+  int i, j, k;
+  const int64_t cell = locate(g, c, i, j, k);
+  double s = 0.0;
+#pragma unroll
+  for (int d = 0; d < NDIR; ++d) {
+    const int64_t nb = nb_pos(g, cell, i, j, k, d);
+    if (nb < 0) continue;
+    const double* blk = cbc + (int64_t)((d * CR + r) * CR) * g.half + t;
+    double tt = 0.0;
+#pragma unroll
+    for (int p = 0; p < CR; ++p) tt += blk[(int64_t)p * g.half] * z[(int64_t)p * n + nb];
+    s += tt;
+  }
+  z[(int64_t)r * n + c] = s;
+}
+
+// Black pass of S6 (H = false): v_b = z_b - Dc_b^-1 sum_d B'_bd y(nb), with
+// K dot products as k_cc_black; H = true: the rhs h = Dc_b^-1 sum_d B'_bd
+// y(nb) into v, out2 and out3 (no dots).
+template <int K, bool H>
+__global__ void __launch_bounds__(32 * CR, CC_MINB) k_cc6_black(
+    Dims g, const double* __restrict__ bp, const double* __restrict__ dinv,
+    const double* __restrict__ z, double* __restrict__ v, const double* __restrict__ w0,
+    const double* __restrict__ w1, double* partial, int stride, int slot0, const double* stop,
+    double* __restrict__ out2, double* __restrict__ out3) {
+  if (stopped(stop)) return;   // block-uniform: before the barrier
+  __shared__ double ts[CR][32];
+  const int64_t n = g.n;
+  const int ls = threadIdx.x, r = threadIdx.y;
+  const int64_t t = g.tw_lo + (int64_t)blockIdx.x * 32 + ls;
+  const bool live = t < g.tw_hi;
+  int64_t c = 0;
+  double acc[K > 0 ? K : 1];
+#pragma unroll
+  for (int q = 0; q < (K > 0 ? K : 1); ++q) acc[q] = 0.0;
+  if (live) {
+    c = colour_pos(g, 1, t);
+    int i, j, k;
+    const int64_t cell = locate(g, c, i, j, k);
+    double s = 0.0;
+#pragma unroll
+    for (int d = 0; d < NDIR; ++d) {
+      const int64_t nb = nb_pos(g, cell, i, j, k, d);
+      if (nb < 0) continue;
+      const double* blk = bp + (int64_t)((d * CR + r) * CR) * g.half + t;
+      double tt = 0.0;
+#pragma unroll
+      for (int e = 0; e < CR; ++e) tt += blk[(int64_t)e * g.half] * z[(int64_t)e * n + nb];
+      s += tt;
+    }
+    ts[r][ls] = s;
+  }
+  __syncthreads();
+  if (live) {
+    const int q = r;   // output row q of Dc^-1 = D^-1[P[q], :CR]
+    const int pq = q + (q >= NCO ? 1 : 0) + (q >= NCO + NCG - 1 ? 1 : 0);
+    double m = 0.0;
+#pragma unroll
+    for (int rr = 0; rr < CR; ++rr) m += dinv[(int64_t)(pq * CR + rr) * n + c] * ts[rr][ls];
+    if (H) {
+      v[(int64_t)q * n + c] = m;
+      out2[(int64_t)q * n + c] = m;
+      out3[(int64_t)q * n + c] = m;
+    } else {
+      const double val = z[(int64_t)q * n + c] - m;
+      v[(int64_t)q * n + c] = val;
+      const double wd = K == 1 ? w0[(int64_t)q * n + c] : (K == 2 ? w1[(int64_t)q * n + c] : 0.0);
+      if (K == 1) acc[0] += val * wd;
+      if (K == 2) { acc[0] += val * val; acc[K - 1] += val * wd; }
+    }
+  }
+#pragma unroll
+  for (int q = 0; q < K; ++q) {
+    double x = acc[q];
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) x += __shfl_down_sync(0xffffffffu, x, o);
+    if (ls == 0) partial[(int64_t)q * stride * CR + (int64_t)(slot0 + blockIdx.x) * CR + r] = x;
+  }
+}
+
+// x_b = g_b + E_b w_b (9 rows out of the 6-component w in rows 0..CR-1 of x)
+__global__ void k_cond_expand(Dims g, const double* __restrict__ es,
+                              const double* __restrict__ gb, double* __restrict__ x) {
+  const int64_t n = g.n;
+  for (int64_t t = g.tw_lo + (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < g.tw_hi;
+       t += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t c = colour_pos(g, 1, t);
+    double w[CR];
+#pragma unroll
+    for (int p = 0; p < CR; ++p) w[p] = x[(int64_t)p * n + c];
+#pragma unroll
+    for (int p = 0; p < CR; ++p)
+      x[(int64_t)cprim(p) * n + c] = gb[(int64_t)cprim(p) * n + c] + w[p];
+#pragma unroll
+    for (int i = 0; i < NCS; ++i) {
+      double s = 0.0;
+#pragma unroll
+      for (int p = 0; p < CR; ++p) s += es[(int64_t)(i * CR + p) * g.half + t] * w[p];
+      x[(int64_t)csec(i) * n + c] = gb[(int64_t)csec(i) * n + c] + s;
+    }
   }
 }
 

@@ -238,8 +238,15 @@ static int sc_warps(const isc_ctx* ctx) { return ctx->compact ? CR : NU; }
 // system's residual (its red rows vanish identically), the Krylov vectors
 // on the black half, each product reading every off-diagonal block once.
 // Control flow as bicgstab() / linsolve.py:481-578.
-static int bicgstab_schur(isc_ctx* ctx, double tol, int maxiter, int* iters) {
-  const int64_t len = (int64_t)NU * ctx->g.n;
+//
+// NC = CR: the condensed form (compact.cu): the same iteration on S6 w = h
+// (6-component vectors, Bc / B' / Dc^-1 passes, U6^-1), started at x_b = g_b,
+// and x_b = g_b + E_b w at the end.
+template <int NC>
+static int bicgstab_schur_t(isc_ctx* ctx, double tol, int maxiter, int* iters) {
+  constexpr bool cnd = NC == CR;
+  const int64_t len = (int64_t)NU * ctx->g.n;      // the full decoupled rhs b
+  const int64_t lenv = (int64_t)NC * ctx->g.n;     // Krylov vectors (black positions used)
   const Dims& g = ctx->g;
   cudaStream_t st = ctx->stream;
   Kry K{ctx, len};
@@ -247,7 +254,7 @@ static int bicgstab_schur(isc_ctx* ctx, double tol, int maxiter, int* iters) {
          *v = ctx->vk, *phat = ctx->phat, *shat = ctx->shat, *s = ctx->sk, *t = ctx->tk;
   const double* uinv = ctx->mc_uinv;
   const int bh = grid1d(g.tw_hi - g.tw_lo, 32);   // blocks of a half pass (owned planes)
-  CK(cudaMemsetAsync(x, 0, len * 8, st));
+  CK(cudaMemsetAsync(x, 0, lenv * 8, st));
   *iters = 0;
   // control state first (the dots below write their slots after this push);
   // ||b||, the breakdown threshold and r^.r are formed on the device, so the
@@ -262,7 +269,22 @@ static int bicgstab_schur(isc_ctx* ctx, double tol, int maxiter, int* iters) {
   TRY(K.dot(b, b, S_BB));   // ||b|| of the full decoupled rhs (the reference's tolerance base)
   // p, v and t need no clearing: p and v are read only after the first
   // iteration wrote them (S_FIRST), t only where the black pass wrote it
-  if (ctx->compact && ctx->gb_fresh) {
+  if (cnd) {
+    // h = Dc_b^-1 sum_d B'_bd y_r(g_b): the raw red pass on g_b (y into its
+    // red positions), then the black pass's product part, into r, rhat, ch6
+    KScope ks(ctx, KT_SPMV);
+    if (ctx->gb_fresh) {
+      ctx->gb_fresh = false;
+      k_cc_red<<<bh, dim3(32, CR), 0, st>>>(g, ctx->offd, ctx->ccnz_d, ctx->cg9, nullptr);
+      k_cc6_black<0, true><<<bh, dim3(32, CR), 0, st>>>(g, ctx->cbp, ctx->diag, ctx->cg9, r,
+                                                        nullptr, nullptr, ctx->partial, 0, 0,
+                                                        nullptr, rhat, ctx->ch6);
+      ctx->launches += 2;
+    } else {
+      CK(cudaMemcpyAsync(r, ctx->ch6, lenv * 8, cudaMemcpyDeviceToDevice, st));
+      CK(cudaMemcpyAsync(rhat, ctx->ch6, lenv * 8, cudaMemcpyDeviceToDevice, st));
+    }
+  } else if (ctx->compact && ctx->gb_fresh) {
     ctx->gb_fresh = false;   // g_b already in r and rhat (k_mc_factor_compact)
   } else {
     TRY(halo_exchange(ctx, b, NU));   // slabs: red neighbours on other ranks
@@ -294,6 +316,11 @@ static int bicgstab_schur(isc_ctx* ctx, double tol, int maxiter, int* iters) {
   const int bh1 = split ? grid1d(gh.tw_hi - gh.tw_lo, 32) : 0;
   const int bparts = split ? bi + bl1 + bh1 : bh;   // black-pass partial slots (blocks)
   auto red_pass = [&](double* z, const double* stop) -> int {
+    if (cnd) {   // (single GPU)
+      k_cc6_red<<<bh, dim3(32, CR), 0, st>>>(g, ctx->cbc, z, stop);
+      ++ctx->launches;
+      return cudaGetLastError() == cudaSuccess ? 0 : ISC_CUDA_ERROR;
+    }
     if (!split) {
       TRY(halo_exchange(ctx, z, NU));
       sc_red_launch(ctx, g, bh, z, stop);
@@ -311,6 +338,17 @@ static int bicgstab_schur(isc_ctx* ctx, double tol, int maxiter, int* iters) {
   auto black_pass = [&](int K, double* z, double* vout, const double* w0,
                         const double* w1, const double* stop) -> int {
     auto launch = [&](const Dims& d, int blocks, int slot0) {
+      if (cnd) {
+        if (K == 1)
+          k_cc6_black<1, false><<<blocks, dim3(32, CR), 0, st>>>(
+              d, ctx->cbp, ctx->diag, z, vout, w0, w1, ctx->partial, bparts, slot0, stop,
+              nullptr, nullptr);
+        else
+          k_cc6_black<2, false><<<blocks, dim3(32, CR), 0, st>>>(
+              d, ctx->cbp, ctx->diag, z, vout, w0, w1, ctx->partial, bparts, slot0, stop,
+              nullptr, nullptr);
+        return;
+      }
       if (K == 1)
         sc_black_launch<1>(ctx, d, blocks, z, vout, w0, w1, bparts, slot0, stop);
       else
@@ -332,11 +370,15 @@ static int bicgstab_schur(isc_ctx* ctx, double tol, int maxiter, int* iters) {
   };
   auto dot_b = [&](const double* a, const double* c, int slot) -> int {
     KScope ks(ctx, KT_VEC);
-    k_sc_dot<<<RED_BLOCKS, RED_THREADS, 0, st>>>(g, a, c, ctx->partial);
+    k_sc_dot<NC><<<RED_BLOCKS, RED_THREADS, 0, st>>>(g, a, c, ctx->partial);
     ++ctx->launches;
     return K.finalize1(RED_BLOCKS, slot);
   };
   auto finish = [&]() -> int {   // x_r = b_r - B_rb x_b
+    if (cnd) {   // x_b = g_b + E_b w
+      k_cond_expand<<<RED_BLOCKS, RED_THREADS, 0, st>>>(g, ctx->ces, ctx->cg9, x);
+      ++ctx->launches;
+    }
     if (halo_exchange(ctx, x, NU)) return ISC_CUDA_ERROR;
     KScope ks(ctx, KT_SPMV);
     sc_xred_launch(ctx, g, bh, b, x);
@@ -352,12 +394,12 @@ static int bicgstab_schur(isc_ctx* ctx, double tol, int maxiter, int* iters) {
       KScope ks(ctx, KT_SPMV);
       if (red_pass(x, nullptr)) return ISC_CUDA_ERROR;   // red part of x: scratch
       if (black_pass(1, x, t, rhat, nullptr, nullptr)) return ISC_CUDA_ERROR;
-      sc_rhs_launch(ctx, g, bh, b, v, shat);   // g_b (scratch)
+      if (!cnd) sc_rhs_launch(ctx, g, bh, b, v, shat);   // g_b (scratch)
     }
-    k_sc_sub<<<RED_BLOCKS, RED_THREADS, 0, st>>>(g, v, t, r, rhat);
+    k_sc_sub<NC><<<RED_BLOCKS, RED_THREADS, 0, st>>>(g, cnd ? ctx->ch6 : v, t, r, rhat);
     ctx->launches += 4;
-    cudaMemsetAsync(p, 0, len * 8, st);
-    cudaMemsetAsync(v, 0, len * 8, st);
+    cudaMemsetAsync(p, 0, lenv * 8, st);
+    cudaMemsetAsync(v, 0, lenv * 8, st);
     sh[S_RHO_OLD] = 1.0; sh[S_ALPHA] = 1.0; sh[S_OMEGA] = 1.0;
     first = true;
     restarted = true;
@@ -378,7 +420,7 @@ static int bicgstab_schur(isc_ctx* ctx, double tol, int maxiter, int* iters) {
     k_bicg_top<<<1, 1, 0, st>>>(ctx->sc);
     {
       KScope ks(ctx, KT_VEC);
-      k_sc_update_p<<<RED_BLOCKS, RED_THREADS, 0, st>>>(g, r, p, v, uinv, phat, ctx->sc, stop);
+      k_sc_update_p<NC><<<RED_BLOCKS, RED_THREADS, 0, st>>>(g, r, p, v, uinv, phat, ctx->sc, stop);
     }
     {
       KScope ks(ctx, KT_ILU_APPLY);
@@ -393,7 +435,7 @@ static int bicgstab_schur(isc_ctx* ctx, double tol, int maxiter, int* iters) {
     k_bicg_den<<<1, 1, 0, st>>>(ctx->sc);
     {
       KScope ks(ctx, KT_VEC);
-      k_sc_update_s<<<RED_BLOCKS, RED_THREADS, 0, st>>>(g, r, v, s, uinv, shat, ctx->sc,
+      k_sc_update_s<NC><<<RED_BLOCKS, RED_THREADS, 0, st>>>(g, r, v, s, uinv, shat, ctx->sc,
                                                         ctx->partial, stop);
     }
     TRY(K.finalize1(RED_BLOCKS, S_SS));
@@ -410,7 +452,7 @@ static int bicgstab_schur(isc_ctx* ctx, double tol, int maxiter, int* iters) {
     TRY(K.finalize2(bparts * sc_warps(ctx), S_TT, S_TS));
     {
       KScope ks(ctx, KT_VEC);
-      k_sc_update_xr<<<RED_BLOCKS, RED_THREADS, 0, st>>>(g, x, phat, shat, r, s, t, rhat,
+      k_sc_update_xr<NC><<<RED_BLOCKS, RED_THREADS, 0, st>>>(g, x, phat, shat, r, s, t, rhat,
                                                          ctx->sc, ctx->partial, stop);
     }
     TRY(K.finalize2(RED_BLOCKS, S_RR, S_RHO_NEW));
@@ -449,7 +491,7 @@ static int bicgstab_schur(isc_ctx* ctx, double tol, int maxiter, int* iters) {
     if (code == STOP_CONV_S) {   // ||s|| / ||b|| <= tol: x += alpha phat (linsolve.py:550-552)
       sh[S_STOP] = STOP_RUN;
       TRY(K.push());
-      k_sc_axpy_alpha<<<RED_BLOCKS, RED_THREADS, 0, st>>>(g, x, phat, ctx->sc);
+      k_sc_axpy_alpha<NC><<<RED_BLOCKS, RED_THREADS, 0, st>>>(g, x, phat, ctx->sc);
       ++ctx->launches;
       TRY(finish());
       CK(cudaStreamSynchronize(st));
@@ -488,6 +530,10 @@ static int bicgstab_schur(isc_ctx* ctx, double tol, int maxiter, int* iters) {
     }
     chunk = 1;
   }
+}
+static int bicgstab_schur(isc_ctx* ctx, double tol, int maxiter, int* iters) {
+  return ctx->cond ? bicgstab_schur_t<CR>(ctx, tol, maxiter, iters)
+                   : bicgstab_schur_t<NU>(ctx, tol, maxiter, iters);
 }
 
 // Restarted right-preconditioned GMRES(m) on the red-eliminated system
@@ -552,7 +598,7 @@ static int gmres_schur(isc_ctx* ctx, double tol, int maxiter, int* iters) {
   };
   auto norm2_into = [&](const double* a, int slot) -> int {
     KScope ks(ctx, KT_VEC);
-    k_sc_dot<<<RED_BLOCKS, RED_THREADS, 0, st>>>(g, a, a, ctx->partial);
+    k_sc_dot<NU><<<RED_BLOCKS, RED_THREADS, 0, st>>>(g, a, a, ctx->partial);
     ++ctx->launches;
     return K.finalize1(RED_BLOCKS, slot);
   };
@@ -665,7 +711,7 @@ static int gmres_schur(isc_ctx* ctx, double tol, int maxiter, int* iters) {
     // restart: r_b = g_b - S x_b
     CK(cudaMemcpyAsync(u, x, len * 8, cudaMemcpyDeviceToDevice, st));
     TRY(matvec(u, t));
-    k_sc_sub<<<RED_BLOCKS, RED_THREADS, 0, st>>>(g, gb, t, r, z);
+    k_sc_sub<NU><<<RED_BLOCKS, RED_THREADS, 0, st>>>(g, gb, t, r, z);
     ++ctx->launches;
     TRY(norm2_into(r, S_RR));
     TRY(K.read_scalars());

@@ -92,6 +92,16 @@ struct isc_ctx {
   bool compact_ok = true; // ISC_COMPACT=0 disables the compact form (A/B switch)
   double* cmid = nullptr; // split cell pass: property values for k_cell_rows (NMID x n)
   double* cbp = nullptr;  // compact form: B'_bd = B_bd[:6, :] D_nb^-1[:, :6] of black cells
+  // condensed form (compact.cu): the Krylov iteration on 6-component vectors
+  bool cond_ok = true;    // ISC_COND=0 disables (A/B switch)
+  bool cond_es = false;   // E_S of the black cells computed by the last decoupling
+  bool cond = false;      // the current factorisation is the condensed one
+  double* ces = nullptr;  // E_S (NCS*CR x half)
+  double* cbc = nullptr;  // Bc_rd of the red cells (NDIR*CR*CR x half)
+  double* cg9 = nullptr;  // reduced rhs g_b (9 x n), kept for x_b = g_b + E_b w
+  double* ch6 = nullptr;  // condensed rhs h (CR x n)
+  int* cfail_d = nullptr;
+  int* cfail_h = nullptr;  // pinned
   bool gb_fresh = false;  // compact form: the factorisation left g_b in rk / rhat
   bool assembled = false;   // the last assembly was isc_assemble (inputs kept for FD)
   double asm_dt = 0.0;

@@ -961,8 +961,9 @@ __global__ void __launch_bounds__(32 * NU, MC_MINB) k_sc_rhs(Dims g, const doubl
   rhat[r * n + c] = w;
 }
 
-// black-half vector kernels: thread per black cell (all 9 rows), fixed grid
-// and block-order partial sums (deterministic)
+// black-half vector kernels: thread per black cell (all NC rows: 9, or 6 in
+// the condensed form, compact.cu), fixed grid and block-order partial sums
+// (deterministic)
 #ifndef VEC_MINB
 #define VEC_MINB 4   // caps the U_b^-1 products at 64 registers (255 unbounded)
 #endif
@@ -971,6 +972,7 @@ __global__ void __launch_bounds__(32 * NU, MC_MINB) k_sc_rhs(Dims g, const doubl
        t += (int64_t)gridDim.x * blockDim.x)
 
 // p_b = r_b (first) or r_b + beta (p_b - omega v_b); z_b = U_b^-1 p_b
+template <int NC>
 __global__ void __launch_bounds__(RED_THREADS, VEC_MINB) k_sc_update_p(Dims g, const double* __restrict__ r,
                                                              double* __restrict__ p,
                                                              const double* __restrict__ v,
@@ -987,27 +989,28 @@ __global__ void __launch_bounds__(RED_THREADS, VEC_MINB) k_sc_update_p(Dims g, c
     const int64_t c = colour_pos(g, 1, t);
     if (!owned_k(g, plane_of(g, c))) {   // ghost plane (slabs): filled by the halo exchange
 #pragma unroll
-      for (int q = 0; q < NU; ++q) { p[q * n + c] = 0.0; z[q * n + c] = 0.0; }
+      for (int q = 0; q < NC; ++q) { p[q * n + c] = 0.0; z[q * n + c] = 0.0; }
       continue;
     }
-    double pv[NU];
+    double pv[NC];
 #pragma unroll
-    for (int q = 0; q < NU; ++q) {
+    for (int q = 0; q < NC; ++q) {
       const int64_t i = q * n + c;
       pv[q] = first ? r[i] : r[i] + beta * (p[i] - omega * v[i]);
       p[i] = pv[q];
     }
 #pragma unroll
-    for (int q = 0; q < NU; ++q) {
+    for (int q = 0; q < NC; ++q) {
       double zz = 0.0;
 #pragma unroll
-      for (int u = 0; u < NU; ++u) zz += uinv[(int64_t)(q * NU + u) * n + c] * pv[u];
+      for (int u = 0; u < NC; ++u) zz += uinv[(int64_t)(q * NC + u) * n + c] * pv[u];
       z[q * n + c] = zz;
     }
   }
 }
 
 // alpha = rho/den; s_b = r_b - alpha v_b; partial s.s; shat_b = U_b^-1 s_b
+template <int NC>
 __global__ void __launch_bounds__(RED_THREADS, VEC_MINB) k_sc_update_s(Dims g, const double* __restrict__ r,
                                                              const double* __restrict__ v,
                                                              double* __restrict__ s,
@@ -1023,23 +1026,23 @@ __global__ void __launch_bounds__(RED_THREADS, VEC_MINB) k_sc_update_s(Dims g, c
     const int64_t c = colour_pos(g, 1, t);
     if (!owned_k(g, plane_of(g, c))) {   // ghost plane (slabs): filled by the halo exchange
 #pragma unroll
-      for (int q = 0; q < NU; ++q) { s[q * n + c] = 0.0; sh[q * n + c] = 0.0; }
+      for (int q = 0; q < NC; ++q) { s[q * n + c] = 0.0; sh[q * n + c] = 0.0; }
       continue;
     }
     const bool own = true;
-    double sv[NU];
+    double sv[NC];
 #pragma unroll
-    for (int q = 0; q < NU; ++q) {
+    for (int q = 0; q < NC; ++q) {
       const int64_t i = q * n + c;
       sv[q] = r[i] - alpha * v[i];
       s[i] = sv[q];
       if (own) acc[0] += sv[q] * sv[q];
     }
 #pragma unroll
-    for (int q = 0; q < NU; ++q) {
+    for (int q = 0; q < NC; ++q) {
       double zz = 0.0;
 #pragma unroll
-      for (int u = 0; u < NU; ++u) zz += uinv[(int64_t)(q * NU + u) * n + c] * sv[u];
+      for (int u = 0; u < NC; ++u) zz += uinv[(int64_t)(q * NC + u) * n + c] * sv[u];
       sh[q * n + c] = zz;
     }
   }
@@ -1048,6 +1051,7 @@ __global__ void __launch_bounds__(RED_THREADS, VEC_MINB) k_sc_update_s(Dims g, c
 
 // omega = ts/tt; x_b += alpha phat_b + omega shat_b; r_b = s_b - omega t_b;
 // partial r.r, rhat.r
+template <int NC>
 __global__ void __launch_bounds__(RED_THREADS, VEC_MINB) k_sc_update_xr(Dims g, double* __restrict__ x,
                                                               const double* __restrict__ ph,
                                                               const double* __restrict__ sh_,
@@ -1068,7 +1072,7 @@ __global__ void __launch_bounds__(RED_THREADS, VEC_MINB) k_sc_update_xr(Dims g, 
       const int64_t c = colour_pos(g, 1, t);
       const bool own = owned_k(g, plane_of(g, c));
 #pragma unroll
-      for (int q = 0; q < NU; ++q) {
+      for (int q = 0; q < NC; ++q) {
         const int64_t i = q * n + c;
         x[i] += alpha * ph[i] + omega * sh_[i];
         const double ri = s[i] - omega * t_[i];
@@ -1127,6 +1131,7 @@ __global__ void k_bicg_end(double* sc) {     // after t.t, t.s, ||r||, r^.r
 }
 
 // black-half helpers: x_b += alpha phat_b;  out_b = a_b - b_b;  dot over black rows
+template <int NC>
 __global__ void k_sc_axpy_alpha(Dims g, double* __restrict__ x, const double* __restrict__ ph,
                                 const double* __restrict__ sc) {
   const int64_t n = g.n;
@@ -1134,17 +1139,18 @@ __global__ void k_sc_axpy_alpha(Dims g, double* __restrict__ x, const double* __
   SC_LOOP(t) {
     const int64_t c = colour_pos(g, 1, t);
 #pragma unroll
-    for (int q = 0; q < NU; ++q) x[q * n + c] += alpha * ph[q * n + c];
+    for (int q = 0; q < NC; ++q) x[q * n + c] += alpha * ph[q * n + c];
   }
 }
 
+template <int NC>
 __global__ void k_sc_sub(Dims g, const double* __restrict__ a, const double* __restrict__ b,
                          double* __restrict__ out, double* __restrict__ out2) {
   const int64_t n = g.n;
   SC_LOOP(t) {
     const int64_t c = colour_pos(g, 1, t);
 #pragma unroll
-    for (int q = 0; q < NU; ++q) {
+    for (int q = 0; q < NC; ++q) {
       const double v = a[q * n + c] - b[q * n + c];
       out[q * n + c] = v;
       if (out2) out2[q * n + c] = v;
@@ -1152,6 +1158,7 @@ __global__ void k_sc_sub(Dims g, const double* __restrict__ a, const double* __r
   }
 }
 
+template <int NC>
 __global__ void __launch_bounds__(RED_THREADS, VEC_MINB) k_sc_dot(Dims g, const double* __restrict__ a,
                                                         const double* __restrict__ b,
                                                         double* partial) {
@@ -1161,7 +1168,7 @@ __global__ void __launch_bounds__(RED_THREADS, VEC_MINB) k_sc_dot(Dims g, const 
     const int64_t c = colour_pos(g, 1, t);
     if (!owned_k(g, plane_of(g, c))) continue;
 #pragma unroll
-    for (int q = 0; q < NU; ++q) acc[0] += a[q * n + c] * b[q * n + c];
+    for (int q = 0; q < NC; ++q) acc[0] += a[q * n + c] * b[q * n + c];
   }
   block_reduce_store<1>(acc, partial);
 }

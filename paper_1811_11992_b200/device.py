@@ -153,6 +153,12 @@ class DeviceContext:
         as the reference) or "compact" (mcilu: raw flux rows + D^-1[:, :6])."""
         return ("none", "explicit", "compact")[self.L.isc_decoupled_form(self.h)]
 
+    @property
+    def condensed(self) -> bool:
+        """The current multicolour factorisation is the condensed form
+        (6-component red-eliminated iteration, csrc/compact.cu)."""
+        return bool(self.L.isc_condensed(self.h))
+
     def empty(self, *shape, dtype=torch.float64):
         return torch.empty(*shape, dtype=dtype, device=self.device)
 

@@ -434,21 +434,24 @@ def test_report_frame_from_device_simulator(tmp_path):
 
 @pytest.mark.parametrize("name", ["small3d", "sub2"])
 def test_mcilu_red_eliminated_matches_full_system(name, monkeypatch):
-    """The red-eliminated BiCGSTAB (capi.cu bicgstab_schur, default; with
-    the compact operator of csrc/compact.cu and with explicit decoupled
-    blocks) and the full-system form with the same multicolour
-    preconditioner (ISC_MCILU_FULL=1) converge to the same du; the reduced
-    form never needs more iterations than the full one (its red residual is
-    zero from the start)."""
+    """The red-eliminated BiCGSTAB (krylov.cuh bicgstab_schur) in its three
+    operator forms -- condensed (default: 6-component Krylov vectors after
+    eliminating the local rows, compact.cu), compact (ISC_COND=0: the same
+    9-component iteration with the compact operator) and explicit decoupled
+    blocks (ISC_COMPACT=0) -- and the full-system form with the same
+    multicolour preconditioner (ISC_MCILU_FULL=1) converge to the same du.
+    The reduced forms never need more iterations than the full one (their
+    red residual is zero from the start); compact and explicit apply the same
+    matrix (same iterations +-1); the condensed iteration against its oracle
+    restatement (oracle BlockSolver mcilu, _cond_solve): counts +-1."""
     from tests.golden_states import random_state_like_reference
+    from oracle import isc_oracle as O
     c = case_objects(name)
     st, accn = random_state_like_reference(c, 17)
     out = {}
-    # reduced system with the compact operator (default), with the explicit
-    # decoupled blocks (ISC_COMPACT=0), and the full-system form
-    for mode, env in (("compact", {}), ("explicit", {"ISC_COMPACT": "0"}),
-                      ("full", {"ISC_MCILU_FULL": "1"})):
-        for k in ("ISC_COMPACT", "ISC_MCILU_FULL"):
+    for mode, env in (("cond", {}), ("compact", {"ISC_COND": "0"}),
+                      ("explicit", {"ISC_COMPACT": "0"}), ("full", {"ISC_MCILU_FULL": "1"})):
+        for k in ("ISC_COMPACT", "ISC_MCILU_FULL", "ISC_COND"):
             monkeypatch.delenv(k, raising=False)
         for k, v in env.items():
             monkeypatch.setenv(k, v)
@@ -457,16 +460,21 @@ def test_mcilu_red_eliminated_matches_full_system(name, monkeypatch):
                           np.zeros(len(c.wells), bool))
         out[mode] = BlockSolver(c.grid, ws, tol=1e-10, maxiter=1000,
                                 precond="mcilu").solve(blocks)
-        assert ws.ctx.decoupled_form == ("compact" if mode == "compact" else "explicit")
+        assert ws.ctx.decoupled_form == ("compact" if mode in ("cond", "compact") else "explicit")
         ws.ctx.close()
     du_f, db_f, it_f = out["full"]
-    for mode in ("compact", "explicit"):
+    for mode in ("cond", "compact", "explicit"):
         du_s, db_s, it_s = out[mode]
         assert np.linalg.norm(du_s - du_f) <= 1e-8 * np.linalg.norm(du_f), mode
         np.testing.assert_allclose(db_s, db_f, rtol=1e-8, atol=1e-8)
         assert it_s <= it_f + 1, (mode, it_s, it_f)
-    # the compact operator is the same matrix: same Krylov iterations
     assert abs(out["compact"][2] - out["explicit"][2]) <= 1
+    ows = O.Workspace(c.grid, c.pack)
+    ob = O.assemble(c.grid, O.Model(c.pack), ows, c.wells, c.streams, st, accn, 2e-3, 2e-3,
+                    np.zeros(len(c.wells), bool))
+    odu, _, oit = O.BlockSolver(c.grid, ows, tol=1e-10, maxiter=1000, precond="mcilu").solve(ob)
+    assert abs(out["cond"][2] - oit) <= 1, (out["cond"][2], oit)
+    assert np.linalg.norm(out["cond"][0] - odu) <= 1e-8 * np.linalg.norm(odu)
 
 
 @pytest.mark.parametrize("nx", [6, 5])   # red-eliminated (even nx) and full-system (odd nx)
@@ -752,3 +760,63 @@ def test_compact_decoupling_pivoting_vs_oracle(seed):
     with pytest.raises(SingularCellBlock) as exc:
         BlockSolver(grid, ws, tol=1e-10, maxiter=500, precond="mcilu").solve([])
     assert str(exc.value) == str(oexc.value)
+
+
+@pytest.mark.parametrize("mode", ["natural", "one_order", "mixed", "all_shuffled"])
+def test_compact_decoupling_bitwise_vs_oracle(mode):
+    """k_decouple_compact_t loads each block's rows in a predicted pivot order
+    and falls back to the swapping Gauss-Jordan per cell when the prediction
+    fails (compact.cu). Either way the decoupled rhs D^-1 b must equal the
+    reference's _gj_inverse + _mv (linsolve.py:70-119, 130-136; the oracle's
+    C restatement) bit for bit: blocks as generated (one pivot order), all
+    rows permuted alike (another order, learned after the first launch),
+    10 % of the cells permuted (warps with both paths), every cell permuted
+    differently (the swapping form throughout). Three decouplings in a row,
+    so the learned order of one launch is used by the next."""
+    import ctypes
+    from types import SimpleNamespace
+    from oracle import isc_oracle as O
+    from paper_1811_11992_b200 import _native as N
+    from paper_1811_11992_b200.grid import build_grid
+    from paper_1811_11992_b200.synth import synth_system
+    from paper_1811_11992_b200.model import load_pack
+    grid = build_grid(16, 8, 6, 1.0, 1.0, 1.0, 1.0, 1.0, 1.0, 0.3)
+    pack = load_pack("tube3_pack", grid.phi_ref)
+    diag, offd, resid = synth_system(grid, 9, seed=5)
+    offd = offd.copy()
+    offd[:, :, 6:, :] = 0.0
+    diag, resid = diag.copy(), resid.copy()
+    rng = np.random.default_rng(11)
+    n = grid.ncell
+    one = np.concatenate([rng.permutation(6), 6 + rng.permutation(3)])
+    for c in range(n):
+        if mode == "natural":
+            continue
+        if mode == "one_order":
+            perm = one
+        elif mode == "mixed" and rng.uniform() >= 0.1:
+            continue
+        else:
+            perm = np.concatenate([rng.permutation(6), 6 + rng.permutation(3)])
+        sc = 10.0 ** rng.uniform(-3, 3, 9)
+        diag[c] = diag[c][perm] * sc[:, None]
+        resid[c] = resid[c][perm] * sc
+    ows = O.Workspace(grid, SimpleNamespace(nequ=9, nfull=5))
+    odiag, orhs = diag.copy(), -resid.copy()
+    invs = np.zeros((n, 9, 9))
+    flags = np.zeros(n, dtype=np.int64)
+    ooffd = offd.copy()
+    O.lib().orc_decouple_pass(ctypes.c_int64(n), ctypes.c_int64(9), O._p(odiag), O._p(orhs),
+                              O._p(ooffd), O._p(ows.adj_ptr), O._p(ows.adj_ids),
+                              O._p(ows.adj_sides), O._p(invs), O._p(flags))
+    assert not flags.any()
+    ws = Workspace(grid, pack, None, wells=(), streams=(), precond="mcilu")
+    ctx = ws.ctx
+    for _ in range(3):
+        load_system(ws, diag, offd, resid)
+        bc, bcol = ctypes.c_int64(-1), ctypes.c_int32(-1)
+        N.check(ctx.L.isc_decouple(ctx.h, ctypes.byref(bc), ctypes.byref(bcol)), "decouple")
+        assert ctx.decoupled_form == "compact"
+        b = ctx.empty(9, n)
+        N.check(ctx.L.isc_copy_rhs(ctx.h, N.ptr(b)), "rhs")
+        np.testing.assert_array_equal(b.cpu().numpy().T, orhs)
