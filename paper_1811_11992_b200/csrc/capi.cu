@@ -682,13 +682,16 @@ static int decouple_enqueue(isc_ctx* ctx, int64_t* bad_cell, int32_t* bad_col) {
                             DCT_SMEM));
     k_decouple_compact_t<<<grid1d(owned, DCT_THREADS), DCT_THREADS, DCT_SMEM, st>>>(
         ctx->g, ctx->diag, ctx->rhs, ctx->flags, ctx->bad_d);
-    // condensed form (single GPU, BiCGSTAB): E_S of the black cells from the
-    // local rows, which the compact decoupling leaves in place
+    // condensed form (BiCGSTAB): E_S of the black cells from the local rows,
+    // which the compact decoupling leaves in place -- also of the ghost planes
+    // (z-slabs), whose local rows the assembly evaluated here too
     ctx->cond_es = false;
-    if (ctx->cond_ok && !ctx->comm.active() && cond_alloc(ctx)) {
+    if (ctx->cond_ok && cond_alloc(ctx)) {
       CK(cudaMemsetAsync(ctx->cfail_d, 0, 4, st));
-      k_cond_es<<<grid1d(ctx->g.tw_hi - ctx->g.tw_lo, 256), 256, 0, st>>>(ctx->g, ctx->diag,
-                                                                          ctx->ces, ctx->cfail_d);
+      Dims ga = ctx->g;
+      ga.tw_lo = 0;
+      ga.tw_hi = ga.half;
+      k_cond_es<<<grid1d(ga.half, 256), 256, 0, st>>>(ga, ctx->diag, ctx->ces, ctx->cfail_d);
       CK(cudaMemcpyAsync(ctx->cfail_h, ctx->cfail_d, 4, cudaMemcpyDeviceToHost, st));
       ctx->cond_es = true;
     }
@@ -717,6 +720,12 @@ static int decouple_enqueue(isc_ctx* ctx, int64_t* bad_cell, int32_t* bad_col) {
 }
 
 static int decouple_check(isc_ctx* ctx, int64_t* bad_cell, int32_t* bad_col) {
+  if (ctx->cond_es && ctx->comm.active()) {   // every rank takes the same form
+    double f = *ctx->cfail_h ? 1.0 : 0.0;
+    int as = isc_comm_allreduce_host(ctx, &f, 1, 1);
+    if (as) return as;
+    *ctx->cfail_h = f > 0.0 ? 1 : 0;
+  }
   {
     double flag = *ctx->bad_h != ~0ULL ? 1.0 : 0.0;
     int as = isc_comm_allreduce_host(ctx, &flag, 1, 1);
@@ -813,6 +822,14 @@ static int precond_enqueue(isc_ctx* ctx) {
         k_mc_factor_compact<true><<<fblocks, dim3(MCFC_CELLS, NU), sizeof(McfcSmem), st>>>(
             ctx->g, ctx->offd, ctx->diag, ctx->mc_uinv, ctx->cbp, ctx->fail_d, ctx->rhs,
             ctx->cg9, nullptr, ctx->ces, ctx->cbc);
+        // slabs: the boundary planes' red blocks towards the ghost planes
+        const int gb = grid1d(ctx->g.ph, 32);
+        if (ctx->comm.has_lo)
+          k_cond_bc_ghost<<<gb, dim3(32, CR), 0, st>>>(ctx->g, ctx->offd, ctx->ces, ctx->cbc,
+                                                        ctx->g.kw_lo, DZM);
+        if (ctx->comm.has_hi)
+          k_cond_bc_ghost<<<gb, dim3(32, CR), 0, st>>>(ctx->g, ctx->offd, ctx->ces, ctx->cbc,
+                                                        ctx->g.kw_hi - 1, DZP);
       } else {
         CK(cudaFuncSetAttribute(k_mc_factor_compact<false>,
                                 cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(McfcSmem)));

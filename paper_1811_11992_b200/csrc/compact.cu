@@ -869,6 +869,33 @@ __global__ void __launch_bounds__(32 * CR, CC_MINB) k_cc6_black(
   }
 }
 
+// z-slabs: Bc of the red cells of plane kp towards the ghost plane in
+// direction d (their black neighbour lives on the next rank, whose
+// factorisation forms it there): the same sums as k_mc_factor_compact<true>
+// from the raw block and the ghost cell's E_S (k_cond_es covers ghost planes)
+__global__ void k_cond_bc_ghost(Dims g, const double* __restrict__ offd,
+                                const double* __restrict__ es, double* __restrict__ cbc, int kp,
+                                int d) {
+  const int ls = threadIdx.x, q = threadIdx.y;
+  const int64_t t = (int64_t)kp * g.ph + (int64_t)blockIdx.x * 32 + ls;
+  if (t >= (int64_t)(kp + 1) * g.ph) return;
+  const int64_t n = g.n, c = colour_pos(g, 0, t);
+  int i, j, k;
+  const int64_t cell = locate(g, c, i, j, k);
+  const int64_t nb = nb_pos(g, cell, i, j, k, d);
+  if (nb < 0) return;
+  const int64_t tb = nb - g.ph * (int64_t)(plane_of(g, nb) + 1);   // black index of nb
+  const double* blk = offd + (int64_t)((d * NU + q) * NU) * n + c;
+#pragma unroll
+  for (int p = 0; p < CR; ++p) {
+    double v = blk[(int64_t)cprim(p) * n];
+#pragma unroll
+    for (int ii = 0; ii < NCS; ++ii)
+      v += blk[(int64_t)csec(ii) * n] * es[(int64_t)(ii * CR + p) * g.half + tb];
+    cbc[(int64_t)((d * CR + q) * CR + p) * g.half + t] = v;
+  }
+}
+
 // x_b = g_b + E_b w_b (9 rows out of the 6-component w in rows 0..CR-1 of x)
 __global__ void k_cond_expand(Dims g, const double* __restrict__ es,
                               const double* __restrict__ gb, double* __restrict__ x) {

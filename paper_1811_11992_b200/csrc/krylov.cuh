@@ -275,7 +275,10 @@ static int bicgstab_schur_t(isc_ctx* ctx, double tol, int maxiter, int* iters) {
     KScope ks(ctx, KT_SPMV);
     if (ctx->gb_fresh) {
       ctx->gb_fresh = false;
+      // (slabs: g_b of the ghost planes' black cells, then their red cells' y)
+      TRY(halo_exchange(ctx, ctx->cg9, NU));
       k_cc_red<<<bh, dim3(32, CR), 0, st>>>(g, ctx->offd, ctx->ccnz_d, ctx->cg9, nullptr);
+      TRY(halo_exchange(ctx, ctx->cg9, CR));
       k_cc6_black<0, true><<<bh, dim3(32, CR), 0, st>>>(g, ctx->cbp, ctx->diag, ctx->cg9, r,
                                                         nullptr, nullptr, ctx->partial, 0, 0,
                                                         nullptr, rhat, ctx->ch6);
@@ -315,23 +318,24 @@ static int bicgstab_schur_t(isc_ctx* ctx, double tol, int maxiter, int* iters) {
   const int bl1 = split ? grid1d(gl.tw_hi - gl.tw_lo, 32) : 0;
   const int bh1 = split ? grid1d(gh.tw_hi - gh.tw_lo, 32) : 0;
   const int bparts = split ? bi + bl1 + bh1 : bh;   // black-pass partial slots (blocks)
+  auto red_launch = [&](const Dims& d, int blocks, double* z, const double* stop) {
+    if (cnd)
+      k_cc6_red<<<blocks, dim3(32, CR), 0, st>>>(d, ctx->cbc, z, stop);
+    else
+      sc_red_launch(ctx, d, blocks, z, stop);
+  };
   auto red_pass = [&](double* z, const double* stop) -> int {
-    if (cnd) {   // (single GPU)
-      k_cc6_red<<<bh, dim3(32, CR), 0, st>>>(g, ctx->cbc, z, stop);
-      ++ctx->launches;
-      return cudaGetLastError() == cudaSuccess ? 0 : ISC_CUDA_ERROR;
-    }
     if (!split) {
-      TRY(halo_exchange(ctx, z, NU));
-      sc_red_launch(ctx, g, bh, z, stop);
+      TRY(halo_exchange(ctx, z, NC));
+      red_launch(g, bh, z, stop);
       ++ctx->launches;
       return cudaGetLastError() == cudaSuccess ? 0 : ISC_CUDA_ERROR;
     }
-    TRY(halo_start(ctx, z, NU));
-    sc_red_launch(ctx, gi, bi, z, stop);
-    TRY(halo_finish(ctx, z, NU));
-    sc_red_launch(ctx, gl, bl1, z, stop);
-    sc_red_launch(ctx, gh, bh1, z, stop);
+    TRY(halo_start(ctx, z, NC));
+    red_launch(gi, bi, z, stop);
+    TRY(halo_finish(ctx, z, NC));
+    red_launch(gl, bl1, z, stop);
+    red_launch(gh, bh1, z, stop);
     ctx->launches += 3;
     return cudaGetLastError() == cudaSuccess ? 0 : ISC_CUDA_ERROR;
   };
@@ -355,14 +359,14 @@ static int bicgstab_schur_t(isc_ctx* ctx, double tol, int maxiter, int* iters) {
         sc_black_launch<2>(ctx, d, blocks, z, vout, w0, w1, bparts, slot0, stop);
     };
     if (!split) {
-      TRY(halo_exchange(ctx, z, NU));
+      TRY(halo_exchange(ctx, z, cnd ? CR : NU));
       launch(g, bh, 0);
       ++ctx->launches;
       return cudaGetLastError() == cudaSuccess ? 0 : ISC_CUDA_ERROR;
     }
-    TRY(halo_start(ctx, z, NU));
+    TRY(halo_start(ctx, z, cnd ? CR : NU));
     launch(gi, bi, 0);
-    TRY(halo_finish(ctx, z, NU));
+    TRY(halo_finish(ctx, z, cnd ? CR : NU));
     launch(gl, bl1, bi);
     launch(gh, bh1, bi + bl1);
     ctx->launches += 3;

@@ -461,6 +461,7 @@ def test_mcilu_red_eliminated_matches_full_system(name, monkeypatch):
         out[mode] = BlockSolver(c.grid, ws, tol=1e-10, maxiter=1000,
                                 precond="mcilu").solve(blocks)
         assert ws.ctx.decoupled_form == ("compact" if mode in ("cond", "compact") else "explicit")
+        assert ws.ctx.condensed == (mode == "cond")
         ws.ctx.close()
     du_f, db_f, it_f = out["full"]
     for mode in ("cond", "compact", "explicit"):
