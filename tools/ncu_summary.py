@@ -14,9 +14,10 @@ import sys
 from collections import defaultdict
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
-KERNELS = ["k_cc_red", "k_cc_black", "k_sc_update_p", "k_sc_update_s", "k_sc_update_xr",
+KERNELS = ["k_cc6_red", "k_cc6_black", "k_mc_factor_compact", "k_cond_es", "k_cond_expand",
+           "k_cc_red", "k_cc_black", "k_sc_update_p", "k_sc_update_s", "k_sc_update_xr",
            "k_face_eval_light", "k_face_eval_energy", "k_face_gather", "k_decouple_compact_t", "k_decouple_compact",
-           "k_cell_props", "k_cell_gas", "k_cell_rows", "k_mc_factor_compact", "k_cc_xred",
+           "k_cell_props", "k_cell_gas", "k_cell_rows", "k_cc_xred",
            "k_wells",
            # one-kernel variants (CELL_SPLIT=0 / FACE_SPLIT=0, earlier captures)
            "k_face_eval", "k_cell",
@@ -115,8 +116,8 @@ def main(tag):
                   "|---|---|---|---|"]
         for name, v in sorted(tot.items(), key=lambda kv: -kv[1])[:20]:
             lines.append(f"| {name} | {cnt[name]} | {v:.2f} | {v / s:.3f} |")
-    for cls, names in (("red_pass", ("k_cc_red", "k_sc_red")),
-                       ("black_pass", ("k_cc_black", "k_mc_black_spmv")),
+    for cls, names in (("red_pass", ("k_cc6_red", "k_cc_red", "k_sc_red")),
+                       ("black_pass", ("k_cc6_black", "k_cc_black", "k_mc_black_spmv")),
                        ("decouple", ("k_decouple_compact_t", "k_decouple_compact", "k_decouple_ws"))):
         for k in names:
             if k in traffic:
