@@ -821,21 +821,13 @@ static int precond_enqueue(isc_ctx* ctx) {
                                 cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(McfcSmem)));
         k_mc_factor_compact<true><<<fblocks, dim3(MCFC_CELLS, NU), sizeof(McfcSmem), st>>>(
             ctx->g, ctx->offd, ctx->diag, ctx->mc_uinv, ctx->cbp, ctx->fail_d, ctx->rhs,
-            ctx->cg9, nullptr, ctx->ces, ctx->cbc);
-        // slabs: the boundary planes' red blocks towards the ghost planes
-        const int gb = grid1d(ctx->g.ph, 32);
-        if (ctx->comm.has_lo)
-          k_cond_bc_ghost<<<gb, dim3(32, CR), 0, st>>>(ctx->g, ctx->offd, ctx->ces, ctx->cbc,
-                                                        ctx->g.kw_lo, DZM);
-        if (ctx->comm.has_hi)
-          k_cond_bc_ghost<<<gb, dim3(32, CR), 0, st>>>(ctx->g, ctx->offd, ctx->ces, ctx->cbc,
-                                                        ctx->g.kw_hi - 1, DZP);
+            ctx->cg9, nullptr, ctx->ces);
       } else {
         CK(cudaFuncSetAttribute(k_mc_factor_compact<false>,
                                 cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(McfcSmem)));
         k_mc_factor_compact<false><<<fblocks, dim3(MCFC_CELLS, NU), sizeof(McfcSmem), st>>>(
             ctx->g, ctx->offd, ctx->diag, ctx->mc_uinv, ctx->cbp, ctx->fail_d, ctx->rhs, ctx->rk,
-            ctx->rhat, nullptr, nullptr);
+            ctx->rhat, nullptr);
       }
       ctx->gb_fresh = true;
     } else

@@ -414,26 +414,23 @@ struct McfcStage {
 struct McfcSmem {
   McfcStage st[2];
   double bpsh[CR][CR][MCFC_CELLS];   // B'_bd = B_bd[:CR, :] D_nb^-1[:, :CR]
-  double bcsh[CR][CR][MCFC_CELLS];   // condensed: Bc_nb,back = B_nb,back[:CR, :] E_b
   double colk[NU][MCFC_CELLS];
   int pivs[MCFC_CELLS];
 };
 
 // COND: the condensed form (see "condensed form" below): U6 = I - Dc_b^-1
-// sum_d B'_bd Bc_nb,back with Bc_nb,back = B_nb,back[:CR, :] E_b written to
-// cbc (red neighbour's index, direction back to b) and the 6 x 6 inverse in
-// uinv; g_b (9 rows) to g1 only.
+// sum_d B'_bd Bc_nb,back = I - Dc_b^-1 Q E_b (Q = sum_d B'_bd B_nb,back[:CR, :]
+// as above, E_b from es), its 6 x 6 inverse in uinv; g_b (9 rows) to g1
+// only. (The Bc blocks themselves are formed by k_cc_red_bc.)
 template <bool COND>
 __global__ void __launch_bounds__(MCFC_CELLS * NU, MCFC_MINB) k_mc_factor_compact(
     Dims g, const double* __restrict__ offd, const double* __restrict__ dinv,
     double* __restrict__ uinv, double* __restrict__ bp, int* fail, const double* __restrict__ b,
-    double* __restrict__ g1, double* __restrict__ g2, const double* __restrict__ es,
-    double* __restrict__ cbc) {
+    double* __restrict__ g1, double* __restrict__ g2, const double* __restrict__ es) {
   constexpr int NC = COND ? CR : NU;   // order of the pivot block
   extern __shared__ __align__(16) unsigned char mcfc_raw[];
   McfcSmem& S = *reinterpret_cast<McfcSmem*>(mcfc_raw);
   auto& bpsh = S.bpsh;
-  auto& bcsh = S.bcsh;
   auto& colk = S.colk;
   auto& pivs = S.pivs;
   const int64_t n = g.n;
@@ -467,25 +464,15 @@ __global__ void __launch_bounds__(MCFC_CELLS * NU, MCFC_MINB) k_mc_factor_compac
   };
   // Register-blocked products (the smem pipe bounds this kernel): thread
   // u = 3 tq + tc owns the 2x2 block B'[2tq.., 2tc..] and the 2x3 block
-  // Q[2tq.., 3tc..] (condensed: the 2x2 blocks Bc[2tq.., 2tc..] and
-  // Q6[2tq.., 2tc..]); each entry is summed in the same order as a plain loop
+  // Q[2tq.., 3tc..]; each entry is summed in the same order as a plain loop
   double grow[2] = {0.0, 0.0};   // (sum_d B_bd b_r(nb))[2tq + qq], by the tc == 0 threads
-  constexpr int QW = COND ? 2 : 3;
-  double qacc[2][QW];            // Q[2tq + qq][QW tc + uu] = sum_d B'_bd B_back[:CR, :] (or Bc)
+  constexpr int QW = 3;
+  double qacc[2][QW];            // Q[2tq + qq][3 tc + uu] = sum_d B'_bd B_back[:CR, :]
 #pragma unroll
   for (int qq = 0; qq < 2; ++qq)
 #pragma unroll
     for (int uu = 0; uu < QW; ++uu) qacc[qq][uu] = 0.0;
   const int tq = u / 3, tc = u - 3 * (u / 3);
-  // condensed: E_b's columns 2tc, 2tc + 1 (the columns of Bc this thread forms)
-  double esr[NCS][2];
-  if (COND) {
-#pragma unroll
-    for (int ii = 0; ii < NCS; ++ii)
-#pragma unroll
-      for (int ss = 0; ss < 2; ++ss)
-        esr[ii][ss] = live ? es[(int64_t)(ii * CR + 2 * tc + ss) * g.half + t] : 0.0;
-  }
   issue(0, 0);
   cp_async_commit();
 #pragma unroll 1
@@ -527,28 +514,9 @@ __global__ void __launch_bounds__(MCFC_CELLS * NU, MCFC_MINB) k_mc_factor_compac
           bp[(int64_t)((d * CR + q) * CR + s2) * g.half + t] = sb;
         }
       }
-      if (COND) {
-        // Bc_nb,back[q][p] = B_back[q][P[p]] + sum_i B_back[q][S[i]] E_b[i][p], stored
-        // for the red neighbour (its index, direction opposite(d))
-        const int64_t tr = nb - g.ph * (int64_t)plane_of(g, nb);
-#pragma unroll
-        for (int qq = 0; qq < 2; ++qq) {
-          const int q = 2 * tq + qq;
-#pragma unroll
-          for (int ss = 0; ss < 2; ++ss) {
-            const int p = 2 * tc + ss;
-            const int pp = p + (p >= NCO ? 1 : 0) + (p >= NCO + NCG - 1 ? 1 : 0);
-            double v = T.o[q][pp][ls];
-#pragma unroll
-            for (int ii = 0; ii < NCS; ++ii) v += T.o[q][csec(ii)][ls] * esr[ii][ss];
-            bcsh[q][p][ls] = v;
-            cbc[(int64_t)((opposite(d) * CR + q) * CR + p) * g.half + tr] = v;
-          }
-        }
-      }
     }
     __syncthreads();
-    if (nb >= 0) {   // Q[2tq.., QW tc..] += B'_bd[2tq.., :] (B_back[:CR, QW tc..] or Bc[:, 2tc..])
+    if (nb >= 0) {   // Q[2tq.., 3tc..] += B'_bd[2tq.., :] B_back[:CR, 3tc..]
       double bpr[2][CR];
 #pragma unroll
       for (int qq = 0; qq < 2; ++qq)
@@ -558,8 +526,7 @@ __global__ void __launch_bounds__(MCFC_CELLS * NU, MCFC_MINB) k_mc_factor_compac
       for (int uu = 0; uu < QW; ++uu) {
         double ocol[CR];
 #pragma unroll
-        for (int r = 0; r < CR; ++r)
-          ocol[r] = COND ? bcsh[r][2 * tc + uu][ls] : T.o[r][3 * tc + uu][ls];
+        for (int r = 0; r < CR; ++r) ocol[r] = T.o[r][3 * tc + uu][ls];
 #pragma unroll
         for (int qq = 0; qq < 2; ++qq) {
           double sq = 0.0;
@@ -585,8 +552,23 @@ __global__ void __launch_bounds__(MCFC_CELLS * NU, MCFC_MINB) k_mc_factor_compac
       colk[2 * tq + 1][ls] = grow[1];
     }
     __syncthreads();
+    if (!COND) {
 #pragma unroll
-    for (int q = 0; q < CR; ++q) qcol[q] = u < NC ? qsh[q][u][ls] : 0.0;
+      for (int q = 0; q < CR; ++q) qcol[q] = qsh[q][u][ls];
+    } else {   // column u < 6 of Q E_b = Q[:, P[u]] + sum_i Q[:, S[i]] E_b[i][u]
+      double e[NCS];
+#pragma unroll
+      for (int ii = 0; ii < NCS; ++ii)
+        e[ii] = live && u < CR ? es[(int64_t)(ii * CR + u) * g.half + t] : 0.0;
+      const int pu = u < CR ? u + (u >= NCO ? 1 : 0) + (u >= NCO + NCG - 1 ? 1 : 0) : 0;
+#pragma unroll
+      for (int q = 0; q < CR; ++q) {
+        double v = qsh[q][pu][ls];
+#pragma unroll
+        for (int ii = 0; ii < NCS; ++ii) v += qsh[q][csec(ii)][ls] * e[ii];
+        qcol[q] = v;
+      }
+    }
   }
   cp_async_wait<0>();
   auto& dsh = S.st[0].d;
@@ -869,30 +851,98 @@ __global__ void __launch_bounds__(32 * CR, CC_MINB) k_cc6_black(
   }
 }
 
-// z-slabs: Bc of the red cells of plane kp towards the ghost plane in
-// direction d (their black neighbour lives on the next rank, whose
-// factorisation forms it there): the same sums as k_mc_factor_compact<true>
-// from the raw block and the ghost cell's E_S (k_cond_es covers ghost planes)
-__global__ void k_cond_bc_ghost(Dims g, const double* __restrict__ offd,
-                                const double* __restrict__ es, double* __restrict__ cbc, int kp,
-                                int d) {
+// The raw red pass on the reduced rhs g (y_r = sum_d B_rd[:CR, :] g(nb), as
+// k_cc_red, for h) fused with forming the condensed red blocks
+//   Bc_rd[q][p] = B_rd[q][P[p]] + sum_i B_rd[q][S[i]] E_nb[i][p]
+// from the same block loads and the black neighbours' E_S (k_cond_es covers
+// ghost planes, so on z-slabs the boundary planes' blocks towards the ghost
+// planes come out here too). Thread (red cell, row q), owned planes.
+__global__ void __launch_bounds__(32 * CR, CC_MINB) k_cc_red_bc(Dims g, const double* __restrict__ offd,
+                                                                const int* __restrict__ ccnz,
+                                                                const double* __restrict__ es,
+                                                                double* __restrict__ z,
+                                                                double* __restrict__ cbc) {
+  const int64_t n = g.n;
   const int ls = threadIdx.x, q = threadIdx.y;
-  const int64_t t = (int64_t)kp * g.ph + (int64_t)blockIdx.x * 32 + ls;
-  if (t >= (int64_t)(kp + 1) * g.ph) return;
-  const int64_t n = g.n, c = colour_pos(g, 0, t);
+  const int64_t t = g.tw_lo + (int64_t)blockIdx.x * 32 + ls;
+  if (t >= g.tw_hi) return;
+  const bool skip_cc = q < ROW_E && *ccnz == 0;   // warp-uniform (one row per warp)
+  const int64_t c = colour_pos(g, 0, t);
   int i, j, k;
   const int64_t cell = locate(g, c, i, j, k);
-  const int64_t nb = nb_pos(g, cell, i, j, k, d);
-  if (nb < 0) return;
-  const int64_t tb = nb - g.ph * (int64_t)(plane_of(g, nb) + 1);   // black index of nb
-  const double* blk = offd + (int64_t)((d * NU + q) * NU) * n + c;
+  double s = 0.0;
 #pragma unroll
-  for (int p = 0; p < CR; ++p) {
-    double v = blk[(int64_t)cprim(p) * n];
+  for (int d = 0; d < NDIR; ++d) {
+    const int64_t nb = nb_pos(g, cell, i, j, k, d);
+    if (nb < 0) continue;
+    const double* blk = offd + (int64_t)((d * NU + q) * NU) * n + c;
+    double bv[NU];
 #pragma unroll
-    for (int ii = 0; ii < NCS; ++ii)
-      v += blk[(int64_t)csec(ii) * n] * es[(int64_t)(ii * CR + p) * g.half + tb];
-    cbc[(int64_t)((d * CR + q) * CR + p) * g.half + t] = v;
+    for (int u = 0; u < NU; ++u) bv[u] = (u == CCC && skip_cc) ? 0.0 : blk[(int64_t)u * n];
+    double tt = 0.0;
+#pragma unroll
+    for (int u = 0; u < NU; ++u) {
+      if (u == CCC && skip_cc) continue;
+      tt += bv[u] * z[(int64_t)u * n + nb];
+    }
+    s += tt;
+    const int64_t tb = nb - g.ph * (int64_t)(plane_of(g, nb) + 1);   // black index of nb
+#pragma unroll
+    for (int p = 0; p < CR; ++p) {
+      double v = bv[cprim(p)];
+#pragma unroll
+      for (int ii = 0; ii < NCS; ++ii)
+        v += bv[csec(ii)] * es[(int64_t)(ii * CR + p) * g.half + tb];
+      cbc[(int64_t)((d * CR + q) * CR + p) * g.half + t] = v;
+    }
+  }
+  z[(int64_t)q * n + c] = s;
+}
+
+// x_r = b_r - D_r^-1[:, :CR] (y_r(g) + sum_d Bc_rd w(nb)) -- the red
+// back-substitution b_r - B_rb x_b with x_b = g_b + E_b w, from the raw red
+// pass on g (kept in g's red positions by k_cc_red_bc) and the 6x6 Bc blocks
+// instead of the 6x9 raw ones. Thread (red cell, row r < CR), then output
+// rows q = r, r + CR as k_cc_xred.
+__global__ void __launch_bounds__(32 * CR, CP_MINB) k_cc6_xred(Dims g, const double* __restrict__ cbc,
+                                                               const double* __restrict__ dinv,
+                                                               const double* __restrict__ yg,
+                                                               const double* __restrict__ b,
+                                                               double* __restrict__ x) {
+  __shared__ double ts[CR][32];
+  const int64_t n = g.n;
+  const int ls = threadIdx.x, r = threadIdx.y;
+  const int64_t t = g.tw_lo + (int64_t)blockIdx.x * 32 + ls;
+  const bool live = t < g.tw_hi;
+  int64_t c = 0;
+  if (live) {
+    c = colour_pos(g, 0, t);
+    int i, j, k;
+    const int64_t cell = locate(g, c, i, j, k);
+    double s = 0.0;
+#pragma unroll
+    for (int d = 0; d < NDIR; ++d) {
+      const int64_t nb = nb_pos(g, cell, i, j, k, d);
+      if (nb < 0) continue;
+      const double* blk = cbc + (int64_t)((d * CR + r) * CR) * g.half + t;
+      double tt = 0.0;
+#pragma unroll
+      for (int p = 0; p < CR; ++p) tt += blk[(int64_t)p * g.half] * x[(int64_t)p * n + nb];
+      s += tt;
+    }
+    ts[r][ls] = yg[(int64_t)r * n + c] + s;
+  }
+  __syncthreads();
+  if (live) {
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const int q = r + h * CR;
+      if (q >= NU) break;
+      double m = 0.0;
+#pragma unroll
+      for (int rr = 0; rr < CR; ++rr) m += dinv[(int64_t)(q * CR + rr) * n + c] * ts[rr][ls];
+      x[(int64_t)q * n + c] = b[(int64_t)q * n + c] - m;
+    }
   }
 }
 

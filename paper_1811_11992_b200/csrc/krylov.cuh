@@ -277,7 +277,8 @@ static int bicgstab_schur_t(isc_ctx* ctx, double tol, int maxiter, int* iters) {
       ctx->gb_fresh = false;
       // (slabs: g_b of the ghost planes' black cells, then their red cells' y)
       TRY(halo_exchange(ctx, ctx->cg9, NU));
-      k_cc_red<<<bh, dim3(32, CR), 0, st>>>(g, ctx->offd, ctx->ccnz_d, ctx->cg9, nullptr);
+      k_cc_red_bc<<<bh, dim3(32, CR), 0, st>>>(g, ctx->offd, ctx->ccnz_d, ctx->ces, ctx->cg9,
+                                               ctx->cbc);
       TRY(halo_exchange(ctx, ctx->cg9, CR));
       k_cc6_black<0, true><<<bh, dim3(32, CR), 0, st>>>(g, ctx->cbp, ctx->diag, ctx->cg9, r,
                                                         nullptr, nullptr, ctx->partial, 0, 0,
@@ -379,9 +380,13 @@ static int bicgstab_schur_t(isc_ctx* ctx, double tol, int maxiter, int* iters) {
     return K.finalize1(RED_BLOCKS, slot);
   };
   auto finish = [&]() -> int {   // x_r = b_r - B_rb x_b
-    if (cnd) {   // x_b = g_b + E_b w
+    if (cnd) {   // x_r from w and y_r(g), then x_b = g_b + E_b w
+      if (halo_exchange(ctx, x, CR)) return ISC_CUDA_ERROR;
+      KScope ks(ctx, KT_SPMV);
+      k_cc6_xred<<<bh, dim3(32, CR), 0, st>>>(g, ctx->cbc, ctx->diag, ctx->cg9, b, x);
       k_cond_expand<<<RED_BLOCKS, RED_THREADS, 0, st>>>(g, ctx->ces, ctx->cg9, x);
-      ++ctx->launches;
+      ctx->launches += 2;
+      return cudaGetLastError() == cudaSuccess ? 0 : ISC_CUDA_ERROR;
     }
     if (halo_exchange(ctx, x, NU)) return ISC_CUDA_ERROR;
     KScope ks(ctx, KT_SPMV);
