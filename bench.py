@@ -258,9 +258,9 @@ def algorithmic_bytes(grid, nw, precond="ras", form="explicit"):
             # v_b and the dot operand (3 x 9 n/2)
             out["ilu_apply"] = 8 * (49 * m + 7.5 * n)
             out["spmv"] = 8 * (36 * m + 43.5 * n)
-            # k_rhs_schur (resid in, rhs out) + k_decouple_compact (diag and rhs
-            # in, D^-1[:, :6] and rhs out)
-            out["decouple"] = 8 * (18 * n + 81 * n + 9 * n + 54 * n + 9 * n)
+            # k_decouple_compact_t with the well Schur fold: diag and resid in,
+            # D^-1[:, :6] and rhs out
+            out["decouple"] = 8 * (81 * n + 9 * n + 54 * n + 9 * n)
             # k_mc_factor_compact per black cell: B_bd and B_back flux rows
             # (54 m each colour), D^-1[:, :6] of both colours (27 n each), the red
             # neighbours' b (9 n/2), B' out (36 m), U_b^-1 out (81 n/2), g_b out
@@ -276,7 +276,7 @@ def algorithmic_bytes(grid, nw, precond="ras", form="explicit"):
             out["spmv"] = 8 * (36 * m + 30 * n)
             # + k_cond_es: the local rows of the black cells' diagonal blocks in
             # (27 n/2), E_S out (18 n/2)
-            out["decouple"] = 8 * (18 * n + 81 * n + 9 * n + 54 * n + 9 * n + 22.5 * n)
+            out["decouple"] = 8 * (81 * n + 9 * n + 54 * n + 9 * n + 22.5 * n)
             # k_mc_factor_compact<COND>: B_bd and B_back flux rows (54 m each),
             # D^-1[:, :6] of both colours (54 n), the red neighbours' b (4.5 n),
             # E_S (9 n), B' out (36 m), U6^-1 out (18 n), g_b (4.5 n); the Bc

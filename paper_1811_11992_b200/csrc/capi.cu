@@ -661,11 +661,6 @@ static int decouple_enqueue(isc_ctx* ctx, int64_t* bad_cell, int32_t* bad_col) {
   STAGE(stage_begin(ctx, 1));
   {
   KScope ks(ctx, KT_DECOUPLE);
-  k_rhs_schur<<<grid1d(n, 256), 256, 0, st>>>(ctx->g, ctx->resid, ctx->rhs, ctx->diag, ctx->nw,
-                                              ctx->wcell_d, ctx->wout_d, WOUT);
-  LAUNCH_CHECK();
-  CK(cudaMemsetAsync(ctx->flags, 0, n * 4, st));
-  CK(cudaMemsetAsync(ctx->bad_d, 0xff, 8, st));
   // compact form: the red-eliminated multicolour solve of an assembled
   // system (compact.cu)
   ctx->compact = ctx->compact_ok && ctx->precond == ISC_PRECOND_MCILU && ctx->g.colored &&
@@ -676,12 +671,23 @@ static int decouple_enqueue(isc_ctx* ctx, int64_t* bad_cell, int32_t* bad_col) {
     ctx->cbp = nullptr;
     ctx->compact = false;   // no room for B': the explicit form
   }
+  if (!ctx->compact) {   // (the compact decoupling folds the wells itself)
+    k_rhs_schur<<<grid1d(n, 256), 256, 0, st>>>(ctx->g, ctx->resid, ctx->rhs, ctx->diag, ctx->nw,
+                                                ctx->wcell_d, ctx->wout_d, WOUT);
+    LAUNCH_CHECK();
+  } else if (ctx->comm.active()) {
+    k_zero_ghost_rows<<<RED_BLOCKS, 256, 0, st>>>(ctx->g, NU, ctx->rhs);
+    LAUNCH_CHECK();
+  }
+  CK(cudaMemsetAsync(ctx->flags, 0, n * 4, st));
+  CK(cudaMemsetAsync(ctx->bad_d, 0xff, 8, st));
   if (ctx->compact) {
     const int64_t owned = (int64_t)(ctx->g.kw_hi - ctx->g.kw_lo) * ctx->g.nxny;
     CK(cudaFuncSetAttribute(k_decouple_compact_t, cudaFuncAttributeMaxDynamicSharedMemorySize,
                             DCT_SMEM));
     k_decouple_compact_t<<<grid1d(owned, DCT_THREADS), DCT_THREADS, DCT_SMEM, st>>>(
-        ctx->g, ctx->diag, ctx->rhs, ctx->flags, ctx->bad_d);
+        ctx->g, ctx->diag, ctx->rhs, ctx->flags, ctx->bad_d, ctx->resid, ctx->nw, ctx->wcell_d,
+        ctx->wout_d, WOUT);
     // condensed form (BiCGSTAB): E_S of the black cells from the local rows,
     // which the compact decoupling leaves in place -- also of the ghost planes
     // (z-slabs), whose local rows the assembly evaluated here too

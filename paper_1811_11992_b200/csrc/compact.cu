@@ -77,22 +77,53 @@ __device__ __forceinline__ int sel_i(bool p, int x, int y) {
 // the row interchanges) with the reference's pivot rule (partial pivoting,
 // failure below 1e-13 max|D|, _gj_inverse linsolve.py:70-119), scaling by the
 // reciprocal and elimination order; no shared memory and no barriers.
-__global__ void __launch_bounds__(DCT_THREADS) k_decouple_compact_t(Dims g, double* diag,
-                                                                   double* rhs, int* flags,
-                                                                   unsigned long long* bad) {
+// The well Schur fold (linsolve.py:362-394; k_rhs_schur for the other forms)
+// is applied on the way in: rhs = -resid, and a perforated cell's block and
+// rhs take the well's bhp column (the local rows' slots are written back:
+// the condensed form reads them).
+__global__ void __launch_bounds__(DCT_THREADS) k_decouple_compact_t(
+    Dims g, double* diag, double* rhs, int* flags, unsigned long long* bad,
+    const double* __restrict__ resid, int nw, const int64_t* __restrict__ wcell,
+    const double* __restrict__ wout, int wstride) {
   const int64_t n = g.n;
   const int64_t p0 = (int64_t)g.kw_lo * g.nxny, p1 = (int64_t)g.kw_hi * g.nxny;
   const int64_t c = p0 + (int64_t)blockIdx.x * DCT_THREADS + threadIdx.x;
   if (c >= p1) return;
   double a[NU][NU];   // a[r][j]: row r, slot j
+#pragma unroll
+  for (int r = 0; r < NU; ++r)
+#pragma unroll
+    for (int j = 0; j < NU; ++j) a[r][j] = diag[(int64_t)(r * NU + j) * n + c];
+  {
+    double rv[NU];
+#pragma unroll
+    for (int r = 0; r < NU; ++r) rv[r] = -resid[(int64_t)r * n + c];
+    for (int w = 0; w < nw; ++w) {
+      if (wcell[w] != c) continue;
+      const double* o = wout + (int64_t)w * wstride;
+      const double resid_w = o[0], dwdb = o[1];
+      const double* wrow = o + 2;
+      const double* bcol = o + 2 + NU;
+      const double inv_d = 1.0 / dwdb;
+#pragma unroll
+      for (int r = 0; r < NU; ++r) {
+        rv[r] += bcol[r] * (resid_w * inv_d);
+#pragma unroll
+        for (int u = 0; u < NU; ++u) a[r][u] -= bcol[r] * wrow[u] * inv_d;
+      }
+#pragma unroll
+      for (int r = CR; r < NU; ++r)
+#pragma unroll
+        for (int u = 0; u < NU; ++u) diag[(int64_t)(r * NU + u) * n + c] = a[r][u];
+    }
+#pragma unroll
+    for (int r = 0; r < NU; ++r) rhs[(int64_t)r * n + c] = rv[r];
+  }
   double amax = 0.0;
 #pragma unroll
   for (int r = 0; r < NU; ++r)
 #pragma unroll
-    for (int j = 0; j < NU; ++j) {
-      a[r][j] = diag[(int64_t)(r * NU + j) * n + c];
-      amax = fmax(amax, fabs(a[r][j]));
-    }
+    for (int j = 0; j < NU; ++j) amax = fmax(amax, fabs(a[r][j]));
   const double tol = 1e-13 * amax;
   int perm[NU];
 #pragma unroll
@@ -174,6 +205,20 @@ __global__ void __launch_bounds__(DCT_THREADS) k_decouple_compact_t(Dims g, doub
   }
 }
 constexpr int DCT_SMEM = NB * DCT_THREADS * 8;
+
+// z-slabs: the ghost planes' rows of v carry no equation (zero), planes
+// [0, kw_lo) and [kw_hi, nz)
+__global__ void k_zero_ghost_rows(Dims g, int rows, double* v) {
+  const int64_t lo = (int64_t)g.kw_lo * g.nxny, hi = (int64_t)(g.nz - g.kw_hi) * g.nxny;
+  const int64_t m = lo + hi;
+  for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < m * rows;
+       t += (int64_t)gridDim.x * blockDim.x) {
+    const int r = (int)(t / m);
+    const int64_t q = t - (int64_t)r * m;
+    const int64_t c = q < lo ? q : (int64_t)g.kw_hi * g.nxny + (q - lo);
+    v[(int64_t)r * g.n + c] = 0.0;
+  }
+}
 
 // One half pass of the compact operator over the owned cells of one colour
 // (thread (cell lane, flux row r < CR), then output rows q = y, y + CR):
