@@ -683,23 +683,28 @@ static int decouple_enqueue(isc_ctx* ctx, int64_t* bad_cell, int32_t* bad_col) {
   CK(cudaMemsetAsync(ctx->bad_d, 0xff, 8, st));
   if (ctx->compact) {
     const int64_t owned = (int64_t)(ctx->g.kw_hi - ctx->g.kw_lo) * ctx->g.nxny;
+    // condensed form (BiCGSTAB): E_S of the black cells from the local rows,
+    // formed by the decoupling of the owned planes and, on z-slabs, by
+    // k_cond_es for the ghost planes (whose local rows the assembly evaluated
+    // here too; the decoupling leaves the local rows' slots in place)
+    ctx->cond_es = ctx->cond_ok && cond_alloc(ctx);
+    if (ctx->cond_es) CK(cudaMemsetAsync(ctx->cfail_d, 0, 4, st));
     CK(cudaFuncSetAttribute(k_decouple_compact_t, cudaFuncAttributeMaxDynamicSharedMemorySize,
                             DCT_SMEM));
     k_decouple_compact_t<<<grid1d(owned, DCT_THREADS), DCT_THREADS, DCT_SMEM, st>>>(
         ctx->g, ctx->diag, ctx->rhs, ctx->flags, ctx->bad_d, ctx->resid, ctx->nw, ctx->wcell_d,
-        ctx->wout_d, WOUT);
-    // condensed form (BiCGSTAB): E_S of the black cells from the local rows,
-    // which the compact decoupling leaves in place -- also of the ghost planes
-    // (z-slabs), whose local rows the assembly evaluated here too
-    ctx->cond_es = false;
-    if (ctx->cond_ok && cond_alloc(ctx)) {
-      CK(cudaMemsetAsync(ctx->cfail_d, 0, 4, st));
-      Dims ga = ctx->g;
-      ga.tw_lo = 0;
-      ga.tw_hi = ga.half;
-      k_cond_es<<<grid1d(ga.half, 256), 256, 0, st>>>(ga, ctx->diag, ctx->ces, ctx->cfail_d);
+        ctx->wout_d, WOUT, ctx->cond_es ? ctx->ces : nullptr, ctx->cfail_d);
+    if (ctx->cond_es) {
+      const Dims& g0 = ctx->g;
+      for (int side = 0; side < 2; ++side) {   // ghost planes [0, kw_lo), [kw_hi, nz)
+        Dims ga = g0;
+        ga.tw_lo = side == 0 ? 0 : (int64_t)g0.kw_hi * g0.ph;
+        ga.tw_hi = side == 0 ? (int64_t)g0.kw_lo * g0.ph : g0.half;
+        if (ga.tw_hi > ga.tw_lo)
+          k_cond_es<<<grid1d(ga.tw_hi - ga.tw_lo, 256), 256, 0, st>>>(ga, ctx->diag, ctx->ces,
+                                                                      ctx->cfail_d);
+      }
       CK(cudaMemcpyAsync(ctx->cfail_h, ctx->cfail_d, 4, cudaMemcpyDeviceToHost, st));
-      ctx->cond_es = true;
     }
   } else {
     ctx->cond_es = false;

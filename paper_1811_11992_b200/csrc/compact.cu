@@ -71,6 +71,68 @@ __device__ __forceinline__ int sel_i(bool p, int x, int y) {
       : "=r"(r) : "r"(x), "r"(y), "r"((unsigned)p));
   return r;
 }
+// E_S of the cell at storage position c from its diagonal block's local rows
+// (Gauss-Jordan with partial pivoting on [D[CR:, S] | D[CR:, P]]); false when
+// a pivot is below 1e-12 of max|D[CR:, S]| or not finite (the form is then
+// not used for this system).
+template <class L>
+__device__ __forceinline__ bool cond_es_from(L ld, double (&es)[NCS][CR]) {
+  double m[NCS][NCS + CR];
+  double mmax = 0.0;
+#pragma unroll
+  for (int i = 0; i < NCS; ++i) {
+#pragma unroll
+    for (int j = 0; j < NCS; ++j) {
+      m[i][j] = ld(CR + i, csec(j));
+      mmax = fmax(mmax, fabs(m[i][j]));
+    }
+#pragma unroll
+    for (int p = 0; p < CR; ++p) m[i][NCS + p] = ld(CR + i, cprim(p));
+  }
+  bool ok = mmax > 0.0 && mmax < INFINITY;
+#pragma unroll
+  for (int k = 0; k < NCS; ++k) {
+    int piv = k;
+    double pv = fabs(m[k][k]);
+#pragma unroll
+    for (int r = k + 1; r < NCS; ++r)
+      if (fabs(m[r][k]) > pv) { pv = fabs(m[r][k]); piv = r; }
+    ok = ok && pv > 1e-12 * mmax;
+#pragma unroll
+    for (int r = k + 1; r < NCS; ++r) {
+      if (r != piv) continue;
+#pragma unroll
+      for (int j = 0; j < NCS + CR; ++j) {
+        const double t = m[k][j];
+        m[k][j] = m[r][j];
+        m[r][j] = t;
+      }
+    }
+    const double dv = 1.0 / m[k][k];
+#pragma unroll
+    for (int j = 0; j < NCS + CR; ++j) m[k][j] *= dv;
+#pragma unroll
+    for (int r = 0; r < NCS; ++r) {
+      if (r == k) continue;
+      const double f = m[r][k];
+#pragma unroll
+      for (int j = 0; j < NCS + CR; ++j) m[r][j] -= f * m[k][j];
+    }
+  }
+#pragma unroll
+  for (int i = 0; i < NCS; ++i)
+#pragma unroll
+    for (int p = 0; p < CR; ++p) {
+      es[i][p] = -m[i][NCS + p];
+      ok = ok && isfinite(es[i][p]);
+    }
+  return ok;
+}
+__device__ __forceinline__ bool cond_es(const double* __restrict__ diag, int64_t n, int64_t c,
+                                        double (&es)[NCS][CR]) {
+  return cond_es_from([&](int r, int u) { return diag[(int64_t)(r * NU + u) * n + c]; }, es);
+}
+
 // D^-1 of every owned cell and rhs <- D^-1 rhs, one thread per cell with the
 // block held in registers: in-place Gauss-Jordan (once column k is
 // eliminated its slot holds column perm[k] of the inverse, where perm tracks
@@ -84,7 +146,7 @@ __device__ __forceinline__ int sel_i(bool p, int x, int y) {
 __global__ void __launch_bounds__(DCT_THREADS) k_decouple_compact_t(
     Dims g, double* diag, double* rhs, int* flags, unsigned long long* bad,
     const double* __restrict__ resid, int nw, const int64_t* __restrict__ wcell,
-    const double* __restrict__ wout, int wstride) {
+    const double* __restrict__ wout, int wstride, double* __restrict__ es, int* cfail) {
   const int64_t n = g.n;
   const int64_t p0 = (int64_t)g.kw_lo * g.nxny, p1 = (int64_t)g.kw_hi * g.nxny;
   const int64_t c = p0 + (int64_t)blockIdx.x * DCT_THREADS + threadIdx.x;
@@ -118,6 +180,18 @@ __global__ void __launch_bounds__(DCT_THREADS) k_decouple_compact_t(
     }
 #pragma unroll
     for (int r = 0; r < NU; ++r) rhs[(int64_t)r * n + c] = rv[r];
+  }
+  if (es) {   // condensed form: E_S of a black cell (warp-uniform colour)
+    const int64_t rem = c - (int64_t)plane_of(g, c) * g.nxny;
+    if (rem >= g.ph) {
+      double e[NCS][CR];
+      if (!cond_es_from([&](int r, int u) { return a[r][u]; }, e)) atomicOr(cfail, 1);
+      const int64_t tb = c - g.ph * (int64_t)(plane_of(g, c) + 1);
+#pragma unroll
+      for (int i = 0; i < NCS; ++i)
+#pragma unroll
+        for (int p = 0; p < CR; ++p) es[(int64_t)(i * CR + p) * g.half + tb] = e[i][p];
+    }
   }
   double amax = 0.0;
 #pragma unroll
@@ -729,64 +803,6 @@ __global__ void __launch_bounds__(MCFC_CELLS * NU, MCFC_MINB) k_mc_factor_compac
 // iteration at LINEAR_TOL 1e-5 and 1e-10. Stopping test
 // ||r6|| / ||b|| (r9 = E r6: the constraint rows' components of the full
 // residual are left out of the norm).
-
-// E_S of the cell at storage position c from its diagonal block's local rows
-// (Gauss-Jordan with partial pivoting on [D[CR:, S] | D[CR:, P]]); false when
-// a pivot is below 1e-12 of max|D[CR:, S]| or not finite (the form is then
-// not used for this system).
-__device__ __forceinline__ bool cond_es(const double* __restrict__ diag, int64_t n, int64_t c,
-                                        double (&es)[NCS][CR]) {
-  double m[NCS][NCS + CR];
-  double mmax = 0.0;
-#pragma unroll
-  for (int i = 0; i < NCS; ++i) {
-#pragma unroll
-    for (int j = 0; j < NCS; ++j) {
-      m[i][j] = diag[(int64_t)((CR + i) * NU + csec(j)) * n + c];
-      mmax = fmax(mmax, fabs(m[i][j]));
-    }
-#pragma unroll
-    for (int p = 0; p < CR; ++p) m[i][NCS + p] = diag[(int64_t)((CR + i) * NU + cprim(p)) * n + c];
-  }
-  bool ok = mmax > 0.0 && mmax < INFINITY;
-#pragma unroll
-  for (int k = 0; k < NCS; ++k) {
-    int piv = k;
-    double pv = fabs(m[k][k]);
-#pragma unroll
-    for (int r = k + 1; r < NCS; ++r)
-      if (fabs(m[r][k]) > pv) { pv = fabs(m[r][k]); piv = r; }
-    ok = ok && pv > 1e-12 * mmax;
-#pragma unroll
-    for (int r = k + 1; r < NCS; ++r) {
-      if (r != piv) continue;
-#pragma unroll
-      for (int j = 0; j < NCS + CR; ++j) {
-        const double t = m[k][j];
-        m[k][j] = m[r][j];
-        m[r][j] = t;
-      }
-    }
-    const double dv = 1.0 / m[k][k];
-#pragma unroll
-    for (int j = 0; j < NCS + CR; ++j) m[k][j] *= dv;
-#pragma unroll
-    for (int r = 0; r < NCS; ++r) {
-      if (r == k) continue;
-      const double f = m[r][k];
-#pragma unroll
-      for (int j = 0; j < NCS + CR; ++j) m[r][j] -= f * m[k][j];
-    }
-  }
-#pragma unroll
-  for (int i = 0; i < NCS; ++i)
-#pragma unroll
-    for (int p = 0; p < CR; ++p) {
-      es[i][p] = -m[i][NCS + p];
-      ok = ok && isfinite(es[i][p]);
-    }
-  return ok;
-}
 
 // E_S of every owned black cell into es[(i*CR + p)*half + t]; *fail = 1 when
 // a cell's local block is not usable (before or after the compact
