@@ -11,6 +11,7 @@ Our grid/pack/well builders feed the oracle, so these tests also pin the
 product's host-side builders bit for bit.
 """
 
+import copy
 import ctypes
 import json
 import math
@@ -375,3 +376,56 @@ def test_oracle_mcilu_solve_agrees_with_reference_solution():
     ref = s["ras_du"]
     assert np.linalg.norm(du - ref) <= 1e-8 * np.linalg.norm(ref)
     assert int(s["ras_iters"]) <= it < int(s["none_iters"])
+
+
+def test_oracle_condensed_mcilu_algebra_and_solution():
+    """The condensed multicolour solve (oracle _cond_setup/_cond_solve, the
+    checker of the device's default mcilu form, csrc/compact.cu): on the
+    reference-assembled small3d system (local rows 6..8 carry no flux)
+    (1) S9 (E w) = E (S6 w) for random w -- the red-eliminated 9-component
+    operator maps range(E) into itself, so x_b = g_b + E_b w is exact;
+    (2) U6 is S6's block diagonal; (3) the condensed du solves the full
+    decoupled system to the tolerance and equals the 9-component solve's
+    (LINEAR_TOL 1e-10) to 1e-8."""
+    g = golden("asm_small3d.npz")
+    c = case_objects("small3d")
+    ws, blocks = _oracle_assemble(c, state_from(g), g["accn"], float(g["dt"]),
+                                  float(g["t_new"]), g["capped"])
+    assert not np.any(ws.offd[:, :, O.CR_:, :] != 0.0)
+    ref_ws = copy.deepcopy(ws)
+    bs = O.BlockSolver(c.grid, ws, tol=1e-10, maxiter=1000, precond="mcilu")
+    rhs = -ws.resid
+    bs._eliminate_wells(blocks, rhs)
+    dloc = ws.diag[:, O.CR_:, :].copy()
+    import ctypes
+    O.lib().orc_decouple_pass(ctypes.c_int64(rhs.shape[0]), ctypes.c_int64(9), O._p(ws.diag),
+                              O._p(rhs), O._p(ws.offd), O._p(ws.adj_ptr), O._p(ws.adj_ids),
+                              O._p(ws.adj_sides), O._p(bs.invs), O._p(bs.flags))
+    C = bs._cond_setup(dloc)
+    assert C is not None
+    nb, e = C["nb"], C["e"]
+    w = np.random.default_rng(7).normal(size=(nb, O.CR_))
+    ew = np.einsum("cij,cj->ci", e, w)
+    s9ew = C["s9"](ew)
+    s6w = s9ew[:, O.COND_P]
+    np.testing.assert_allclose(s9ew, np.einsum("cij,cj->ci", e, s6w), rtol=1e-12, atol=1e-12)
+    # block diagonal: S6 applied to a single black cell's unit vectors
+    q = nb // 2
+    for u in range(O.CR_):
+        wu = np.zeros((nb, O.CR_))
+        wu[q, u] = 1.0
+        col = C["s9"](np.einsum("cij,cj->ci", e, wu))[q, O.COND_P]
+        np.testing.assert_allclose(np.linalg.inv(C["u6inv"][q])[:, u], col, rtol=1e-10,
+                                   atol=1e-12)
+    # solutions
+    du6, _, it6 = O.BlockSolver(c.grid, copy.deepcopy(ref_ws), tol=1e-10, maxiter=1000,
+                                precond="mcilu").solve(blocks)
+    saved = O.BlockSolver.condensed
+    try:
+        O.BlockSolver.condensed = False
+        du9, _, it9 = O.BlockSolver(c.grid, copy.deepcopy(ref_ws), tol=1e-10, maxiter=1000,
+                                    precond="mcilu").solve(blocks)
+    finally:
+        O.BlockSolver.condensed = saved
+    assert np.linalg.norm(du6 - du9) <= 1e-8 * np.linalg.norm(du9)
+    assert it6 <= it9 + 1
