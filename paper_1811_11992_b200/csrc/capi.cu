@@ -150,6 +150,8 @@ extern "C" int isc_create(const isc_model_desc* md, const isc_grid_desc* gdsc, i
   ALLOC(ctx->upw, (size_t)9 * n);
   CK(cudaMemset(ctx->upw, 0, (size_t)9 * n));
   ALLOC(ctx->bad_d, 8);
+  ALLOC(ctx->ticket_d, 4);
+  CK(cudaMemset(ctx->ticket_d, 0, 4));
   CK(cudaMallocHost(&ctx->bad_h, 16));   // [0] bad cell (cell pass / decoupling), [1] factor status
   // solver vectors
   double** vecs[] = {&ctx->rhs, &ctx->xk, &ctx->rk, &ctx->rhat, &ctx->pk,
@@ -181,7 +183,7 @@ extern "C" int isc_destroy(isc_ctx* ctx) {
   void* ptrs[] = {ctx->depth, ctx->vol, ctx->phi_ref, ctx->gd, ctx->td, ctx->hl_area,
                   ctx->conn_id, ctx->wells_d, ctx->wcell_d, ctx->wout_d, ctx->bhp_d,
                   ctx->capped_d, ctx->rec, ctx->acc, ctx->src, ctx->resid, ctx->diag,
-                  ctx->offd, ctx->upw, ctx->bad_d, ctx->rhs, ctx->xk, ctx->rk, ctx->rhat,
+                  ctx->offd, ctx->upw, ctx->bad_d, ctx->ticket_d, ctx->rhs, ctx->xk, ctx->rk, ctx->rhat,
                   ctx->pk, ctx->vk, ctx->phat, ctx->shat, ctx->sk, ctx->tk, ctx->sc,
                   ctx->partial, ctx->partial2, ctx->fbuf, ctx->flags, ctx->fail_d, ctx->ccnz_d, ctx->st_c, ctx->accn_c, ctx->stage,
                   ctx->halo_send_lo, ctx->halo_send_hi, ctx->halo_recv_lo, ctx->halo_recv_hi,

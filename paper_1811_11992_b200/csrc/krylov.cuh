@@ -13,28 +13,39 @@ struct Kry {
   // fixed-order sums: one block for RED_BLOCKS partials, two stages for the
   // per-warp partials of the stencil passes
   template <int K>
-  void finalize(int nparts, int s0, int s1) {
+  void finalize(int nparts, int s0, int s1, int post) {
     if (nparts <= RED_BLOCKS) {
       k_finalize<K><<<1, 256, 0, ctx->stream>>>(ctx->partial, nparts, ctx->sc, s0, s1, s1,
-                                                stop);
+                                                stop, post);
       ++ctx->launches;
       return;
     }
-    k_partial_sum<K><<<FIN_BLOCKS, 256, 0, ctx->stream>>>(ctx->partial, nparts, ctx->partial2,
-                                                          stop);
-    k_finalize<K><<<1, 256, 0, ctx->stream>>>(ctx->partial2, FIN_BLOCKS, ctx->sc, s0, s1, s1,
-                                              stop);
-    ctx->launches += 2;
+    k_partial_sum_fin<K><<<FIN_BLOCKS, 256, 0, ctx->stream>>>(
+        ctx->partial, nparts, ctx->partial2, ctx->sc, s0, s1, stop, post, ctx->ticket_d);
+    ++ctx->launches;
   }
-  int finalize1(int nparts, int s0) {
-    finalize<1>(nparts, s0, s0);
-    if (cudaGetLastError() != cudaSuccess) return ISC_CUDA_ERROR;
-    return allreduce_dev(ctx, ctx->sc + s0, 1);
+  // post: the device-driven iteration's scalar step that needs these sums
+  // (POST_DEN / _SS / _END), fused into the sum on one GPU; after the
+  // all-reduce as its own kernel on z-slabs
+  int post_step(int post) {
+    if (post == POST_NONE || !ctx->comm.active()) return 0;
+    if (post == POST_DEN) k_bicg_den<<<1, 1, 0, ctx->stream>>>(ctx->sc);
+    else if (post == POST_SS) k_bicg_ss<<<1, 1, 0, ctx->stream>>>(ctx->sc);
+    else k_bicg_end<<<1, 1, 0, ctx->stream>>>(ctx->sc);
+    ++ctx->launches;
+    return cudaGetLastError() == cudaSuccess ? 0 : ISC_CUDA_ERROR;
   }
-  int finalize2(int nparts, int s0, int s1) {   // s1 == s0 + 1
-    finalize<2>(nparts, s0, s1);
+  int finalize1(int nparts, int s0, int post = POST_NONE) {
+    finalize<1>(nparts, s0, s0, ctx->comm.active() ? POST_NONE : post);
     if (cudaGetLastError() != cudaSuccess) return ISC_CUDA_ERROR;
-    return allreduce_dev(ctx, ctx->sc + s0, 2);
+    const int s = allreduce_dev(ctx, ctx->sc + s0, 1);
+    return s ? s : post_step(post);
+  }
+  int finalize2(int nparts, int s0, int s1, int post = POST_NONE) {   // s1 == s0 + 1
+    finalize<2>(nparts, s0, s1, ctx->comm.active() ? POST_NONE : post);
+    if (cudaGetLastError() != cudaSuccess) return ISC_CUDA_ERROR;
+    const int s = allreduce_dev(ctx, ctx->sc + s0, 2);
+    return s ? s : post_step(post);
   }
   int dot(const double* a, const double* b, int slot) {
     k_dots<1><<<RED_BLOCKS, RED_THREADS, 0, ctx->stream>>>(len, a, b, nullptr, nullptr, nullptr,
@@ -440,15 +451,13 @@ static int bicgstab_schur_t(isc_ctx* ctx, double tol, int maxiter, int* iters) {
       TRY(black_pass(1, phat, v, rhat, nullptr, stop));
     }
     CK(cudaGetLastError());
-    TRY(K.finalize1(bparts * sc_warps(ctx), S_DEN));
-    k_bicg_den<<<1, 1, 0, st>>>(ctx->sc);
+    TRY(K.finalize1(bparts * sc_warps(ctx), S_DEN, POST_DEN));
     {
       KScope ks(ctx, KT_VEC);
       k_sc_update_s<NC><<<RED_BLOCKS, RED_THREADS, 0, st>>>(g, r, v, s, uinv, shat, ctx->sc,
                                                         ctx->partial, stop);
     }
-    TRY(K.finalize1(RED_BLOCKS, S_SS));
-    k_bicg_ss<<<1, 1, 0, st>>>(ctx->sc);
+    TRY(K.finalize1(RED_BLOCKS, S_SS, POST_SS));
     {
       KScope ks(ctx, KT_ILU_APPLY);
       TRY(red_pass(shat, stop));
@@ -464,9 +473,8 @@ static int bicgstab_schur_t(isc_ctx* ctx, double tol, int maxiter, int* iters) {
       k_sc_update_xr<NC><<<RED_BLOCKS, RED_THREADS, 0, st>>>(g, x, phat, shat, r, s, t, rhat,
                                                          ctx->sc, ctx->partial, stop);
     }
-    TRY(K.finalize2(RED_BLOCKS, S_RR, S_RHO_NEW));
-    k_bicg_end<<<1, 1, 0, st>>>(ctx->sc);
-    ctx->launches += 7;   // 3 vector updates + 4 control kernels (passes and sums count themselves)
+    TRY(K.finalize2(RED_BLOCKS, S_RR, S_RHO_NEW, POST_END));
+    ctx->launches += 4;   // 3 vector updates + k_bicg_top (passes, sums and steps count themselves)
     return cudaGetLastError() == cudaSuccess ? 0 : ISC_CUDA_ERROR;
   };
   // a restart by the host: device state -> sh, restart, new rho, state -> HBM

@@ -43,6 +43,30 @@ enum { STOP_RUN = 0, STOP_TOP = 1, STOP_DEN = 2, STOP_CONV_S = 3, STOP_TT = 4, S
 // (nullable: host-driven callers) holds a nonzero code
 __device__ __forceinline__ bool stopped(const double* stop) { return stop && *stop != 0.0; }
 
+// scalar steps of the device-driven BiCGSTAB (linsolve.py:500-575), run by
+// one thread after the dot product they need (k_bicg_* or fused into the
+// fixed-order sum that produced it, k_finalize's `post`)
+enum { POST_NONE = 0, POST_DEN = 1, POST_SS = 2, POST_END = 3 };
+__device__ __forceinline__ void bicg_den(double* sc) {   // after r^.v: denominator test, alpha
+  if (sc[S_STOP] != 0.0) return;
+  const double den = sc[S_DEN];
+  if (fabs(den) < sc[S_BRK]) { sc[S_STOP] = STOP_DEN; return; }
+  sc[S_ALPHA] = sc[S_RHO] / den;
+}
+__device__ __forceinline__ void bicg_ss(double* sc) {    // after ||s||: early convergence
+  if (sc[S_STOP] != 0.0) return;
+  if (sqrt(sc[S_SS]) / sc[S_NB] <= sc[S_TOL]) sc[S_STOP] = STOP_CONV_S;
+}
+__device__ __forceinline__ void bicg_end(double* sc) {   // after t.t, t.s, ||r||, r^.r
+  if (sc[S_STOP] != 0.0) return;
+  const double tt = sc[S_TT];
+  if (tt == 0.0) { sc[S_STOP] = STOP_TT; return; }
+  sc[S_OMEGA] = sc[S_TS] / tt;
+  if (sqrt(sc[S_RR]) / sc[S_NB] <= sc[S_TOL]) { sc[S_STOP] = STOP_CONV; return; }
+  sc[S_RHO_OLD] = sc[S_RHO];
+  sc[S_FIRST] = 0.0;
+}
+
 template <int K>
 __device__ __forceinline__ void block_reduce_store(double (&v)[K], double* partial) {
   __shared__ double sh[K][32];
@@ -118,11 +142,9 @@ __global__ void __launch_bounds__(256) k_partial_sum(const double* __restrict__ 
 
 // sum the per-block partials in fixed order into sc[slot_k] (256 threads)
 template <int K>
-__global__ void __launch_bounds__(256) k_finalize(const double* __restrict__ partial, int nparts,
-                                                  double* sc, int s0, int s1, int s2,
-                                                  const double* stop) {
-  if (stopped(stop)) return;
-  const int slots[3] = {s0, s1, s2};
+__device__ __forceinline__ void finalize_block(const double* __restrict__ partial, int nparts,
+                                               double* sc, int s0, int s1, int post) {
+  const int slots[2] = {s0, s1};
   __shared__ double sh[K][8];
   const int t = threadIdx.x, lane = t & 31, w = t >> 5;
 #pragma unroll
@@ -141,7 +163,58 @@ __global__ void __launch_bounds__(256) k_finalize(const double* __restrict__ par
       for (int i = 0; i < 8; ++i) s += sh[k][i];
       sc[slots[k]] = s;
     }
+    if (post == POST_DEN) bicg_den(sc);
+    else if (post == POST_SS) bicg_ss(sc);
+    else if (post == POST_END) bicg_end(sc);
   }
+}
+template <int K>
+__global__ void __launch_bounds__(256) k_finalize(const double* __restrict__ partial, int nparts,
+                                                  double* sc, int s0, int s1, int s2,
+                                                  const double* stop, int post) {
+  if (stopped(stop)) return;
+  finalize_block<K>(partial, nparts, sc, s0, s1, post);
+}
+
+// both stages of the fixed-order sum in one launch: the last block to finish
+// its chunk (ticket) runs the second stage over out[] exactly as k_finalize
+// would, then resets the ticket
+template <int K>
+__global__ void __launch_bounds__(256) k_partial_sum_fin(const double* __restrict__ partial,
+                                                         int64_t nparts, double* out, double* sc,
+                                                         int s0, int s1, const double* stop,
+                                                         int post, unsigned* ticket) {
+  if (stopped(stop)) return;
+  __shared__ double sh[K][8];
+  __shared__ bool last;
+  const int t = threadIdx.x, lane = t & 31, w = t >> 5;
+  const int64_t chunk = (nparts + gridDim.x - 1) / gridDim.x;
+  const int64_t lo = (int64_t)blockIdx.x * chunk;
+  const int64_t hi = lo + chunk < nparts ? lo + chunk : nparts;
+#pragma unroll
+  for (int k = 0; k < K; ++k) {
+    double s = 0.0;
+    for (int64_t i = lo + t; i < hi; i += 256) s += partial[(int64_t)k * nparts + i];
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) s += __shfl_down_sync(0xffffffffu, s, o);
+    if (lane == 0) sh[k][w] = s;
+  }
+  __syncthreads();
+  if (t == 0) {
+#pragma unroll
+    for (int k = 0; k < K; ++k) {
+      double s = 0.0;
+      for (int i = 0; i < 8; ++i) s += sh[k][i];
+      out[(int64_t)k * gridDim.x + blockIdx.x] = s;
+    }
+    __threadfence();
+    last = atomicAdd(ticket, 1u) == gridDim.x - 1;
+  }
+  __syncthreads();
+  if (!last) return;
+  __threadfence();
+  finalize_block<K>(out, gridDim.x, sc, s0, s1, post);
+  if (t == 0) *ticket = 0u;
 }
 
 // partial dot products of up to 3 vector pairs over len entries
@@ -1110,25 +1183,9 @@ __global__ void k_bicg_top(double* sc) {     // loop head: it += 1; rho / omega 
   }
   sc[S_RHO] = rho;
 }
-__global__ void k_bicg_den(double* sc) {     // after r^.v: denominator test, alpha
-  if (sc[S_STOP] != 0.0) return;
-  const double den = sc[S_DEN];
-  if (fabs(den) < sc[S_BRK]) { sc[S_STOP] = STOP_DEN; return; }
-  sc[S_ALPHA] = sc[S_RHO] / den;
-}
-__global__ void k_bicg_ss(double* sc) {      // after ||s||: early convergence
-  if (sc[S_STOP] != 0.0) return;
-  if (sqrt(sc[S_SS]) / sc[S_NB] <= sc[S_TOL]) sc[S_STOP] = STOP_CONV_S;
-}
-__global__ void k_bicg_end(double* sc) {     // after t.t, t.s, ||r||, r^.r
-  if (sc[S_STOP] != 0.0) return;
-  const double tt = sc[S_TT];
-  if (tt == 0.0) { sc[S_STOP] = STOP_TT; return; }
-  sc[S_OMEGA] = sc[S_TS] / tt;
-  if (sqrt(sc[S_RR]) / sc[S_NB] <= sc[S_TOL]) { sc[S_STOP] = STOP_CONV; return; }
-  sc[S_RHO_OLD] = sc[S_RHO];
-  sc[S_FIRST] = 0.0;
-}
+__global__ void k_bicg_den(double* sc) { bicg_den(sc); }
+__global__ void k_bicg_ss(double* sc) { bicg_ss(sc); }
+__global__ void k_bicg_end(double* sc) { bicg_end(sc); }
 
 // black-half helpers: x_b += alpha phat_b;  out_b = a_b - b_b;  dot over black rows
 template <int NC>
