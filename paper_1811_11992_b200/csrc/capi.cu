@@ -151,6 +151,8 @@ extern "C" int isc_create(const isc_model_desc* md, const isc_grid_desc* gdsc, i
   CK(cudaMemset(ctx->upw, 0, (size_t)9 * n));
   ALLOC(ctx->bad_d, 8);
   ALLOC(ctx->ticket_d, 4);
+  ALLOC(ctx->wdu_d, std::max(1, nwells) * NU * 8);
+  CK(cudaMallocHost(&ctx->wdu_h, std::max(1, nwells) * NU * 8));
   CK(cudaMemset(ctx->ticket_d, 0, 4));
   CK(cudaMallocHost(&ctx->bad_h, 16));   // [0] bad cell (cell pass / decoupling), [1] factor status
   // solver vectors
@@ -183,7 +185,7 @@ extern "C" int isc_destroy(isc_ctx* ctx) {
   void* ptrs[] = {ctx->depth, ctx->vol, ctx->phi_ref, ctx->gd, ctx->td, ctx->hl_area,
                   ctx->conn_id, ctx->wells_d, ctx->wcell_d, ctx->wout_d, ctx->bhp_d,
                   ctx->capped_d, ctx->rec, ctx->acc, ctx->src, ctx->resid, ctx->diag,
-                  ctx->offd, ctx->upw, ctx->bad_d, ctx->ticket_d, ctx->rhs, ctx->xk, ctx->rk, ctx->rhat,
+                  ctx->offd, ctx->upw, ctx->bad_d, ctx->ticket_d, ctx->wdu_d, ctx->rhs, ctx->xk, ctx->rk, ctx->rhat,
                   ctx->pk, ctx->vk, ctx->phat, ctx->shat, ctx->sk, ctx->tk, ctx->sc,
                   ctx->partial, ctx->partial2, ctx->fbuf, ctx->flags, ctx->fail_d, ctx->ccnz_d, ctx->st_c, ctx->accn_c, ctx->stage,
                   ctx->halo_send_lo, ctx->halo_send_hi, ctx->halo_recv_lo, ctx->halo_recv_hi,
@@ -196,6 +198,7 @@ extern "C" int isc_destroy(isc_ctx* ctx) {
   if (ctx->wout_h) cudaFreeHost(ctx->wout_h);
   if (ctx->bad_h) cudaFreeHost(ctx->bad_h);
   if (ctx->cfail_h) cudaFreeHost(ctx->cfail_h);
+  if (ctx->wdu_h) cudaFreeHost(ctx->wdu_h);
   if (ctx->sc_h) cudaFreeHost(ctx->sc_h);
   for (auto& e : ctx->ev)
     if (e) cudaEventDestroy(e);
@@ -614,6 +617,15 @@ extern "C" int isc_synth_system(isc_ctx* ctx, uint64_t seed) {
 // the Gauss-Jordan pass and queues the read-back of the first singular cell;
 // decouple_check (after a synchronisation) reports it. isc_solve queues the
 // preconditioner setup in between, so the two share one synchronisation.
+// v[u*n + pos[w]] for every well w and row u -> out[w*NU + u]
+__global__ void k_gather_rows(int64_t n, const double* __restrict__ v,
+                              const int64_t* __restrict__ pos, int nw, double* __restrict__ out) {
+  const int t = threadIdx.x;
+  if (t >= nw * NU) return;
+  const int w = t / NU, u = t - w * NU;
+  out[t] = v[(int64_t)u * n + pos[w]];
+}
+
 // condensed-form buffers (lazy; false when the device has no room: the
 // 9-component compact form is used instead)
 static bool cond_alloc(isc_ctx* ctx) {
@@ -1054,15 +1066,21 @@ extern "C" int isc_solve(isc_ctx* ctx, double tol, int32_t maxiter, double* d_du
     k_from_pos<double><<<grid1d(n, 256), 256, 0, ctx->stream>>>(ctx->g, NU, ctx->xk, d_du);
     LAUNCH_CHECK();
   }
-  // bhp back-substitution dbhp = -(r_w + wrow . du_c) / dwdb (linsolve.py:473-478)
-  if (ctx->nw > 0 && h_dbhp) {
-    std::vector<double> duc(NU);
+  // bhp back-substitution dbhp = -(r_w + wrow . du_c) / dwdb (linsolve.py:473-478):
+  // the perforated cells' du gathered in one launch, read back with the final
+  // synchronisation
+  const bool wells = ctx->nw > 0 && h_dbhp;
+  if (wells) {
+    k_gather_rows<<<1, 32 * ((ctx->nw * NU + 31) / 32), 0, ctx->stream>>>(
+        n, ctx->xk, ctx->wcell_d, ctx->nw, ctx->wdu_d);
+    LAUNCH_CHECK();
+    CK(cudaMemcpyAsync(ctx->wdu_h, ctx->wdu_d, (size_t)ctx->nw * NU * 8, cudaMemcpyDeviceToHost,
+                       ctx->stream));
+  }
+  CK(cudaStreamSynchronize(ctx->stream));
+  if (wells) {
     for (int w = 0; w < ctx->nw; ++w) {
-      const int64_t c = ctx->wpos_h[w];
-      for (int u = 0; u < NU; ++u)
-        CK(cudaMemcpyAsync(&duc[u], ctx->xk + (int64_t)u * n + c, 8, cudaMemcpyDeviceToHost,
-                           ctx->stream));
-      CK(cudaStreamSynchronize(ctx->stream));
+      const double* duc = ctx->wdu_h + (size_t)w * NU;
       const double* o = ctx->wout_h + w * WOUT;
       double dotv = 0.0;
       for (int u = 0; u < NU; ++u) dotv += o[2 + u] * duc[u];
@@ -1070,7 +1088,6 @@ extern "C" int isc_solve(isc_ctx* ctx, double tol, int32_t maxiter, double* d_du
       h_dbhp[w] = -s / o[1];
     }
   }
-  CK(cudaStreamSynchronize(ctx->stream));
   return ISC_OK;
 }
 

@@ -113,6 +113,7 @@ struct isc_ctx {
   double* partial = nullptr;
   double* partial2 = nullptr;   // second stage of the fixed-order sums
   unsigned* ticket_d = nullptr; // last-block ticket of k_partial_sum_fin (zero between launches)
+  double *wdu_d = nullptr, *wdu_h = nullptr;   // du of the perforated cells (dbhp)
   double* fbuf = nullptr;       // face fluxes of the face-centric assembly (3*ROW_OS x n)
   int64_t npartial = 0;
   int* flags = nullptr;
