@@ -14,7 +14,8 @@ import sys
 from collections import defaultdict
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
-KERNELS = ["k_cc6_red", "k_cc6_black", "k_mc_factor_compact", "k_cond_es", "k_cond_expand",
+KERNELS = ["k_cc6_red", "k_cc6_black", "k_mc_factor_compact", "k_cc_red_bc", "k_cc6_xred",
+           "k_cond_es", "k_cond_expand",
            "k_cc_red", "k_cc_black", "k_sc_update_p", "k_sc_update_s", "k_sc_update_xr",
            "k_face_eval_light", "k_face_eval_energy", "k_face_gather", "k_decouple_compact_t", "k_decouple_compact",
            "k_cell_props", "k_cell_gas", "k_cell_rows", "k_cc_xred",
@@ -76,8 +77,11 @@ def main(tag):
         p = os.path.join(src, f"full_{tag}_{k}_raw.csv")
         if not os.path.exists(p):
             continue
+        recs = read_raw(p)
+        if not recs:   # the kernel did not launch in this configuration
+            continue
         shutil.copy(p, os.path.join(dst, os.path.basename(p)))
-        d = read_raw(p)[0]
+        d = recs[0]
         u = d["_units"]
         cells = []
         for key, _, _ in METRICS:
