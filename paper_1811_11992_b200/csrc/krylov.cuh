@@ -283,7 +283,9 @@ static int bicgstab_schur_t(isc_ctx* ctx, double tol, int maxiter, int* iters) {
   if (cnd) {
     // h = Dc_b^-1 sum_d B'_bd y_r(g_b): the raw red pass on g_b (y into its
     // red positions), then the black pass's product part, into r, rhat, ch6
-    KScope ks(ctx, KT_SPMV);
+    // (timed with the vector kernels: the half-pass classes keep the
+    // iteration's products only)
+    KScope ks(ctx, KT_VEC);
     if (ctx->gb_fresh) {
       ctx->gb_fresh = false;
       // (slabs: g_b of the ghost planes' black cells, then their red cells' y)
@@ -393,7 +395,7 @@ static int bicgstab_schur_t(isc_ctx* ctx, double tol, int maxiter, int* iters) {
   auto finish = [&]() -> int {   // x_r = b_r - B_rb x_b
     if (cnd) {   // x_r from w and y_r(g), then x_b = g_b + E_b w
       if (halo_exchange(ctx, x, CR)) return ISC_CUDA_ERROR;
-      KScope ks(ctx, KT_SPMV);
+      KScope ks(ctx, KT_VEC);
       k_cc6_xred<<<bh, dim3(32, CR), 0, st>>>(g, ctx->cbc, ctx->diag, ctx->cg9, b, x);
       k_cond_expand<<<RED_BLOCKS, RED_THREADS, 0, st>>>(g, ctx->ces, ctx->cg9, x);
       ctx->launches += 2;
