@@ -821,3 +821,47 @@ def test_compact_decoupling_bitwise_vs_oracle(mode):
         b = ctx.empty(9, n)
         N.check(ctx.L.isc_copy_rhs(ctx.h, N.ptr(b)), "rhs")
         np.testing.assert_array_equal(b.cpu().numpy().T, orhs)
+
+
+@pytest.mark.parametrize("bad_cell", [None, 9, 10])   # cell 9 red, cell 10 black (6x4x4)
+def test_condensed_form_and_its_fallback(bad_cell):
+    """The condensed multicolour solve (compact.cu "condensed form") on an
+    imported flux-row system: with usable local blocks it runs (ctx.condensed)
+    and du solves the system (dense check) with the oracle's condensed
+    iteration count (+-1). Only the black cells are parametrised by E: a red
+    cell whose local rows cannot be condensed (D[6:, S] = 0 while D stays
+    regular) changes nothing, a black one makes the solve refactor in the
+    9-component compact form -- the same du, the oracle taking its
+    9-component path too."""
+    from oracle import isc_oracle as O
+    from types import SimpleNamespace
+    from paper_1811_11992_b200.grid import build_grid
+    from paper_1811_11992_b200.synth import synth_system
+    from paper_1811_11992_b200.model import load_pack
+    grid = build_grid(6, 4, 4, 1.0, 1.0, 1.0, 1.0, 1.0, 1.0, 0.3)
+    pack = load_pack("tube3_pack", grid.phi_ref)
+    diag, offd, resid = synth_system(grid, 9, seed=13)
+    diag, offd = diag.copy(), offd.copy()
+    offd[:, :, 6:, :] = 0.0
+    if bad_cell is not None:
+        diag[bad_cell, 6:, [2, 4, 8]] = 0.0
+        assert abs(np.linalg.det(diag[bad_cell])) > 0.0
+    ws = Workspace(grid, pack, None, wells=(), streams=(), precond="mcilu")
+    load_system(ws, diag, offd, resid)
+    du, _, it = BlockSolver(grid, ws, tol=1e-12, maxiter=500, precond="mcilu").solve([])
+    assert ws.ctx.decoupled_form == "compact"
+    assert ws.ctx.condensed == (bad_cell is None or bad_cell == 9)
+    n = grid.ncell
+    A = np.zeros((9 * n, 9 * n))
+    for c in range(n):
+        A[9 * c:9 * c + 9, 9 * c:9 * c + 9] = diag[c]
+    for ic in range(grid.nconn):
+        a, b = int(grid.conn_a[ic]), int(grid.conn_b[ic])
+        A[9 * a:9 * a + 9, 9 * b:9 * b + 9] = offd[ic, 0]
+        A[9 * b:9 * b + 9, 9 * a:9 * a + 9] = offd[ic, 1]
+    ref = np.linalg.solve(A, -resid.reshape(-1)).reshape(n, 9)
+    assert np.linalg.norm(du - ref) <= 1e-9 * np.linalg.norm(ref), it
+    ows = O.Workspace(grid, SimpleNamespace(nequ=9, nfull=5))
+    ows.diag, ows.offd, ows.resid = diag.copy(), offd.copy(), resid.copy()
+    odu, _, oit = O.BlockSolver(grid, ows, tol=1e-12, maxiter=500, precond="mcilu").solve([])
+    assert abs(it - oit) <= 1, (it, oit)
