@@ -804,10 +804,11 @@ __global__ void __launch_bounds__(MCFC_CELLS * NU, MCFC_MINB) k_mc_factor_compac
 // ||r6|| / ||b|| (r9 = E r6: the constraint rows' components of the full
 // residual are left out of the norm).
 
-// E_S of every owned black cell into es[(i*CR + p)*half + t]; *fail = 1 when
-// a cell's local block is not usable (before or after the compact
-// decoupling: that keeps D^-1[:, :CR] in slots < CR*NU and leaves the local
-// rows' slots alone)
+// E_S of the black cells of g's [tw_lo, tw_hi) into es[(i*CR + p)*half + t];
+// *fail = 1 when a cell's local block is not usable. The decoupling forms the
+// owned cells' E_S from its registers; this kernel covers the ghost planes
+// of a z-slab (their diagonal blocks are assembled here but not decoupled;
+// the local rows' slots are never overwritten).
 __global__ void k_cond_es(Dims g, const double* __restrict__ diag, double* __restrict__ es,
                           int* fail) {
   const int64_t t = g.tw_lo + (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
