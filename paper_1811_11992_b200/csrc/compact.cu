@@ -518,6 +518,9 @@ __global__ void __launch_bounds__(32 * CR, CC_MINB) k_cc_black(
 #ifndef MCFC_MINB
 #define MCFC_MINB 2     // two CTAs per SM: the double-buffered stages take ~99 KB of smem each (16 cells at 3 or 4 per SM: no faster)
 #endif
+// The products use fused multiply-adds (fma(); the translation unit is
+// compiled --fmad=false for the assembly's reference operation order, which
+// this preconditioner -- no reference counterpart -- does not need).
 // Direction tiles are double-buffered with cp.async (LDGSTS: global -> shared
 // without register staging): the loads of direction d+1 -- B_bd rows, the red
 // neighbour's D^-1[:, :CR] and back block rows, its b -- are in flight while
@@ -613,7 +616,7 @@ __global__ void __launch_bounds__(MCFC_CELLS * NU, MCFC_MINB) k_mc_factor_compac
         for (int qq = 0; qq < 2; ++qq) {
           double sr = 0.0;
 #pragma unroll
-          for (int a = 0; a < NU; ++a) sr += brow[qq][a] * T.r[a][ls];
+          for (int a = 0; a < NU; ++a) sr = fma(brow[qq][a], T.r[a][ls], sr);
           grow[qq] += sr;
         }
       }
@@ -627,7 +630,7 @@ __global__ void __launch_bounds__(MCFC_CELLS * NU, MCFC_MINB) k_mc_factor_compac
         for (int qq = 0; qq < 2; ++qq) {
           double sb = 0.0;
 #pragma unroll
-          for (int a = 0; a < NU; ++a) sb += brow[qq][a] * dcol[a];
+          for (int a = 0; a < NU; ++a) sb = fma(brow[qq][a], dcol[a], sb);
           const int q = 2 * tq + qq, s2 = 2 * tc + ss;
           bpsh[q][s2][ls] = sb;
           bp[(int64_t)((d * CR + q) * CR + s2) * g.half + t] = sb;
@@ -650,7 +653,7 @@ __global__ void __launch_bounds__(MCFC_CELLS * NU, MCFC_MINB) k_mc_factor_compac
         for (int qq = 0; qq < 2; ++qq) {
           double sq = 0.0;
 #pragma unroll
-          for (int r = 0; r < CR; ++r) sq += bpr[qq][r] * ocol[r];
+          for (int r = 0; r < CR; ++r) sq = fma(bpr[qq][r], ocol[r], sq);
           qacc[qq][uu] += sq;
         }
       }
@@ -684,7 +687,7 @@ __global__ void __launch_bounds__(MCFC_CELLS * NU, MCFC_MINB) k_mc_factor_compac
       for (int q = 0; q < CR; ++q) {
         double v = qsh[q][pu][ls];
 #pragma unroll
-        for (int ii = 0; ii < NCS; ++ii) v += qsh[q][csec(ii)][ls] * e[ii];
+        for (int ii = 0; ii < NCS; ++ii) v = fma(qsh[q][csec(ii)][ls], e[ii], v);
         qcol[q] = v;
       }
     }
@@ -703,7 +706,7 @@ __global__ void __launch_bounds__(MCFC_CELLS * NU, MCFC_MINB) k_mc_factor_compac
   if (g1 && live) {
     double m = 0.0;
 #pragma unroll
-    for (int r = 0; r < CR; ++r) m += dsh[u][r][ls] * colk[r][ls];
+    for (int r = 0; r < CR; ++r) m = fma(dsh[u][r][ls], colk[r][ls], m);
     const double gv = b[(int64_t)u * n + c] - m;
     g1[(int64_t)u * n + c] = gv;
     if (g2) g2[(int64_t)u * n + c] = gv;
@@ -714,7 +717,7 @@ __global__ void __launch_bounds__(MCFC_CELLS * NU, MCFC_MINB) k_mc_factor_compac
     const int pq = COND ? q + (q >= NCO ? 1 : 0) + (q >= NCO + NCG - 1 ? 1 : 0) : q;
     double s = 0.0;
 #pragma unroll
-    for (int r = 0; r < CR; ++r) s += dsh[pq][r][ls] * qcol[r];
+    for (int r = 0; r < CR; ++r) s = fma(dsh[pq][r][ls], qcol[r], s);
     ucol[q] = (q == u ? 1.0 : 0.0) - s;
     icol[q] = (q == u) ? 1.0 : 0.0;
   }
@@ -769,7 +772,7 @@ __global__ void __launch_bounds__(MCFC_CELLS * NU, MCFC_MINB) k_mc_factor_compac
     for (int r = 0; r < NC; ++r) {
       if (r == kk) continue;
       const double f = colk[r][ls];
-      if (f != 0.0) { ucol[r] -= f * ucol[kk]; icol[r] -= f * icol[kk]; }
+      if (f != 0.0) { ucol[r] = fma(-f, ucol[kk], ucol[r]); icol[r] = fma(-f, icol[kk], icol[r]); }
     }
     __syncthreads();
   }
