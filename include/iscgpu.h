@@ -170,9 +170,8 @@ int isc_set_precond(isc_ctx *ctx, int32_t precond);
  * D^-1[:, :6], the same operator). */
 int isc_decoupled_form(const isc_ctx *ctx);
 /* 1 when the current multicolour factorisation is the condensed one (the
- * red-eliminated BiCGSTAB on 6-component vectors after eliminating each
- * cell's local constraint rows, compact.cu; single GPU, BiCGSTAB, ISC_COND
- * != 0), else 0. No reference counterpart (an internal form of
+ * red-eliminated BiCGSTAB / GMRES on 6-component vectors after eliminating
+ * each cell's local constraint rows, compact.cu; ISC_COND != 0), else 0. No reference counterpart (an internal form of
  * linsolve.BlockSolver.solve, linsolve.py:438-479). */
 int isc_condensed(const isc_ctx *ctx);
 /* Select the Krylov method (isc_krylov); restart = GMRES restart length

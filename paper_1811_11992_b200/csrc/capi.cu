@@ -837,9 +837,8 @@ static int precond_enqueue(isc_ctx* ctx) {
       if (cross && halo_exchange(ctx, ctx->rhs, NU)) return ISC_CUDA_ERROR;
       // condensed form when the decoupling's E_S are usable (checked after
       // its synchronisation; isc_solve refactors in the 9-component form
-      // otherwise) and the iteration is BiCGSTAB
-      ctx->cond = ctx->cond_es && !(ctx->cfail_h && *ctx->cfail_h && ctx->decoupled) &&
-                  ctx->krylov == ISC_KRYLOV_BICGSTAB;
+      // otherwise)
+      ctx->cond = ctx->cond_es && !(ctx->cfail_h && *ctx->cfail_h && ctx->decoupled);
       const int fblocks = grid1d(ctx->g.tw_hi - ctx->g.tw_lo, MCFC_CELLS);
       if (ctx->cond) {
         CK(cudaFuncSetAttribute(k_mc_factor_compact<true>,
@@ -1017,7 +1016,6 @@ extern "C" int isc_set_krylov(isc_ctx* ctx, int32_t krylov, int32_t restart) {
     g_err = "GMRES restart length out of range (1..31, 0 = default)";
     return ISC_BAD_ARGUMENT;
   }
-  if (krylov != ctx->krylov) ctx->factored = false;   // (the condensed form is BiCGSTAB's)
   ctx->krylov = krylov;
   if (restart > 0) ctx->gm_m = restart;
   return ISC_OK;

@@ -564,14 +564,19 @@ static int bicgstab_schur(isc_ctx* ctx, double tol, int maxiter, int* iters) {
 // iteration (BiCGSTAB: two). Stopping test as bicgstab_schur: ||r|| / ||b||
 // of the full system (the Givens residual estimate within a cycle, the true
 // reduced residual at each restart).
-static int gmres_schur(isc_ctx* ctx, double tol, int maxiter, int* iters) {
-  const int64_t len = (int64_t)NU * ctx->g.n;
+// NC = CR: the condensed form (as bicgstab_schur_t): S6 w = h from w = 0,
+// x_b = g_b + E_b w at the end.
+template <int NC>
+static int gmres_schur_t(isc_ctx* ctx, double tol, int maxiter, int* iters) {
+  constexpr bool cnd = NC == CR;
+  const int64_t len9 = (int64_t)NU * ctx->g.n;   // the full decoupled rhs b
+  const int64_t len = (int64_t)NC * ctx->g.n;    // Krylov vectors and basis stride
   const Dims& g = ctx->g;
   cudaStream_t st = ctx->stream;
-  Kry K{ctx, len};
+  Kry K{ctx, len9};
   const int m = std::max(1, std::min(ctx->gm_m, GM_MAXV - 1));
   if (!ctx->gm_V) {
-    if (cudaMalloc(&ctx->gm_V, (size_t)GM_MAXV * len * 8) != cudaSuccess ||
+    if (cudaMalloc(&ctx->gm_V, (size_t)GM_MAXV * len9 * 8) != cudaSuccess ||
         cudaMalloc(&ctx->gm_h, (size_t)4 * (GM_MAXV + 1) * 8) != cudaSuccess) {
       cudaGetLastError();
       g_err = "cannot allocate the GMRES basis";
@@ -590,7 +595,23 @@ static int gmres_schur(isc_ctx* ctx, double tol, int maxiter, int* iters) {
   const double nb = std::sqrt(ctx->sc_h[S_BB]);
   *iters = 0;
   if (nb == 0.0) return ISC_OK;
-  if (ctx->compact && ctx->gb_fresh) {   // g_b from the factorisation
+  if (cnd) {   // h into r and gb (as bicgstab_schur_t)
+    KScope ks(ctx, KT_VEC);
+    if (ctx->gb_fresh) {
+      ctx->gb_fresh = false;
+      TRY(halo_exchange(ctx, ctx->cg9, NU));
+      k_cc_red_bc<<<bh, dim3(32, CR), 0, st>>>(g, ctx->offd, ctx->ccnz_d, ctx->ces, ctx->cg9,
+                                               ctx->cbc);
+      TRY(halo_exchange(ctx, ctx->cg9, CR));
+      k_cc6_black<0, true><<<bh, dim3(32, CR), 0, st>>>(g, ctx->cbp, ctx->diag, ctx->cg9, r,
+                                                        nullptr, nullptr, ctx->partial, 0, 0,
+                                                        nullptr, gb, ctx->ch6);
+      ctx->launches += 2;
+    } else {
+      CK(cudaMemcpyAsync(r, ctx->ch6, len * 8, cudaMemcpyDeviceToDevice, st));
+      CK(cudaMemcpyAsync(gb, ctx->ch6, len * 8, cudaMemcpyDeviceToDevice, st));
+    }
+  } else if (ctx->compact && ctx->gb_fresh) {   // g_b from the factorisation
     ctx->gb_fresh = false;
     CK(cudaMemcpyAsync(gb, r, len * 8, cudaMemcpyDeviceToDevice, st));
   } else {
@@ -604,26 +625,34 @@ static int gmres_schur(isc_ctx* ctx, double tol, int maxiter, int* iters) {
   auto matvec = [&](double* zz, double* out) -> int {   // out = S zz (zz: black in, red scratch)
     {
       KScope ks(ctx, KT_ILU_APPLY);
-      TRY(halo_exchange(ctx, zz, NU));
-      sc_red_launch(ctx, g, bh, zz);
+      TRY(halo_exchange(ctx, zz, NC));
+      if (cnd)
+        k_cc6_red<<<bh, dim3(32, CR), 0, st>>>(g, ctx->cbc, zz, nullptr);
+      else
+        sc_red_launch(ctx, g, bh, zz);
     }
     {
       KScope ks(ctx, KT_SPMV);
-      TRY(halo_exchange(ctx, zz, NU));
-      sc_black_launch<1>(ctx, g, bh, zz, out, zz, nullptr, bh, 0);
+      TRY(halo_exchange(ctx, zz, cnd ? CR : NU));
+      if (cnd)
+        k_cc6_black<1, false><<<bh, dim3(32, CR), 0, st>>>(g, ctx->cbp, ctx->diag, zz, out, zz,
+                                                           nullptr, ctx->partial, bh, 0, nullptr,
+                                                           nullptr, nullptr);
+      else
+        sc_black_launch<1>(ctx, g, bh, zz, out, zz, nullptr, bh, 0);
     }
     ctx->launches += 2;
     return cudaGetLastError() == cudaSuccess ? 0 : ISC_CUDA_ERROR;
   };
   auto norm2_into = [&](const double* a, int slot) -> int {
     KScope ks(ctx, KT_VEC);
-    k_sc_dot<NU><<<RED_BLOCKS, RED_THREADS, 0, st>>>(g, a, a, ctx->partial);
+    k_sc_dot<NC><<<RED_BLOCKS, RED_THREADS, 0, st>>>(g, a, a, ctx->partial);
     ++ctx->launches;
     return K.finalize1(RED_BLOCKS, slot);
   };
   auto multidot = [&](int nv, const double* w, double* hout) -> int {
     KScope ks(ctx, KT_VEC);
-    k_sc_multidot<<<RED_BLOCKS, RED_THREADS, 0, st>>>(g, V, len, nv, w, ctx->partial);
+    k_sc_multidot<NC><<<RED_BLOCKS, RED_THREADS, 0, st>>>(g, V, len, nv, w, ctx->partial);
     k_sum_partials<<<GM_MAXV + 1, 32, 0, st>>>(ctx->partial, RED_BLOCKS, GM_MAXV + 1, hout);
     ctx->launches += 2;
     if (cudaGetLastError() != cudaSuccess) return ISC_CUDA_ERROR;
@@ -644,7 +673,7 @@ static int gmres_schur(isc_ctx* ctx, double tol, int maxiter, int* iters) {
     }
     {
       KScope ks(ctx, KT_VEC);
-      k_sc_scale<<<RED_BLOCKS, RED_THREADS, 0, st>>>(g, r, ctx->sc + S_RR, V);   // v0 = r / beta
+      k_sc_scale<NC><<<RED_BLOCKS, RED_THREADS, 0, st>>>(g, r, ctx->sc + S_RR, V);   // v0 = r / beta
     }
     ++ctx->launches;
     std::fill(gv.begin(), gv.end(), 0.0);
@@ -657,22 +686,22 @@ static int gmres_schur(isc_ctx* ctx, double tol, int maxiter, int* iters) {
       double* w = V + (int64_t)(j + 1) * len;
       {
         KScope ks(ctx, KT_VEC);
-        k_sc_precond<<<RED_BLOCKS, RED_THREADS, 0, st>>>(g, vj, uinv, z);
+        k_sc_precond<NC><<<RED_BLOCKS, RED_THREADS, 0, st>>>(g, vj, uinv, z);
       }
       ++ctx->launches;
       TRY(matvec(z, w));
       TRY(multidot(j + 1, w, h1));
       {
         KScope ks(ctx, KT_VEC);
-        k_sc_multiaxpy<<<RED_BLOCKS, RED_THREADS, 0, st>>>(g, V, len, j + 1, h1, 1.0, w, 0,
-                                                           nullptr);
+        k_sc_multiaxpy<NC><<<RED_BLOCKS, RED_THREADS, 0, st>>>(g, V, len, j + 1, h1, 1.0, w, 0,
+                                                               nullptr);
       }
       ++ctx->launches;
       TRY(multidot(j + 1, w, h2));
       {
         KScope ks(ctx, KT_VEC);
-        k_sc_multiaxpy<<<RED_BLOCKS, RED_THREADS, 0, st>>>(g, V, len, j + 1, h2, 1.0, w, 0,
-                                                           ctx->partial);
+        k_sc_multiaxpy<NC><<<RED_BLOCKS, RED_THREADS, 0, st>>>(g, V, len, j + 1, h2, 1.0, w, 0,
+                                                               ctx->partial);
       }
       ++ctx->launches;
       TRY(K.finalize1(RED_BLOCKS, S_TT));   // ||w||^2 after CGS2
@@ -689,7 +718,7 @@ static int gmres_schur(isc_ctx* ctx, double tol, int maxiter, int* iters) {
       }
       if (hn > 0.0) {
         KScope ks(ctx, KT_VEC);
-        k_sc_scale<<<RED_BLOCKS, RED_THREADS, 0, st>>>(g, w, ctx->sc + S_TT, w);
+        k_sc_scale<NC><<<RED_BLOCKS, RED_THREADS, 0, st>>>(g, w, ctx->sc + S_TT, w);
         ++ctx->launches;
       }
       for (int i = 0; i < j; ++i) {
@@ -721,20 +750,31 @@ static int gmres_schur(isc_ctx* ctx, double tol, int maxiter, int* iters) {
     CK(cudaMemcpyAsync(yd, y.data(), j * 8, cudaMemcpyHostToDevice, st));
     {
       KScope ks(ctx, KT_VEC);
-      k_sc_multiaxpy<<<RED_BLOCKS, RED_THREADS, 0, st>>>(g, V, len, j, yd, -1.0, u, 1, nullptr);
-      k_sc_precond<<<RED_BLOCKS, RED_THREADS, 0, st>>>(g, u, uinv, z);
-      k_sc_add<<<RED_BLOCKS, RED_THREADS, 0, st>>>(g, z, x);
+      k_sc_multiaxpy<NC><<<RED_BLOCKS, RED_THREADS, 0, st>>>(g, V, len, j, yd, -1.0, u, 1,
+                                                             nullptr);
+      k_sc_precond<NC><<<RED_BLOCKS, RED_THREADS, 0, st>>>(g, u, uinv, z);
+      k_sc_add<NC><<<RED_BLOCKS, RED_THREADS, 0, st>>>(g, z, x);
     }
     ctx->launches += 3;
     if (res / nb <= tol) break;
     // restart: r_b = g_b - S x_b
     CK(cudaMemcpyAsync(u, x, len * 8, cudaMemcpyDeviceToDevice, st));
     TRY(matvec(u, t));
-    k_sc_sub<NU><<<RED_BLOCKS, RED_THREADS, 0, st>>>(g, gb, t, r, z);
+    k_sc_sub<NC><<<RED_BLOCKS, RED_THREADS, 0, st>>>(g, gb, t, r, z);
     ++ctx->launches;
     TRY(norm2_into(r, S_RR));
     TRY(K.read_scalars());
     beta = std::sqrt(ctx->sc_h[S_RR]);
+  }
+  if (cnd) {   // x_r from w and y_r(g), then x_b = g_b + E_b w
+    TRY(halo_exchange(ctx, x, CR));
+    KScope ks(ctx, KT_VEC);
+    k_cc6_xred<<<bh, dim3(32, CR), 0, st>>>(g, ctx->cbc, ctx->diag, ctx->cg9, b, x);
+    k_cond_expand<<<RED_BLOCKS, RED_THREADS, 0, st>>>(g, ctx->ces, ctx->cg9, x);
+    ctx->launches += 2;
+    *iters = it;
+    CK(cudaStreamSynchronize(st));
+    return ISC_OK;
   }
   // x_r = b_r - B_rb x_b
   TRY(halo_exchange(ctx, x, NU));
@@ -746,6 +786,10 @@ static int gmres_schur(isc_ctx* ctx, double tol, int maxiter, int* iters) {
   *iters = it;
   CK(cudaStreamSynchronize(st));
   return ISC_OK;
+}
+static int gmres_schur(isc_ctx* ctx, double tol, int maxiter, int* iters) {
+  return ctx->cond ? gmres_schur_t<CR>(ctx, tol, maxiter, iters)
+                   : gmres_schur_t<NU>(ctx, tol, maxiter, iters);
 }
 
 // 0: not decoupled, 1: explicit decoupled blocks, 2: compact form (compact.cu)

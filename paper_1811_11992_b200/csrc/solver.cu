@@ -1238,6 +1238,7 @@ __global__ void __launch_bounds__(RED_THREADS, VEC_MINB) k_sc_dot(Dims g, const 
 constexpr int GM_MAXV = 32;   // basis vectors held (restart length GM_MAXV - 1)
 
 // z_b = U_b^-1 v_b
+template <int NC>
 __global__ void __launch_bounds__(RED_THREADS, VEC_MINB) k_sc_precond(Dims g,
                                                                       const double* __restrict__ v,
                                                                       const double* __restrict__ uinv,
@@ -1247,17 +1248,17 @@ __global__ void __launch_bounds__(RED_THREADS, VEC_MINB) k_sc_precond(Dims g,
     const int64_t c = colour_pos(g, 1, t);
     if (!owned_k(g, plane_of(g, c))) {   // ghost plane (slabs): filled by the halo exchange
 #pragma unroll
-      for (int q = 0; q < NU; ++q) z[q * n + c] = 0.0;
+      for (int q = 0; q < NC; ++q) z[q * n + c] = 0.0;
       continue;
     }
-    double pv[NU];
+    double pv[NC];
 #pragma unroll
-    for (int q = 0; q < NU; ++q) pv[q] = v[q * n + c];
+    for (int q = 0; q < NC; ++q) pv[q] = v[q * n + c];
 #pragma unroll
-    for (int q = 0; q < NU; ++q) {
+    for (int q = 0; q < NC; ++q) {
       double zz = 0.0;
 #pragma unroll
-      for (int u = 0; u < NU; ++u) zz += uinv[(int64_t)(q * NU + u) * n + c] * pv[u];
+      for (int u = 0; u < NC; ++u) zz += uinv[(int64_t)(q * NC + u) * n + c] * pv[u];
       z[q * n + c] = zz;
     }
   }
@@ -1265,6 +1266,7 @@ __global__ void __launch_bounds__(RED_THREADS, VEC_MINB) k_sc_precond(Dims g,
 
 // per-block partials of h_i = V_i . w (i < nv) and, when w2 == nullptr, of
 // w . w in slot nv; partial[i * gridDim.x + block] (fixed order, owned rows)
+template <int NC>
 __global__ void __launch_bounds__(RED_THREADS, 2) k_sc_multidot(Dims g, const double* __restrict__ V,
                                                                 int64_t vs, int nv,
                                                                 const double* __restrict__ w,
@@ -1277,7 +1279,7 @@ __global__ void __launch_bounds__(RED_THREADS, 2) k_sc_multidot(Dims g, const do
     const int64_t c = colour_pos(g, 1, t);
     if (!owned_k(g, plane_of(g, c))) continue;
 #pragma unroll 1
-    for (int q = 0; q < NU; ++q) {
+    for (int q = 0; q < NC; ++q) {
       const double wq = w[q * n + c];
 #pragma unroll
       for (int i = 0; i < GM_MAXV; ++i)
@@ -1316,6 +1318,7 @@ __global__ void k_sum_partials(const double* __restrict__ partial, int nparts, i
 
 // w = (zero ? 0 : w) - sum_{i<nv} h_i V_i over owned black rows; partial w.w
 // (when partial != nullptr)
+template <int NC>
 __global__ void __launch_bounds__(RED_THREADS, VEC_MINB) k_sc_multiaxpy(Dims g, const double* __restrict__ V,
                                                                         int64_t vs, int nv,
                                                                         const double* __restrict__ h,
@@ -1331,11 +1334,11 @@ __global__ void __launch_bounds__(RED_THREADS, VEC_MINB) k_sc_multiaxpy(Dims g, 
     const int64_t c = colour_pos(g, 1, t);
     if (!owned_k(g, plane_of(g, c))) {
 #pragma unroll
-      for (int q = 0; q < NU; ++q) w[q * n + c] = 0.0;
+      for (int q = 0; q < NC; ++q) w[q * n + c] = 0.0;
       continue;
     }
 #pragma unroll 1
-    for (int q = 0; q < NU; ++q) {
+    for (int q = 0; q < NC; ++q) {
       double x = zero ? 0.0 : w[q * n + c];
       for (int i = 0; i < nv; ++i) x -= hs[i] * V[(int64_t)i * vs + q * n + c];
       w[q * n + c] = x;
@@ -1346,6 +1349,7 @@ __global__ void __launch_bounds__(RED_THREADS, VEC_MINB) k_sc_multiaxpy(Dims g, 
 }
 
 // out = w / sqrt(nn[0]) (owned black rows)
+template <int NC>
 __global__ void k_sc_scale(Dims g, const double* __restrict__ w, const double* __restrict__ nn,
                            double* __restrict__ out) {
   const int64_t n = g.n;
@@ -1353,17 +1357,18 @@ __global__ void k_sc_scale(Dims g, const double* __restrict__ w, const double* _
   SC_LOOP(t) {
     const int64_t c = colour_pos(g, 1, t);
 #pragma unroll
-    for (int q = 0; q < NU; ++q) out[q * n + c] = w[q * n + c] * inv;
+    for (int q = 0; q < NC; ++q) out[q * n + c] = w[q * n + c] * inv;
   }
 }
 
 // x_b += z_b
+template <int NC>
 __global__ void k_sc_add(Dims g, const double* __restrict__ z, double* __restrict__ x) {
   const int64_t n = g.n;
   SC_LOOP(t) {
     const int64_t c = colour_pos(g, 1, t);
 #pragma unroll
-    for (int q = 0; q < NU; ++q) x[q * n + c] += z[q * n + c];
+    for (int q = 0; q < NC; ++q) x[q * n + c] += z[q * n + c];
   }
 }
 
