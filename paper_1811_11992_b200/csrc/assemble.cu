@@ -1230,12 +1230,14 @@ __global__ void __launch_bounds__(32 * 3, FEVE_MINB) k_face_eval_energy(const Fa
 #ifndef FG_MINB
 #define FG_MINB 4   // C4 sweep 1..8: 4 (85 registers) best; without a minimum the compiler capped at 64
 #endif
-__global__ void __launch_bounds__(32 * ROW_OS, FG_MINB) k_face_gather(const FaceArgs2 A2) {
+__global__ void __launch_bounds__(32 * ROW_OS, FG_MINB) k_face_gather(const FaceArgs2 A2,
+                                                                      int64_t c_begin,
+                                                                      int64_t c_end) {
   const FaceArgs& F = A2.F;
   const int64_t n = F.g.n;
-  const int64_t c = (int64_t)F.g.kw_lo * F.g.nxny + (int64_t)blockIdx.x * 32 + threadIdx.x;
+  const int64_t c = c_begin + (int64_t)blockIdx.x * 32 + threadIdx.x;
   const int row = threadIdx.y;
-  if (c >= (int64_t)F.g.kw_hi * F.g.nxny) return;
+  if (c >= c_end) return;
   int i, j, k;
   const int64_t cell = locate(F.g, c, i, j, k);
   double res = F.resid[row * n + c];

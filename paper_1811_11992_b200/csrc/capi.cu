@@ -276,8 +276,8 @@ extern "C" int isc_assemble(isc_ctx* ctx, const double* d_state, const double* h
   cudaStream_t st = ctx->stream;
   ctx->assembled = false;
   // set by isc_assemble_host when it ran these passes while staging
-  const bool cell_pre = ctx->cell_pre, face_pre = ctx->face_pre;
-  ctx->cell_pre = ctx->face_pre = false;
+  const bool cell_pre = ctx->cell_pre, face_pre = ctx->face_pre, gather_pre = ctx->gather_pre;
+  ctx->cell_pre = ctx->face_pre = ctx->gather_pre = false;
   STAGE(stage_begin(ctx, 0));
   if (ctx->nw > 0) {
     CK(cudaMemcpyAsync(ctx->bhp_d, h_bhp, ctx->nw * 8, cudaMemcpyHostToDevice, st));
@@ -318,9 +318,11 @@ extern "C" int isc_assemble(isc_ctx* ctx, const double* d_state, const double* h
       CK(cudaMemsetAsync(ctx->ccnz_d, 0, 4, st));   // set by k_face_eval* on a nonzero
       launch_face_eval(F2, 0, n, 0, 3, st);
     }
-    k_face_gather<<<grid1d((int64_t)(ctx->g.kw_hi - ctx->g.kw_lo) * ctx->g.nxny, 32),
-                    dim3(32, ROW_OS), 0, st>>>(F2);
-    ++ctx->launches;
+    if (!gather_pre) {
+      const int64_t c0 = (int64_t)ctx->g.kw_lo * ctx->g.nxny, c1 = (int64_t)ctx->g.kw_hi * ctx->g.nxny;
+      k_face_gather<<<grid1d(c1 - c0, 32), dim3(32, ROW_OS), 0, st>>>(F2, c0, c1);
+      ++ctx->launches;
+    }
   }
   LAUNCH_CHECK();
   if (ctx->nw > 0) {
@@ -415,7 +417,30 @@ extern "C" int isc_assemble_host(isc_ctx* ctx, const double* h_p, const double* 
   // overlaps the cell kernel (one chunk on z-slabs, whose cell pass needs
   // the halo exchange of the whole state first).
   const bool pipe = !ctx->comm.active();
-  const int nq = pipe ? std::min(8, g.nz) : 1;
+  static const int nq_max = [] {   // plane chunks of the staged copy (ISC_H2D_CHUNKS, 1..32)
+    const char* e = std::getenv("ISC_H2D_CHUNKS");
+    const int v = e ? std::atoi(e) : 9;
+    return std::max(1, std::min(32, v));
+  }();
+  static const int first_planes = [] {   // planes of the first chunk (ISC_H2D_FIRST)
+    const char* e = std::getenv("ISC_H2D_FIRST");
+    return std::max(1, e ? std::atoi(e) : 3);
+  }();
+  // chunk bounds: a thin first chunk (the compute starts as soon as it has
+  // landed), the remaining planes in nq - 1 equal chunks (every chunk costs
+  // the ramp and tail of its ~10 kernels)
+  int kb[34];
+  int nq = 1;
+  kb[0] = 0;
+  kb[1] = g.nz;
+  if (pipe && nq_max > 1 && g.nz > first_planes) {
+    const int nrest = std::min(nq_max - 1, g.nz - first_planes);
+    nq = 1 + nrest;
+    kb[1] = first_planes;
+    for (int q = 1; q <= nrest; ++q)
+      kb[1 + q] = first_planes + (int)((int64_t)(g.nz - first_planes) * q / nrest);
+  }
+  int64_t gathered = 0;   // positions whose faces are all evaluated and gathered
   CK(cudaMemsetAsync(ctx->bad_d, 0xff, 8, st));
   CK(cudaEventRecord(ctx->chunk_ev[0], st));
   CK(cudaStreamWaitEvent(ctx->cstream, ctx->chunk_ev[0], 0));   // stage buffer free
@@ -427,7 +452,7 @@ extern "C" int isc_assemble_host(isc_ctx* ctx, const double* h_p, const double* 
   FaceArgs2 F2{F, ctx->fbuf};
   if (pipe) CK(cudaMemsetAsync(ctx->ccnz_d, 0, 4, st));
   for (int q = 0; q < nq; ++q) {
-    const int64_t k0 = (int64_t)g.nz * q / nq, k1 = (int64_t)g.nz * (q + 1) / nq;
+    const int64_t k0 = kb[q], k1 = kb[q + 1];
     const int64_t c0 = k0 * g.nxny, c1 = k1 * g.nxny, cnt = c1 - c0;
     const size_t b = (size_t)cnt * 8;
     cudaStream_t cs = ctx->cstream;
@@ -452,24 +477,34 @@ extern "C" int isc_assemble_host(isc_ctx* ctx, const double* h_p, const double* 
         launch_cell(ctx, A, st);
       }
       KScope ks(ctx, KT_FACE);
-      // x/y faces of this chunk's cells; z faces of the plane below it and of
-      // all but its last plane (their upper records now exist)
-      launch_face_eval(F2, c0, c1, 0, 2, st);
+      // all three axes of the planes whose upper neighbours' records now
+      // exist: the last plane of the previous chunk up to this chunk's last
+      // but one (one launch per row class, the axes share the record loads)
       const int64_t z0 = std::max<int64_t>(0, (k0 - 1) * g.nxny), z1 = (k1 - 1) * g.nxny;
-      if (z1 > z0)
-        launch_face_eval(F2, z0, z1, 2, 1, st);
-      ctx->launches += 3;
+      if (z1 > z0) {
+        launch_face_eval(F2, z0, z1, 0, 3, st);
+        ctx->launches += 2;
+      }
+      // every face of the planes below k1 - 1 is now evaluated: gather them
+      // while the next chunk is still on the bus
+      if (z1 > gathered) {
+        k_face_gather<<<grid1d(z1 - gathered, 32), dim3(32, ROW_OS), 0, st>>>(F2, gathered, z1);
+        ++ctx->launches;
+        gathered = z1;
+      }
     }
   }
-  if (pipe) {   // z faces of the top plane (boundary: zero blocks)
+  if (pipe) {   // the top plane's faces (+z: boundary, zero blocks), the last planes' gather
     KScope ks(ctx, KT_FACE);
     const int64_t z0 = (int64_t)(g.nz - 1) * g.nxny;
-    launch_face_eval(F2, z0, n, 2, 1, st);
-    ++ctx->launches;
+    launch_face_eval(F2, z0, n, 0, 3, st);
+    k_face_gather<<<grid1d(n - gathered, 32), dim3(32, ROW_OS), 0, st>>>(F2, gathered, n);
+    ctx->launches += 2;
   }
   LAUNCH_CHECK();
   ctx->cell_pre = pipe;
   ctx->face_pre = pipe;
+  ctx->gather_pre = pipe;
   return isc_assemble(ctx, nullptr, h_bhp, nullptr, dt, t_new, h_capped, freeze, h_wells_out,
                       bad_cell);
 }

@@ -50,10 +50,11 @@ struct isc_ctx {
   cudaStream_t stream = nullptr;
   cudaStream_t own_stream = nullptr;
   cudaStream_t cstream = nullptr;          // host->device staging copies (isc_assemble_host)
-  cudaEvent_t chunk_ev[8] = {};
+  cudaEvent_t chunk_ev[32] = {};
   cudaEvent_t halo_ev[2] = {};             // halo planes packed / landed
   bool cell_pre = false;                   // k_cell already ran (pipelined host staging)
   bool face_pre = false;                   // k_face_eval too
+  bool gather_pre = false;                 // and k_face_gather
   bool mc_schur = true;   // mcilu: red-eliminated BiCGSTAB (ISC_MCILU_FULL=1: full system)
   int krylov = ISC_KRYLOV_BICGSTAB;   // mcilu red-eliminated system: BiCGSTAB or GMRES(m)
   int gm_m = 30;                      // GMRES restart length (<= GM_MAXV - 1)
