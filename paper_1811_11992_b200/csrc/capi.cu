@@ -875,7 +875,15 @@ static int precond_enqueue(isc_ctx* ctx) {
       // otherwise)
       ctx->cond = ctx->cond_es && !(ctx->cfail_h && *ctx->cfail_h && ctx->decoupled);
       const int fblocks = grid1d(ctx->g.tw_hi - ctx->g.tw_lo, MCFC_CELLS);
-      if (ctx->cond) {
+      // ISC_MCF_T=0: the cooperative (shared-memory) kernel instead of the
+      // thread-per-cell one (same values; tests compare them)
+      const char* mcf_env = std::getenv("ISC_MCF_T");
+      const bool factor_t = !mcf_env || std::atoi(mcf_env) != 0;
+      if (ctx->cond && factor_t) {
+        k_mc_factor_cond_t<<<grid1d(ctx->g.tw_hi - ctx->g.tw_lo, MCFT_THREADS), MCFT_THREADS, 0,
+                             st>>>(ctx->g, ctx->offd, ctx->diag, ctx->mc_uinv, ctx->cbp,
+                                   ctx->fail_d, ctx->rhs, ctx->cg9, ctx->ces);
+      } else if (ctx->cond) {
         CK(cudaFuncSetAttribute(k_mc_factor_compact<true>,
                                 cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(McfcSmem)));
         k_mc_factor_compact<true><<<fblocks, dim3(MCFC_CELLS, NU), sizeof(McfcSmem), st>>>(

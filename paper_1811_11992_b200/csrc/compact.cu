@@ -782,6 +782,207 @@ __global__ void __launch_bounds__(MCFC_CELLS * NU, MCFC_MINB) k_mc_factor_compac
   }
 }
 
+// The condensed factorisation with one thread per black cell and everything
+// in registers (no shared memory, no barriers): Q (6 x 9), the direction's
+// B' (6 x 6) and the streamed rows / columns of the tiles. Per direction the
+// thread streams column a of B_bd[:CR, :] with row a of the red neighbour's
+// D^-1[:, :CR] (36 fused multiply-adds per 12 loads), then column u of the
+// back block (36 per 6 loads); the sums run in the cooperative kernel's
+// order (each B' and per-direction Q entry a chain over the inner index from
+// zero), so the two kernels give the same values. Then U6 = I - Dc_b^-1 Q E_b
+// and its Gauss-Jordan inverse on [U6 | I] (row interchanges by opaque
+// selects, as k_decouple_compact_t).
+#ifndef MCFT_THREADS
+#define MCFT_THREADS 64
+#endif
+#ifndef MCFT_MINB
+#define MCFT_MINB 4   // C4 sweep 3..8 (64 threads): 3-4 best (222 registers, no spills)
+#endif
+#ifndef MCFT_UA
+#define MCFT_UA 9   // unroll of the streamed loops = loads in flight per thread (C4: 9/3 best; 9/9 spills)
+#endif
+#ifndef MCFT_UU
+#define MCFT_UU 3
+#endif
+constexpr int kMcftUA = MCFT_UA, kMcftUU = MCFT_UU;
+#ifndef MCFT_QSMEM
+#define MCFT_QSMEM 1   // Q in shared memory (one slot per thread): registers for more resident warps
+#endif
+__global__ void __launch_bounds__(MCFT_THREADS, MCFT_MINB) k_mc_factor_cond_t(
+    Dims g, const double* __restrict__ offd, const double* __restrict__ dinv,
+    double* __restrict__ uinv, double* __restrict__ bp, int* fail, const double* __restrict__ b,
+    double* __restrict__ g1, const double* __restrict__ es) {
+  const int64_t n = g.n;
+  const int64_t t = g.tw_lo + (int64_t)blockIdx.x * MCFT_THREADS + threadIdx.x;
+  if (t >= g.tw_hi) return;
+  const int64_t c = colour_pos(g, 1, t);
+  int i, j, k;
+  const int64_t cell = locate(g, c, i, j, k);
+  if (!owned_k(g, k)) return;
+#if MCFT_QSMEM
+  __shared__ double Qs[CR * NU][MCFT_THREADS];
+#define QREF(q, u) Qs[(q) * NU + (u)][threadIdx.x]
+#else
+  double Qr[CR][NU];
+#define QREF(q, u) Qr[q][u]
+#endif
+  double grow[CR];
+#pragma unroll
+  for (int q = 0; q < CR; ++q) {
+    grow[q] = 0.0;
+#pragma unroll
+    for (int u = 0; u < NU; ++u) QREF(q, u) = 0.0;
+  }
+#pragma unroll 1
+  for (int d = 0; d < NDIR; ++d) {
+    const int64_t nb = nb_pos(g, cell, i, j, k, d);
+    if (nb < 0) continue;
+    const double* Bd = offd + (int64_t)d * NB * n + c;              // B_bd[q][a] at (q*NU + a)*n
+    const double* Dn = dinv + nb;                                    // D_nb^-1[a][s] at (a*CR + s)*n
+    const double* Bk = offd + (int64_t)opposite(d) * NB * n + nb;    // B_back[r][u] at (r*NU + u)*n
+    double Bp[CR][CR], sr[CR];
+#pragma unroll
+    for (int q = 0; q < CR; ++q) {
+      sr[q] = 0.0;
+#pragma unroll
+      for (int s2 = 0; s2 < CR; ++s2) Bp[q][s2] = 0.0;
+    }
+#pragma unroll(kMcftUA)
+    for (int a = 0; a < NU; ++a) {
+      double bc[CR], dr[CR];
+#pragma unroll
+      for (int q = 0; q < CR; ++q) bc[q] = Bd[(int64_t)(q * NU + a) * n];
+#pragma unroll
+      for (int s2 = 0; s2 < CR; ++s2) dr[s2] = Dn[(int64_t)(a * CR + s2) * n];
+      const double ra = b[(int64_t)a * n + nb];
+#pragma unroll
+      for (int q = 0; q < CR; ++q) {
+        sr[q] = fma(bc[q], ra, sr[q]);
+#pragma unroll
+        for (int s2 = 0; s2 < CR; ++s2) Bp[q][s2] = fma(bc[q], dr[s2], Bp[q][s2]);
+      }
+    }
+#pragma unroll
+    for (int q = 0; q < CR; ++q) {
+      grow[q] += sr[q];
+#pragma unroll
+      for (int s2 = 0; s2 < CR; ++s2)
+        bp[(int64_t)((d * CR + q) * CR + s2) * g.half + t] = Bp[q][s2];
+    }
+#pragma unroll(kMcftUU)
+    for (int u = 0; u < NU; ++u) {
+      double oc[CR];
+#pragma unroll
+      for (int r = 0; r < CR; ++r) oc[r] = Bk[(int64_t)(r * NU + u) * n];
+#pragma unroll
+      for (int q = 0; q < CR; ++q) {
+        double sq = 0.0;
+#pragma unroll
+        for (int r = 0; r < CR; ++r) sq = fma(Bp[q][r], oc[r], sq);
+        QREF(q, u) += sq;
+      }
+    }
+  }
+  // QE = Q E_b: column u of the primary unknowns plus the secondary columns through E_S
+  double QE[CR][CR];
+  {
+    double e[NCS][CR];
+#pragma unroll
+    for (int ii = 0; ii < NCS; ++ii)
+#pragma unroll
+      for (int u = 0; u < CR; ++u) e[ii][u] = es[(int64_t)(ii * CR + u) * g.half + t];
+#pragma unroll
+    for (int q = 0; q < CR; ++q)
+#pragma unroll
+      for (int u = 0; u < CR; ++u) {
+        double v = QREF(q, cprim(u));
+#pragma unroll
+        for (int ii = 0; ii < NCS; ++ii) v = fma(QREF(q, csec(ii)), e[ii][u], v);
+        QE[q][u] = v;
+      }
+  }
+#undef QREF
+  // rows of D_b^-1[:, :CR]: g_b = b_b - D_b^-1[:, :CR] grow (all nine), and
+  // U6 = I - Dc_b^-1 QE from the primary rows
+  double a[CR][CR];
+#pragma unroll
+  for (int q9 = 0; q9 < NU; ++q9) {
+    double dr[CR];
+#pragma unroll
+    for (int r = 0; r < CR; ++r) dr[r] = dinv[(int64_t)(q9 * CR + r) * n + c];
+    double m = 0.0;
+#pragma unroll
+    for (int r = 0; r < CR; ++r) m = fma(dr[r], grow[r], m);
+    g1[(int64_t)q9 * n + c] = b[(int64_t)q9 * n + c] - m;
+    const bool prim = q9 != csec(0) && q9 != csec(1) && q9 != csec(2);
+    if (prim) {
+      const int q = q9 - (q9 > csec(0) ? 1 : 0) - (q9 > csec(1) ? 1 : 0);
+#pragma unroll
+      for (int u = 0; u < CR; ++u) {
+        double s2 = 0.0;
+#pragma unroll
+        for (int r = 0; r < CR; ++r) s2 = fma(dr[r], QE[r][u], s2);
+        a[q][u] = (q == u ? 1.0 : 0.0) - s2;
+      }
+    }
+  }
+  // in-place Gauss-Jordan (slot j ends as column perm[j] of the inverse):
+  // the cooperative kernel's pivot rule and operations
+  double amax = 0.0;
+#pragma unroll
+  for (int r = 0; r < CR; ++r)
+#pragma unroll
+    for (int u = 0; u < CR; ++u) amax = fmax(amax, fabs(a[r][u]));
+  const double tol = 1e-13 * amax;
+  bool bad = false;
+  int perm[CR];
+#pragma unroll
+  for (int r = 0; r < CR; ++r) perm[r] = r;
+#pragma unroll
+  for (int kk = 0; kk < CR; ++kk) {
+    int piv = kk;
+    double pv = fabs(a[kk][kk]);
+#pragma unroll
+    for (int r = kk + 1; r < CR; ++r) {
+      const double v = fabs(a[r][kk]);
+      if (v > pv) { pv = v; piv = r; }
+    }
+    bad = bad || pv <= tol || amax == 0.0;
+#pragma unroll
+    for (int q = kk + 1; q < CR; ++q) {
+      const bool sw = q == piv;
+#pragma unroll
+      for (int u = 0; u < CR; ++u) {
+        const double x = a[kk][u];
+        a[kk][u] = sel_d(sw, a[q][u], x);
+        a[q][u] = sel_d(sw, x, a[q][u]);
+      }
+      const int x = perm[kk];
+      perm[kk] = sel_i(sw, perm[q], x);
+      perm[q] = sel_i(sw, x, perm[q]);
+    }
+    const double dv = 1.0 / a[kk][kk];
+#pragma unroll
+    for (int u = 0; u < CR; ++u) a[kk][u] = (u == kk ? 1.0 : a[kk][u]) * dv;
+#pragma unroll
+    for (int r = 0; r < CR; ++r) {
+      if (r == kk) continue;
+      const double f = a[r][kk];
+      if (f != 0.0) {
+#pragma unroll
+        for (int u = 0; u < CR; ++u) a[r][u] = fma(-f, a[kk][u], u == kk ? 0.0 : a[r][u]);
+      }
+    }
+  }
+  if (bad) atomicMin(fail, 1);
+#pragma unroll
+  for (int u = 0; u < CR; ++u) {
+    double* dst = uinv + (int64_t)perm[u] * n + c;
+#pragma unroll
+    for (int r = 0; r < CR; ++r) dst[(int64_t)(r * CR) * n] = a[r][u];
+  }
+}
+
 // ------------------------------------------------------ condensed form
 //
 // The local rows ROW_OS.. of an assembled system (the oil and gas mole-

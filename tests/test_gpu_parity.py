@@ -865,3 +865,42 @@ def test_condensed_form_and_its_fallback(bad_cell):
     ows.diag, ows.offd, ows.resid = diag.copy(), offd.copy(), resid.copy()
     odu, _, oit = O.BlockSolver(grid, ows, tol=1e-12, maxiter=500, precond="mcilu").solve([])
     assert abs(it - oit) <= 1, (it, oit)
+
+
+@pytest.mark.parametrize("shape,scale", [((6, 4, 4), 1.0), ((10, 6, 5), 1.0), ((10, 6, 5), 1.3), ((6, 4, 4), 1.6)])
+def test_condensed_factorisation_kernels_agree(shape, scale, monkeypatch):
+    """The thread-per-cell condensed factorisation (k_mc_factor_cond_t, the
+    default) against the cooperative shared-memory kernel
+    (k_mc_factor_compact<true>, ISC_MCF_T=0) on an imported flux-row system
+    (also with doubled off-diagonal blocks: pivot blocks far from the
+    identity): same operations in the same order, so the same du bit for bit
+    and the same iteration count; both solve the system (dense check)."""
+    from paper_1811_11992_b200.grid import build_grid
+    from paper_1811_11992_b200.synth import synth_system
+    from paper_1811_11992_b200.model import load_pack
+    grid = build_grid(*shape, 1.0, 1.0, 1.0, 1.0, 1.0, 1.0, 0.3)
+    pack = load_pack("tube3_pack", grid.phi_ref)
+    diag, offd, resid = synth_system(grid, 9, seed=29)
+    diag, offd = diag.copy(), offd.copy() * scale
+    offd[:, :, 6:, :] = 0.0
+    out = {}
+    for mode in ("1", "0"):
+        monkeypatch.setenv("ISC_MCF_T", mode)
+        ws = Workspace(grid, pack, None, wells=(), streams=(), precond="mcilu")
+        load_system(ws, diag, offd, resid)
+        du, _, it = BlockSolver(grid, ws, tol=1e-12, maxiter=500, precond="mcilu").solve([])
+        assert ws.ctx.condensed
+        out[mode] = (du.copy(), it)
+        ws.ctx.close()
+    n = grid.ncell
+    A = np.zeros((9 * n, 9 * n))
+    for c in range(n):
+        A[9 * c:9 * c + 9, 9 * c:9 * c + 9] = diag[c]
+    for ic in range(grid.nconn):
+        a, b = int(grid.conn_a[ic]), int(grid.conn_b[ic])
+        A[9 * a:9 * a + 9, 9 * b:9 * b + 9] = offd[ic, 0]
+        A[9 * b:9 * b + 9, 9 * a:9 * a + 9] = offd[ic, 1]
+    ref = np.linalg.solve(A, -resid.reshape(-1)).reshape(n, 9)
+    assert np.linalg.norm(out["1"][0] - ref) <= 1e-8 * np.linalg.norm(ref)
+    assert out["1"][1] == out["0"][1]
+    np.testing.assert_array_equal(out["1"][0], out["0"][0])
