@@ -277,7 +277,7 @@ def algorithmic_bytes(grid, nw, precond="ras", form="explicit"):
             # + k_cond_es: the local rows of the black cells' diagonal blocks in
             # (27 n/2), E_S out (18 n/2)
             out["decouple"] = 8 * (81 * n + 9 * n + 54 * n + 9 * n + 22.5 * n)
-            # k_mc_factor_compact<COND>: B_bd and B_back flux rows (54 m each),
+            # k_mc_factor_cond_t (condensed form): B_bd and B_back flux rows (54 m each),
             # D^-1[:, :6] of both colours (54 n), the red neighbours' b (4.5 n),
             # E_S (9 n), B' out (36 m), U6^-1 out (18 n), g_b (4.5 n); the Bc
             # blocks are formed with the raw red pass on g (k_cc_red_bc)

@@ -14,7 +14,7 @@ import sys
 from collections import defaultdict
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
-KERNELS = ["k_cc6_red", "k_cc6_black", "k_mc_factor_compact", "k_cc_red_bc", "k_cc6_xred",
+KERNELS = ["k_cc6_red", "k_cc6_black", "k_mc_factor_cond_t", "k_mc_factor_compact", "k_cc_red_bc", "k_cc6_xred",
            "k_cond_es", "k_cond_expand",
            "k_cc_red", "k_cc_black", "k_sc_update_p", "k_sc_update_s", "k_sc_update_xr",
            "k_face_eval_light", "k_face_eval_energy", "k_face_gather", "k_decouple_compact_t", "k_decouple_compact",
