@@ -193,6 +193,14 @@ int isc_synth_system_slab(isc_ctx *ctx, uint64_t seed, int32_t nz_global);
  * status 2, *bad_cell/*bad_col identify the block (-1 when not a cell). */
 int isc_solve(isc_ctx *ctx, double tol, int32_t maxiter, double *d_du, double *h_dbhp,
               int32_t *iters, int64_t *bad_cell, int32_t *bad_col);
+
+/* isc_solve delivering du as the reference's BlockSolver.solve does
+ * (linsolve.py:396-479: a host (n, 9) array in natural cell order; pinned
+ * memory for an asynchronous copy). On the single-GPU condensed path the
+ * solve's last kernels run per plane chunk with each chunk's copy under the
+ * next chunk's kernels; otherwise isc_solve(d_du = NULL) + isc_download_du. */
+int isc_solve_host(isc_ctx *ctx, double tol, int32_t maxiter, double *h_du, double *h_dbhp,
+                   int32_t *iters, int64_t *bad_cell, int32_t *bad_col);
 /* Decouple only (tests): leaves D^-1-scaled blocks/rhs inside the context
  * (the compact form for mcilu on an assembled system: isc_decoupled_form). */
 int isc_decouple(isc_ctx *ctx, int64_t *bad_cell, int32_t *bad_col);

@@ -81,6 +81,9 @@ _SIGS = {
     "isc_solve": (ctypes.c_int, [VP, ctypes.c_double, ctypes.c_int32, VP, VP,
                                  ctypes.POINTER(ctypes.c_int32), c_int64_p,
                                  ctypes.POINTER(ctypes.c_int32)]),
+    "isc_solve_host": (ctypes.c_int, [VP, ctypes.c_double, ctypes.c_int32, VP, VP,
+                                      ctypes.POINTER(ctypes.c_int32), c_int64_p,
+                                      ctypes.POINTER(ctypes.c_int32)]),
     "isc_decouple": (ctypes.c_int, [VP, c_int64_p, ctypes.POINTER(ctypes.c_int32)]),
     "isc_precond_setup": (ctypes.c_int, [VP, c_int64_p]),
     "isc_spmv": (ctypes.c_int, [VP, VP, VP]),

@@ -1550,10 +1550,11 @@ __global__ void k_stage_state(Dims g, const double* __restrict__ stage, double* 
 }
 
 // SoA (storage order) -> AoS (n, NU) natural order, for a host download
-__global__ void k_unstage_rows(Dims g, const double* __restrict__ v, double* __restrict__ out) {
+__global__ void k_unstage_rows(Dims g, const double* __restrict__ v, double* __restrict__ out,
+                               int64_t c0, int64_t c1) {
   const int64_t n = g.n;
-  const int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (c >= n) return;
+  const int64_t c = c0 + (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (c >= c1) return;
   const int64_t p = pos_of(g, c);
 #pragma unroll
   for (int r = 0; r < NU; ++r) out[c * NU + r] = v[(int64_t)r * n + p];

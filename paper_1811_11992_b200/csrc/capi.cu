@@ -512,7 +512,7 @@ extern "C" int isc_assemble_host(isc_ctx* ctx, const double* h_p, const double* 
 // du of the last isc_solve as a host (n, NU) array in natural cell order
 extern "C" int isc_download_du(isc_ctx* ctx, double* h_du) {
   const int64_t n = ctx->g.n;
-  k_unstage_rows<<<grid1d(n, 256), 256, 0, ctx->stream>>>(ctx->g, ctx->xk, ctx->stage);
+  k_unstage_rows<<<grid1d(n, 256), 256, 0, ctx->stream>>>(ctx->g, ctx->xk, ctx->stage, 0, n);
   LAUNCH_CHECK();
   CK(cudaMemcpyAsync(h_du, ctx->stage, (size_t)n * NU * 8, cudaMemcpyDeviceToHost, ctx->stream));
   CK(cudaStreamSynchronize(ctx->stream));
@@ -1130,6 +1130,25 @@ extern "C" int isc_solve(isc_ctx* ctx, double tol, int32_t maxiter, double* d_du
     }
   }
   return ISC_OK;
+}
+
+// isc_solve with du delivered to the host (n, NU) array h_du (natural cell
+// order; pinned memory for an asynchronous copy): on the condensed
+// single-GPU path the solve's last kernels (red back-substitution, x_b = g_b
+// + E_b w, transpose) run per plane chunk and each chunk's copy overlaps the
+// next chunk's kernels; otherwise isc_solve + isc_download_du.
+extern "C" int isc_solve_host(isc_ctx* ctx, double tol, int32_t maxiter, double* h_du,
+                              double* h_dbhp, int32_t* iters, int64_t* bad_cell,
+                              int32_t* bad_col) {
+  ctx->h_du = h_du;
+  ctx->h_du_queued = false;
+  const int s = isc_solve(ctx, tol, maxiter, nullptr, h_dbhp, iters, bad_cell, bad_col);
+  ctx->h_du = nullptr;
+  const bool queued = ctx->h_du_queued;
+  ctx->h_du_queued = false;
+  if (queued) CK(cudaStreamSynchronize(ctx->cstream));
+  if (s) return s;
+  return queued ? ISC_OK : isc_download_du(ctx, h_du);
 }
 
 // -------------------------------------------------------------- Newton

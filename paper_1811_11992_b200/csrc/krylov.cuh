@@ -393,6 +393,44 @@ static int bicgstab_schur_t(isc_ctx* ctx, double tol, int maxiter, int* iters) {
     return K.finalize1(RED_BLOCKS, slot);
   };
   auto finish = [&]() -> int {   // x_r = b_r - B_rb x_b
+    if (cnd && ctx->h_du && !ctx->comm.active() && x == ctx->xk) {
+      // du goes to the host (isc_solve_host): the same kernels per plane
+      // chunk, each chunk's transpose + copy (copy stream) under the next
+      // chunk's kernels. A red cell reads w of the black cells one plane
+      // below and above it, so chunk q + 1's back-substitution runs before
+      // chunk q's x_b overwrites w.
+      KScope ks(ctx, KT_VEC);
+      const int nq = std::min(6, g.nz);
+      auto gq_of = [&](int q) {
+        Dims gq = g;
+        gq.tw_lo = (int64_t)(g.nz * (int64_t)q / nq) * g.ph;
+        gq.tw_hi = (int64_t)(g.nz * (int64_t)(q + 1) / nq) * g.ph;
+        return gq;
+      };
+      auto xred_q = [&](int q) {
+        const Dims gq = gq_of(q);
+        k_cc6_xred<<<grid1d(gq.tw_hi - gq.tw_lo, 32), dim3(32, CR), 0, st>>>(gq, ctx->cbc, ctx->diag,
+                                                                             ctx->cg9, b, x);
+      };
+      xred_q(0);
+      for (int q = 0; q < nq; ++q) {
+        if (q + 1 < nq) xred_q(q + 1);
+        const Dims gq = gq_of(q);
+        const int64_t cnt = gq.tw_hi - gq.tw_lo;
+        k_cond_expand<<<(int)std::min<int64_t>(RED_BLOCKS, grid1d(cnt, RED_THREADS)), RED_THREADS, 0,
+                        st>>>(gq, ctx->ces, ctx->cg9, x);
+        const int64_t c0 = 2 * gq.tw_lo, c1 = 2 * gq.tw_hi;   // the chunk's planes, both colours
+        k_unstage_rows<<<grid1d(c1 - c0, 256), 256, 0, st>>>(g, x, ctx->stage, c0, c1);
+        if (cudaEventRecord(ctx->chunk_ev[q], st) != cudaSuccess) return ISC_CUDA_ERROR;
+        if (cudaStreamWaitEvent(ctx->cstream, ctx->chunk_ev[q], 0) != cudaSuccess) return ISC_CUDA_ERROR;
+        if (cudaMemcpyAsync(ctx->h_du + c0 * NU, ctx->stage + c0 * NU, (size_t)(c1 - c0) * NU * 8,
+                            cudaMemcpyDeviceToHost, ctx->cstream) != cudaSuccess)
+          return ISC_CUDA_ERROR;
+        ctx->launches += 3;
+      }
+      ctx->h_du_queued = true;
+      return cudaGetLastError() == cudaSuccess ? 0 : ISC_CUDA_ERROR;
+    }
     if (cnd) {   // x_r from w and y_r(g), then x_b = g_b + E_b w
       if (halo_exchange(ctx, x, CR)) return ISC_CUDA_ERROR;
       KScope ks(ctx, KT_VEC);

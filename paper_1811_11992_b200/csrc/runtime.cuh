@@ -55,6 +55,8 @@ struct isc_ctx {
   bool cell_pre = false;                   // k_cell already ran (pipelined host staging)
   bool face_pre = false;                   // k_face_eval too
   bool gather_pre = false;                 // and k_face_gather
+  double* h_du = nullptr;                  // isc_solve_host: du streamed to this host array by the solve
+  bool h_du_queued = false;                // ... its copies are on cstream
   bool mc_schur = true;   // mcilu: red-eliminated BiCGSTAB (ISC_MCILU_FULL=1: full system)
   int krylov = ISC_KRYLOV_BICGSTAB;   // mcilu red-eliminated system: BiCGSTAB or GMRES(m)
   int gm_m = 30;                      // GMRES restart length (<= GM_MAXV - 1)

@@ -209,23 +209,22 @@ class DeviceContext:
         return self.wout[:self.nw].copy()
 
     def solve_host(self, tol, maxiter):
-        """isc_solve + isc_download_du -> (du (n, 9) numpy, dbhp, iters).
+        """isc_solve_host -> (du (n, 9) numpy, dbhp, iters).
 
         du lands in one of two pinned host buffers used in turn (the caller
         consumes it before the next-but-one solve, as the Newton loop does)."""
         dbhp = np.zeros(max(1, self.nw))
         it = ctypes.c_int32(0)
         bc, bcol = ctypes.c_int64(-1), ctypes.c_int32(-1)
-        st = self.L.isc_solve(self.h, float(tol), int(maxiter), N.VP(0), N.ptr(dbhp),
-                              ctypes.byref(it), ctypes.byref(bc), ctypes.byref(bcol))
-        N.check(st, "isc_solve", bad_cell=bc.value, bad_col=bcol.value)
         if not hasattr(self, "_du_pool"):
             self._du_pool = [torch.empty(self.n, NU, dtype=torch.float64).pin_memory()
                              for _ in range(2)]
             self._du_turn = 0
         buf = self._du_pool[self._du_turn]
         self._du_turn ^= 1
-        N.check(self.L.isc_download_du(self.h, N.ptr(buf)), "isc_download_du")
+        st = self.L.isc_solve_host(self.h, float(tol), int(maxiter), N.ptr(buf), N.ptr(dbhp),
+                                   ctypes.byref(it), ctypes.byref(bc), ctypes.byref(bcol))
+        N.check(st, "isc_solve", bad_cell=bc.value, bad_col=bcol.value)
         return buf.numpy(), dbhp[:self.nw], int(it.value)
 
     def solve(self, tol, maxiter, d_du):
