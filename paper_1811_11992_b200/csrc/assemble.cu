@@ -1138,8 +1138,10 @@ __device__ __forceinline__ void face_row(const CellView& A_, const CellView& B_,
 // ------------------------------------------------------- face-centric pair
 //
 // Each face is evaluated once:
-//   k_face_eval    thread per (lower cell a, axis, row < ROW_OS): flux row
-//                  and both derivative rows of face (a, a+axis); writes
+//   k_face_eval_*  thread per (lower cell a, axis) -- the five light rows in
+//                  one thread (_light), the energy row in another (_energy):
+//                  per row the flux and both derivative rows of face (a,
+//                  a+axis); writes
 //                  offd[a][+axis] row = dfb, offd[b][-axis] row = -dfa and
 //                  the flux into fbuf[(axis*ROW_OS + row)*n + a]; zero rows
 //                  for boundary blocks.
@@ -1191,9 +1193,13 @@ __device__ __forceinline__ void face_eval_row(const FaceArgs2& A2, int64_t c, in
 }
 
 // The light rows (0..4) and the energy row (5, every phase) as separate
-// kernels so that each gets its own register budget / occupancy.
+// kernels so that each gets its own register budget / occupancy. A thread
+// evaluates all five light rows of its face: the rows share the phase
+// potentials, the upwind choice and the upstream partials, which stay in
+// registers across the inlined rows (same expressions, so the same values as
+// the earlier thread per (face, row): face pair 3.70 -> 3.52 ms at C4).
 #ifndef FEVL_MINB
-#define FEVL_MINB 8
+#define FEVL_MINB 5   // C4: 128 registers, 5 CTAs per SM (4: 132 registers, no gain; 6-7: spills, none)
 #endif
 #ifndef FEVE_MINB
 #define FEVE_MINB 5   // C4 sweep 4..8: face pair 4.06 -> 3.97 ms at 5
@@ -1206,13 +1212,11 @@ __global__ void __launch_bounds__(32 * 3, FEVL_MINB) k_face_eval_light(const Fac
   const int axis = axis_lo + threadIdx.y;
   int i, j, k;
   const int64_t cell = locate(A2.F.g, c, i, j, k);
-  switch (blockIdx.y) {   // block-uniform
-    case 0: face_eval_row<0>(A2, c, cell, i, j, k, axis); break;
-    case 1: face_eval_row<1>(A2, c, cell, i, j, k, axis); break;
-    case 2: face_eval_row<2>(A2, c, cell, i, j, k, axis); break;
-    case 3: face_eval_row<3>(A2, c, cell, i, j, k, axis); break;
-    default: face_eval_row<4>(A2, c, cell, i, j, k, axis); break;
-  }
+  face_eval_row<0>(A2, c, cell, i, j, k, axis);
+  face_eval_row<1>(A2, c, cell, i, j, k, axis);
+  face_eval_row<2>(A2, c, cell, i, j, k, axis);
+  face_eval_row<3>(A2, c, cell, i, j, k, axis);
+  face_eval_row<4>(A2, c, cell, i, j, k, axis);
 }
 __global__ void __launch_bounds__(32 * 3, FEVE_MINB) k_face_eval_energy(const FaceArgs2 A2,
                                                                         int64_t c_begin,

@@ -252,7 +252,7 @@ extern "C" int isc_kernel_times(isc_ctx* ctx, double* ms8, int64_t* count8, int3
 static void launch_face_eval(const FaceArgs2& F2, int64_t c0, int64_t c1, int axis_lo, int naxes,
                              cudaStream_t st) {
   const int blocks = grid1d(c1 - c0, 32);
-  k_face_eval_light<<<dim3(blocks, ROW_E), dim3(32, naxes), 0, st>>>(F2, c0, c1, axis_lo);
+  k_face_eval_light<<<blocks, dim3(32, naxes), 0, st>>>(F2, c0, c1, axis_lo);
   k_face_eval_energy<<<blocks, dim3(32, naxes), 0, st>>>(F2, c0, c1, axis_lo);
 }
 
