@@ -236,3 +236,41 @@ def test_c5_slab_generator_and_solve_match_single_gpu(nranks):
     for cx in ctxs:
         cx.close()
     hub.close()
+
+
+def test_nccl_transport_one_rank():
+    """The NCCL transport itself on one GPU: a one-rank communicator (the
+    dlopen binding of torch's NCCL, `ncclCommInitRank`, the packed
+    `ncclAllReduce` of the Krylov scalars, the Newton norm and the host
+    all-reduce) under the slab code path of the library — assembly, solve and
+    norm equal the plain single-context run, and a NaN norm stays NaN through
+    the reduction (NCCL's max alone would drop it). The halo send/recv needs
+    a second GPU and stays with the hub tests above."""
+    from paper_1811_11992_b200.distributed import attach_nccl, nccl_unique_id
+    c = case_objects("sub2")
+    st, accn = random_state_like_reference(c, 37)
+    ref_resid, ref_du, ref_dbhp, ref_it, ref_wout = _single(c, st, accn, "mcilu", 1e-10)
+    piece = split_case(c.case, 1, 0)
+    assert piece.g_lo == 0 and piece.g_hi == 0 and piece.grid.ncell == c.grid.ncell
+    ctx = DeviceContext(piece.grid, piece.pack, piece.wells, piece.streams, "mcilu")
+    attach_nccl(ctx, nccl_unique_id(), piece)
+    d_accn = soa_from_rows(accn, ctx.device)
+    wout = ctx.assemble(state_to_device(st, ctx.device), st.bhp, d_accn, 2e-3, 2e-3,
+                        np.zeros(len(c.wells), bool), False)
+    np.testing.assert_array_equal(ctx.copy_out(0, 9).cpu().numpy(), ref_resid)
+    np.testing.assert_array_equal(wout, ref_wout)
+    norm = ctx.scaled_norm_cells(d_accn, 2e-3)
+    assert np.isfinite(norm) and norm > 0.0
+    du = ctx.empty(9, c.grid.ncell)
+    dbhp, it = ctx.solve(1e-10, 1000, du)
+    assert abs(it - ref_it) <= 1
+    a = du.cpu().numpy()
+    assert np.linalg.norm(a - ref_du) <= 1e-8 * np.linalg.norm(ref_du)
+    np.testing.assert_allclose(dbhp, ref_dbhp, rtol=1e-7)
+    # a NaN residual on this rank survives the rank reduction
+    bad = accn.copy()
+    bad[3, 2] = np.nan
+    ctx.assemble(state_to_device(st, ctx.device), st.bhp, soa_from_rows(bad, ctx.device), 2e-3,
+                 2e-3, np.zeros(len(c.wells), bool), False)
+    assert np.isnan(ctx.scaled_norm_cells(soa_from_rows(bad, ctx.device), 2e-3))
+    ctx.close()
