@@ -232,6 +232,9 @@ int isc_audit_sums(isc_ctx *ctx, const double *d_accn, double *h_out);
 int isc_comm_nccl(isc_ctx *ctx, const void *unique_id, int32_t rank, int32_t nranks,
                   int32_t has_lo, int32_t has_hi, int32_t kw_lo, int32_t kw_hi);
 int isc_nccl_unique_id(void *out128);   /* ncclGetUniqueId on the calling rank */
+/* 1 when the context reduces / exchanges through an NCCL communicator (nranks > 1, or one
+ * rank with ISC_NCCL_SINGLE=1 in the environment of isc_comm_nccl: transport check on one GPU) */
+int isc_comm_is_nccl(isc_ctx *ctx);
 void *isc_hub_create(int32_t nranks);
 int isc_hub_destroy(void *hub);
 int isc_comm_hub(isc_ctx *ctx, void *hub, int32_t rank, int32_t has_lo, int32_t has_hi,

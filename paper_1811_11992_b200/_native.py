@@ -96,6 +96,7 @@ _SIGS = {
     "isc_comm_nccl": (ctypes.c_int, [VP, VP, ctypes.c_int32, ctypes.c_int32, ctypes.c_int32,
                                      ctypes.c_int32, ctypes.c_int32, ctypes.c_int32]),
     "isc_nccl_unique_id": (ctypes.c_int, [VP]),
+    "isc_comm_is_nccl": (ctypes.c_int, [VP]),
     "isc_hub_create": (VP, [ctypes.c_int32]),
     "isc_hub_destroy": (ctypes.c_int, [VP]),
     "isc_comm_hub": (ctypes.c_int, [VP, VP, ctypes.c_int32, ctypes.c_int32, ctypes.c_int32,

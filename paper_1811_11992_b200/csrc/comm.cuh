@@ -99,7 +99,8 @@ struct Comm {
   bool has_lo = false, has_hi = false;
   ncclComm_t nccl = nullptr;
   Hub* hub = nullptr;
-  bool active() const { return nranks > 1; }
+  bool single = false;   // one-rank NCCL communicator driven through the slab path (tests)
+  bool active() const { return nranks > 1 || single; }
 };
 
 // pack / unpack the `rows` x plane-k values of a storage-order vector. The

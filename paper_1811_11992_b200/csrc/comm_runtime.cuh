@@ -38,7 +38,12 @@ extern "C" int isc_comm_nccl(isc_ctx* ctx, const void* unique_id, int32_t rank, 
                              int32_t has_lo, int32_t has_hi, int32_t kw_lo, int32_t kw_hi) {
   int s = setup_window(ctx, rank, nranks, has_lo, has_hi, kw_lo, kw_hi);
   if (s) return s;
-  if (nranks > 1) {
+  // ISC_NCCL_SINGLE=1: a one-rank communicator is created and used as well
+  // (the slab code path with no neighbours: every all-reduce goes through
+  // NCCL) -- the transport check that one GPU allows
+  const char* single_env = std::getenv("ISC_NCCL_SINGLE");
+  ctx->comm.single = nranks == 1 && single_env && std::atoi(single_env) != 0;
+  if (nranks > 1 || ctx->comm.single) {
     NcclApi& api = nccl_api();
     if (!api.ok) { g_err = "libnccl.so.2 not available in this process"; return ISC_UNSUPPORTED; }
     ncclUniqueId id;
@@ -50,6 +55,10 @@ extern "C" int isc_comm_nccl(isc_ctx* ctx, const void* unique_id, int32_t rank, 
     }
   }
   return ISC_OK;
+}
+
+extern "C" int isc_comm_is_nccl(isc_ctx* ctx) {
+  return ctx->comm.active() && ctx->comm.nccl != nullptr ? 1 : 0;
 }
 
 extern "C" int isc_nccl_unique_id(void* out128) {

@@ -238,8 +238,9 @@ def test_c5_slab_generator_and_solve_match_single_gpu(nranks):
     hub.close()
 
 
-def test_nccl_transport_one_rank():
-    """The NCCL transport itself on one GPU: a one-rank communicator (the
+def test_nccl_transport_one_rank(monkeypatch):
+    """The NCCL transport itself on one GPU: a one-rank communicator
+    (ISC_NCCL_SINGLE=1 makes the library create and use it; the
     dlopen binding of torch's NCCL, `ncclCommInitRank`, the packed
     `ncclAllReduce` of the Krylov scalars, the Newton norm and the host
     all-reduce) under the slab code path of the library — assembly, solve and
@@ -253,7 +254,9 @@ def test_nccl_transport_one_rank():
     piece = split_case(c.case, 1, 0)
     assert piece.g_lo == 0 and piece.g_hi == 0 and piece.grid.ncell == c.grid.ncell
     ctx = DeviceContext(piece.grid, piece.pack, piece.wells, piece.streams, "mcilu")
+    monkeypatch.setenv("ISC_NCCL_SINGLE", "1")
     attach_nccl(ctx, nccl_unique_id(), piece)
+    assert N.lib().isc_comm_is_nccl(ctx.h) == 1
     d_accn = soa_from_rows(accn, ctx.device)
     wout = ctx.assemble(state_to_device(st, ctx.device), st.bhp, d_accn, 2e-3, 2e-3,
                         np.zeros(len(c.wells), bool), False)

@@ -904,3 +904,37 @@ def test_condensed_factorisation_kernels_agree(shape, scale, monkeypatch):
     assert np.linalg.norm(out["1"][0] - ref) <= 1e-8 * np.linalg.norm(ref)
     assert out["1"][1] == out["0"][1]
     np.testing.assert_array_equal(out["1"][0], out["0"][0])
+
+
+@pytest.mark.parametrize("name,krylov", [("sub2", "bicgstab"), ("small3d", "bicgstab"),
+                                         ("sub2", "gmres")])
+def test_solve_host_streams_the_same_du(name, krylov):
+    """isc_solve_host (du delivered to a host (n, 9) array; on the condensed
+    BiCGSTAB path the back-substitution / expansion / transpose run per plane
+    chunk under the chunks' D2H copies) against isc_solve's device du of an
+    identically assembled context: the same values bit for bit, the same
+    dbhp and iteration count. GMRES takes the isc_solve + isc_download_du
+    fallback."""
+    from paper_1811_11992_b200.device import DeviceContext, soa_from_rows, state_to_device
+    from tests.golden_states import random_state_like_reference
+    c = case_objects(name)
+    st, accn = random_state_like_reference(c, 41)
+    out = []
+    for host in (False, True):
+        ctx = DeviceContext(c.grid, c.pack, c.wells, c.streams, "mcilu")
+        ctx.set_krylov(krylov)
+        ctx.assemble(state_to_device(st, ctx.device), st.bhp, soa_from_rows(accn, ctx.device),
+                     2e-3, 2e-3, np.zeros(len(c.wells), bool), False)
+        if host:
+            du, dbhp, it = ctx.solve_host(1e-10, 1000)
+            du = np.array(du).T
+        else:
+            d = ctx.empty(9, c.grid.ncell)
+            dbhp, it = ctx.solve(1e-10, 1000, d)
+            du = d.cpu().numpy()
+        assert ctx.condensed
+        out.append((du.copy(), np.array(dbhp), it))
+        ctx.close()
+    np.testing.assert_array_equal(out[0][0], out[1][0])
+    np.testing.assert_array_equal(out[0][1], out[1][1])
+    assert out[0][2] == out[1][2]
