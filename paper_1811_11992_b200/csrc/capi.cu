@@ -78,6 +78,9 @@ extern "C" int isc_create(const isc_model_desc* md, const isc_grid_desc* gdsc, i
   ctx->stream = ctx->own_stream;
   CK(cudaStreamCreateWithFlags(&ctx->cstream, cudaStreamNonBlocking));
   for (auto& e : ctx->chunk_ev) CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+  CK(cudaStreamCreateWithFlags(&ctx->stream2, cudaStreamNonBlocking));
+  for (auto& e : ctx->cell_ev) CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+  for (auto& e : ctx->face_ev) CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
   for (auto& e : ctx->halo_ev) CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
   for (auto& e : ctx->ev) CK(cudaEventCreate(&e));
   // static grid arrays
@@ -205,6 +208,11 @@ extern "C" int isc_destroy(isc_ctx* ctx) {
   if (ctx->own_stream) cudaStreamDestroy(ctx->own_stream);
   if (ctx->cstream) cudaStreamDestroy(ctx->cstream);
   for (auto& e : ctx->chunk_ev)
+    if (e) cudaEventDestroy(e);
+  if (ctx->stream2) cudaStreamDestroy(ctx->stream2);
+  for (auto& e : ctx->cell_ev)
+    if (e) cudaEventDestroy(e);
+  for (auto& e : ctx->face_ev)
     if (e) cudaEventDestroy(e);
   for (auto& e : ctx->halo_ev)
     if (e) cudaEventDestroy(e);
@@ -420,7 +428,7 @@ extern "C" int isc_assemble_host(isc_ctx* ctx, const double* h_p, const double* 
   static const int nq_max = [] {   // plane chunks of the staged copy (ISC_H2D_CHUNKS, 1..32)
     const char* e = std::getenv("ISC_H2D_CHUNKS");
     const int v = e ? std::atoi(e) : 9;
-    return std::max(1, std::min(32, v));
+    return std::max(1, std::min(30, v));
   }();
   static const int first_planes = [] {   // planes of the first chunk (ISC_H2D_FIRST)
     const char* e = std::getenv("ISC_H2D_FIRST");
@@ -441,9 +449,22 @@ extern "C" int isc_assemble_host(isc_ctx* ctx, const double* h_p, const double* 
       kb[1 + q] = first_planes + (int)((int64_t)(g.nz - first_planes) * q / nrest);
   }
   int64_t gathered = 0;   // positions whose faces are all evaluated and gathered
+  // Alternate chunks run on two compute streams so that one chunk's kernels
+  // fill the ramps and tails of the other's (ten dependent kernels per chunk
+  // otherwise drain the GPU at every boundary). Chunk q's face evaluation
+  // reads the records of chunk q - 1's last plane (cell_ev[q - 1]) and its
+  // gather the blocks chunk q - 1's faces wrote (face_ev[q - 1]); everything
+  // else a chunk touches lies in its own planes. The per-kernel-class timers
+  // record on the main stream only: one stream while profiling.
+  static const bool two_env = [] {
+    const char* e = std::getenv("ISC_H2D_TWO_STREAMS");
+    return !e || std::atoi(e) != 0;
+  }();
+  const bool two = pipe && two_env && !ctx->profiling && nq > 2;
   CK(cudaMemsetAsync(ctx->bad_d, 0xff, 8, st));
   CK(cudaEventRecord(ctx->chunk_ev[0], st));
   CK(cudaStreamWaitEvent(ctx->cstream, ctx->chunk_ev[0], 0));   // stage buffer free
+  if (two) CK(cudaStreamWaitEvent(ctx->stream2, ctx->chunk_ev[0], 0));
   CellArgs A{g, ctx->st_c, ctx->phi_ref, ctx->vol, ctx->hl_area, ctx->hl_kob, ctx->hl_d,
              ctx->hl_rho, ctx->hl_tini, ctx->accn_c, dt, ctx->rec, ctx->acc, ctx->src,
              ctx->resid, ctx->diag, ctx->bad_d, 0, n};
@@ -451,7 +472,13 @@ extern "C" int isc_assemble_host(isc_ctx* ctx, const double* h_p, const double* 
              ctx->resid, ctx->diag, ctx->offd, ctx->ccnz_d};
   FaceArgs2 F2{F, ctx->fbuf};
   if (pipe) CK(cudaMemsetAsync(ctx->ccnz_d, 0, 4, st));
+  if (two) {   // stream2's first kernels follow the two flag resets
+    CK(cudaEventRecord(ctx->face_ev[31], st));
+    CK(cudaStreamWaitEvent(ctx->stream2, ctx->face_ev[31], 0));
+  }
+  cudaStream_t st_main = st;
   for (int q = 0; q < nq; ++q) {
+    st = two && (q & 1) ? ctx->stream2 : st_main;
     const int64_t k0 = kb[q], k1 = kb[q + 1];
     const int64_t c0 = k0 * g.nxny, c1 = k1 * g.nxny, cnt = c1 - c0;
     const size_t b = (size_t)cnt * 8;
@@ -476,6 +503,10 @@ extern "C" int isc_assemble_host(isc_ctx* ctx, const double* h_p, const double* 
         KScope ks(ctx, KT_CELL);
         launch_cell(ctx, A, st);
       }
+      if (two) {
+        CK(cudaEventRecord(ctx->cell_ev[q], st));
+        if (q > 0) CK(cudaStreamWaitEvent(st, ctx->cell_ev[q - 1], 0));
+      }
       KScope ks(ctx, KT_FACE);
       // all three axes of the planes whose upper neighbours' records now
       // exist: the last plane of the previous chunk up to this chunk's last
@@ -485,6 +516,10 @@ extern "C" int isc_assemble_host(isc_ctx* ctx, const double* h_p, const double* 
         launch_face_eval(F2, z0, z1, 0, 3, st);
         ctx->launches += 2;
       }
+      if (two) {
+        CK(cudaEventRecord(ctx->face_ev[q], st));
+        if (q > 0) CK(cudaStreamWaitEvent(st, ctx->face_ev[q - 1], 0));
+      }
       // every face of the planes below k1 - 1 is now evaluated: gather them
       // while the next chunk is still on the bus
       if (z1 > gathered) {
@@ -493,6 +528,11 @@ extern "C" int isc_assemble_host(isc_ctx* ctx, const double* h_p, const double* 
         gathered = z1;
       }
     }
+  }
+  st = st_main;
+  if (two) {   // join: the main stream continues after both streams' last chunks
+    CK(cudaEventRecord(ctx->face_ev[30], ctx->stream2));
+    CK(cudaStreamWaitEvent(st, ctx->face_ev[30], 0));
   }
   if (pipe) {   // the top plane's faces (+z: boundary, zero blocks), the last planes' gather
     KScope ks(ctx, KT_FACE);

@@ -51,6 +51,8 @@ struct isc_ctx {
   cudaStream_t own_stream = nullptr;
   cudaStream_t cstream = nullptr;          // host->device staging copies (isc_assemble_host)
   cudaEvent_t chunk_ev[32] = {};
+  cudaStream_t stream2 = nullptr;          // second compute stream of the staged assembly (alternate chunks)
+  cudaEvent_t cell_ev[32] = {}, face_ev[32] = {};   // chunk q's cell pass / face evaluation done
   cudaEvent_t halo_ev[2] = {};             // halo planes packed / landed
   bool cell_pre = false;                   // k_cell already ran (pipelined host staging)
   bool face_pre = false;                   // k_face_eval too

@@ -938,3 +938,34 @@ def test_solve_host_streams_the_same_du(name, krylov):
     np.testing.assert_array_equal(out[0][0], out[1][0])
     np.testing.assert_array_equal(out[0][1], out[1][1])
     assert out[0][2] == out[1][2]
+
+
+@pytest.mark.parametrize("two", ["1", "0"])
+def test_staged_assembly_equals_resident_assembly(two, monkeypatch):
+    """isc_assemble_host (host State + accn in plane chunks; per chunk the
+    cell pass, the three-axis face evaluation one plane behind it and the
+    gather of the planes it completes, alternate chunks on two compute
+    streams) against isc_assemble on the same state resident in HBM: the
+    exported residual, diagonal and off-diagonal blocks and the well rows are
+    the same bit for bit, on every repetition (C3: 20 planes, nine chunks)."""
+    monkeypatch.setenv("ISC_H2D_TWO_STREAMS", two)
+    from tests.golden_states import random_state_like_reference
+    c = case_objects("c3")
+    st, accn = random_state_like_reference(c, 43)
+    capped = np.zeros(len(c.wells), dtype=bool)
+    ws_d = Workspace(c.grid, c.pack, None, wells=c.wells, streams=c.streams, precond="mcilu")
+    from paper_1811_11992_b200.device import soa_from_rows, state_to_device
+    ctx = ws_d.bind(c.wells, c.streams)
+    wout_d = ctx.assemble(state_to_device(st, ctx.device), st.bhp, soa_from_rows(accn, ctx.device),
+                          2e-3, 2e-3, capped, False)
+    ws_d._invalidate()
+    ref = (ws_d.resid.copy(), ws_d.diag.copy(), ws_d.offd.copy())
+    ws_h = Workspace(c.grid, c.pack, None, wells=c.wells, streams=c.streams, precond="mcilu")
+    for rep in range(4):
+        blocks = assemble(c.grid, c.pack, ws_h, c.wells, c.streams, st, accn, 2e-3, 2e-3, capped)
+        np.testing.assert_array_equal(ws_h.last_wout, wout_d)
+        np.testing.assert_array_equal(ws_h.resid, ref[0])
+        np.testing.assert_array_equal(ws_h.diag, ref[1])
+        np.testing.assert_array_equal(ws_h.offd, ref[2])
+    ws_d.ctx.close()
+    ws_h.ctx.close()
