@@ -57,6 +57,9 @@ __device__ __forceinline__ void cp_async_wait() {
 #ifndef DCT_THREADS
 #define DCT_THREADS 128
 #endif
+#ifndef DCT_UNIFORM_SWAP
+#define DCT_UNIFORM_SWAP 1
+#endif
 // opaque selects: a plain `q == piv ? x : y` chain over an unrolled register
 // array is folded back into a dynamically indexed (local-memory) array
 __device__ __forceinline__ double sel_d(bool p, double x, double y) {
@@ -213,18 +216,28 @@ __global__ void __launch_bounds__(DCT_THREADS) k_decouple_compact_t(
       if (v > pv) { pv = v; piv = r; }
     }
     if (pv <= tol || amax == 0.0) failc = amax == 0.0 ? 0 : min(failc, k);
+#if DCT_UNIFORM_SWAP
+    // No interchange anywhere in the warp (about every other step on the C4
+    // blocks): the select chain over the candidate rows is skipped -- a
+    // warp-uniform branch around it, the values are untouched either way.
+    // (A vote per candidate row, or a plain register swap of the row a
+    // uniform warp picked, makes the compiler move the block to local memory.)
+    if (!__all_sync(__activemask(), piv == k))
+#endif
+    {
 #pragma unroll
-    for (int q = k + 1; q < NU; ++q) {
-      const bool sw = q == piv;
+      for (int q = k + 1; q < NU; ++q) {
+        const bool sw = q == piv;
 #pragma unroll
-      for (int j = 0; j < NU; ++j) {
-        const double t = a[k][j];
-        a[k][j] = sel_d(sw, a[q][j], t);
-        a[q][j] = sel_d(sw, t, a[q][j]);
+        for (int j = 0; j < NU; ++j) {
+          const double t = a[k][j];
+          a[k][j] = sel_d(sw, a[q][j], t);
+          a[q][j] = sel_d(sw, t, a[q][j]);
+        }
+        const int t = perm[k];
+        perm[k] = sel_i(sw, perm[q], t);
+        perm[q] = sel_i(sw, t, perm[q]);
       }
-      const int t = perm[k];
-      perm[k] = sel_i(sw, perm[q], t);
-      perm[q] = sel_i(sw, t, perm[q]);
     }
     const double dv = 1.0 / a[k][k];
     // row k: the pivot slot becomes column perm[k] of the inverse (1 * dv)
