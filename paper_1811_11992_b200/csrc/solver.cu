@@ -369,7 +369,10 @@ struct IluDev {
   double* aup;                         // [(q*NB + e)*nslots + s]  upper blocks, slot order
 };
 
-constexpr int IL_SLOTS = 32;
+#ifndef IL_SLOTS_N
+#define IL_SLOTS_N 32
+#endif
+constexpr int IL_SLOTS = IL_SLOTS_N;   // slots per tile (CTA = IL_SLOTS x NU threads)
 
 // U = I - sum_j (A_cj U_j^-1) A_jc ; uinv = U^-1 (GJ, partial pivoting)
 // Thread (slot, column u). The three lower blocks A_cj are staged through
