@@ -427,12 +427,12 @@ extern "C" int isc_assemble_host(isc_ctx* ctx, const double* h_p, const double* 
   const bool pipe = !ctx->comm.active();
   static const int nq_max = [] {   // plane chunks of the staged copy (ISC_H2D_CHUNKS, 1..32)
     const char* e = std::getenv("ISC_H2D_CHUNKS");
-    const int v = e ? std::atoi(e) : 9;
+    const int v = e ? std::atoi(e) : 13;
     return std::max(1, std::min(30, v));
   }();
   static const int first_planes = [] {   // planes of the first chunk (ISC_H2D_FIRST)
     const char* e = std::getenv("ISC_H2D_FIRST");
-    return std::max(1, e ? std::atoi(e) : 3);
+    return std::max(1, e ? std::atoi(e) : 2);
   }();
   // chunk bounds: a thin first chunk (the compute starts as soon as it has
   // landed), the remaining planes in nq - 1 equal chunks (every chunk costs

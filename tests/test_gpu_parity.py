@@ -947,7 +947,7 @@ def test_staged_assembly_equals_resident_assembly(two, monkeypatch):
     gather of the planes it completes, alternate chunks on two compute
     streams) against isc_assemble on the same state resident in HBM: the
     exported residual, diagonal and off-diagonal blocks and the well rows are
-    the same bit for bit, on every repetition (C3: 20 planes, nine chunks)."""
+    the same bit for bit, on every repetition (C3: 20 planes, thirteen chunks)."""
     monkeypatch.setenv("ISC_H2D_TWO_STREAMS", two)
     from tests.golden_states import random_state_like_reference
     c = case_objects("c3")
